@@ -1,0 +1,509 @@
+/*
+ * pm_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, obviously-correct CPU oracle for the particle hot path of
+ * arXiv 1804.07598 (OpenFPM).  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * It shares no code, header, table or constant with the CUDA path.
+ *
+ * Build: gcc -O2 -ffp-contract=off -fno-fast-math -fopenmp -shared -fPIC
+ * (-ffp-contract=off: every float expression below is evaluated exactly as
+ * written, one IEEE round-to-nearest per operation; x86-64 uses SSE, not x87).
+ *
+ * What it computes:
+ *  - Integer structures (wrap, cell ids, counts, start, perm, Verlet sets) are
+ *    defined by fp32 decision functions (readings R1-R6 in DESIGN.md), written
+ *    here as plain C float expressions.
+ *  - Real-valued results (forces, energies, densities, accelerations) are
+ *    evaluated in fp64 from the same fp32 inputs, by the plain O(N) per row
+ *    sum over ALL other particles -- the definition the cell/Verlet lists
+ *    reorganise (§2: "Cell Lists [45] or Verlet Lists [46] ...
+ *    reduces the computational cost to O(N)").
+ *
+ * Pins: tests/test_oracle_pins.py.  Functions with no independent pin say
+ * "parity unpinned" below (only the SPH viscosity constants, R20).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+int orc_num_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+void orc_set_num_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
+/* ------------------------------------------------------------------ */
+/* R1: fp32 periodic wrap into the half-open box [lo, hi).             */
+/* PAPER.md:166 (§4.1) "Periodic boundary conditions are imposed in all */
+/* three coordinate directions"; the face convention is reading R1.    */
+/* ------------------------------------------------------------------ */
+static float wrap1(float x, float lo, float hi) {
+  float L = hi - lo;
+  if (x >= hi) {
+    x = x - L;
+  } else if (x < lo) {
+    x = x + L;
+  }
+  if (x >= hi) x = lo; /* fl(-tiny + L) == L */
+  return x;
+}
+
+/* Returns the number of particles outside [lo,hi) on a non-periodic axis. */
+int64_t orc_wrap(int64_t n, float *pos4, const float lo[3], const float hi[3],
+                 const int32_t per[3]) {
+  int64_t bad = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    for (int d = 0; d < 3; ++d) {
+      float x = pos4[4 * i + d];
+      if (per[d]) {
+        pos4[4 * i + d] = wrap1(x, lo[d], hi[d]);
+      } else if (!(x >= lo[d] && x < hi[d])) {
+        bad++;
+      }
+    }
+  }
+  return bad;
+}
+
+/* ------------------------------------------------------------------ */
+/* R2: cell grid.  n_d = floor((hi-lo) / (r_v / cell_div)) in fp64 on the */
+/* fp32 inputs; inv_w_d = fp32(n_d / (hi-lo)).  PAPER.md:48 (§2) Cell   */
+/* Lists; cell side >= interaction radius so a 27-cell stencil suffices. */
+/* ------------------------------------------------------------------ */
+int orc_cell_grid(const float lo[3], const float hi[3], float rv, int32_t cell_div,
+                  int32_t ncell[3], float inv_w[3]) {
+  for (int d = 0; d < 3; ++d) {
+    double ext = (double)hi[d] - (double)lo[d];
+    double side = (double)rv / (double)cell_div;
+    double nd = floor(ext / side);
+    if (nd < 1) nd = 1;
+    ncell[d] = (int32_t)nd;
+    inv_w[d] = (float)(nd / ext);
+  }
+  return 0;
+}
+
+/* R3: c_d = min(max(floor(fl(fl(x - lo) * inv_w)), 0), n_d - 1);
+ *     id = c_x + n_x (c_y + n_y c_z). */
+void orc_cell_ids(int64_t n, const float *pos4, const float lo[3], const float inv_w[3],
+                  const int32_t ncell[3], int32_t *cell_of) {
+  for (int64_t i = 0; i < n; ++i) {
+    int32_t c[3];
+    for (int d = 0; d < 3; ++d) {
+      float t = pos4[4 * i + d] - lo[d];
+      float u = t * inv_w[d];
+      float f = floorf(u);
+      int32_t cd = (int32_t)f;
+      if (f < 0.0f) cd = 0;
+      if (cd > ncell[d] - 1) cd = ncell[d] - 1;
+      c[d] = cd;
+    }
+    cell_of[i] = c[0] + ncell[0] * (c[1] + ncell[1] * c[2]);
+  }
+}
+
+/* Step 5 of the oracle definition: counts, exclusive start (start[ncell] = n)
+ * and the stable permutation: perm[k] = storage index of the k-th particle in
+ * (cell, storage index) order.  Plain stable counting sort. */
+void orc_counting_sort(int64_t n, const int32_t *cell_of, int64_t ncell_total,
+                       int32_t *count, int32_t *start, int32_t *perm) {
+  memset(count, 0, sizeof(int32_t) * (size_t)ncell_total);
+  for (int64_t i = 0; i < n; ++i) count[cell_of[i]]++;
+  int64_t acc = 0;
+  for (int64_t c = 0; c < ncell_total; ++c) {
+    start[c] = (int32_t)acc;
+    acc += count[c];
+  }
+  start[ncell_total] = (int32_t)acc;
+  int32_t *next = (int32_t *)malloc(sizeof(int32_t) * (size_t)(ncell_total > 0 ? ncell_total : 1));
+  memcpy(next, start, sizeof(int32_t) * (size_t)ncell_total);
+  for (int64_t i = 0; i < n; ++i) perm[next[cell_of[i]]++] = (int32_t)i;
+  free(next);
+}
+
+/* ------------------------------------------------------------------ */
+/* R4: fp32 pair difference delta = x_j - x_i with the Sterbenz-ordered  */
+/* periodic correction, and d2 = fma(dz,dz, fma(dy,dy, dx*dx)) (reading  */
+/* R4': single-rounded fused multiply-adds, fmaf is exact).   */
+/* ------------------------------------------------------------------ */
+static float pair_delta1(float a, float b, float L, float halfL, int per) {
+  float e = b - a;
+  if (per) {
+    if (e > halfL) {
+      float bb = b - L;
+      return bb - a;
+    } else if (e < -halfL) {
+      float aa = a - L;
+      return b - aa;
+    }
+  }
+  return e;
+}
+
+static float pair_d2_f32(const float *xi, const float *xj, const float L[3],
+                         const float halfL[3], const int32_t per[3], int8_t shift[3]) {
+  float dl[3];
+  for (int d = 0; d < 3; ++d) {
+    dl[d] = pair_delta1(xi[d], xj[d], L[d], halfL[d], per[d]);
+    if (shift) {
+      float e = xj[d] - xi[d];
+      shift[d] = (int8_t)(per[d] ? (e > halfL[d] ? -1 : (e < -halfL[d] ? 1 : 0)) : 0);
+    }
+  }
+  float s = dl[0] * dl[0];
+  s = fmaf(dl[1], dl[1], s);
+  s = fmaf(dl[2], dl[2], s);
+  return s;
+}
+
+static void box_consts(const float lo[3], const float hi[3], float L[3], float halfL[3]) {
+  for (int d = 0; d < 3; ++d) {
+    L[d] = hi[d] - lo[d];
+    halfL[d] = L[d] * 0.5f;
+  }
+}
+
+float orc_pair_d2(const float xi[3], const float xj[3], const float lo[3], const float hi[3],
+                  const int32_t per[3]) {
+  float L[3], hL[3];
+  box_consts(lo, hi, L, hL);
+  return pair_d2_f32(xi, xj, L, hL, per, NULL);
+}
+
+/* fp64 minimum-image delta x_i - x_j of the fp64 values of fp32 positions,
+ * with L the fp64 value of the fp32 box length (oracle step 8). */
+static void delta64(const float *xi, const float *xj, const double L[3], const int32_t per[3],
+                    double out[3]) {
+  for (int d = 0; d < 3; ++d) {
+    double e = (double)xi[d] - (double)xj[d];
+    if (per[d]) {
+      if (e > 0.5 * L[d]) e -= L[d];
+      else if (e < -0.5 * L[d]) e += L[d];
+    }
+    out[d] = e;
+  }
+}
+
+/* ------------------------------------------------------------------ */
+/* R5: Verlet set N_i = { j != i : d2_32(i,j) < fl(rv*rv) }, brute force  */
+/* over all j (§4.1 Verlet lists [46]).        */
+/* rows: which particles (storage index) to build; output CSR over rows   */
+/* with cols = storage index of j (ascending) and shift codes.            */
+/* Returns total entries, or -(needed) if cap is too small.               */
+/* ------------------------------------------------------------------ */
+int64_t orc_verlet_rows(int64_t n, const float *pos4, const float lo[3], const float hi[3],
+                        const int32_t per[3], float rv, const int64_t *rows, int64_t nrows,
+                        int64_t *row_ptr, int32_t *cols, int8_t *shifts, int64_t cap) {
+  float L[3], hL[3];
+  box_consts(lo, hi, L, hL);
+  float rv2 = rv * rv;
+  int64_t *cnt = (int64_t *)calloc((size_t)(nrows > 0 ? nrows : 1), sizeof(int64_t));
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t r = 0; r < nrows; ++r) {
+    int64_t i = rows[r];
+    int64_t c = 0;
+    for (int64_t j = 0; j < n; ++j) {
+      if (j == i) continue;
+      if (pair_d2_f32(pos4 + 4 * i, pos4 + 4 * j, L, hL, per, NULL) < rv2) c++;
+    }
+    cnt[r] = c;
+  }
+  int64_t tot = 0;
+  for (int64_t r = 0; r < nrows; ++r) {
+    row_ptr[r] = tot;
+    tot += cnt[r];
+  }
+  row_ptr[nrows] = tot;
+  if (tot > cap) {
+    free(cnt);
+    return -tot;
+  }
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t r = 0; r < nrows; ++r) {
+    int64_t i = rows[r];
+    int64_t k = row_ptr[r];
+    for (int64_t j = 0; j < n; ++j) {
+      if (j == i) continue;
+      int8_t sh[3];
+      if (pair_d2_f32(pos4 + 4 * i, pos4 + 4 * j, L, hL, per, sh) < rv2) {
+        cols[k] = (int32_t)j;
+        if (shifts) {
+          shifts[3 * k + 0] = sh[0];
+          shifts[3 * k + 1] = sh[1];
+          shifts[3 * k + 2] = sh[2];
+        }
+        k++;
+      }
+    }
+  }
+  free(cnt);
+  return tot;
+}
+
+/* ------------------------------------------------------------------ */
+/* Lennard-Jones (§4.1):                                  */
+/*   V(r) = 4 eps [ (sigma/r)^12 - (sigma/r)^6 ]                        */
+/*   F_i = sum_j -dV/dr * (x_i - x_j)/r                                  */
+/*       = sum_j 24 eps (2 sigma^12 / r^14 - sigma^6 / r^8) (x_i - x_j)  */
+/* (reading R7: the Listing 4.1 exponent at PAPER.md:212 is a typo).     */
+/* Inclusion: d2_32 < fl(rc*rc) (R6, strict).  Capped mode (R22):        */
+/* r_eff = max(r, r_min), f = -V'(r_eff) along (x_i - x_j)/r.            */
+/* Outputs per row (fp64): F[3], U_i = 1/2 sum_j V, W_i = 1/2 sum_j d.f, */
+/* npair_i = #included j.  Returns #pairs with r == 0 (coincident).      */
+/* ------------------------------------------------------------------ */
+static double lj_V(double r, double eps, double sig) {
+  double sr6 = pow(sig / r, 6.0);
+  return 4.0 * eps * (sr6 * sr6 - sr6);
+}
+
+/* -dV/dr */
+static double lj_mdVdr(double r, double eps, double sig) {
+  double sr6 = pow(sig / r, 6.0);
+  return 24.0 * eps * (2.0 * sr6 * sr6 - sr6) / r;
+}
+
+int64_t orc_lj_rows(int64_t n, const float *pos4, const float lo[3], const float hi[3],
+                    const int32_t per[3], float rc, double eps, double sigma, double r_min,
+                    const int64_t *rows, int64_t nrows, double *F3, double *U, double *W,
+                    int64_t *npair) {
+  float L[3], hL[3];
+  box_consts(lo, hi, L, hL);
+  double L64[3] = {L[0], L[1], L[2]};
+  float rc2 = rc * rc;
+  int64_t ncoinc = 0;
+#pragma omp parallel for schedule(dynamic, 16) reduction(+ : ncoinc)
+  for (int64_t r = 0; r < nrows; ++r) {
+    int64_t i = rows[r];
+    double f[3] = {0, 0, 0}, u = 0, w = 0;
+    int64_t np = 0;
+    for (int64_t j = 0; j < n; ++j) {
+      if (j == i) continue;
+      if (!(pair_d2_f32(pos4 + 4 * i, pos4 + 4 * j, L, hL, per, NULL) < rc2)) continue;
+      double dl[3];
+      delta64(pos4 + 4 * i, pos4 + 4 * j, L64, per, dl);
+      double rr = sqrt(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
+      if (rr == 0.0) {
+        ncoinc++;
+        continue;
+      }
+      double re = (r_min > 0 && rr < r_min) ? r_min : rr;
+      double fm = lj_mdVdr(re, eps, sigma); /* magnitude along +(x_i - x_j) */
+      for (int d = 0; d < 3; ++d) f[d] += fm * dl[d] / rr;
+      u += 0.5 * lj_V(re, eps, sigma);
+      w += 0.5 * fm * rr;
+      np++;
+    }
+    F3[3 * r + 0] = f[0];
+    F3[3 * r + 1] = f[1];
+    F3[3 * r + 2] = f[2];
+    if (U) U[r] = u;
+    if (W) W[r] = w;
+    if (npair) npair[r] = np;
+  }
+  return ncoinc;
+}
+
+double orc_lj_V(double r, double eps, double sigma) { return lj_V(r, eps, sigma); }
+double orc_lj_mdVdr(double r, double eps, double sigma) { return lj_mdVdr(r, eps, sigma); }
+
+/* ------------------------------------------------------------------ */
+/* Velocity Verlet in fp64 ("symplectic Velocity-verlet",  */
+/* Listing 4.1 lines 58-59, 72 at PAPER.md:291-293, 320), m = mass:     */
+/*   v += dt/2 F/m ; x += dt v ; wrap ; F = F(x) ; v += dt/2 F/m          */
+/* Forces by the plain O(N^2) fp64 sum with fp64 cutoff r < rc (this is   */
+/* an fp64 trajectory: no fp32 decisions).  trace[(s)*4 + {0,1,2,3}] =  */
+/* {KE, U_raw, U_shift, npairs} at s = 0..nsteps.                         */
+/* ------------------------------------------------------------------ */
+static void forces64(int64_t n, const double *x, const double L[3], const int32_t per[3],
+                     double rc, double eps, double sig, double r_min, double *F, double *Uraw,
+                     double *Ushift, double *npairs) {
+  double vrc = lj_V(rc, eps, sig);
+  double u = 0, us = 0, np = 0;
+#pragma omp parallel for schedule(dynamic, 64) reduction(+ : u, us, np)
+  for (int64_t i = 0; i < n; ++i) {
+    double f[3] = {0, 0, 0};
+    for (int64_t j = 0; j < n; ++j) {
+      if (j == i) continue;
+      double dl[3];
+      for (int d = 0; d < 3; ++d) {
+        double e = x[3 * i + d] - x[3 * j + d];
+        if (per[d]) {
+          if (e > 0.5 * L[d]) e -= L[d];
+          else if (e < -0.5 * L[d]) e += L[d];
+        }
+        dl[d] = e;
+      }
+      double rr = sqrt(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
+      if (!(rr < rc) || rr == 0.0) continue;
+      double re = (r_min > 0 && rr < r_min) ? r_min : rr;
+      double fm = lj_mdVdr(re, eps, sig);
+      for (int d = 0; d < 3; ++d) f[d] += fm * dl[d] / rr;
+      double v = lj_V(re, eps, sig);
+      u += 0.5 * v;
+      us += 0.5 * (v - vrc);
+      np += 1.0;
+    }
+    F[3 * i + 0] = f[0];
+    F[3 * i + 1] = f[1];
+    F[3 * i + 2] = f[2];
+  }
+  *Uraw = u;
+  *Ushift = us;
+  *npairs = np;
+}
+
+void orc_vv_run(int64_t n, double *x, double *v, const double lo[3], const double hi[3],
+                const int32_t per[3], double rc, double eps, double sigma, double r_min,
+                double mass, double dt, int64_t nsteps, double *trace) {
+  double L[3] = {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]};
+  double *F = (double *)malloc(sizeof(double) * 3 * (size_t)(n > 0 ? n : 1));
+  double u, us, np;
+  forces64(n, x, L, per, rc, eps, sigma, r_min, F, &u, &us, &np);
+  for (int64_t s = 0;; ++s) {
+    if (trace) {
+      double ke = 0;
+      for (int64_t i = 0; i < 3 * n; ++i) ke += 0.5 * mass * v[i] * v[i];
+      trace[4 * s + 0] = ke;
+      trace[4 * s + 1] = u;
+      trace[4 * s + 2] = us;
+      trace[4 * s + 3] = np;
+    }
+    if (s == nsteps) break;
+    for (int64_t i = 0; i < 3 * n; ++i) v[i] += 0.5 * dt * F[i] / mass;
+    for (int64_t i = 0; i < n; ++i) {
+      for (int d = 0; d < 3; ++d) {
+        double xx = x[3 * i + d] + dt * v[3 * i + d];
+        if (per[d]) {
+          if (xx >= hi[d]) xx -= L[d];
+          else if (xx < lo[d]) xx += L[d];
+        }
+        x[3 * i + d] = xx;
+      }
+    }
+    forces64(n, x, L, per, rc, eps, sigma, r_min, F, &u, &us, &np);
+    for (int64_t i = 0; i < 3 * n; ++i) v[i] += 0.5 * dt * F[i] / mass;
+  }
+  free(F);
+}
+
+/* ------------------------------------------------------------------ */
+/* SPH (§4.2, Eqs. 1, 3, 4, 5; readings R15-R21).     */
+/* Cubic spline W (the "classic cubic SPH kernel [34]"):  */
+/*   W(r,h) = 1/(pi h^3) { 1 - 1.5 q^2 + 0.75 q^3   (0 <= q < 1)         */
+/*                         0.25 (2 - q)^3          (1 <= q < 2)         */
+/*                         0                        (q >= 2) },  q = r/h */
+/* ------------------------------------------------------------------ */
+static const double ORC_PI = 3.14159265358979323846;
+
+double orc_sph_W(double r, double h) {
+  double q = r / h;
+  double c = 1.0 / (ORC_PI * h * h * h);
+  if (q < 1.0) return c * (1.0 - 1.5 * q * q + 0.75 * q * q * q);
+  if (q < 2.0) {
+    double t = 2.0 - q;
+    return c * 0.25 * t * t * t;
+  }
+  return 0.0;
+}
+
+double orc_sph_dWdr(double r, double h) {
+  double q = r / h;
+  double c = 1.0 / (ORC_PI * h * h * h * h);
+  if (q < 1.0) return c * (-3.0 * q + 2.25 * q * q);
+  if (q < 2.0) {
+    double t = 2.0 - q;
+    return c * (-0.75 * t * t);
+  }
+  return 0.0;
+}
+
+/* Density by summation (reading R16) including the self term, and the Tait
+ * EOS Eq. 3: P = b [ (rho/rho0)^gamma - 1 ].  All particles (fluid and
+ * boundary) get rho and P.  Neighbours: every q != p with fp64 r < 2h. */
+void orc_sph_density_rows(int64_t n, const float *pos4, const float lo[3], const float hi[3],
+                          const int32_t per[3], double h, double mass, double rho0, double b,
+                          double gamma, const int64_t *rows, int64_t nrows, double *rho_out,
+                          double *P_out) {
+  float L[3], hL[3];
+  box_consts(lo, hi, L, hL);
+  double L64[3] = {L[0], L[1], L[2]};
+  double w0 = orc_sph_W(0.0, h);
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t r = 0; r < nrows; ++r) {
+    int64_t p = rows[r];
+    double rho = mass * w0;
+    for (int64_t q = 0; q < n; ++q) {
+      if (q == p) continue;
+      double dl[3];
+      delta64(pos4 + 4 * p, pos4 + 4 * q, L64, per, dl);
+      double rr = sqrt(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
+      if (rr < 2.0 * h) rho += mass * orc_sph_W(rr, h);
+    }
+    rho_out[r] = rho;
+    P_out[r] = b * (pow(rho / rho0, gamma) - 1.0);
+  }
+}
+
+/* Eq. 1 with readings R17 (sign: a_p = -sum m (...) grad_p W(x_p - x_q)),
+ * R18 ((P_p + P_q)/(rho_p rho_q) as printed), R20 (Pi_pq: Monaghan, nonzero
+ * only for v_pq . r_pq < 0; cbar = c0, alpha, eta2 given; "parity unpinned"
+ * beyond the branch/sign pins), g added to fluid particles only; boundary
+ * particles (kind 1) get a = 0.  rho/P are per-particle inputs (storage
+ * order, fp64) so the force pass can be pinned independently of the
+ * density pass. */
+void orc_sph_accel_rows(int64_t n, const float *pos4, const float *vel4, const double *rho,
+                        const double *P, const int32_t *kind, const float lo[3],
+                        const float hi[3], const int32_t per[3], double h, double mass,
+                        double alpha, double cbar, double eta2, const double g[3],
+                        const int64_t *rows, int64_t nrows, double *a_out) {
+  float L[3], hL[3];
+  box_consts(lo, hi, L, hL);
+  double L64[3] = {L[0], L[1], L[2]};
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t r = 0; r < nrows; ++r) {
+    int64_t p = rows[r];
+    double a[3] = {0, 0, 0};
+    if (kind && kind[p] != 0) {
+      a_out[3 * r + 0] = a_out[3 * r + 1] = a_out[3 * r + 2] = 0.0;
+      continue;
+    }
+    for (int64_t q = 0; q < n; ++q) {
+      if (q == p) continue;
+      double dl[3]; /* r_pq = x_p - x_q */
+      delta64(pos4 + 4 * p, pos4 + 4 * q, L64, per, dl);
+      double rr = sqrt(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
+      if (!(rr < 2.0 * h) || rr == 0.0) continue;
+      double dw = orc_sph_dWdr(rr, h);
+      double gradW[3] = {dl[0] / rr * dw, dl[1] / rr * dw, dl[2] / rr * dw};
+      double vpq[3] = {(double)vel4[4 * p + 0] - vel4[4 * q + 0],
+                       (double)vel4[4 * p + 1] - vel4[4 * q + 1],
+                       (double)vel4[4 * p + 2] - vel4[4 * q + 2]};
+      double vr = vpq[0] * dl[0] + vpq[1] * dl[1] + vpq[2] * dl[2];
+      double Pi = 0.0;
+      if (vr < 0.0) {
+        double mu = h * vr / (rr * rr + eta2);
+        double rbar = 0.5 * (rho[p] + rho[q]);
+        Pi = -alpha * cbar * mu / rbar;
+      }
+      double coef = mass * ((P[p] + P[q]) / (rho[p] * rho[q]) + Pi);
+      for (int d = 0; d < 3; ++d) a[d] -= coef * gradW[d];
+    }
+    for (int d = 0; d < 3; ++d) a_out[3 * r + d] = a[d] + g[d];
+  }
+}

@@ -1,0 +1,412 @@
+"""Pins of the CPU oracle against things other than itself (no GPU).
+
+Each test fixes part of the oracle with a value the paper / mathematics fixes:
+closed forms (golden files), finite-difference derivatives, lattice sums by
+integer enumeration, invariants, symmetry, brute-force fp64 band checks, and
+conservation laws.  A dropped term, wrong sign, wrong index or transposed
+operand in oracle/pm_oracle.c fails at least one of these.
+"""
+import itertools
+import math
+import os
+
+import numpy as np
+import pytest
+
+from paper_1804_07598_b200 import inputs
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _golden_rows(name):
+    rows = []
+    with open(os.path.join(GOLD, name)) as f:
+        for line in f:
+            line = line.strip()
+            if line and not line.startswith("#"):
+                rows.append(line.split())
+    return rows
+
+
+# ------------------------------------------------------------------ LJ pair
+def test_lj_golden_closed_forms(orc):
+    """zero crossing at sigma, minimum -eps at 2^(1/6) sigma,
+    SPEC.md:698 worked example (240 at r = sigma = 0.1)."""
+    for eps, sig, r, V, F in (map(float, row) for row in _golden_rows("lj_closed_forms.txt")):
+        assert orc.lj_V(r, eps, sig) == pytest.approx(V, abs=1e-12 * max(1.0, abs(V)))
+        assert orc.lj_mdVdr(r, eps, sig) == pytest.approx(F, abs=1e-9 * max(1.0, abs(F)))
+
+
+@pytest.mark.parametrize("r", [0.85, 0.95, 1.0, 1.05, 1.3, 1.5, 2.0, 2.4, 2.5])
+def test_lj_force_is_minus_dV_dr(orc, r):
+    """-dV/dr from a central finite difference of V (pins the force formula
+    against the potential of PAPER.md:162, reading R7)."""
+    h = 1e-5
+    fd = -(orc.lj_V(r + h) - orc.lj_V(r - h)) / (2 * h)
+    assert orc.lj_mdVdr(r) == pytest.approx(fd, rel=1e-7, abs=1e-8)
+
+
+def test_lj_two_particle_spec_example(orc):
+    """sigma = 0.1, eps = 1, r = sigma along x, q at +x:
+    F_p = (-240, 0, 0), F_q = (+240, 0, 0); energy = V(sigma) = 0.  Also a
+    two-particle energy equals the analytic V (BJ north_star)."""
+    pos = np.zeros((2, 4), np.float32)
+    pos[0, :3] = [0.5, 0.5, 0.5]
+    pos[1, :3] = [0.625, 0.5, 0.5]  # exact fp32 distance 0.125 (sigma = 0.125 below)
+    res = orc.lj_rows(pos, [0, 0, 0], [1, 1, 1], [1, 1, 1], rc=0.3, eps=1.0, sigma=0.125)
+    assert res["F"][0] == pytest.approx([-24.0 / 0.125, 0, 0], abs=1e-9)
+    assert res["F"][1] == pytest.approx([24.0 / 0.125, 0, 0], abs=1e-9)
+    assert res["U"].sum() == pytest.approx(0.0, abs=1e-12)
+    # analytic two-particle energy at r = 1.5 sigma
+    pos[1, 0] = 0.5 + 1.5 * 0.125
+    res = orc.lj_rows(pos, [0, 0, 0], [1, 1, 1], [1, 1, 1], rc=0.3, eps=1.0, sigma=0.125)
+    V = 4 * ((1 / 1.5) ** 12 - (1 / 1.5) ** 6)
+    assert res["U"].sum() == pytest.approx(V, rel=1e-12)
+    assert res["F"][0, 0] < 0 < res["F"][1, 0] or res["F"][0, 0] > 0 > res["F"][1, 0]
+    # attractive at 1.5 sigma: p (left) is pulled to +x
+    assert res["F"][0, 0] > 0
+
+
+def test_lj_cutoff_strict_and_periodic_image(orc):
+    """R6 strict inclusion; the minimum image across a periodic face gives the
+    same force as the direct pair (PAPER.md:166 periodic BCs)."""
+    lo, hi, per = [0, 0, 0], [10, 10, 10], [1, 1, 1]
+    pos = np.zeros((2, 4), np.float32)
+    pos[0, :3] = [0.25, 5, 5]
+    pos[1, :3] = [9.25, 5, 5]  # image distance exactly 1.0
+    res = orc.lj_rows(pos, lo, hi, per, rc=2.5)
+    assert res["F"][0] == pytest.approx([24.0, 0, 0], rel=1e-12)  # pushed to +x
+    pos[1, :3] = [2.75, 5, 5]  # distance exactly 2.5 == rc: excluded (strict)
+    res = orc.lj_rows(pos, lo, hi, per, rc=2.5)
+    assert res["npair"].sum() == 0 and np.all(res["F"] == 0)
+    pos[1, :3] = [np.nextafter(np.float32(2.75), np.float32(0)), 5, 5]
+    res = orc.lj_rows(pos, lo, hi, per, rc=2.5)
+    assert res["npair"].sum() == 2
+    # non-periodic: no image
+    res = orc.lj_rows(np.array([[0.25, 5, 5, 0], [9.25, 5, 5, 0]], np.float32), lo, hi,
+                      [0, 1, 1], rc=2.5)
+    assert res["npair"].sum() == 0
+
+
+def _sc_lattice_sum(a, rc, eps=1.0, sigma=1.0):
+    """U/N = 1/2 sum over SC lattice vectors n != 0 with |n| a < rc of V --
+    by integer enumeration (independent of the oracle's pair loop)."""
+    m = int(math.ceil(rc / a)) + 1
+    u, cnt = 0.0, 0
+    for n in itertools.product(range(-m, m + 1), repeat=3):
+        if n == (0, 0, 0):
+            continue
+        r = a * math.sqrt(n[0] ** 2 + n[1] ** 2 + n[2] ** 2)
+        if r < rc:
+            sr6 = (sigma / r) ** 6
+            u += 0.5 * 4 * eps * (sr6 * sr6 - sr6)
+            cnt += 1
+    return u, cnt
+
+
+def test_lj_perfect_lattice_closed_form(orc):
+    """Exactly representable SC lattice (a = 9/8): F == 0 by symmetry and U/N
+    equals the lattice sum; 56 neighbours inside rc = 2.5 at rho = 0.8 spacing."""
+    a = 1.125
+    s = inputs.lj_lattice_system(16, 16, 16, jitter_key=(0,), a=a, jitter=0.0)
+    res = orc.lj_rows(s.pos, s.lo, s.hi, s.periodic, rc=2.5)
+    u_ref, cnt = _sc_lattice_sum(a, 2.5)
+    assert np.max(np.abs(res["F"])) < 1e-10
+    assert np.all(res["npair"] == cnt)
+    assert res["U"].mean() == pytest.approx(u_ref, rel=1e-12)
+    # rho = 0.8 spacing: neighbour shells |n|^2 <= 5 -> 6 + 12 + 8 + 6 + 24 = 56
+    _, cnt08 = _sc_lattice_sum(inputs.A_RHO08, 2.5)
+    assert cnt08 == 56
+
+
+def test_lj_newton_third_law_cfg1(orc):
+    """Sum of forces ~ 0 (pairwise antisymmetry) on BJ configs[0]."""
+    s = inputs.cfg1()
+    res = orc.lj_rows(s.pos, s.lo, s.hi, s.periodic, rc=2.5)
+    tot = res["F"].sum(axis=0)
+    scale = np.abs(res["F"]).sum()
+    assert np.all(np.abs(tot) < 1e-12 * scale)
+    rms = np.sqrt(np.mean(res["F"] ** 2))
+    assert 5.0 < rms < 20.0  # liquid-like jittered lattice (~10)
+
+
+# ------------------------------------------------------------------ cells
+def test_wrap_rule_adversarial(orc):
+    """R1: half-open [lo, hi); -tiny wraps to lo (fl(-tiny + L) == L case)."""
+    lo, hi = np.float32(0.0), np.float32(17.235477)
+    tiny = np.float32(1e-9)
+    xs = np.array([0.0, -tiny, hi, np.nextafter(hi, np.float32(0)), hi + np.float32(1.0),
+                   np.float32(-1.0), np.float32(5.0)], np.float32)
+    pos = np.zeros((xs.size, 4), np.float32)
+    pos[:, 0] = xs
+    pos[:, 1] = 1.0
+    pos[:, 2] = 1.0
+    w, bad = orc.wrap(pos, [lo, 0, 0], [hi, 20, 20], [1, 1, 1])
+    assert bad == 0
+    x = w[:, 0]
+    assert np.all(x >= lo) and np.all(x < hi)
+    assert x[0] == 0.0 and x[1] == 0.0 and x[2] == 0.0
+    assert x[3] == np.nextafter(hi, np.float32(0))
+    assert x[4] == pytest.approx(1.0, abs=1e-5)
+    assert x[5] == pytest.approx(float(hi) - 1.0, abs=1e-5)
+    # non-periodic out-of-range is reported, not wrapped
+    _, bad = orc.wrap(pos, [lo, 0, 0], [hi, 20, 20], [0, 1, 1])
+    assert bad == 4
+
+
+def _check_cell_list(cl, pos_wrapped, lo, hi):
+    n = pos_wrapped.shape[0]
+    nc = cl["ncell"]
+    count, start, perm, cell_of = cl["count"], cl["start"], cl["perm"], cl["cell_of"]
+    assert count.sum() == n and start[-1] == n and start[0] == 0
+    assert np.all(np.diff(start) == count)
+    assert np.array_equal(np.sort(perm), np.arange(n))
+    keys = cell_of[perm]
+    assert np.all(np.diff(keys) >= 0)
+    same = np.diff(keys) == 0
+    assert np.all(np.diff(perm)[same] > 0)  # stable: ties in storage order
+    # each particle lies in its cell (fp64, up to one fp32 rounding)
+    c = np.stack([cell_of % nc[0], (cell_of // nc[0]) % nc[1], cell_of // (nc[0] * nc[1])], 1)
+    ext = hi.astype(np.float64) - lo.astype(np.float64)
+    w = ext / nc
+    x = pos_wrapped[:, :3].astype(np.float64) - lo
+    tol = 4e-7 * ext
+    assert np.all(x >= c * w - tol) and np.all(x < (c + 1) * w + tol)
+
+
+def test_cell_list_invariants_cfg1_shuffled(orc):
+    s = inputs.shuffled(inputs.cfg1(), (11,))
+    cl = orc.cell_list(s.pos, s.lo, s.hi, s.periodic, rv=2.8)
+    assert list(cl["ncell"]) == [6, 6, 6]
+    _check_cell_list(cl, cl["pos"], s.lo, s.hi)
+    assert cl["count"].mean() == pytest.approx(4096 / 216)
+
+
+def test_cell_list_adversarial_faces(orc):
+    """Particles exactly on cell faces, at lo, at hi - ulp, all in one cell."""
+    lo = np.zeros(3, np.float32)
+    hi = np.full(3, 9.0, np.float32)
+    nc, iw = orc.cell_grid(lo, hi, 2.8)
+    assert list(nc) == [3, 3, 3]
+    faces = np.array([0.0, 3.0, 6.0, np.nextafter(np.float32(9.0), np.float32(0)),
+                      np.nextafter(np.float32(3.0), np.float32(0)), 4.5], np.float32)
+    pts = np.array(list(itertools.product(faces, repeat=3)), np.float32)
+    pos = np.zeros((pts.shape[0] + 50, 4), np.float32)
+    pos[:pts.shape[0], :3] = pts
+    pos[pts.shape[0]:, :3] = 1.0  # 50 particles in one cell
+    cl = orc.cell_list(pos, lo, hi, [1, 1, 1], rv=2.8)
+    _check_cell_list(cl, cl["pos"], lo, hi)
+    # x = 3.0 exactly: fl(3 * fl(3/9)) rounds to 1.0 -> cell 1
+    i = np.where((pts == [3.0, 0.0, 0.0]).all(1))[0][0]
+    assert cl["cell_of"][i] == 1
+    assert cl["count"].max() >= 50
+
+
+def test_pair_d2_symmetric_and_periodic(orc):
+    """R4: d2(i,j) == d2(j,i) bitwise; across the face equals the direct
+    distance of the shifted pair to fp32 accuracy."""
+    r = np.random.default_rng(5)
+    lo, hi, per = [0, 0, 0], [137.88, 137.88, 68.94], [1, 1, 1]
+    for _ in range(2000):
+        xi = r.uniform(0, [137.88, 137.88, 68.94]).astype(np.float32)
+        xj = (xi + r.uniform(-3, 3, 3)).astype(np.float32)
+        xj = np.where(xj >= np.float32(hi), xj - np.float32(hi), xj)
+        xj = np.where(xj < 0, xj + np.float32(hi), xj).astype(np.float32)
+        d1 = orc.pair_d2(xi, xj, lo, hi, per)
+        d2 = orc.pair_d2(xj, xi, lo, hi, per)
+        assert d1 == d2
+        e = xj.astype(np.float64) - xi.astype(np.float64)
+        L = np.asarray(hi, np.float32).astype(np.float64)
+        e = np.where(e > L / 2, e - L, np.where(e < -L / 2, e + L, e))
+        assert float(d1) == pytest.approx(float((e * e).sum()), rel=1e-5, abs=1e-6)
+
+
+# ------------------------------------------------------------------ Verlet
+def _fp64_pairs(pos, lo, hi, per):
+    x = pos[:, :3].astype(np.float64)
+    L = (np.asarray(hi, np.float32) - np.asarray(lo, np.float32)).astype(np.float64)
+    e = x[None, :, :] - x[:, None, :]
+    for d in range(3):
+        if per[d]:
+            e[..., d] = np.where(e[..., d] > L[d] / 2, e[..., d] - L[d],
+                                 np.where(e[..., d] < -L[d] / 2, e[..., d] + L[d], e[..., d]))
+    return (e * e).sum(-1)
+
+
+@pytest.mark.parametrize("per", [(1, 1, 1), (1, 0, 1)])
+def test_verlet_brute_force_band(orc, per):
+    """R5 against an independent numpy fp64 O(N^2): every pair clearly inside
+    r_v is listed, every pair clearly outside is not, sets are symmetric."""
+    s = inputs.random_box(1500, 12.0, (7,), periodic=per)
+    rv = 2.8
+    rp, cols, sh = orc.verlet_rows(s.pos, s.lo, s.hi, s.periodic, rv)
+    n = s.n
+    d2 = _fp64_pairs(s.pos, s.lo, s.hi, per)
+    np.fill_diagonal(d2, np.inf)
+    M = np.zeros((n, n), bool)
+    for i in range(n):
+        M[i, cols[rp[i]:rp[i + 1]]] = True
+    rv2 = rv * rv
+    assert np.all(M[d2 < rv2 * (1 - 1e-6)])
+    assert not np.any(M[d2 > rv2 * (1 + 1e-6)])
+    assert np.array_equal(M, M.T)
+    # shift codes: only on periodic axes, and consistent with the jump
+    if sh.size:
+        assert np.all(sh[:, 1] == 0) if per[1] == 0 else True
+
+
+def test_verlet_cfg1_counts(orc):
+    s = inputs.cfg1()
+    rows = np.arange(0, s.n, 7)
+    rp, cols, _ = orc.verlet_rows(s.pos, s.lo, s.hi, s.periodic, 2.8, rows=rows)
+    cnt = np.diff(rp)
+    # SC rho = 0.8 lattice + 0.05 jitter: the shells |n|^2 <= 6 lie inside 2.8
+    # (6 a^2 = 6.96 < 7.84 < 8 a^2 = 9.28): 6+12+8+6+24+24 = 80 per particle.
+    assert np.all(cnt == 80)
+
+
+# ------------------------------------------------------------------ VV / NVE
+def test_vv_energy_conservation_and_momentum(orc):
+    """PAPER.md:166 'the total energy was conserved'; reading R25 bound 1e-3
+    on the shifted energy; total momentum conserved (pairwise forces)."""
+    s = inputs.lj_lattice_system(8, 8, 8, jitter_key=(9,), vel_key=(109,))
+    x, v, tr = orc.vv_run(s.pos, s.vel, s.lo, s.hi, s.periodic, rc=2.5, dt=0.005, nsteps=200)
+    E = tr[:, 0] + tr[:, 2]
+    drift = np.max(np.abs(E - E[0])) / abs(E[0])
+    assert drift < 1e-3
+    p0 = s.vel[:, :3].astype(np.float64).sum(0)
+    assert np.allclose(v.sum(0), p0, atol=1e-9)
+    assert np.all(x >= 0) and np.all(x < s.hi.astype(np.float64))
+    # KE changes (the lattice melts): integrator actually moves things
+    assert abs(tr[-1, 0] - tr[0, 0]) > 1e-3 * tr[0, 0]
+
+
+def test_vv_second_order(orc):
+    """Velocity Verlet is 2nd order: halving dt reduces the energy error ~4x."""
+    s = inputs.lj_lattice_system(6, 6, 6, jitter_key=(8,), vel_key=(108,))
+    errs = []
+    for dt, n in [(0.004, 50), (0.002, 100)]:
+        _, _, tr = orc.vv_run(s.pos, s.vel, s.lo, s.hi, s.periodic, rc=2.5, dt=dt, nsteps=n)
+        E = tr[:, 0] + tr[:, 2]
+        errs.append(np.max(np.abs(E - E[0])))
+    assert 2.5 < errs[0] / errs[1] < 6.0
+
+
+# ------------------------------------------------------------------ SPH
+def test_sph_golden_constants():
+    rows = {r[0]: float(r[1]) for r in _golden_rows("sph_constants.txt")}
+    p = inputs.cfg4(dp=1 / 16.0)  # parameters only depend on dp through h
+    assert p.params["gamma"] == rows["gamma"]
+    assert p.params["b"] == pytest.approx(rows["b"], rel=1e-12)
+    assert p.params["c0"] == pytest.approx(rows["c0"], rel=1e-10)
+
+
+def test_sph_kernel_normalisation_and_continuity(orc):
+    from scipy.integrate import quad
+    h = 0.008125
+    W0 = float([r for r in _golden_rows("sph_constants.txt") if r[0] == "W0_h0.008125"][0][1])
+    assert orc.sph_W(0.0, h) == pytest.approx(W0, rel=1e-6)
+    integral = quad(lambda r: 4 * math.pi * r * r * orc.sph_W(r, h), 0, 2 * h, points=[h],
+                    epsabs=0, epsrel=1e-12)[0]
+    assert integral == pytest.approx(1.0, abs=1e-10)
+    for q in (1.0, 2.0):
+        a, b = orc.sph_W(q * h * (1 - 1e-9), h), orc.sph_W(q * h * (1 + 1e-9), h)
+        assert a == pytest.approx(b, rel=1e-6, abs=1e-3)
+    assert orc.sph_W(2.0 * h, h) == 0.0 and orc.sph_W(3 * h, h) == 0.0
+    for q in (0.3, 0.9, 1.2, 1.7, 1.99):
+        r, e = q * h, 1e-7 * h
+        fd = (orc.sph_W(r + e, h) - orc.sph_W(r - e, h)) / (2 * e)
+        assert orc.sph_dWdr(r, h) == pytest.approx(fd, rel=1e-6)
+
+
+def _sph_lattice_density(dp, h, m):
+    """rho = m sum over SC lattice vectors (incl. 0) of W -- enumeration."""
+    from oracle import oracle as o
+    k = int(math.ceil(2 * h / dp)) + 1
+    s = 0.0
+    for n in itertools.product(range(-k, k + 1), repeat=3):
+        s += o.sph_W(dp * math.sqrt(sum(c * c for c in n)), h)
+    return m * s
+
+
+def test_sph_interior_density_and_hydrostatic_balance(orc):
+    """Interior fluid particle of a full lattice: rho = lattice sum of m W;
+    sum_q grad W = 0 so a = g (Eq. 1, readings R16-R18)."""
+    s = inputs.cfg4(dp=1.0 / 16.0)
+    p = s.params
+    x = s.pos[:, :3].astype(np.float64)
+    centre = np.array([0.5, 0.5, 0.25])
+    i = int(np.argmin(((x - centre) ** 2).sum(1)))
+    assert s.kind[i] == 0
+    rho, P = orc.sph_density_rows(s.pos, s.lo, s.hi, s.periodic, p, rows=[i])
+    ref = _sph_lattice_density(p["dp"], p["h"], p["mass"])
+    assert rho[0] == pytest.approx(ref, rel=1e-12)
+    assert rho[0] == pytest.approx(997.2618283038771, rel=1e-9)  # SURVEY §8(c) pin value
+    assert P[0] == pytest.approx(p["b"] * ((rho[0] / p["rho0"]) ** 7 - 1), rel=1e-12)
+    n = s.n
+    rho_all = np.full(n, rho[0])
+    P_all = np.full(n, P[0])
+    a = orc.sph_accel_rows(s.pos, s.vel, rho_all, P_all, s.kind, s.lo, s.hi, s.periodic, p,
+                           rows=[i])
+    assert a[0] == pytest.approx(p["g"], abs=1e-9)
+
+
+def test_sph_two_particle_pressure_repels(orc):
+    """Two fluid particles at distance dp, rho = rho0, P = 1000 Pa:
+    a_p = -m (2P / rho0^2) W'(dp) (x_p - x_q)/r  (W' by finite difference);
+    antisymmetric; positive pressure repels (reading R17)."""
+    s = inputs.cfg4(dp=1.0 / 160.0)
+    p = dict(s.params)
+    p["g"] = (0.0, 0.0, 0.0)
+    dp = p["dp"]
+    pos = np.array([[0.5, 0.5, 0.25, 0], [0.5 + dp, 0.5, 0.25, 0]], np.float32)
+    r = float(np.float64(pos[1, 0]) - np.float64(pos[0, 0]))
+    vel = np.zeros_like(pos)
+    rho = np.array([1000.0, 1000.0])
+    P = np.array([1000.0, 1000.0])
+    a = orc.sph_accel_rows(pos, vel, rho, P, np.zeros(2, np.int32), s.lo, s.hi, s.periodic, p)
+    e = 1e-9
+    dW = (orc.sph_W(r + e, p["h"]) - orc.sph_W(r - e, p["h"])) / (2 * e)
+    expect = -p["mass"] * (2000.0 / 1e6) * dW * (-1.0)  # (x_p - x_q)/r = -1 along x
+    assert a[0, 0] == pytest.approx(expect, rel=1e-6)
+    assert a[0, 0] < 0 < a[1, 0]  # repulsion
+    assert a[1] == pytest.approx(-a[0], rel=1e-12)
+    assert abs(a[0, 0]) == pytest.approx(34.8196, rel=1e-4)  # SURVEY §8(c) pin value
+
+
+def test_sph_viscosity_branches(orc):
+    """Eq. 5 (reading R20): Pi = 0 for v = 0 and for a
+    receding pair; an approaching pair is pushed apart more.  Parity of the
+    constants alpha, eta is unpinned by the paper."""
+    s = inputs.cfg4(dp=1.0 / 160.0)
+    p = dict(s.params)
+    p["g"] = (0.0, 0.0, 0.0)
+    dp = p["dp"]
+    pos = np.array([[0.5, 0.5, 0.25, 0], [0.5 + dp, 0.5, 0.25, 0]], np.float32)
+    rho = np.array([1000.0, 1000.0])
+    P = np.array([500.0, 500.0])
+    kinds = np.zeros(2, np.int32)
+
+    def acc(vx):
+        vel = np.zeros_like(pos)
+        vel[0, 0], vel[1, 0] = vx, -vx
+        return orc.sph_accel_rows(pos, vel, rho, P, kinds, s.lo, s.hi, s.periodic, p)
+
+    a0, a_app, a_rec = acc(0.0), acc(0.5), acc(-0.5)
+    assert np.array_equal(a0, a_rec)
+    assert a_app[0, 0] < a0[0, 0] < 0  # approaching: extra repulsion of p (to -x)
+
+
+def test_sph_momentum_conservation_random(orc):
+    """sum_p m (a_p - g) = 0 for an all-fluid system: the Eq. 1 pair terms
+    (incl. Pi_pq) are antisymmetric."""
+    s = inputs.random_box(400, 0.08, (21,), periodic=(1, 1, 1))
+    p = dict(inputs.cfg4(dp=1.0 / 160.0).params)
+    r = np.random.default_rng(3)
+    vel = np.zeros_like(s.pos)
+    vel[:, :3] = r.uniform(-0.2, 0.2, (s.n, 3))
+    rho, P = orc.sph_density_rows(s.pos, s.lo, s.hi, s.periodic, p)
+    a = orc.sph_accel_rows(s.pos, vel, rho, P, np.zeros(s.n, np.int32), s.lo, s.hi,
+                           s.periodic, p)
+    net = (a - np.asarray(p["g"])).sum(0)
+    assert np.all(np.abs(net) < 1e-9 * np.abs(a - np.asarray(p["g"])).sum())
