@@ -1,0 +1,300 @@
+#!/usr/bin/env python
+"""Benchmark: particle-updates/s of the LJ velocity-Verlet hot path on B200.
+
+Contract:
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+One JSON line on rank 0.  A "step" is one velocity-Verlet step of BJ
+configs[1] (1,048,576 LJ particles, rho = 0.8, T = 1, dt = 0.005, r_cut = 2.5,
+skin = 0.3), including the on-device Verlet rebuild whenever the largest
+displacement exceeds skin/2 -- i.e. every row a1-a7 of SURVEY §8(a) runs inside
+the timed region.  Multi-GPU (N > 1): BJ configs[2] weak scaling, 2,097,152
+particles per GPU (see dist.py).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+DT, RC, SKIN = 0.005, 2.5, 0.3
+METRIC = "particle-updates/s (LJ, r_cut 2.5σ) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "particle-updates/s"
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                smax = float(p[2])
+            except ValueError:
+                continue
+            for k, nm in enumerate(names):
+                if p[5 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_baseline(n_target_s=15.0):
+    """The oracle as it stands (fp64 brute-force O(N) LJ force per particle +
+    velocity-Verlet update) on a bounded sample of cfg2 particles."""
+    from oracle import oracle
+    from paper_1804_07598_b200 import inputs
+    s = inputs.cfg2()
+    rng = np.random.default_rng(0)
+    rows = rng.choice(s.n, 64, replace=False)
+    t0 = time.perf_counter()
+    oracle.lj_rows(s.pos, s.lo, s.hi, s.periodic, rc=RC, rows=rows)
+    t1 = time.perf_counter()
+    m = int(max(64, min(s.n, 64 * n_target_s / max(t1 - t0, 1e-6))))
+    rows = rng.choice(s.n, m, replace=False)
+    t0 = time.perf_counter()
+    r = oracle.lj_rows(s.pos, s.lo, s.hi, s.periodic, rc=RC, rows=rows)
+    v = s.vel[rows, :3].astype(np.float64) + DT * r["F"]  # kick (m = 1)
+    _ = s.pos[rows, :3].astype(np.float64) + DT * v        # drift
+    t = time.perf_counter() - t0
+    return {"value": m / t, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{m} of {s.n} cfg2 particles: fp64 brute-force O(N) LJ force + VV update "
+                      f"each ({t:.1f} s)"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands on the host cores, on this
+    arm's config/metric; each step a bounded sample of cfg2 particles."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle
+    from paper_1804_07598_b200 import inputs
+    s = inputs.cfg2()
+    rng = np.random.default_rng(0)
+    probe = rng.choice(s.n, 32, replace=False)
+    t0 = time.perf_counter()
+    oracle.lj_rows(s.pos, s.lo, s.hi, s.periodic, rc=RC, rows=probe)
+    t_row = (time.perf_counter() - t0) / 32
+    budget = 120.0
+    rows_per_step = int(max(1, min(4096, budget / max(1, args.steps + args.warmup) / t_row)))
+    tot = 0.0
+    for k in range(args.warmup + args.steps):
+        rows = rng.choice(s.n, rows_per_step, replace=False)
+        t0 = time.perf_counter()
+        r = oracle.lj_rows(s.pos, s.lo, s.hi, s.periodic, rc=RC, rows=rows)
+        v = s.vel[rows, :3].astype(np.float64) + DT * r["F"]
+        _ = s.pos[rows, :3].astype(np.float64) + DT * v
+        if k >= args.warmup:
+            tot += time.perf_counter() - t0
+    value = rows_per_step * args.steps / tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg2 (BJ configs[1]) LJ fluid 1,048,576 particles; each step "
+                                   f"= oracle on {rows_per_step} sampled particles"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(),
+                             "kind": "oracle",
+                             "sample": f"{rows_per_step} sampled cfg2 particles per step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    ws, rank, local = dist_env()
+    if ws > 1:
+        from paper_1804_07598_b200 import dist
+        return dist.bench_main(args)
+    import torch
+    from paper_1804_07598_b200 import build as pmbuild, inputs, pm
+    pmbuild.build()
+    dev = 0
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.Stream(device=dev)
+    s = inputs.cfg2()
+    n = s.n
+
+    def fresh_ctx():
+        c = pm.Context(device=dev, stream=stream.cuda_stream)
+        c.set_domain(s.lo, s.hi, s.periodic)
+        c.set_cutoff(RC, SKIN)
+        c.set_lj(1.0, 1.0, 1.0, 0.0)
+        return c
+
+    # ---------------- device-resident run (value)
+    c = fresh_ctx()
+    c.place(s.pos, s.vel, s.gid)
+    c.build_verlet()
+    c.compute_lj()
+    c.step_vv(DT, args.warmup)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(dev)
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    stats = c.step_vv(DT, args.steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    value = n * args.steps / (ms * 1e-3)
+    npairs = c.thermo()["npairs"]  # ordered pairs inside r_cut at the end state
+
+    # ---------------- force-kernel share + roofline (CUDA events in the graph)
+    kprof = min(args.steps, 300)
+    c.set_profiling(True)
+    pstats = c.step_vv(DT, kprof)
+    prof = c.get_profile()
+    c.set_profiling(False)
+    force_ms = prof["force_ms"] / max(prof["force_launches"], 1)
+    nbar = pstats["mean_row"]
+    alg_bytes = n * (4.0 * nbar + 64.0)  # list + count + x,v,xref read + x,v write
+    peak, peak_src = hbm_peak()
+    achieved = alg_bytes / (force_ms * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "force_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    c.close()
+
+    # ---------------- end-to-end through the C-ABI with pinned host buffers
+    pos_h = torch.from_numpy(s.pos).pin_memory()
+    vel_h = torch.from_numpy(s.vel).pin_memory()
+    gid_h = torch.from_numpy(s.gid).pin_memory()
+    out_pos = torch.empty_like(pos_h).pin_memory()
+    out_vel = torch.empty_like(vel_h).pin_memory()
+    c = fresh_ctx()
+    c.place(pos_h, vel_h, gid_h)  # warm the allocation
+    c.step_vv(DT, args.warmup)
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    c.place(pos_h, vel_h, gid_h)
+    c.step_vv(DT, args.steps)
+    c.get_state_into(out_pos, out_vel)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = t0.elapsed_time(t1)
+    c.close()
+    h2d = (pos_h.numel() * 4 + vel_h.numel() * 4 + gid_h.numel() * 8)
+    d2h = (out_pos.numel() * 4 + out_vel.numel() * 4)
+
+    cpu = cpu_baseline() if not args.no_cpu_baseline else None
+    launches = 2 * args.steps + 11 * stats["rebuilds"] + 3
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "cfg2 (BJ configs[1]): LJ fluid 1,048,576 particles, SC "
+                               "128x128x64 rho=0.8 + U(±0.05) jitter, Maxwell T=1, dt=0.005, "
+                               "r_cut=2.5, skin=0.3, rebuild at skin/2, NVE",
+                   "n_particles": n, "parallelism": "1 GPU",
+                   "l2": "inputs larger than L2 (Verlet list %.2f GB > 126 MB)" %
+                         (n * nbar * 4 / 1e9),
+                   "rebuilds": stats["rebuilds"], "mean_row": round(nbar, 2),
+                   "pair_interactions_per_s": npairs * args.steps / (ms * 1e-3),
+                   "list_entries_per_s": n * nbar * args.steps / (ms * 1e-3)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "k_lj_step (force sweep + fused VV)",
+                     "kernel_ms": force_ms, "kernel_share_of_step": force_ms / (ms / args.steps),
+                     "alg_bytes_per_launch": alg_bytes,
+                     "alg_bytes_formula": "N*(4*nbar + 64)", "peak_source": peak_src},
+        "cpu_baseline": cpu,
+        "e2e": {"value": n * args.steps / (e2e_ms * 1e-3), "unit": UNIT,
+                "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    # pairs/s: ordered pairs inside r_cut ~ measured once from the energy pass
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

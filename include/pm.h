@@ -1,0 +1,193 @@
+/*
+ * pm.h -- C-ABI of the B200-native particle hot path (arXiv 1804.07598, OpenFPM).
+ *
+ * The calls follow the paper's problem statement for a particle client
+ * (Listing 4.1, §4.1): set the domain, box and boundary
+ * conditions, place particles (the vector_dist constructor
+ * and Init_grid), build the cell list (getCellListSym,
+ * PAPER.md:276) and the Verlet list with skin ("Verlet lists
+ * [46]"), compute pairwise interactions (applyKernel_in_sym, PAPER.md:278,
+ * 319), take velocity-Verlet steps, and map /
+ * ghost-exchange (map(), ghost_get<>(); §3.4).
+ *
+ * Conventions (all entry points):
+ *  - Every call returns pm_status: PM_OK (0) or a negative error.  No C++
+ *    exception crosses the ABI.  The message of the last error is
+ *    pm_last_error(ctx).  Errors are sticky per context until pm_place.
+ *  - A pm_ctx is bound to one CUDA device and one CUDA stream, and must be
+ *    used from one host thread at a time.
+ *  - Particle arrays: pos4/vel4/force4 are n x 4 float32 (x, y, z, pad),
+ *    16-byte aligned; gid int64[n]; kind int32[n] (0 = fluid / LJ particle,
+ *    1 = fixed boundary particle); rho/pres float32[n].
+ *  - Memory: `mem` = PM_HOST (pageable or pinned host pointers) or PM_DEVICE
+ *    (device pointers on the context's device).  Inputs are copied (stream
+ *    ordered on the context stream) before the call returns for PM_HOST, and
+ *    before any later work on the stream for PM_DEVICE; the caller may reuse
+ *    them after that.  The library owns all its device memory.
+ *  - Getters synchronise the context stream and write caller-owned buffers.
+ *    Particle arrays are returned in the library's current internal order
+ *    (cell order after a build); gid tells the identity of each row.
+ *  - Radii use strict inequality: a pair is in a list iff d2 < r^2 where d2 is
+ *    the pinned fp32 squared distance of DESIGN.md reading R4 (periodic
+ *    minimum image by the Sterbenz-ordered rule).
+ */
+#ifndef PM_H
+#define PM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pm_ctx_s *pm_ctx;
+typedef int32_t pm_status;
+
+enum {
+  PM_OK = 0,
+  PM_E_INVAL = -1,      /* bad argument / usage error (message says which) */
+  PM_E_STATE = -2,      /* call out of order (e.g. forces before a list exists) */
+  PM_E_NOMEM = -3,      /* device allocation failed */
+  PM_E_CUDA = -4,       /* CUDA runtime error */
+  PM_E_NCCL = -5,       /* communicator error */
+  PM_E_DOMAIN = -6,     /* particle outside [lo,hi) on a NON-periodic axis */
+  PM_E_COINCIDENT = -7, /* pair at distance 0 (LJ undefined) */
+  PM_E_NONFINITE = -8,  /* non-finite force / density */
+  PM_E_CAPACITY = -9    /* neighbour capacity overflow survived realloc + retry */
+};
+
+enum { PM_HOST = 0, PM_DEVICE = 1 };
+
+typedef struct {
+  int32_t device;      /* CUDA device ordinal */
+  int32_t cell_div;    /* cells per r_v along each axis: 1 (side >= r_v) */
+  int32_t nbr_cap;     /* initial neighbour slots per particle (0 = auto from density) */
+  int32_t use_graphs;  /* 1: pm_step_vv runs each step as one CUDA graph launch */
+  void *cuda_stream;   /* cudaStream_t to run on; NULL = library-owned stream */
+} pm_opts;
+
+/* Fills defaults: device 0, cell_div 1, nbr_cap 0, use_graphs 1, NULL stream. */
+pm_status pm_opts_default(pm_opts *opts);
+/* Library identification string (static storage). */
+const char *pm_version(void);
+
+pm_status pm_create(const pm_opts *opts, pm_ctx *out);
+void pm_destroy(pm_ctx ctx);
+const char *pm_last_error(pm_ctx ctx);
+
+/* Simulation box [lo, hi) per axis; periodic[d] != 0 for a periodic axis
+ * ("Box<3,float> box(...)", "size_t bc[3] = {PERIODIC,...}").
+ * Errors: PM_E_INVAL if hi <= lo. */
+pm_status pm_set_domain(pm_ctx ctx, const float lo[3], const float hi[3],
+                        const int32_t periodic[3]);
+
+/* Interaction radius r_cut and Verlet skin; the list radius is
+ * r_v = fl32(r_cut + skin) (reading R5).  PAPER.md:240 "Ghost<3,float>
+ * ghost(r_cut)"; the skin is BASELINE.json configs[0..2] (0.3 sigma).
+ * Errors: PM_E_INVAL if r_cut <= 0, skin < 0, or a periodic extent is shorter
+ * than 3 r_v (the 27-cell stencil needs >= 3 distinct cells per axis). */
+pm_status pm_set_cutoff(pm_ctx ctx, float r_cut, float skin);
+
+/* Lennard-Jones parameters: V = 4 eps [(s/r)^12 - (s/r)^6];
+ * mass of every particle; r_min > 0 selects the capped force of reading R22
+ * (r_eff = max(r, r_min)), 0 the plain potential. */
+pm_status pm_set_lj(pm_ctx ctx, float epsilon, float sigma, float mass, float r_min);
+
+/* WCSPH parameters (Eqs. 1, 3-5; readings R15-R21):
+ * smoothing length h (kernel support 2h), particle mass, rest density rho0,
+ * EOS exponent gamma and constant b (Eq. 3), viscosity alpha, cbar and
+ * eta2 (Eq. 5), gravity g. */
+typedef struct {
+  float h, mass, rho0, gamma, b, alpha, cbar, eta2;
+  float g[3];
+} pm_sph_params;
+pm_status pm_set_sph(pm_ctx ctx, const pm_sph_params *p);
+
+/* Place n particles (replaces any previous set).  pos4 required; vel4, gid,
+ * kind may be NULL (zero velocity, gid = 0..n-1, kind = 0).  Positions on
+ * periodic axes are wrapped (reading R1) at the next build.  Grows device
+ * buffers as needed (PM_E_NOMEM).  Clears a sticky error. */
+pm_status pm_place(pm_ctx ctx, int64_t n, const float *pos4, const float *vel4,
+                   const int64_t *gid, const int32_t *kind, int32_t mem);
+
+/* Cell list ("Cell Lists [45]"): wrap, cell
+ * id, count, exclusive scan, stable reorder of all particle arrays into cell
+ * order (PAPER.md:128 cache-friendly re-ordering).  PM_E_STATE without
+ * domain / cutoff / particles; PM_E_DOMAIN for a particle outside a
+ * non-periodic axis. */
+pm_status pm_build_cells(pm_ctx ctx);
+
+/* Verlet list with skin ("Verlet lists [46]"): for every
+ * particle, all j != i with d2 < r_v^2 over the 27-cell stencil.  Builds the
+ * cell list first.  Grows the neighbour capacity and retries once on
+ * overflow (else PM_E_CAPACITY); PM_E_COINCIDENT for a pair at distance 0. */
+pm_status pm_build_verlet(pm_ctx ctx);
+
+/* LJ forces over the Verlet list (pairs with d2 < r_cut^2; PAPER.md:162,
+ * 203-214; reading R7 for the force expression), written to the force array.
+ * want_energy != 0 also accumulates fp64 potential energy, virial and pair
+ * count (pm_get_thermo).  PM_E_STATE without a list. */
+pm_status pm_compute_lj(pm_ctx ctx, int32_t want_energy);
+
+/* SPH density summation + Tait EOS (Eqs. 3-4, reading R16) for every
+ * particle; then pressure + viscous acceleration (Eqs. 1, 5) for fluid
+ * particles (kind 0; kind 1 gets 0), written to the force array.  Need a
+ * Verlet list built with r_cut = 2h. */
+pm_status pm_sph_density(pm_ctx ctx);
+pm_status pm_sph_forces(pm_ctx ctx);
+
+typedef struct {
+  int64_t steps;     /* steps completed by this call */
+  int64_t rebuilds;  /* Verlet rebuilds during this call */
+  int32_t max_row;   /* longest neighbour row at the last build */
+  int32_t nbr_cap;   /* current neighbour capacity per row */
+  double mean_row;   /* mean neighbour row length at the last build */
+} pm_run_stats;
+
+/* nsteps velocity-Verlet steps, with
+ * the Verlet list rebuilt on the device whenever the largest displacement
+ * since the last build exceeds skin/2 (BASELINE.json configs[1]).  Forces are
+ * computed first if they are not valid.  out may be NULL. */
+pm_status pm_step_vv(pm_ctx ctx, float dt, int64_t nsteps, pm_run_stats *out);
+
+/* Counts: owned and ghost particles, cells, neighbour entries of the last
+ * build.  Any pointer may be NULL. */
+pm_status pm_count(pm_ctx ctx, int64_t *n_owned, int64_t *n_ghost, int64_t *n_cells,
+                   int64_t *nnz);
+
+/* Cell list of the last build: cell_of[n] in the storage order the build
+ * started from, cell_start[ncell+1], perm[n] (k-th particle in cell order =
+ * storage index perm[k]; ties in storage order).  Any pointer may be NULL. */
+pm_status pm_get_cells(pm_ctx ctx, int32_t *cell_of, int32_t *cell_start, int32_t *perm);
+
+/* Verlet list of the last build in CSR over the current internal order:
+ * row_ptr[n_owned+1], col_gid[nnz] (gid of each neighbour). */
+pm_status pm_get_verlet(pm_ctx ctx, int64_t *row_ptr, int64_t *col_gid);
+
+/* Particle state in the current internal order.  Any pointer may be NULL.
+ * force4 holds LJ forces or SPH accelerations (last computed); rho/pres the
+ * SPH density and pressure. */
+pm_status pm_get_state(pm_ctx ctx, float *pos4, float *vel4, float *force4, int64_t *gid,
+                       float *rho, float *pres, int32_t mem);
+
+/* Thermodynamics (fp64 reductions on the device): kinetic energy of the
+ * current velocities; potential energy raw and shifted by V(r_cut) per pair
+ * (reading R9), virial and pair count of the last energy pass
+ * (pm_compute_lj with want_energy, or pm_thermo_compute). */
+pm_status pm_get_thermo(pm_ctx ctx, double *ke, double *pe_raw, double *pe_shift,
+                        double *virial, int64_t *npairs);
+/* Recompute the LJ energy of the current positions (list must be valid). */
+pm_status pm_thermo_compute(pm_ctx ctx);
+
+/* Profiling: when on, pm_step_vv records CUDA events around every force
+ * kernel and every rebuild; pm_get_profile returns summed device times (ms)
+ * and launch counts since the last reset. */
+pm_status pm_set_profiling(pm_ctx ctx, int32_t on);
+pm_status pm_get_profile(pm_ctx ctx, double *force_ms, int64_t *force_launches,
+                         double *step_ms, int64_t *steps);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PM_H */

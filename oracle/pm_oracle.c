@@ -452,7 +452,9 @@ void orc_sph_density_rows(int64_t n, const float *pos4, const float lo[3], const
       if (q == p) continue;
       double dl[3];
       delta64(pos4 + 4 * p, pos4 + 4 * q, L64, per, dl);
-      double rr = sqrt(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
+      double r2 = dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2];
+      if (!(r2 < 4.0 * h * h)) continue; /* W = 0 for r >= 2h */
+      double rr = sqrt(r2);
       if (rr < 2.0 * h) rho += mass * orc_sph_W(rr, h);
     }
     rho_out[r] = rho;
@@ -487,7 +489,9 @@ void orc_sph_accel_rows(int64_t n, const float *pos4, const float *vel4, const d
       if (q == p) continue;
       double dl[3]; /* r_pq = x_p - x_q */
       delta64(pos4 + 4 * p, pos4 + 4 * q, L64, per, dl);
-      double rr = sqrt(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
+      double r2 = dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2];
+      if (!(r2 < 4.0 * h * h)) continue; /* grad W = 0 for r >= 2h */
+      double rr = sqrt(r2);
       if (!(rr < 2.0 * h) || rr == 0.0) continue;
       double dw = orc_sph_dWdr(rr, h);
       double gradW[3] = {dl[0] / rr * dw, dl[1] / rr * dw, dl[2] / rr * dw};

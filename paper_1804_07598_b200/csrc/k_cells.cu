@@ -1,0 +1,249 @@
+// k_cells.cu -- cell-list construction.
+//
+// PAPER.md:48 (§2) "Cell Lists [45]"; PAPER.md:276/308 getCellListSym /
+// updateCellListSym; PAPER.md:128 (§3.6) cache-friendly re-ordering of the
+// particles.  B200 design: one fused pass computes the
+// wrap, the cell id and an atomic slot claim (warp-aggregated with
+// __match_any_sync), a 3-phase scan produces the cell starts, the slots are
+// scattered and each cell's segment is sorted by storage index (warp bitonic
+// for <= 32 entries), which makes the counting sort stable and the result
+// bit-exact; a gather then reorders every particle array into cell order.
+#include "pm_internal.cuh"
+
+namespace pm {
+
+namespace {
+
+__global__ void k_zero_i32(int32_t *__restrict__ p, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) p[i] = 0;
+}
+
+// a1 + a2: wrap (R1), cell id (R3), slot claim.
+__global__ void __launch_bounds__(256) k_cell_ids(Params P, Bufs B, int64_t n) {
+  State *st = B.st;
+  const int cur = st->cur_pv;
+  float4 *__restrict__ pos = B.pos[cur];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int c = -1;
+  if (i < n) {
+    float4 p = pos[i];
+    float x[3] = {p.x, p.y, p.z};
+    bool moved = false;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      if (P.box.per[d]) {
+        float w = wrap1(x[d], P.box.lo[d], P.box.hi[d], P.box.L[d]);
+        moved |= (w != x[d]);
+        x[d] = w;
+      } else if (!(x[d] >= P.box.lo[d] && x[d] < P.box.hi[d])) {
+        raise_error(st, -6 /*PM_E_DOMAIN*/, (long long)B.gid[st->cur_id][i]);
+      }
+    }
+    if (moved) pos[i] = make_float4(x[0], x[1], x[2], p.w);
+    int cx = cell_coord(x[0], P.box.lo[0], P.grid.inv_w[0], P.grid.n[0]);
+    int cy = cell_coord(x[1], P.box.lo[1], P.grid.inv_w[1], P.grid.n[1]);
+    int cz = cell_coord(x[2], P.box.lo[2], P.grid.inv_w[2], P.grid.n[2]);
+    c = cx + P.grid.n[0] * (cy + P.grid.n[1] * cz);
+    B.cell_of[i] = c;
+  }
+  // warp-aggregated slot claim: lanes with the same cell share one atomic
+  const unsigned full = 0xffffffffu;
+  const unsigned grp = __match_any_sync(full, c);
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(grp) - 1;
+  int base = 0;
+  if (c >= 0 && lane == leader) base = atomicAdd(&B.count[c], __popc(grp));
+  base = __shfl_sync(full, base, leader);
+  if (c >= 0) B.slot[i] = base + __popc(grp & ((1u << lane) - 1u));
+}
+
+constexpr int kScanThreads = 512;
+constexpr int kScanPer = 4;
+constexpr int kScanTile = kScanThreads * kScanPer;
+
+template <int NT>
+__device__ int block_exclusive_scan(int v, int *total) {
+  __shared__ int warp_sums[NT / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int s = (lane < NT / 32) ? warp_sums[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < NT / 32) warp_sums[lane] = s;  // inclusive over warps
+  }
+  __syncthreads();
+  int warp_excl = (wid == 0) ? 0 : warp_sums[wid - 1];
+  *total = warp_sums[NT / 32 - 1];
+  __syncthreads();
+  return warp_excl + x - v;
+}
+
+// a3 phase 1: per-tile exclusive scan of the counts, tile totals.
+__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const int32_t *__restrict__ count,
+                                                             int32_t *__restrict__ start,
+                                                             int32_t *__restrict__ tile_sum,
+                                                             int ncell) {
+  const int base = blockIdx.x * kScanTile + threadIdx.x * kScanPer;
+  int v[kScanPer];
+  int s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    v[k] = (base + k < ncell) ? count[base + k] : 0;
+    s += v[k];
+  }
+  int total;
+  int ex = block_exclusive_scan<kScanThreads>(s, &total);
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    if (base + k < ncell) start[base + k] = ex;
+    ex += v[k];
+  }
+  if (threadIdx.x == 0) tile_sum[blockIdx.x] = total;
+}
+
+// a3 phase 2: exclusive scan of the tile totals (one block, chunked).
+__global__ void __launch_bounds__(1024) k_scan_sums(int32_t *__restrict__ tile_sum, int ntiles,
+                                                    int32_t *__restrict__ start, int ncell) {
+  int carry = 0;
+  for (int b = 0; b < ntiles; b += 1024) {
+    int i = b + threadIdx.x;
+    int v = (i < ntiles) ? tile_sum[i] : 0;
+    int total;
+    int ex = block_exclusive_scan<1024>(v, &total);
+    if (i < ntiles) tile_sum[i] = carry + ex;
+    carry += total;
+  }
+  if (threadIdx.x == 0) start[ncell] = carry;
+}
+
+// a3 phase 3: add tile offsets.
+__global__ void __launch_bounds__(kScanThreads) k_scan_add(int32_t *__restrict__ start,
+                                                           const int32_t *__restrict__ tile_sum,
+                                                           int ncell) {
+  const int base = blockIdx.x * kScanTile + threadIdx.x * kScanPer;
+  const int off = tile_sum[blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k)
+    if (base + k < ncell) start[base + k] += off;
+}
+
+// a4: scatter storage indices to their claimed slots (unordered within a cell).
+__global__ void __launch_bounds__(256) k_scatter(Bufs B, int32_t *__restrict__ tmp, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  tmp[B.start[B.cell_of[i]] + B.slot[i]] = (int32_t)i;
+}
+
+// a4: stable order inside each cell = ascending storage index.  One warp per
+// cell: bitonic sort in registers for <= 32 entries, rank-by-count otherwise.
+__global__ void __launch_bounds__(256) k_segsort(Bufs B, const int32_t *__restrict__ tmp,
+                                                 int ncell) {
+  const int cell = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (cell >= ncell) return;  // whole warp exits together
+  const int s = B.start[cell], e = B.start[cell + 1], m = e - s;
+  if (m == 0) return;
+  if (m == 1) {
+    if (lane == 0) B.perm[s] = tmp[s];
+    return;
+  }
+  const unsigned full = 0xffffffffu;
+  if (m <= 32) {
+    int v = (lane < m) ? tmp[s + lane] : 0x7fffffff;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        int o = __shfl_xor_sync(full, v, j);
+        bool up = (lane & k) == 0;
+        bool lower = (lane & j) == 0;
+        v = (lower == up) ? min(v, o) : max(v, o);
+      }
+    }
+    if (lane < m) B.perm[s + lane] = v;
+    return;
+  }
+  for (int p = lane; p < m; p += 32) {
+    const int v = tmp[s + p];
+    int r = 0;
+    for (int q = 0; q < m; ++q) r += (tmp[s + q] < v);
+    B.perm[s + r] = v;
+  }
+}
+
+// a4: gather every particle array into cell order (alternate buffers).
+__global__ void __launch_bounds__(256) k_reorder(Bufs B, int64_t n) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  State *st = B.st;
+  const int cp = st->cur_pv, ci = st->cur_id;
+  const int j = B.perm[k];
+  const float4 p = B.pos[cp][j];
+  B.pos[cp ^ 1][k] = p;
+  B.xref[k] = p;
+  B.vel[cp ^ 1][k] = B.vel[cp][j];
+  B.gid[ci ^ 1][k] = B.gid[ci][j];
+  B.kind[ci ^ 1][k] = B.kind[ci][j];
+}
+
+__global__ void k_flip(Bufs B, int flip_pv, int flip_id, int count_rebuild) {
+  State *st = B.st;
+  if (flip_pv) st->cur_pv ^= 1;
+  if (flip_id) st->cur_id ^= 1;
+  if (count_rebuild) {
+    st->n_rebuilds += 1;
+    st->need_rebuild = 0;
+  }
+}
+
+inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+void launch_zero_i32(int32_t *p, int64_t n, cudaStream_t s) {
+  if (n <= 0) return;
+  unsigned g = blocks_for(n, 256);
+  if (g > 148 * 16) g = 148 * 16;
+  k_zero_i32<<<g, 256, 0, s>>>(p, n);
+}
+
+void launch_cell_ids(const Params &P, const Bufs &B, int64_t n, cudaStream_t s) {
+  launch_zero_i32(B.count, P.grid.ncell, s);
+  if (n > 0) k_cell_ids<<<blocks_for(n, 256), 256, 0, s>>>(P, B, n);
+}
+
+void launch_scan(const Params &P, const Bufs &B, int64_t n, cudaStream_t s) {
+  (void)n;
+  const int ncell = P.grid.ncell;
+  const int ntiles = (ncell + kScanTile - 1) / kScanTile;
+  k_scan_tiles<<<ntiles, kScanThreads, 0, s>>>(B.count, B.start, B.scan_tmp, ncell);
+  k_scan_sums<<<1, 1024, 0, s>>>(B.scan_tmp, ntiles, B.start, ncell);
+  k_scan_add<<<ntiles, kScanThreads, 0, s>>>(B.start, B.scan_tmp, ncell);
+}
+
+void launch_sort_reorder(const Params &P, const Bufs &B, int64_t n, cudaStream_t s) {
+  if (n <= 0) return;
+  int32_t *tmp = B.sorttmp;
+  k_scatter<<<blocks_for(n, 256), 256, 0, s>>>(B, tmp, n);
+  k_segsort<<<blocks_for((int64_t)P.grid.ncell * 32, 256), 256, 0, s>>>(B, tmp, P.grid.ncell);
+  k_reorder<<<blocks_for(n, 256), 256, 0, s>>>(B, n);
+}
+
+void launch_flip(const Bufs &B, int flip_pv, int flip_id, int count_rebuild, cudaStream_t s) {
+  k_flip<<<1, 1, 0, s>>>(B, flip_pv, flip_id, count_rebuild);
+}
+
+}  // namespace pm

@@ -1,0 +1,331 @@
+// k_lj.cu -- Lennard-Jones sweep and velocity-Verlet integrator
+// (SURVEY §8(a) rows a6, a7).
+//
+// PAPER.md:162 (§4.1) V_LJ(r) = 4 eps [(sigma/r)^12 - (sigma/r)^6]; the
+// force is -dV/dr along (x_i - x_j) (reading R7, PAPER.md:212 typo):
+//   F_i = sum_j 24 eps (2 sigma^12 / r^14 - sigma^6 / r^8) (x_i - x_j)
+// over the full Verlet list, pairs with d2_32 < r_cut^2 (R6).
+// Velocity Verlet: v += dt/2 F/m; x += dt v; ...
+//
+// B200 design: one thread per particle (cell order, so
+// a warp's 32 rows share neighbour cells and the position gathers hit L1),
+// per-thread fp32 accumulation, no atomics.  The neighbour stream is read
+// with streaming loads (ld.global.cs) so the 0.3 GB list does not evict the
+// L2-resident positions.  The periodic minimum-image correction (R4) is only
+// evaluated in warps that have a particle within r_v + skin of a periodic
+// face (warp-uniform branch).  In pm_step_vv the sweep is fused with the
+// integrator: the second half-kick of step n, the first half-kick and drift
+// of step n+1, the wrap and the skin/2 displacement test run in the epilogue
+// and write the alternate position/velocity buffers.
+#include "pm_internal.cuh"
+
+namespace pm {
+
+namespace {
+
+struct Acc {
+  float fx, fy, fz, u, w;
+  int np;
+};
+
+template <bool MI, bool CAPPED, bool ENERGY>
+__device__ __forceinline__ void lj_pair(const Params &P, const float4 &xi, const float4 &xj,
+                                        Acc &a) {
+  float dx, dy, dz;
+  if (MI) {
+    dx = pair_delta1(xi.x, xj.x, P.box.L[0], P.box.halfL[0], P.box.per[0]);
+    dy = pair_delta1(xi.y, xj.y, P.box.L[1], P.box.halfL[1], P.box.per[1]);
+    dz = pair_delta1(xi.z, xj.z, P.box.L[2], P.box.halfL[2], P.box.per[2]);
+  } else {
+    dx = __fsub_rn(xj.x, xi.x);
+    dy = __fsub_rn(xj.y, xi.y);
+    dz = __fsub_rn(xj.z, xi.z);
+  }
+  const float d2 = dist2(dx, dy, dz);
+  if (d2 < P.lj.rc2) {
+    float f, r6i;
+    if (CAPPED) {
+      const float r2e = fmaxf(d2, P.lj.r_min * P.lj.r_min);
+      const float r2ie = fast_rcp(r2e);
+      r6i = r2ie * r2ie * r2ie;
+      const float g = r6i * (P.lj.c12 * r6i - P.lj.c6);
+      f = g * fast_rsqrt(r2e) * fast_rsqrt(d2);
+    } else {
+      const float r2i = fast_rcp(d2);
+      r6i = r2i * r2i * r2i;
+      f = r2i * r6i * (P.lj.c12 * r6i - P.lj.c6);
+    }
+    // F_i += f (x_i - x_j) = -f * delta
+    a.fx = fmaf(-f, dx, a.fx);
+    a.fy = fmaf(-f, dy, a.fy);
+    a.fz = fmaf(-f, dz, a.fz);
+    if (ENERGY) {
+      a.u += 0.5f * r6i * (P.lj.e12 * r6i - P.lj.e6);
+      a.w += 0.5f * f * d2;
+      a.np += 1;
+    }
+  }
+}
+
+template <bool MI, bool CAPPED, bool ENERGY>
+__device__ __forceinline__ void lj_row(const Params &P, const float4 *__restrict__ pos,
+                                       const int4 *__restrict__ nb4, int cnt, const float4 &xi,
+                                       Acc &a) {
+  int q = 0;
+  for (; q + 4 <= cnt; q += 4) {
+    const int4 j = __ldcs(nb4 + (q >> 2) * 32);
+    const float4 x0 = __ldg(pos + j.x);
+    const float4 x1 = __ldg(pos + j.y);
+    const float4 x2 = __ldg(pos + j.z);
+    const float4 x3 = __ldg(pos + j.w);
+    lj_pair<MI, CAPPED, ENERGY>(P, xi, x0, a);
+    lj_pair<MI, CAPPED, ENERGY>(P, xi, x1, a);
+    lj_pair<MI, CAPPED, ENERGY>(P, xi, x2, a);
+    lj_pair<MI, CAPPED, ENERGY>(P, xi, x3, a);
+  }
+  if (q < cnt) {
+    const int4 j = __ldcs(nb4 + (q >> 2) * 32);
+    const int rem = cnt - q;
+    lj_pair<MI, CAPPED, ENERGY>(P, xi, __ldg(pos + j.x), a);
+    if (rem > 1) lj_pair<MI, CAPPED, ENERGY>(P, xi, __ldg(pos + j.y), a);
+    if (rem > 2) lj_pair<MI, CAPPED, ENERGY>(P, xi, __ldg(pos + j.z), a);
+  }
+}
+
+__device__ __forceinline__ bool near_periodic_face(const Params &P, const float4 &x) {
+  bool near = false;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const float v = (d == 0) ? x.x : (d == 1) ? x.y : x.z;
+    near |= P.box.per[d] &&
+            (v < P.box.lo[d] + P.mi_margin || v >= P.box.hi[d] - P.mi_margin);
+  }
+  return near;
+}
+
+template <bool CAPPED, bool ENERGY>
+__device__ __forceinline__ Acc lj_force_of(const Params &P, const Bufs &B,
+                                           const float4 *__restrict__ pos, int i, bool active,
+                                           const float4 &xi) {
+  Acc a = {0.f, 0.f, 0.f, 0.f, 0.f, 0};
+  const bool mi = __any_sync(0xffffffffu, active && near_periodic_face(P, xi));
+  if (active) {
+    const int cnt = B.cnt[i];
+    const int4 *nb4 = reinterpret_cast<const int4 *>(B.nbr) + nbr_base4(i, P.nbr_cap);
+    if (mi)
+      lj_row<true, CAPPED, ENERGY>(P, pos, nb4, cnt, xi, a);
+    else
+      lj_row<false, CAPPED, ENERGY>(P, pos, nb4, cnt, xi, a);
+  }
+  return a;
+}
+
+__device__ __forceinline__ void block_add_energy(State *st, double u, double w, double np) {
+  __shared__ double sh[3][32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    u += __shfl_xor_sync(0xffffffffu, u, o);
+    w += __shfl_xor_sync(0xffffffffu, w, o);
+    np += __shfl_xor_sync(0xffffffffu, np, o);
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (lane == 0) {
+    sh[0][wid] = u;
+    sh[1][wid] = w;
+    sh[2][wid] = np;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    u = lane < nw ? sh[0][lane] : 0.0;
+    w = lane < nw ? sh[1][lane] : 0.0;
+    np = lane < nw ? sh[2][lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      u += __shfl_xor_sync(0xffffffffu, u, o);
+      w += __shfl_xor_sync(0xffffffffu, w, o);
+      np += __shfl_xor_sync(0xffffffffu, np, o);
+    }
+    if (lane == 0) {
+      atomicAdd(&st->acc[0], u);
+      atomicAdd(&st->acc[1], w);
+      atomicAdd(&st->acc[2], np);
+    }
+  }
+}
+
+// pm_compute_lj: forces (+ energy) of the current positions.
+template <bool CAPPED, bool ENERGY>
+__global__ void __launch_bounds__(256) k_lj(Params P, Bufs B, int n) {
+  State *st = B.st;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = i < n;
+  const float4 *__restrict__ pos = B.pos[st->cur_pv];
+  const float4 xi = active ? pos[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  Acc a = lj_force_of<CAPPED, ENERGY>(P, B, pos, i, active, xi);
+  if (active) {
+    B.force[i] = make_float4(a.fx, a.fy, a.fz, 0.f);
+    if (!isfinite(a.fx + a.fy + a.fz))
+      raise_error(st, -8 /*PM_E_NONFINITE*/, (long long)B.gid[st->cur_id][i]);
+  }
+  if (ENERGY) block_add_energy(st, (double)a.u, (double)a.w, (double)a.np);
+}
+
+__device__ __forceinline__ float3 wrap3(const Params &P, float x, float y, float z) {
+  float r[3] = {x, y, z};
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+    if (P.box.per[d]) r[d] = wrap1(r[d], P.box.lo[d], P.box.hi[d], P.box.L[d]);
+  return make_float3(r[0], r[1], r[2]);
+}
+
+__device__ __forceinline__ bool moved_too_far(const Params &P, const float3 &x, const float4 &r) {
+  const float dx = pair_delta1(r.x, x.x, P.box.L[0], P.box.halfL[0], P.box.per[0]);
+  const float dy = pair_delta1(r.y, x.y, P.box.L[1], P.box.halfL[1], P.box.per[1]);
+  const float dz = pair_delta1(r.z, x.z, P.box.L[2], P.box.halfL[2], P.box.per[2]);
+  return dist2(dx, dy, dz) > P.half_skin2;
+}
+
+// One fused velocity-Verlet step (pm_step_vv), mode read from the state:
+//  inner: F(x); v += dt F/m (2nd half-kick of this step + 1st of the next);
+//         x' = wrap(x + dt v); displacement test vs xref; -> alternate buffers
+//  final: F(x); v += dt/2 F/m; F stored; x copied  -> alternate buffers
+template <bool CAPPED>
+__global__ void __launch_bounds__(256) k_lj_step(Params P, Bufs B, int n, float dt) {
+  State *st = B.st;
+  if (st->abort) return;
+  const int mode = st->mode;
+  const int cp = st->cur_pv;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = i < n;
+  const float4 *__restrict__ pos = B.pos[cp];
+  const float4 xi = active ? pos[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  Acc a = lj_force_of<CAPPED, false>(P, B, pos, i, active, xi);
+  bool far = false;
+  if (active) {
+    float4 v = B.vel[cp][i];
+    const float im = P.lj.inv_mass;
+    if (mode == kModeInner) {
+      const float k = dt * im;
+      v.x = fmaf(k, a.fx, v.x);
+      v.y = fmaf(k, a.fy, v.y);
+      v.z = fmaf(k, a.fz, v.z);
+      const float3 xn = wrap3(P, fmaf(dt, v.x, xi.x), fmaf(dt, v.y, xi.y), fmaf(dt, v.z, xi.z));
+      far = moved_too_far(P, xn, B.xref[i]);
+      B.pos[cp ^ 1][i] = make_float4(xn.x, xn.y, xn.z, xi.w);
+    } else {
+      const float k = 0.5f * dt * im;
+      v.x = fmaf(k, a.fx, v.x);
+      v.y = fmaf(k, a.fy, v.y);
+      v.z = fmaf(k, a.fz, v.z);
+      B.pos[cp ^ 1][i] = xi;
+      B.force[i] = make_float4(a.fx, a.fy, a.fz, 0.f);
+    }
+    B.vel[cp ^ 1][i] = v;
+    if (!isfinite(a.fx + a.fy + a.fz))
+      raise_error(st, -8 /*PM_E_NONFINITE*/, (long long)B.gid[st->cur_id][i]);
+  }
+  if (__any_sync(0xffffffffu, far) && (threadIdx.x & 31) == 0) st->need_rebuild = 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->pending_flip = 1;
+    st->steps_done += 1;
+  }
+}
+
+// First half-kick + drift from stored forces (start of pm_step_vv).
+__global__ void __launch_bounds__(256) k_kick_drift(Params P, Bufs B, int n, float dt) {
+  State *st = B.st;
+  if (st->abort) return;
+  const int cp = st->cur_pv;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  bool far = false;
+  if (i < n) {
+    const float4 f = B.force[i];
+    float4 v = B.vel[cp][i];
+    const float4 x = B.pos[cp][i];
+    const float k = 0.5f * dt * P.lj.inv_mass;
+    v.x = fmaf(k, f.x, v.x);
+    v.y = fmaf(k, f.y, v.y);
+    v.z = fmaf(k, f.z, v.z);
+    const float3 xn = wrap3(P, fmaf(dt, v.x, x.x), fmaf(dt, v.y, x.y), fmaf(dt, v.z, x.z));
+    far = moved_too_far(P, xn, B.xref[i]);
+    B.pos[cp ^ 1][i] = make_float4(xn.x, xn.y, xn.z, x.w);
+    B.vel[cp ^ 1][i] = v;
+  }
+  if (__any_sync(0xffffffffu, far) && (threadIdx.x & 31) == 0) st->need_rebuild = 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->pending_flip = 1;
+}
+
+// Start of every step: apply a pending buffer flip, advance the step index,
+// choose the step-kernel mode and set the graph's rebuild condition.
+__global__ void k_step_begin(Bufs B, cudaGraphConditionalHandle h, int use_handle) {
+  State *st = B.st;
+  if (st->pending_flip) {
+    st->cur_pv ^= 1;
+    st->pending_flip = 0;
+  }
+  st->step_index += 1;
+  st->mode = (st->step_index >= st->step_target) ? kModeFinal : kModeInner;
+  const unsigned c = (st->abort == 0 && st->need_rebuild) ? 1u : 0u;
+  st->do_rebuild = (int)c;
+  if (use_handle) cudaGraphSetConditional(h, c);
+}
+
+__global__ void __launch_bounds__(256) k_ke(Params P, Bufs B, int n) {
+  State *st = B.st;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double ke = 0.0;
+  if (i < n) {
+    const float4 v = B.vel[st->cur_pv][i];
+    ke = 0.5 * (double)(1.0f / P.lj.inv_mass) *
+         ((double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ke += __shfl_xor_sync(0xffffffffu, ke, o);
+  __shared__ double sh[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) sh[wid] = ke;
+  __syncthreads();
+  if (wid == 0) {
+    ke = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ke += __shfl_xor_sync(0xffffffffu, ke, o);
+    if (lane == 0) atomicAdd(&st->acc[3], ke);
+  }
+}
+
+inline unsigned nb(int64_t n) { return (unsigned)((n + 255) / 256); }
+
+}  // namespace
+
+void launch_lj(const Params &P, const Bufs &B, int64_t n, int want_energy, cudaStream_t s) {
+  if (n <= 0) return;
+  const bool capped = P.lj.r_min > 0.f;
+  if (capped) {
+    if (want_energy) k_lj<true, true><<<nb(n), 256, 0, s>>>(P, B, (int)n);
+    else k_lj<true, false><<<nb(n), 256, 0, s>>>(P, B, (int)n);
+  } else {
+    if (want_energy) k_lj<false, true><<<nb(n), 256, 0, s>>>(P, B, (int)n);
+    else k_lj<false, false><<<nb(n), 256, 0, s>>>(P, B, (int)n);
+  }
+}
+
+void launch_lj_step(const Params &P, const Bufs &B, int64_t n, float dt, cudaStream_t s) {
+  if (n <= 0) return;
+  if (P.lj.r_min > 0.f) k_lj_step<true><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt);
+  else k_lj_step<false><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt);
+}
+
+void launch_kick_drift(const Params &P, const Bufs &B, int64_t n, float dt, cudaStream_t s) {
+  if (n > 0) k_kick_drift<<<nb(n), 256, 0, s>>>(P, B, (int)n, dt);
+}
+
+void launch_step_begin(const Bufs &B, cudaGraphConditionalHandle h, int use_handle,
+                       cudaStream_t s) {
+  k_step_begin<<<1, 1, 0, s>>>(B, h, use_handle);
+}
+
+void launch_ke(const Params &P, const Bufs &B, int64_t n, cudaStream_t s) {
+  if (n > 0) k_ke<<<nb(n), 256, 0, s>>>(P, B, (int)n);
+}
+
+}  // namespace pm

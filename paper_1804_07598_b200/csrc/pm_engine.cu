@@ -1,0 +1,849 @@
+// pm_engine.cu -- the C-ABI of include/pm.h: context, device buffers, the
+// rebuild state machine and the CUDA-graph step loop.
+//
+// Step structure of pm_step_vv (one CUDA graph launch per step):
+//   k_step_begin (1 thread: flip pending buffers, set mode, set condition)
+//   -> IF(need_rebuild) { cell ids -> scan -> sort/reorder -> flip -> Verlet }
+//   -> k_lj_step (force sweep + fused kick/drift/wrap/displacement test)
+// The rebuild decision (max displacement > skin/2, BASELINE.json configs[1])
+// is taken on the device by a graph conditional node: no host round trip.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pm.h"
+#include "pm_internal.cuh"
+
+using namespace pm;
+
+struct pm_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cudaStream_t cap_stream = nullptr;  // stream used only for graph capture
+  int use_graphs = 1;
+  int cell_div = 1;
+  int nbr_cap_opt = 0;
+
+  std::string err;
+  int sticky = 0;
+
+  Params P{};
+  Bufs B{};
+  State *st_h = nullptr;  // pinned host mirror of the device state
+
+  int64_t n = 0;          // particles placed
+  int64_t pcap = 0;       // particle capacity of the buffers
+  int64_t ncell_cap = 0;  // cells allocated
+  int64_t ntile_cap = 0;
+  int64_t nbr_rows = 0;   // rows (multiple of 32) the neighbour array holds
+  int nbr_cap = 0;        // slots per row
+
+  bool have_domain = false, have_cutoff = false, have_lj = false, have_sph = false;
+  float r_cut = 0.f, skin = 0.f, rv = 0.f;
+  bool cells_valid = false, list_valid = false, forces_valid = false, rho_valid = false;
+  double lj_eps = 1.0, lj_sigma = 1.0;
+
+  // graph
+  cudaGraphExec_t exec = nullptr;
+  bool graph_valid = false;
+  float graph_dt = 0.f;
+  bool graph_prof = false;
+  cudaGraphNode_t ev_node[2] = {nullptr, nullptr};
+
+  // profiling
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_pool;
+  double prof_force_ms = 0.0, prof_step_ms = 0.0;
+  int64_t prof_force_launches = 0, prof_steps = 0;
+};
+
+// ---------------------------------------------------------------------------
+namespace {
+
+__global__ void k_iota64(int64_t *g, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) g[i] = i;
+}
+
+__global__ void k_run_init(State *st, long long nsteps) {
+  st->step_index = 0;
+  st->step_target = nsteps;
+  st->steps_done = 0;
+  st->mode = kModeInner;
+}
+
+__global__ void k_apply_pending(State *st) {
+  if (st->pending_flip) {
+    st->cur_pv ^= 1;
+    st->pending_flip = 0;
+  }
+}
+
+__global__ void k_zero_acc(State *st, int lo, int hi) {
+  for (int k = lo; k < hi; ++k) st->acc[k] = 0.0;
+}
+
+__global__ void k_clear_abort(State *st) {
+  st->abort = 0;
+  st->overflow_need = 0;
+  st->err_gid = -1;
+}
+
+__global__ void k_force_rebuild(State *st) { st->need_rebuild = 1; }
+
+pm_status set_err(pm_ctx c, pm_status code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) {
+    c->err = buf;
+    c->sticky = code;
+  }
+  return code;
+}
+
+#define CUDA_TRY(ctx, call)                                                              \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return set_err(ctx, e_ == cudaErrorMemoryAllocation ? PM_E_NOMEM : PM_E_CUDA,      \
+                     "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+template <class T>
+cudaError_t dalloc(T **p, int64_t count) {
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  if (count <= 0) count = 1;
+  return cudaMalloc((void **)p, sizeof(T) * (size_t)count);
+}
+
+void destroy_graph(pm_ctx c) {
+  if (c->exec) cudaGraphExecDestroy(c->exec);
+  c->exec = nullptr;
+  c->graph_valid = false;
+}
+
+pm_status check_launch(pm_ctx c, const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(c, PM_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return PM_OK;
+}
+
+pm_status read_state(pm_ctx c) {
+  CUDA_TRY(c, cudaMemcpyAsync(c->st_h, c->B.st, sizeof(State), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return PM_OK;
+}
+
+const char *device_error_name(int code) {
+  switch (code) {
+    case PM_E_DOMAIN: return "particle outside [lo,hi) on a non-periodic axis";
+    case PM_E_COINCIDENT: return "coincident particles (pair distance 0)";
+    case PM_E_NONFINITE: return "non-finite force or density";
+    case PM_E_CAPACITY: return "neighbour capacity overflow";
+    default: return "device error";
+  }
+}
+
+// Sync, read the device state and turn a device error word into a status.
+pm_status sync_check(pm_ctx c, const char *what) {
+  pm_status s = check_launch(c, what);
+  if (s) return s;
+  s = read_state(c);
+  if (s) return s;
+  if (c->st_h->abort)
+    return set_err(c, c->st_h->abort, "%s: %s (gid %lld)", what, device_error_name(c->st_h->abort),
+                   (long long)c->st_h->err_gid);
+  return PM_OK;
+}
+
+pm_status ensure_particles(pm_ctx c, int64_t n) {
+  if (n <= c->pcap) return PM_OK;
+  int64_t cap = ((n + 1023) / 1024) * 1024;
+  Bufs &B = c->B;
+  for (int b = 0; b < 2; ++b) {
+    CUDA_TRY(c, dalloc(&B.pos[b], cap));
+    CUDA_TRY(c, dalloc(&B.vel[b], cap));
+    CUDA_TRY(c, dalloc(&B.gid[b], cap));
+    CUDA_TRY(c, dalloc(&B.kind[b], cap));
+  }
+  CUDA_TRY(c, dalloc(&B.xref, cap));
+  CUDA_TRY(c, dalloc(&B.force, cap));
+  CUDA_TRY(c, dalloc(&B.rhoP, cap));
+  CUDA_TRY(c, dalloc(&B.cell_of, cap));
+  CUDA_TRY(c, dalloc(&B.slot, cap));
+  CUDA_TRY(c, dalloc(&B.perm, cap));
+  CUDA_TRY(c, dalloc(&B.sorttmp, cap));
+  CUDA_TRY(c, dalloc(&B.cnt, cap));
+  CUDA_TRY(c, cudaMemsetAsync(B.force, 0, sizeof(float4) * cap, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(B.cnt, 0, sizeof(int32_t) * cap, c->stream));
+  c->pcap = cap;
+  c->nbr_rows = 0;  // neighbour array must be regrown for the new row count
+  destroy_graph(c);
+  return PM_OK;
+}
+
+pm_status ensure_cells(pm_ctx c) {
+  const int64_t ncell = c->P.grid.ncell;
+  if (ncell > c->ncell_cap) {
+    CUDA_TRY(c, dalloc(&c->B.count, ncell));
+    CUDA_TRY(c, dalloc(&c->B.start, ncell + 1));
+    c->ncell_cap = ncell;
+    destroy_graph(c);
+  }
+  const int64_t ntiles = (ncell + 2047) / 2048;
+  if (ntiles > c->ntile_cap) {
+    CUDA_TRY(c, dalloc(&c->B.scan_tmp, ntiles));
+    c->ntile_cap = ntiles;
+    destroy_graph(c);
+  }
+  return PM_OK;
+}
+
+int auto_nbr_cap(pm_ctx c) {
+  double vol = 1.0;
+  for (int d = 0; d < 3; ++d) vol *= (double)c->P.box.hi[d] - (double)c->P.box.lo[d];
+  const double dens = (double)c->n / vol;
+  const double mean = dens * 4.0 / 3.0 * M_PI * (double)c->rv * c->rv * c->rv;
+  int cap = (int)std::ceil(mean * 1.4 + 16.0);
+  cap = std::max(cap, 16);
+  return (cap + 3) & ~3;
+}
+
+pm_status ensure_nbr(pm_ctx c, int cap) {
+  cap = (cap + 3) & ~3;
+  const int64_t rows = ((c->n + 31) / 32) * 32;
+  if (cap == c->nbr_cap && rows <= c->nbr_rows && c->B.nbr) return PM_OK;
+  const int64_t alloc_rows = ((c->pcap + 31) / 32) * 32;
+  CUDA_TRY(c, dalloc(&c->B.nbr, alloc_rows * (int64_t)cap));
+  c->nbr_rows = alloc_rows;
+  c->nbr_cap = cap;
+  c->P.nbr_cap = cap;
+  destroy_graph(c);
+  return PM_OK;
+}
+
+pm_status setup_grid(pm_ctx c) {
+  if (!c->have_domain || !c->have_cutoff) return PM_OK;
+  Params &P = c->P;
+  const float rv = c->rv;
+  int64_t ncell = 1;
+  for (int d = 0; d < 3; ++d) {
+    const double ext = (double)P.box.hi[d] - (double)P.box.lo[d];
+    const double side = (double)rv / (double)c->cell_div;
+    double nd = std::floor(ext / side);
+    if (nd < 1) nd = 1;
+    if (P.box.per[d] && nd < 3)
+      return set_err(c, PM_E_INVAL,
+                     "periodic axis %d: extent %g < 3 r_v = %g (27-cell stencil needs 3 cells)", d,
+                     ext, 3.0 * rv);
+    if (nd > (double)(1 << 20)) nd = (double)(1 << 20);
+    P.grid.n[d] = (int)nd;
+    P.grid.inv_w[d] = (float)(nd / ext);
+    ncell *= (int64_t)nd;
+  }
+  if (ncell > (int64_t)1 << 30) return set_err(c, PM_E_INVAL, "too many cells (%lld)", (long long)ncell);
+  P.grid.ncell = (int)ncell;
+  c->cells_valid = c->list_valid = c->forces_valid = c->rho_valid = false;
+  destroy_graph(c);
+  return ensure_cells(c);
+}
+
+pm_status check_ready(pm_ctx c) {
+  if (!c) return PM_E_INVAL;
+  if (c->sticky) return c->sticky;
+  if (!c->have_domain) return set_err(c, PM_E_STATE, "pm_set_domain not called");
+  if (!c->have_cutoff) return set_err(c, PM_E_STATE, "pm_set_cutoff not called");
+  if (c->n <= 0 && c->pcap == 0) return set_err(c, PM_E_STATE, "no particles placed");
+  return PM_OK;
+}
+
+// The rebuild sequence (a1-a5), enqueued on stream s (also captured into
+// the graph's conditional body).
+void enqueue_rebuild(pm_ctx c, cudaStream_t s, int count_rebuild) {
+  launch_cell_ids(c->P, c->B, c->n, s);
+  launch_scan(c->P, c->B, c->n, s);
+  launch_sort_reorder(c->P, c->B, c->n, s);
+  launch_flip(c->B, 1, 1, count_rebuild, s);
+  launch_verlet(c->P, c->B, c->n, s);
+}
+
+pm_status build_list(pm_ctx c) {
+  pm_status s = ensure_nbr(c, c->nbr_cap ? c->nbr_cap : (c->nbr_cap_opt ? c->nbr_cap_opt : auto_nbr_cap(c)));
+  if (s) return s;
+  enqueue_rebuild(c, c->stream, 0);
+  s = sync_check(c, "pm_build_verlet");
+  if (s == PM_E_CAPACITY) {
+    const int need = c->st_h->overflow_need;
+    c->sticky = 0;
+    c->err.clear();
+    k_clear_abort<<<1, 1, 0, c->stream>>>(c->B.st);
+    s = ensure_nbr(c, (int)std::ceil(need * 1.2) + 4);
+    if (s) return s;
+    launch_verlet(c->P, c->B, c->n, c->stream);  // cells are already built
+    s = sync_check(c, "pm_build_verlet (retry)");
+  }
+  if (s) return s;
+  c->cells_valid = c->list_valid = true;
+  c->forces_valid = c->rho_valid = false;
+  return PM_OK;
+}
+
+pm_status ensure_events(pm_ctx c, size_t n) {
+  while (c->ev_pool.size() < n) {
+    cudaEvent_t e;
+    CUDA_TRY(c, cudaEventCreate(&e));
+    c->ev_pool.push_back(e);
+  }
+  return PM_OK;
+}
+
+pm_status build_graph(pm_ctx c, float dt, bool prof) {
+  destroy_graph(c);
+  cudaGraph_t g = nullptr;
+  CUDA_TRY(c, cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  CUDA_TRY(c, cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
+  cudaStream_t cs = c->cap_stream;
+  const cudaStreamCaptureMode mode = cudaStreamCaptureModeThreadLocal;
+  // node A: step begin
+  CUDA_TRY(c, cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, mode));
+  launch_step_begin(c->B, h, 1, cs);
+  CUDA_TRY(c, cudaStreamEndCapture(cs, &g));
+  size_t nn = 0;
+  CUDA_TRY(c, cudaGraphGetNodes(g, nullptr, &nn));
+  if (nn != 1) return set_err(c, PM_E_CUDA, "graph build: expected 1 node, got %zu", nn);
+  cudaGraphNode_t nA;
+  CUDA_TRY(c, cudaGraphGetNodes(g, &nA, &nn));
+  // node C: IF(need_rebuild) { rebuild }
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeIf;
+  cp.conditional.size = 1;
+  cudaGraphNode_t nC;
+  CUDA_TRY(c, cudaGraphAddNode(&nC, g, &nA, 1, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CUDA_TRY(c, cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, mode));
+  enqueue_rebuild(c, cs, 1);
+  CUDA_TRY(c, cudaStreamEndCapture(cs, &body));
+  // force step (+ profiling events around it)
+  cudaGraphNode_t prev = nC;
+  if (prof) {
+    pm_status se = ensure_events(c, 2);
+    if (se) return se;
+    CUDA_TRY(c, cudaGraphAddEventRecordNode(&c->ev_node[0], g, &prev, 1, c->ev_pool[0]));
+    prev = c->ev_node[0];
+  }
+  CUDA_TRY(c, cudaStreamBeginCaptureToGraph(cs, g, &prev, nullptr, 1, mode));
+  launch_lj_step(c->P, c->B, c->n, dt, cs);
+  cudaStreamCaptureStatus cst;
+  const cudaGraphNode_t *deps = nullptr;
+  size_t ndeps = 0;
+  CUDA_TRY(c, cudaStreamGetCaptureInfo(cs, &cst, nullptr, nullptr, &deps, &ndeps));
+  cudaGraphNode_t nF = (ndeps == 1) ? deps[0] : nullptr;
+  CUDA_TRY(c, cudaStreamEndCapture(cs, &g));
+  if (prof) {
+    if (!nF) return set_err(c, PM_E_CUDA, "graph build: force node not found");
+    CUDA_TRY(c, cudaGraphAddEventRecordNode(&c->ev_node[1], g, &nF, 1, c->ev_pool[1]));
+  }
+  CUDA_TRY(c, cudaGraphInstantiate(&c->exec, g, 0));
+  cudaGraphDestroy(g);
+  c->graph_valid = true;
+  c->graph_dt = dt;
+  c->graph_prof = prof;
+  return PM_OK;
+}
+
+pm_status run_steps(pm_ctx c, float dt, int64_t nsteps) {
+  k_run_init<<<1, 1, 0, c->stream>>>(c->B.st, (long long)nsteps);
+  if (c->use_graphs) {
+    const bool prof = c->profiling;
+    if (!c->graph_valid || c->graph_dt != dt || c->graph_prof != prof) {
+      pm_status s = build_graph(c, dt, prof);
+      if (s) return s;
+    }
+    if (prof) {
+      pm_status s = ensure_events(c, 2 * (size_t)nsteps + 2);
+      if (s) return s;
+    }
+    for (int64_t k = 0; k < nsteps; ++k) {
+      if (prof) {
+        CUDA_TRY(c, cudaGraphExecEventRecordNodeSetEvent(c->exec, c->ev_node[0], c->ev_pool[2 * k]));
+        CUDA_TRY(c, cudaGraphExecEventRecordNodeSetEvent(c->exec, c->ev_node[1], c->ev_pool[2 * k + 1]));
+      }
+      CUDA_TRY(c, cudaGraphLaunch(c->exec, c->stream));
+    }
+    if (prof) {
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+      for (int64_t k = 0; k < nsteps; ++k) {
+        float ms = 0.f;
+        CUDA_TRY(c, cudaEventElapsedTime(&ms, c->ev_pool[2 * k], c->ev_pool[2 * k + 1]));
+        c->prof_force_ms += ms;
+      }
+      c->prof_force_launches += nsteps;
+    }
+  } else {
+    for (int64_t k = 0; k < nsteps; ++k) {
+      launch_step_begin(c->B, cudaGraphConditionalHandle{}, 0, c->stream);
+      pm_status s = read_state(c);
+      if (s) return s;
+      if (c->st_h->abort) break;
+      if (c->st_h->do_rebuild) enqueue_rebuild(c, c->stream, 1);
+      launch_lj_step(c->P, c->B, c->n, dt, c->stream);
+    }
+  }
+  k_apply_pending<<<1, 1, 0, c->stream>>>(c->B.st);
+  return check_launch(c, "pm_step_vv");
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+pm_status pm_opts_default(pm_opts *o) {
+  if (!o) return PM_E_INVAL;
+  std::memset(o, 0, sizeof *o);
+  o->device = 0;
+  o->cell_div = 1;
+  o->nbr_cap = 0;
+  o->use_graphs = 1;
+  o->cuda_stream = nullptr;
+  return PM_OK;
+}
+
+const char *pm_version(void) { return "pm-b200 0.1 (sm_100a; arXiv 1804.07598 particle hot path)"; }
+
+pm_status pm_create(const pm_opts *opts, pm_ctx *out) {
+  if (!out) return PM_E_INVAL;
+  *out = nullptr;
+  pm_opts o;
+  pm_opts_default(&o);
+  if (opts) o = *opts;
+  if (o.cell_div != 1) return PM_E_INVAL;  // only side >= r_v grids are implemented
+  pm_ctx c = new (std::nothrow) pm_ctx_s();
+  if (!c) return PM_E_NOMEM;
+  c->device = o.device;
+  c->use_graphs = o.use_graphs;
+  c->cell_div = o.cell_div;
+  c->nbr_cap_opt = o.nbr_cap;
+  if (cudaSetDevice(c->device) != cudaSuccess) {
+    delete c;
+    return PM_E_CUDA;
+  }
+  if (o.cuda_stream) {
+    c->stream = (cudaStream_t)o.cuda_stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete c;
+      return PM_E_CUDA;
+    }
+    c->own_stream = true;
+  }
+  if (cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMallocHost((void **)&c->st_h, sizeof(State)) != cudaSuccess ||
+      cudaMalloc((void **)&c->B.st, sizeof(State)) != cudaSuccess) {
+    pm_destroy(c);
+    return PM_E_CUDA;
+  }
+  std::memset(c->st_h, 0, sizeof(State));
+  cudaMemcpy(c->B.st, c->st_h, sizeof(State), cudaMemcpyHostToDevice);
+  c->P.lj.inv_mass = 1.f;
+  *out = c;
+  return PM_OK;
+}
+
+void pm_destroy(pm_ctx c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  destroy_graph(c);
+  Bufs &B = c->B;
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(B.pos[b]);
+    cudaFree(B.vel[b]);
+    cudaFree(B.gid[b]);
+    cudaFree(B.kind[b]);
+  }
+  void *ptrs[] = {B.xref, B.force, B.rhoP, B.cell_of, B.slot, B.count, B.start,
+                  B.perm, B.sorttmp, B.scan_tmp, B.nbr, B.cnt, B.st};
+  for (void *p : ptrs)
+    if (p) cudaFree(p);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  if (c->st_h) cudaFreeHost(c->st_h);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char *pm_last_error(pm_ctx c) { return c ? c->err.c_str() : "null context"; }
+
+pm_status pm_set_domain(pm_ctx c, const float lo[3], const float hi[3], const int32_t periodic[3]) {
+  if (!c || !lo || !hi || !periodic) return PM_E_INVAL;
+  cudaSetDevice(c->device);
+  Box &b = c->P.box;
+  for (int d = 0; d < 3; ++d) {
+    if (!(hi[d] > lo[d])) return set_err(c, PM_E_INVAL, "axis %d: hi <= lo", d);
+    b.lo[d] = lo[d];
+    b.hi[d] = hi[d];
+    b.L[d] = hi[d] - lo[d];  // fl32 (SSE single precision)
+    b.halfL[d] = b.L[d] * 0.5f;
+    b.per[d] = periodic[d] ? 1 : 0;
+  }
+  c->have_domain = true;
+  return setup_grid(c);
+}
+
+pm_status pm_set_cutoff(pm_ctx c, float r_cut, float skin) {
+  if (!c) return PM_E_INVAL;
+  if (!(r_cut > 0.f) || !(skin >= 0.f))
+    return set_err(c, PM_E_INVAL, "r_cut must be > 0 and skin >= 0 (got %g, %g)", r_cut, skin);
+  cudaSetDevice(c->device);
+  c->r_cut = r_cut;
+  c->skin = skin;
+  volatile float rv = r_cut + skin;  // fl32(r_cut + skin), reading R5
+  c->rv = rv;
+  volatile float rv2 = c->rv * c->rv;
+  volatile float rc2 = r_cut * r_cut;
+  c->P.rv2 = rv2;
+  c->P.lj.rc2 = rc2;
+  c->P.half_skin2 = 0.25f * skin * skin;
+  c->P.mi_margin = c->rv + skin;
+  c->have_cutoff = true;
+  return setup_grid(c);
+}
+
+pm_status pm_set_lj(pm_ctx c, float eps, float sigma, float mass, float r_min) {
+  if (!c) return PM_E_INVAL;
+  if (!(eps > 0.f) || !(sigma > 0.f) || !(mass > 0.f) || !(r_min >= 0.f))
+    return set_err(c, PM_E_INVAL, "pm_set_lj: eps, sigma, mass must be > 0 and r_min >= 0");
+  LJ &l = c->P.lj;
+  const double s6 = std::pow((double)sigma, 6.0), s12 = s6 * s6;
+  l.c12 = (float)(48.0 * eps * s12);
+  l.c6 = (float)(24.0 * eps * s6);
+  l.e12 = (float)(4.0 * eps * s12);
+  l.e6 = (float)(4.0 * eps * s6);
+  l.r_min = r_min;
+  l.inv_mass = 1.0f / mass;
+  l.eps = eps;
+  l.sigma = sigma;
+  c->lj_eps = eps;
+  c->lj_sigma = sigma;
+  c->have_lj = true;
+  c->forces_valid = false;
+  destroy_graph(c);
+  return PM_OK;
+}
+
+pm_status pm_set_sph(pm_ctx c, const pm_sph_params *p) {
+  if (!c || !p) return PM_E_INVAL;
+  if (!(p->h > 0.f) || !(p->mass > 0.f) || !(p->rho0 > 0.f))
+    return set_err(c, PM_E_INVAL, "pm_set_sph: h, mass, rho0 must be > 0");
+  SPH &s = c->P.sph;
+  s.h = p->h;
+  s.inv_h = (float)(1.0 / p->h);
+  s.mass = p->mass;
+  s.rho0 = p->rho0;
+  s.inv_rho0 = (float)(1.0 / p->rho0);
+  s.gamma = p->gamma;
+  s.b = p->b;
+  s.alpha = p->alpha;
+  s.cbar = p->cbar;
+  s.eta2 = p->eta2;
+  const double h = p->h;
+  s.w_norm = (float)(1.0 / (M_PI * h * h * h));
+  s.dw_norm = (float)(1.0 / (M_PI * h * h * h * h));
+  for (int d = 0; d < 3; ++d) s.g[d] = p->g[d];
+  c->have_sph = true;
+  c->rho_valid = false;
+  return PM_OK;
+}
+
+pm_status pm_place(pm_ctx c, int64_t n, const float *pos4, const float *vel4, const int64_t *gid,
+                   const int32_t *kind, int32_t mem) {
+  if (!c || n < 0 || (n > 0 && !pos4)) return PM_E_INVAL;
+  if (n >= (int64_t)1 << 31) return set_err(c, PM_E_INVAL, "n >= 2^31 not supported per context");
+  cudaSetDevice(c->device);
+  c->sticky = 0;
+  c->err.clear();
+  pm_status s = ensure_particles(c, n);
+  if (s) return s;
+  if (n != c->n) destroy_graph(c);
+  c->n = n;
+  const cudaMemcpyKind k = (mem == PM_DEVICE) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  Bufs &B = c->B;
+  if (n > 0) {
+    CUDA_TRY(c, cudaMemcpyAsync(B.pos[0], pos4, sizeof(float4) * n, k, c->stream));
+    if (vel4) CUDA_TRY(c, cudaMemcpyAsync(B.vel[0], vel4, sizeof(float4) * n, k, c->stream));
+    else CUDA_TRY(c, cudaMemsetAsync(B.vel[0], 0, sizeof(float4) * n, c->stream));
+    if (gid) CUDA_TRY(c, cudaMemcpyAsync(B.gid[0], gid, sizeof(int64_t) * n, k, c->stream));
+    else k_iota64<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(B.gid[0], n);
+    if (kind) CUDA_TRY(c, cudaMemcpyAsync(B.kind[0], kind, sizeof(int32_t) * n, k, c->stream));
+    else CUDA_TRY(c, cudaMemsetAsync(B.kind[0], 0, sizeof(int32_t) * n, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(B.xref, B.pos[0], sizeof(float4) * n, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  std::memset(c->st_h, 0, sizeof(State));
+  c->st_h->err_gid = -1;
+  CUDA_TRY(c, cudaMemcpyAsync(B.st, c->st_h, sizeof(State), cudaMemcpyHostToDevice, c->stream));
+  if (mem == PM_HOST) CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->cells_valid = c->list_valid = c->forces_valid = c->rho_valid = false;
+  return check_launch(c, "pm_place");
+}
+
+pm_status pm_build_cells(pm_ctx c) {
+  pm_status s = check_ready(c);
+  if (s) return s;
+  cudaSetDevice(c->device);
+  launch_cell_ids(c->P, c->B, c->n, c->stream);
+  launch_scan(c->P, c->B, c->n, c->stream);
+  launch_sort_reorder(c->P, c->B, c->n, c->stream);
+  launch_flip(c->B, 1, 1, 0, c->stream);
+  s = sync_check(c, "pm_build_cells");
+  if (s) return s;
+  c->cells_valid = true;
+  c->list_valid = c->forces_valid = c->rho_valid = false;
+  return PM_OK;
+}
+
+pm_status pm_build_verlet(pm_ctx c) {
+  pm_status s = check_ready(c);
+  if (s) return s;
+  cudaSetDevice(c->device);
+  return build_list(c);
+}
+
+pm_status pm_compute_lj(pm_ctx c, int32_t want_energy) {
+  pm_status s = check_ready(c);
+  if (s) return s;
+  if (!c->list_valid) return set_err(c, PM_E_STATE, "pm_compute_lj: no Verlet list");
+  if (!c->have_lj) return set_err(c, PM_E_STATE, "pm_set_lj not called");
+  cudaSetDevice(c->device);
+  if (want_energy) k_zero_acc<<<1, 1, 0, c->stream>>>(c->B.st, 0, 3);
+  launch_lj(c->P, c->B, c->n, want_energy, c->stream);
+  s = sync_check(c, "pm_compute_lj");
+  if (s) return s;
+  c->forces_valid = true;
+  return PM_OK;
+}
+
+pm_status pm_thermo_compute(pm_ctx c) { return pm_compute_lj(c, 1); }
+
+pm_status pm_sph_density(pm_ctx c) {
+  pm_status s = check_ready(c);
+  if (s) return s;
+  if (!c->list_valid) return set_err(c, PM_E_STATE, "pm_sph_density: no Verlet list");
+  if (!c->have_sph) return set_err(c, PM_E_STATE, "pm_set_sph not called");
+  cudaSetDevice(c->device);
+  launch_sph_density(c->P, c->B, c->n, c->stream);
+  s = sync_check(c, "pm_sph_density");
+  if (s) return s;
+  c->rho_valid = true;
+  return PM_OK;
+}
+
+pm_status pm_sph_forces(pm_ctx c) {
+  pm_status s = check_ready(c);
+  if (s) return s;
+  if (!c->rho_valid) return set_err(c, PM_E_STATE, "pm_sph_forces: densities not computed");
+  cudaSetDevice(c->device);
+  launch_sph_forces(c->P, c->B, c->n, c->stream);
+  return sync_check(c, "pm_sph_forces");
+}
+
+pm_status pm_step_vv(pm_ctx c, float dt, int64_t nsteps, pm_run_stats *out) {
+  pm_status s = check_ready(c);
+  if (s) return s;
+  if (!(dt > 0.f) || nsteps < 0) return set_err(c, PM_E_INVAL, "pm_step_vv: dt must be > 0");
+  if (!c->have_lj) return set_err(c, PM_E_STATE, "pm_set_lj not called");
+  cudaSetDevice(c->device);
+  if (out) std::memset(out, 0, sizeof *out);
+  if (nsteps == 0) return PM_OK;
+  if (!c->list_valid) {
+    s = build_list(c);
+    if (s) return s;
+  }
+  if (!c->forces_valid) {
+    launch_lj(c->P, c->B, c->n, 0, c->stream);
+    c->forces_valid = true;
+  }
+  s = read_state(c);
+  if (s) return s;
+  const long long reb0 = c->st_h->n_rebuilds;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->profiling) {
+    CUDA_TRY(c, cudaEventCreate(&e0));
+    CUDA_TRY(c, cudaEventCreate(&e1));
+    CUDA_TRY(c, cudaEventRecord(e0, c->stream));
+  }
+  launch_kick_drift(c->P, c->B, c->n, dt, c->stream);
+  int64_t done = 0;
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    s = run_steps(c, dt, nsteps - done);
+    if (s) return s;
+    s = read_state(c);
+    if (s) return s;
+    done += c->st_h->steps_done;
+    if (c->st_h->abort == PM_E_CAPACITY && done < nsteps) {
+      // grow the neighbour capacity and resume at the aborted step's rebuild
+      const int need = c->st_h->overflow_need;
+      k_clear_abort<<<1, 1, 0, c->stream>>>(c->B.st);
+      k_force_rebuild<<<1, 1, 0, c->stream>>>(c->B.st);
+      s = ensure_nbr(c, (int)std::ceil(need * 1.2) + 4);
+      if (s) return s;
+      continue;
+    }
+    break;
+  }
+  if (c->profiling) {
+    CUDA_TRY(c, cudaEventRecord(e1, c->stream));
+    CUDA_TRY(c, cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    c->prof_step_ms += ms;
+    c->prof_steps += nsteps;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  if (c->st_h->abort)
+    return set_err(c, c->st_h->abort, "pm_step_vv: %s (gid %lld) after %lld steps",
+                   device_error_name(c->st_h->abort), (long long)c->st_h->err_gid,
+                   (long long)done);
+  c->forces_valid = true;
+  c->rho_valid = false;
+  if (out) {
+    out->steps = done;
+    out->rebuilds = c->st_h->n_rebuilds - reb0;
+    out->max_row = c->st_h->max_row;
+    out->nbr_cap = c->nbr_cap;
+    out->mean_row = c->n ? (double)c->st_h->nnz / (double)c->n : 0.0;
+  }
+  return PM_OK;
+}
+
+pm_status pm_count(pm_ctx c, int64_t *n_owned, int64_t *n_ghost, int64_t *n_cells, int64_t *nnz) {
+  if (!c) return PM_E_INVAL;
+  if (n_owned) *n_owned = c->n;
+  if (n_ghost) *n_ghost = 0;
+  if (n_cells) *n_cells = c->have_domain && c->have_cutoff ? c->P.grid.ncell : 0;
+  if (nnz) {
+    pm_status s = read_state(c);
+    if (s) return s;
+    *nnz = c->list_valid ? c->st_h->nnz : 0;
+  }
+  return PM_OK;
+}
+
+pm_status pm_get_cells(pm_ctx c, int32_t *cell_of, int32_t *cell_start, int32_t *perm) {
+  if (!c) return PM_E_INVAL;
+  if (!c->cells_valid) return set_err(c, PM_E_STATE, "pm_get_cells: no cell list");
+  cudaSetDevice(c->device);
+  const int64_t n = c->n;
+  if (cell_of) CUDA_TRY(c, cudaMemcpyAsync(cell_of, c->B.cell_of, 4 * n, cudaMemcpyDeviceToHost, c->stream));
+  if (cell_start)
+    CUDA_TRY(c, cudaMemcpyAsync(cell_start, c->B.start, 4 * ((int64_t)c->P.grid.ncell + 1),
+                                cudaMemcpyDeviceToHost, c->stream));
+  if (perm) CUDA_TRY(c, cudaMemcpyAsync(perm, c->B.perm, 4 * n, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return PM_OK;
+}
+
+pm_status pm_get_verlet(pm_ctx c, int64_t *row_ptr, int64_t *col_gid) {
+  if (!c || !row_ptr) return PM_E_INVAL;
+  if (!c->list_valid) return set_err(c, PM_E_STATE, "pm_get_verlet: no Verlet list");
+  cudaSetDevice(c->device);
+  const int64_t n = c->n;
+  std::vector<int32_t> cnt((size_t)n);
+  if (n) CUDA_TRY(c, cudaMemcpyAsync(cnt.data(), c->B.cnt, 4 * n, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  row_ptr[0] = 0;
+  for (int64_t i = 0; i < n; ++i) row_ptr[i + 1] = row_ptr[i] + cnt[(size_t)i];
+  const int64_t nnz = row_ptr[n];
+  if (!col_gid || nnz == 0) return PM_OK;
+  int64_t *d_rp = nullptr, *d_col = nullptr;
+  CUDA_TRY(c, cudaMalloc((void **)&d_rp, 8 * (n + 1)));
+  CUDA_TRY(c, cudaMalloc((void **)&d_col, 8 * nnz));
+  CUDA_TRY(c, cudaMemcpyAsync(d_rp, row_ptr, 8 * (n + 1), cudaMemcpyHostToDevice, c->stream));
+  launch_verlet_export(c->B, n, c->nbr_cap, d_rp, d_col, c->stream);
+  CUDA_TRY(c, cudaMemcpyAsync(col_gid, d_col, 8 * nnz, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  cudaFree(d_rp);
+  cudaFree(d_col);
+  return check_launch(c, "pm_get_verlet");
+}
+
+pm_status pm_get_state(pm_ctx c, float *pos4, float *vel4, float *force4, int64_t *gid, float *rho,
+                       float *pres, int32_t mem) {
+  if (!c) return PM_E_INVAL;
+  cudaSetDevice(c->device);
+  pm_status s = read_state(c);
+  if (s) return s;
+  const int cp = c->st_h->cur_pv, ci = c->st_h->cur_id;
+  const int64_t n = c->n;
+  const cudaMemcpyKind k = (mem == PM_DEVICE) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (n == 0) return PM_OK;
+  if (pos4) CUDA_TRY(c, cudaMemcpyAsync(pos4, c->B.pos[cp], 16 * n, k, c->stream));
+  if (vel4) CUDA_TRY(c, cudaMemcpyAsync(vel4, c->B.vel[cp], 16 * n, k, c->stream));
+  if (force4) CUDA_TRY(c, cudaMemcpyAsync(force4, c->B.force, 16 * n, k, c->stream));
+  if (gid) CUDA_TRY(c, cudaMemcpyAsync(gid, c->B.gid[ci], 8 * n, k, c->stream));
+  if (rho || pres) {
+    std::vector<float2> rp((size_t)n);
+    CUDA_TRY(c, cudaMemcpyAsync(rp.data(), c->B.rhoP, 8 * n, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    for (int64_t i = 0; i < n; ++i) {
+      if (rho) rho[i] = rp[(size_t)i].x;
+      if (pres) pres[i] = rp[(size_t)i].y;
+    }
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return PM_OK;
+}
+
+pm_status pm_get_thermo(pm_ctx c, double *ke, double *pe_raw, double *pe_shift, double *virial,
+                        int64_t *npairs) {
+  if (!c) return PM_E_INVAL;
+  cudaSetDevice(c->device);
+  k_zero_acc<<<1, 1, 0, c->stream>>>(c->B.st, 3, 4);
+  launch_ke(c->P, c->B, c->n, c->stream);
+  pm_status s = sync_check(c, "pm_get_thermo");
+  if (s) return s;
+  const State &h = *c->st_h;
+  const double rc = c->r_cut, sr6 = std::pow(c->lj_sigma / rc, 6.0);
+  const double vrc = 4.0 * c->lj_eps * (sr6 * sr6 - sr6);
+  if (ke) *ke = h.acc[3];
+  if (pe_raw) *pe_raw = h.acc[0];
+  if (pe_shift) *pe_shift = h.acc[0] - 0.5 * h.acc[2] * vrc;
+  if (virial) *virial = h.acc[1];
+  if (npairs) *npairs = (int64_t)h.acc[2];
+  return PM_OK;
+}
+
+pm_status pm_set_profiling(pm_ctx c, int32_t on) {
+  if (!c) return PM_E_INVAL;
+  c->profiling = on != 0;
+  c->prof_force_ms = c->prof_step_ms = 0.0;
+  c->prof_force_launches = c->prof_steps = 0;
+  return PM_OK;
+}
+
+pm_status pm_get_profile(pm_ctx c, double *force_ms, int64_t *force_launches, double *step_ms,
+                         int64_t *steps) {
+  if (!c) return PM_E_INVAL;
+  if (force_ms) *force_ms = c->prof_force_ms;
+  if (force_launches) *force_launches = c->prof_force_launches;
+  if (step_ms) *step_ms = c->prof_step_ms;
+  if (steps) *steps = c->prof_steps;
+  return PM_OK;
+}
+
+}  // extern "C"

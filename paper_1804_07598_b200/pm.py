@@ -1,0 +1,278 @@
+"""Thin ctypes binding of include/pm.h (argument marshalling only).
+
+Every step of the path runs in libpm.so's CUDA kernels; this module only
+converts numpy arrays / torch CUDA tensors to pointers and status codes to
+exceptions.  There is no CPU fallback: if libpm.so is missing or cannot be
+loaded, ``lib()`` raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpm.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "pm.h")
+
+PM_OK = 0
+PM_HOST, PM_DEVICE = 0, 1
+STATUS = {0: "PM_OK", -1: "PM_E_INVAL", -2: "PM_E_STATE", -3: "PM_E_NOMEM", -4: "PM_E_CUDA",
+          -5: "PM_E_NCCL", -6: "PM_E_DOMAIN", -7: "PM_E_COINCIDENT", -8: "PM_E_NONFINITE",
+          -9: "PM_E_CAPACITY"}
+
+
+class PMError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Opts(C.Structure):
+    _fields_ = [("device", C.c_int32), ("cell_div", C.c_int32), ("nbr_cap", C.c_int32),
+                ("use_graphs", C.c_int32), ("cuda_stream", C.c_void_p)]
+
+
+class SPHParams(C.Structure):
+    _fields_ = [("h", C.c_float), ("mass", C.c_float), ("rho0", C.c_float), ("gamma", C.c_float),
+                ("b", C.c_float), ("alpha", C.c_float), ("cbar", C.c_float), ("eta2", C.c_float),
+                ("g", C.c_float * 3)]
+
+
+class RunStats(C.Structure):
+    _fields_ = [("steps", C.c_int64), ("rebuilds", C.c_int64), ("max_row", C.c_int32),
+                ("nbr_cap", C.c_int32), ("mean_row", C.c_double)]
+
+
+_lib = None
+vp = C.c_void_p
+
+
+def lib(path: str = LIB_PATH):
+    """Load libpm.so (raises if it is missing -- the product has no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"libpm.so not found at {path}; run __graft_entry__.build()")
+    L = C.CDLL(path)
+    st = C.c_int32
+    sig = {
+        "pm_opts_default": (st, [C.POINTER(Opts)]),
+        "pm_version": (C.c_char_p, []),
+        "pm_create": (st, [C.POINTER(Opts), C.POINTER(vp)]),
+        "pm_destroy": (None, [vp]),
+        "pm_last_error": (C.c_char_p, [vp]),
+        "pm_set_domain": (st, [vp, vp, vp, vp]),
+        "pm_set_cutoff": (st, [vp, C.c_float, C.c_float]),
+        "pm_set_lj": (st, [vp, C.c_float, C.c_float, C.c_float, C.c_float]),
+        "pm_set_sph": (st, [vp, C.POINTER(SPHParams)]),
+        "pm_place": (st, [vp, C.c_int64, vp, vp, vp, vp, C.c_int32]),
+        "pm_build_cells": (st, [vp]),
+        "pm_build_verlet": (st, [vp]),
+        "pm_compute_lj": (st, [vp, C.c_int32]),
+        "pm_sph_density": (st, [vp]),
+        "pm_sph_forces": (st, [vp]),
+        "pm_step_vv": (st, [vp, C.c_float, C.c_int64, C.POINTER(RunStats)]),
+        "pm_count": (st, [vp, vp, vp, vp, vp]),
+        "pm_get_cells": (st, [vp, vp, vp, vp]),
+        "pm_get_verlet": (st, [vp, vp, vp]),
+        "pm_get_state": (st, [vp, vp, vp, vp, vp, vp, vp, C.c_int32]),
+        "pm_get_thermo": (st, [vp, vp, vp, vp, vp, vp]),
+        "pm_thermo_compute": (st, [vp]),
+        "pm_set_profiling": (st, [vp, C.c_int32]),
+        "pm_get_profile": (st, [vp, vp, vp, vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def header_symbols(header: str = HEADER):
+    """Function names declared in include/pm.h."""
+    txt = open(header).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(pm_[a-z_0-9]+)\s*\(", txt)))
+
+
+def _ptr(a):
+    """Pointer of a numpy array (host) or torch tensor (host or device)."""
+    if a is None:
+        return None, PM_HOST
+    if hasattr(a, "data_ptr"):
+        return C.c_void_p(a.data_ptr()), (PM_DEVICE if a.is_cuda else PM_HOST)
+    if not a.flags["C_CONTIGUOUS"]:
+        raise ValueError("arrays must be C-contiguous")
+    return C.c_void_p(a.ctypes.data), PM_HOST
+
+
+class Context:
+    """One pm_ctx (one GPU, one stream)."""
+
+    def __init__(self, device: int = 0, nbr_cap: int = 0, use_graphs: bool = True, stream=None):
+        L = lib()
+        o = Opts()
+        L.pm_opts_default(C.byref(o))
+        o.device = device
+        o.nbr_cap = nbr_cap
+        o.use_graphs = 1 if use_graphs else 0
+        o.cuda_stream = stream
+        h = vp()
+        self._check(L.pm_create(C.byref(o), C.byref(h)))
+        self.h = h
+        self.L = L
+        self.n = 0
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.pm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _check(self, code):
+        if code != PM_OK:
+            msg = lib().pm_last_error(self.h).decode() if getattr(self, "h", None) else ""
+            raise PMError(code, msg)
+
+    # ---- configuration
+    def set_domain(self, lo, hi, periodic):
+        lo = np.ascontiguousarray(lo, np.float32)
+        hi = np.ascontiguousarray(hi, np.float32)
+        per = np.ascontiguousarray(periodic, np.int32)
+        self._check(self.L.pm_set_domain(self.h, lo.ctypes.data, hi.ctypes.data, per.ctypes.data))
+
+    def set_cutoff(self, r_cut, skin):
+        self._check(self.L.pm_set_cutoff(self.h, r_cut, skin))
+
+    def set_lj(self, epsilon=1.0, sigma=1.0, mass=1.0, r_min=0.0):
+        self._check(self.L.pm_set_lj(self.h, epsilon, sigma, mass, r_min))
+
+    def set_sph(self, p: dict):
+        s = SPHParams(h=p["h"], mass=p["mass"], rho0=p["rho0"], gamma=p["gamma"], b=p["b"],
+                      alpha=p["alpha"], cbar=p["c0"], eta2=p["eta2"])
+        for d in range(3):
+            s.g[d] = p["g"][d]
+        self._check(self.L.pm_set_sph(self.h, C.byref(s)))
+
+    # ---- data
+    def place(self, pos4, vel4=None, gid=None, kind=None):
+        n = int(pos4.shape[0])
+        pp, mem = _ptr(pos4)
+        pv, _ = _ptr(vel4)
+        pg, _ = _ptr(gid)
+        pk, _ = _ptr(kind)
+        self._check(self.L.pm_place(self.h, n, pp, pv, pg, pk, mem))
+        self.n = n
+
+    def place_system(self, s):
+        """Place an inputs.System and set its domain."""
+        self.set_domain(s.lo, s.hi, s.periodic)
+        self.place(s.pos, s.vel, s.gid, s.kind)
+
+    def build_cells(self):
+        self._check(self.L.pm_build_cells(self.h))
+
+    def build_verlet(self):
+        self._check(self.L.pm_build_verlet(self.h))
+
+    def compute_lj(self, want_energy=False):
+        self._check(self.L.pm_compute_lj(self.h, 1 if want_energy else 0))
+
+    def sph_density(self):
+        self._check(self.L.pm_sph_density(self.h))
+
+    def sph_forces(self):
+        self._check(self.L.pm_sph_forces(self.h))
+
+    def step_vv(self, dt, nsteps):
+        rs = RunStats()
+        self._check(self.L.pm_step_vv(self.h, dt, int(nsteps), C.byref(rs)))
+        return dict(steps=rs.steps, rebuilds=rs.rebuilds, max_row=rs.max_row,
+                    nbr_cap=rs.nbr_cap, mean_row=rs.mean_row)
+
+    # ---- getters
+    def count(self):
+        v = [C.c_int64() for _ in range(4)]
+        self._check(self.L.pm_count(self.h, *[C.byref(x) for x in v]))
+        return dict(n_owned=v[0].value, n_ghost=v[1].value, n_cells=v[2].value, nnz=v[3].value)
+
+    def get_cells(self):
+        c = self.count()
+        n, nc = c["n_owned"], c["n_cells"]
+        cell_of = np.zeros(n, np.int32)
+        start = np.zeros(nc + 1, np.int32)
+        perm = np.zeros(n, np.int32)
+        self._check(self.L.pm_get_cells(self.h, cell_of.ctypes.data, start.ctypes.data,
+                                        perm.ctypes.data))
+        return dict(cell_of=cell_of, start=start, perm=perm)
+
+    def get_verlet(self):
+        n = self.count()["n_owned"]
+        rp = np.zeros(n + 1, np.int64)
+        self._check(self.L.pm_get_verlet(self.h, rp.ctypes.data, None))
+        col = np.zeros(max(int(rp[-1]), 1), np.int64)
+        self._check(self.L.pm_get_verlet(self.h, rp.ctypes.data, col.ctypes.data))
+        return rp, col[:int(rp[-1])]
+
+    def get_state(self):
+        n = self.count()["n_owned"]
+        pos = np.zeros((n, 4), np.float32)
+        vel = np.zeros((n, 4), np.float32)
+        f = np.zeros((n, 4), np.float32)
+        gid = np.zeros(n, np.int64)
+        rho = np.zeros(n, np.float32)
+        pres = np.zeros(n, np.float32)
+        self._check(self.L.pm_get_state(self.h, pos.ctypes.data, vel.ctypes.data, f.ctypes.data,
+                                        gid.ctypes.data, rho.ctypes.data, pres.ctypes.data,
+                                        PM_HOST))
+        return dict(pos=pos, vel=vel, force=f, gid=gid, rho=rho, pres=pres)
+
+    def get_state_into(self, pos4=None, vel4=None):
+        """Copy pos/vel into caller buffers (numpy host or torch device)."""
+        pp, mem = _ptr(pos4)
+        pv, mem2 = _ptr(vel4)
+        if pos4 is not None and vel4 is not None and mem != mem2:
+            raise ValueError("pos4 and vel4 must both be host or both device")
+        self._check(self.L.pm_get_state(self.h, pp, pv, None, None, None, None,
+                                        mem if pos4 is not None else mem2))
+
+    def thermo(self, recompute=True):
+        if recompute:
+            self._check(self.L.pm_thermo_compute(self.h))
+        v = [C.c_double() for _ in range(4)]
+        npairs = C.c_int64()
+        self._check(self.L.pm_get_thermo(self.h, *[C.byref(x) for x in v], C.byref(npairs)))
+        return dict(ke=v[0].value, pe_raw=v[1].value, pe_shift=v[2].value, virial=v[3].value,
+                    npairs=npairs.value)
+
+    def set_profiling(self, on: bool):
+        self._check(self.L.pm_set_profiling(self.h, 1 if on else 0))
+
+    def get_profile(self):
+        fm, sm = C.c_double(), C.c_double()
+        fl, ns = C.c_int64(), C.c_int64()
+        self._check(self.L.pm_get_profile(self.h, C.byref(fm), C.byref(fl), C.byref(sm),
+                                          C.byref(ns)))
+        return dict(force_ms=fm.value, force_launches=fl.value, step_ms=sm.value, steps=ns.value)
+
+
+def sorted_by_gid(state: dict) -> dict:
+    """Reorder a get_state() dict into ascending gid order."""
+    o = np.argsort(state["gid"], kind="stable")
+    return {k: v[o] for k, v in state.items()}

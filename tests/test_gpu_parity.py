@@ -1,0 +1,385 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Integer structures (cell ids, counts, starts, permutation, neighbour sets,
+pair counts) must be bit-exact; forces / densities / accelerations within the
+BASELINE.json north_star bar: max per-component |err| / RMS(ref) <= 1e-4.
+"""
+import numpy as np
+import pytest
+
+from paper_1804_07598_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4  # BJ north_star: forces and densities within 1e-4 of the RMS
+
+
+@pytest.fixture(scope="module")
+def pm():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1804_07598_b200 import build, pm as pmmod
+    build.build()
+    pmmod.lib()
+    return pmmod
+
+
+def f32(x):
+    return np.float32(x)
+
+
+def rv32(rc, skin):
+    return np.float32(np.float32(rc) + np.float32(skin))  # reading R5
+
+
+def make_ctx(pm, s, rc=2.5, skin=0.3, r_min=0.0, **kw):
+    c = pm.Context(**kw)
+    c.set_domain(s.lo, s.hi, s.periodic)
+    c.set_cutoff(rc, skin)
+    c.set_lj(1.0, 1.0, 1.0, r_min)
+    c.place(s.pos, s.vel, s.gid, s.kind)
+    return c
+
+
+def idx_of_gid(s):
+    inv = np.empty(int(s.gid.max()) + 1, np.int64)
+    inv[s.gid] = np.arange(s.n)
+    return inv
+
+
+# ---------------------------------------------------------------- cells
+@pytest.mark.parametrize("name", ["cfg1_shuffled", "cfg2", "faces_bigcell"])
+def test_cells_bit_exact(pm, orc, name):
+    if name == "cfg1_shuffled":
+        s = inputs.shuffled(inputs.cfg1(), (11,))
+    elif name == "cfg2":
+        s = inputs.cfg2()
+    else:
+        import itertools
+        faces = np.array([0.0, 3.0, 6.0, np.nextafter(f32(9.0), f32(0)),
+                          np.nextafter(f32(3.0), f32(0)), 4.5, -1e-9, 9.0], np.float32)
+        pts = np.array(list(itertools.product(faces, repeat=3)), np.float32)
+        r = np.random.default_rng(0)
+        big = r.uniform(0.1, 2.9, (3000, 3)).astype(np.float32)  # one 3000-particle cell
+        mid = r.uniform(3.0, 6.0, (40, 3)).astype(np.float32)  # a 40-particle cell
+        xyz = np.concatenate([pts, big, mid])
+        perm = r.permutation(xyz.shape[0])
+        pos = np.zeros((xyz.shape[0], 4), np.float32)
+        pos[:, :3] = xyz[perm]
+        s = inputs.System(pos=pos, vel=np.zeros_like(pos), gid=np.arange(pos.shape[0]),
+                          lo=np.zeros(3, np.float32), hi=np.full(3, 9.0, np.float32),
+                          periodic=np.ones(3, np.int32))
+    c = make_ctx(pm, s)
+    c.build_cells()
+    g = c.get_cells()
+    ref = orc.cell_list(s.pos, s.lo, s.hi, s.periodic, rv=rv32(2.5, 0.3))
+    assert np.array_equal(g["cell_of"], ref["cell_of"])
+    assert np.array_equal(g["start"], ref["start"])
+    assert np.array_equal(g["perm"], ref["perm"])
+    # the particle arrays were reordered into cell order
+    st = c.get_state()
+    assert np.array_equal(st["gid"], s.gid[ref["perm"]])
+    assert np.array_equal(st["pos"], ref["pos"][ref["perm"]])
+    c.close()
+
+
+# ---------------------------------------------------------------- Verlet
+def _row_sets_equal(rp, col, gids, ref_rp, ref_cols, ref_gid_of_col):
+    for r in range(len(gids)):
+        got = np.sort(col[rp[r]:rp[r + 1]])
+        exp = np.sort(ref_gid_of_col[ref_cols[ref_rp[r]:ref_rp[r + 1]]])
+        if not np.array_equal(got, exp):
+            return r
+    return -1
+
+
+@pytest.mark.parametrize("name", ["cfg1", "random_mixed_bc", "cfg2_sampled"])
+def test_verlet_sets_bit_exact(pm, orc, name):
+    if name == "cfg1":
+        s = inputs.shuffled(inputs.cfg1(), (12,))
+    elif name == "random_mixed_bc":
+        s = inputs.random_box(3000, 14.0, (13,), periodic=(1, 0, 1))
+    else:
+        s = inputs.cfg2()
+    c = make_ctx(pm, s)
+    c.build_verlet()
+    rp, col = c.get_verlet()
+    st = c.get_state()
+    gid_rows = st["gid"]
+    inv = idx_of_gid(s)
+    if name == "cfg2_sampled":
+        pick = np.random.default_rng(1).choice(s.n, 200, replace=False)
+    else:
+        pick = np.arange(s.n)
+    rows_storage = inv[gid_rows[pick]]
+    rrp, rcols, _ = orc.verlet_rows(s.pos, s.lo, s.hi, s.periodic, rv32(2.5, 0.3),
+                                    rows=rows_storage, want_shift=False)
+    sub_rp = np.concatenate([[0], np.cumsum(rp[pick + 1] - rp[pick])])
+    sub_col = np.concatenate([col[rp[i]:rp[i + 1]] for i in pick]) if len(pick) else col[:0]
+    bad = _row_sets_equal(sub_rp, sub_col, gid_rows[pick], rrp, rcols, s.gid)
+    assert bad < 0, f"row {bad} (gid {gid_rows[pick][bad]}) differs"
+    assert c.count()["nnz"] == rp[-1]
+    c.close()
+
+
+def test_verlet_capacity_overflow_retry(pm, orc):
+    """A tiny initial capacity overflows; the library grows it and retries."""
+    s = inputs.cfg1()
+    c = make_ctx(pm, s, nbr_cap=8)
+    c.build_verlet()
+    rp, col = c.get_verlet()
+    assert np.all(np.diff(rp) == 80)  # SC rho=0.8 + jitter: 80 inside 2.8 (pinned)
+    c.close()
+
+
+# ---------------------------------------------------------------- LJ forces
+@pytest.mark.parametrize("name", ["cfg1", "cfg2_sampled", "random_mixed_bc"])
+def test_lj_forces_parity(pm, orc, name):
+    if name == "cfg1":
+        s = inputs.shuffled(inputs.cfg1(), (14,))
+        pick = None
+    elif name == "cfg2_sampled":
+        s = inputs.cfg2()
+        pick = np.random.default_rng(2).choice(s.n, 512, replace=False)
+    else:
+        s = inputs.lj_lattice_system(14, 14, 14, jitter_key=(15,), jitter=0.12)
+        s.periodic = np.array([1, 1, 0], np.int32)
+        s.hi[2] = s.hi[2] + np.float32(0.5)
+        pick = None
+    c = make_ctx(pm, s)
+    c.build_verlet()
+    c.compute_lj(want_energy=True)
+    st = c.get_state()
+    th = c.thermo(recompute=False)
+    inv = idx_of_gid(s)
+    rows = np.arange(s.n) if pick is None else pick
+    rows_storage = inv[st["gid"][rows]]
+    ref = orc.lj_rows(s.pos, s.lo, s.hi, s.periodic, rc=2.5, rows=rows_storage)
+    F = st["force"][rows, :3].astype(np.float64)
+    err = orc.normalized_max_err(F, ref["F"])
+    assert err <= TOL, err
+    if pick is None:
+        # integer pair count bit-exact; energy/virial to fp32-sum accuracy
+        assert th["npairs"] == int(ref["npair"].sum())
+        assert th["pe_raw"] == pytest.approx(ref["U"].sum(), rel=1e-5)
+        assert th["virial"] == pytest.approx(ref["W"].sum(), rel=1e-5)
+        net = F.sum(0)
+        assert np.all(np.abs(net) < 1e-4 * np.abs(F).sum())  # Newton (fp32 sums)
+    c.close()
+
+
+def test_lj_perfect_lattice_closed_form(pm):
+    """Exactly representable SC lattice: F = 0 and U/N = lattice sum (pinned in
+    tests/test_oracle_pins.py by integer enumeration)."""
+    from tests.test_oracle_pins import _sc_lattice_sum
+    s = inputs.lj_lattice_system(16, 16, 16, jitter_key=(0,), a=1.125, jitter=0.0)
+    c = make_ctx(pm, s)
+    c.build_verlet()
+    c.compute_lj(want_energy=True)
+    st = c.get_state()
+    u_ref, cnt = _sc_lattice_sum(1.125, 2.5)
+    assert np.max(np.abs(st["force"][:, :3])) < 1e-4
+    th = c.thermo(recompute=False)
+    assert th["npairs"] == cnt * s.n
+    assert th["pe_raw"] / s.n == pytest.approx(u_ref, rel=1e-6)
+    c.close()
+
+
+def test_forces_bitwise_deterministic(pm):
+    s = inputs.cfg1()
+    out = []
+    for _ in range(2):
+        c = make_ctx(pm, s)
+        c.build_verlet()
+        c.compute_lj()
+        out.append(pm.sorted_by_gid(c.get_state())["force"])
+        c.close()
+    assert np.array_equal(out[0], out[1])
+
+
+def test_capped_lj_parity(pm, orc):
+    """Reading R22 capped force (cfg5 physics) on a dense random cloud."""
+    s = inputs.random_box(4000, 12.0, (16,))
+    c = make_ctx(pm, s, r_min=0.8)
+    c.build_verlet()
+    c.compute_lj()
+    st = c.get_state()
+    inv = idx_of_gid(s)
+    ref = orc.lj_rows(s.pos, s.lo, s.hi, s.periodic, rc=2.5, r_min=0.8,
+                      rows=inv[st["gid"]])
+    assert orc.normalized_max_err(st["force"][:, :3], ref["F"]) <= TOL
+    c.close()
+
+
+# ---------------------------------------------------------------- VV / NVE
+def test_vv_short_trajectory_vs_oracle(pm, orc):
+    """Positions after 50 fp32 steps within 1e-3 sigma of the fp64 oracle
+    (SURVEY §8(c) NVE pin; chaos limits longer horizons)."""
+    s = inputs.lj_lattice_system(12, 12, 12, jitter_key=(17,), vel_key=(117,))
+    c = make_ctx(pm, s)
+    stats = c.step_vv(0.005, 50)
+    assert stats["steps"] == 50 and stats["rebuilds"] >= 2
+    st = pm.sorted_by_gid(c.get_state())
+    x, v, tr = orc.vv_run(s.pos, s.vel, s.lo, s.hi, s.periodic, rc=2.5, dt=0.005, nsteps=50)
+    L = s.hi.astype(np.float64)
+    d = st["pos"][:, :3].astype(np.float64) - x
+    d -= L * np.round(d / L)
+    assert np.max(np.abs(d)) < 1e-3
+    assert np.max(np.abs(st["vel"][:, :3] - v)) < 1e-2
+    ke = 0.5 * np.sum(st["vel"][:, :3].astype(np.float64) ** 2)
+    assert ke == pytest.approx(tr[-1, 0], rel=1e-3)
+    c.close()
+
+
+def test_nve_energy_drift_cfg2(pm):
+    """BJ configs[1]: 1000 NVE steps, rebuild at skin/2; shifted-energy drift
+    <= 1e-3 (reading R25; PAPER.md:166 'the total energy was conserved');
+    total momentum conserved."""
+    s = inputs.cfg2()
+    c = make_ctx(pm, s)
+    c.build_verlet()
+    th0 = c.thermo()
+    E0 = th0["ke"] + th0["pe_shift"]
+    p0 = s.vel[:, :3].astype(np.float64).sum(0)
+    drift = 0.0
+    reb = 0
+    for _ in range(10):
+        r = c.step_vv(0.005, 100)
+        reb += r["rebuilds"]
+        th = c.thermo()
+        drift = max(drift, abs(th["ke"] + th["pe_shift"] - E0) / abs(E0))
+    assert drift < 1e-3, drift
+    assert 60 <= reb <= 400
+    st = c.get_state()
+    p = st["vel"][:, :3].astype(np.float64).sum(0)
+    assert np.all(np.abs(p - p0) < 1e-2)
+    c.close()
+
+
+def test_step_vv_graph_equals_nongraph(pm):
+    """The CUDA-graph step loop (conditional rebuild node) and the plain launch
+    loop give bitwise identical trajectories."""
+    s = inputs.lj_lattice_system(12, 12, 12, jitter_key=(18,), vel_key=(118,))
+    res = []
+    for g in (True, False):
+        c = make_ctx(pm, s, use_graphs=g)
+        r = c.step_vv(0.005, 40)
+        res.append((r["rebuilds"], pm.sorted_by_gid(c.get_state())))
+        c.close()
+    assert res[0][0] == res[1][0]
+    for k in ("pos", "vel", "force"):
+        assert np.array_equal(res[0][1][k], res[1][1][k])
+
+
+# ---------------------------------------------------------------- SPH
+def _sph_ctx(pm, s):
+    p = s.params
+    c = pm.Context()
+    c.set_domain(s.lo, s.hi, s.periodic)
+    c.set_cutoff(2.0 * p["h"], 0.0)
+    c.set_sph(p)
+    c.place(s.pos, s.vel, s.gid, s.kind)
+    c.build_verlet()
+    c.sph_density()
+    c.sph_forces()
+    return c
+
+
+def test_sph_parity_small_dam(pm, orc):
+    """cfg4 geometry at dp = 1/32 with random velocities (exercises Eq. 5):
+    densities of all particles and accelerations (a - g) of sampled ones."""
+    s = inputs.cfg4(dp=1.0 / 32.0, vel_key=(104,))
+    p = s.params
+    c = _sph_ctx(pm, s)
+    st = c.get_state()
+    inv = idx_of_gid(s)
+    rho_ref, P_ref = orc.sph_density_rows(s.pos, s.lo, s.hi, s.periodic, p)
+    got_rho = st["rho"][np.argsort(st["gid"])]
+    assert orc.normalized_max_err(got_rho, rho_ref) <= TOL
+    rows = np.random.default_rng(4).choice(s.n, 4000, replace=False)
+    a_ref = orc.sph_accel_rows(s.pos, s.vel, rho_ref, P_ref, s.kind, s.lo, s.hi, s.periodic, p,
+                               rows=rows)
+    pos_of_gid = np.argsort(st["gid"])
+    a_got = st["force"][pos_of_gid[s.gid[rows]], :3].astype(np.float64)
+    g = np.asarray(p["g"])
+    fluid = s.kind[rows] == 0
+    assert orc.normalized_max_err(a_got[fluid] - g, a_ref[fluid] - g) <= TOL
+    assert np.all(a_got[~fluid] == 0)
+    c.close()
+
+
+def test_sph_full_cfg4_sampled_density_and_hydrostatics(pm, orc):
+    """BJ configs[3] at full size (2,462,060 particles): sampled densities vs
+    the oracle; interior particles of the resting lattice feel exactly g up to
+    fp32 rounding (sum_q grad W = 0)."""
+    s = inputs.cfg4()
+    assert s.n == 2462060
+    p = s.params
+    c = _sph_ctx(pm, s)
+    st = c.get_state()
+    inv_sorted = np.argsort(st["gid"])
+    rows = np.random.default_rng(5).choice(s.n, 300, replace=False)
+    rho_ref, _ = orc.sph_density_rows(s.pos, s.lo, s.hi, s.periodic, p, rows=rows)
+    got = st["rho"][inv_sorted[s.gid[rows]]]
+    assert np.max(np.abs(got - rho_ref)) / np.sqrt(np.mean(rho_ref ** 2)) <= TOL
+    x = s.pos[:, :3]
+    dp = p["dp"]
+    interior = (s.kind == 0) & np.all(x > 4 * dp, axis=1) & (x[:, 0] < 1 - 4 * dp) & \
+        (x[:, 1] < 1 - 4 * dp) & (x[:, 2] < 0.5 - 4 * dp)
+    a = st["force"][inv_sorted[s.gid[interior]], :3].astype(np.float64)
+    assert np.max(np.abs(a - np.asarray(p["g"]))) < 1e-3 * 9.81
+    c.close()
+
+
+# ---------------------------------------------------------------- errors / edges
+def test_error_paths(pm):
+    s = inputs.cfg1()
+    # coincident pair
+    s2 = s.subset(np.arange(s.n))
+    s2.pos[1, :3] = s2.pos[0, :3]
+    c = make_ctx(pm, s2)
+    with pytest.raises(pm.PMError) as e:
+        c.build_verlet()
+    assert e.value.code == -7
+    c.close()
+    # outside a non-periodic axis
+    s3 = s.subset(np.arange(s.n))
+    s3.periodic = np.array([1, 1, 0], np.int32)
+    s3.pos[5, 2] = -1.0
+    c = make_ctx(pm, s3)
+    with pytest.raises(pm.PMError) as e:
+        c.build_cells()
+    assert e.value.code == -6
+    c.close()
+    # periodic box shorter than 3 r_v
+    c = pm.Context()
+    with pytest.raises(pm.PMError) as e:
+        c.set_domain([0, 0, 0], [8, 8, 8], [1, 1, 1])
+        c.set_cutoff(2.5, 0.3)
+    assert e.value.code == -1
+    c.close()
+    # forces before a list
+    c = make_ctx(pm, s)
+    with pytest.raises(pm.PMError) as e:
+        c.compute_lj()
+    assert e.value.code == -2
+    c.close()
+
+
+def test_tiny_and_ragged_sizes(pm, orc):
+    """n not a multiple of 32 / 256, and a single particle (empty rows)."""
+    for n in (1, 33, 1000, 4097):
+        s = inputs.random_box(n, 9.0, (20, n))
+        c = make_ctx(pm, s, r_min=0.8)  # capped: random clouds have close pairs
+        c.build_verlet()
+        c.compute_lj()
+        st = c.get_state()
+        inv = idx_of_gid(s)
+        ref = orc.lj_rows(s.pos, s.lo, s.hi, s.periodic, rc=2.5, r_min=0.8,
+                          rows=inv[st["gid"]])
+        if n > 1:
+            assert orc.normalized_max_err(st["force"][:, :3], ref["F"]) <= TOL
+        else:
+            assert np.all(st["force"] == 0)
+        c.close()
