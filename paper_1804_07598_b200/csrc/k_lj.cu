@@ -28,9 +28,11 @@ struct Acc {
   int np;
 };
 
+// One pair, branch-free: the contribution is selected to zero when the pair
+// is outside r_cut (R6) or the slot is padding (valid == false).
 template <bool MI, bool CAPPED, bool ENERGY>
 __device__ __forceinline__ void lj_pair(const Params &P, const float4 &xi, const float4 &xj,
-                                        Acc &a) {
+                                        bool valid, Acc &a) {
   float dx, dy, dz;
   if (MI) {
     dx = pair_delta1(xi.x, xj.x, P.box.L[0], P.box.halfL[0], P.box.per[0]);
@@ -42,53 +44,57 @@ __device__ __forceinline__ void lj_pair(const Params &P, const float4 &xi, const
     dz = __fsub_rn(xj.z, xi.z);
   }
   const float d2 = dist2(dx, dy, dz);
-  if (d2 < P.lj.rc2) {
-    float f, r6i;
-    if (CAPPED) {
-      const float r2e = fmaxf(d2, P.lj.r_min * P.lj.r_min);
-      const float r2ie = fast_rcp(r2e);
-      r6i = r2ie * r2ie * r2ie;
-      const float g = r6i * (P.lj.c12 * r6i - P.lj.c6);
-      f = g * fast_rsqrt(r2e) * fast_rsqrt(d2);
-    } else {
-      const float r2i = fast_rcp(d2);
-      r6i = r2i * r2i * r2i;
-      f = r2i * r6i * (P.lj.c12 * r6i - P.lj.c6);
-    }
-    // F_i += f (x_i - x_j) = -f * delta
-    a.fx = fmaf(-f, dx, a.fx);
-    a.fy = fmaf(-f, dy, a.fy);
-    a.fz = fmaf(-f, dz, a.fz);
-    if (ENERGY) {
-      a.u += 0.5f * r6i * (P.lj.e12 * r6i - P.lj.e6);
-      a.w += 0.5f * f * d2;
-      a.np += 1;
-    }
+  const bool in = valid && (d2 < P.lj.rc2);
+  float f, r6i;
+  if (CAPPED) {
+    const float r2e = fmaxf(d2, P.lj.r_min * P.lj.r_min);
+    const float r2ie = fast_rcp(r2e);
+    r6i = r2ie * r2ie * r2ie;
+    const float g = r6i * (P.lj.c12 * r6i - P.lj.c6);
+    f = g * fast_rsqrt(r2e) * fast_rsqrt(d2);
+  } else {
+    const float r2i = fast_rcp(d2);
+    r6i = r2i * r2i * r2i;
+    f = r2i * r6i * (P.lj.c12 * r6i - P.lj.c6);
+  }
+  f = in ? f : 0.0f;
+  // F_i += f (x_i - x_j) = -f * delta
+  a.fx = fmaf(-f, dx, a.fx);
+  a.fy = fmaf(-f, dy, a.fy);
+  a.fz = fmaf(-f, dz, a.fz);
+  if (ENERGY) {
+    a.u += in ? 0.5f * r6i * (P.lj.e12 * r6i - P.lj.e6) : 0.0f;
+    a.w += in ? 0.5f * f * d2 : 0.0f;
+    a.np += in ? 1 : 0;
   }
 }
 
+// Row sweep, software-pipelined: the index stream (the only HBM-resident
+// operand) is prefetched two groups of 4 ahead with streaming loads; the 4
+// position gathers of a group are issued together.  Padding slots of the last
+// group hold valid particle indices (the builder pads with real entries), so
+// every gather is in bounds and is only masked out.
 template <bool MI, bool CAPPED, bool ENERGY>
 __device__ __forceinline__ void lj_row(const Params &P, const float4 *__restrict__ pos,
                                        const int4 *__restrict__ nb4, int cnt, const float4 &xi,
                                        Acc &a) {
-  int q = 0;
-  for (; q + 4 <= cnt; q += 4) {
-    const int4 j = __ldcs(nb4 + (q >> 2) * 32);
-    const float4 x0 = __ldg(pos + j.x);
-    const float4 x1 = __ldg(pos + j.y);
-    const float4 x2 = __ldg(pos + j.z);
-    const float4 x3 = __ldg(pos + j.w);
-    lj_pair<MI, CAPPED, ENERGY>(P, xi, x0, a);
-    lj_pair<MI, CAPPED, ENERGY>(P, xi, x1, a);
-    lj_pair<MI, CAPPED, ENERGY>(P, xi, x2, a);
-    lj_pair<MI, CAPPED, ENERGY>(P, xi, x3, a);
-  }
-  if (q < cnt) {
-    const int4 j = __ldcs(nb4 + (q >> 2) * 32);
-    const int rem = cnt - q;
-    lj_pair<MI, CAPPED, ENERGY>(P, xi, __ldg(pos + j.x), a);
-    if (rem > 1) lj_pair<MI, CAPPED, ENERGY>(P, xi, __ldg(pos + j.y), a);
-    if (rem > 2) lj_pair<MI, CAPPED, ENERGY>(P, xi, __ldg(pos + j.z), a);
+  const int ng = (cnt + 3) >> 2;
+  if (ng == 0) return;
+  int4 j0 = __ldcs(nb4);
+  int4 j1 = (ng > 1) ? __ldcs(nb4 + 32) : j0;
+  for (int g = 0; g < ng; ++g) {
+    const int4 j2 = (g + 2 < ng) ? __ldcs(nb4 + (g + 2) * 32) : j1;
+    const int rem = cnt - 4 * g;
+    const float4 x0 = __ldg(pos + j0.x);
+    const float4 x1 = __ldg(pos + j0.y);
+    const float4 x2 = __ldg(pos + j0.z);
+    const float4 x3 = __ldg(pos + j0.w);
+    lj_pair<MI, CAPPED, ENERGY>(P, xi, x0, true, a);
+    lj_pair<MI, CAPPED, ENERGY>(P, xi, x1, rem > 1, a);
+    lj_pair<MI, CAPPED, ENERGY>(P, xi, x2, rem > 2, a);
+    lj_pair<MI, CAPPED, ENERGY>(P, xi, x3, rem > 3, a);
+    j0 = j1;
+    j1 = j2;
   }
 }
 

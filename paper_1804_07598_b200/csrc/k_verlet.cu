@@ -10,78 +10,182 @@
 // per 4 neighbours.
 #include "pm_internal.cuh"
 
+#include <algorithm>
+
 namespace pm {
 
 namespace {
 
-__device__ __forceinline__ void put4(int4 &acc, int k, int j) {
-  switch (k & 3) {
-    case 0: acc.x = j; break;
-    case 1: acc.y = j; break;
-    case 2: acc.z = j; break;
-    default: acc.w = j; break;
+// Append j to this lane's row when hit: entries are collected in an int4
+// register and flushed every 4 hits with one predicated 16-byte store; all
+// updates are selects, so there is no divergent branch per candidate.
+struct RowBuf {
+  int4 acc;
+  int k;
+};
+
+__device__ __forceinline__ void append(RowBuf &r, bool hit, int j, int4 *__restrict__ out, int cap) {
+  const int s = r.k & 3;
+  r.acc.x = (hit && s == 0) ? j : r.acc.x;
+  r.acc.y = (hit && s == 1) ? j : r.acc.y;
+  r.acc.z = (hit && s == 2) ? j : r.acc.z;
+  r.acc.w = (hit && s == 3) ? j : r.acc.w;
+  if (hit && s == 3 && r.k < cap) out[(r.k >> 2) * 32] = r.acc;
+  r.k += hit ? 1 : 0;
+}
+
+// Scan one contiguous candidate range [b, e) (one x-run of cells in cell
+// order).  Periodic images are handled per run (R4 "per-run
+// shift"): if the run's cells were reached across the low face the whole run
+// lies at the high end of the box and every candidate is shifted by -L
+// (fl(x_j - L), exact by Sterbenz); if reached across the high face, the
+// lane's own coordinate is shifted instead (xi_eff = fl(x_i - L), exact).
+// For n >= 3 cells per periodic axis this reproduces R4's choice for every
+// pair that can be a neighbour, so membership is bit-identical.
+template <bool MIX>
+__device__ __forceinline__ void scan_run(const Params &P, const float4 *__restrict__ pos, int b,
+                                         int e, int i, const float4 &xi_eff, float3 csh,
+                                         bool mine, int cap, int4 *__restrict__ out, RowBuf &r,
+                                         bool &coinc) {
+  const float rv2 = P.rv2;
+  int j = b;
+  for (; j + 8 <= e; j += 8) {
+    float4 x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = pos[j + u];  // same address in all lanes
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const float dx = MIX ? pair_delta1(xi_eff.x, x[u].x, P.box.L[0], P.box.halfL[0], 1)
+                           : __fsub_rn(__fsub_rn(x[u].x, csh.x), xi_eff.x);
+      const float dy = __fsub_rn(__fsub_rn(x[u].y, csh.y), xi_eff.y);
+      const float dz = __fsub_rn(__fsub_rn(x[u].z, csh.z), xi_eff.z);
+      const float d2 = dist2(dx, dy, dz);
+      const bool hit = mine && (d2 < rv2) && (j + u != i);
+      coinc |= hit && (d2 == 0.0f);
+      append(r, hit, j + u, out, cap);
+    }
+  }
+  for (; j < e; ++j) {
+    const float4 xj = pos[j];
+    const float dx = MIX ? pair_delta1(xi_eff.x, xj.x, P.box.L[0], P.box.halfL[0], 1)
+                         : __fsub_rn(__fsub_rn(xj.x, csh.x), xi_eff.x);
+    const float dy = __fsub_rn(__fsub_rn(xj.y, csh.y), xi_eff.y);
+    const float dz = __fsub_rn(__fsub_rn(xj.z, csh.z), xi_eff.z);
+    const float d2 = dist2(dx, dy, dz);
+    const bool hit = mine && (d2 < rv2) && (j != i);
+    coinc |= hit && (d2 == 0.0f);
+    append(r, hit, j, out, cap);
   }
 }
 
-__global__ void __launch_bounds__(256) k_verlet(Params P, Bufs B, int n) {
+// Thread per particle (row), warp-uniform candidate stream.  The warp's 32
+// consecutive cell-ordered particles occupy a few consecutive cells; for each
+// x-row segment [c_first, c_last] of those cells, every lane scans the union
+// of the segment's 27-cell stencils: 9 (dy, dz) rows, each one contiguous x
+// range [c_first - 1, c_last + 1] of cells = one contiguous index range in
+// cell order.  A lane only tests candidates of its own segment, and the
+// union has no repeats, so row i gets every j with d2 < r_v^2 exactly once
+// (the extra candidates of the union are farther than r_v and rejected by
+// the same pinned test).  All lanes read the same position each iteration
+// (broadcast), there is no divergence, and rows come out in a fixed order.
+__global__ void __launch_bounds__(256, 3) k_verlet(Params P, Bufs B, int n) {
   State *st = B.st;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int wbase = i - lane;
+  if (wbase >= n) return;  // whole warp out of range
+  const bool active = i < n;
   const int cap = P.nbr_cap;
-  int k = 0;
-  if (i < n) {
-    const float4 *__restrict__ pos = B.pos[st->cur_pv];
-    const float4 xi = pos[i];
-    const int c0 = cell_coord(xi.x, P.box.lo[0], P.grid.inv_w[0], P.grid.n[0]);
-    const int c1 = cell_coord(xi.y, P.box.lo[1], P.grid.inv_w[1], P.grid.n[1]);
-    const int c2 = cell_coord(xi.z, P.box.lo[2], P.grid.inv_w[2], P.grid.n[2]);
-    int4 *__restrict__ out = reinterpret_cast<int4 *>(B.nbr) + nbr_base4(i, cap);
-    int4 acc = make_int4(i, i, i, i);
-    bool coincident = false;
+  const int nx = P.grid.n[0], ny = P.grid.n[1], nz = P.grid.n[2];
+  const float4 *__restrict__ pos = B.pos[st->cur_pv];
+  const float4 xi = active ? pos[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  int cell = -1;
+  if (active) {
+    const int c0 = cell_coord(xi.x, P.box.lo[0], P.grid.inv_w[0], nx);
+    const int c1 = cell_coord(xi.y, P.box.lo[1], P.grid.inv_w[1], ny);
+    const int c2 = cell_coord(xi.z, P.box.lo[2], P.grid.inv_w[2], nz);
+    cell = c0 + nx * (c1 + ny * c2);
+  }
+  const int row_id = active ? cell / nx : 0x7fffffff;  // (cy, cz) row of my cell
+  int4 *__restrict__ out = reinterpret_cast<int4 *>(B.nbr) + nbr_base4(i, cap);
+  RowBuf rb;
+  rb.acc = make_int4(i, i, i, i);  // padding = own index (valid, masked later)
+  rb.k = 0;
+  bool coinc = false;
+  const float Lx = P.box.L[0], Ly = P.box.L[1], Lz = P.box.L[2];
+  unsigned todo = __ballot_sync(0xffffffffu, active);
+  while (todo) {
+    // segment = lanes whose cell lies in the row of the lowest pending lane
+    const int lead = __ffs(todo) - 1;
+    const int seg_row = __shfl_sync(0xffffffffu, row_id, lead);
+    const bool mine = active && row_id == seg_row;
+    const unsigned seg = __ballot_sync(0xffffffffu, mine);
+    todo &= ~seg;
+    int cmin = mine ? cell % nx : 0x7fffffff, cmax = mine ? cell % nx : -1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      cmin = min(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
+      cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+    }
+    const int cy = seg_row % ny, cz = seg_row / ny;
+    int xa = cmin - 1, xb = cmax + 1;
+    bool mix = false;  // whole periodic x-row: per-pair R4 rule along x
+    if (!P.box.per[0]) {
+      xa = max(xa, 0);
+      xb = min(xb, nx - 1);
+    } else if (xb - xa + 1 >= nx) {
+      xa = 0;
+      xb = nx - 1;
+      mix = true;
+    }
     for (int dz = -1; dz <= 1; ++dz) {
-      int cz = c2 + dz;
-      if (cz < 0 || cz >= P.grid.n[2]) {
+      int qz = cz + dz;
+      float shz = 0.f, lz = 0.f;  // candidate shift / own shift along z
+      if (qz < 0 || qz >= nz) {
         if (!P.box.per[2]) continue;
-        cz += (cz < 0) ? P.grid.n[2] : -P.grid.n[2];
+        if (qz < 0) { qz += nz; shz = Lz; } else { qz -= nz; lz = Lz; }
       }
       for (int dy = -1; dy <= 1; ++dy) {
-        int cy = c1 + dy;
-        if (cy < 0 || cy >= P.grid.n[1]) {
+        int qy = cy + dy;
+        float shy = 0.f, ly = 0.f;
+        if (qy < 0 || qy >= ny) {
           if (!P.box.per[1]) continue;
-          cy += (cy < 0) ? P.grid.n[1] : -P.grid.n[1];
+          if (qy < 0) { qy += ny; shy = Ly; } else { qy -= ny; ly = Ly; }
         }
-        const int row = P.grid.n[0] * (cy + P.grid.n[1] * cz);
-        for (int dx = -1; dx <= 1; ++dx) {
-          int cx = c0 + dx;
-          if (cx < 0 || cx >= P.grid.n[0]) {
-            if (!P.box.per[0]) continue;
-            cx += (cx < 0) ? P.grid.n[0] : -P.grid.n[0];
-          }
-          const int c = cx + row;
-          const int s = B.start[c], e = B.start[c + 1];
-          for (int j = s; j < e; ++j) {
-            if (j == i) continue;
-            const float4 xj = pos[j];
-            const float dx_ = pair_delta1(xi.x, xj.x, P.box.L[0], P.box.halfL[0], P.box.per[0]);
-            const float dy_ = pair_delta1(xi.y, xj.y, P.box.L[1], P.box.halfL[1], P.box.per[1]);
-            const float dz_ = pair_delta1(xi.z, xj.z, P.box.L[2], P.box.halfL[2], P.box.per[2]);
-            const float d2 = dist2(dx_, dy_, dz_);
-            if (d2 < P.rv2) {
-              coincident |= (d2 == 0.0f);
-              if (k < cap) {
-                put4(acc, k, j);
-                if ((k & 3) == 3) out[(k >> 2) * 32] = acc;
-              }
-              ++k;
-            }
-          }
+        const int rowc = nx * (qy + ny * qz);
+        // x range [xa, xb] of cells, split at the periodic seam
+        int a0 = xa, b0 = xb, a1 = 0, b1 = -1;
+        float sx0 = 0.f, lx0 = 0.f, sx1 = 0.f, lx1 = 0.f;
+        if (xa < 0) {  // part [xa, -1] wrapped to the high end
+          a0 = xa + nx; b0 = nx - 1; sx0 = Lx;
+          a1 = 0; b1 = xb;
+        } else if (xb > nx - 1) {  // part [nx, xb] wrapped to the low end
+          a0 = xa; b0 = nx - 1;
+          a1 = 0; b1 = xb - nx; lx1 = Lx;
+        }
+        const float4 xe0 = make_float4(__fsub_rn(xi.x, lx0), __fsub_rn(xi.y, ly),
+                                       __fsub_rn(xi.z, lz), 0.f);
+        if (mix)
+          scan_run<true>(P, pos, B.start[rowc + a0], B.start[rowc + b0 + 1], i, xe0,
+                         make_float3(0.f, shy, shz), mine, cap, out, rb, coinc);
+        else
+          scan_run<false>(P, pos, B.start[rowc + a0], B.start[rowc + b0 + 1], i, xe0,
+                          make_float3(sx0, shy, shz), mine, cap, out, rb, coinc);
+        if (b1 >= a1) {
+          const float4 xe1 = make_float4(__fsub_rn(xi.x, lx1), __fsub_rn(xi.y, ly),
+                                         __fsub_rn(xi.z, lz), 0.f);
+          scan_run<false>(P, pos, B.start[rowc + a1], B.start[rowc + b1 + 1], i, xe1,
+                          make_float3(sx1, shy, shz), mine, cap, out, rb, coinc);
         }
       }
     }
-    if ((k & 3) != 0 && k < cap) out[(k >> 2) * 32] = acc;
-    B.cnt[i] = k < cap ? k : cap;
-    if (coincident) raise_error(st, -7 /*PM_E_COINCIDENT*/, (long long)B.gid[st->cur_id][i]);
   }
-  // warp reductions of the row statistics
+  const int k = rb.k;
+  if (active) {
+    if ((k & 3) != 0 && k < cap) out[(k >> 2) * 32] = rb.acc;
+    B.cnt[i] = k;
+    if (coinc) raise_error(st, -7 /*PM_E_COINCIDENT*/, (long long)B.gid[st->cur_id][i]);
+  }
   int kmax = k;
   long long ksum = k;
 #pragma unroll
@@ -89,7 +193,7 @@ __global__ void __launch_bounds__(256) k_verlet(Params P, Bufs B, int n) {
     kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
     ksum += __shfl_xor_sync(0xffffffffu, ksum, o);
   }
-  if ((threadIdx.x & 31) == 0 && ksum > 0) {
+  if (lane == 0 && ksum > 0) {
     atomicMax(&st->max_row, kmax);
     atomicAdd(reinterpret_cast<unsigned long long *>(&st->nnz), (unsigned long long)ksum);
     if (kmax > cap) {

@@ -52,6 +52,7 @@ struct pm_ctx_s {
 
   // graph
   cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;  // kept alive: exec node updates need its nodes
   bool graph_valid = false;
   float graph_dt = 0.f;
   bool graph_prof = false;
@@ -129,7 +130,9 @@ cudaError_t dalloc(T **p, int64_t count) {
 
 void destroy_graph(pm_ctx c) {
   if (c->exec) cudaGraphExecDestroy(c->exec);
+  if (c->graph) cudaGraphDestroy(c->graph);
   c->exec = nullptr;
+  c->graph = nullptr;
   c->graph_valid = false;
 }
 
@@ -358,7 +361,7 @@ pm_status build_graph(pm_ctx c, float dt, bool prof) {
     CUDA_TRY(c, cudaGraphAddEventRecordNode(&c->ev_node[1], g, &nF, 1, c->ev_pool[1]));
   }
   CUDA_TRY(c, cudaGraphInstantiate(&c->exec, g, 0));
-  cudaGraphDestroy(g);
+  c->graph = g;
   c->graph_valid = true;
   c->graph_dt = dt;
   c->graph_prof = prof;

@@ -123,6 +123,25 @@ def test_verlet_sets_bit_exact(pm, orc, name):
     c.close()
 
 
+@pytest.mark.parametrize("L,n,per", [(8.5, 600, (1, 1, 1)), (11.5, 1500, (1, 1, 1)),
+                                     (14.5, 2500, (1, 0, 1)), (25.0, 300, (1, 1, 1)),
+                                     (9.0, 700, (0, 1, 1)), (40.0, 3000, (1, 1, 0))])
+def test_verlet_small_grids_and_sparse(pm, orc, L, n, per):
+    """3, 4 and 5 cells per periodic axis (every stencil wraps), sparse boxes
+    (a warp spans many cells: whole-row path), mixed boundary conditions."""
+    s = inputs.random_box(n, L, (31, n), periodic=per)
+    c = make_ctx(pm, s)
+    c.build_verlet()
+    rp, col = c.get_verlet()
+    st = c.get_state()
+    inv = idx_of_gid(s)
+    rrp, rcols, _ = orc.verlet_rows(s.pos, s.lo, s.hi, s.periodic, rv32(2.5, 0.3),
+                                    rows=inv[st["gid"]], want_shift=False)
+    bad = _row_sets_equal(rp, col, st["gid"], rrp, rcols, s.gid)
+    assert bad < 0, f"row {bad} differs"
+    c.close()
+
+
 def test_verlet_capacity_overflow_retry(pm, orc):
     """A tiny initial capacity overflows; the library grows it and retries."""
     s = inputs.cfg1()
@@ -172,7 +191,7 @@ def test_lj_forces_parity(pm, orc, name):
 def test_lj_perfect_lattice_closed_form(pm):
     """Exactly representable SC lattice: F = 0 and U/N = lattice sum (pinned in
     tests/test_oracle_pins.py by integer enumeration)."""
-    from tests.test_oracle_pins import _sc_lattice_sum
+    from test_oracle_pins import _sc_lattice_sum
     s = inputs.lj_lattice_system(16, 16, 16, jitter_key=(0,), a=1.125, jitter=0.0)
     c = make_ctx(pm, s)
     c.build_verlet()
@@ -309,26 +328,62 @@ def test_sph_parity_small_dam(pm, orc):
     c.close()
 
 
-def test_sph_full_cfg4_sampled_density_and_hydrostatics(pm, orc):
-    """BJ configs[3] at full size (2,462,060 particles): sampled densities vs
-    the oracle; interior particles of the resting lattice feel exactly g up to
-    fp32 rounding (sum_q grad W = 0)."""
-    s = inputs.cfg4()
+def test_sph_full_cfg4_sampled_parity(pm, orc):
+    """BJ configs[3] at full size (2,462,060 particles, dp = 1/160): sampled
+    densities, and accelerations of a stratified sample (free surface, wall,
+    interior) against the oracle, which gets its own densities of the sampled
+    rows' whole neighbourhoods (brute force, fp64)."""
+    s = inputs.cfg4(vel_key=(104,))
     assert s.n == 2462060
     p = s.params
     c = _sph_ctx(pm, s)
     st = c.get_state()
     inv_sorted = np.argsort(st["gid"])
-    rows = np.random.default_rng(5).choice(s.n, 300, replace=False)
+    rng = np.random.default_rng(5)
+    rows = rng.choice(s.n, 200, replace=False)
     rho_ref, _ = orc.sph_density_rows(s.pos, s.lo, s.hi, s.periodic, p, rows=rows)
     got = st["rho"][inv_sorted[s.gid[rows]]]
     assert np.max(np.abs(got - rho_ref)) / np.sqrt(np.mean(rho_ref ** 2)) <= TOL
     x = s.pos[:, :3]
     dp = p["dp"]
-    interior = (s.kind == 0) & np.all(x > 4 * dp, axis=1) & (x[:, 0] < 1 - 4 * dp) & \
-        (x[:, 1] < 1 - 4 * dp) & (x[:, 2] < 0.5 - 4 * dp)
-    a = st["force"][inv_sorted[s.gid[interior]], :3].astype(np.float64)
-    assert np.max(np.abs(a - np.asarray(p["g"]))) < 1e-3 * 9.81
+    fluid = s.kind == 0
+    surf = np.where(fluid & (x[:, 2] > 0.5 - 2 * dp))[0]
+    wall = np.where(fluid & (x[:, 0] < 2 * dp))[0]
+    inner = np.where(fluid & np.all(np.abs(x - [0.5, 0.5, 0.25]) < 0.1, axis=1))[0]
+    sample = np.concatenate([rng.choice(g, 12, replace=False) for g in (surf, wall, inner)])
+    rp, cols, _ = orc.verlet_rows(s.pos, s.lo, s.hi, s.periodic,
+                                  np.float32(2 * np.float32(p["h"])), rows=sample,
+                                  want_shift=False)
+    need = np.unique(np.concatenate([sample, cols]))
+    rho_n, P_n = orc.sph_density_rows(s.pos, s.lo, s.hi, s.periodic, p, rows=need)
+    rho_all = np.full(s.n, np.nan)
+    P_all = np.full(s.n, np.nan)
+    rho_all[need] = rho_n
+    P_all[need] = P_n
+    a_ref = orc.sph_accel_rows(s.pos, s.vel, rho_all, P_all, s.kind, s.lo, s.hi, s.periodic, p,
+                               rows=sample)
+    assert np.all(np.isfinite(a_ref))
+    g = np.asarray(p["g"])
+    a_got = st["force"][inv_sorted[s.gid[sample]], :3].astype(np.float64)
+    assert orc.normalized_max_err(a_got - g, a_ref - g) <= TOL
+    c.close()
+
+
+def test_sph_hydrostatic_exact_lattice(pm):
+    """On a lattice exactly representable in fp32 (dp = 1/64), interior fluid
+    particles at rest feel exactly g up to fp32 rounding: sum_q grad W = 0
+    (pinned for the oracle in test_oracle_pins.py)."""
+    s = inputs.cfg4(dp=1.0 / 64.0)
+    p = s.params
+    c = _sph_ctx(pm, s)
+    st = c.get_state()
+    x = st["pos"][:, :3]
+    dp = p["dp"]
+    interior = (st["gid"] >= 0) & (s.kind[st["gid"]] == 0) & np.all(x > 4 * dp, axis=1) & \
+        (x[:, 0] < 1 - 6 * dp) & (x[:, 1] < 1 - 4 * dp) & (x[:, 2] < 0.5 - 6 * dp)
+    a = st["force"][interior, :3].astype(np.float64)
+    assert interior.sum() > 10000
+    assert np.max(np.abs(a - np.asarray(p["g"]))) < 1e-3
     c.close()
 
 
