@@ -70,25 +70,39 @@ __device__ __forceinline__ void lj_pair(const Params &P, const float4 &xi, const
 }
 
 // Row sweep, software-pipelined: the index stream (the only HBM-resident
-// operand) is prefetched two groups of 4 ahead with streaming loads; the 4
-// position gathers of a group are issued together.  Padding slots of the last
-// group hold valid particle indices (the builder pads with real entries), so
-// every gather is in bounds and is only masked out.
+// operand) is prefetched two groups of 4 ahead with streaming loads (each a
+// coalesced 128-byte line across the warp); the 4 position gathers of a group
+// are issued together.  Rows are padded to a multiple of 4 with valid
+// particle indices (the builder pads with the row's own index), so every
+// gather is in bounds and padding is only masked out.
+struct Idx4 {
+  int a, b, c, d;
+};
+
+__device__ __forceinline__ Idx4 ld_idx4(const int *__restrict__ p) {
+  Idx4 r;
+  r.a = __ldcs(p);
+  r.b = __ldcs(p + 32);
+  r.c = __ldcs(p + 64);
+  r.d = __ldcs(p + 96);
+  return r;
+}
+
 template <bool MI, bool CAPPED, bool ENERGY>
 __device__ __forceinline__ void lj_row(const Params &P, const float4 *__restrict__ pos,
-                                       const int4 *__restrict__ nb4, int cnt, const float4 &xi,
+                                       const int *__restrict__ nb, int cnt, const float4 &xi,
                                        Acc &a) {
   const int ng = (cnt + 3) >> 2;
   if (ng == 0) return;
-  int4 j0 = __ldcs(nb4);
-  int4 j1 = (ng > 1) ? __ldcs(nb4 + 32) : j0;
+  Idx4 j0 = ld_idx4(nb);
+  Idx4 j1 = (ng > 1) ? ld_idx4(nb + 128) : j0;
   for (int g = 0; g < ng; ++g) {
-    const int4 j2 = (g + 2 < ng) ? __ldcs(nb4 + (g + 2) * 32) : j1;
+    const Idx4 j2 = (g + 2 < ng) ? ld_idx4(nb + (g + 2) * 128) : j1;
     const int rem = cnt - 4 * g;
-    const float4 x0 = __ldg(pos + j0.x);
-    const float4 x1 = __ldg(pos + j0.y);
-    const float4 x2 = __ldg(pos + j0.z);
-    const float4 x3 = __ldg(pos + j0.w);
+    const float4 x0 = __ldg(pos + j0.a);
+    const float4 x1 = __ldg(pos + j0.b);
+    const float4 x2 = __ldg(pos + j0.c);
+    const float4 x3 = __ldg(pos + j0.d);
     lj_pair<MI, CAPPED, ENERGY>(P, xi, x0, true, a);
     lj_pair<MI, CAPPED, ENERGY>(P, xi, x1, rem > 1, a);
     lj_pair<MI, CAPPED, ENERGY>(P, xi, x2, rem > 2, a);
@@ -117,11 +131,11 @@ __device__ __forceinline__ Acc lj_force_of(const Params &P, const Bufs &B,
   const bool mi = __any_sync(0xffffffffu, active && near_periodic_face(P, xi));
   if (active) {
     const int cnt = B.cnt[i];
-    const int4 *nb4 = reinterpret_cast<const int4 *>(B.nbr) + nbr_base4(i, P.nbr_cap);
+    const int *nb = B.nbr + nbr_row_base(i, P.nbr_cap);
     if (mi)
-      lj_row<true, CAPPED, ENERGY>(P, pos, nb4, cnt, xi, a);
+      lj_row<true, CAPPED, ENERGY>(P, pos, nb, cnt, xi, a);
     else
-      lj_row<false, CAPPED, ENERGY>(P, pos, nb4, cnt, xi, a);
+      lj_row<false, CAPPED, ENERGY>(P, pos, nb, cnt, xi, a);
   }
   return a;
 }

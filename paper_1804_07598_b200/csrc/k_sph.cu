@@ -50,11 +50,11 @@ __global__ void __launch_bounds__(256) k_sph_density(Params P, Bufs B, int n) {
   const float4 *__restrict__ pos = B.pos[st->cur_pv];
   const float4 xi = pos[i];
   const int cnt = B.cnt[i];
-  const int *nb = B.nbr + nbr_base4(i, P.nbr_cap) * 4;
+  const int *nb = B.nbr + nbr_row_base(i, P.nbr_cap);
   const double inv_h = 1.0 / (double)P.sph.h;
   double s = 0.0;
   for (int k = 0; k < cnt; ++k) {
-    const int j = __ldcs(nb + (k >> 2) * 128 + (k & 3));
+    const int j = __ldcs(nb + (k << 5));
     const float4 xj = __ldg(pos + j);
     double d[3];
 #pragma unroll
@@ -96,11 +96,11 @@ __global__ void __launch_bounds__(256) k_sph_forces(Params P, Bufs B, int n) {
   const float4 vi = vel[i];
   const float2 rpi = B.rhoP[i];
   const int cnt = B.cnt[i];
-  const int *nb = B.nbr + nbr_base4(i, P.nbr_cap) * 4;
+  const int *nb = B.nbr + nbr_row_base(i, P.nbr_cap);
   float ax = 0.f, ay = 0.f, az = 0.f;
   const float acb = P.sph.alpha * P.sph.cbar;
   for (int k = 0; k < cnt; ++k) {
-    const int j = __ldcs(nb + (k >> 2) * 128 + (k & 3));
+    const int j = __ldcs(nb + (k << 5));
     const float3 d = delta3(P, xi, __ldg(pos + j));  // x_j - x_i
     const float d2 = dist2(d.x, d.y, d.z);
     const float rinv = fast_rsqrt(d2);

@@ -5,9 +5,8 @@
 // the FULL list (both directions, no atomics in the force sweep): row i holds
 // every j != i with d2_32(i, j) < r_v^2 (R4/R5), found over the 27-cell
 // stencil of the cell list.  Layout: SELL-32 (one slice = one warp of 32
-// consecutive cell-ordered particles) with a fixed per-row capacity, entries
-// interleaved by 4 so that the force sweep reads one coalesced int4 per lane
-// per 4 neighbours.
+// consecutive cell-ordered particles) with a fixed per-row capacity; entry k
+// of the 32 rows of a slice is one contiguous 128-byte line.
 #include "pm_internal.cuh"
 
 #include <algorithm>
@@ -16,22 +15,20 @@ namespace pm {
 
 namespace {
 
-// Append j to this lane's row when hit: entries are collected in an int4
-// register and flushed every 4 hits with one predicated 16-byte store; all
-// updates are selects, so there is no divergent branch per candidate.
-struct RowBuf {
-  int4 acc;
-  int k;
-};
-
-__device__ __forceinline__ void append(RowBuf &r, bool hit, int j, int4 *__restrict__ out, int cap) {
-  const int s = r.k & 3;
-  r.acc.x = (hit && s == 0) ? j : r.acc.x;
-  r.acc.y = (hit && s == 1) ? j : r.acc.y;
-  r.acc.z = (hit && s == 2) ? j : r.acc.z;
-  r.acc.w = (hit && s == 3) ? j : r.acc.w;
-  if (hit && s == 3 && r.k < cap) out[(r.k >> 2) * 32] = r.acc;
-  r.k += hit ? 1 : 0;
+// Append j to this lane's row when hit: one predicated 4-byte store (inline
+// PTX: no divergent branch) at row + 128*k bytes (mad.wide.u32).  CLAMP: the
+// run could overflow the row, so the slot is clamped to cap-1 (an overflowing
+// row only rewrites its last slot; the build is then retried with a larger
+// capacity).
+template <bool CLAMP>
+__device__ __forceinline__ void append(int *__restrict__ row, int cap, int &k, bool hit, int j) {
+  const unsigned kk = CLAMP ? (unsigned)min(k, cap - 1) : (unsigned)k;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 a;\n\tsetp.ne.b32 p, %2, 0;\n\t"
+      "mad.wide.u32 a, %3, 128, %0;\n\t@p st.global.b32 [a], %1;\n\t}" ::"l"(row),
+      "r"(j), "r"((int)hit), "r"(kk)
+      : "memory");
+  k += hit ? 1 : 0;
 }
 
 // Scan one contiguous candidate range [b, e) (one x-run of cells in cell
@@ -41,40 +38,58 @@ __device__ __forceinline__ void append(RowBuf &r, bool hit, int j, int4 *__restr
 // (fl(x_j - L), exact by Sterbenz); if reached across the high face, the
 // lane's own coordinate is shifted instead (xi_eff = fl(x_i - L), exact).
 // For n >= 3 cells per periodic axis this reproduces R4's choice for every
-// pair that can be a neighbour, so membership is bit-identical.
-template <bool MIX>
+// pair that can be a neighbour, so membership is bit-identical.  MIX: the
+// run covers a whole periodic x-row, use the per-pair R4 rule along x.
+// dmin tracks the smallest d2 of a hit: 0 means two coincident particles.
+template <bool SHIFTJ, bool MIX, bool CLAMP>
+__device__ __forceinline__ void test_append(const Params &P, const float4 &xi_eff,
+                                            const float3 &csh, const float4 &xj, int j, int i,
+                                            bool mine, int *__restrict__ row, int cap, int &k,
+                                            float &dmin) {
+  float dx, dy, dz;
+  if (MIX) dx = pair_delta1(xi_eff.x, xj.x, P.box.L[0], P.box.halfL[0], 1);
+  else dx = SHIFTJ ? __fsub_rn(__fsub_rn(xj.x, csh.x), xi_eff.x) : __fsub_rn(xj.x, xi_eff.x);
+  dy = SHIFTJ ? __fsub_rn(__fsub_rn(xj.y, csh.y), xi_eff.y) : __fsub_rn(xj.y, xi_eff.y);
+  dz = SHIFTJ ? __fsub_rn(__fsub_rn(xj.z, csh.z), xi_eff.z) : __fsub_rn(xj.z, xi_eff.z);
+  const float d2 = dist2(dx, dy, dz);
+  const bool hit = mine && (d2 < P.rv2) && (j != i);
+  dmin = fminf(dmin, hit ? d2 : 1.0f);
+  append<CLAMP>(row, cap, k, hit, j);
+}
+
+template <bool SHIFTJ, bool MIX, bool CLAMP>
 __device__ __forceinline__ void scan_run(const Params &P, const float4 *__restrict__ pos, int b,
                                          int e, int i, const float4 &xi_eff, float3 csh,
-                                         bool mine, int cap, int4 *__restrict__ out, RowBuf &r,
-                                         bool &coinc) {
-  const float rv2 = P.rv2;
+                                         bool mine, int cap, int *__restrict__ row, int &k,
+                                         float &dmin) {
   int j = b;
   for (; j + 8 <= e; j += 8) {
     float4 x[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) x[u] = pos[j + u];  // same address in all lanes
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const float dx = MIX ? pair_delta1(xi_eff.x, x[u].x, P.box.L[0], P.box.halfL[0], 1)
-                           : __fsub_rn(__fsub_rn(x[u].x, csh.x), xi_eff.x);
-      const float dy = __fsub_rn(__fsub_rn(x[u].y, csh.y), xi_eff.y);
-      const float dz = __fsub_rn(__fsub_rn(x[u].z, csh.z), xi_eff.z);
-      const float d2 = dist2(dx, dy, dz);
-      const bool hit = mine && (d2 < rv2) && (j + u != i);
-      coinc |= hit && (d2 == 0.0f);
-      append(r, hit, j + u, out, cap);
-    }
+    for (int u = 0; u < 8; ++u)
+      test_append<SHIFTJ, MIX, CLAMP>(P, xi_eff, csh, x[u], j + u, i, mine, row, cap, k, dmin);
   }
-  for (; j < e; ++j) {
-    const float4 xj = pos[j];
-    const float dx = MIX ? pair_delta1(xi_eff.x, xj.x, P.box.L[0], P.box.halfL[0], 1)
-                         : __fsub_rn(__fsub_rn(xj.x, csh.x), xi_eff.x);
-    const float dy = __fsub_rn(__fsub_rn(xj.y, csh.y), xi_eff.y);
-    const float dz = __fsub_rn(__fsub_rn(xj.z, csh.z), xi_eff.z);
-    const float d2 = dist2(dx, dy, dz);
-    const bool hit = mine && (d2 < rv2) && (j != i);
-    coinc |= hit && (d2 == 0.0f);
-    append(r, hit, j, out, cap);
+  for (; j < e; ++j)
+    test_append<SHIFTJ, MIX, CLAMP>(P, xi_eff, csh, pos[j], j, i, mine, row, cap, k, dmin);
+}
+
+__device__ __forceinline__ void scan_any(const Params &P, const float4 *__restrict__ pos, int b,
+                                         int e, int i, const float4 &xi_eff, float3 csh, bool mix,
+                                         bool mine, int cap, int *__restrict__ row, int &k,
+                                         float &dmin) {
+  const bool sj = csh.x != 0.f || csh.y != 0.f || csh.z != 0.f;
+  // warp-uniform: can any lane of the warp overflow its row in this run?
+  const bool clamp = __any_sync(0xffffffffu, k + (e - b) > cap);
+  if (!clamp && !mix && !sj) {
+    scan_run<false, false, false>(P, pos, b, e, i, xi_eff, csh, mine, cap, row, k, dmin);
+  } else if (!clamp && !mix) {
+    scan_run<true, false, false>(P, pos, b, e, i, xi_eff, csh, mine, cap, row, k, dmin);
+  } else if (mix) {
+    scan_run<true, true, true>(P, pos, b, e, i, xi_eff, csh, mine, cap, row, k, dmin);
+  } else {
+    scan_run<true, false, true>(P, pos, b, e, i, xi_eff, csh, mine, cap, row, k, dmin);
   }
 }
 
@@ -107,11 +122,9 @@ __global__ void __launch_bounds__(256, 3) k_verlet(Params P, Bufs B, int n) {
     cell = c0 + nx * (c1 + ny * c2);
   }
   const int row_id = active ? cell / nx : 0x7fffffff;  // (cy, cz) row of my cell
-  int4 *__restrict__ out = reinterpret_cast<int4 *>(B.nbr) + nbr_base4(i, cap);
-  RowBuf rb;
-  rb.acc = make_int4(i, i, i, i);  // padding = own index (valid, masked later)
-  rb.k = 0;
-  bool coinc = false;
+  int *__restrict__ row = B.nbr + nbr_row_base(i, cap);
+  int k = 0;
+  float dmin = 1.0f;
   const float Lx = P.box.L[0], Ly = P.box.L[1], Lz = P.box.L[2];
   unsigned todo = __ballot_sync(0xffffffffu, active);
   while (todo) {
@@ -165,26 +178,23 @@ __global__ void __launch_bounds__(256, 3) k_verlet(Params P, Bufs B, int n) {
         }
         const float4 xe0 = make_float4(__fsub_rn(xi.x, lx0), __fsub_rn(xi.y, ly),
                                        __fsub_rn(xi.z, lz), 0.f);
-        if (mix)
-          scan_run<true>(P, pos, B.start[rowc + a0], B.start[rowc + b0 + 1], i, xe0,
-                         make_float3(0.f, shy, shz), mine, cap, out, rb, coinc);
-        else
-          scan_run<false>(P, pos, B.start[rowc + a0], B.start[rowc + b0 + 1], i, xe0,
-                          make_float3(sx0, shy, shz), mine, cap, out, rb, coinc);
+        scan_any(P, pos, B.start[rowc + a0], B.start[rowc + b0 + 1], i, xe0,
+                 make_float3(mix ? 0.f : sx0, shy, shz), mix, mine, cap, row, k, dmin);
         if (b1 >= a1) {
           const float4 xe1 = make_float4(__fsub_rn(xi.x, lx1), __fsub_rn(xi.y, ly),
                                          __fsub_rn(xi.z, lz), 0.f);
-          scan_run<false>(P, pos, B.start[rowc + a1], B.start[rowc + b1 + 1], i, xe1,
-                          make_float3(sx1, shy, shz), mine, cap, out, rb, coinc);
+          scan_any(P, pos, B.start[rowc + a1], B.start[rowc + b1 + 1], i, xe1,
+                   make_float3(sx1, shy, shz), false, mine, cap, row, k, dmin);
         }
       }
     }
   }
-  const int k = rb.k;
   if (active) {
-    if ((k & 3) != 0 && k < cap) out[(k >> 2) * 32] = rb.acc;
+    // pad the row to a multiple of 4 with this particle's own index (a valid
+    // index; the force sweep reads groups of 4 and masks padding slots)
+    for (int q = k; q < cap && (q & 3) != 0; ++q) row[q << 5] = i;
     B.cnt[i] = k;
-    if (coinc) raise_error(st, -7 /*PM_E_COINCIDENT*/, (long long)B.gid[st->cur_id][i]);
+    if (dmin == 0.0f) raise_error(st, -7 /*PM_E_COINCIDENT*/, (long long)B.gid[st->cur_id][i]);
   }
   int kmax = k;
   long long ksum = k;
@@ -215,9 +225,9 @@ __global__ void __launch_bounds__(256) k_verlet_export(Bufs B, int n, int cap,
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int64_t *gid = B.gid[B.st->cur_id];
-  const int *nb = B.nbr + nbr_base4(i, cap) * 4;
+  const int *nb = B.nbr + nbr_row_base(i, cap);
   const int c = B.cnt[i];
-  for (int k = 0; k < c; ++k) col_gid[row_ptr[i] + k] = gid[nb[(k >> 2) * 128 + (k & 3)]];
+  for (int k = 0; k < c; ++k) col_gid[row_ptr[i] + k] = gid[nb[k << 5]];
 }
 
 }  // namespace

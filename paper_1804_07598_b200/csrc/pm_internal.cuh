@@ -160,11 +160,11 @@ PM_DEV float fast_rsqrt(float x) {
   return r;
 }
 
-// SELL-32 neighbour slot layout, int4-interleaved: row i = 32 * slice + lane;
-// entry k of the row lives at nbr[((slice * cap/4 + k/4) * 32 + lane) * 4 + k%4].
-PM_DEV int64_t nbr_base4(int i, int cap) {
-  const int slice = i >> 5, lane = i & 31;
-  return (int64_t)slice * (cap >> 2) * 32 + lane;  // in int4 units; + q*32 per group
+// SELL-32 neighbour slot layout: row i = 32 * slice + lane; entry k of the
+// row lives at nbr[(slice * cap + k) * 32 + lane] -- a warp reading entry k
+// of its 32 rows touches one contiguous 128-byte line.
+PM_DEV int64_t nbr_row_base(int i, int cap) {
+  return (int64_t)(i >> 5) * cap * 32 + (i & 31);
 }
 
 PM_DEV void raise_error(State *st, int code, long long gid) {
