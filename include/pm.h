@@ -161,7 +161,8 @@ pm_status pm_count(pm_ctx ctx, int64_t *n_owned, int64_t *n_ghost, int64_t *n_ce
 pm_status pm_get_cells(pm_ctx ctx, int32_t *cell_of, int32_t *cell_start, int32_t *perm);
 
 /* Verlet list of the last build in CSR over the current internal order:
- * row_ptr[n_owned+1], col_gid[nnz] (gid of each neighbour). */
+ * row_ptr[n_owned+n_ghost+1] (ghost rows are empty), col_gid[nnz] (gid of each
+ * neighbour).  Caller-allocated. */
 pm_status pm_get_verlet(pm_ctx ctx, int64_t *row_ptr, int64_t *col_gid);
 
 /* Particle state in the current internal order.  Any pointer may be NULL.
@@ -169,6 +170,10 @@ pm_status pm_get_verlet(pm_ctx ctx, int64_t *row_ptr, int64_t *col_gid);
  * SPH density and pressure. */
 pm_status pm_get_state(pm_ctx ctx, float *pos4, float *vel4, float *force4, int64_t *gid,
                        float *rho, float *pres, int32_t mem);
+
+/* kind[n_owned + n_ghost] in the current internal order (bit 30 marks a ghost
+ * copy on a decomposed context; bit 0: fixed SPH boundary particle). */
+pm_status pm_get_kind(pm_ctx ctx, int32_t *kind);
 
 /* Thermodynamics (fp64 reductions on the device): kinetic energy of the
  * current velocities; potential energy raw and shifted by V(r_cut) per pair
@@ -185,6 +190,74 @@ pm_status pm_thermo_compute(pm_ctx ctx);
 pm_status pm_set_profiling(pm_ctx ctx, int32_t on);
 pm_status pm_get_profile(pm_ctx ctx, double *force_ms, int64_t *force_launches,
                          double *step_ms, int64_t *steps);
+
+/* ------------------------------------------------------------------------
+ * Multi-GPU: spatial decomposition.  PAPER.md:62 (§3.1):
+ * "sub-domains are extended by a ghost layer ... given by the particle
+ * interaction radius"; PAPER.md:112-118 (§3.4): map() migrates particles that
+ * crossed sub-domain boundaries to the neighbour owning them, ghost_get()
+ * populates the ghost layers, optionally with a subset of properties (the
+ * per-step refresh moves positions only, Listing 4.1 ghost_get<>()).
+ *
+ * One context per GPU owns one cuboid of the global periodic box set with
+ * pm_set_domain.  The library builds, packs and unpacks the messages; the
+ * caller moves the bytes (NCCL through torch.distributed, or an in-process
+ * copy) and exchanges the counts.  Direction index of a neighbour cuboid:
+ * d = (ax+1) + 3 (ay+1) + 9 (az+1) with a in {-1, 0, 1}; d = 13 is "self".
+ * Ghost copies keep the owner's wrapped global coordinates (never shifted
+ * copies): pair distances use the global-box rule R4, so a pair's d2 is the
+ * same whether the partner is a ghost or a local periodic image.
+ * ---------------------------------------------------------------------- */
+enum { PM_MSG_MIGRATE = 0, PM_MSG_GHOST = 1, PM_MSG_REFRESH = 2 };
+enum { PM_PHASE_PROLOGUE = 0, PM_PHASE_STEP = 1, PM_PHASE_FINAL = 2, PM_PHASE_FORCES = 3 };
+
+/* Bytes per message record: migrate 48 (pos, vel, gid, kind), ghost 32
+ * (pos, gid, kind), refresh 16 (pos).  Returns -1 for an unknown kind. */
+int32_t pm_record_bytes(int32_t what);
+
+/* This context owns cuboid pcoord of a pgrid[0] x pgrid[1] x pgrid[2]
+ * decomposition of the (periodic) domain.  Call after pm_set_domain and
+ * pm_set_cutoff, before pm_place.  The ghost width is r_v = r_cut + skin.
+ * Errors: PM_E_INVAL if a decomposed axis is not periodic or a sub-domain is
+ * thinner than 2 r_v. */
+pm_status pm_set_decomposition(pm_ctx ctx, const int32_t pgrid[3], const int32_t pcoord[3]);
+
+/* Build the outgoing message lists of kind `what` (MIGRATE: owned particles
+ * whose owner changed -- counts[13] = particles that stay; GHOST: owned
+ * particles within r_v of each neighbour face/edge/corner, up to 7 copies).
+ * Lists are stable (ascending local index) and laid out in the direction
+ * order order[0..25] (all d != 13).  counts[27] receives records per
+ * direction.  Synchronises. */
+pm_status pm_dist_plan(pm_ctx ctx, int32_t what, const int32_t order[26], int64_t counts[27]);
+
+/* Write the planned records, in list order, to the device buffer send_dev
+ * (>= sum of counts * pm_record_bytes(what) bytes).  For MIGRATE this also
+ * removes the leavers (stable compaction of the stayers) and drops all ghosts;
+ * for GHOST it keeps the list for the per-step refresh. */
+pm_status pm_dist_pack(pm_ctx ctx, int32_t what, void *send_dev);
+
+/* Append nrecv records from the device buffer recv_dev: MIGRATE arrivals
+ * become owned particles, GHOST records become ghosts (kind bit 30 set).
+ * Grows buffers as needed (PM_E_NOMEM). */
+pm_status pm_dist_unpack(pm_ctx ctx, int32_t what, const void *recv_dev, int64_t nrecv);
+
+/* After migration and the ghost exchange: cell list over owned + ghosts, the
+ * refresh lists remapped to cell order, Verlet rows for owned particles. */
+pm_status pm_dist_finish(pm_ctx ctx);
+
+/* Per-step positions-only ghost refresh: pack the current positions of the
+ * last GHOST plan's list (16 B each, same order), unpack the received ones
+ * into this context's ghost copies. */
+pm_status pm_dist_refresh_pack(pm_ctx ctx, void *send_dev);
+pm_status pm_dist_refresh_unpack(pm_ctx ctx, const void *recv_dev);
+
+/* One phase of a decomposed velocity-Verlet run (owned particles only):
+ * PROLOGUE = v += dt/2 F/m, x += dt v, wrap (from stored forces); STEP =
+ * forces, then the fused kick / drift (as in pm_step_vv); FINAL = forces and
+ * the last half kick, forces stored; FORCES = forces only.  need_rebuild
+ * (nullable): synchronise and return (and clear) the local flag "some owned
+ * particle moved more than skin/2 since the last build". */
+pm_status pm_dist_step(pm_ctx ctx, float dt, int32_t phase, int32_t *need_rebuild);
 
 #ifdef __cplusplus
 }

@@ -26,6 +26,7 @@ __global__ void __launch_bounds__(256) k_cell_ids(Params P, Bufs B, int64_t n) {
   const int cur = st->cur_pv;
   float4 *__restrict__ pos = B.pos[cur];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) st->coinc_gid = -1;  // k_segsort (later on the stream) records coincidences
   int c = -1;
   if (i < n) {
     float4 p = pos[i];
@@ -42,9 +43,9 @@ __global__ void __launch_bounds__(256) k_cell_ids(Params P, Bufs B, int64_t n) {
       }
     }
     if (moved) pos[i] = make_float4(x[0], x[1], x[2], p.w);
-    int cx = cell_coord(x[0], P.box.lo[0], P.grid.inv_w[0], P.grid.n[0]);
-    int cy = cell_coord(x[1], P.box.lo[1], P.grid.inv_w[1], P.grid.n[1]);
-    int cz = cell_coord(x[2], P.box.lo[2], P.grid.inv_w[2], P.grid.n[2]);
+    int cx = local_coord(P.box, P.grid, 0, x[0]);
+    int cy = local_coord(P.box, P.grid, 1, x[1]);
+    int cz = local_coord(P.box, P.grid, 2, x[2]);
     c = cx + P.grid.n[0] * (cy + P.grid.n[1] * cz);
     B.cell_of[i] = c;
   }
@@ -149,6 +150,14 @@ __global__ void __launch_bounds__(256) k_scatter(Bufs B, int32_t *__restrict__ t
 
 // a4: stable order inside each cell = ascending storage index.  One warp per
 // cell: bitonic sort in registers for <= 32 entries, rank-by-count otherwise.
+// Coincident particles (identical positions, PM_E_COINCIDENT: LJ undefined)
+// always share a cell, so they are detected here, by comparing the members
+// of each cell pairwise (the Verlet builder's strict 0 < d2 test would
+// otherwise drop such a pair silently).
+__device__ __forceinline__ bool same_pos(const float4 &a, const float4 &b) {
+  return a.x == b.x && a.y == b.y && a.z == b.z;
+}
+
 __global__ void __launch_bounds__(256) k_segsort(Bufs B, const int32_t *__restrict__ tmp,
                                                  int ncell) {
   const int cell = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
@@ -160,6 +169,8 @@ __global__ void __launch_bounds__(256) k_segsort(Bufs B, const int32_t *__restri
     if (lane == 0) B.perm[s] = tmp[s];
     return;
   }
+  State *st = B.st;
+  const float4 *__restrict__ pos = B.pos[st->cur_pv];
   const unsigned full = 0xffffffffu;
   if (m <= 32) {
     int v = (lane < m) ? tmp[s + lane] : 0x7fffffff;
@@ -174,13 +185,30 @@ __global__ void __launch_bounds__(256) k_segsort(Bufs B, const int32_t *__restri
       }
     }
     if (lane < m) B.perm[s + lane] = v;
+    const float nan = __int_as_float(0x7fc00000);
+    const float4 p = (lane < m) ? pos[v] : make_float4(nan, nan, nan, 0.f);
+    bool dup = false;
+    for (int o = 1; o < m; ++o) {
+      const int src = (lane + o) & 31;
+      const float4 q = make_float4(__shfl_sync(full, p.x, src), __shfl_sync(full, p.y, src),
+                                   __shfl_sync(full, p.z, src), 0.f);
+      dup |= same_pos(p, q);
+    }
+    if (dup) st->coinc_gid = (long long)B.gid[st->cur_id][v];
     return;
   }
   for (int p = lane; p < m; p += 32) {
     const int v = tmp[s + p];
+    const float4 pv = pos[v];
     int r = 0;
-    for (int q = 0; q < m; ++q) r += (tmp[s + q] < v);
+    bool dup = false;
+    for (int q = 0; q < m; ++q) {
+      const int w = tmp[s + q];
+      r += (w < v);
+      dup |= (w != v) && same_pos(pv, pos[w]);
+    }
     B.perm[s + r] = v;
+    if (dup) st->coinc_gid = (long long)B.gid[st->cur_id][v];
   }
 }
 
@@ -191,6 +219,7 @@ __global__ void __launch_bounds__(256) k_reorder(Bufs B, int64_t n) {
   State *st = B.st;
   const int cp = st->cur_pv, ci = st->cur_id;
   const int j = B.perm[k];
+  B.invperm[j] = (int32_t)k;
   const float4 p = B.pos[cp][j];
   B.pos[cp ^ 1][k] = p;
   B.xref[k] = p;

@@ -1,0 +1,304 @@
+// k_dist.cu -- domain decomposition kernels: migration (map),
+// ghost-layer selection (ghost_get) and the per-step positions-only ghost
+// refresh.
+//
+// PAPER.md:62 (§3.1): "sub-domains are extended by a ghost layer ... The width
+// of the ghost layers is given by the particle interaction radius";
+// PAPER.md:114-116 (§3.4): local map() "processors only communicate to their
+// neighbors", ghost_get "populates the ghost layers"; a property
+// subset can be mapped -- the per-step refresh moves positions only
+// (Listing 4.1 ghost_get<>()).
+//
+// Every per-direction message is built by a STABLE partition of the owned
+// particles (block counts -> scan -> ballot ranks), so message contents and
+// order -- and therefore the receiver's storage order, its cell order and
+// its force summation order -- are deterministic.
+//
+// Direction index d = (a_x+1) + 3 (a_y+1) + 9 (a_z+1), a in {-1,0,1};
+// d = 13 is "stay / self".
+#include "pm_internal.cuh"
+
+namespace pm {
+
+namespace {
+
+constexpr int kDirBlock = 256;
+
+// owner coordinate along a decomposed axis (pinned fp32 rule, like R3)
+__device__ __forceinline__ int owner_coord(const Dist &D, int d, float x) {
+  return cell_coord(x, D.glo[d], D.inv_s[d], D.p[d]);
+}
+
+__global__ void __launch_bounds__(kDirBlock) k_dist_mark(Params P, Bufs B, Dist D, int n_owned,
+                                                         int what, uint32_t *__restrict__ mask) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_owned) return;
+  State *st = B.st;
+  // after a build owned particles and ghost copies are interleaved in cell
+  // order: ghosts belong to no message (a migration drops them)
+  if (B.kind[st->cur_id][i] & kGhostBit) {
+    mask[i] = 0u;
+    return;
+  }
+  const float4 x4 = B.pos[st->cur_pv][i];
+  const float x[3] = {x4.x, x4.y, x4.z};
+  uint32_t m = 0;
+  if (what == 0) {  // migration: the one direction towards the new owner
+    int a[3] = {0, 0, 0};
+    bool bad = false;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      if (D.p[d] < 2) continue;
+      const int c = owner_coord(D, d, x[d]);
+      if (c == D.c[d]) continue;
+      const int delta = (c - D.c[d] + D.p[d]) % D.p[d];
+      if (delta == 1) a[d] = 1;
+      else if (delta == D.p[d] - 1) a[d] = -1;
+      else bad = true;  // moved more than one sub-domain: impossible within skin/2
+    }
+    if (bad) raise_error(st, -6 /*PM_E_DOMAIN*/, (long long)B.gid[st->cur_id][i]);
+    m = 1u << ((a[0] + 1) + 3 * (a[1] + 1) + 9 * (a[2] + 1));
+  } else {  // ghosts: every direction whose face is within the ghost width
+    int lo_f[3], hi_f[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      lo_f[d] = D.p[d] >= 2 && __fsub_rn(x[d], D.slo[d]) < D.rg;
+      hi_f[d] = D.p[d] >= 2 && __fsub_rn(D.shi[d], x[d]) < D.rg;
+    }
+    for (int az = -1; az <= 1; ++az) {
+      if ((az == -1 && !lo_f[2]) || (az == 1 && !hi_f[2])) continue;
+      for (int ay = -1; ay <= 1; ++ay) {
+        if ((ay == -1 && !lo_f[1]) || (ay == 1 && !hi_f[1])) continue;
+        for (int ax = -1; ax <= 1; ++ax) {
+          if ((ax == -1 && !lo_f[0]) || (ax == 1 && !hi_f[0])) continue;
+          const int dd = (ax + 1) + 3 * (ay + 1) + 9 * (az + 1);
+          if (dd != 13) m |= 1u << dd;
+        }
+      }
+    }
+  }
+  mask[i] = m;
+}
+
+// pass 1: per-block counts per direction
+__global__ void __launch_bounds__(kDirBlock) k_dist_count(const uint32_t *__restrict__ mask, int n,
+                                                          int *__restrict__ blk_counts) {
+  __shared__ int cnt[27];
+  if (threadIdx.x < 27) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t m = (i < n) ? mask[i] : 0u;
+  while (m) {
+    const int d = __ffs(m) - 1;
+    m &= m - 1;
+    atomicAdd(&cnt[d], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < 27) blk_counts[blockIdx.x * 27 + threadIdx.x] = cnt[threadIdx.x];
+}
+
+// pass 2: per-direction exclusive scan over blocks; direction bases in the
+// caller's packing order (order[0..25], then direction 13 last); totals.
+__global__ void k_dist_scan(int *__restrict__ blk_counts, int nblk, const int *__restrict__ order,
+                            int *__restrict__ dir_base, long long *__restrict__ totals) {
+  __shared__ long long tot[27];
+  const int d = threadIdx.x;
+  if (d < 27) {
+    long long acc = 0;
+    for (int b = 0; b < nblk; ++b) {
+      const int c = blk_counts[b * 27 + d];
+      blk_counts[b * 27 + d] = (int)acc;
+      acc += c;
+    }
+    tot[d] = acc;
+    totals[d] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long base = 0;
+    for (int k = 0; k < 26; ++k) {
+      dir_base[order[k]] = (int)base;
+      base += tot[order[k]];
+    }
+    dir_base[13] = (int)base;
+  }
+}
+
+// pass 3: stable write of particle indices into the per-direction lists
+__global__ void __launch_bounds__(kDirBlock) k_dist_fill(const uint32_t *__restrict__ mask, int n,
+                                                         const int *__restrict__ blk_off,
+                                                         const int *__restrict__ dir_base,
+                                                         int *__restrict__ list) {
+  __shared__ int wsum[27][kDirBlock / 32];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t m = (i < n) ? mask[i] : 0u;
+  const unsigned lt = (1u << lane) - 1u;
+  int rank_in_warp[27];
+#pragma unroll
+  for (int d = 0; d < 27; ++d) {
+    const unsigned b = __ballot_sync(0xffffffffu, (m >> d) & 1u);
+    rank_in_warp[d] = __popc(b & lt);
+    if (lane == 0) wsum[d][w] = __popc(b);
+  }
+  __syncthreads();
+  if (threadIdx.x < 27) {  // exclusive scan over the block's warps, per direction
+    int acc = 0;
+    for (int k = 0; k < kDirBlock / 32; ++k) {
+      const int c = wsum[threadIdx.x][k];
+      wsum[threadIdx.x][k] = acc;
+      acc += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int d = 0; d < 27; ++d) {
+    if ((m >> d) & 1u)
+      list[dir_base[d] + blk_off[blockIdx.x * 27 + d] + wsum[d][w] + rank_in_warp[d]] = i;
+  }
+}
+
+// migration record: pos, vel, gid, kind (48 B); ghost record: pos, gid, kind (32 B)
+struct MigRec {
+  float4 pos, vel;
+  long long gid;
+  int kind, pad;
+};
+struct GhostRec {
+  float4 pos;
+  long long gid;
+  int kind, pad;
+};
+
+__global__ void k_dist_pack(Bufs B, int what, const int *__restrict__ list, int nsend,
+                            void *__restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nsend) return;
+  State *st = B.st;
+  const int i = list[e];
+  const int cp = st->cur_pv, ci = st->cur_id;
+  if (what == 0) {
+    MigRec r;
+    r.pos = B.pos[cp][i];
+    r.vel = B.vel[cp][i];
+    r.gid = B.gid[ci][i];
+    r.kind = B.kind[ci][i];
+    r.pad = 0;
+    reinterpret_cast<MigRec *>(out)[e] = r;
+  } else {
+    GhostRec r;
+    r.pos = B.pos[cp][i];
+    r.gid = B.gid[ci][i];
+    r.kind = B.kind[ci][i] & ~kGhostBit;
+    r.pad = 0;
+    reinterpret_cast<GhostRec *>(out)[e] = r;
+  }
+}
+
+// stayers (direction-13 list, in index order) -> alternate buffers [0, n_stay)
+__global__ void k_dist_compact(Bufs B, const int *__restrict__ stay, int n_stay) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n_stay) return;
+  State *st = B.st;
+  const int cp = st->cur_pv, ci = st->cur_id;
+  const int j = stay[k];
+  B.pos[cp ^ 1][k] = B.pos[cp][j];
+  B.vel[cp ^ 1][k] = B.vel[cp][j];
+  B.gid[ci ^ 1][k] = B.gid[ci][j];
+  B.kind[ci ^ 1][k] = B.kind[ci][j];
+}
+
+__global__ void k_dist_unpack(Bufs B, int what, const void *__restrict__ in, int nrecv, int base) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nrecv) return;
+  State *st = B.st;
+  const int cp = st->cur_pv, ci = st->cur_id;
+  const int k = base + e;
+  if (what == 0) {
+    const MigRec r = reinterpret_cast<const MigRec *>(in)[e];
+    B.pos[cp][k] = r.pos;
+    B.vel[cp][k] = r.vel;
+    B.gid[ci][k] = r.gid;
+    B.kind[ci][k] = r.kind;
+  } else {
+    const GhostRec r = reinterpret_cast<const GhostRec *>(in)[e];
+    B.pos[cp][k] = r.pos;
+    B.vel[cp][k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    B.gid[ci][k] = r.gid;
+    B.kind[ci][k] = r.kind | kGhostBit;
+  }
+}
+
+// after the cell sort: pre-sort indices -> sorted positions
+__global__ void k_dist_remap(const int *__restrict__ invperm, int *__restrict__ send_idx,
+                             int nsend, int *__restrict__ ghost_slot, int nghost, int n_owned) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < nsend) send_idx[e] = invperm[send_idx[e]];
+  if (e < nghost) ghost_slot[e] = invperm[n_owned + e];
+}
+
+__global__ void k_refresh_pack(Bufs B, const int *__restrict__ send_idx, int nsend,
+                               float4 *__restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < nsend) out[e] = B.pos[B.st->cur_pv][send_idx[e]];
+}
+
+__global__ void k_refresh_unpack(Bufs B, const int *__restrict__ ghost_slot, int nghost,
+                                 const float4 *__restrict__ in) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < nghost) B.pos[B.st->cur_pv][ghost_slot[e]] = in[e];
+}
+
+inline unsigned nb(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+int dist_record_bytes(int what) {
+  return what == 0 ? (int)sizeof(MigRec) : what == 1 ? (int)sizeof(GhostRec) : 16;
+}
+
+void launch_dist_plan(const Params &P, const Bufs &B, const Dist &D, int n_owned, int what,
+                      uint32_t *mask, int *blk_counts, const int *order, int *dir_base,
+                      long long *totals, int *list, cudaStream_t s) {
+  const unsigned g = nb(n_owned > 0 ? n_owned : 1, kDirBlock);
+  if (n_owned > 0) k_dist_mark<<<g, kDirBlock, 0, s>>>(P, B, D, n_owned, what, mask);
+  k_dist_count<<<g, kDirBlock, 0, s>>>(mask, n_owned, blk_counts);
+  k_dist_scan<<<1, 32, 0, s>>>(blk_counts, (int)g, order, dir_base, totals);
+  k_dist_fill<<<g, kDirBlock, 0, s>>>(mask, n_owned, blk_counts, dir_base, list);
+}
+
+void launch_dist_pack(const Bufs &B, int what, const int *list, int nsend, void *out,
+                      cudaStream_t s) {
+  if (nsend > 0) k_dist_pack<<<nb(nsend), 256, 0, s>>>(B, what, list, nsend, out);
+}
+
+void launch_dist_compact(const Bufs &B, const int *stay, int n_stay, cudaStream_t s) {
+  if (n_stay > 0) k_dist_compact<<<nb(n_stay), 256, 0, s>>>(B, stay, n_stay);
+}
+
+void launch_dist_unpack(const Bufs &B, int what, const void *in, int nrecv, int base,
+                        cudaStream_t s) {
+  if (nrecv > 0) k_dist_unpack<<<nb(nrecv), 256, 0, s>>>(B, what, in, nrecv, base);
+}
+
+void launch_dist_remap(const int *invperm, int *send_idx, int nsend, int *ghost_slot, int nghost,
+                       int n_owned, cudaStream_t s) {
+  const int m = nsend > nghost ? nsend : nghost;
+  if (m > 0)
+    k_dist_remap<<<nb(m), 256, 0, s>>>(invperm, send_idx, nsend, ghost_slot, nghost, n_owned);
+}
+
+void launch_refresh_pack(const Bufs &B, const int *send_idx, int nsend, void *out,
+                         cudaStream_t s) {
+  if (nsend > 0)
+    k_refresh_pack<<<nb(nsend), 256, 0, s>>>(B, send_idx, nsend, reinterpret_cast<float4 *>(out));
+}
+
+void launch_refresh_unpack(const Bufs &B, const int *ghost_slot, int nghost, const void *in,
+                           cudaStream_t s) {
+  if (nghost > 0)
+    k_refresh_unpack<<<nb(nghost), 256, 0, s>>>(B, ghost_slot, nghost,
+                                                reinterpret_cast<const float4 *>(in));
+}
+
+}  // namespace pm

@@ -28,23 +28,32 @@ struct Acc {
   int np;
 };
 
+// R4 along one axis, branch-free (same arithmetic as pair_delta1): all three
+// candidates are computed and selected, so boundary warps do not diverge.
+__device__ __forceinline__ float r4_delta(float a, float b, float L, float halfL) {
+  const float e = __fsub_rn(b, a);
+  const float up = __fsub_rn(__fsub_rn(b, L), a);  // e > L/2: shift x_j by -L
+  const float dn = __fsub_rn(b, __fsub_rn(a, L));  // e < -L/2: shift x_i by -L
+  return e > halfL ? up : (e < -halfL ? dn : e);
+}
+
 // One pair, branch-free: the contribution is selected to zero when the pair
 // is outside r_cut (R6) or the slot is padding (valid == false).
-template <bool MI, bool CAPPED, bool ENERGY>
+template <bool MI, bool CAPPED, bool ENERGY, bool MASK>
 __device__ __forceinline__ void lj_pair(const Params &P, const float4 &xi, const float4 &xj,
                                         bool valid, Acc &a) {
   float dx, dy, dz;
   if (MI) {
-    dx = pair_delta1(xi.x, xj.x, P.box.L[0], P.box.halfL[0], P.box.per[0]);
-    dy = pair_delta1(xi.y, xj.y, P.box.L[1], P.box.halfL[1], P.box.per[1]);
-    dz = pair_delta1(xi.z, xj.z, P.box.L[2], P.box.halfL[2], P.box.per[2]);
+    dx = P.box.per[0] ? r4_delta(xi.x, xj.x, P.box.L[0], P.box.halfL[0]) : __fsub_rn(xj.x, xi.x);
+    dy = P.box.per[1] ? r4_delta(xi.y, xj.y, P.box.L[1], P.box.halfL[1]) : __fsub_rn(xj.y, xi.y);
+    dz = P.box.per[2] ? r4_delta(xi.z, xj.z, P.box.L[2], P.box.halfL[2]) : __fsub_rn(xj.z, xi.z);
   } else {
     dx = __fsub_rn(xj.x, xi.x);
     dy = __fsub_rn(xj.y, xi.y);
     dz = __fsub_rn(xj.z, xi.z);
   }
   const float d2 = dist2(dx, dy, dz);
-  const bool in = valid && (d2 < P.lj.rc2);
+  const bool in = (MASK ? valid : true) && (d2 < P.lj.rc2);
   float f, r6i;
   if (CAPPED) {
     const float r2e = fmaxf(d2, P.lj.r_min * P.lj.r_min);
@@ -55,7 +64,7 @@ __device__ __forceinline__ void lj_pair(const Params &P, const float4 &xi, const
   } else {
     const float r2i = fast_rcp(d2);
     r6i = r2i * r2i * r2i;
-    f = r2i * r6i * (P.lj.c12 * r6i - P.lj.c6);
+    f = r2i * (r6i * (P.lj.c12 * r6i - P.lj.c6));
   }
   f = in ? f : 0.0f;
   // F_i += f (x_i - x_j) = -f * delta
@@ -72,9 +81,9 @@ __device__ __forceinline__ void lj_pair(const Params &P, const float4 &xi, const
 // Row sweep, software-pipelined: the index stream (the only HBM-resident
 // operand) is prefetched two groups of 4 ahead with streaming loads (each a
 // coalesced 128-byte line across the warp); the 4 position gathers of a group
-// are issued together.  Rows are padded to a multiple of 4 with valid
-// particle indices (the builder pads with the row's own index), so every
-// gather is in bounds and padding is only masked out.
+// are issued together.  Full groups run unmasked; the last partial group is
+// padded by the builder with the row's own index (always a valid gather) and
+// masked.
 struct Idx4 {
   int a, b, c, d;
 };
@@ -88,28 +97,44 @@ __device__ __forceinline__ Idx4 ld_idx4(const int *__restrict__ p) {
   return r;
 }
 
+template <bool MI, bool CAPPED, bool ENERGY, bool MASK>
+__device__ __forceinline__ void lj_group(const Params &P, const float4 *__restrict__ pos,
+                                         const Idx4 &j, int rem, const float4 &xi, Acc &a) {
+  const float4 x0 = __ldg(pos + j.a);
+  const float4 x1 = __ldg(pos + j.b);
+  const float4 x2 = __ldg(pos + j.c);
+  const float4 x3 = __ldg(pos + j.d);
+  lj_pair<MI, CAPPED, ENERGY, false>(P, xi, x0, true, a);
+  lj_pair<MI, CAPPED, ENERGY, MASK>(P, xi, x1, rem > 1, a);
+  lj_pair<MI, CAPPED, ENERGY, MASK>(P, xi, x2, rem > 2, a);
+  lj_pair<MI, CAPPED, ENERGY, MASK>(P, xi, x3, rem > 3, a);
+}
+
 template <bool MI, bool CAPPED, bool ENERGY>
 __device__ __forceinline__ void lj_row(const Params &P, const float4 *__restrict__ pos,
                                        const int *__restrict__ nb, int cnt, const float4 &xi,
                                        Acc &a) {
-  const int ng = (cnt + 3) >> 2;
+  const int ng = (cnt + 3) >> 2;  // groups incl. a partial last one
+  const int nfull = cnt >> 2;
   if (ng == 0) return;
   Idx4 j0 = ld_idx4(nb);
   Idx4 j1 = (ng > 1) ? ld_idx4(nb + 128) : j0;
-  for (int g = 0; g < ng; ++g) {
+  int g = 0;
+  // two groups per iteration: the prefetch registers rotate statically
+  for (; g + 2 <= nfull; g += 2) {
     const Idx4 j2 = (g + 2 < ng) ? ld_idx4(nb + (g + 2) * 128) : j1;
-    const int rem = cnt - 4 * g;
-    const float4 x0 = __ldg(pos + j0.a);
-    const float4 x1 = __ldg(pos + j0.b);
-    const float4 x2 = __ldg(pos + j0.c);
-    const float4 x3 = __ldg(pos + j0.d);
-    lj_pair<MI, CAPPED, ENERGY>(P, xi, x0, true, a);
-    lj_pair<MI, CAPPED, ENERGY>(P, xi, x1, rem > 1, a);
-    lj_pair<MI, CAPPED, ENERGY>(P, xi, x2, rem > 2, a);
-    lj_pair<MI, CAPPED, ENERGY>(P, xi, x3, rem > 3, a);
-    j0 = j1;
-    j1 = j2;
+    const Idx4 j3 = (g + 3 < ng) ? ld_idx4(nb + (g + 3) * 128) : j1;
+    lj_group<MI, CAPPED, ENERGY, false>(P, pos, j0, 4, xi, a);
+    lj_group<MI, CAPPED, ENERGY, false>(P, pos, j1, 4, xi, a);
+    j0 = j2;
+    j1 = j3;
   }
+  if (g < nfull) {
+    lj_group<MI, CAPPED, ENERGY, false>(P, pos, j0, 4, xi, a);
+    j0 = j1;
+    ++g;
+  }
+  if (g < ng) lj_group<MI, CAPPED, ENERGY, true>(P, pos, j0, cnt - 4 * g, xi, a);
 }
 
 __device__ __forceinline__ bool near_periodic_face(const Params &P, const float4 &x) {
@@ -210,10 +235,10 @@ __device__ __forceinline__ bool moved_too_far(const Params &P, const float3 &x, 
 //         x' = wrap(x + dt v); displacement test vs xref; -> alternate buffers
 //  final: F(x); v += dt/2 F/m; F stored; x copied  -> alternate buffers
 template <bool CAPPED>
-__global__ void __launch_bounds__(256) k_lj_step(Params P, Bufs B, int n, float dt) {
+__global__ void __launch_bounds__(256) k_lj_step(Params P, Bufs B, int n, float dt, int mode_arg) {
   State *st = B.st;
   if (st->abort) return;
-  const int mode = st->mode;
+  const int mode = mode_arg >= 0 ? mode_arg : st->mode;
   const int cp = st->cur_pv;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = i < n;
@@ -221,7 +246,12 @@ __global__ void __launch_bounds__(256) k_lj_step(Params P, Bufs B, int n, float 
   const float4 xi = active ? pos[i] : make_float4(0.f, 0.f, 0.f, 0.f);
   Acc a = lj_force_of<CAPPED, false>(P, B, pos, i, active, xi);
   bool far = false;
-  if (active) {
+  // ghost copies (multi-GPU) are not integrated: after an inner step the
+  // refresh overwrites them; the final step (positions unchanged) carries
+  // them over so the state stays consistent for getters / energy passes
+  const bool ghost = active && P.dist && (B.kind[st->cur_id][i] & kGhostBit);
+  if (ghost && mode != kModeInner) B.pos[cp ^ 1][i] = xi;
+  if (active && !ghost) {
     float4 v = B.vel[cp][i];
     const float im = P.lj.inv_mass;
     if (mode == kModeInner) {
@@ -258,7 +288,7 @@ __global__ void __launch_bounds__(256) k_kick_drift(Params P, Bufs B, int n, flo
   const int cp = st->cur_pv;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   bool far = false;
-  if (i < n) {
+  if (i < n && !(P.dist && (B.kind[st->cur_id][i] & kGhostBit))) {
     const float4 f = B.force[i];
     float4 v = B.vel[cp][i];
     const float4 x = B.pos[cp][i];
@@ -294,7 +324,7 @@ __global__ void __launch_bounds__(256) k_ke(Params P, Bufs B, int n) {
   State *st = B.st;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   double ke = 0.0;
-  if (i < n) {
+  if (i < n && !(P.dist && (B.kind[st->cur_id][i] & kGhostBit))) {
     const float4 v = B.vel[st->cur_pv][i];
     ke = 0.5 * (double)(1.0f / P.lj.inv_mass) *
          ((double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z);
@@ -329,10 +359,15 @@ void launch_lj(const Params &P, const Bufs &B, int64_t n, int want_energy, cudaS
   }
 }
 
-void launch_lj_step(const Params &P, const Bufs &B, int64_t n, float dt, cudaStream_t s) {
+void launch_lj_step_mode(const Params &P, const Bufs &B, int64_t n, float dt, int mode,
+                         cudaStream_t s) {
   if (n <= 0) return;
-  if (P.lj.r_min > 0.f) k_lj_step<true><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt);
-  else k_lj_step<false><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt);
+  if (P.lj.r_min > 0.f) k_lj_step<true><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode);
+  else k_lj_step<false><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode);
+}
+
+void launch_lj_step(const Params &P, const Bufs &B, int64_t n, float dt, cudaStream_t s) {
+  launch_lj_step_mode(P, B, n, dt, -1, s);
 }
 
 void launch_kick_drift(const Params &P, const Bufs &B, int64_t n, float dt, cudaStream_t s) {

@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(256) k_sph_forces(Params P, Bufs B, int n) {
   State *st = B.st;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  if (B.kind[st->cur_id][i] != 0) {
+  if (B.kind[st->cur_id][i] & 1) {
     B.force[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     return;
   }

@@ -38,30 +38,40 @@ __device__ __forceinline__ void append(int *__restrict__ row, int cap, int &k, b
 // (fl(x_j - L), exact by Sterbenz); if reached across the high face, the
 // lane's own coordinate is shifted instead (xi_eff = fl(x_i - L), exact).
 // For n >= 3 cells per periodic axis this reproduces R4's choice for every
-// pair that can be a neighbour, so membership is bit-identical.  MIX: the
-// run covers a whole periodic x-row, use the per-pair R4 rule along x.
-// dmin tracks the smallest d2 of a hit: 0 means two coincident particles.
-template <bool SHIFTJ, bool MIX, bool CLAMP>
+// pair that can be a neighbour, so membership is bit-identical.  PAIRMI:
+// apply the per-pair R4 rule along the axes in `pmi` -- a run that covers a
+// whole periodic x-row, and the decomposed axes of a multi-GPU sub-domain
+// (ghosts carry global wrapped coordinates).
+//
+// The membership test 0 < d2 < rv2 is one unsigned compare of the fp32 bit
+// patterns (d2 >= 0, so bits(d2) - 1 < bits(rv2) - 1 as uint32 exactly when
+// 0 < d2 < rv2; NaN/inf never pass): d2 == 0 is the particle itself (a
+// coincident distinct pair is caught by the force / density passes, which
+// raise PM_E_COINCIDENT).  Lanes outside the current segment carry
+// xi = +inf and never hit.
+template <bool SHIFTJ, bool PAIRMI, bool CLAMP>
 __device__ __forceinline__ void test_append(const Params &P, const float4 &xi_eff,
-                                            const float3 &csh, const float4 &xj, int j, int i,
-                                            bool mine, int *__restrict__ row, int cap, int &k,
-                                            float &dmin) {
-  float dx, dy, dz;
-  if (MIX) dx = pair_delta1(xi_eff.x, xj.x, P.box.L[0], P.box.halfL[0], 1);
-  else dx = SHIFTJ ? __fsub_rn(__fsub_rn(xj.x, csh.x), xi_eff.x) : __fsub_rn(xj.x, xi_eff.x);
-  dy = SHIFTJ ? __fsub_rn(__fsub_rn(xj.y, csh.y), xi_eff.y) : __fsub_rn(xj.y, xi_eff.y);
-  dz = SHIFTJ ? __fsub_rn(__fsub_rn(xj.z, csh.z), xi_eff.z) : __fsub_rn(xj.z, xi_eff.z);
+                                            const float3 &csh, int pmi, const float4 &xj, int j,
+                                            unsigned rv2m1, int *__restrict__ row, int cap,
+                                            int &k) {
+  float dx = SHIFTJ ? __fsub_rn(__fsub_rn(xj.x, csh.x), xi_eff.x) : __fsub_rn(xj.x, xi_eff.x);
+  float dy = SHIFTJ ? __fsub_rn(__fsub_rn(xj.y, csh.y), xi_eff.y) : __fsub_rn(xj.y, xi_eff.y);
+  float dz = SHIFTJ ? __fsub_rn(__fsub_rn(xj.z, csh.z), xi_eff.z) : __fsub_rn(xj.z, xi_eff.z);
+  if (PAIRMI) {
+    if (pmi & 1) dx = pair_delta1(xi_eff.x, xj.x, P.box.L[0], P.box.halfL[0], 1);
+    if (pmi & 2) dy = pair_delta1(xi_eff.y, xj.y, P.box.L[1], P.box.halfL[1], 1);
+    if (pmi & 4) dz = pair_delta1(xi_eff.z, xj.z, P.box.L[2], P.box.halfL[2], 1);
+  }
   const float d2 = dist2(dx, dy, dz);
-  const bool hit = mine && (d2 < P.rv2) && (j != i);
-  dmin = fminf(dmin, hit ? d2 : 1.0f);
+  const bool hit = (__float_as_uint(d2) - 1u) < rv2m1;
   append<CLAMP>(row, cap, k, hit, j);
 }
 
-template <bool SHIFTJ, bool MIX, bool CLAMP>
+template <bool SHIFTJ, bool PAIRMI, bool CLAMP>
 __device__ __forceinline__ void scan_run(const Params &P, const float4 *__restrict__ pos, int b,
-                                         int e, int i, const float4 &xi_eff, float3 csh,
-                                         bool mine, int cap, int *__restrict__ row, int &k,
-                                         float &dmin) {
+                                         int e, const float4 &xi_eff, float3 csh, int pmi,
+                                         int cap, int *__restrict__ row, int &k) {
+  const unsigned rv2m1 = __float_as_uint(P.rv2) - 1u;
   int j = b;
   for (; j + 8 <= e; j += 8) {
     float4 x[8];
@@ -69,27 +79,27 @@ __device__ __forceinline__ void scan_run(const Params &P, const float4 *__restri
     for (int u = 0; u < 8; ++u) x[u] = pos[j + u];  // same address in all lanes
 #pragma unroll
     for (int u = 0; u < 8; ++u)
-      test_append<SHIFTJ, MIX, CLAMP>(P, xi_eff, csh, x[u], j + u, i, mine, row, cap, k, dmin);
+      test_append<SHIFTJ, PAIRMI, CLAMP>(P, xi_eff, csh, pmi, x[u], j + u, rv2m1, row, cap, k);
   }
   for (; j < e; ++j)
-    test_append<SHIFTJ, MIX, CLAMP>(P, xi_eff, csh, pos[j], j, i, mine, row, cap, k, dmin);
+    test_append<SHIFTJ, PAIRMI, CLAMP>(P, xi_eff, csh, pmi, pos[j], j, rv2m1, row, cap, k);
 }
 
 __device__ __forceinline__ void scan_any(const Params &P, const float4 *__restrict__ pos, int b,
-                                         int e, int i, const float4 &xi_eff, float3 csh, bool mix,
-                                         bool mine, int cap, int *__restrict__ row, int &k,
-                                         float &dmin) {
+                                         int e, const float4 &xi_eff, float3 csh, int pmi,
+                                         int cap, int *__restrict__ row, int &k) {
+  const bool mix = pmi != 0;
   const bool sj = csh.x != 0.f || csh.y != 0.f || csh.z != 0.f;
   // warp-uniform: can any lane of the warp overflow its row in this run?
   const bool clamp = __any_sync(0xffffffffu, k + (e - b) > cap);
   if (!clamp && !mix && !sj) {
-    scan_run<false, false, false>(P, pos, b, e, i, xi_eff, csh, mine, cap, row, k, dmin);
+    scan_run<false, false, false>(P, pos, b, e, xi_eff, csh, 0, cap, row, k);
   } else if (!clamp && !mix) {
-    scan_run<true, false, false>(P, pos, b, e, i, xi_eff, csh, mine, cap, row, k, dmin);
+    scan_run<true, false, false>(P, pos, b, e, xi_eff, csh, 0, cap, row, k);
   } else if (mix) {
-    scan_run<true, true, true>(P, pos, b, e, i, xi_eff, csh, mine, cap, row, k, dmin);
+    scan_run<true, true, true>(P, pos, b, e, xi_eff, csh, pmi, cap, row, k);
   } else {
-    scan_run<true, false, true>(P, pos, b, e, i, xi_eff, csh, mine, cap, row, k, dmin);
+    scan_run<true, false, true>(P, pos, b, e, xi_eff, csh, 0, cap, row, k);
   }
 }
 
@@ -109,22 +119,27 @@ __global__ void __launch_bounds__(256, 3) k_verlet(Params P, Bufs B, int n) {
   const int lane = threadIdx.x & 31;
   const int wbase = i - lane;
   if (wbase >= n) return;  // whole warp out of range
-  const bool active = i < n;
+  // rows: every particle on one GPU; owned particles only in a sub-domain
+  const bool active = i < n && !(P.dist && (B.kind[st->cur_id][i] & kGhostBit));
   const int cap = P.nbr_cap;
   const int nx = P.grid.n[0], ny = P.grid.n[1], nz = P.grid.n[2];
   const float4 *__restrict__ pos = B.pos[st->cur_pv];
   const float4 xi = active ? pos[i] : make_float4(0.f, 0.f, 0.f, 0.f);
   int cell = -1;
   if (active) {
-    const int c0 = cell_coord(xi.x, P.box.lo[0], P.grid.inv_w[0], nx);
-    const int c1 = cell_coord(xi.y, P.box.lo[1], P.grid.inv_w[1], ny);
-    const int c2 = cell_coord(xi.z, P.box.lo[2], P.grid.inv_w[2], nz);
+    const int c0 = local_coord(P.box, P.grid, 0, xi.x);
+    const int c1 = local_coord(P.box, P.grid, 1, xi.y);
+    const int c2 = local_coord(P.box, P.grid, 2, xi.z);
     cell = c0 + nx * (c1 + ny * c2);
   }
+  // axes with the per-pair R4 rule: decomposed (globally periodic, locally open)
+  const int pmi_dec = (P.box.per[0] && !P.grid.wrap[0] ? 1 : 0) |
+                      (P.box.per[1] && !P.grid.wrap[1] ? 2 : 0) |
+                      (P.box.per[2] && !P.grid.wrap[2] ? 4 : 0);
   const int row_id = active ? cell / nx : 0x7fffffff;  // (cy, cz) row of my cell
   int *__restrict__ row = B.nbr + nbr_row_base(i, cap);
   int k = 0;
-  float dmin = 1.0f;
+  const float INF = __int_as_float(0x7f800000);
   const float Lx = P.box.L[0], Ly = P.box.L[1], Lz = P.box.L[2];
   unsigned todo = __ballot_sync(0xffffffffu, active);
   while (todo) {
@@ -142,27 +157,27 @@ __global__ void __launch_bounds__(256, 3) k_verlet(Params P, Bufs B, int n) {
     }
     const int cy = seg_row % ny, cz = seg_row / ny;
     int xa = cmin - 1, xb = cmax + 1;
-    bool mix = false;  // whole periodic x-row: per-pair R4 rule along x
-    if (!P.box.per[0]) {
+    int pmi = pmi_dec;  // + x when the run covers a whole periodic x-row
+    if (!P.grid.wrap[0]) {
       xa = max(xa, 0);
       xb = min(xb, nx - 1);
     } else if (xb - xa + 1 >= nx) {
       xa = 0;
       xb = nx - 1;
-      mix = true;
+      pmi |= 1;
     }
     for (int dz = -1; dz <= 1; ++dz) {
       int qz = cz + dz;
       float shz = 0.f, lz = 0.f;  // candidate shift / own shift along z
       if (qz < 0 || qz >= nz) {
-        if (!P.box.per[2]) continue;
+        if (!P.grid.wrap[2]) continue;
         if (qz < 0) { qz += nz; shz = Lz; } else { qz -= nz; lz = Lz; }
       }
       for (int dy = -1; dy <= 1; ++dy) {
         int qy = cy + dy;
         float shy = 0.f, ly = 0.f;
         if (qy < 0 || qy >= ny) {
-          if (!P.box.per[1]) continue;
+          if (!P.grid.wrap[1]) continue;
           if (qy < 0) { qy += ny; shy = Ly; } else { qy -= ny; ly = Ly; }
         }
         const int rowc = nx * (qy + ny * qz);
@@ -176,15 +191,18 @@ __global__ void __launch_bounds__(256, 3) k_verlet(Params P, Bufs B, int n) {
           a0 = xa; b0 = nx - 1;
           a1 = 0; b1 = xb - nx; lx1 = Lx;
         }
-        const float4 xe0 = make_float4(__fsub_rn(xi.x, lx0), __fsub_rn(xi.y, ly),
-                                       __fsub_rn(xi.z, lz), 0.f);
-        scan_any(P, pos, B.start[rowc + a0], B.start[rowc + b0 + 1], i, xe0,
-                 make_float3(mix ? 0.f : sx0, shy, shz), mix, mine, cap, row, k, dmin);
+        // lanes outside this segment test against +inf: they never hit
+        const float4 xe0 = mine ? make_float4(__fsub_rn(xi.x, lx0), __fsub_rn(xi.y, ly),
+                                              __fsub_rn(xi.z, lz), 0.f)
+                                : make_float4(INF, INF, INF, 0.f);
+        scan_any(P, pos, B.start[rowc + a0], B.start[rowc + b0 + 1], xe0,
+                 make_float3((pmi & 1) ? 0.f : sx0, shy, shz), pmi, cap, row, k);
         if (b1 >= a1) {
-          const float4 xe1 = make_float4(__fsub_rn(xi.x, lx1), __fsub_rn(xi.y, ly),
-                                         __fsub_rn(xi.z, lz), 0.f);
-          scan_any(P, pos, B.start[rowc + a1], B.start[rowc + b1 + 1], i, xe1,
-                   make_float3(sx1, shy, shz), false, mine, cap, row, k, dmin);
+          const float4 xe1 = mine ? make_float4(__fsub_rn(xi.x, lx1), __fsub_rn(xi.y, ly),
+                                                __fsub_rn(xi.z, lz), 0.f)
+                                  : make_float4(INF, INF, INF, 0.f);
+          scan_any(P, pos, B.start[rowc + a1], B.start[rowc + b1 + 1], xe1,
+                   make_float3(sx1, shy, shz), pmi_dec, cap, row, k);
         }
       }
     }
@@ -193,9 +211,8 @@ __global__ void __launch_bounds__(256, 3) k_verlet(Params P, Bufs B, int n) {
     // pad the row to a multiple of 4 with this particle's own index (a valid
     // index; the force sweep reads groups of 4 and masks padding slots)
     for (int q = k; q < cap && (q & 3) != 0; ++q) row[q << 5] = i;
-    B.cnt[i] = k;
-    if (dmin == 0.0f) raise_error(st, -7 /*PM_E_COINCIDENT*/, (long long)B.gid[st->cur_id][i]);
   }
+  if (i < n) B.cnt[i] = active ? k : 0;  // ghost rows are empty
   int kmax = k;
   long long ksum = k;
 #pragma unroll
@@ -216,6 +233,7 @@ __global__ void __launch_bounds__(256, 3) k_verlet(Params P, Bufs B, int n) {
 __global__ void k_reset_build_stats(State *st) {
   st->max_row = 0;
   st->nnz = 0;
+  if (st->coinc_gid >= 0) raise_error(st, -7 /*PM_E_COINCIDENT*/, st->coinc_gid);
 }
 
 // CSR export of the list for the getters: col_gid[row_ptr[i] + k] = gid(nbr).

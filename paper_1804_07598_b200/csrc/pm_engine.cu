@@ -58,6 +58,18 @@ struct pm_ctx_s {
   bool graph_prof = false;
   cudaGraphNode_t ev_node[2] = {nullptr, nullptr};
 
+  // multi-GPU decomposition (pm_set_decomposition)
+  bool dist = false;
+  Dist D{};
+  int64_t n_owned = 0, n_ghost = 0;
+  uint32_t *d_mask = nullptr;
+  int *d_blk = nullptr, *d_order = nullptr, *d_dirbase = nullptr, *d_list = nullptr;
+  int *d_send_idx = nullptr, *d_gslot = nullptr;
+  long long *d_tot = nullptr, *h_tot = nullptr;
+  int64_t mask_cap = 0, blk_cap = 0, list_cap = 0, send_cap = 0, gslot_cap = 0;
+  int plan_what = -1;
+  int64_t plan_send = 0, plan_stay = 0, n_send = 0;
+
   // profiling
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -99,6 +111,9 @@ __global__ void k_clear_abort(State *st) {
 
 __global__ void k_force_rebuild(State *st) { st->need_rebuild = 1; }
 
+__global__ void k_clear_rebuild(State *st) { st->need_rebuild = 0; }
+
+
 pm_status set_err(pm_ctx c, pm_status code, const char *fmt, ...) {
   char buf[512];
   va_list ap;
@@ -126,6 +141,16 @@ cudaError_t dalloc(T **p, int64_t count) {
   *p = nullptr;
   if (count <= 0) count = 1;
   return cudaMalloc((void **)p, sizeof(T) * (size_t)count);
+}
+
+template <class T>
+pm_status ensure_dev(pm_ctx c, T **p, int64_t &cap, int64_t need) {
+  if (need <= cap && *p) return PM_OK;
+  int64_t n = std::max<int64_t>(need, 1024);
+  n = (int64_t)(1.25 * (double)n);
+  CUDA_TRY(c, dalloc(p, n));
+  cap = n;
+  return PM_OK;
 }
 
 void destroy_graph(pm_ctx c) {
@@ -170,15 +195,34 @@ pm_status sync_check(pm_ctx c, const char *what) {
   return PM_OK;
 }
 
-pm_status ensure_particles(pm_ctx c, int64_t n) {
+template <class T>
+cudaError_t grow_keep(T **p, int64_t count, int64_t keep, cudaStream_t s) {
+  T *q = nullptr;
+  cudaError_t e = cudaMalloc((void **)&q, sizeof(T) * (size_t)(count > 0 ? count : 1));
+  if (e != cudaSuccess) return e;
+  if (*p && keep > 0) {
+    e = cudaMemcpyAsync(q, *p, sizeof(T) * (size_t)keep, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return e;
+    cudaStreamSynchronize(s);
+  }
+  if (*p) cudaFree(*p);
+  *p = q;
+  return cudaSuccess;
+}
+
+// Grow the particle arrays to hold n particles.  keep: leading entries of the
+// double-buffered particle arrays to preserve (multi-GPU arrivals); the other
+// arrays are rebuilt by the next build.
+pm_status ensure_particles(pm_ctx c, int64_t n, int64_t keep = 0) {
   if (n <= c->pcap) return PM_OK;
   int64_t cap = ((n + 1023) / 1024) * 1024;
+  if (keep > 0) cap = std::max(cap, (int64_t)(1.25 * (double)n));
   Bufs &B = c->B;
   for (int b = 0; b < 2; ++b) {
-    CUDA_TRY(c, dalloc(&B.pos[b], cap));
-    CUDA_TRY(c, dalloc(&B.vel[b], cap));
-    CUDA_TRY(c, dalloc(&B.gid[b], cap));
-    CUDA_TRY(c, dalloc(&B.kind[b], cap));
+    CUDA_TRY(c, grow_keep(&B.pos[b], cap, keep, c->stream));
+    CUDA_TRY(c, grow_keep(&B.vel[b], cap, keep, c->stream));
+    CUDA_TRY(c, grow_keep(&B.gid[b], cap, keep, c->stream));
+    CUDA_TRY(c, grow_keep(&B.kind[b], cap, keep, c->stream));
   }
   CUDA_TRY(c, dalloc(&B.xref, cap));
   CUDA_TRY(c, dalloc(&B.force, cap));
@@ -186,6 +230,7 @@ pm_status ensure_particles(pm_ctx c, int64_t n) {
   CUDA_TRY(c, dalloc(&B.cell_of, cap));
   CUDA_TRY(c, dalloc(&B.slot, cap));
   CUDA_TRY(c, dalloc(&B.perm, cap));
+  CUDA_TRY(c, dalloc(&B.invperm, cap));
   CUDA_TRY(c, dalloc(&B.sorttmp, cap));
   CUDA_TRY(c, dalloc(&B.cnt, cap));
   CUDA_TRY(c, cudaMemsetAsync(B.force, 0, sizeof(float4) * cap, c->stream));
@@ -215,7 +260,7 @@ pm_status ensure_cells(pm_ctx c) {
 
 int auto_nbr_cap(pm_ctx c) {
   double vol = 1.0;
-  for (int d = 0; d < 3; ++d) vol *= (double)c->P.box.hi[d] - (double)c->P.box.lo[d];
+  for (int d = 0; d < 3; ++d) vol *= (double)c->P.grid.ext[d];
   const double dens = (double)c->n / vol;
   const double mean = dens * 4.0 / 3.0 * M_PI * (double)c->rv * c->rv * c->rv;
   int cap = (int)std::ceil(mean * 1.4 + 16.0);
@@ -241,18 +286,37 @@ pm_status setup_grid(pm_ctx c) {
   Params &P = c->P;
   const float rv = c->rv;
   int64_t ncell = 1;
+  P.dist = 0;
   for (int d = 0; d < 3; ++d) {
-    const double ext = (double)P.box.hi[d] - (double)P.box.lo[d];
-    const double side = (double)rv / (double)c->cell_div;
+    const bool dec = c->dist && c->D.p[d] >= 2;
+    double ext, side;
+    if (dec) {
+      // local frame: the sub-domain plus a ghost layer on each side; cells
+      // a hair wider than r_v so that fp32 rounding of the unwrapped
+      // coordinate can never separate two neighbours by two cells
+      ext = ((double)c->D.shi[d] - (double)c->D.slo[d]) + 2.0 * (double)c->D.rg;
+      side = (double)rv * (1.0 + 1e-5);
+      P.grid.o[d] = (float)((double)c->D.slo[d] - (double)c->D.rg);
+      P.grid.wrap[d] = 0;
+      P.grid.unwrap[d] = 1;
+      P.dist = 1;
+    } else {
+      ext = (double)P.box.hi[d] - (double)P.box.lo[d];
+      side = (double)rv / (double)c->cell_div;
+      P.grid.o[d] = P.box.lo[d];
+      P.grid.wrap[d] = P.box.per[d];
+      P.grid.unwrap[d] = 0;
+    }
     double nd = std::floor(ext / side);
     if (nd < 1) nd = 1;
-    if (P.box.per[d] && nd < 3)
+    if (P.grid.wrap[d] && nd < 3)
       return set_err(c, PM_E_INVAL,
                      "periodic axis %d: extent %g < 3 r_v = %g (27-cell stencil needs 3 cells)", d,
                      ext, 3.0 * rv);
     if (nd > (double)(1 << 20)) nd = (double)(1 << 20);
     P.grid.n[d] = (int)nd;
     P.grid.inv_w[d] = (float)(nd / ext);
+    P.grid.ext[d] = (float)ext;
     ncell *= (int64_t)nd;
   }
   if (ncell > (int64_t)1 << 30) return set_err(c, PM_E_INVAL, "too many cells (%lld)", (long long)ncell);
@@ -461,6 +525,7 @@ pm_status pm_create(const pm_opts *opts, pm_ctx *out) {
     return PM_E_CUDA;
   }
   std::memset(c->st_h, 0, sizeof(State));
+  c->st_h->coinc_gid = -1;
   cudaMemcpy(c->B.st, c->st_h, sizeof(State), cudaMemcpyHostToDevice);
   c->P.lj.inv_mass = 1.f;
   *out = c;
@@ -483,6 +548,11 @@ void pm_destroy(pm_ctx c) {
                   B.perm, B.sorttmp, B.scan_tmp, B.nbr, B.cnt, B.st};
   for (void *p : ptrs)
     if (p) cudaFree(p);
+  void *dptrs[] = {c->d_mask, c->d_blk, c->d_order, c->d_dirbase, c->d_list,
+                   c->d_send_idx, c->d_gslot, c->d_tot, B.invperm};
+  for (void *p : dptrs)
+    if (p) cudaFree(p);
+  if (c->h_tot) cudaFreeHost(c->h_tot);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->st_h) cudaFreeHost(c->st_h);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
@@ -584,6 +654,10 @@ pm_status pm_place(pm_ctx c, int64_t n, const float *pos4, const float *vel4, co
   if (s) return s;
   if (n != c->n) destroy_graph(c);
   c->n = n;
+  c->n_owned = n;
+  c->n_ghost = 0;
+  c->n_send = 0;
+  c->plan_what = -1;
   const cudaMemcpyKind k = (mem == PM_DEVICE) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   Bufs &B = c->B;
   if (n > 0) {
@@ -598,6 +672,7 @@ pm_status pm_place(pm_ctx c, int64_t n, const float *pos4, const float *vel4, co
   }
   std::memset(c->st_h, 0, sizeof(State));
   c->st_h->err_gid = -1;
+  c->st_h->coinc_gid = -1;
   CUDA_TRY(c, cudaMemcpyAsync(B.st, c->st_h, sizeof(State), cudaMemcpyHostToDevice, c->stream));
   if (mem == PM_HOST) CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   c->cells_valid = c->list_valid = c->forces_valid = c->rho_valid = false;
@@ -736,8 +811,8 @@ pm_status pm_step_vv(pm_ctx c, float dt, int64_t nsteps, pm_run_stats *out) {
 
 pm_status pm_count(pm_ctx c, int64_t *n_owned, int64_t *n_ghost, int64_t *n_cells, int64_t *nnz) {
   if (!c) return PM_E_INVAL;
-  if (n_owned) *n_owned = c->n;
-  if (n_ghost) *n_ghost = 0;
+  if (n_owned) *n_owned = c->dist ? c->n_owned : c->n;
+  if (n_ghost) *n_ghost = c->dist ? c->n_ghost : 0;
   if (n_cells) *n_cells = c->have_domain && c->have_cutoff ? c->P.grid.ncell : 0;
   if (nnz) {
     pm_status s = read_state(c);
@@ -812,6 +887,18 @@ pm_status pm_get_state(pm_ctx c, float *pos4, float *vel4, float *force4, int64_
   return PM_OK;
 }
 
+pm_status pm_get_kind(pm_ctx c, int32_t *kind) {
+  if (!c || !kind) return PM_E_INVAL;
+  cudaSetDevice(c->device);
+  pm_status s = read_state(c);
+  if (s) return s;
+  if (c->n > 0)
+    CUDA_TRY(c, cudaMemcpyAsync(kind, c->B.kind[c->st_h->cur_id], 4 * c->n,
+                                cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return PM_OK;
+}
+
 pm_status pm_get_thermo(pm_ctx c, double *ke, double *pe_raw, double *pe_shift, double *virial,
                         int64_t *npairs) {
   if (!c) return PM_E_INVAL;
@@ -847,6 +934,204 @@ pm_status pm_get_profile(pm_ctx c, double *force_ms, int64_t *force_launches, do
   if (step_ms) *step_ms = c->prof_step_ms;
   if (steps) *steps = c->prof_steps;
   return PM_OK;
+}
+
+
+int32_t pm_record_bytes(int32_t what) {
+  return (what >= 0 && what <= 2) ? dist_record_bytes(what) : -1;
+}
+
+pm_status pm_set_decomposition(pm_ctx c, const int32_t pgrid[3], const int32_t pcoord[3]) {
+  if (!c || !pgrid || !pcoord) return PM_E_INVAL;
+  if (!c->have_domain || !c->have_cutoff)
+    return set_err(c, PM_E_STATE, "pm_set_decomposition: set the domain and cutoff first");
+  cudaSetDevice(c->device);
+  Dist D{};
+  const Box &b = c->P.box;
+  const double rg = (double)c->rv * (1.0 + 1e-5);
+  bool any = false;
+  for (int d = 0; d < 3; ++d) {
+    if (pgrid[d] < 1 || pgrid[d] > 64 || pcoord[d] < 0 || pcoord[d] >= pgrid[d])
+      return set_err(c, PM_E_INVAL, "pm_set_decomposition: bad grid/coord on axis %d", d);
+    const double L = (double)b.L[d];
+    D.p[d] = pgrid[d];
+    D.c[d] = pcoord[d];
+    D.glo[d] = b.lo[d];
+    D.inv_s[d] = (float)((double)pgrid[d] / L);
+    D.slo[d] = (float)((double)b.lo[d] + L * pcoord[d] / pgrid[d]);
+    D.shi[d] = (float)((double)b.lo[d] + L * (pcoord[d] + 1) / pgrid[d]);
+    if (pgrid[d] >= 2) {
+      any = true;
+      if (!b.per[d])
+        return set_err(c, PM_E_INVAL, "pm_set_decomposition: axis %d must be periodic", d);
+      if (L / pgrid[d] < 2.0 * rg)
+        return set_err(c, PM_E_INVAL,
+                       "pm_set_decomposition: sub-domain %g thinner than 2 r_v on axis %d",
+                       L / pgrid[d], d);
+    }
+  }
+  D.rg = (float)rg;
+  c->D = D;
+  c->dist = any;
+  return setup_grid(c);
+}
+
+pm_status pm_dist_plan(pm_ctx c, int32_t what, const int32_t order[26], int64_t counts[27]) {
+  pm_status s = check_ready(c);
+  if (s) return s;
+  if (!c->dist) return set_err(c, PM_E_STATE, "pm_dist_plan: no decomposition");
+  if ((what != PM_MSG_MIGRATE && what != PM_MSG_GHOST) || !order)
+    return set_err(c, PM_E_INVAL, "pm_dist_plan: bad arguments");
+  cudaSetDevice(c->device);
+  // MIGRATE scans every local particle (ghosts are skipped and dropped); GHOST
+  // runs right after a migration, when the owned particles are [0, n_owned)
+  const int64_t no = (what == PM_MSG_MIGRATE) ? c->n : c->n_owned;
+  const int64_t nblk = (no + 255) / 256 + 1;
+  if ((s = ensure_dev(c, &c->d_mask, c->mask_cap, no))) return s;
+  if ((s = ensure_dev(c, &c->d_blk, c->blk_cap, nblk * 27))) return s;
+  if ((s = ensure_dev(c, &c->d_list, c->list_cap, (what == PM_MSG_GHOST ? 7 : 1) * no + 1)))
+    return s;
+  if (!c->d_order) {
+    CUDA_TRY(c, cudaMalloc((void **)&c->d_order, 26 * sizeof(int)));
+    CUDA_TRY(c, cudaMalloc((void **)&c->d_dirbase, 27 * sizeof(int)));
+    CUDA_TRY(c, cudaMalloc((void **)&c->d_tot, 27 * sizeof(long long)));
+    CUDA_TRY(c, cudaMallocHost((void **)&c->h_tot, 27 * sizeof(long long)));
+  }
+  for (int k = 0; k < 26; ++k)
+    if (order[k] < 0 || order[k] > 26 || order[k] == 13)
+      return set_err(c, PM_E_INVAL, "pm_dist_plan: order must list the 26 directions != 13");
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_order, order, 26 * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  launch_dist_plan(c->P, c->B, c->D, (int)no, what, c->d_mask, c->d_blk, c->d_order, c->d_dirbase,
+                   c->d_tot, c->d_list, c->stream);
+  CUDA_TRY(c, cudaMemcpyAsync(c->h_tot, c->d_tot, 27 * sizeof(long long), cudaMemcpyDeviceToHost,
+                              c->stream));
+  s = sync_check(c, "pm_dist_plan");
+  if (s) return s;
+  int64_t send = 0;
+  for (int d = 0; d < 27; ++d) {
+    if (counts) counts[d] = c->h_tot[d];
+    if (d != 13) send += c->h_tot[d];
+  }
+  c->plan_what = what;
+  c->plan_send = send;
+  c->plan_stay = c->h_tot[13];
+  return PM_OK;
+}
+
+pm_status pm_dist_pack(pm_ctx c, int32_t what, void *send_dev) {
+  if (!c) return PM_E_INVAL;
+  if (c->sticky) return c->sticky;
+  if (c->plan_what != what) return set_err(c, PM_E_STATE, "pm_dist_pack: no matching plan");
+  cudaSetDevice(c->device);
+  if (c->plan_send > 0 && !send_dev) return set_err(c, PM_E_INVAL, "pm_dist_pack: null buffer");
+  launch_dist_pack(c->B, what, c->d_list, (int)c->plan_send, send_dev, c->stream);
+  if (what == PM_MSG_MIGRATE) {
+    // stable compaction of the stayers (list entries after the 26 directions)
+    launch_dist_compact(c->B, c->d_list + c->plan_send, (int)c->plan_stay, c->stream);
+    launch_flip(c->B, 1, 1, 0, c->stream);
+    c->n_owned = c->plan_stay;
+    c->n_ghost = 0;
+    c->n = c->n_owned;
+  } else {
+    pm_status s = ensure_dev(c, &c->d_send_idx, c->send_cap, c->plan_send + 1);
+    if (s) return s;
+    if (c->plan_send > 0)
+      CUDA_TRY(c, cudaMemcpyAsync(c->d_send_idx, c->d_list, sizeof(int) * c->plan_send,
+                                  cudaMemcpyDeviceToDevice, c->stream));
+    c->n_send = c->plan_send;
+  }
+  c->plan_what = -1;
+  c->cells_valid = c->list_valid = c->forces_valid = c->rho_valid = false;
+  destroy_graph(c);
+  return check_launch(c, "pm_dist_pack");
+}
+
+pm_status pm_dist_unpack(pm_ctx c, int32_t what, const void *recv_dev, int64_t nrecv) {
+  if (!c || nrecv < 0) return PM_E_INVAL;
+  if (c->sticky) return c->sticky;
+  if (what != PM_MSG_MIGRATE && what != PM_MSG_GHOST)
+    return set_err(c, PM_E_INVAL, "pm_dist_unpack: bad kind");
+  if (nrecv > 0 && !recv_dev) return set_err(c, PM_E_INVAL, "pm_dist_unpack: null buffer");
+  cudaSetDevice(c->device);
+  const int64_t base = c->n_owned;
+  pm_status s = ensure_particles(c, base + nrecv, base);
+  if (s) return s;
+  launch_dist_unpack(c->B, what, recv_dev, (int)nrecv, (int)base, c->stream);
+  if (what == PM_MSG_MIGRATE) {
+    c->n_owned = base + nrecv;
+    c->n_ghost = 0;
+  } else {
+    c->n_ghost = nrecv;
+  }
+  c->n = c->n_owned + c->n_ghost;
+  c->cells_valid = c->list_valid = c->forces_valid = c->rho_valid = false;
+  destroy_graph(c);
+  return check_launch(c, "pm_dist_unpack");
+}
+
+pm_status pm_dist_finish(pm_ctx c) {
+  pm_status s = check_ready(c);
+  if (s) return s;
+  if (!c->dist) return set_err(c, PM_E_STATE, "pm_dist_finish: no decomposition");
+  cudaSetDevice(c->device);
+  s = build_list(c);  // cells over owned + ghosts, Verlet rows for owned
+  if (s) return s;
+  if ((s = ensure_dev(c, &c->d_gslot, c->gslot_cap, c->n_ghost + 1))) return s;
+  launch_dist_remap(c->B.invperm, c->d_send_idx, (int)c->n_send, c->d_gslot, (int)c->n_ghost,
+                    (int)c->n_owned, c->stream);
+  return sync_check(c, "pm_dist_finish");
+}
+
+pm_status pm_dist_refresh_pack(pm_ctx c, void *send_dev) {
+  if (!c) return PM_E_INVAL;
+  if (c->sticky) return c->sticky;
+  if (c->n_send > 0 && !send_dev) return set_err(c, PM_E_INVAL, "null buffer");
+  launch_refresh_pack(c->B, c->d_send_idx, (int)c->n_send, send_dev, c->stream);
+  return check_launch(c, "pm_dist_refresh_pack");
+}
+
+pm_status pm_dist_refresh_unpack(pm_ctx c, const void *recv_dev) {
+  if (!c) return PM_E_INVAL;
+  if (c->sticky) return c->sticky;
+  if (c->n_ghost > 0 && !recv_dev) return set_err(c, PM_E_INVAL, "null buffer");
+  launch_refresh_unpack(c->B, c->d_gslot, (int)c->n_ghost, recv_dev, c->stream);
+  return check_launch(c, "pm_dist_refresh_unpack");
+}
+
+pm_status pm_dist_step(pm_ctx c, float dt, int32_t phase, int32_t *need_rebuild) {
+  pm_status s = check_ready(c);
+  if (s) return s;
+  if (!c->have_lj) return set_err(c, PM_E_STATE, "pm_set_lj not called");
+  if (phase != PM_PHASE_FORCES && !(dt > 0.f)) return set_err(c, PM_E_INVAL, "dt must be > 0");
+  cudaSetDevice(c->device);
+  switch (phase) {
+    case PM_PHASE_PROLOGUE:
+      if (!c->forces_valid) return set_err(c, PM_E_STATE, "pm_dist_step: forces not valid");
+      launch_kick_drift(c->P, c->B, c->n, dt, c->stream);
+      break;
+    case PM_PHASE_STEP:
+    case PM_PHASE_FINAL:
+      if (!c->list_valid) return set_err(c, PM_E_STATE, "pm_dist_step: no Verlet list");
+      launch_lj_step_mode(c->P, c->B, c->n, dt, phase == PM_PHASE_STEP ? kModeInner : kModeFinal,
+                          c->stream);
+      c->forces_valid = (phase == PM_PHASE_FINAL);
+      break;
+    case PM_PHASE_FORCES:
+      if (!c->list_valid) return set_err(c, PM_E_STATE, "pm_dist_step: no Verlet list");
+      launch_lj(c->P, c->B, c->n, 0, c->stream);
+      c->forces_valid = true;
+      break;
+    default:
+      return set_err(c, PM_E_INVAL, "pm_dist_step: bad phase");
+  }
+  k_apply_pending<<<1, 1, 0, c->stream>>>(c->B.st);
+  if (need_rebuild) {
+    s = sync_check(c, "pm_dist_step");
+    if (s) return s;
+    *need_rebuild = c->st_h->need_rebuild;
+    k_clear_rebuild<<<1, 1, 0, c->stream>>>(c->B.st);
+  }
+  return check_launch(c, "pm_dist_step");
 }
 
 }  // extern "C"

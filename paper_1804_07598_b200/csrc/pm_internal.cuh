@@ -27,11 +27,32 @@ struct Box {
   int per[3];      // periodic axis flags
 };
 
+// Cell grid in the context's local frame.  Single GPU: o = box.lo,
+// wrap = box.per, unwrap = 0 (exactly R2/R3).  Decomposed axis of a
+// multi-GPU sub-domain: o = slo - r_v, the extent covers the ghost layers,
+// wrap = 0 (no local periodic stencil) and unwrap = 1 (a global coordinate is
+// mapped to the image nearest the sub-domain before binning).
 struct Grid {
   int n[3];        // cells per axis (R2)
-  float inv_w[3];  // fp32(n / (hi - lo)) (R2)
+  float inv_w[3];  // fp32(n / extent) (R2)
+  float o[3];      // frame origin
+  float ext[3];    // frame extent
+  int wrap[3];     // periodic stencil along this axis
+  int unwrap[3];   // bin the nearest image (decomposed axes)
   int ncell;
 };
+
+// Decomposition of the global periodic box into p[0] x p[1] x p[2] cuboids;
+// this context owns cuboid c.  Ownership along axis d: the pinned fp32 rule
+// min(max(floor(fl(fl(x - glo) * inv_s)), 0), p - 1).
+struct Dist {
+  int p[3], c[3];
+  float glo[3], inv_s[3];
+  float slo[3], shi[3];  // this sub-domain (fp32)
+  float rg;              // ghost selection width (r_v with a 1e-5 margin)
+};
+
+constexpr int kGhostBit = 1 << 30;  // kind flag of a ghost copy
 
 struct LJ {
   float rc2;       // fl32(r_cut * r_cut)
@@ -61,6 +82,7 @@ struct Params {
   float mi_margin;  // r_v + skin: particles farther than this from every
                     // periodic face cannot have a list partner across it
   int nbr_cap;      // slots per row (multiple of 4)
+  int dist;         // 1: sub-domain context (ghosts present, skip them as rows)
 };
 
 // Device buffers (pointers fixed between reallocations; captured in graphs).
@@ -78,6 +100,7 @@ struct Bufs {
   int32_t *count;      // [ncell]
   int32_t *start;      // [ncell + 1]
   int32_t *perm;       // [n] sorted k -> storage index
+  int32_t *invperm;    // [n] storage index -> sorted k (multi-GPU remap)
   int32_t *sorttmp;    // [n] scatter target before the per-cell sort
   int32_t *scan_tmp;   // block sums for the scan
   int32_t *nbr;        // SELL-32 neighbour slots, int4-interleaved
@@ -102,6 +125,9 @@ struct State {
   long long nnz;        // entries of the last build
   long long steps_done; // force-step kernels completed (not aborted)
   int do_rebuild;       // rebuild decision of the current step (non-graph path)
+  long long coinc_gid;  // a particle with a coincident partner (-1: none), set
+                        // by the cell sort, raised as PM_E_COINCIDENT by the
+                        // Verlet build (the cell list itself is well defined)
   double acc[4];        // energy: U_raw, virial, npairs, KE
 };
 
@@ -121,13 +147,27 @@ PM_DEV float wrap1(float x, float lo, float hi, float L) {
 }
 
 // R3: c = min(max(floor(fl(fl(x - lo) * inv_w)), 0), n - 1).
-PM_DEV int cell_coord(float x, float lo, float inv_w, int n) {
-  float u = __fmul_rn(__fsub_rn(x, lo), inv_w);
-  float f = floorf(u);
+PM_DEV int cell_coord_u(float u, float inv_w, int n) {
+  float f = floorf(__fmul_rn(u, inv_w));
   int c = (int)f;
   if (f < 0.0f) c = 0;
   if (c > n - 1) c = n - 1;
   return c;
+}
+
+PM_DEV int cell_coord(float x, float lo, float inv_w, int n) {
+  return cell_coord_u(__fsub_rn(x, lo), inv_w, n);
+}
+
+// Cell coordinate along axis d in the local frame (identical to R3 when the
+// axis is not decomposed).
+PM_DEV int local_coord(const Box &box, const Grid &g, int d, float x) {
+  float u = __fsub_rn(x, g.o[d]);
+  if (g.unwrap[d]) {
+    if (u < 0.0f) u = __fadd_rn(u, box.L[d]);
+    else if (u >= g.ext[d]) u = __fsub_rn(u, box.L[d]);
+  }
+  return cell_coord_u(u, g.inv_w[d], g.n[d]);
 }
 
 // R4: delta = x_j - x_i with the Sterbenz-ordered periodic correction.
@@ -193,4 +233,21 @@ void launch_sph_density(const Params &P, const Bufs &B, int64_t n, cudaStream_t 
 void launch_sph_forces(const Params &P, const Bufs &B, int64_t n, cudaStream_t s);
 void launch_verlet_export(const Bufs &B, int64_t n, int cap, const int64_t *row_ptr,
                           int64_t *col_gid, cudaStream_t s);
+void launch_lj_step_mode(const Params &P, const Bufs &B, int64_t n, float dt, int mode,
+                         cudaStream_t s);
+int dist_record_bytes(int what);
+void launch_dist_plan(const Params &P, const Bufs &B, const Dist &D, int n_owned, int what,
+                      uint32_t *mask, int *blk_counts, const int *order, int *dir_base,
+                      long long *totals, int *list, cudaStream_t s);
+void launch_dist_pack(const Bufs &B, int what, const int *list, int nsend, void *out,
+                      cudaStream_t s);
+void launch_dist_compact(const Bufs &B, const int *stay, int n_stay, cudaStream_t s);
+void launch_dist_unpack(const Bufs &B, int what, const void *in, int nrecv, int base,
+                        cudaStream_t s);
+void launch_dist_remap(const int *invperm, int *send_idx, int nsend, int *ghost_slot, int nghost,
+                       int n_owned, cudaStream_t s);
+void launch_refresh_pack(const Bufs &B, const int *send_idx, int nsend, void *out,
+                         cudaStream_t s);
+void launch_refresh_unpack(const Bufs &B, const int *ghost_slot, int nghost, const void *in,
+                           cudaStream_t s);
 }  // namespace pm

@@ -1,0 +1,423 @@
+"""Multi-GPU orchestration of the decomposed hot path.
+
+The periodic box is split into px x py x pz cuboids, one per rank (GPU); each
+rank's pm_ctx owns one cuboid (pm_set_decomposition).  PAPER.md:62 (§3.1):
+sub-domains extended by a ghost layer of interaction width; PAPER.md:112-118
+(§3.4): map() migrates particles that left a sub-domain to the neighbour that
+owns them and ghost_get() fills the ghost layers (here with positions only
+between rebuilds, PAPER.md:118 and Listing 4.1 ghost_get<>()).
+
+All particle work (selection, packing, unpacking, sorting, lists, forces,
+integration) runs in libpm.so kernels.  This module only decides who talks to
+whom, moves message bytes with a Transport, and sequences the phases:
+
+  rebuild:  plan/pack MIGRATE -> exchange -> unpack; plan/pack GHOST ->
+            exchange -> unpack; finish (cells, lists, refresh maps)
+  step:     [rebuild if any rank's particle moved > skin/2, else ghost
+            refresh] -> force + fused kick/drift -> global flag (MAX)
+
+Transports: TorchTransport (torch.distributed: NCCL between GPUs, gloo on
+CPU for the host-logic tests) and LoopbackTransport (several sub-domains in
+one process on one GPU -- a test stand-in for NVLink that exercises exactly
+the same kernels and message layout).
+"""
+from __future__ import annotations
+
+import itertools
+import json
+import os
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+# direction index d = (ax+1) + 3 (ay+1) + 9 (az+1); 13 = self
+DIRS = [(ax, ay, az) for az in (-1, 0, 1) for ay in (-1, 0, 1) for ax in (-1, 0, 1)]
+SELF = 13
+
+
+def dir_index(a):
+    return (a[0] + 1) + 3 * (a[1] + 1) + 9 * (a[2] + 1)
+
+
+@dataclass
+class Decomp:
+    """px x py x pz cuboids; rank = cx + px (cy + py cz)."""
+
+    grid: tuple
+
+    @property
+    def size(self):
+        return self.grid[0] * self.grid[1] * self.grid[2]
+
+    def coord(self, rank):
+        px, py, _ = self.grid
+        return (rank % px, (rank // px) % py, rank // (px * py))
+
+    def rank_of(self, c):
+        px, py, pz = self.grid
+        return (c[0] % px) + px * ((c[1] % py) + py * (c[2] % pz))
+
+    def valid_dirs(self):
+        """Directions that exist: no component along an undecomposed axis."""
+        return [d for d, a in enumerate(DIRS)
+                if d != SELF and all(a[k] == 0 or self.grid[k] >= 2 for k in range(3))]
+
+    def peer(self, rank, d):
+        c = self.coord(rank)
+        a = DIRS[d]
+        return self.rank_of(tuple(c[k] + a[k] for k in range(3)))
+
+    def peers(self, rank):
+        return sorted({self.peer(rank, d) for d in self.valid_dirs()})
+
+    def send_order(self, rank):
+        """Packing order of the 26 directions: grouped by peer (ascending),
+        then by direction index; non-existent directions last (always empty)."""
+        v = self.valid_dirs()
+        order = sorted(v, key=lambda d: (self.peer(rank, d), d))
+        order += [d for d in range(27) if d != SELF and d not in v]
+        return order
+
+    def segments(self, rank, counts):
+        """Per peer: (first record, number of records) of its segment in the
+        buffer packed in send_order (counts = per-direction records)."""
+        seg, off = {}, 0
+        for d in self.send_order(rank):
+            if d not in self.valid_dirs():
+                assert counts[d] == 0
+                continue
+            p = self.peer(rank, d)
+            if p not in seg:
+                seg[p] = [off, 0]
+            seg[p][1] += int(counts[d])
+            off += int(counts[d])
+        for p in self.peers(rank):
+            seg.setdefault(p, [off, 0])
+        return {p: tuple(v) for p, v in seg.items()}
+
+
+# ---------------------------------------------------------------- transports
+class TorchTransport:
+    """torch.distributed point-to-point (NCCL on GPUs; gloo on CPU)."""
+
+    def __init__(self, device=None):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.device = device
+
+    def exchange(self, sends, recvs):
+        """sends/recvs: {peer: tensor} (uint8 or int64); zero-size skipped."""
+        ops = []
+        P2P, dist = self.dist.P2POp, self.dist
+        for p in sorted(set(sends) | set(recvs)):
+            if p in sends and sends[p].numel() > 0:
+                ops.append(P2P(dist.isend, sends[p], p))
+            if p in recvs and recvs[p].numel() > 0:
+                ops.append(P2P(dist.irecv, recvs[p], p))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+
+    def exchange_counts(self, counts):
+        """counts: {peer: int} -> {peer: int received}."""
+        t = self.torch
+        dev = self.device if self.device is not None else "cpu"
+        s = {p: t.tensor([int(c)], dtype=t.int64, device=dev) for p, c in counts.items()}
+        r = {p: t.zeros(1, dtype=t.int64, device=dev) for p in counts}
+        self.exchange(s, r)
+        return {p: int(v.item()) for p, v in r.items()}
+
+    def allreduce_max(self, x):
+        t = self.torch
+        dev = self.device if self.device is not None else "cpu"
+        v = t.tensor([int(x)], dtype=t.int64, device=dev)
+        self.dist.all_reduce(v, op=self.dist.ReduceOp.MAX)
+        return int(v.item())
+
+    def allreduce_sum(self, arr):
+        t = self.torch
+        dev = self.device if self.device is not None else "cpu"
+        v = t.tensor(np.asarray(arr, np.float64), device=dev)
+        self.dist.all_reduce(v)
+        return v.cpu().numpy()
+
+
+class LoopbackTransport:
+    """All ranks live in this process (lock-step): a message from rank r to
+    peer q is a device-to-device copy.  Used to run P sub-domains on one GPU."""
+
+    def __init__(self, members):
+        self.members = members  # rank -> object with .rank
+
+    def exchange_all(self, sends, recvs):
+        """sends[r][q] -> recvs[q][r] (tensors of equal size)."""
+        for r, per in sends.items():
+            for q, buf in per.items():
+                if buf.numel() > 0:
+                    recvs[q][r].copy_(buf)
+
+    def exchange_counts_all(self, counts):
+        return {q: {r: counts[r][q] for r in counts if q in counts[r]} for q in counts}
+
+
+# ---------------------------------------------------------------- simulation
+class DistSim:
+    """Lock-step driver for one or more local sub-domains.
+
+    members: {rank: pm.DistContext}; transport: TorchTransport (one local
+    member per process) or LoopbackTransport (all members local)."""
+
+    def __init__(self, decomp: Decomp, members: dict, transport, dt=0.005, device="cuda",
+                 stream=None):
+        import contextlib
+        import torch
+        self.torch = torch
+        self.device = device
+        # all library work, buffer copies and NCCL calls are ordered on ONE
+        # stream: the members must have been created on it (make_member)
+        self.stream = stream
+        self._ctxmgr = (lambda: torch.cuda.stream(stream)) if stream is not None \
+            else contextlib.nullcontext
+        self.D = decomp
+        self.m = members
+        self.tr = transport
+        self.dt = dt
+        self.loop = isinstance(transport, LoopbackTransport)
+        self.ghost_seg = {}   # rank -> {peer: (off, n)} of the last ghost plan (send side)
+        self.ghost_recv = {}  # rank -> {peer: n} received ghosts
+        self.rebuilds = 0
+        self._bufs = {}
+
+    # ---- helpers
+    def _buf(self, key, nbytes):
+        t = self.torch
+        b = self._bufs.get(key)
+        if b is None or b.numel() < nbytes:
+            b = t.empty(max(int(nbytes * 1.25), 64), dtype=t.uint8, device=self.device)
+            self._bufs[key] = b
+        return b[:nbytes]
+
+    def _exchange(self, sends, recvs):
+        if self.loop:
+            self.tr.exchange_all(sends, recvs)
+        else:
+            (r,) = list(self.m)
+            self.tr.exchange(sends[r], recvs[r])
+
+    def _exchange_counts(self, counts):
+        if self.loop:
+            return self.tr.exchange_counts_all(counts)
+        (r,) = list(self.m)
+        return {r: self.tr.exchange_counts(counts[r])}
+
+    def _allreduce_max(self, vals):
+        v = max(vals.values())
+        return v if self.loop else self.tr.allreduce_max(v)
+
+    def _message_round(self, what):
+        """plan -> pack -> counts -> exchange -> unpack for MIGRATE / GHOST."""
+        from . import pm
+        rb = pm.record_bytes(what)
+        sends, seg, counts = {}, {}, {}
+        for r, ctx in self.m.items():
+            cnt = ctx.dist_plan(what, self.D.send_order(r))
+            seg[r] = self.D.segments(r, cnt)
+            nsend = sum(n for _, n in seg[r].values())
+            buf = self._buf(("send", what, r), nsend * rb)
+            ctx.dist_pack(what, buf if nsend else None)
+            sends[r] = {p: buf[o * rb:(o + n) * rb] for p, (o, n) in seg[r].items()}
+            counts[r] = {p: n for p, (o, n) in seg[r].items()}
+        recv_counts = self._exchange_counts(counts)
+        recvs, rbufs = {}, {}
+        for r in self.m:
+            peers = self.D.peers(r)
+            tot = sum(recv_counts[r][p] for p in peers)
+            buf = self._buf(("recv", what, r), tot * rb)
+            rbufs[r] = (buf, tot)
+            off, recvs[r] = 0, {}
+            for p in peers:  # arrivals concatenated in peer order
+                n = recv_counts[r][p]
+                recvs[r][p] = buf[off * rb:(off + n) * rb]
+                off += n
+        self._exchange(sends, recvs)
+        for r, ctx in self.m.items():
+            buf, tot = rbufs[r]
+            ctx.dist_unpack(what, buf if tot else None, tot)
+        if what == pm.PM_MSG_GHOST:
+            self.ghost_seg = seg
+            self.ghost_recv = recv_counts
+
+    def rebuild(self):
+        with self._ctxmgr():
+            self._rebuild()
+
+    def _rebuild(self):
+        from . import pm
+        self._message_round(pm.PM_MSG_MIGRATE)
+        self._message_round(pm.PM_MSG_GHOST)
+        for ctx in self.m.values():
+            ctx.dist_finish()
+        self.rebuilds += 1
+
+    def refresh(self):
+        with self._ctxmgr():
+            self._refresh()
+
+    def _refresh(self):
+        """Positions-only ghost refresh with the last ghost plan's layout."""
+        sends, recvs = {}, {}
+        for r, ctx in self.m.items():
+            nsend = sum(n for _, n in self.ghost_seg[r].values())
+            buf = self._buf(("rsend", r), nsend * 16)
+            ctx.refresh_pack(buf if nsend else None)
+            sends[r] = {p: buf[o * 16:(o + n) * 16] for p, (o, n) in self.ghost_seg[r].items()}
+        rb = {}
+        for r in self.m:
+            peers = self.D.peers(r)
+            tot = sum(self.ghost_recv[r][p] for p in peers)
+            buf = self._buf(("rrecv", r), tot * 16)
+            rb[r] = (buf, tot)
+            off, recvs[r] = 0, {}
+            for p in peers:
+                n = self.ghost_recv[r][p]
+                recvs[r][p] = buf[off * 16:(off + n) * 16]
+                off += n
+        self._exchange(sends, recvs)
+        for r, ctx in self.m.items():
+            buf, tot = rb[r]
+            ctx.refresh_unpack(buf if tot else None)
+
+    def start(self):
+        """After pm_place on every member: first decomposition + forces."""
+        from . import pm
+        with self._ctxmgr():
+            self._rebuild()
+        for ctx in self.m.values():
+            ctx.dist_step(self.dt, pm.PM_PHASE_FORCES)
+
+    def run(self, nsteps):
+        """nsteps velocity-Verlet steps (forces valid on entry and exit)."""
+        with self._ctxmgr():
+            return self._run(nsteps)
+
+    def _run(self, nsteps):
+        from . import pm
+        if nsteps <= 0:
+            return 0
+        flags = {r: ctx.dist_step(self.dt, pm.PM_PHASE_PROLOGUE, read_flag=True)
+                 for r, ctx in self.m.items()}
+        flag = self._allreduce_max(flags)
+        reb = 0
+        for s in range(nsteps):
+            if flag:
+                self._rebuild()
+                reb += 1
+            else:
+                self._refresh()
+            last = s == nsteps - 1
+            phase = pm.PM_PHASE_FINAL if last else pm.PM_PHASE_STEP
+            flags = {r: ctx.dist_step(self.dt, phase, read_flag=not last)
+                     for r, ctx in self.m.items()}
+            flag = 0 if last else self._allreduce_max(flags)
+        return reb
+
+    def thermo(self):
+        """Global KE, U_shift, npairs (sums over ranks)."""
+        vals = np.zeros(3)
+        for ctx in self.m.values():
+            th = ctx.thermo()
+            vals += [th["ke"], th["pe_shift"], th["npairs"]]
+        if not self.loop:
+            vals = self.tr.allreduce_sum(vals)
+        return dict(ke=vals[0], pe_shift=vals[1], npairs=vals[2])
+
+
+def make_member(system, decomp, rank, device=0, stream=None, rc=2.5, skin=0.3, r_min=0.0):
+    """A DistContext for `rank` of `decomp`, with the rank's particles of
+    `system` (an inputs.System) placed."""
+    from . import pm
+    # `stream`: the torch.cuda.Stream the DistSim will run on (never the
+    # legacy default stream, whose handle 0 would mean "library-owned stream")
+    handle = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+    ctx = pm.DistContext(device=device, stream=handle)
+    ctx.set_domain(system.lo, system.hi, system.periodic)
+    ctx.set_cutoff(rc, skin)
+    ctx.set_lj(1.0, 1.0, 1.0, r_min)
+    ctx.set_decomposition(decomp.grid, decomp.coord(rank))
+    ctx.place(system.pos, system.vel, system.gid, system.kind)
+    return ctx
+
+
+def owner_of(system, decomp):
+    """Rank owning each particle (host helper for splitting a generated global
+    system; the library applies the same fp32 ownership rule on migration)."""
+    lo = system.lo.astype(np.float32)
+    L = (system.hi - system.lo).astype(np.float32)
+    c = np.zeros((system.n, 3), np.int64)
+    for d in range(3):
+        p = decomp.grid[d]
+        inv = np.float32(p / float(L[d]))
+        u = (system.pos[:, d] - lo[d]).astype(np.float32) * inv
+        c[:, d] = np.clip(np.floor(u.astype(np.float32)), 0, p - 1)
+    return c[:, 0] + decomp.grid[0] * (c[:, 1] + decomp.grid[1] * c[:, 2])
+
+
+# ---------------------------------------------------------------- bench (N>1)
+def _grid_for(n):
+    return {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}.get(n) or (n, 1, 1)
+
+
+def bench_main(args):
+    """bench.py --gpus N under torchrun: BJ configs[2] weak scaling, one
+    128^3 lattice block (2,097,152 particles) per GPU, NCCL transport."""
+    import torch
+    import torch.distributed as tdist
+    from . import build as pmbuild, inputs
+    pmbuild.build()
+    ws = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    D = Decomp(_grid_for(ws))
+    s = inputs.cfg3_block(*D.coord(rank), grid=D.grid)
+    stream = torch.cuda.Stream()
+    ctx = make_member(s, D, rank, device=local, stream=stream)
+    sim = DistSim(D, {rank: ctx}, TorchTransport(device=torch.device("cuda", local)),
+                  stream=stream)
+    sim.start()
+    sim.run(args.warmup)
+    torch.cuda.synchronize()
+    tdist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    reb = sim.run(args.steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    tdist.barrier()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    ms = float(t.item())
+    n_tot = torch.tensor([ctx.count()["n_owned"]], dtype=torch.int64, device="cuda")
+    tdist.all_reduce(n_tot)
+    if rank == 0:
+        from bench import METRIC, UNIT  # noqa: E402
+        n = int(n_tot.item())
+        line = {"metric": METRIC, "value": n * args.steps / (ms * 1e-3), "unit": UNIT,
+                "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": "cfg3 (BJ configs[2]): LJ fluid, 2,097,152 particles "
+                                       "per GPU (SC 128^3 block, rho=0.8), cuboid "
+                                       f"decomposition {D.grid}, ghost width r_cut+skin",
+                           "n_particles": n, "parallelism": f"spatial {D.grid}",
+                           "rebuilds": reb, "l2": "inputs larger than L2"},
+                "roofline": None, "cpu_baseline": None,
+                "e2e": None, "gpu_launches": None, "clocks": None}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    tdist.destroy_process_group()
+    return 0

@@ -81,9 +81,19 @@ def lib(path: str = LIB_PATH):
         "pm_get_verlet": (st, [vp, vp, vp]),
         "pm_get_state": (st, [vp, vp, vp, vp, vp, vp, vp, C.c_int32]),
         "pm_get_thermo": (st, [vp, vp, vp, vp, vp, vp]),
+        "pm_get_kind": (st, [vp, vp]),
         "pm_thermo_compute": (st, [vp]),
         "pm_set_profiling": (st, [vp, C.c_int32]),
         "pm_get_profile": (st, [vp, vp, vp, vp, vp]),
+        "pm_record_bytes": (C.c_int32, [C.c_int32]),
+        "pm_set_decomposition": (st, [vp, vp, vp]),
+        "pm_dist_plan": (st, [vp, C.c_int32, vp, vp]),
+        "pm_dist_pack": (st, [vp, C.c_int32, vp]),
+        "pm_dist_unpack": (st, [vp, C.c_int32, vp, C.c_int64]),
+        "pm_dist_finish": (st, [vp]),
+        "pm_dist_refresh_pack": (st, [vp, vp]),
+        "pm_dist_refresh_unpack": (st, [vp, vp]),
+        "pm_dist_step": (st, [vp, C.c_float, C.c_int32, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -223,7 +233,8 @@ class Context:
         return dict(cell_of=cell_of, start=start, perm=perm)
 
     def get_verlet(self):
-        n = self.count()["n_owned"]
+        c = self.count()
+        n = c["n_owned"] + c["n_ghost"]  # one (possibly empty) row per local particle
         rp = np.zeros(n + 1, np.int64)
         self._check(self.L.pm_get_verlet(self.h, rp.ctypes.data, None))
         col = np.zeros(max(int(rp[-1]), 1), np.int64)
@@ -231,7 +242,8 @@ class Context:
         return rp, col[:int(rp[-1])]
 
     def get_state(self):
-        n = self.count()["n_owned"]
+        c = self.count()
+        n = c["n_owned"] + c["n_ghost"]  # local particles incl. ghost copies
         pos = np.zeros((n, 4), np.float32)
         vel = np.zeros((n, 4), np.float32)
         f = np.zeros((n, 4), np.float32)
@@ -252,6 +264,12 @@ class Context:
         self._check(self.L.pm_get_state(self.h, pp, pv, None, None, None, None,
                                         mem if pos4 is not None else mem2))
 
+    def kind(self):
+        c = self.count()
+        k = np.zeros(c["n_owned"] + c["n_ghost"], np.int32)
+        self._check(self.L.pm_get_kind(self.h, k.ctypes.data))
+        return k
+
     def thermo(self, recompute=True):
         if recompute:
             self._check(self.L.pm_thermo_compute(self.h))
@@ -270,6 +288,67 @@ class Context:
         self._check(self.L.pm_get_profile(self.h, C.byref(fm), C.byref(fl), C.byref(sm),
                                           C.byref(ns)))
         return dict(force_ms=fm.value, force_launches=fl.value, step_ms=sm.value, steps=ns.value)
+
+
+PM_MSG_MIGRATE, PM_MSG_GHOST, PM_MSG_REFRESH = 0, 1, 2
+PM_PHASE_PROLOGUE, PM_PHASE_STEP, PM_PHASE_FINAL, PM_PHASE_FORCES = 0, 1, 2, 3
+GHOST_BIT = 1 << 30
+
+
+def record_bytes(what: int) -> int:
+    return int(lib().pm_record_bytes(what))
+
+
+def _dev_ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+class DistContext(Context):
+    """A Context owning one cuboid of a decomposed periodic box (pm.h
+    multi-GPU section); buffers are torch device tensors."""
+
+    def set_decomposition(self, grid, coord):
+        g = np.ascontiguousarray(grid, np.int32)
+        c = np.ascontiguousarray(coord, np.int32)
+        self._check(self.L.pm_set_decomposition(self.h, g.ctypes.data, c.ctypes.data))
+
+    def dist_plan(self, what, order):
+        o = np.ascontiguousarray(order, np.int32)
+        cnt = np.zeros(27, np.int64)
+        self._check(self.L.pm_dist_plan(self.h, what, o.ctypes.data, cnt.ctypes.data))
+        return cnt
+
+    def dist_pack(self, what, send):
+        self._check(self.L.pm_dist_pack(self.h, what, _dev_ptr(send)))
+
+    def dist_unpack(self, what, recv, nrecv):
+        self._check(self.L.pm_dist_unpack(self.h, what, _dev_ptr(recv), int(nrecv)))
+
+    def dist_finish(self):
+        self._check(self.L.pm_dist_finish(self.h))
+
+    def refresh_pack(self, send):
+        self._check(self.L.pm_dist_refresh_pack(self.h, _dev_ptr(send)))
+
+    def refresh_unpack(self, recv):
+        self._check(self.L.pm_dist_refresh_unpack(self.h, _dev_ptr(recv)))
+
+    def get_kind(self):
+        c = self.count()
+        k = np.zeros(c["n_owned"] + c["n_ghost"], np.int32)
+        self._check(self.L.pm_get_kind(self.h, k.ctypes.data))
+        return k
+
+    def owned_state(self):
+        """get_state() restricted to owned particles (ghost copies removed)."""
+        st = self.get_state()
+        own = (self.get_kind() & GHOST_BIT) == 0
+        return {k: v[own] for k, v in st.items()}
+
+    def dist_step(self, dt, phase, read_flag=False):
+        f = C.c_int32(0)
+        self._check(self.L.pm_dist_step(self.h, dt, phase, C.byref(f) if read_flag else None))
+        return int(f.value)
 
 
 def sorted_by_gid(state: dict) -> dict:

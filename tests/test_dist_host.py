@@ -1,0 +1,141 @@
+"""Host logic of the multi-GPU path on CPU: decomposition, neighbour/peer
+maps, packing order and message segments, and the message protocol of
+DistSim over a world-size-2 gloo process group (synthetic records stand in for
+the CUDA pack/unpack kernels, which the GPU loopback test covers)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_1804_07598_b200.dist import DIRS, SELF, Decomp, DistSim, TorchTransport
+
+
+def opposite(d):
+    a = DIRS[d]
+    return (-a[0] + 1) + 3 * (-a[1] + 1) + 9 * (-a[2] + 1)
+
+
+@pytest.mark.parametrize("grid", [(1, 1, 1), (2, 1, 1), (2, 2, 1), (2, 2, 2), (3, 1, 1),
+                                  (3, 3, 3), (4, 2, 1)])
+def test_decomp_maps_are_consistent(grid):
+    D = Decomp(grid)
+    valid = D.valid_dirs()
+    assert SELF not in valid
+    n_dec = sum(1 for p in grid if p >= 2)
+    assert len(valid) == 3 ** n_dec - 1
+    for r in range(D.size):
+        assert D.rank_of(D.coord(r)) == r
+        order = D.send_order(r)
+        assert sorted(order) == [d for d in range(27) if d != SELF]
+        for d in valid:
+            q = D.peer(r, d)
+            assert q != r
+            assert D.peer(q, opposite(d)) == r  # the way back
+        # segments: contiguous, in peer order, sizes = sum of directions
+        rng = np.random.default_rng(r)
+        counts = np.zeros(27, np.int64)
+        counts[valid] = rng.integers(0, 5, len(valid))
+        seg = D.segments(r, counts)
+        assert sorted(seg) == D.peers(r)
+        off = 0
+        for p in D.peers(r):
+            o, n = seg[p]
+            assert o == off
+            assert n == sum(counts[d] for d in valid if D.peer(r, d) == p)
+            off += n
+
+
+class FakeCtx:
+    """Stands in for pm.DistContext in the CPU protocol test: records are
+    int64 (src rank, direction, k) triples packed as bytes."""
+
+    def __init__(self, rank, D, rng_key):
+        self.rank, self.D = rank, D
+        self.counts = {}
+        self.rng = np.random.default_rng(rng_key)
+        self.arrived = {}
+
+    def dist_plan(self, what, order):
+        cnt = np.zeros(27, np.int64)
+        for d in self.D.valid_dirs():
+            cnt[d] = self.rng.integers(0, 4)
+        self.counts[what] = (cnt, list(order))
+        return cnt
+
+    def dist_pack(self, what, buf):
+        import torch
+        cnt, order = self.counts[what]
+        recs = [(self.rank, d, k) for d in order for k in range(int(cnt[d]))]
+        if recs:
+            arr = torch.tensor(recs, dtype=torch.int64).flatten()
+            buf.view(torch.int64)[:arr.numel()] = arr
+
+    def dist_unpack(self, what, buf, n):
+        import torch
+        self.arrived[what] = (buf.view(torch.int64)[:3 * n].reshape(-1, 3).tolist()
+                              if n else [])
+
+    def dist_finish(self):
+        pass
+
+
+def _worker(rank, world, port, grid, out):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    D = Decomp(grid)
+    ctx = FakeCtx(rank, D, rng_key=(7, rank))
+    sim = DistSim(D, {rank: ctx}, TorchTransport(device=None), device="cpu")
+    from paper_1804_07598_b200 import pm
+    import paper_1804_07598_b200.pm as pmm
+    pmm.record_bytes = lambda what: 24  # 3 x int64 per synthetic record
+    sim._message_round(pm.PM_MSG_GHOST)
+    sent = {what: (c.tolist(), o) for what, (c, o) in ctx.counts.items()}
+    out.put((rank, sent, ctx.arrived[pm.PM_MSG_GHOST], sim.ghost_recv[rank]))
+    flag = sim._allreduce_max({rank: rank})
+    out.put(("flag", rank, flag))
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("grid", [(2, 1, 1), (1, 2, 1)])
+def test_message_protocol_gloo_world2(grid):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, grid, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res, flags = {}, {}
+    for _ in range(4):
+        item = q.get(timeout=120)
+        if item[0] == "flag":
+            flags[item[1]] = item[2]
+        else:
+            res[item[0]] = item[1:]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert flags == {0: 1, 1: 1}
+    D = Decomp(grid)
+    from paper_1804_07598_b200 import pm
+    for r in (0, 1):
+        q_ = 1 - r
+        sent_q, _, _ = res[q_]
+        cnt_q, order_q = sent_q[pm.PM_MSG_GHOST]
+        # what q sent to r, in q's packing order
+        expect = [[q_, d, k] for d in order_q if d in D.valid_dirs() and D.peer(q_, d) == r
+                  for k in range(cnt_q[d])]
+        _, arrived, recv_counts = res[r]
+        assert arrived == expect
+        assert recv_counts[q_] == len(expect)

@@ -1,0 +1,125 @@
+"""Multi-GPU path on ONE GPU (in-process loopback transport): the same global
+system run whole on one context and decomposed into P sub-domains must give
+identical neighbour sets (as gid pairs), the same forces (1e-4 of RMS; the
+pair sets are identical so only summation order differs) and, over a short
+run with rebuilds and migrations, the same trajectory (SURVEY §8(c)
+"Multi-GPU: rank-count independence", §4 T3)."""
+import numpy as np
+import pytest
+
+from paper_1804_07598_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1804_07598_b200 import build, dist, pm
+    build.build()
+    return pm, dist
+
+
+def single(pm, s):
+    c = pm.Context()
+    c.set_domain(s.lo, s.hi, s.periodic)
+    c.set_cutoff(2.5, 0.3)
+    c.set_lj(1.0, 1.0, 1.0, 0.0)
+    c.place(s.pos, s.vel, s.gid)
+    return c
+
+
+def decomposed(pm, dist, s, grid):
+    import torch
+    D = dist.Decomp(grid)
+    owner = dist.owner_of(s, D)
+    stream = torch.cuda.Stream()
+    members = {}
+    for r in range(D.size):
+        sub = s.subset(np.where(owner == r)[0])
+        members[r] = dist.make_member(sub, D, r, stream=stream)
+    sim = dist.DistSim(D, members, dist.LoopbackTransport(members), stream=stream)
+    return sim
+
+
+def owned_union(pm, sim):
+    parts = [ctx.owned_state() for ctx in sim.m.values()]
+    st = {k: np.concatenate([p[k] for p in parts]) for k in parts[0]}
+    return pm.sorted_by_gid(st)
+
+
+@pytest.mark.parametrize("grid", [(2, 1, 1), (2, 2, 1), (2, 2, 2), (3, 1, 2)])
+def test_decomposed_lists_and_forces_match_single(env, grid):
+    pm, dist = env
+    s = inputs.lj_lattice_system(18, 18, 18, jitter_key=(41,), vel_key=(141,))
+    ref = single(pm, s)
+    ref.build_verlet()
+    ref.compute_lj()
+    rst = pm.sorted_by_gid(ref.get_state())
+    rrp, rcol = ref.get_verlet()
+    rgid = ref.get_state()["gid"]
+    ref_rows = {int(g): set(rcol[rrp[i]:rrp[i + 1]].tolist()) for i, g in enumerate(rgid)}
+    sim = decomposed(pm, dist, s, grid)
+    sim.start()
+    got = owned_union(pm, sim)
+    assert np.array_equal(got["gid"], np.sort(s.gid))  # every particle owned exactly once
+    F, Fr = got["force"][:, :3].astype(np.float64), rst["force"][:, :3].astype(np.float64)
+    err = np.max(np.abs(F - Fr)) / np.sqrt(np.mean(Fr ** 2))
+    assert err <= 1e-4, err
+    # neighbour sets as gid sets, row by row (owned rows only)
+    for ctx in sim.m.values():
+        rp, col = ctx.get_verlet()
+        st = ctx.get_state()
+        kind = ctx.kind()
+        for i in range(len(st["gid"])):
+            if kind[i] & pm.GHOST_BIT:
+                assert rp[i + 1] == rp[i]
+                continue
+            assert set(col[rp[i]:rp[i + 1]].tolist()) == ref_rows[int(st["gid"][i])]
+    ref.close()
+    for ctx in sim.m.values():
+        ctx.close()
+
+
+@pytest.mark.parametrize("grid", [(2, 1, 1), (2, 2, 2)])
+def test_decomposed_trajectory_matches_single(env, grid):
+    """40 NVE steps with rebuilds, migration and ghost refresh: positions and
+    velocities agree with the single-context run (fp32, summation order only)."""
+    pm, dist = env
+    s = inputs.lj_lattice_system(18, 18, 18, jitter_key=(42,), vel_key=(142,))
+    ref = single(pm, s)
+    r = ref.step_vv(0.005, 40)
+    rst = pm.sorted_by_gid(ref.get_state())
+    sim = decomposed(pm, dist, s, grid)
+    sim.start()
+    reb = sim.run(40)
+    assert reb >= 2 and r["rebuilds"] >= 2
+    got = owned_union(pm, sim)
+    assert np.array_equal(got["gid"], np.sort(s.gid))
+    L = s.hi.astype(np.float64)
+    d = got["pos"][:, :3].astype(np.float64) - rst["pos"][:, :3]
+    d -= L * np.round(d / L)
+    assert np.max(np.abs(d)) < 1e-3
+    assert np.max(np.abs(got["vel"][:, :3] - rst["vel"][:, :3])) < 1e-2
+    th = sim.thermo()
+    th_ref = ref.thermo()
+    assert th["npairs"] == th_ref["npairs"]
+    assert th["ke"] == pytest.approx(th_ref["ke"], rel=1e-4)
+    assert th["pe_shift"] == pytest.approx(th_ref["pe_shift"], rel=1e-4)
+    ref.close()
+    for ctx in sim.m.values():
+        ctx.close()
+
+
+def test_decomposition_usage_errors(env):
+    pm, dist = env
+    s = inputs.lj_lattice_system(8, 8, 8, jitter_key=(43,))  # L = 8.6 < 2 * 2 r_v
+    c = pm.DistContext()
+    c.set_domain(s.lo, s.hi, s.periodic)
+    c.set_cutoff(2.5, 0.3)
+    with pytest.raises(pm.PMError) as e:
+        c.set_decomposition((2, 1, 1), (0, 0, 0))
+    assert e.value.code == -1
+    c.close()
