@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -461,13 +462,27 @@ pm_status run_steps(pm_ctx c, float dt, int64_t nsteps) {
       c->prof_force_launches += nsteps;
     }
   } else {
+    const bool prof = c->profiling;
+    if (prof) {
+      pm_status s = ensure_events(c, 2);
+      if (s) return s;
+    }
     for (int64_t k = 0; k < nsteps; ++k) {
       launch_step_begin(c->B, cudaGraphConditionalHandle{}, 0, c->stream);
       pm_status s = read_state(c);
       if (s) return s;
       if (c->st_h->abort) break;
       if (c->st_h->do_rebuild) enqueue_rebuild(c, c->stream, 1);
+      if (prof) CUDA_TRY(c, cudaEventRecord(c->ev_pool[0], c->stream));
       launch_lj_step(c->P, c->B, c->n, dt, c->stream);
+      if (prof) {
+        CUDA_TRY(c, cudaEventRecord(c->ev_pool[1], c->stream));
+        CUDA_TRY(c, cudaEventSynchronize(c->ev_pool[1]));
+        float ms = 0.f;
+        CUDA_TRY(c, cudaEventElapsedTime(&ms, c->ev_pool[0], c->ev_pool[1]));
+        c->prof_force_ms += ms;
+        c->prof_force_launches += 1;
+      }
     }
   }
   k_apply_pending<<<1, 1, 0, c->stream>>>(c->B.st);
@@ -485,7 +500,10 @@ pm_status pm_opts_default(pm_opts *o) {
   o->device = 0;
   o->cell_div = 1;
   o->nbr_cap = 0;
-  o->use_graphs = 1;
+  // PM_USE_GRAPHS=0 in the environment: plain launches (the profiling pass --
+  // ncu cannot see kernel nodes of graphs that contain conditional nodes)
+  const char *g = std::getenv("PM_USE_GRAPHS");
+  o->use_graphs = (g && g[0] == '0') ? 0 : 1;
   o->cuda_stream = nullptr;
   return PM_OK;
 }
