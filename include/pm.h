@@ -93,6 +93,11 @@ pm_status pm_set_cutoff(pm_ctx ctx, float r_cut, float skin);
  * (r_eff = max(r, r_min)), 0 the plain potential. */
 pm_status pm_set_lj(pm_ctx ctx, float epsilon, float sigma, float mass, float r_min);
 
+/* Velocity limit of reading R22 (clustered BASELINE.json configs[4]): after
+ * every kick, v <- v * min(1, vmax / |v|), so no particle drifts more than
+ * vmax * dt per step.  vmax = 0 (default) disables the limit. */
+pm_status pm_set_vlimit(pm_ctx ctx, float vmax);
+
 /* WCSPH parameters (Eqs. 1, 3-5; readings R15-R21):
  * smoothing length h (kernel support 2h), particle mass, rest density rho0,
  * EOS exponent gamma and constant b (Eq. 3), viscosity alpha, cbar and

@@ -26,7 +26,10 @@ __global__ void __launch_bounds__(256) k_cell_ids(Params P, Bufs B, int64_t n) {
   const int cur = st->cur_pv;
   float4 *__restrict__ pos = B.pos[cur];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i == 0) st->coinc_gid = -1;  // k_segsort (later on the stream) records coincidences
+  if (i == 0) {  // k_segsort (later on the stream) records coincidences / big cells
+    st->coinc_gid = -1;
+    st->n_big = 0;
+  }
   int c = -1;
   if (i < n) {
     float4 p = pos[i];
@@ -197,18 +200,54 @@ __global__ void __launch_bounds__(256) k_segsort(Bufs B, const int32_t *__restri
     if (dup) st->coinc_gid = (long long)B.gid[st->cur_id][v];
     return;
   }
-  for (int p = lane; p < m; p += 32) {
-    const int v = tmp[s + p];
-    const float4 pv = pos[v];
-    int r = 0;
-    bool dup = false;
-    for (int q = 0; q < m; ++q) {
-      const int w = tmp[s + q];
-      r += (w < v);
-      dup |= (w != v) && same_pos(pv, pos[w]);
+  // more than 32 members: defer to the block-level sort (k_segsort_big)
+  if (lane == 0) B.big_cells[atomicAdd(&st->n_big, 1)] = cell;
+}
+
+// Cells with more than 32 members (clustered inputs, up to ~3000): one block
+// per cell, bitonic sort of the storage indices in shared memory (<= 8192
+// members; beyond, rank by counting).  Coincident particles in such cells are
+// left to the force / density passes (PM_E_NONFINITE).
+constexpr int kBigSort = 8192;
+
+__global__ void __launch_bounds__(512) k_segsort_big(Bufs B, const int32_t *__restrict__ tmp) {
+  __shared__ int key[kBigSort];
+  State *st = B.st;
+  const int nbig = st->n_big;
+  for (int b = blockIdx.x; b < nbig; b += gridDim.x) {
+    const int cell = B.big_cells[b];
+    const int s = B.start[cell], m = B.start[cell + 1] - s;
+    if (m <= kBigSort) {
+      int n2 = 64;
+      while (n2 < m) n2 <<= 1;
+      for (int t = threadIdx.x; t < n2; t += blockDim.x) key[t] = (t < m) ? tmp[s + t] : 0x7fffffff;
+      __syncthreads();
+      for (int k = 2; k <= n2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          for (int t = threadIdx.x; t < n2; t += blockDim.x) {
+            const int u = t ^ j;
+            if (u > t) {
+              const int a = key[t], c = key[u];
+              const bool up = (t & k) == 0;
+              if ((a > c) == up) {
+                key[t] = c;
+                key[u] = a;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      }
+      for (int t = threadIdx.x; t < m; t += blockDim.x) B.perm[s + t] = key[t];
+      __syncthreads();
+    } else {
+      for (int p = threadIdx.x; p < m; p += blockDim.x) {
+        const int v = tmp[s + p];
+        int r = 0;
+        for (int q = 0; q < m; ++q) r += (tmp[s + q] < v);
+        B.perm[s + r] = v;
+      }
     }
-    B.perm[s + r] = v;
-    if (dup) st->coinc_gid = (long long)B.gid[st->cur_id][v];
   }
 }
 
@@ -268,6 +307,7 @@ void launch_sort_reorder(const Params &P, const Bufs &B, int64_t n, cudaStream_t
   int32_t *tmp = B.sorttmp;
   k_scatter<<<blocks_for(n, 256), 256, 0, s>>>(B, tmp, n);
   k_segsort<<<blocks_for((int64_t)P.grid.ncell * 32, 256), 256, 0, s>>>(B, tmp, P.grid.ncell);
+  k_segsort_big<<<148, 512, 0, s>>>(B, tmp);
   k_reorder<<<blocks_for(n, 256), 256, 0, s>>>(B, n);
 }
 

@@ -156,7 +156,7 @@ __device__ __forceinline__ Acc lj_force_of(const Params &P, const Bufs &B,
   const bool mi = __any_sync(0xffffffffu, active && near_periodic_face(P, xi));
   if (active) {
     const int cnt = B.cnt[i];
-    const int *nb = B.nbr + nbr_row_base(i, P.nbr_cap);
+    const int *nb = B.nbr + nbr_row_base(B, i);
     if (mi)
       lj_row<true, CAPPED, ENERGY>(P, pos, nb, cnt, xi, a);
     else
@@ -230,6 +230,22 @@ __device__ __forceinline__ bool moved_too_far(const Params &P, const float3 &x, 
   return dist2(dx, dy, dz) > P.half_skin2;
 }
 
+// v += k F, then (vmax > 0, reading R22) v <- v min(1, vmax / |v|).
+__device__ __forceinline__ void kick_limited(float4 &v, float k, const Acc &a, float vmax) {
+  v.x = fmaf(k, a.fx, v.x);
+  v.y = fmaf(k, a.fy, v.y);
+  v.z = fmaf(k, a.fz, v.z);
+  if (vmax > 0.f) {
+    const float s2 = v.x * v.x + v.y * v.y + v.z * v.z;
+    if (s2 > vmax * vmax) {
+      const float sc = vmax * rsqrtf(s2);
+      v.x *= sc;
+      v.y *= sc;
+      v.z *= sc;
+    }
+  }
+}
+
 // One fused velocity-Verlet step (pm_step_vv), mode read from the state:
 //  inner: F(x); v += dt F/m (2nd half-kick of this step + 1st of the next);
 //         x' = wrap(x + dt v); displacement test vs xref; -> alternate buffers
@@ -255,18 +271,20 @@ __global__ void __launch_bounds__(256) k_lj_step(Params P, Bufs B, int n, float 
     float4 v = B.vel[cp][i];
     const float im = P.lj.inv_mass;
     if (mode == kModeInner) {
-      const float k = dt * im;
-      v.x = fmaf(k, a.fx, v.x);
-      v.y = fmaf(k, a.fy, v.y);
-      v.z = fmaf(k, a.fz, v.z);
+      if (P.vmax > 0.f) {  // reading R22: limit after each of the two half kicks
+        kick_limited(v, 0.5f * dt * im, a, P.vmax);
+        kick_limited(v, 0.5f * dt * im, a, P.vmax);
+      } else {
+        const float k = dt * im;
+        v.x = fmaf(k, a.fx, v.x);
+        v.y = fmaf(k, a.fy, v.y);
+        v.z = fmaf(k, a.fz, v.z);
+      }
       const float3 xn = wrap3(P, fmaf(dt, v.x, xi.x), fmaf(dt, v.y, xi.y), fmaf(dt, v.z, xi.z));
       far = moved_too_far(P, xn, B.xref[i]);
       B.pos[cp ^ 1][i] = make_float4(xn.x, xn.y, xn.z, xi.w);
     } else {
-      const float k = 0.5f * dt * im;
-      v.x = fmaf(k, a.fx, v.x);
-      v.y = fmaf(k, a.fy, v.y);
-      v.z = fmaf(k, a.fz, v.z);
+      kick_limited(v, 0.5f * dt * im, a, P.vmax);
       B.pos[cp ^ 1][i] = xi;
       B.force[i] = make_float4(a.fx, a.fy, a.fz, 0.f);
     }
@@ -292,10 +310,8 @@ __global__ void __launch_bounds__(256) k_kick_drift(Params P, Bufs B, int n, flo
     const float4 f = B.force[i];
     float4 v = B.vel[cp][i];
     const float4 x = B.pos[cp][i];
-    const float k = 0.5f * dt * P.lj.inv_mass;
-    v.x = fmaf(k, f.x, v.x);
-    v.y = fmaf(k, f.y, v.y);
-    v.z = fmaf(k, f.z, v.z);
+    Acc fa = {f.x, f.y, f.z, 0.f, 0.f, 0};
+    kick_limited(v, 0.5f * dt * P.lj.inv_mass, fa, P.vmax);
     const float3 xn = wrap3(P, fmaf(dt, v.x, x.x), fmaf(dt, v.y, x.y), fmaf(dt, v.z, x.z));
     far = moved_too_far(P, xn, B.xref[i]);
     B.pos[cp ^ 1][i] = make_float4(xn.x, xn.y, xn.z, x.w);

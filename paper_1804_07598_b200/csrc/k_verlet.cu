@@ -121,7 +121,8 @@ __global__ void __launch_bounds__(256, 3) k_verlet(Params P, Bufs B, int n) {
   if (wbase >= n) return;  // whole warp out of range
   // rows: every particle on one GPU; owned particles only in a sub-domain
   const bool active = i < n && !(P.dist && (B.kind[st->cur_id][i] & kGhostBit));
-  const int cap = P.nbr_cap;
+  // capacity of this warp's slice (warp == slice: 256-thread blocks)
+  const int cap = (i - lane < n) ? nbr_row_cap(B, i - lane) : 0;
   const int nx = P.grid.n[0], ny = P.grid.n[1], nz = P.grid.n[2];
   const float4 *__restrict__ pos = B.pos[st->cur_pv];
   const float4 xi = active ? pos[i] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(256, 3) k_verlet(Params P, Bufs B, int n) {
                       (P.box.per[1] && !P.grid.wrap[1] ? 2 : 0) |
                       (P.box.per[2] && !P.grid.wrap[2] ? 4 : 0);
   const int row_id = active ? cell / nx : 0x7fffffff;  // (cy, cz) row of my cell
-  int *__restrict__ row = B.nbr + nbr_row_base(i, cap);
+  int *__restrict__ row = B.nbr + nbr_row_base(B, i - lane) + lane;
   int k = 0;
   const float INF = __int_as_float(0x7f800000);
   const float Lx = P.box.L[0], Ly = P.box.L[1], Lz = P.box.L[2];
@@ -223,7 +224,7 @@ __global__ void __launch_bounds__(256, 3) k_verlet(Params P, Bufs B, int n) {
   if (lane == 0 && ksum > 0) {
     atomicMax(&st->max_row, kmax);
     atomicAdd(reinterpret_cast<unsigned long long *>(&st->nnz), (unsigned long long)ksum);
-    if (kmax > cap) {
+    if (kmax > cap) {  // the host re-lays the slices out from the exact counts
       atomicMax(&st->overflow_need, kmax);
       raise_error(st, -9 /*PM_E_CAPACITY*/, -1);
     }
@@ -237,13 +238,13 @@ __global__ void k_reset_build_stats(State *st) {
 }
 
 // CSR export of the list for the getters: col_gid[row_ptr[i] + k] = gid(nbr).
-__global__ void __launch_bounds__(256) k_verlet_export(Bufs B, int n, int cap,
+__global__ void __launch_bounds__(256) k_verlet_export(Bufs B, int n,
                                                       const int64_t *__restrict__ row_ptr,
                                                       int64_t *__restrict__ col_gid) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int64_t *gid = B.gid[B.st->cur_id];
-  const int *nb = B.nbr + nbr_row_base(i, cap);
+  const int *nb = B.nbr + nbr_row_base(B, i);
   const int c = B.cnt[i];
   for (int k = 0; k < c; ++k) col_gid[row_ptr[i] + k] = gid[nb[k << 5]];
 }
@@ -255,10 +256,10 @@ void launch_verlet(const Params &P, const Bufs &B, int64_t n, cudaStream_t s) {
   if (n > 0) k_verlet<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, B, (int)n);
 }
 
-void launch_verlet_export(const Bufs &B, int64_t n, int cap, const int64_t *row_ptr,
-                          int64_t *col_gid, cudaStream_t s) {
+void launch_verlet_export(const Bufs &B, int64_t n, const int64_t *row_ptr, int64_t *col_gid,
+                          cudaStream_t s) {
   if (n > 0)
-    k_verlet_export<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(B, (int)n, cap, row_ptr, col_gid);
+    k_verlet_export<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(B, (int)n, row_ptr, col_gid);
 }
 
 }  // namespace pm

@@ -43,8 +43,10 @@ struct pm_ctx_s {
   int64_t pcap = 0;       // particle capacity of the buffers
   int64_t ncell_cap = 0;  // cells allocated
   int64_t ntile_cap = 0;
-  int64_t nbr_rows = 0;   // rows (multiple of 32) the neighbour array holds
-  int nbr_cap = 0;        // slots per row
+  int64_t nbr_ints = 0;   // ints allocated for the neighbour array
+  int64_t slice_cap = 0;  // entries allocated for slice_off
+  int64_t layout_pcap = -1;  // particle capacity the slice layout covers
+  int nbr_cap = 0;        // widest slice of the current layout
 
   bool have_domain = false, have_cutoff = false, have_lj = false, have_sph = false;
   float r_cut = 0.f, skin = 0.f, rv = 0.f;
@@ -237,7 +239,7 @@ pm_status ensure_particles(pm_ctx c, int64_t n, int64_t keep = 0) {
   CUDA_TRY(c, cudaMemsetAsync(B.force, 0, sizeof(float4) * cap, c->stream));
   CUDA_TRY(c, cudaMemsetAsync(B.cnt, 0, sizeof(int32_t) * cap, c->stream));
   c->pcap = cap;
-  c->nbr_rows = 0;  // neighbour array must be regrown for the new row count
+  // the slice layout must be redone for the new capacity (ensure_layout)
   destroy_graph(c);
   return PM_OK;
 }
@@ -247,6 +249,7 @@ pm_status ensure_cells(pm_ctx c) {
   if (ncell > c->ncell_cap) {
     CUDA_TRY(c, dalloc(&c->B.count, ncell));
     CUDA_TRY(c, dalloc(&c->B.start, ncell + 1));
+    CUDA_TRY(c, dalloc(&c->B.big_cells, ncell));
     c->ncell_cap = ncell;
     destroy_graph(c);
   }
@@ -269,17 +272,81 @@ int auto_nbr_cap(pm_ctx c) {
   return (cap + 3) & ~3;
 }
 
-pm_status ensure_nbr(pm_ctx c, int cap) {
-  cap = (cap + 3) & ~3;
-  const int64_t rows = ((c->n + 31) / 32) * 32;
-  if (cap == c->nbr_cap && rows <= c->nbr_rows && c->B.nbr) return PM_OK;
-  const int64_t alloc_rows = ((c->pcap + 31) / 32) * 32;
-  CUDA_TRY(c, dalloc(&c->B.nbr, alloc_rows * (int64_t)cap));
-  c->nbr_rows = alloc_rows;
-  c->nbr_cap = cap;
-  c->P.nbr_cap = cap;
-  destroy_graph(c);
+// Upload a SELL slice layout (widths per 32-row slice, multiples of 4) over all
+// pcap/32 slices and make sure the neighbour array can hold it.
+pm_status upload_layout(pm_ctx c, const std::vector<int64_t> &width) {
+  const int64_t ns = (int64_t)width.size();
+  std::vector<int64_t> off((size_t)ns + 1);
+  off[0] = 0;
+  int wmax = 0;
+  for (int64_t s = 0; s < ns; ++s) {
+    off[(size_t)s + 1] = off[(size_t)s] + width[(size_t)s];
+    wmax = std::max<int>(wmax, (int)width[(size_t)s]);
+  }
+  if (ns + 1 > c->slice_cap) {
+    CUDA_TRY(c, dalloc(&c->B.slice_off, ns + 1));
+    c->slice_cap = ns + 1;
+    destroy_graph(c);
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(c->B.slice_off, off.data(), sizeof(int64_t) * (ns + 1),
+                              cudaMemcpyHostToDevice, c->stream));
+  const int64_t ints = off[(size_t)ns] * 32;
+  if (ints > c->nbr_ints || !c->B.nbr) {
+    CUDA_TRY(c, dalloc(&c->B.nbr, std::max<int64_t>(ints, 32)));
+    c->nbr_ints = std::max<int64_t>(ints, 32);
+    destroy_graph(c);
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));  // `off` is a host temporary
+  c->nbr_cap = wmax;
+  c->P.nbr_cap = wmax;
+  c->layout_pcap = c->pcap;
   return PM_OK;
+}
+
+// Equal widths for every slice (uniform liquids; first build).
+pm_status layout_uniform(pm_ctx c, int cap) {
+  cap = std::max(4, (cap + 3) & ~3);
+  const int64_t ns = (c->pcap + 31) / 32;
+  return upload_layout(c, std::vector<int64_t>((size_t)ns, cap));
+}
+
+// Widths from the exact row counts of the last (overflowing) build: per
+// slice 1.2 x its longest row + 4, so clustered inputs (rows from 0 to ~12k)
+// do not pay the global maximum on every row.
+pm_status layout_from_counts(pm_ctx c) {
+  const int64_t n = c->n, ns = (c->pcap + 31) / 32;
+  std::vector<int32_t> cnt((size_t)std::max<int64_t>(n, 1));
+  if (n > 0)
+    CUDA_TRY(c, cudaMemcpyAsync(cnt.data(), c->B.cnt, 4 * n, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  const int64_t nused = (n + 31) / 32;
+  std::vector<int64_t> smax((size_t)std::max<int64_t>(nused, 1), 0);
+  for (int64_t s = 0; s < nused; ++s) {
+    int m = 0;
+    for (int64_t i = s * 32; i < std::min<int64_t>(n, s * 32 + 32); ++i) m = std::max(m, cnt[(size_t)i]);
+    smax[(size_t)s] = m;
+  }
+  // particles drift along the cell order between builds: take the maximum
+  // over the neighbouring slices too, plus a 25% + 8 margin
+  std::vector<int64_t> w((size_t)ns, 0);
+  int64_t wmax = 4;
+  for (int64_t s = 0; s < nused; ++s) {
+    int64_t m = 0;
+    for (int64_t t = std::max<int64_t>(0, s - 2); t <= std::min<int64_t>(nused - 1, s + 2); ++t)
+      m = std::max(m, smax[(size_t)t]);
+    int64_t wi = (int64_t)std::ceil(1.25 * (double)m) + 8;
+    wi = (wi + 3) & ~(int64_t)3;
+    w[(size_t)s] = wi;
+    wmax = std::max(wmax, wi);
+  }
+  for (int64_t s = (n + 31) / 32; s < ns; ++s) w[(size_t)s] = wmax;  // rows not in use
+  return upload_layout(c, w);
+}
+
+pm_status ensure_layout(pm_ctx c) {
+  if (c->B.slice_off && c->layout_pcap == c->pcap) return PM_OK;
+  int cap = c->nbr_cap ? c->nbr_cap : (c->nbr_cap_opt ? c->nbr_cap_opt : auto_nbr_cap(c));
+  return layout_uniform(c, cap);
 }
 
 pm_status setup_grid(pm_ctx c) {
@@ -347,16 +414,15 @@ void enqueue_rebuild(pm_ctx c, cudaStream_t s, int count_rebuild) {
 }
 
 pm_status build_list(pm_ctx c) {
-  pm_status s = ensure_nbr(c, c->nbr_cap ? c->nbr_cap : (c->nbr_cap_opt ? c->nbr_cap_opt : auto_nbr_cap(c)));
+  pm_status s = ensure_layout(c);
   if (s) return s;
   enqueue_rebuild(c, c->stream, 0);
   s = sync_check(c, "pm_build_verlet");
   if (s == PM_E_CAPACITY) {
-    const int need = c->st_h->overflow_need;
     c->sticky = 0;
     c->err.clear();
     k_clear_abort<<<1, 1, 0, c->stream>>>(c->B.st);
-    s = ensure_nbr(c, (int)std::ceil(need * 1.2) + 4);
+    s = layout_from_counts(c);  // the failed pass stored every row's exact count
     if (s) return s;
     launch_verlet(c->P, c->B, c->n, c->stream);  // cells are already built
     s = sync_check(c, "pm_build_verlet (retry)");
@@ -562,8 +628,8 @@ void pm_destroy(pm_ctx c) {
     cudaFree(B.gid[b]);
     cudaFree(B.kind[b]);
   }
-  void *ptrs[] = {B.xref, B.force, B.rhoP, B.cell_of, B.slot, B.count, B.start,
-                  B.perm, B.sorttmp, B.scan_tmp, B.nbr, B.cnt, B.st};
+  void *ptrs[] = {B.xref, B.force, B.rhoP, B.cell_of, B.slot, B.count, B.start, B.perm,
+                  B.sorttmp, B.scan_tmp, B.nbr, B.cnt, B.st, B.slice_off, B.big_cells};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   void *dptrs[] = {c->d_mask, c->d_blk, c->d_order, c->d_dirbase, c->d_list,
@@ -633,6 +699,14 @@ pm_status pm_set_lj(pm_ctx c, float eps, float sigma, float mass, float r_min) {
   c->lj_sigma = sigma;
   c->have_lj = true;
   c->forces_valid = false;
+  destroy_graph(c);
+  return PM_OK;
+}
+
+pm_status pm_set_vlimit(pm_ctx c, float vmax) {
+  if (!c) return PM_E_INVAL;
+  if (!(vmax >= 0.f)) return set_err(c, PM_E_INVAL, "pm_set_vlimit: vmax must be >= 0");
+  c->P.vmax = vmax;
   destroy_graph(c);
   return PM_OK;
 }
@@ -784,7 +858,9 @@ pm_status pm_step_vv(pm_ctx c, float dt, int64_t nsteps, pm_run_stats *out) {
   }
   launch_kick_drift(c->P, c->B, c->n, dt, c->stream);
   int64_t done = 0;
-  for (int attempt = 0; attempt < 4; ++attempt) {
+  // every resume makes progress (the resumed rebuild sees the sorted order the
+  // new widths were computed from), so nsteps + 2 attempts always suffice
+  for (int64_t attempt = 0; attempt < nsteps + 2; ++attempt) {
     s = run_steps(c, dt, nsteps - done);
     if (s) return s;
     s = read_state(c);
@@ -792,10 +868,9 @@ pm_status pm_step_vv(pm_ctx c, float dt, int64_t nsteps, pm_run_stats *out) {
     done += c->st_h->steps_done;
     if (c->st_h->abort == PM_E_CAPACITY && done < nsteps) {
       // grow the neighbour capacity and resume at the aborted step's rebuild
-      const int need = c->st_h->overflow_need;
       k_clear_abort<<<1, 1, 0, c->stream>>>(c->B.st);
       k_force_rebuild<<<1, 1, 0, c->stream>>>(c->B.st);
-      s = ensure_nbr(c, (int)std::ceil(need * 1.2) + 4);
+      s = layout_from_counts(c);  // exact counts of the aborted build
       if (s) return s;
       continue;
     }
@@ -870,7 +945,7 @@ pm_status pm_get_verlet(pm_ctx c, int64_t *row_ptr, int64_t *col_gid) {
   CUDA_TRY(c, cudaMalloc((void **)&d_rp, 8 * (n + 1)));
   CUDA_TRY(c, cudaMalloc((void **)&d_col, 8 * nnz));
   CUDA_TRY(c, cudaMemcpyAsync(d_rp, row_ptr, 8 * (n + 1), cudaMemcpyHostToDevice, c->stream));
-  launch_verlet_export(c->B, n, c->nbr_cap, d_rp, d_col, c->stream);
+  launch_verlet_export(c->B, n, d_rp, d_col, c->stream);
   CUDA_TRY(c, cudaMemcpyAsync(col_gid, d_col, 8 * nnz, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   cudaFree(d_rp);

@@ -83,6 +83,7 @@ struct Params {
                     // periodic face cannot have a list partner across it
   int nbr_cap;      // slots per row (multiple of 4)
   int dist;         // 1: sub-domain context (ghosts present, skip them as rows)
+  float vmax;       // velocity limit (reading R22), 0 = off
 };
 
 // Device buffers (pointers fixed between reallocations; captured in graphs).
@@ -103,7 +104,9 @@ struct Bufs {
   int32_t *invperm;    // [n] storage index -> sorted k (multi-GPU remap)
   int32_t *sorttmp;    // [n] scatter target before the per-cell sort
   int32_t *scan_tmp;   // block sums for the scan
-  int32_t *nbr;        // SELL-32 neighbour slots, int4-interleaved
+  int32_t *nbr;        // SELL-32 neighbour slots (see nbr_row_base)
+  int64_t *slice_off;  // [nslices + 1] slice offsets in 128-byte lines
+  int32_t *big_cells;  // cells with > 32 particles (block-level sort)
   int32_t *cnt;        // [n] neighbour row lengths
   struct State *st;    // device-resident state
 };
@@ -125,6 +128,7 @@ struct State {
   long long nnz;        // entries of the last build
   long long steps_done; // force-step kernels completed (not aborted)
   int do_rebuild;       // rebuild decision of the current step (non-graph path)
+  int n_big;            // number of entries in Bufs::big_cells
   long long coinc_gid;  // a particle with a coincident partner (-1: none), set
                         // by the cell sort, raised as PM_E_COINCIDENT by the
                         // Verlet build (the cell list itself is well defined)
@@ -200,11 +204,18 @@ PM_DEV float fast_rsqrt(float x) {
   return r;
 }
 
-// SELL-32 neighbour slot layout: row i = 32 * slice + lane; entry k of the
-// row lives at nbr[(slice * cap + k) * 32 + lane] -- a warp reading entry k
-// of its 32 rows touches one contiguous 128-byte line.
-PM_DEV int64_t nbr_row_base(int i, int cap) {
-  return (int64_t)(i >> 5) * cap * 32 + (i & 31);
+// SELL-32 neighbour slot layout with per-slice widths: row i = 32 * slice +
+// lane; entry k of the row lives at nbr[(slice_off[slice] + k) * 32 + lane]
+// (a warp reading entry k of its 32 rows touches one contiguous 128-byte
+// line); the slice's capacity is slice_off[slice + 1] - slice_off[slice].
+// Uniform liquids get equal widths; clustered inputs (rows from 0 to ~12k
+// entries) get widths from the exact counts of the previous build.
+PM_DEV int64_t nbr_row_base(const Bufs &B, int i) {
+  return B.slice_off[i >> 5] * 32 + (i & 31);
+}
+
+PM_DEV int nbr_row_cap(const Bufs &B, int i) {
+  return (int)(B.slice_off[(i >> 5) + 1] - B.slice_off[i >> 5]);
 }
 
 PM_DEV void raise_error(State *st, int code, long long gid) {
@@ -231,8 +242,8 @@ void launch_step_begin(const Bufs &B, cudaGraphConditionalHandle h, int use_hand
 void launch_ke(const Params &P, const Bufs &B, int64_t n, cudaStream_t s);
 void launch_sph_density(const Params &P, const Bufs &B, int64_t n, cudaStream_t s);
 void launch_sph_forces(const Params &P, const Bufs &B, int64_t n, cudaStream_t s);
-void launch_verlet_export(const Bufs &B, int64_t n, int cap, const int64_t *row_ptr,
-                          int64_t *col_gid, cudaStream_t s);
+void launch_verlet_export(const Bufs &B, int64_t n, const int64_t *row_ptr, int64_t *col_gid,
+                          cudaStream_t s);
 void launch_lj_step_mode(const Params &P, const Bufs &B, int64_t n, float dt, int mode,
                          cudaStream_t s);
 int dist_record_bytes(int what);

@@ -68,6 +68,7 @@ def lib(path: str = LIB_PATH):
         "pm_set_domain": (st, [vp, vp, vp, vp]),
         "pm_set_cutoff": (st, [vp, C.c_float, C.c_float]),
         "pm_set_lj": (st, [vp, C.c_float, C.c_float, C.c_float, C.c_float]),
+        "pm_set_vlimit": (st, [vp, C.c_float]),
         "pm_set_sph": (st, [vp, C.POINTER(SPHParams)]),
         "pm_place": (st, [vp, C.c_int64, vp, vp, vp, vp, C.c_int32]),
         "pm_build_cells": (st, [vp]),
@@ -173,6 +174,9 @@ class Context:
 
     def set_lj(self, epsilon=1.0, sigma=1.0, mass=1.0, r_min=0.0):
         self._check(self.L.pm_set_lj(self.h, epsilon, sigma, mass, r_min))
+
+    def set_vlimit(self, vmax):
+        self._check(self.L.pm_set_vlimit(self.h, vmax))
 
     def set_sph(self, p: dict):
         s = SPHParams(h=p["h"], mass=p["mass"], rho0=p["rho0"], gamma=p["gamma"], b=p["b"],

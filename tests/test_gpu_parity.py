@@ -231,6 +231,64 @@ def test_capped_lj_parity(pm, orc):
     c.close()
 
 
+# ---------------------------------------------------------------- clustered (cfg5)
+@pytest.fixture(scope="module")
+def clustered():
+    """BJ configs[4] at its full local density: 4 of the 64 Gaussian clusters
+    (131,072 particles each, sigma_c = 4, mean density 0.5): cells of ~3000
+    particles (block-level sort), rows of up to ~12k entries (per-slice list
+    widths), capped LJ (reading R22)."""
+    return inputs.cfg5(n_clusters=4)
+
+
+def test_clustered_cells_lists_forces(pm, orc, clustered):
+    s = clustered
+    c = make_ctx(pm, s, r_min=0.8)
+    c.build_cells()
+    g = c.get_cells()
+    ref = orc.cell_list(s.pos, s.lo, s.hi, s.periodic, rv=rv32(2.5, 0.3))
+    assert ref["count"].max() > 1000  # big cells exercised
+    assert np.array_equal(g["cell_of"], ref["cell_of"])
+    assert np.array_equal(g["start"], ref["start"])
+    assert np.array_equal(g["perm"], ref["perm"])
+    c.build_verlet()
+    c.compute_lj()
+    rp, col = c.get_verlet()
+    st = c.get_state()
+    lens = np.diff(rp)
+    assert lens.max() > 4000 and lens.min() < 50  # strongly non-uniform rows
+    # sample rows across the whole length distribution (dense cores included)
+    order = np.argsort(lens)
+    pick = order[np.linspace(0, len(order) - 1, 48).astype(int)]
+    inv = idx_of_gid(s)
+    rows_storage = inv[st["gid"][pick]]
+    rrp, rcols, _ = orc.verlet_rows(s.pos, s.lo, s.hi, s.periodic, rv32(2.5, 0.3),
+                                    rows=rows_storage, want_shift=False)
+    sub_rp = np.concatenate([[0], np.cumsum(rp[pick + 1] - rp[pick])])
+    sub_col = np.concatenate([col[rp[i]:rp[i + 1]] for i in pick])
+    bad = _row_sets_equal(sub_rp, sub_col, st["gid"][pick], rrp, rcols, s.gid)
+    assert bad < 0, f"row {bad} differs"
+    fr = orc.lj_rows(s.pos, s.lo, s.hi, s.periodic, rc=2.5, r_min=0.8, rows=rows_storage)
+    assert orc.normalized_max_err(st["force"][pick, :3], fr["F"]) <= TOL
+    c.close()
+
+
+def test_clustered_short_run_with_vlimit(pm, clustered):
+    """Reading R22 dynamics: capped LJ + velocity limit (skin/2)/dt; runs with a
+    rebuild (incl. relayout of the list widths) nearly every step."""
+    s = clustered
+    c = make_ctx(pm, s, r_min=0.8)
+    c.set_vlimit(0.15 / 0.005)
+    r = c.step_vv(0.005, 6)
+    assert r["steps"] == 6 and r["rebuilds"] >= 3
+    st = c.get_state()
+    assert np.all(np.isfinite(st["pos"])) and np.all(np.isfinite(st["vel"]))
+    v = np.linalg.norm(st["vel"][:, :3], axis=1)
+    assert v.max() <= 30.0 * (1 + 1e-5)
+    assert np.array_equal(np.sort(st["gid"]), np.sort(s.gid))
+    c.close()
+
+
 # ---------------------------------------------------------------- VV / NVE
 def test_vv_short_trajectory_vs_oracle(pm, orc):
     """Positions after 50 fp32 steps within 1e-3 sigma of the fp64 oracle
