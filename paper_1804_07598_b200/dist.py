@@ -101,14 +101,28 @@ class Decomp:
 class TorchTransport:
     """torch.distributed point-to-point (NCCL on GPUs; gloo on CPU)."""
 
-    def __init__(self, device=None):
+    def __init__(self, device=None, stage_host=False):
         import torch
         import torch.distributed as dist
         self.torch, self.dist = torch, dist
         self.device = device
+        # gloo between ranks that share a GPU (tests): device buffers go through
+        # host copies; the library kernels never wait on another rank
+        self.stage_host = stage_host
 
     def exchange(self, sends, recvs):
         """sends/recvs: {peer: tensor} (uint8 or int64); zero-size skipped."""
+        if self.stage_host:
+            hs = {p: t.cpu() for p, t in sends.items()}
+            hr = {p: self.torch.empty(t.shape, dtype=t.dtype) for p, t in recvs.items()}
+            self._exchange(hs, hr)
+            for p, t in recvs.items():
+                if t.numel() > 0:
+                    t.copy_(hr[p])
+            return
+        self._exchange(sends, recvs)
+
+    def _exchange(self, sends, recvs):
         ops = []
         P2P, dist = self.dist.P2POp, self.dist
         for p in sorted(set(sends) | set(recvs)):
@@ -371,7 +385,9 @@ def _grid_for(n):
 
 def bench_main(args):
     """bench.py --gpus N under torchrun: BJ configs[2] weak scaling, one
-    128^3 lattice block (2,097,152 particles) per GPU, NCCL transport."""
+    128^3 lattice block (2,097,152 particles) per GPU, NCCL transport.
+    PM_DIST_BACKEND=gloo (tests only): ranks may share a GPU, messages are
+    staged through host memory.  PM_CFG3_BLOCK=m: m^3 particles per rank."""
     import torch
     import torch.distributed as tdist
     from . import build as pmbuild, inputs
@@ -379,45 +395,89 @@ def bench_main(args):
     ws = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ["RANK"])
     local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    backend = os.environ.get("PM_DIST_BACKEND", "nccl")
+    m = int(os.environ.get("PM_CFG3_BLOCK", "128"))
+    dev = local % torch.cuda.device_count()
+    torch.cuda.set_device(dev)
+    if backend == "nccl":
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        tr = TorchTransport(device=torch.device("cuda", dev))
+        red_dev = "cuda"
+    else:
+        tdist.init_process_group("gloo")
+        tr = TorchTransport(device=None, stage_host=True)
+        red_dev = "cpu"
     D = Decomp(_grid_for(ws))
-    s = inputs.cfg3_block(*D.coord(rank), grid=D.grid)
+    s = inputs.cfg3_block(*D.coord(rank), grid=D.grid, m=m)
     stream = torch.cuda.Stream()
-    ctx = make_member(s, D, rank, device=local, stream=stream)
-    sim = DistSim(D, {rank: ctx}, TorchTransport(device=torch.device("cuda", local)),
-                  stream=stream)
+
+    def max_ms(ms):
+        t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident run (value)
+    ctx = make_member(s, D, rank, device=dev, stream=stream)
+    sim = DistSim(D, {rank: ctx}, tr, stream=stream)
     sim.start()
     sim.run(args.warmup)
     torch.cuda.synchronize()
     tdist.barrier()
+    clocks = None
+    if rank == 0:
+        from bench import ClockSampler  # noqa: E402
+        clocks = ClockSampler(dev)
+        clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     reb = sim.run(args.steps)
     e1.record(stream)
     torch.cuda.synchronize()
     tdist.barrier()
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-    ms = float(t.item())
-    n_tot = torch.tensor([ctx.count()["n_owned"]], dtype=torch.int64, device="cuda")
+    clk = clocks.stop() if clocks else None
+    ms = max_ms(e0.elapsed_time(e1))
+    n_tot = torch.tensor([ctx.count()["n_owned"]], dtype=torch.int64, device=red_dev)
     tdist.all_reduce(n_tot)
+    n = int(n_tot.item())
+    ctx.close()
+    # ---- end to end: pinned host state in, K steps, owned state out
+    pos_h = torch.from_numpy(s.pos).pin_memory()
+    vel_h = torch.from_numpy(s.vel).pin_memory()
+    gid_h = torch.from_numpy(s.gid).pin_memory()
+    ctx = make_member(s, D, rank, device=dev, stream=stream)
+    sim = DistSim(D, {rank: ctx}, tr, stream=stream)
+    torch.cuda.synchronize()
+    tdist.barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    ctx.place(pos_h, vel_h, gid_h)
+    with torch.cuda.stream(stream):
+        sim.start()
+        sim.run(args.steps)
+    out = ctx.owned_state()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    tdist.barrier()
+    e2e_ms = max_ms(t0.elapsed_time(t1))
+    ctx.close()
     if rank == 0:
         from bench import METRIC, UNIT  # noqa: E402
-        n = int(n_tot.item())
+        h2d = s.n * (16 + 16 + 8)
+        d2h = int(out["pos"].nbytes + out["vel"].nbytes)
         line = {"metric": METRIC, "value": n * args.steps / (ms * 1e-3), "unit": UNIT,
                 "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": "cfg3 (BJ configs[2]): LJ fluid, 2,097,152 particles "
-                                       "per GPU (SC 128^3 block, rho=0.8), cuboid "
-                                       f"decomposition {D.grid}, ghost width r_cut+skin",
-                           "n_particles": n, "parallelism": f"spatial {D.grid}",
-                           "rebuilds": reb, "l2": "inputs larger than L2"},
+                "config": {"workload": f"cfg3 (BJ configs[2]): LJ fluid, {m**3:,} particles per "
+                                       f"GPU (SC {m}^3 block, rho=0.8), cuboid decomposition "
+                                       f"{D.grid}, ghost width r_cut+skin, NVE",
+                           "n_particles": n, "parallelism": f"spatial {D.grid} ({backend})",
+                           "rebuilds": reb, "l2": "inputs larger than L2 (Verlet lists)"},
                 "roofline": None, "cpu_baseline": None,
-                "e2e": None, "gpu_launches": None, "clocks": None}
+                "e2e": {"value": n * args.steps / (e2e_ms * 1e-3), "unit": UNIT,
+                        "h2d_bytes_per_step": h2d * ws / args.steps,
+                        "d2h_bytes_per_step": d2h * ws / args.steps},
+                "gpu_launches": None, "clocks": clk}
         print(json.dumps(line), flush=True)
-    ctx.close()
     tdist.destroy_process_group()
     return 0

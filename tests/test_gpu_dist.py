@@ -123,3 +123,30 @@ def test_decomposition_usage_errors(env):
         c.set_decomposition((2, 1, 1), (0, 0, 0))
     assert e.value.code == -1
     c.close()
+
+
+def test_bench_torchrun_two_ranks_share_one_gpu(env, tmp_path):
+    """The N>1 bench path end to end under torchrun (2 ranks, gloo with host
+    staging so both ranks can share the single GPU; no kernel ever waits on
+    another rank): one JSON line with the whole-job value."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env_ = dict(os.environ, PM_DIST_BACKEND="gloo", PM_CFG3_BLOCK="32")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "12", "--warmup", "3"]
+    r = subprocess.run(cmd, capture_output=True, text=True, env=env_, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    b = json.loads(lines[0])
+    assert b["n_gpus"] == 2 and b["config"]["n_particles"] == 2 * 32 ** 3
+    assert b["value"] > 0 and b["e2e"]["value"] > 0
