@@ -97,39 +97,63 @@ __global__ void __launch_bounds__(kDirBlock) k_dist_count(const uint32_t *__rest
   if (threadIdx.x < 27) blk_counts[blockIdx.x * 27 + threadIdx.x] = cnt[threadIdx.x];
 }
 
-// pass 2: per-direction exclusive scan over blocks; direction bases in the
-// caller's packing order (order[0..25], then direction 13 last); totals.
-__global__ void k_dist_scan(int *__restrict__ blk_counts, int nblk, const int *__restrict__ order,
-                            int *__restrict__ dir_base, long long *__restrict__ totals) {
-  __shared__ long long tot[27];
-  const int d = threadIdx.x;
-  if (d < 27) {
-    long long acc = 0;
-    for (int b = 0; b < nblk; ++b) {
-      const int c = blk_counts[b * 27 + d];
-      blk_counts[b * 27 + d] = (int)acc;
-      acc += c;
+// pass 2: per-direction exclusive scan over blocks (one 1024-thread block per
+// direction, block-wide scan of the column); totals per direction.
+__global__ void __launch_bounds__(1024) k_dist_scan(int *__restrict__ blk_counts, int nblk,
+                                                    long long *__restrict__ totals) {
+  __shared__ int wsum[32];
+  const int d = blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int carry = 0;
+  for (int b0 = 0; b0 < nblk; b0 += 1024) {
+    const int b = b0 + threadIdx.x;
+    const int c = (b < nblk) ? blk_counts[b * 27 + d] : 0;
+    int x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
-    tot[d] = acc;
-    totals[d] = acc;
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int t = wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += y;
+      }
+      wsum[lane] = t;  // inclusive over warps
+    }
+    __syncthreads();
+    const int excl = carry + (w ? wsum[w - 1] : 0) + x - c;
+    if (b < nblk) blk_counts[b * 27 + d] = excl;
+    carry += wsum[31];
+    __syncthreads();
   }
-  __syncthreads();
+  if (threadIdx.x == 0) totals[d] = carry;
+}
+
+// pass 3: stable write of particle indices into the per-direction lists
+// direction bases in the caller's packing order (order[0..25], then 13 last)
+__global__ void __launch_bounds__(kDirBlock) k_dist_fill(const uint32_t *__restrict__ mask, int n,
+                                                         const int *__restrict__ blk_off,
+                                                         const long long *__restrict__ totals,
+                                                         const int *__restrict__ order,
+                                                         int *__restrict__ dir_base_out,
+                                                         int *__restrict__ list) {
+  __shared__ int wsum[27][kDirBlock / 32];
+  __shared__ int dir_base[27];
   if (threadIdx.x == 0) {
     long long base = 0;
     for (int k = 0; k < 26; ++k) {
       dir_base[order[k]] = (int)base;
-      base += tot[order[k]];
+      base += totals[order[k]];
     }
     dir_base[13] = (int)base;
+    if (blockIdx.x == 0)
+      for (int k = 0; k < 27; ++k) dir_base_out[k] = dir_base[k];
   }
-}
-
-// pass 3: stable write of particle indices into the per-direction lists
-__global__ void __launch_bounds__(kDirBlock) k_dist_fill(const uint32_t *__restrict__ mask, int n,
-                                                         const int *__restrict__ blk_off,
-                                                         const int *__restrict__ dir_base,
-                                                         int *__restrict__ list) {
-  __shared__ int wsum[27][kDirBlock / 32];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t m = (i < n) ? mask[i] : 0u;
@@ -263,8 +287,8 @@ void launch_dist_plan(const Params &P, const Bufs &B, const Dist &D, int n_owned
   const unsigned g = nb(n_owned > 0 ? n_owned : 1, kDirBlock);
   if (n_owned > 0) k_dist_mark<<<g, kDirBlock, 0, s>>>(P, B, D, n_owned, what, mask);
   k_dist_count<<<g, kDirBlock, 0, s>>>(mask, n_owned, blk_counts);
-  k_dist_scan<<<1, 32, 0, s>>>(blk_counts, (int)g, order, dir_base, totals);
-  k_dist_fill<<<g, kDirBlock, 0, s>>>(mask, n_owned, blk_counts, dir_base, list);
+  k_dist_scan<<<27, 1024, 0, s>>>(blk_counts, (int)g, totals);
+  k_dist_fill<<<g, kDirBlock, 0, s>>>(mask, n_owned, blk_counts, totals, order, dir_base, list);
 }
 
 void launch_dist_pack(const Bufs &B, int what, const int *list, int nsend, void *out,

@@ -158,14 +158,17 @@ __global__ void __launch_bounds__(256, 3) k_verlet(Params P, Bufs B, int n) {
     }
     const int cy = seg_row % ny, cz = seg_row / ny;
     int xa = cmin - 1, xb = cmax + 1;
-    int pmi = pmi_dec;  // + x when the run covers a whole periodic x-row
+    // per-pair R4 along x: a run covering a whole periodic x-row, or (a
+    // decomposed x) a run touching cells that may hold wrapped particles
+    int pmi_x = 0;
     if (!P.grid.wrap[0]) {
       xa = max(xa, 0);
       xb = min(xb, nx - 1);
+      if ((pmi_dec & 1) && !(xa >= P.grid.safe_lo[0] && xb <= P.grid.safe_hi[0])) pmi_x = 1;
     } else if (xb - xa + 1 >= nx) {
       xa = 0;
       xb = nx - 1;
-      pmi |= 1;
+      pmi_x = 1;
     }
     for (int dz = -1; dz <= 1; ++dz) {
       int qz = cz + dz;
@@ -182,6 +185,11 @@ __global__ void __launch_bounds__(256, 3) k_verlet(Params P, Bufs B, int n) {
           if (qy < 0) { qy += ny; shy = Ly; } else { qy -= ny; ly = Ly; }
         }
         const int rowc = nx * (qy + ny * qz);
+        const int pmi = pmi_x |
+                        ((pmi_dec & 2) && !(min(cy, qy) >= P.grid.safe_lo[1] &&
+                                            max(cy, qy) <= P.grid.safe_hi[1]) ? 2 : 0) |
+                        ((pmi_dec & 4) && !(min(cz, qz) >= P.grid.safe_lo[2] &&
+                                            max(cz, qz) <= P.grid.safe_hi[2]) ? 4 : 0);
         // x range [xa, xb] of cells, split at the periodic seam
         int a0 = xa, b0 = xb, a1 = 0, b1 = -1;
         float sx0 = 0.f, lx0 = 0.f, sx1 = 0.f, lx1 = 0.f;
@@ -203,7 +211,7 @@ __global__ void __launch_bounds__(256, 3) k_verlet(Params P, Bufs B, int n) {
                                                 __fsub_rn(xi.z, lz), 0.f)
                                   : make_float4(INF, INF, INF, 0.f);
           scan_any(P, pos, B.start[rowc + a1], B.start[rowc + b1 + 1], xe1,
-                   make_float3(sx1, shy, shz), pmi_dec, cap, row, k);
+                   make_float3(sx1, shy, shz), pmi & ~1, cap, row, k);
         }
       }
     }

@@ -377,6 +377,20 @@ pm_status setup_grid(pm_ctx c) {
     }
     double nd = std::floor(ext / side);
     if (nd < 1) nd = 1;
+    P.grid.safe_lo[d] = 0;
+    P.grid.safe_hi[d] = (int)nd - 1;
+    if (dec) {
+      // cells whose extent lies strictly inside the global box (a margin of
+      // 1e-3 cell covers the fp32 rounding of the unwrapped coordinate): no
+      // particle binned there is a wrapped image, so plain differences are R4
+      const double w = ext / nd, o = (double)P.grid.o[d], mg = 1e-3 * w;
+      const double glo = (double)P.box.lo[d], ghi = (double)P.box.hi[d];
+      int lo_c = 0, hi_c = (int)nd - 1;
+      while (lo_c < (int)nd && o + lo_c * w < glo + mg) ++lo_c;
+      while (hi_c >= 0 && o + (hi_c + 1) * w > ghi - mg) --hi_c;
+      P.grid.safe_lo[d] = lo_c;
+      P.grid.safe_hi[d] = hi_c;
+    }
     if (P.grid.wrap[d] && nd < 3)
       return set_err(c, PM_E_INVAL,
                      "periodic axis %d: extent %g < 3 r_v = %g (27-cell stencil needs 3 cells)", d,

@@ -39,6 +39,8 @@ struct Grid {
   float ext[3];    // frame extent
   int wrap[3];     // periodic stencil along this axis
   int unwrap[3];   // bin the nearest image (decomposed axes)
+  int safe_lo[3], safe_hi[3];  // decomposed axes: cells whose extent lies strictly
+                               // inside the global box (no wrapped particle)
   int ncell;
 };
 
