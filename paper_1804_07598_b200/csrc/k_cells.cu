@@ -96,7 +96,9 @@ __device__ int block_exclusive_scan(int v, int *total) {
 }
 
 // a3 phase 1: per-tile exclusive scan of the counts, tile totals.
-__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const int32_t *__restrict__ count,
+// The counts are consumed here and reset to zero for the next build (so no
+// separate zeroing pass runs before k_cell_ids).
+__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(int32_t *__restrict__ count,
                                                              int32_t *__restrict__ start,
                                                              int32_t *__restrict__ tile_sum,
                                                              int ncell) {
@@ -108,6 +110,9 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const int32_t *__re
     v[k] = (base + k < ncell) ? count[base + k] : 0;
     s += v[k];
   }
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k)
+    if (base + k < ncell) count[base + k] = 0;
   int total;
   int ex = block_exclusive_scan<kScanThreads>(s, &total);
 #pragma unroll
@@ -188,14 +193,22 @@ __global__ void __launch_bounds__(256) k_segsort(Bufs B, const int32_t *__restri
       }
     }
     if (lane < m) B.perm[s + lane] = v;
-    const float nan = __int_as_float(0x7fc00000);
+    // coincidence: lanes with equal position bits have equal hashes; one
+    // match_any finds candidate groups, an exact compare confirms (rare)
+    const float nan = __int_as_float(0x7fc00000);  // idle lanes never compare equal
     const float4 p = (lane < m) ? pos[v] : make_float4(nan, nan, nan, 0.f);
+    const unsigned hx = __float_as_uint(p.x), hy = __float_as_uint(p.y), hz = __float_as_uint(p.z);
+    const unsigned h = (lane < m) ? (hx * 0x9E3779B1u) ^ (hy * 0x85EBCA77u) ^ (hz * 0xC2B2AE3Du)
+                                  : 0xFFFFFFFFu - (unsigned)lane;  // distinct for idle lanes
+    const unsigned grp = __match_any_sync(full, h) & ~(1u << lane);
     bool dup = false;
-    for (int o = 1; o < m; ++o) {
-      const int src = (lane + o) & 31;
-      const float4 q = make_float4(__shfl_sync(full, p.x, src), __shfl_sync(full, p.y, src),
-                                   __shfl_sync(full, p.z, src), 0.f);
-      dup |= same_pos(p, q);
+    if (__any_sync(full, grp != 0u)) {
+      for (int o = 1; o < 32; ++o) {  // exact check, only when hashes collide
+        const int src = (lane + o) & 31;
+        const float4 q = make_float4(__shfl_sync(full, p.x, src), __shfl_sync(full, p.y, src),
+                                     __shfl_sync(full, p.z, src), 0.f);
+        dup |= ((grp >> src) & 1u) && same_pos(p, q);
+      }
     }
     if (dup) st->coinc_gid = (long long)B.gid[st->cur_id][v];
     return;
@@ -289,7 +302,7 @@ void launch_zero_i32(int32_t *p, int64_t n, cudaStream_t s) {
 }
 
 void launch_cell_ids(const Params &P, const Bufs &B, int64_t n, cudaStream_t s) {
-  launch_zero_i32(B.count, P.grid.ncell, s);
+  // B.count is all zero here: allocated zeroed, and every scan resets it
   if (n > 0) k_cell_ids<<<blocks_for(n, 256), 256, 0, s>>>(P, B, n);
 }
 

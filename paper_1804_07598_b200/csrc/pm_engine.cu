@@ -248,6 +248,7 @@ pm_status ensure_cells(pm_ctx c) {
   const int64_t ncell = c->P.grid.ncell;
   if (ncell > c->ncell_cap) {
     CUDA_TRY(c, dalloc(&c->B.count, ncell));
+    CUDA_TRY(c, cudaMemset(c->B.count, 0, sizeof(int32_t) * ncell));  // kept zero by the scan
     CUDA_TRY(c, dalloc(&c->B.start, ncell + 1));
     CUDA_TRY(c, dalloc(&c->B.big_cells, ncell));
     c->ncell_cap = ncell;
