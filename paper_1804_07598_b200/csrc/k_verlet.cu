@@ -15,22 +15,6 @@ namespace pm {
 
 namespace {
 
-// Append j to this lane's row when hit: one predicated 4-byte store (inline
-// PTX: no divergent branch) at row + 128*k bytes (mad.wide.u32).  CLAMP: the
-// run could overflow the row, so the slot is clamped to cap-1 (an overflowing
-// row only rewrites its last slot; the build is then retried with a larger
-// capacity).
-template <bool CLAMP>
-__device__ __forceinline__ void append(int *__restrict__ row, int cap, int &k, bool hit, int j) {
-  const unsigned kk = CLAMP ? (unsigned)min(k, cap - 1) : (unsigned)k;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t.reg .b64 a;\n\tsetp.ne.b32 p, %2, 0;\n\t"
-      "mad.wide.u32 a, %3, 128, %0;\n\t@p st.global.b32 [a], %1;\n\t}" ::"l"(row),
-      "r"(j), "r"((int)hit), "r"(kk)
-      : "memory");
-  k += hit ? 1 : 0;
-}
-
 // Scan one contiguous candidate range [b, e) (one x-run of cells in cell
 // order).  Periodic images are handled per run (R4 "per-run
 // shift"): if the run's cells were reached across the low face the whole run
@@ -49,11 +33,9 @@ __device__ __forceinline__ void append(int *__restrict__ row, int cap, int &k, b
 // coincident distinct pair is caught by the force / density passes, which
 // raise PM_E_COINCIDENT).  Lanes outside the current segment carry
 // xi = +inf and never hit.
-template <bool SHIFTJ, bool PAIRMI, bool CLAMP>
-__device__ __forceinline__ void test_append(const Params &P, const float4 &xi_eff,
-                                            const float3 &csh, int pmi, const float4 &xj, int j,
-                                            unsigned rv2m1, int *__restrict__ row, int cap,
-                                            int &k) {
+template <bool SHIFTJ, bool PAIRMI>
+__device__ __forceinline__ bool hit_of(const Params &P, const float4 &xi_eff, const float3 &csh,
+                                       int pmi, const float4 &xj, unsigned rv2m1) {
   float dx = SHIFTJ ? __fsub_rn(__fsub_rn(xj.x, csh.x), xi_eff.x) : __fsub_rn(xj.x, xi_eff.x);
   float dy = SHIFTJ ? __fsub_rn(__fsub_rn(xj.y, csh.y), xi_eff.y) : __fsub_rn(xj.y, xi_eff.y);
   float dz = SHIFTJ ? __fsub_rn(__fsub_rn(xj.z, csh.z), xi_eff.z) : __fsub_rn(xj.z, xi_eff.z);
@@ -63,44 +45,50 @@ __device__ __forceinline__ void test_append(const Params &P, const float4 &xi_ef
     if (pmi & 4) dz = pair_delta1(xi_eff.z, xj.z, P.box.L[2], P.box.halfL[2], 1);
   }
   const float d2 = dist2(dx, dy, dz);
-  const bool hit = (__float_as_uint(d2) - 1u) < rv2m1;
-  append<CLAMP>(row, cap, k, hit, j);
+  return (__float_as_uint(d2) - 1u) < rv2m1;
 }
 
-template <bool SHIFTJ, bool PAIRMI, bool CLAMP>
+// Candidates are tested 32 at a time into a per-lane hit mask (one bit per
+// candidate, ~1 instruction each); only the set bits (about 11% of them) are
+// expanded into row entries, in candidate order.  An overflowing row keeps
+// rewriting its last slot (min(k, cap-1)) and the build is retried.
+template <bool SHIFTJ, bool PAIRMI>
 __device__ __forceinline__ void scan_run(const Params &P, const float4 *__restrict__ pos, int b,
                                          int e, const float4 &xi_eff, float3 csh, int pmi,
                                          int cap, int *__restrict__ row, int &k) {
   const unsigned rv2m1 = __float_as_uint(P.rv2) - 1u;
-  int j = b;
-  for (; j + 8 <= e; j += 8) {
-    float4 x[8];
+  for (int j0 = b; j0 < e; j0 += 32) {
+    unsigned msk = 0u;
+    if (j0 + 32 <= e) {
+#pragma unroll 1
+      for (int u0 = 0; u0 < 32; u0 += 8) {
+        float4 x[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) x[u] = pos[j + u];  // same address in all lanes
+        for (int u = 0; u < 8; ++u) x[u] = pos[j0 + u0 + u];  // same address in all lanes
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
-      test_append<SHIFTJ, PAIRMI, CLAMP>(P, xi_eff, csh, pmi, x[u], j + u, rv2m1, row, cap, k);
+        for (int u = 0; u < 8; ++u)
+          msk |= (hit_of<SHIFTJ, PAIRMI>(P, xi_eff, csh, pmi, x[u], rv2m1) ? 1u : 0u) << (u0 + u);
+      }
+    } else {
+      for (int u = 0; u < e - j0; ++u)
+        msk |= (hit_of<SHIFTJ, PAIRMI>(P, xi_eff, csh, pmi, pos[j0 + u], rv2m1) ? 1u : 0u) << u;
+    }
+    while (msk) {
+      const int u = __ffs(msk) - 1;
+      msk &= msk - 1u;
+      row[(int64_t)min(k, cap - 1) << 5] = j0 + u;
+      ++k;
+    }
   }
-  for (; j < e; ++j)
-    test_append<SHIFTJ, PAIRMI, CLAMP>(P, xi_eff, csh, pmi, pos[j], j, rv2m1, row, cap, k);
 }
 
 __device__ __forceinline__ void scan_any(const Params &P, const float4 *__restrict__ pos, int b,
                                          int e, const float4 &xi_eff, float3 csh, int pmi,
                                          int cap, int *__restrict__ row, int &k) {
-  const bool mix = pmi != 0;
   const bool sj = csh.x != 0.f || csh.y != 0.f || csh.z != 0.f;
-  // warp-uniform: can any lane of the warp overflow its row in this run?
-  const bool clamp = __any_sync(0xffffffffu, k + (e - b) > cap);
-  if (!clamp && !mix && !sj) {
-    scan_run<false, false, false>(P, pos, b, e, xi_eff, csh, 0, cap, row, k);
-  } else if (!clamp && !mix) {
-    scan_run<true, false, false>(P, pos, b, e, xi_eff, csh, 0, cap, row, k);
-  } else if (mix) {
-    scan_run<true, true, true>(P, pos, b, e, xi_eff, csh, pmi, cap, row, k);
-  } else {
-    scan_run<true, false, true>(P, pos, b, e, xi_eff, csh, 0, cap, row, k);
-  }
+  if (pmi) scan_run<true, true>(P, pos, b, e, xi_eff, csh, pmi, cap, row, k);
+  else if (sj) scan_run<true, false>(P, pos, b, e, xi_eff, csh, 0, cap, row, k);
+  else scan_run<false, false>(P, pos, b, e, xi_eff, csh, 0, cap, row, k);
 }
 
 // Thread per particle (row), warp-uniform candidate stream.  The warp's 32
