@@ -34,8 +34,8 @@ namespace {
 // raise PM_E_COINCIDENT).  Lanes outside the current segment carry
 // xi = +inf and never hit.
 template <bool SHIFTJ, bool PAIRMI>
-__device__ __forceinline__ bool hit_of(const Params &P, const float4 &xi_eff, const float3 &csh,
-                                       int pmi, const float4 &xj, unsigned rv2m1) {
+__device__ __forceinline__ float d2_of(const Params &P, const float4 &xi_eff, const float3 &csh,
+                                       int pmi, const float4 &xj) {
   float dx = SHIFTJ ? __fsub_rn(__fsub_rn(xj.x, csh.x), xi_eff.x) : __fsub_rn(xj.x, xi_eff.x);
   float dy = SHIFTJ ? __fsub_rn(__fsub_rn(xj.y, csh.y), xi_eff.y) : __fsub_rn(xj.y, xi_eff.y);
   float dz = SHIFTJ ? __fsub_rn(__fsub_rn(xj.z, csh.z), xi_eff.z) : __fsub_rn(xj.z, xi_eff.z);
@@ -44,35 +44,53 @@ __device__ __forceinline__ bool hit_of(const Params &P, const float4 &xi_eff, co
     if (pmi & 2) dy = pair_delta1(xi_eff.y, xj.y, P.box.L[1], P.box.halfL[1], 1);
     if (pmi & 4) dz = pair_delta1(xi_eff.z, xj.z, P.box.L[2], P.box.halfL[2], 1);
   }
-  const float d2 = dist2(dx, dy, dz);
-  return (__float_as_uint(d2) - 1u) < rv2m1;
+  return dist2(dx, dy, dz);
 }
 
-// Candidates are tested 32 at a time into a per-lane hit mask (one bit per
-// candidate, ~1 instruction each); only the set bits (about 11% of them) are
-// expanded into row entries, in candidate order.  An overflowing row keeps
-// rewriting its last slot (min(k, cap-1)) and the build is retried.
+// Eight candidates j0 + u0 + u (u < 8) into bits u0 + u of the lane's hit
+// mask: one compare d2 < rv2 and one predicated OR with an immediate each.
+// The particle itself (d2 = 0) passes and is dropped at expansion; CLAMP:
+// loads past the range end e are clamped to e - 1 (their bits are masked).
+template <bool SHIFTJ, bool PAIRMI, int U0, bool CLAMP>
+__device__ __forceinline__ void test8(const Params &P, const float4 *__restrict__ pos, int j0,
+                                      int e, const float4 &xi_eff, const float3 &csh, int pmi,
+                                      unsigned &msk) {
+  float4 x[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u)  // same address in all lanes
+    x[u] = pos[CLAMP ? min(j0 + U0 + u, e - 1) : j0 + U0 + u];
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+    if (d2_of<SHIFTJ, PAIRMI>(P, xi_eff, csh, pmi, x[u]) < P.rv2) msk |= 1u << (U0 + u);
+}
+
+// Candidates are tested 32 at a time into a per-lane hit mask; only the set
+// bits (about 11% of them) are expanded into row entries, in candidate order.
+// Membership is 0 < d2 < rv2 (R5): d2 == 0 is the particle itself (dropped
+// by index; a coincident distinct pair is raised as PM_E_COINCIDENT by the
+// cell sort).  Lanes outside the current segment carry xi = +inf and never
+// hit.  An overflowing row keeps rewriting its last slot (min(k, cap-1)) and
+// the build is retried.
 template <bool SHIFTJ, bool PAIRMI>
 __device__ __forceinline__ void scan_run(const Params &P, const float4 *__restrict__ pos, int b,
                                          int e, const float4 &xi_eff, float3 csh, int pmi,
-                                         int cap, int *__restrict__ row, int &k) {
-  const unsigned rv2m1 = __float_as_uint(P.rv2) - 1u;
+                                         int self, int cap, int *__restrict__ row, int &k) {
   for (int j0 = b; j0 < e; j0 += 32) {
     unsigned msk = 0u;
     if (j0 + 32 <= e) {
-#pragma unroll 1
-      for (int u0 = 0; u0 < 32; u0 += 8) {
-        float4 x[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) x[u] = pos[j0 + u0 + u];  // same address in all lanes
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          msk |= (hit_of<SHIFTJ, PAIRMI>(P, xi_eff, csh, pmi, x[u], rv2m1) ? 1u : 0u) << (u0 + u);
-      }
+      test8<SHIFTJ, PAIRMI, 0, false>(P, pos, j0, e, xi_eff, csh, pmi, msk);
+      test8<SHIFTJ, PAIRMI, 8, false>(P, pos, j0, e, xi_eff, csh, pmi, msk);
+      test8<SHIFTJ, PAIRMI, 16, false>(P, pos, j0, e, xi_eff, csh, pmi, msk);
+      test8<SHIFTJ, PAIRMI, 24, false>(P, pos, j0, e, xi_eff, csh, pmi, msk);
     } else {
-      for (int u = 0; u < e - j0; ++u)
-        msk |= (hit_of<SHIFTJ, PAIRMI>(P, xi_eff, csh, pmi, pos[j0 + u], rv2m1) ? 1u : 0u) << u;
+      const int rem = e - j0;  // 1..31, warp-uniform
+      test8<SHIFTJ, PAIRMI, 0, true>(P, pos, j0, e, xi_eff, csh, pmi, msk);
+      if (rem > 8) test8<SHIFTJ, PAIRMI, 8, true>(P, pos, j0, e, xi_eff, csh, pmi, msk);
+      if (rem > 16) test8<SHIFTJ, PAIRMI, 16, true>(P, pos, j0, e, xi_eff, csh, pmi, msk);
+      if (rem > 24) test8<SHIFTJ, PAIRMI, 24, true>(P, pos, j0, e, xi_eff, csh, pmi, msk);
+      msk &= (1u << rem) - 1u;
     }
+    if (self >= j0 && self < j0 + 32) msk &= ~(1u << (self - j0));
     while (msk) {
       const int u = __ffs(msk) - 1;
       msk &= msk - 1u;
@@ -84,11 +102,11 @@ __device__ __forceinline__ void scan_run(const Params &P, const float4 *__restri
 
 __device__ __forceinline__ void scan_any(const Params &P, const float4 *__restrict__ pos, int b,
                                          int e, const float4 &xi_eff, float3 csh, int pmi,
-                                         int cap, int *__restrict__ row, int &k) {
+                                         int self, int cap, int *__restrict__ row, int &k) {
   const bool sj = csh.x != 0.f || csh.y != 0.f || csh.z != 0.f;
-  if (pmi) scan_run<true, true>(P, pos, b, e, xi_eff, csh, pmi, cap, row, k);
-  else if (sj) scan_run<true, false>(P, pos, b, e, xi_eff, csh, 0, cap, row, k);
-  else scan_run<false, false>(P, pos, b, e, xi_eff, csh, 0, cap, row, k);
+  if (pmi) scan_run<true, true>(P, pos, b, e, xi_eff, csh, pmi, self, cap, row, k);
+  else if (sj) scan_run<true, false>(P, pos, b, e, xi_eff, csh, 0, self, cap, row, k);
+  else scan_run<false, false>(P, pos, b, e, xi_eff, csh, 0, self, cap, row, k);
 }
 
 // Thread per particle (row), warp-uniform candidate stream.  The warp's 32
@@ -193,13 +211,13 @@ __global__ void __launch_bounds__(256, 3) k_verlet(Params P, Bufs B, int n) {
                                               __fsub_rn(xi.z, lz), 0.f)
                                 : make_float4(INF, INF, INF, 0.f);
         scan_any(P, pos, B.start[rowc + a0], B.start[rowc + b0 + 1], xe0,
-                 make_float3((pmi & 1) ? 0.f : sx0, shy, shz), pmi, cap, row, k);
+                 make_float3((pmi & 1) ? 0.f : sx0, shy, shz), pmi, i, cap, row, k);
         if (b1 >= a1) {
           const float4 xe1 = mine ? make_float4(__fsub_rn(xi.x, lx1), __fsub_rn(xi.y, ly),
                                                 __fsub_rn(xi.z, lz), 0.f)
                                   : make_float4(INF, INF, INF, 0.f);
           scan_any(P, pos, B.start[rowc + a1], B.start[rowc + b1 + 1], xe1,
-                   make_float3(sx1, shy, shz), pmi & ~1, cap, row, k);
+                   make_float3(sx1, shy, shz), pmi & ~1, i, cap, row, k);
         }
       }
     }
