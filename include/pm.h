@@ -141,6 +141,30 @@ pm_status pm_compute_lj(pm_ctx ctx, int32_t want_energy);
 pm_status pm_sph_density(pm_ctx ctx);
 pm_status pm_sph_forces(pm_ctx ctx);
 
+/* WCSPH time stepping (Eq. 2 continuity
+ * density, :358 "Verlet time-stepping [46] with dynamic step size" as in
+ * DualSPHysics; readings R26-R28 in DESIGN.md).  nsteps steps of:
+ *   D_p = sum_q m v_pq . grad_p W (all particles), a_p = Eq. 1 + g (fluid),
+ *   dt  = cfl * min( min_fluid sqrt(h/|a_p|), min_p h/(c0 + max_q |mu_pq|) ),
+ *   Verlet: v' = v_prev + 2 dt a, rho' = rho_prev + 2 dt D (an Euler step
+ *   v' = v + dt a, rho' = rho + dt D on the first and every `every`-th
+ *   step), x' = x + dt v + dt^2/2 a for fluid; boundary particles (kind 1)
+ *   keep x and v, their density evolves; P' = Tait EOS (Eq. 3).
+ * The densities at the start are the current ones (pm_sph_density is run
+ * first if they are not valid); the Verlet list (r_cut = 2h, skin > 0) is
+ * rebuilt whenever a particle moved more than skin/2 or left an open axis.
+ * Single context only (PM_E_STATE on a decomposed context).  Errors:
+ * PM_E_NONFINITE (rates or dt), PM_E_DOMAIN (a fluid particle left an open
+ * axis).  out may be NULL. */
+typedef struct {
+  int64_t steps;     /* steps completed */
+  int64_t rebuilds;  /* Verlet rebuilds during the call */
+  double time;       /* simulated time of the call */
+  float dt_min, dt_max, dt_last;
+} pm_sph_run_stats;
+pm_status pm_sph_run(pm_ctx ctx, int64_t nsteps, float cfl, int32_t every,
+                     pm_sph_run_stats *out);
+
 typedef struct {
   int64_t steps;     /* steps completed by this call */
   int64_t rebuilds;  /* Verlet rebuilds during this call */

@@ -80,6 +80,10 @@ def lib():
         L.orc_sph_accel_rows.argtypes = [C.c_int64, f32p, f32p, f64p, f64p, C.c_void_p, f32p,
                                          f32p, i32p, C.c_double, C.c_double, C.c_double,
                                          C.c_double, C.c_double, f64p, i64p, C.c_int64, f64p]
+        L.orc_sph_run.argtypes = [C.c_int64, f64p, f64p, f64p, C.c_void_p, f64p, f64p, i32p,
+                                  C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
+                                  C.c_double, C.c_double, C.c_double, f64p, C.c_double,
+                                  C.c_int64, C.c_int64, f64p]
         _lib = L
     return _lib
 
@@ -251,6 +255,29 @@ def sph_accel_rows(pos4, vel4, rho, P, kind, lo, hi, per, params, rows=None):
                              float(params["alpha"]), float(params["c0"]),
                              float(params["eta2"]), g, r, r.shape[0], a)
     return a
+
+
+def sph_run(pos4, vel4, rho, kind, lo, hi, per, params, nsteps, cfl=0.2, every=40):
+    """WCSPH time stepping (SURVEY NEXT-3; PAPER.md:335 Eq. 2, :358 'Verlet
+    time-stepping [46] with dynamic step size'; readings R26-R28): continuity
+    density, Tait EOS, Eq. 1 + Eq. 5 accelerations, Verlet scheme with an
+    Euler step every `every` steps, dt = cfl * min(dt_f, dt_cv).  fp64 state
+    from the fp32 inputs.  Returns (x (n,3), v (n,3), rho (n,), dt (nsteps,))."""
+    n = pos4.shape[0]
+    x = np.ascontiguousarray(np.asarray(pos4, np.float32)[:, :3].astype(np.float64))
+    v = np.ascontiguousarray(np.asarray(vel4, np.float32)[:, :3].astype(np.float64))
+    r = np.ascontiguousarray(np.asarray(rho, np.float64).copy())
+    k = None if kind is None else np.ascontiguousarray(kind, dtype=np.int32)
+    g = np.ascontiguousarray(np.asarray(params["g"], np.float64).reshape(3))
+    lo64 = np.ascontiguousarray(np.asarray(lo, np.float32).astype(np.float64))
+    hi64 = np.ascontiguousarray(np.asarray(hi, np.float32).astype(np.float64))
+    tr = np.zeros(max(int(nsteps), 1), np.float64)
+    lib().orc_sph_run(n, x.reshape(-1), v.reshape(-1), r, k.ctypes.data if k is not None else None,
+                      lo64, hi64, _i3(per), float(params["h"]), float(params["mass"]),
+                      float(params["rho0"]), float(params["b"]), float(params["gamma"]),
+                      float(params["alpha"]), float(params["c0"]), float(params["eta2"]), g,
+                      float(cfl), int(every), int(nsteps), tr)
+    return x, v, r, tr[:nsteps]
 
 
 # ---------------------------------------------------------------- parity metric

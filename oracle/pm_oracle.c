@@ -511,3 +511,117 @@ void orc_sph_accel_rows(int64_t n, const float *pos4, const float *vel4, const d
     for (int d = 0; d < 3; ++d) a_out[3 * r + d] = a[d] + g[d];
   }
 }
+
+/* ------------------------------------------------------------------ */
+/* WCSPH time stepping (§4.2):   */
+/* continuity density Eq. 2, Tait EOS Eq. 3, momentum Eq. 1 with Eq. 5,  */
+/* "Verlet time-stepping [46] with dynamic step size" as in DualSPHysics */
+/* (the scheme itself is not in the paper -- readings      */
+/* R26-R28 in DESIGN.md; parity unpinned beyond the self-consistency     */
+/* pins of tests/test_oracle_pins.py).  fp64 state, O(N^2) pair loop.    */
+/*   D_p  = sum_q m v_pq . grad_p W(r_pq)          (R26, all particles)   */
+/*   a_p  = Eq. 1 (fluid; boundary a = 0)                                 */
+/*   dt   = cfl * min( min_fluid sqrt(h/|a_p|),                          */
+/*                     min_p h / (c0 + max_q |h v_pq.r_pq/(r^2+eta2)|) )  */
+/*   Verlet (R27): v' = v_prev + 2 dt a, rho' = rho_prev + 2 dt D;       */
+/*   every Ns-th step and the first: v' = v + dt a, rho' = rho + dt D;   */
+/*   x' = x + dt v + dt^2/2 a (fluid); boundary x, v fixed, rho evolves. */
+/* ------------------------------------------------------------------ */
+static void sph_rates64(int64_t n, const double *x, const double *v, const double *rho,
+                        const double *P, const int32_t *kind, const double L[3],
+                        const int32_t per[3], double h, double mass, double alpha, double cbar,
+                        double eta2, const double g[3], double *a, double *D, double *dtf,
+                        double *dtcv) {
+  double fmin = 1e300, cvmin = 1e300;
+#pragma omp parallel for schedule(dynamic, 16) reduction(min : fmin, cvmin)
+  for (int64_t p = 0; p < n; ++p) {
+    double ap[3] = {0, 0, 0}, dp = 0.0, mumax = 0.0;
+    for (int64_t q = 0; q < n; ++q) {
+      if (q == p) continue;
+      double dl[3]; /* r_pq = x_p - x_q (minimum image on periodic axes) */
+      for (int d = 0; d < 3; ++d) {
+        double e = x[3 * p + d] - x[3 * q + d];
+        if (per[d]) {
+          if (e > 0.5 * L[d]) e -= L[d];
+          else if (e < -0.5 * L[d]) e += L[d];
+        }
+        dl[d] = e;
+      }
+      double r2 = dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2];
+      if (!(r2 < 4.0 * h * h) || r2 == 0.0) continue;
+      double rr = sqrt(r2);
+      double dw = orc_sph_dWdr(rr, h);
+      double gw[3] = {dl[0] / rr * dw, dl[1] / rr * dw, dl[2] / rr * dw};
+      double vpq[3] = {v[3 * p] - v[3 * q], v[3 * p + 1] - v[3 * q + 1],
+                       v[3 * p + 2] - v[3 * q + 2]};
+      double vr = vpq[0] * dl[0] + vpq[1] * dl[1] + vpq[2] * dl[2];
+      dp += mass * (vpq[0] * gw[0] + vpq[1] * gw[1] + vpq[2] * gw[2]);
+      double mu = h * vr / (r2 + eta2);
+      if (fabs(mu) > mumax) mumax = fabs(mu);
+      double Pi = 0.0;
+      if (vr < 0.0) Pi = -alpha * cbar * mu / (0.5 * (rho[p] + rho[q]));
+      double coef = mass * ((P[p] + P[q]) / (rho[p] * rho[q]) + Pi);
+      for (int d = 0; d < 3; ++d) ap[d] -= coef * gw[d];
+    }
+    D[p] = dp;
+    double cv = h / (cbar + mumax);
+    if (cv < cvmin) cvmin = cv;
+    if (kind && kind[p] != 0) {
+      a[3 * p] = a[3 * p + 1] = a[3 * p + 2] = 0.0;
+    } else {
+      for (int d = 0; d < 3; ++d) a[3 * p + d] = ap[d] + g[d];
+      double am = sqrt(a[3 * p] * a[3 * p] + a[3 * p + 1] * a[3 * p + 1] +
+                       a[3 * p + 2] * a[3 * p + 2]);
+      double f = am > 0 ? sqrt(h / am) : 1e300;
+      if (f < fmin) fmin = f;
+    }
+  }
+  *dtf = fmin;
+  *dtcv = cvmin;
+}
+
+/* x, v: fp64 (n x 3) in/out; rho: fp64 in/out.  trace[s] = dt of step s.
+ * Positions on periodic axes are wrapped into [lo, hi). */
+void orc_sph_run(int64_t n, double *x, double *v, double *rho, const int32_t *kind,
+                 const double lo[3], const double hi[3], const int32_t per[3], double h,
+                 double mass, double rho0, double b, double gamma, double alpha, double cbar,
+                 double eta2, const double g[3], double cfl, int64_t every, int64_t nsteps,
+                 double *trace) {
+  double L[3] = {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]};
+  size_t n3 = sizeof(double) * 3 * (size_t)(n > 0 ? n : 1), n1 = n3 / 3;
+  double *a = (double *)malloc(n3), *D = (double *)malloc(n1), *P = (double *)malloc(n1);
+  double *vprev = (double *)malloc(n3), *rprev = (double *)malloc(n1);
+  memcpy(vprev, v, n3);
+  memcpy(rprev, rho, n1);
+  for (int64_t s = 0; s < nsteps; ++s) {
+    for (int64_t p = 0; p < n; ++p) P[p] = b * (pow(rho[p] / rho0, gamma) - 1.0);
+    double dtf, dtcv;
+    sph_rates64(n, x, v, rho, P, kind, L, per, h, mass, alpha, cbar, eta2, g, a, D, &dtf, &dtcv);
+    double dt = cfl * (dtf < dtcv ? dtf : dtcv);
+    if (trace) trace[s] = dt;
+    int euler = (s == 0) || (every > 0 && (s + 1) % every == 0);
+    for (int64_t p = 0; p < n; ++p) {
+      double rn = euler ? rho[p] + dt * D[p] : rprev[p] + 2.0 * dt * D[p];
+      rprev[p] = rho[p];
+      rho[p] = rn;
+      if (kind && kind[p] != 0) continue;
+      for (int d = 0; d < 3; ++d) {
+        double vo = v[3 * p + d], an = a[3 * p + d];
+        double vn = euler ? vo + dt * an : vprev[3 * p + d] + 2.0 * dt * an;
+        double xx = x[3 * p + d] + dt * vo + 0.5 * dt * dt * an;
+        if (per[d]) {
+          if (xx >= hi[d]) xx -= L[d];
+          else if (xx < lo[d]) xx += L[d];
+        }
+        x[3 * p + d] = xx;
+        vprev[3 * p + d] = vo;
+        v[3 * p + d] = vn;
+      }
+    }
+  }
+  free(a);
+  free(D);
+  free(P);
+  free(vprev);
+  free(rprev);
+}

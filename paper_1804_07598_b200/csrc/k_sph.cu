@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(256) k_sph_density(Params P, Bufs B, int n) {
     xg = pow(x, (double)P.sph.gamma);
   }
   const double pr = (double)P.sph.b * (xg - 1.0);
-  B.rhoP[i] = make_float2((float)rho, (float)pr);
+  B.rhoP[st->cur_id][i] = make_float2((float)rho, (float)pr);
   if (!isfinite(rho + pr)) raise_error(st, -8 /*PM_E_NONFINITE*/, (long long)B.gid[st->cur_id][i]);
 }
 
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(256) k_sph_forces(Params P, Bufs B, int n) {
   }
   const float4 *__restrict__ pos = B.pos[st->cur_pv];
   const float4 *__restrict__ vel = B.vel[st->cur_pv];
-  const float2 *__restrict__ rhoP = B.rhoP;
+  const float2 *__restrict__ rhoP = B.rhoP[st->cur_id];
   const float4 xi = pos[i];
   const float4 vi = vel[i];
   const float2 rpi = rhoP[i];
@@ -171,6 +171,187 @@ __global__ void __launch_bounds__(256) k_sph_forces(Params P, Bufs B, int n) {
   if (!isfinite(ax + ay + az)) raise_error(st, -8 /*PM_E_NONFINITE*/, (long long)B.gid[st->cur_id][i]);
 }
 
+// ---------------------------------------------------------------------------
+// WCSPH time stepping (SURVEY §8(f) NEXT-3; PAPER.md:335 Eq. 2, :358
+// "Verlet time-stepping [46] with dynamic step size"; readings R26-R28 in
+// DESIGN.md, the same definitions as oracle/pm_oracle.c orc_sph_run):
+//   k_sph_rates : D_p = sum_q m v_pq . grad_p W (all particles), a_p = Eq. 1
+//                 + g (fluid), and the step-size bounds sqrt(h/|a_p|) (fluid)
+//                 and h/(c0 + max_q |mu_pq|), reduced with atomicMin;
+//   k_sph_dt    : dt = cfl * min(bounds); Euler step on the first and every
+//                 `every`-th step, else leapfrog Verlet;
+//   k_sph_verlet: rho' (all), v', x' (fluid), P' = EOS(rho'), rebuild test.
+// fp32 like the sweeps; the previous-step state (vold, rold) and rhoP travel
+// with the particles through the cell-sort reorder (Params::sph_state).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void warp_min_atomic(unsigned *dst, float v) {
+  unsigned u = __float_as_uint(v);  // v >= 0: uint order = float order
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) u = min(u, __shfl_xor_sync(0xffffffffu, u, o));
+  if ((threadIdx.x & 31) == 0) atomicMin(dst, u);
+}
+
+__global__ void __launch_bounds__(256) k_sph_rates(Params P, Bufs B, int n) {
+  State *st = B.st;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = i < n;
+  const int cp = st->cur_pv, ci = st->cur_id;
+  const float4 *__restrict__ pos = B.pos[cp];
+  const float4 *__restrict__ vel = B.vel[cp];
+  const float2 *__restrict__ rhoP = B.rhoP[ci];
+  float ax = 0.f, ay = 0.f, az = 0.f, D = 0.f, mumax = 0.f;
+  bool fluid = false;
+  if (active) {
+    fluid = !(B.kind[ci][i] & 1);
+    const float4 xi = pos[i];
+    const float4 vi = vel[i];
+    const float2 rpi = rhoP[i];
+    const float acb = P.sph.alpha * P.sph.cbar;
+    auto pair = [&](int j, bool valid) {
+      const float3 d = delta3(P, xi, __ldg(pos + j));  // x_j - x_i
+      const float d2 = dist2(d.x, d.y, d.z);
+      const float rinv = fast_rsqrt(d2);
+      const float q = d2 * rinv * P.sph.inv_h;
+      const bool in = valid && q < 2.0f && d2 > 0.0f;
+      const float dwdr = P.sph.dw_norm * dw_shape(q);
+      const float4 vj = __ldg(vel + j);
+      const float2 rpj = __ldg(rhoP + j);
+      // r_ij = x_i - x_j = -d;  grad_i W = r_ij / r dW/dr = -d rinv dwdr
+      const float vx = vi.x - vj.x, vy = vi.y - vj.y, vz = vi.z - vj.z;
+      const float vd = vx * d.x + vy * d.y + vz * d.z;  // = -(v_ij . r_ij)
+      const float gsc = rinv * dwdr;
+      const float vr = -vd;
+      const float mu = P.sph.h * vr / (d2 + P.sph.eta2);
+      const float pi_ij = vr < 0.0f ? -acb * mu / (0.5f * (rpi.x + rpj.x)) : 0.0f;
+      const float coef = P.sph.mass * ((rpi.y + rpj.y) / (rpi.x * rpj.x) + pi_ij);
+      const float sc = in ? coef * gsc : 0.0f;
+      ax = fmaf(sc, d.x, ax);  // a_i -= coef grad_i W
+      ay = fmaf(sc, d.y, ay);
+      az = fmaf(sc, d.z, az);
+      D += in ? -P.sph.mass * vd * gsc : 0.0f;  // m v_ij . grad_i W
+      mumax = in ? fmaxf(mumax, fabsf(mu)) : mumax;
+    };
+    const int cnt = B.cnt[i];
+    const int *nb = B.nbr + nbr_row_base(B, i);
+    for_row(nb, cnt, [&](int ja, int jb, int jc, int jd, int rem) {
+      pair(ja, true);
+      pair(jb, rem > 1);
+      pair(jc, rem > 2);
+      pair(jd, rem > 3);
+    });
+    if (fluid) {
+      ax += P.sph.g[0];
+      ay += P.sph.g[1];
+      az += P.sph.g[2];
+    } else {
+      ax = ay = az = 0.f;
+    }
+    B.force[i] = make_float4(ax, ay, az, 0.f);
+    B.drho[i] = D;
+    if (!isfinite(ax + ay + az + D))
+      raise_error(st, -8 /*PM_E_NONFINITE*/, (long long)B.gid[ci][i]);
+  }
+  const float INF = __int_as_float(0x7f800000);
+  const float am = sqrtf(ax * ax + ay * ay + az * az);
+  const float dtf = (active && fluid && am > 0.f) ? sqrtf(P.sph.h / am) : INF;
+  const float dtcv = active ? P.sph.h / (P.sph.cbar + mumax) : INF;
+  warp_min_atomic(&st->dtf_bits, dtf);
+  warp_min_atomic(&st->dtcv_bits, dtcv);
+}
+
+__global__ void k_sph_dt(State *st, float cfl, int every) {
+  const float dt = cfl * fminf(__uint_as_float(st->dtf_bits), __uint_as_float(st->dtcv_bits));
+  st->sph_dt = dt;
+  st->sph_dt_min = fminf(st->sph_dt_min, dt);
+  st->sph_dt_max = fmaxf(st->sph_dt_max, dt);
+  st->sph_time += (double)dt;
+  const long long s = st->sph_step;
+  st->mode = (s == 0 || (every > 0 && (s + 1) % every == 0)) ? 1 : 0;  // 1: Euler step
+  st->sph_step = s + 1;
+  st->dtf_bits = 0x7f800000u;
+  st->dtcv_bits = 0x7f800000u;
+  if (!(dt > 0.f) || !isfinite(dt)) {
+    if (atomicCAS(&st->abort, 0, -8 /*PM_E_NONFINITE*/) == 0) st->err_gid = -1;
+  }
+}
+
+__device__ __forceinline__ float tait(const Params &P, float rho) {
+  const float x = rho * P.sph.inv_rho0;
+  float xg;
+  if (P.sph.gamma == 7.0f) {
+    const float x2 = x * x;
+    xg = x2 * x2 * x2 * x;
+  } else {
+    xg = powf(x, P.sph.gamma);
+  }
+  return P.sph.b * (xg - 1.0f);
+}
+
+__global__ void __launch_bounds__(256) k_sph_verlet(Params P, Bufs B, int n) {
+  State *st = B.st;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int cp = st->cur_pv, ci = st->cur_id;
+  bool far = false;
+  if (i < n) {
+    const float dt = st->sph_dt;
+    const bool euler = st->mode == 1;
+    const float D = B.drho[i];
+    const float rho = B.rhoP[ci][i].x, rold = B.rold[ci][i];
+    const float rn = euler ? fmaf(dt, D, rho) : fmaf(2.0f * dt, D, rold);
+    B.rold[ci][i] = rho;
+    B.rhoP[ci][i] = make_float2(rn, tait(P, rn));
+    const float4 x = B.pos[cp][i];
+    const float4 v = B.vel[cp][i];
+    float4 xn = x, vn = v;
+    if (!(B.kind[ci][i] & 1)) {
+      const float4 a = B.force[i];
+      const float4 vo = B.vold[ci][i];
+      const float h2 = 0.5f * dt * dt;
+      vn.x = euler ? fmaf(dt, a.x, v.x) : fmaf(2.0f * dt, a.x, vo.x);
+      vn.y = euler ? fmaf(dt, a.y, v.y) : fmaf(2.0f * dt, a.y, vo.y);
+      vn.z = euler ? fmaf(dt, a.z, v.z) : fmaf(2.0f * dt, a.z, vo.z);
+      float r3[3] = {fmaf(h2, a.x, fmaf(dt, v.x, x.x)), fmaf(h2, a.y, fmaf(dt, v.y, x.y)),
+                     fmaf(h2, a.z, fmaf(dt, v.z, x.z))};
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+        if (P.box.per[d]) r3[d] = wrap1(r3[d], P.box.lo[d], P.box.hi[d], P.box.L[d]);
+      xn = make_float4(r3[0], r3[1], r3[2], x.w);
+      const float4 xr = B.xref[i];
+      const float dx = pair_delta1(xr.x, xn.x, P.box.L[0], P.box.halfL[0], P.box.per[0]);
+      const float dy = pair_delta1(xr.y, xn.y, P.box.L[1], P.box.halfL[1], P.box.per[1]);
+      const float dz = pair_delta1(xr.z, xn.z, P.box.L[2], P.box.halfL[2], P.box.per[2]);
+      far = dist2(dx, dy, dz) > P.half_skin2;
+      if (!P.box.per[0] && (xn.x < P.box.lo[0] || xn.x >= P.box.hi[0])) far = true;
+      if (!P.box.per[1] && (xn.y < P.box.lo[1] || xn.y >= P.box.hi[1])) far = true;
+      if (!P.box.per[2] && (xn.z < P.box.lo[2] || xn.z >= P.box.hi[2])) far = true;
+    }
+    B.vold[ci][i] = v;
+    B.pos[cp ^ 1][i] = xn;
+    B.vel[cp ^ 1][i] = vn;
+  }
+  if (__any_sync(0xffffffffu, far) && (threadIdx.x & 31) == 0) st->need_rebuild = 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->pending_flip = 1;
+}
+
+__global__ void __launch_bounds__(256) k_sph_init_run(Bufs B, int n) {
+  State *st = B.st;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ci = st->cur_id;
+  if (i < n) {
+    B.rold[ci][i] = B.rhoP[ci][i].x;
+    B.vold[ci][i] = B.vel[st->cur_pv][i];
+  }
+  if (i == 0) {
+    st->sph_step = 0;
+    st->sph_time = 0.0;
+    st->sph_dt = 0.f;
+    st->sph_dt_min = __int_as_float(0x7f800000);
+    st->sph_dt_max = 0.f;
+    st->dtf_bits = 0x7f800000u;
+    st->dtcv_bits = 0x7f800000u;
+  }
+}
+
 inline unsigned nb(int64_t n) { return (unsigned)((n + 255) / 256); }
 
 }  // namespace
@@ -181,6 +362,20 @@ void launch_sph_density(const Params &P, const Bufs &B, int64_t n, cudaStream_t 
 
 void launch_sph_forces(const Params &P, const Bufs &B, int64_t n, cudaStream_t s) {
   if (n > 0) k_sph_forces<<<nb(n), 256, 0, s>>>(P, B, (int)n);
+}
+
+void launch_sph_init_run(const Bufs &B, int64_t n, cudaStream_t s) {
+  k_sph_init_run<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(B, (int)n);
+}
+
+// rates -> dt -> integrate (the caller applies the buffer flip)
+void launch_sph_step(const Params &P, const Bufs &B, int64_t n, float cfl, int every,
+                     cudaStream_t s) {
+  if (n <= 0) return;
+  const unsigned nb = (unsigned)((n + 255) / 256);
+  k_sph_rates<<<nb, 256, 0, s>>>(P, B, (int)n);
+  k_sph_dt<<<1, 1, 0, s>>>(B.st, cfl, every);
+  k_sph_verlet<<<nb, 256, 0, s>>>(P, B, (int)n);
 }
 
 }  // namespace pm

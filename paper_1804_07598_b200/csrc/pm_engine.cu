@@ -229,7 +229,16 @@ pm_status ensure_particles(pm_ctx c, int64_t n, int64_t keep = 0) {
   }
   CUDA_TRY(c, dalloc(&B.xref, cap));
   CUDA_TRY(c, dalloc(&B.force, cap));
-  CUDA_TRY(c, dalloc(&B.rhoP, cap));
+  CUDA_TRY(c, dalloc(&B.rhoP[0], cap));
+  CUDA_TRY(c, dalloc(&B.rhoP[1], cap));
+  for (int b = 0; b < 2; ++b) {  // SPH stepping state: allocated by pm_sph_run
+    if (B.vold[b]) cudaFree(B.vold[b]);
+    if (B.rold[b]) cudaFree(B.rold[b]);
+    B.vold[b] = nullptr;
+    B.rold[b] = nullptr;
+  }
+  if (B.drho) cudaFree(B.drho);
+  B.drho = nullptr;
   CUDA_TRY(c, dalloc(&B.cell_of, cap));
   CUDA_TRY(c, dalloc(&B.slot, cap));
   CUDA_TRY(c, dalloc(&B.perm, cap));
@@ -643,7 +652,8 @@ void pm_destroy(pm_ctx c) {
     cudaFree(B.gid[b]);
     cudaFree(B.kind[b]);
   }
-  void *ptrs[] = {B.xref, B.force, B.rhoP, B.cell_of, B.slot, B.count, B.start, B.perm,
+  void *ptrs[] = {B.xref, B.force, B.rhoP[0], B.rhoP[1], B.vold[0], B.vold[1], B.rold[0],
+                  B.rold[1], B.drho, B.cell_of, B.slot, B.count, B.start, B.perm,
                   B.sorttmp, B.scan_tmp, B.nbr, B.cnt, B.st, B.slice_off, B.big_cells};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -846,6 +856,83 @@ pm_status pm_sph_forces(pm_ctx c) {
   return sync_check(c, "pm_sph_forces");
 }
 
+pm_status pm_sph_run(pm_ctx c, int64_t nsteps, float cfl, int32_t every,
+                     pm_sph_run_stats *out) {
+  pm_status s = check_ready(c);
+  if (s) return s;
+  if (out) std::memset(out, 0, sizeof *out);
+  if (!c->have_sph) return set_err(c, PM_E_STATE, "pm_set_sph not called");
+  if (c->dist) return set_err(c, PM_E_STATE, "pm_sph_run: single (non-decomposed) context only");
+  if (!(cfl > 0.f) || nsteps < 0 || every < 0)
+    return set_err(c, PM_E_INVAL, "pm_sph_run: cfl must be > 0, nsteps and every >= 0");
+  if (!(c->skin > 0.f))
+    return set_err(c, PM_E_INVAL, "pm_sph_run: needs a Verlet skin > 0 (pm_set_cutoff)");
+  cudaSetDevice(c->device);
+  if (nsteps == 0) return PM_OK;
+  Bufs &B = c->B;
+  for (int b = 0; b < 2; ++b) {
+    if (!B.vold[b]) CUDA_TRY(c, dalloc(&B.vold[b], c->pcap));
+    if (!B.rold[b]) CUDA_TRY(c, dalloc(&B.rold[b], c->pcap));
+  }
+  if (!B.drho) CUDA_TRY(c, dalloc(&B.drho, c->pcap));
+  if (!c->P.sph_state) {  // the cell-sort reorder now carries the stepping state
+    c->P.sph_state = 1;
+    destroy_graph(c);
+  }
+  if (!c->list_valid) {
+    s = build_list(c);
+    if (s) return s;
+  }
+  if (!c->rho_valid) {
+    launch_sph_density(c->P, B, c->n, c->stream);
+    c->rho_valid = true;
+  }
+  s = read_state(c);
+  if (s) return s;
+  const long long reb0 = c->st_h->n_rebuilds;
+  launch_sph_init_run(B, c->n, c->stream);
+  k_clear_rebuild<<<1, 1, 0, c->stream>>>(B.st);
+  int64_t done = 0;
+  for (; done < nsteps; ++done) {
+    s = read_state(c);  // the rebuild decision of the previous step
+    if (s) return s;
+    if (c->st_h->abort) break;
+    if (c->st_h->need_rebuild) {
+      enqueue_rebuild(c, c->stream, 1);
+      s = sync_check(c, "pm_sph_run (rebuild)");
+      if (s == PM_E_CAPACITY) {  // grow the rows and rebuild from the sorted order
+        c->sticky = 0;
+        c->err.clear();
+        k_clear_abort<<<1, 1, 0, c->stream>>>(B.st);
+        s = layout_from_counts(c);
+        if (s) return s;
+        launch_verlet(c->P, B, c->n, c->stream);
+        s = sync_check(c, "pm_sph_run (rebuild retry)");
+      }
+      if (s) return s;
+    }
+    launch_sph_step(c->P, B, c->n, cfl, every, c->stream);
+    k_apply_pending<<<1, 1, 0, c->stream>>>(B.st);
+  }
+  s = read_state(c);
+  if (s) return s;
+  if (c->st_h->abort)
+    return set_err(c, c->st_h->abort, "pm_sph_run: %s (gid %lld) after %lld steps",
+                   device_error_name(c->st_h->abort), (long long)c->st_h->err_gid,
+                   (long long)done);
+  c->forces_valid = false;  // force[] holds the last step's accelerations
+  c->rho_valid = true;
+  if (out) {
+    out->steps = done;
+    out->rebuilds = c->st_h->n_rebuilds - reb0;
+    out->time = c->st_h->sph_time;
+    out->dt_min = c->st_h->sph_dt_min;
+    out->dt_max = c->st_h->sph_dt_max;
+    out->dt_last = c->st_h->sph_dt;
+  }
+  return check_launch(c, "pm_sph_run");
+}
+
 pm_status pm_step_vv(pm_ctx c, float dt, int64_t nsteps, pm_run_stats *out) {
   pm_status s = check_ready(c);
   if (s) return s;
@@ -984,7 +1071,8 @@ pm_status pm_get_state(pm_ctx c, float *pos4, float *vel4, float *force4, int64_
   if (gid) CUDA_TRY(c, cudaMemcpyAsync(gid, c->B.gid[ci], 8 * n, k, c->stream));
   if (rho || pres) {
     std::vector<float2> rp((size_t)n);
-    CUDA_TRY(c, cudaMemcpyAsync(rp.data(), c->B.rhoP, 8 * n, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(rp.data(), c->B.rhoP[ci], 8 * n, cudaMemcpyDeviceToHost,
+                                c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     for (int64_t i = 0; i < n; ++i) {
       if (rho) rho[i] = rp[(size_t)i].x;

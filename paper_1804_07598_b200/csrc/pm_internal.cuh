@@ -86,6 +86,7 @@ struct Params {
   int nbr_cap;      // slots per row (multiple of 4)
   int dist;         // 1: sub-domain context (ghosts present, skip them as rows)
   float vmax;       // velocity limit (reading R22), 0 = off
+  int sph_state;    // 1: the cell-sort reorder also permutes the SPH stepping state
 };
 
 // Device buffers (pointers fixed between reallocations; captured in graphs).
@@ -97,7 +98,11 @@ struct Bufs {
   int32_t *kind[2];
   float4 *xref;        // positions at the last build (cell order)
   float4 *force;       // forces / SPH accelerations (current order)
-  float2 *rhoP;        // SPH density, pressure (current order)
+  float2 *rhoP[2];     // SPH density, pressure (by State::cur_id: the stepping
+                       // reorder permutes them with the particles)
+  float4 *vold[2];     // SPH stepping: velocities of the previous step (Verlet)
+  float *rold[2];      // SPH stepping: densities of the previous step
+  float *drho;         // SPH stepping: density rate (Eq. 2), current order
   int32_t *cell_of;    // cell id in the storage order the build started from
   int32_t *slot;       // unordered slot within the cell (atomic claim)
   int32_t *count;      // [ncell]
@@ -134,6 +139,13 @@ struct State {
   long long coinc_gid;  // a particle with a coincident partner (-1: none), set
                         // by the cell sort, raised as PM_E_COINCIDENT by the
                         // Verlet build (the cell list itself is well defined)
+  // SPH time stepping (pm_sph_run)
+  unsigned dtf_bits;    // min over fluid of sqrt(h/|a|) (fp32 bits; >= 0 so uint order)
+  unsigned dtcv_bits;   // min over particles of h/(c0 + max |mu|)
+  float sph_dt;         // step size of the current step
+  float sph_dt_min, sph_dt_max;
+  long long sph_step;   // steps taken (Euler step every `every`)
+  double sph_time;      // simulated time
   double acc[4];        // energy: U_raw, virial, npairs, KE
 };
 
@@ -244,6 +256,9 @@ void launch_step_begin(const Bufs &B, cudaGraphConditionalHandle h, int use_hand
 void launch_ke(const Params &P, const Bufs &B, int64_t n, cudaStream_t s);
 void launch_sph_density(const Params &P, const Bufs &B, int64_t n, cudaStream_t s);
 void launch_sph_forces(const Params &P, const Bufs &B, int64_t n, cudaStream_t s);
+void launch_sph_init_run(const Bufs &B, int64_t n, cudaStream_t s);
+void launch_sph_step(const Params &P, const Bufs &B, int64_t n, float cfl, int every,
+                     cudaStream_t s);
 void launch_verlet_export(const Bufs &B, int64_t n, const int64_t *row_ptr, int64_t *col_gid,
                           cudaStream_t s);
 void launch_lj_step_mode(const Params &P, const Bufs &B, int64_t n, float dt, int mode,

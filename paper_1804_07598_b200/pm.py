@@ -41,6 +41,11 @@ class SPHParams(C.Structure):
                 ("g", C.c_float * 3)]
 
 
+class SPHRunStats(C.Structure):
+    _fields_ = [("steps", C.c_int64), ("rebuilds", C.c_int64), ("time", C.c_double),
+                ("dt_min", C.c_float), ("dt_max", C.c_float), ("dt_last", C.c_float)]
+
+
 class RunStats(C.Structure):
     _fields_ = [("steps", C.c_int64), ("rebuilds", C.c_int64), ("max_row", C.c_int32),
                 ("nbr_cap", C.c_int32), ("mean_row", C.c_double)]
@@ -76,6 +81,7 @@ def lib(path: str = LIB_PATH):
         "pm_compute_lj": (st, [vp, C.c_int32]),
         "pm_sph_density": (st, [vp]),
         "pm_sph_forces": (st, [vp]),
+        "pm_sph_run": (st, [vp, C.c_int64, C.c_float, C.c_int32, C.POINTER(SPHRunStats)]),
         "pm_step_vv": (st, [vp, C.c_float, C.c_int64, C.POINTER(RunStats)]),
         "pm_count": (st, [vp, vp, vp, vp, vp]),
         "pm_get_cells": (st, [vp, vp, vp, vp]),
@@ -214,6 +220,13 @@ class Context:
 
     def sph_forces(self):
         self._check(self.L.pm_sph_forces(self.h))
+
+    def sph_run(self, nsteps, cfl=0.2, every=40):
+        """WCSPH time stepping (pm_sph_run): continuity density, Verlet scheme."""
+        rs = SPHRunStats()
+        self._check(self.L.pm_sph_run(self.h, int(nsteps), float(cfl), int(every), C.byref(rs)))
+        return dict(steps=rs.steps, rebuilds=rs.rebuilds, time=rs.time, dt_min=rs.dt_min,
+                    dt_max=rs.dt_max, dt_last=rs.dt_last)
 
     def step_vv(self, dt, nsteps):
         rs = RunStats()

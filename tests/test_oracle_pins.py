@@ -410,3 +410,56 @@ def test_sph_momentum_conservation_random(orc):
                            s.periodic, p)
     net = (a - np.asarray(p["g"])).sum(0)
     assert np.all(np.abs(net) < 1e-9 * np.abs(a - np.asarray(p["g"])).sum())
+
+
+# ------------------------------------------------------------------ WCSPH stepping (NEXT-3)
+def _sph_params(h=0.01, c0=44.294):
+    return dict(h=h, mass=1e-3, rho0=1000.0, b=c0 * c0 * 1000.0 / 7.0, gamma=7.0, alpha=0.1,
+                c0=c0, eta2=0.01 * h * h, g=(0.0, 0.0, -9.81))
+
+
+def test_sph_run_free_fall_is_exact(orc):
+    """An isolated fluid particle: D = 0, a = g.  The Verlet scheme (reading
+    R27) integrates constant acceleration exactly, so x(t) = x0 + g t^2 / 2
+    and v(t) = g t with t = sum dt; dt (R28) = cfl * min(sqrt(h/|g|), h/c0)."""
+    p = _sph_params()
+    pos = np.array([[0.5, 0.5, 0.5, 0.0]], np.float32)
+    vel = np.zeros((1, 4), np.float32)
+    x, v, rho, dt = orc.sph_run(pos, vel, np.array([1000.0]), np.zeros(1, np.int32), [0, 0, 0],
+                                [1, 1, 1], [0, 0, 0], p, 120, cfl=0.2, every=40)
+    dt_ref = 0.2 * min(math.sqrt(p["h"] / 9.81), p["h"] / p["c0"])
+    assert np.allclose(dt, dt_ref, rtol=1e-14)
+    t = dt.sum()
+    assert x[0, 2] == pytest.approx(0.5 - 0.5 * 9.81 * t * t, abs=1e-14)
+    assert v[0, 2] == pytest.approx(-9.81 * t, rel=1e-12)
+    assert rho[0] == 1000.0 and x[0, 0] == 0.5 and v[0, 0] == 0.0
+
+
+def test_sph_run_continuity_sign(orc):
+    """Eq. 2 with reading R26: approaching particles compress
+    (density rises), receding ones expand; the two densities stay equal."""
+    p = dict(_sph_params(), g=(0.0, 0.0, 0.0), alpha=0.0)
+    for vx, sign in ((1.0, 1.0), (-1.0, -1.0)):
+        pos = np.array([[0.5, 0.5, 0.5, 0], [0.51, 0.5, 0.5, 0]], np.float32)
+        vel = np.array([[vx, 0, 0, 0], [-vx, 0, 0, 0]], np.float32)
+        _, _, rho, _ = orc.sph_run(pos, vel, np.array([1000.0, 1000.0]), np.zeros(2, np.int32),
+                                   [0, 0, 0], [1, 1, 1], [0, 0, 0], p, 3)
+        assert sign * (rho[0] - 1000.0) > 0
+        assert rho[0] == pytest.approx(rho[1], rel=1e-14)
+
+
+def test_sph_run_conserves_momentum(orc):
+    """No gravity, no boundary particles, periodic box: the pair terms of
+    Eq. 1 are antisymmetric, and the leapfrog update v' = v_prev + 2 dt a
+    (and the Euler steps) keeps sum m v constant."""
+    s = inputs.random_box(300, 0.1, (77,), periodic=(1, 1, 1))
+    p = dict(_sph_params(h=0.012), g=(0.0, 0.0, 0.0))
+    rng = np.random.default_rng(5)
+    vel = np.zeros((s.n, 4), np.float32)
+    vel[:, :3] = rng.uniform(-0.5, 0.5, (s.n, 3)).astype(np.float32)
+    rho0 = np.full(s.n, 1000.0)
+    x, v, rho, dt = orc.sph_run(s.pos, vel, rho0, np.zeros(s.n, np.int32), s.lo, s.hi,
+                                s.periodic, p, 25, every=10)
+    m0 = vel[:, :3].astype(np.float64).sum(axis=0)
+    assert np.max(np.abs(v.sum(axis=0) - m0)) < 1e-11 * np.abs(vel[:, :3]).sum()
+    assert np.all(dt > 0) and np.all(np.isfinite(rho))
