@@ -156,6 +156,11 @@ pm_status pm_sph_forces(pm_ctx ctx);
  * Single context only (PM_E_STATE on a decomposed context).  Errors:
  * PM_E_NONFINITE (rates or dt), PM_E_DOMAIN (a fluid particle left an open
  * axis).  out may be NULL. */
+/* Set the SPH densities (n floats, in the CURRENT internal order -- the order
+ * pm_get_state returns) and their pressures by the Tait EOS (Eq. 3); e.g. a
+ * hydrostatic initial profile for pm_sph_run.  mem: PM_HOST / PM_DEVICE. */
+pm_status pm_set_rho(pm_ctx ctx, const float *rho, int32_t mem);
+
 typedef struct {
   int64_t steps;     /* steps completed */
   int64_t rebuilds;  /* Verlet rebuilds during the call */

@@ -333,6 +333,11 @@ __global__ void __launch_bounds__(256) k_sph_verlet(Params P, Bufs B, int n) {
   if (blockIdx.x == 0 && threadIdx.x == 0) st->pending_flip = 1;
 }
 
+__global__ void __launch_bounds__(256) k_sph_set_rho(Params P, Bufs B, int n, const float *rho) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) B.rhoP[B.st->cur_id][i] = make_float2(rho[i], tait(P, rho[i]));
+}
+
 __global__ void __launch_bounds__(256) k_sph_init_run(Bufs B, int n) {
   State *st = B.st;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -362,6 +367,11 @@ void launch_sph_density(const Params &P, const Bufs &B, int64_t n, cudaStream_t 
 
 void launch_sph_forces(const Params &P, const Bufs &B, int64_t n, cudaStream_t s) {
   if (n > 0) k_sph_forces<<<nb(n), 256, 0, s>>>(P, B, (int)n);
+}
+
+void launch_sph_set_rho(const Params &P, const Bufs &B, int64_t n, const float *rho,
+                        cudaStream_t s) {
+  if (n > 0) k_sph_set_rho<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, B, (int)n, rho);
 }
 
 void launch_sph_init_run(const Bufs &B, int64_t n, cudaStream_t s) {

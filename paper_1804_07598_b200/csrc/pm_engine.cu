@@ -856,6 +856,29 @@ pm_status pm_sph_forces(pm_ctx c) {
   return sync_check(c, "pm_sph_forces");
 }
 
+pm_status pm_set_rho(pm_ctx c, const float *rho, int32_t mem) {
+  pm_status s = check_ready(c);
+  if (s) return s;
+  if (!rho) return PM_E_INVAL;
+  if (!c->have_sph) return set_err(c, PM_E_STATE, "pm_set_sph not called");
+  cudaSetDevice(c->device);
+  const int64_t n = c->n;
+  if (n == 0) return PM_OK;
+  const float *d = rho;
+  float *tmp = nullptr;
+  if (mem != PM_DEVICE) {
+    CUDA_TRY(c, cudaMalloc((void **)&tmp, 4 * n));
+    CUDA_TRY(c, cudaMemcpyAsync(tmp, rho, 4 * n, cudaMemcpyHostToDevice, c->stream));
+    d = tmp;
+  }
+  launch_sph_set_rho(c->P, c->B, n, d, c->stream);
+  s = sync_check(c, "pm_set_rho");
+  if (tmp) cudaFree(tmp);
+  if (s) return s;
+  c->rho_valid = true;
+  return PM_OK;
+}
+
 pm_status pm_sph_run(pm_ctx c, int64_t nsteps, float cfl, int32_t every,
                      pm_sph_run_stats *out) {
   pm_status s = check_ready(c);

@@ -257,6 +257,8 @@ void launch_ke(const Params &P, const Bufs &B, int64_t n, cudaStream_t s);
 void launch_sph_density(const Params &P, const Bufs &B, int64_t n, cudaStream_t s);
 void launch_sph_forces(const Params &P, const Bufs &B, int64_t n, cudaStream_t s);
 void launch_sph_init_run(const Bufs &B, int64_t n, cudaStream_t s);
+void launch_sph_set_rho(const Params &P, const Bufs &B, int64_t n, const float *rho,
+                        cudaStream_t s);
 void launch_sph_step(const Params &P, const Bufs &B, int64_t n, float cfl, int every,
                      cudaStream_t s);
 void launch_verlet_export(const Bufs &B, int64_t n, const int64_t *row_ptr, int64_t *col_gid,

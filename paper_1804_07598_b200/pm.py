@@ -82,6 +82,7 @@ def lib(path: str = LIB_PATH):
         "pm_sph_density": (st, [vp]),
         "pm_sph_forces": (st, [vp]),
         "pm_sph_run": (st, [vp, C.c_int64, C.c_float, C.c_int32, C.POINTER(SPHRunStats)]),
+        "pm_set_rho": (st, [vp, vp, C.c_int32]),
         "pm_step_vv": (st, [vp, C.c_float, C.c_int64, C.POINTER(RunStats)]),
         "pm_count": (st, [vp, vp, vp, vp, vp]),
         "pm_get_cells": (st, [vp, vp, vp, vp]),
@@ -220,6 +221,11 @@ class Context:
 
     def sph_forces(self):
         self._check(self.L.pm_sph_forces(self.h))
+
+    def set_rho(self, rho):
+        """Densities in the current internal order (as get_state returns them)."""
+        r = np.ascontiguousarray(rho, dtype=np.float32)
+        self._check(self.L.pm_set_rho(self.h, r.ctypes.data, PM_HOST))
 
     def sph_run(self, nsteps, cfl=0.2, every=40):
         """WCSPH time stepping (pm_sph_run): continuity density, Verlet scheme."""

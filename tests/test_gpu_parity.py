@@ -498,10 +498,18 @@ def test_tiny_and_ragged_sizes(pm, orc):
         c.close()
 
 
+def hydrostatic_rho(z, p):
+    """Initial density of a fluid column at rest (the DualSPHysics dam-break
+    start): P = rho0 |g| (h_swl - z) for z < h_swl, rho = rho0 (1 + P/b)^(1/gamma)
+    (the Tait EOS Eq. 3 inverted); rho0 above the surface."""
+    P = p["rho0"] * 9.81 * np.maximum(p["h_swl"] - np.asarray(z, np.float64), 0.0)
+    return (p["rho0"] * (1.0 + P / p["b"]) ** (1.0 / p["gamma"])).astype(np.float32)
+
+
 def test_sph_run_parity_small_dam(pm, orc):
     """WCSPH time stepping (pm_sph_run, readings R26-R28)
-    against the fp64 oracle (oracle.sph_run): a dp = 1/16 dam-break block,
-    densities from the summation pass, 30 Verlet steps with dynamic dt and an
+    against the fp64 oracle (oracle.sph_run): a dp = 1/16 dam-break block
+    with a hydrostatic initial density, 30 Verlet steps with dynamic dt and an
     Euler step every 10.  fp32 state on the GPU, fp64 in the oracle: dt per
     step, positions, velocities and densities must agree closely over this
     short horizon."""
@@ -513,9 +521,9 @@ def test_sph_run_parity_small_dam(pm, orc):
     c.set_sph(p)
     c.place(s.pos, s.vel, s.gid, s.kind)
     c.build_verlet()
-    c.sph_density()
     st0 = c.get_state()
-    rho_init = st0["rho"][np.argsort(st0["gid"])].astype(np.float64)
+    c.set_rho(hydrostatic_rho(st0["pos"][:, 2], p))
+    rho_init = hydrostatic_rho(s.pos[:, 2], p).astype(np.float64)
     nsteps = 30
     r = c.sph_run(nsteps, cfl=0.2, every=10)
     assert r["steps"] == nsteps
