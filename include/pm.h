@@ -256,6 +256,16 @@ int32_t pm_record_bytes(int32_t what);
  * thinner than 2 r_v. */
 pm_status pm_set_decomposition(pm_ctx ctx, const int32_t pgrid[3], const int32_t pcoord[3]);
 
+/* The same with load-balanced (non-uniform) cuboids (
+ * PAPER.md:122, §3.5 dynamic load balancing): cuts holds the interior cut
+ * positions of axis x (pgrid[0]-1 floats, increasing), then y, then z; a
+ * particle belongs to slab c = #{k : x >= cut_k} along each axis (exact fp32
+ * compares).  The cuts are a tensor product, so neighbours stay the 26 grid
+ * directions.  Errors: PM_E_INVAL for more than 15 cuts per axis, cuts not
+ * increasing inside the box, or a slab thinner than 2 r_v. */
+pm_status pm_set_decomposition_cuts(pm_ctx ctx, const int32_t pgrid[3], const int32_t pcoord[3],
+                                    const float *cuts);
+
 /* Build the outgoing message lists of kind `what` (MIGRATE: owned particles
  * whose owner changed -- counts[13] = particles that stay; GHOST: owned
  * particles within r_v of each neighbour face/edge/corner, up to 7 copies).

@@ -24,8 +24,15 @@ namespace {
 
 constexpr int kDirBlock = 256;
 
-// owner coordinate along a decomposed axis (pinned fp32 rule, like R3)
+// owner coordinate along a decomposed axis: the pinned fp32 rule (like R3)
+// for equal cuboids, or the number of cut positions <= x for the
+// load-balanced cuts of pm_set_decomposition_cuts (exact fp32 compares)
 __device__ __forceinline__ int owner_coord(const Dist &D, int d, float x) {
+  if (D.cuts) {
+    int c = 0;
+    for (int k = 0; k < D.p[d] - 1; ++k) c += (x >= D.cut[d][k]) ? 1 : 0;
+    return c;
+  }
   return cell_coord(x, D.glo[d], D.inv_s[d], D.p[d]);
 }
 

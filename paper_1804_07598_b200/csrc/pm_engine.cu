@@ -1195,6 +1195,42 @@ pm_status pm_set_decomposition(pm_ctx c, const int32_t pgrid[3], const int32_t p
   return setup_grid(c);
 }
 
+pm_status pm_set_decomposition_cuts(pm_ctx c, const int32_t pgrid[3], const int32_t pcoord[3],
+                                    const float *cuts) {
+  if (!c || !pgrid || !pcoord || !cuts) return PM_E_INVAL;
+  pm_status s = pm_set_decomposition(c, pgrid, pcoord);  // checks grid, periodicity
+  if (s) return s;
+  Dist D = c->D;
+  const Box &b = c->P.box;
+  D.cuts = 1;
+  int off = 0;
+  for (int d = 0; d < 3; ++d) {
+    const int p = pgrid[d];
+    if (p - 1 > kMaxCuts)
+      return set_err(c, PM_E_INVAL, "pm_set_decomposition_cuts: more than %d cuts on axis %d",
+                     kMaxCuts, d);
+    float prev = b.lo[d];
+    for (int k = 0; k < p - 1; ++k) {
+      const float x = cuts[off + k];
+      if (!(x > prev) || !(x < b.hi[d]) || (double)x - (double)prev < 2.0 * (double)D.rg)
+        return set_err(c, PM_E_INVAL,
+                       "pm_set_decomposition_cuts: cut %d on axis %d (%g) not increasing inside "
+                       "the box with slabs >= 2 r_v",
+                       k, d, (double)x);
+      D.cut[d][k] = x;
+      prev = x;
+    }
+    if (p >= 2 && (double)b.hi[d] - (double)prev < 2.0 * (double)D.rg)
+      return set_err(c, PM_E_INVAL, "pm_set_decomposition_cuts: last slab on axis %d < 2 r_v",
+                     d);
+    D.slo[d] = pcoord[d] == 0 ? b.lo[d] : cuts[off + pcoord[d] - 1];
+    D.shi[d] = pcoord[d] == p - 1 ? b.hi[d] : cuts[off + pcoord[d]];
+    off += p - 1;
+  }
+  c->D = D;
+  return setup_grid(c);
+}
+
 pm_status pm_dist_plan(pm_ctx c, int32_t what, const int32_t order[26], int64_t counts[27]) {
   pm_status s = check_ready(c);
   if (s) return s;

@@ -47,11 +47,16 @@ struct Grid {
 // Decomposition of the global periodic box into p[0] x p[1] x p[2] cuboids;
 // this context owns cuboid c.  Ownership along axis d: the pinned fp32 rule
 // min(max(floor(fl(fl(x - glo) * inv_s)), 0), p - 1).
+constexpr int kMaxCuts = 15;  // non-uniform cuts: at most 16 slabs per axis
+
 struct Dist {
   int p[3], c[3];
   float glo[3], inv_s[3];
   float slo[3], shi[3];  // this sub-domain (fp32)
   float rg;              // ghost selection width (r_v with a 1e-5 margin)
+  int cuts;              // 1: ownership by the cut positions below (load balancing)
+  float cut[3][kMaxCuts];  // interior cut positions per axis, increasing: slab c =
+                           // #{k : x >= cut[d][k]}
 };
 
 constexpr int kGhostBit = 1 << 30;  // kind flag of a ghost copy

@@ -42,9 +42,12 @@ def dir_index(a):
 
 @dataclass
 class Decomp:
-    """px x py x pz cuboids; rank = cx + px (cy + py cz)."""
+    """px x py x pz cuboids; rank = cx + px (cy + py cz).  cuts: None (equal
+    cuboids) or, per axis, the grid[d]-1 interior cut positions of a
+    load-balanced tensor-product decomposition (pm_set_decomposition_cuts)."""
 
     grid: tuple
+    cuts: tuple = None
 
     @property
     def size(self):
@@ -359,7 +362,10 @@ def make_member(system, decomp, rank, device=0, stream=None, rc=2.5, skin=0.3, r
     ctx.set_domain(system.lo, system.hi, system.periodic)
     ctx.set_cutoff(rc, skin)
     ctx.set_lj(1.0, 1.0, 1.0, r_min)
-    ctx.set_decomposition(decomp.grid, decomp.coord(rank))
+    if decomp.cuts is None:
+        ctx.set_decomposition(decomp.grid, decomp.coord(rank))
+    else:
+        ctx.set_decomposition_cuts(decomp.grid, decomp.coord(rank), decomp.cuts)
     ctx.place(system.pos, system.vel, system.gid, system.kind)
     return ctx
 
@@ -372,10 +378,88 @@ def owner_of(system, decomp):
     c = np.zeros((system.n, 3), np.int64)
     for d in range(3):
         p = decomp.grid[d]
+        if decomp.cuts is not None:  # slab = number of cuts <= x (fp32 compares)
+            cuts = np.asarray(decomp.cuts[d], np.float32)
+            c[:, d] = (system.pos[:, d, None] >= cuts[None, :]).sum(axis=1)
+            continue
         inv = np.float32(p / float(L[d]))
         u = (system.pos[:, d] - lo[d]).astype(np.float32) * inv
         c[:, d] = np.clip(np.floor(u.astype(np.float32)), 0, p - 1)
     return c[:, 0] + decomp.grid[0] * (c[:, 1] + decomp.grid[1] * c[:, 2])
+
+
+# ---------------------------------------------------------------- load balancing (NEXT-2)
+def weighted_cuts(x, w, p, lo, hi, min_width):
+    """Interior cut positions splitting [lo, hi) into p slabs of (nearly) equal
+    total weight -- the weighted quantiles k/p of the coordinates x -- then
+    moved apart so that every slab is at least min_width wide (PAPER.md:122,
+    §3.5: re-balance the work; the per-particle weight is its pair count).
+    Returns float32 cuts, increasing."""
+    x = np.asarray(x, np.float64)
+    w = np.asarray(w, np.float64)
+    if p <= 1:
+        return np.zeros(0, np.float32)
+    if x.size == 0 or w.sum() <= 0:
+        cuts = lo + (hi - lo) * np.arange(1, p) / p
+    else:
+        o = np.argsort(x, kind="stable")
+        xs, cw = x[o], np.cumsum(w[o])
+        targets = cw[-1] * np.arange(1, p) / p
+        k = np.searchsorted(cw, targets)
+        cuts = xs[np.minimum(k, xs.size - 1)]
+    cuts = np.asarray(cuts, np.float64)
+    # enforce the minimum slab width: forward, then backward passes
+    span = hi - lo
+    if span < p * min_width * (1 + 1e-6):
+        raise ValueError("box too small for p slabs of min_width")
+    mw = min_width * (1 + 1e-5)
+    for i in range(p - 1):
+        cuts[i] = max(cuts[i], (cuts[i - 1] if i else lo) + mw)
+    for i in range(p - 2, -1, -1):
+        cuts[i] = min(cuts[i], (cuts[i + 1] if i < p - 2 else hi) - mw)
+    return cuts.astype(np.float32)
+
+
+def balanced_decomp(grid, pos, weights, lo, hi, rv):
+    """Tensor-product load-balanced cuts: per axis, weighted quantiles of all
+    particles' coordinates (identical on every rank given the same global
+    data, e.g. all-reduced histograms)."""
+    cuts = tuple(weighted_cuts(pos[:, d], weights, grid[d], float(lo[d]), float(hi[d]),
+                               2.0 * rv * (1 + 1e-5)) for d in range(3))
+    return Decomp(tuple(grid), cuts)
+
+
+def imbalance(work):
+    """max / mean of the per-rank work (1.0 = perfectly balanced)."""
+    work = np.asarray(list(work), np.float64)
+    return float(work.max() / work.mean()) if work.size and work.mean() > 0 else 1.0
+
+
+class SAR:
+    """Stop-At-Rise re-balancing trigger (PAPER.md:122 '[56]'):
+    per step record the degradation delta = max - mean of the per-rank step
+    times; W(n) = (C + sum delta) / n with C the cost of a re-balance;
+    re-balance at the first rise W(n) > W(n-1) (W(0) = +inf)."""
+
+    def __init__(self, cost):
+        self.C = float(cost)
+        self.reset()
+
+    def reset(self, cost=None):
+        if cost is not None:
+            self.C = float(cost)
+        self.n, self.sum, self.W = 0, 0.0, float("inf")
+
+    def record(self, per_rank_times):
+        t = np.asarray(per_rank_times, np.float64)
+        self.sum += float(t.max() - t.mean())
+        self.n += 1
+
+    def decide(self):
+        W = (self.C + self.sum) / self.n
+        rise = W > self.W
+        self.W = W
+        return rise
 
 
 # ---------------------------------------------------------------- bench (N>1)

@@ -95,6 +95,7 @@ def lib(path: str = LIB_PATH):
         "pm_get_profile": (st, [vp, vp, vp, vp, vp]),
         "pm_record_bytes": (C.c_int32, [C.c_int32]),
         "pm_set_decomposition": (st, [vp, vp, vp]),
+        "pm_set_decomposition_cuts": (st, [vp, vp, vp, vp]),
         "pm_dist_plan": (st, [vp, C.c_int32, vp, vp]),
         "pm_dist_pack": (st, [vp, C.c_int32, vp]),
         "pm_dist_unpack": (st, [vp, C.c_int32, vp, C.c_int64]),
@@ -335,6 +336,15 @@ class DistContext(Context):
         g = np.ascontiguousarray(grid, np.int32)
         c = np.ascontiguousarray(coord, np.int32)
         self._check(self.L.pm_set_decomposition(self.h, g.ctypes.data, c.ctypes.data))
+
+    def set_decomposition_cuts(self, grid, coord, cuts):
+        """cuts: per-axis sequences of interior cut positions (len grid[d]-1)."""
+        g = np.ascontiguousarray(grid, np.int32)
+        c = np.ascontiguousarray(coord, np.int32)
+        flat = np.ascontiguousarray(np.concatenate([np.asarray(cuts[d], np.float32).reshape(-1)
+                                                    for d in range(3)] + [np.zeros(1, np.float32)]))
+        self._check(self.L.pm_set_decomposition_cuts(self.h, g.ctypes.data, c.ctypes.data,
+                                                     flat.ctypes.data))
 
     def dist_plan(self, what, order):
         o = np.ascontiguousarray(order, np.int32)

@@ -139,3 +139,51 @@ def test_message_protocol_gloo_world2(grid):
         _, arrived, recv_counts = res[r]
         assert arrived == expect
         assert recv_counts[q_] == len(expect)
+
+
+# ---------------------------------------------------------------- load balancing (NEXT-2)
+def test_sar_stop_at_rise_examples():
+    """SPEC.md:512-517 worked examples of the Stop-At-Rise rule W(n) =
+    (C + sum delta)/n, re-balance at the first rise."""
+    from paper_1804_07598_b200.dist import SAR
+    s = SAR(10.0)
+    out = []
+    for times in ([1.0, 1.0], [2.0, 2.0]):  # delta 0, 0 -> W = 10, 5
+        s.record(times)
+        out.append(s.decide())
+    assert out == [False, False]
+    s.record([60.0, 0.0])  # delta 30 -> W = 40/3 > 5
+    assert s.decide() is True
+    s.reset()
+    assert not any((s.record([2.0, 0.0]), s.decide())[1] for _ in range(50))  # (10+n)/n falls
+
+
+def test_weighted_cuts_balance_and_min_width():
+    from paper_1804_07598_b200.dist import weighted_cuts
+    rng = np.random.default_rng(3)
+    x = rng.uniform(0, 100, 200000)
+    c = weighted_cuts(x, np.ones_like(x), 4, 0.0, 100.0, 5.0)
+    assert np.allclose(c, [25, 50, 75], atol=0.5)
+    # a hotspot: 80% of the weight in [0, 20) pulls the cuts left
+    w = np.where(x < 20, 16.0, 1.0)
+    c = weighted_cuts(x, w, 4, 0.0, 100.0, 5.0)
+    parts = [w[(x >= a) & (x < b)].sum() for a, b in zip([0, *c], [*c, 100])]
+    assert max(parts) / np.mean(parts) < 1.02
+    assert c[0] < 10 and np.all(np.diff(np.concatenate([[0], c, [100]])) >= 5.0)
+    # the minimum width wins over the balance
+    c = weighted_cuts(x, np.where(x < 2, 1e6, 1.0), 4, 0.0, 100.0, 5.0)
+    assert np.all(np.diff(np.concatenate([[0], c, [100]])) >= 5.0 - 1e-9)
+
+
+def test_owner_of_cuts_rule():
+    """Ownership with cuts: slab = number of cuts <= x (the rule k_dist.cu
+    applies); equal cuts reproduce the slabs of the uniform rule away from
+    the rounding-sensitive faces."""
+    from paper_1804_07598_b200 import dist, inputs
+    s = inputs.random_box(5000, 40.0, (9,))
+    D = dist.Decomp((2, 2, 1), cuts=(np.array([13.0], np.float32), np.array([30.0], np.float32),
+                                     np.zeros(0, np.float32)))
+    own = dist.owner_of(s, D)
+    cx = (s.pos[:, 0] >= 13.0).astype(int)
+    cy = (s.pos[:, 1] >= 30.0).astype(int)
+    assert np.array_equal(own, cx + 2 * cy)

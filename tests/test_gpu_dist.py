@@ -150,3 +150,51 @@ def test_bench_torchrun_two_ranks_share_one_gpu(env, tmp_path):
     b = json.loads(lines[0])
     assert b["n_gpus"] == 2 and b["config"]["n_particles"] == 2 * 32 ** 3
     assert b["value"] > 0 and b["e2e"]["value"] > 0
+
+
+def test_load_balanced_cuts_clustered(env):
+    """SURVEY NEXT-2 (§3.5): on a clustered system (cfg5-like,
+    8 Gaussian clusters) the tensor-product cuts at weighted quantiles of the
+    pair counts lower the per-sub-domain work imbalance (max/mean list
+    entries) of a 2x2x2 decomposition, and the balanced decomposition gives
+    the same neighbour sets and forces as one context."""
+    import torch
+    pm, dist = env
+    s = inputs.cfg5(n_clusters=8, per_cluster=8192, sigma_c=6.0, rho=0.3, key=55)
+    ref = pm.Context()
+    ref.set_domain(s.lo, s.hi, s.periodic)
+    ref.set_cutoff(2.5, 0.3)
+    ref.set_lj(1.0, 1.0, 1.0, 0.8)
+    ref.place(s.pos, s.vel, s.gid)
+    ref.build_verlet()
+    ref.compute_lj()
+    rst = pm.sorted_by_gid(ref.get_state())
+    rp, _ = ref.get_verlet()
+    w = np.zeros(s.n)
+    w[ref.get_state()["gid"]] = np.diff(rp)  # pair work per particle (by gid)
+    rv = np.float32(2.8)
+
+    def run(D):
+        owner = dist.owner_of(s, D)
+        stream = torch.cuda.Stream()
+        members = {r: dist.make_member(s.subset(np.where(owner == r)[0]), D, r, stream=stream,
+                                       r_min=0.8) for r in range(D.size)}
+        sim = dist.DistSim(D, members, dist.LoopbackTransport(members), stream=stream)
+        sim.start()
+        work = [ctx.count()["nnz"] for ctx in sim.m.values()]
+        got = pm.sorted_by_gid(
+            {k: np.concatenate([ctx.owned_state()[k] for ctx in sim.m.values()])
+             for k in ("gid", "force")})
+        for ctx in sim.m.values():
+            ctx.close()
+        return work, got
+
+    w_uni, _ = run(dist.Decomp((2, 2, 2)))
+    Db = dist.balanced_decomp((2, 2, 2), s.pos[:, :3], w, s.lo, s.hi, float(rv))
+    w_bal, got = run(Db)
+    assert sum(w_uni) == sum(w_bal)  # same pairs, other owners
+    assert dist.imbalance(w_bal) < dist.imbalance(w_uni)
+    assert np.array_equal(got["gid"], np.sort(s.gid))
+    F, Fr = got["force"][:, :3].astype(np.float64), rst["force"][:, :3].astype(np.float64)
+    assert np.max(np.abs(F - Fr)) / np.sqrt(np.mean(Fr ** 2)) <= 1e-4
+    ref.close()
