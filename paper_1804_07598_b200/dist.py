@@ -180,6 +180,87 @@ class LoopbackTransport:
 
 
 # ---------------------------------------------------------------- simulation
+class HybridTransport:
+    """Over-decomposition (the paper assigns sub-sub-domains
+    to processors): several sub-domains per process.
+    Messages between local sub-domains are device copies; all messages from
+    this process to one remote process travel as ONE point-to-point transfer
+    (torch.distributed, NCCL on GPUs), concatenated in (sender, receiver)
+    sub-domain order, and are split the same way on arrival.
+
+    assign[sd] = rank of sub-domain sd; local = the sub-domains of this
+    process; torch_tr = TorchTransport (None: every sub-domain is local)."""
+
+    def __init__(self, assign, my_rank, torch_tr=None):
+        self.assign = np.asarray(assign, np.int64)
+        self.rank = int(my_rank)
+        self.tr = torch_tr
+        self.local = [int(s) for s in np.where(self.assign == self.rank)[0]]
+
+    def exchange_counts_all(self, counts):
+        """counts[r][q] (r local) -> {q local: {r: n}} over all senders r."""
+        S = self.assign.size
+        M = np.zeros((S, S), np.int64)
+        for r, per in counts.items():
+            for q, n in per.items():
+                M[r, q] = int(n)
+        if self.tr is not None:
+            M = np.rint(self.tr.allreduce_sum(M.astype(np.float64).reshape(-1))).astype(
+                np.int64).reshape(S, S)
+        return {q: {r: int(M[r, q]) for r in range(S) if r != q} for q in self.local}
+
+    def exchange_all(self, sends, recvs):
+        """sends[r][q] (r local) -> recvs[q][r] (q local), uint8 tensors."""
+        import torch
+        remote_out, remote_in = {}, {}
+        for r in sorted(sends):
+            for q in sorted(sends[r]):
+                buf = sends[r][q]
+                if buf.numel() == 0:
+                    continue
+                R = int(self.assign[q])
+                if R == self.rank:
+                    recvs[q][r].copy_(buf)
+                else:
+                    remote_out.setdefault(R, []).append(buf)
+        # incoming pieces in the senders' (sender, receiver) order
+        pairs = sorted((r, q) for q in recvs for r in recvs[q]
+                       if int(self.assign[r]) != self.rank and recvs[q][r].numel() > 0)
+        for r, q in pairs:
+            remote_in.setdefault(int(self.assign[r]), []).append(recvs[q][r])
+        if not remote_out and not remote_in:
+            return
+        if self.tr is None:
+            raise RuntimeError("HybridTransport: remote sub-domain without a process group")
+        outs = {R: torch.cat(v) for R, v in remote_out.items()}
+        ins = {R: torch.empty(sum(t.numel() for t in v), dtype=torch.uint8, device=v[0].device)
+               for R, v in remote_in.items()}
+        self.tr.exchange(outs, ins)
+        for R, v in remote_in.items():
+            off = 0
+            for t in v:
+                t.copy_(ins[R][off:off + t.numel()])
+                off += t.numel()
+
+    def allreduce_max(self, x):
+        return x if self.tr is None else self.tr.allreduce_max(x)
+
+    def allreduce_sum(self, arr):
+        return np.asarray(arr, np.float64) if self.tr is None else self.tr.allreduce_sum(arr)
+
+
+def lpt_assign(work, nranks):
+    """Longest-processing-time greedy assignment of sub-domains to ranks
+    (heaviest first onto the least loaded rank; deterministic)."""
+    load = np.zeros(nranks)
+    assign = np.zeros(len(work), np.int64)
+    for i in np.argsort(-np.asarray(work, np.float64), kind="stable"):
+        r = int(np.argmin(load))
+        assign[i] = r
+        load[r] += work[i]
+    return assign
+
+
 class DistSim:
     """Lock-step driver for one or more local sub-domains.
 
@@ -202,6 +283,7 @@ class DistSim:
         self.tr = transport
         self.dt = dt
         self.loop = isinstance(transport, LoopbackTransport)
+        self.multi = hasattr(transport, "exchange_all")  # all local members at once
         self.ghost_seg = {}   # rank -> {peer: (off, n)} of the last ghost plan (send side)
         self.ghost_recv = {}  # rank -> {peer: n} received ghosts
         self.rebuilds = 0
@@ -217,14 +299,14 @@ class DistSim:
         return b[:nbytes]
 
     def _exchange(self, sends, recvs):
-        if self.loop:
+        if self.multi:
             self.tr.exchange_all(sends, recvs)
         else:
             (r,) = list(self.m)
             self.tr.exchange(sends[r], recvs[r])
 
     def _exchange_counts(self, counts):
-        if self.loop:
+        if self.multi:
             return self.tr.exchange_counts_all(counts)
         (r,) = list(self.m)
         return {r: self.tr.exchange_counts(counts[r])}

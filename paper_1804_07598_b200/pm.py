@@ -257,11 +257,14 @@ class Context:
                                         perm.ctypes.data))
         return dict(cell_of=cell_of, start=start, perm=perm)
 
-    def get_verlet(self):
+    def get_verlet(self, cols=True):
+        """CSR (row_ptr, col_gid) of the list; cols=False: row_ptr only."""
         c = self.count()
         n = c["n_owned"] + c["n_ghost"]  # one (possibly empty) row per local particle
         rp = np.zeros(n + 1, np.int64)
         self._check(self.L.pm_get_verlet(self.h, rp.ctypes.data, None))
+        if not cols:
+            return rp, None
         col = np.zeros(max(int(rp[-1]), 1), np.int64)
         self._check(self.L.pm_get_verlet(self.h, rp.ctypes.data, col.ctypes.data))
         return rp, col[:int(rp[-1])]

@@ -187,3 +187,58 @@ def test_owner_of_cuts_rule():
     cx = (s.pos[:, 0] >= 13.0).astype(int)
     cy = (s.pos[:, 1] >= 30.0).astype(int)
     assert np.array_equal(own, cx + 2 * cy)
+
+
+def _hybrid_worker(rank, world, port, grid, assign, out):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1804_07598_b200.dist import HybridTransport
+    import paper_1804_07598_b200.pm as pmm
+    pmm.record_bytes = lambda what: 24  # 3 x int64 per synthetic record
+    D = Decomp(grid)
+    tr = HybridTransport(assign, rank, TorchTransport(device=None))
+    ctxs = {sd: FakeCtx(sd, D, rng_key=(11, sd)) for sd in tr.local}
+    sim = DistSim(D, ctxs, tr, device="cpu")
+    sim._message_round(pmm.PM_MSG_GHOST)
+    for sd, ctx in ctxs.items():
+        out.put((sd, {w: (c.tolist(), o) for w, (c, o) in ctx.counts.items()},
+                 ctx.arrived[pmm.PM_MSG_GHOST]))
+    out.put(("flag", rank, sim._allreduce_max({sd: sd for sd in ctxs})))
+    dist.destroy_process_group()
+
+
+def test_hybrid_transport_over_decomposition_gloo_world2():
+    """Over-decomposition (NEXT-2): 8 sub-domains of a 2x2x2 grid on 2
+    processes with a mixed assignment; every sub-domain receives exactly the
+    records its peers packed for it, in peer order, whether the peer is local
+    (device copy) or remote (one concatenated transfer per process pair)."""
+    import torch.multiprocessing as mp
+    grid, assign = (2, 2, 2), [0, 1, 1, 0, 1, 0, 0, 1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_hybrid_worker, args=(r, 2, port, grid, assign, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    res, flags = {}, {}
+    for _ in range(10):
+        item = q.get(timeout=120)
+        if item[0] == "flag":
+            flags[item[1]] = item[2]
+        else:
+            res[item[0]] = item[1:]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert flags == {0: 7, 1: 7}
+    D = Decomp(grid)
+    from paper_1804_07598_b200 import pm
+    for r in range(8):
+        expect = []
+        for q_ in D.peers(r):  # arrivals are concatenated in peer order
+            cnt_q, order_q = res[q_][0][pm.PM_MSG_GHOST]
+            expect += [[q_, d, k] for d in order_q if d in D.valid_dirs() and D.peer(q_, d) == r
+                       for k in range(cnt_q[d])]
+        assert res[r][1] == expect

@@ -198,3 +198,49 @@ def test_load_balanced_cuts_clustered(env):
     F, Fr = got["force"][:, :3].astype(np.float64), rst["force"][:, :3].astype(np.float64)
     assert np.max(np.abs(F - Fr)) / np.sqrt(np.mean(Fr ** 2)) <= 1e-4
     ref.close()
+
+
+def test_over_decomposition_hybrid_clustered(env):
+    """SURVEY NEXT-2 via over-decomposition (the paper's sub-sub-domains,
+    PAPER.md:66-88, 122): a 4x4x4 grid of sub-domains on the clustered
+    system, assigned to 8 ranks by LPT on the measured pair work, all run in
+    this process through HybridTransport's local path: the rank loads are
+    balanced and neighbour sets/forces equal the one-context run."""
+    import torch
+    pm, dist = env
+    s = inputs.cfg5(n_clusters=8, per_cluster=8192, sigma_c=6.0, rho=0.3, key=56)
+    ref = pm.Context()
+    ref.set_domain(s.lo, s.hi, s.periodic)
+    ref.set_cutoff(2.5, 0.3)
+    ref.set_lj(1.0, 1.0, 1.0, 0.8)
+    ref.place(s.pos, s.vel, s.gid)
+    ref.build_verlet()
+    ref.compute_lj()
+    rst = pm.sorted_by_gid(ref.get_state())
+    rp, _ = ref.get_verlet(cols=False)
+    w = np.zeros(s.n)
+    w[ref.get_state()["gid"]] = np.diff(rp)
+    D = dist.Decomp((4, 4, 4))
+    owner = dist.owner_of(s, D)
+    work = np.bincount(owner, weights=w, minlength=D.size)
+    assign = dist.lpt_assign(work, 8)
+    load = np.bincount(assign, weights=work, minlength=8)
+    assert dist.imbalance(load) < 1.05 < dist.imbalance(
+        np.bincount(dist.owner_of(s, dist.Decomp((2, 2, 2))), weights=w, minlength=8))
+    stream = torch.cuda.Stream()
+    members = {r: dist.make_member(s.subset(np.where(owner == r)[0]), D, r, stream=stream,
+                                   r_min=0.8) for r in range(D.size)}
+    tr = dist.HybridTransport(np.zeros(D.size, np.int64), 0)  # every sub-domain local
+    sim = dist.DistSim(D, members, tr, stream=stream)
+    sim.start()
+    got = pm.sorted_by_gid({k: np.concatenate([c.owned_state()[k] for c in sim.m.values()])
+                            for k in ("gid", "force")})
+    assert np.array_equal(got["gid"], np.sort(s.gid))
+    F, Fr = got["force"][:, :3].astype(np.float64), rst["force"][:, :3].astype(np.float64)
+    assert np.max(np.abs(F - Fr)) / np.sqrt(np.mean(Fr ** 2)) <= 1e-4
+    assert sum(c.count()["nnz"] for c in sim.m.values()) == int(rp[-1])
+    reb = sim.run(10)
+    assert reb >= 0
+    for c in sim.m.values():
+        c.close()
+    ref.close()
