@@ -108,6 +108,32 @@ typedef struct {
 } pm_sph_params;
 pm_status pm_set_sph(pm_ctx ctx, const pm_sph_params *p);
 
+/* DEM parameters (§4.5 Eqs. 9-13;
+ * readings R29-R33): particle radius R, mass m, moment of inertia I,
+ * normal/tangential elastic constants kn, kt (Eqs. 11-12), damping gamma_n,
+ * gamma_t, Coulomb coefficient mu, gravity g, and plane walls at the box
+ * faces (flags x-lo, x-hi, y-lo, y-hi, z-lo, z-hi; only on non-periodic
+ * axes).  Contacts come from the Verlet list: set r_cut = 2R and a skin. */
+typedef struct {
+  float R, m, I, kn, kt, gamma_n, gamma_t, mu;
+  float g[3];
+  int32_t walls[6];
+} pm_dem_params;
+pm_status pm_set_dem(pm_ctx ctx, const pm_dem_params *p);
+
+/* nsteps DEM steps of size dt: Hertzian normal force with damping (Eq. 11),
+ * tangential spring with per-contact history (Eq. 10) and damping (Eq. 12),
+ * Coulomb cap, torques, walls, gravity; leapfrog (Eq. 13) for velocity,
+ * position and angular velocity.  Angular velocities start at 0 at
+ * pm_place.  The contact histories follow the particles through Verlet
+ * rebuilds (matched by gid).  Errors: PM_E_DOMAIN (a particle left an open
+ * axis), PM_E_NONFINITE.  rebuilds may be NULL. */
+pm_status pm_dem_run(pm_ctx ctx, float dt, int64_t nsteps, int64_t *rebuilds);
+
+/* Angular velocities and torques (n x 4 floats each, current internal order
+ * as pm_get_state); either may be NULL. */
+pm_status pm_get_dem(pm_ctx ctx, float *omega4, float *torque4);
+
 /* Place n particles (replaces any previous set).  pos4 required; vel4, gid,
  * kind may be NULL (zero velocity, gid = 0..n-1, kind = 0).  Positions on
  * periodic axes are wrapped (reading R1) at the next build.  Grows device

@@ -80,6 +80,11 @@ def lib():
         L.orc_sph_accel_rows.argtypes = [C.c_int64, f32p, f32p, f64p, f64p, C.c_void_p, f32p,
                                          f32p, i32p, C.c_double, C.c_double, C.c_double,
                                          C.c_double, C.c_double, f64p, i64p, C.c_int64, f64p]
+        L.orc_dem_run.restype = C.c_int64
+        L.orc_dem_run.argtypes = [C.c_int64, f64p, f64p, f64p, i64p, f64p, f64p, i32p, i32p,
+                                  C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
+                                  C.c_double, C.c_double, C.c_double, f64p, C.c_double,
+                                  C.c_int64, C.c_int64]
         L.orc_sph_run.argtypes = [C.c_int64, f64p, f64p, f64p, C.c_void_p, f64p, f64p, i32p,
                                   C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
                                   C.c_double, C.c_double, C.c_double, f64p, C.c_double,
@@ -278,6 +283,27 @@ def sph_run(pos4, vel4, rho, kind, lo, hi, per, params, nsteps, cfl=0.2, every=4
                       float(params["alpha"]), float(params["c0"]), float(params["eta2"]), g,
                       float(cfl), int(every), int(nsteps), tr)
     return x, v, r, tr[:nsteps]
+
+
+def dem_run(pos4, vel4, omega, gid, lo, hi, per, walls, params, dt, nsteps):
+    """DEM (Eqs. 9-13; readings R29-R33):
+    Hertzian normal force with damping, tangential spring with history and
+    Coulomb cap, torques, planar walls, leapfrog.  fp64 state from the fp32
+    inputs; O(N^2).  Returns (x, v, w (n,3) fp64, number of contacts)."""
+    x = np.ascontiguousarray(np.asarray(pos4, np.float32)[:, :3].astype(np.float64))
+    v = np.ascontiguousarray(np.asarray(vel4, np.float32)[:, :3].astype(np.float64))
+    w = np.ascontiguousarray(np.asarray(omega, np.float32)[:, :3].astype(np.float64))
+    n = x.shape[0]
+    g = np.ascontiguousarray(np.asarray(params["g"], np.float64).reshape(3))
+    lo64 = np.ascontiguousarray(np.asarray(lo, np.float32).astype(np.float64))
+    hi64 = np.ascontiguousarray(np.asarray(hi, np.float32).astype(np.float64))
+    nh = lib().orc_dem_run(n, x.reshape(-1), v.reshape(-1), w.reshape(-1),
+                           np.ascontiguousarray(gid, dtype=np.int64), lo64, hi64, _i3(per),
+                           np.ascontiguousarray(walls, dtype=np.int32), float(params["R"]),
+                           float(params["m"]), float(params["I"]), float(params["kn"]),
+                           float(params["kt"]), float(params["gn"]), float(params["gt"]),
+                           float(params["mu"]), g, float(dt), int(nsteps), 64 * n + 64)
+    return x, v, w, int(nh)
 
 
 # ---------------------------------------------------------------- parity metric

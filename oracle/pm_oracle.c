@@ -625,3 +625,153 @@ void orc_sph_run(int64_t n, double *x, double *v, double *rho, const int32_t *ki
   free(vprev);
   free(rprev);
 }
+
+/* ------------------------------------------------------------------ */
+/* DEM (§4.5, Eqs. 9-13), fp64,   */
+/* O(N^2) contact search, contact history keyed by the (gid_p, gid_q)    */
+/* pair.  Readings (R29-R33):                                   */
+/*   n = r_pq / |r_pq| (r_pq = r_p - r_q, minimum image on periodic axes), */
+/*   delta = 2R - |r_pq| (Eq. 9), contact iff delta > 0;                  */
+/*   v_pq = v_p - v_q - R (w_p + w_q) x n (relative velocity at the       */
+/*   contact point); v_n = (v_pq.n) n, v_t = v_pq - v_n;                  */
+/*   u_t <- u_t - (u_t.n) n + v_t dt (Eq. 10, kept tangential);           */
+/*   s = sqrt(delta / 2R); F_n = s (kn delta n - gn meff v_n) (Eq. 11);    */
+/*   F_t = s (-kt u_t - gt meff v_t) (Eq. 12), meff = m/2; Coulomb: if    */
+/*   |F_t| > mu |F_n|, F_t <- F_t mu|F_n|/|F_t| and u_t is rescaled to    */
+/*   match (u_t = -(F_t/s + gt meff v_t)/kt);                              */
+/*   F_p += F_n + F_t; T_p += (-R n) x F_t;  walls (flags per box face,   */
+/*   planes at the faces) act like a fixed sphere touching the plane:     */
+/*   normal Hertz force with damping only;  gravity g.                    */
+/*   Leapfrog (Eq. 13): v += dt F/m; x += dt v; w += dt T/I.              */
+/* A contact that ends loses its history.                                 */
+/* ------------------------------------------------------------------ */
+typedef struct {
+  int64_t a, b;
+  double u[3];
+} dem_hist_t;
+
+static int64_t dem_find(dem_hist_t *h, int64_t nh, int64_t a, int64_t b) {
+  for (int64_t k = 0; k < nh; ++k)
+    if (h[k].a == a && h[k].b == b) return k;
+  return -1;
+}
+
+static void cross3(const double a[3], const double b[3], double c[3]) {
+  c[0] = a[1] * b[2] - a[2] * b[1];
+  c[1] = a[2] * b[0] - a[0] * b[2];
+  c[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+/* x, v, w: fp64 (n x 3) in/out; gid: unique ids; walls[6]: x-lo, x-hi,
+ * y-lo, y-hi, z-lo, z-hi plane flags.  hist_cap: max stored contacts. */
+int64_t orc_dem_run(int64_t n, double *x, double *v, double *w, const int64_t *gid,
+                    const double lo[3], const double hi[3], const int32_t per[3],
+                    const int32_t walls[6], double R, double m, double I, double kn, double kt,
+                    double gn, double gt, double mu, const double g[3], double dt,
+                    int64_t nsteps, int64_t hist_cap) {
+  double L[3] = {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]};
+  dem_hist_t *hist = (dem_hist_t *)calloc((size_t)(hist_cap > 0 ? hist_cap : 1), sizeof(dem_hist_t));
+  dem_hist_t *nhist = (dem_hist_t *)calloc((size_t)(hist_cap > 0 ? hist_cap : 1), sizeof(dem_hist_t));
+  int64_t nh = 0;
+  double *F = (double *)malloc(sizeof(double) * 3 * (size_t)(n > 0 ? n : 1));
+  double *T = (double *)malloc(sizeof(double) * 3 * (size_t)(n > 0 ? n : 1));
+  const double meff = 0.5 * m;
+  for (int64_t s = 0; s < nsteps; ++s) {
+    int64_t nn = 0;
+    for (int64_t p = 0; p < n; ++p) {
+      double f[3] = {m * g[0], m * g[1], m * g[2]}, t[3] = {0, 0, 0};
+      for (int64_t q = 0; q < n; ++q) {
+        if (q == p) continue;
+        double r[3];
+        for (int d = 0; d < 3; ++d) {
+          double e = x[3 * p + d] - x[3 * q + d];
+          if (per[d]) {
+            if (e > 0.5 * L[d]) e -= L[d];
+            else if (e < -0.5 * L[d]) e += L[d];
+          }
+          r[d] = e;
+        }
+        double rr = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+        double delta = 2.0 * R - rr;
+        if (!(delta > 0.0) || rr == 0.0) continue;
+        double nv[3] = {r[0] / rr, r[1] / rr, r[2] / rr};
+        double ws[3] = {w[3 * p] + w[3 * q], w[3 * p + 1] + w[3 * q + 1], w[3 * p + 2] + w[3 * q + 2]};
+        double wxn[3];
+        cross3(ws, nv, wxn);
+        double vpq[3];
+        for (int d = 0; d < 3; ++d) vpq[d] = v[3 * p + d] - v[3 * q + d] - R * wxn[d];
+        double vn = vpq[0] * nv[0] + vpq[1] * nv[1] + vpq[2] * nv[2];
+        double vnv[3] = {vn * nv[0], vn * nv[1], vn * nv[2]};
+        double vt[3] = {vpq[0] - vnv[0], vpq[1] - vnv[1], vpq[2] - vnv[2]};
+        double u[3] = {0, 0, 0};
+        int64_t k = dem_find(hist, nh, gid[p], gid[q]);
+        if (k >= 0) memcpy(u, hist[k].u, sizeof u);
+        double un = u[0] * nv[0] + u[1] * nv[1] + u[2] * nv[2];
+        for (int d = 0; d < 3; ++d) u[d] = u[d] - un * nv[d] + vt[d] * dt;
+        double sq = sqrt(delta / (2.0 * R));
+        double fn[3], ft[3];
+        for (int d = 0; d < 3; ++d) {
+          fn[d] = sq * (kn * delta * nv[d] - gn * meff * vnv[d]);
+          ft[d] = sq * (-kt * u[d] - gt * meff * vt[d]);
+        }
+        double fnm = sqrt(fn[0] * fn[0] + fn[1] * fn[1] + fn[2] * fn[2]);
+        double ftm = sqrt(ft[0] * ft[0] + ft[1] * ft[1] + ft[2] * ft[2]);
+        if (ftm > mu * fnm && ftm > 0.0) {
+          double sc = mu * fnm / ftm;
+          for (int d = 0; d < 3; ++d) {
+            ft[d] *= sc;
+            u[d] = -(ft[d] / sq + gt * meff * vt[d]) / kt;
+          }
+        }
+        if (nn < hist_cap) {
+          nhist[nn].a = gid[p];
+          nhist[nn].b = gid[q];
+          memcpy(nhist[nn].u, u, sizeof u);
+          ++nn;
+        }
+        double arm[3] = {-R * nv[0], -R * nv[1], -R * nv[2]}, tq[3];
+        cross3(arm, ft, tq);
+        for (int d = 0; d < 3; ++d) {
+          f[d] += fn[d] + ft[d];
+          t[d] += tq[d];
+        }
+      }
+      /* walls: plane at the face, normal Hertz + damping */
+      for (int d = 0; d < 3; ++d) {
+        for (int side = 0; side < 2; ++side) {
+          if (!walls[2 * d + side]) continue;
+          double dist = side == 0 ? x[3 * p + d] - lo[d] : hi[d] - x[3 * p + d];
+          double delta = R - dist;
+          if (!(delta > 0.0)) continue;
+          double nd = side == 0 ? 1.0 : -1.0; /* normal into the domain */
+          double vn = v[3 * p + d] * nd;
+          double sq = sqrt(delta / (2.0 * R));
+          f[d] += sq * (kn * delta - gn * meff * vn) * nd;
+        }
+      }
+      memcpy(F + 3 * p, f, sizeof f);
+      memcpy(T + 3 * p, t, sizeof t);
+    }
+    dem_hist_t *tmp = hist;
+    hist = nhist;
+    nhist = tmp;
+    nh = nn;
+    for (int64_t p = 0; p < n; ++p) {
+      for (int d = 0; d < 3; ++d) {
+        v[3 * p + d] += dt / m * F[3 * p + d];
+        double xx = x[3 * p + d] + dt * v[3 * p + d];
+        if (per[d]) {
+          if (xx >= hi[d]) xx -= L[d];
+          else if (xx < lo[d]) xx += L[d];
+        }
+        x[3 * p + d] = xx;
+        w[3 * p + d] += dt / I * T[3 * p + d];
+      }
+    }
+  }
+  free(F);
+  free(T);
+  free(hist);
+  free(nhist);
+  return nh;
+}

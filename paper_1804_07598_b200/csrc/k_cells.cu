@@ -265,7 +265,8 @@ __global__ void __launch_bounds__(512) k_segsort_big(Bufs B, const int32_t *__re
 }
 
 // a4: gather every particle array into cell order (alternate buffers).
-__global__ void __launch_bounds__(256) k_reorder(Bufs B, int64_t n, int sph_state) {
+__global__ void __launch_bounds__(256) k_reorder(Bufs B, int64_t n, int sph_state,
+                                                 int dem_state) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   State *st = B.st;
@@ -283,6 +284,7 @@ __global__ void __launch_bounds__(256) k_reorder(Bufs B, int64_t n, int sph_stat
     B.vold[ci ^ 1][k] = B.vold[ci][j];
     B.rold[ci ^ 1][k] = B.rold[ci][j];
   }
+  if (dem_state) B.omega[ci ^ 1][k] = B.omega[ci][j];
 }
 
 __global__ void k_flip(Bufs B, int flip_pv, int flip_id, int count_rebuild) {
@@ -326,7 +328,7 @@ void launch_sort_reorder(const Params &P, const Bufs &B, int64_t n, cudaStream_t
   k_scatter<<<blocks_for(n, 256), 256, 0, s>>>(B, tmp, n);
   k_segsort<<<blocks_for((int64_t)P.grid.ncell * 32, 256), 256, 0, s>>>(B, tmp, P.grid.ncell);
   k_segsort_big<<<148, 512, 0, s>>>(B, tmp);
-  k_reorder<<<blocks_for(n, 256), 256, 0, s>>>(B, n, P.sph_state);
+  k_reorder<<<blocks_for(n, 256), 256, 0, s>>>(B, n, P.sph_state, P.dem_state);
 }
 
 void launch_flip(const Bufs &B, int flip_pv, int flip_id, int count_rebuild, cudaStream_t s) {

@@ -1,0 +1,197 @@
+// k_dem.cu -- discrete element method.
+//
+// PAPER.md:520-540 (§4.5): Hertzian contacts with elastic deformation of the
+// grains.  Eq. 9 overlap delta = 2R - r_pq; Eq. 10 tangential deformation
+// u_t += v_t dt over the duration of a contact; Eqs. 11-12 normal and
+// tangential forces sqrt(delta/2R)(k delta n - gamma m_eff v); Coulomb cap
+// ("rescaled to enforce Coulomb's law"); Eq. 13 leapfrog for v, r and the
+// angular velocity.  Readings R29-R33 fix what the paper leaves
+// open: relative velocity at the contact point with the rotation term,
+// u_t kept tangential, gamma_t, mu, torque arm -R n, plane walls.  The same
+// definitions are written out in oracle/pm_oracle.c orc_dem_run.
+//
+// Contacts are found in the Verlet list (r_v = 2R + skin, the int32 rows of
+// k_verlet.cu); the tangential history of an ordered pair (p, q) lives in the
+// list slot of q in p's row (float4, same SELL layout) and is carried to the
+// new list at a rebuild by matching partner gids (k_dem_remap).  Both ordered
+// pairs evolve with opposite v_t, so F_qp = -F_pq: linear momentum is kept up
+// to rounding.  fp32, thread per particle, no atomics.
+#include "pm_internal.cuh"
+
+namespace pm {
+
+namespace {
+
+__device__ __forceinline__ float3 cross3(const float3 &a, const float3 &b) {
+  return make_float3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+
+__global__ void __launch_bounds__(256) k_dem_forces(Params P, Bufs B, int n, float dt) {
+  State *st = B.st;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int cp = st->cur_pv, ci = st->cur_id;
+  const float4 *__restrict__ pos = B.pos[cp];
+  const float4 *__restrict__ vel = B.vel[cp];
+  const float4 *__restrict__ om = B.omega[ci];
+  const DEM &D = P.dem;
+  const float4 xi = pos[i], vi = vel[i], wi = om[i];
+  float3 f = make_float3(D.m * D.g[0], D.m * D.g[1], D.m * D.g[2]);
+  float3 tq = make_float3(0.f, 0.f, 0.f);
+  const int cnt = B.cnt[i];
+  const int64_t base = nbr_row_base(B, i);
+  const float twoR = 2.0f * D.R, inv2R = 1.0f / (2.0f * D.R);
+  for (int k = 0; k < cnt; ++k) {
+    const int64_t slot = base + ((int64_t)k << 5);
+    const int j = B.nbr[slot];
+    const float4 xj = __ldg(pos + j);
+    // r_pq = x_i - x_j (R4 minimum image on periodic axes)
+    const float rx = -pair_delta1(xi.x, xj.x, P.box.L[0], P.box.halfL[0], P.box.per[0]);
+    const float ry = -pair_delta1(xi.y, xj.y, P.box.L[1], P.box.halfL[1], P.box.per[1]);
+    const float rz = -pair_delta1(xi.z, xj.z, P.box.L[2], P.box.halfL[2], P.box.per[2]);
+    const float r2 = rx * rx + ry * ry + rz * rz;
+    const float rr = sqrtf(r2);
+    const float delta = twoR - rr;
+    if (!(delta > 0.0f) || rr == 0.0f) {  // no contact: the history ends
+      B.hist[slot] = make_float4(0.f, 0.f, 0.f, 0.f);
+      continue;
+    }
+    const float inv_r = 1.0f / rr;
+    const float3 nv = make_float3(rx * inv_r, ry * inv_r, rz * inv_r);
+    const float4 vj = __ldg(vel + j), wj = __ldg(om + j);
+    const float3 wxn = cross3(make_float3(wi.x + wj.x, wi.y + wj.y, wi.z + wj.z), nv);
+    const float3 vpq = make_float3(vi.x - vj.x - D.R * wxn.x, vi.y - vj.y - D.R * wxn.y,
+                                   vi.z - vj.z - D.R * wxn.z);
+    const float vn = vpq.x * nv.x + vpq.y * nv.y + vpq.z * nv.z;
+    const float3 vnv = make_float3(vn * nv.x, vn * nv.y, vn * nv.z);
+    const float3 vt = make_float3(vpq.x - vnv.x, vpq.y - vnv.y, vpq.z - vnv.z);
+    const float4 h = B.hist[slot];
+    const float un = h.x * nv.x + h.y * nv.y + h.z * nv.z;
+    float3 u = make_float3(h.x - un * nv.x + vt.x * dt, h.y - un * nv.y + vt.y * dt,
+                           h.z - un * nv.z + vt.z * dt);
+    const float sq = sqrtf(delta * inv2R);
+    const float3 fn = make_float3(sq * (D.kn * delta * nv.x - D.gn * D.meff * vnv.x),
+                                  sq * (D.kn * delta * nv.y - D.gn * D.meff * vnv.y),
+                                  sq * (D.kn * delta * nv.z - D.gn * D.meff * vnv.z));
+    float3 ft = make_float3(sq * (-D.kt * u.x - D.gt * D.meff * vt.x),
+                            sq * (-D.kt * u.y - D.gt * D.meff * vt.y),
+                            sq * (-D.kt * u.z - D.gt * D.meff * vt.z));
+    const float fnm = sqrtf(fn.x * fn.x + fn.y * fn.y + fn.z * fn.z);
+    const float ftm = sqrtf(ft.x * ft.x + ft.y * ft.y + ft.z * ft.z);
+    if (ftm > D.mu * fnm && ftm > 0.0f) {  // Coulomb: slide, rescale the spring
+      const float sc = D.mu * fnm / ftm;
+      ft = make_float3(ft.x * sc, ft.y * sc, ft.z * sc);
+      u = make_float3(-(ft.x / sq + D.gt * D.meff * vt.x) / D.kt,
+                      -(ft.y / sq + D.gt * D.meff * vt.y) / D.kt,
+                      -(ft.z / sq + D.gt * D.meff * vt.z) / D.kt);
+    }
+    B.hist[slot] = make_float4(u.x, u.y, u.z, 0.f);
+    const float3 tc = cross3(make_float3(-D.R * nv.x, -D.R * nv.y, -D.R * nv.z), ft);
+    f = make_float3(f.x + fn.x + ft.x, f.y + fn.y + ft.y, f.z + fn.z + ft.z);
+    tq = make_float3(tq.x + tc.x, tq.y + tc.y, tq.z + tc.z);
+  }
+  // plane walls at the box faces: normal Hertz force with damping (R33)
+  const float xv[3] = {xi.x, xi.y, xi.z}, vv[3] = {vi.x, vi.y, vi.z};
+  float fw[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      if (!D.walls[2 * d + side]) continue;
+      const float dist = side == 0 ? xv[d] - P.box.lo[d] : P.box.hi[d] - xv[d];
+      const float delta = D.R - dist;
+      if (!(delta > 0.0f)) continue;
+      const float nd = side == 0 ? 1.0f : -1.0f;
+      const float sq = sqrtf(delta * inv2R);
+      fw[d] += sq * (D.kn * delta - D.gn * D.meff * vv[d] * nd) * nd;
+    }
+  }
+  f = make_float3(f.x + fw[0], f.y + fw[1], f.z + fw[2]);
+  B.force[i] = make_float4(f.x, f.y, f.z, 0.f);
+  B.torque[i] = make_float4(tq.x, tq.y, tq.z, 0.f);
+  if (!isfinite(f.x + f.y + f.z + tq.x + tq.y + tq.z))
+    raise_error(st, -8 /*PM_E_NONFINITE*/, (long long)B.gid[ci][i]);
+}
+
+// Eq. 13 leapfrog: v += dt F/m; x += dt v; w += dt T/I; rebuild test
+__global__ void __launch_bounds__(256) k_dem_integrate(Params P, Bufs B, int n, float dt) {
+  State *st = B.st;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int cp = st->cur_pv, ci = st->cur_id;
+  bool far = false;
+  if (i < n) {
+    const float4 f = B.force[i], t = B.torque[i];
+    float4 v = B.vel[cp][i];
+    const float4 x = B.pos[cp][i];
+    v.x = fmaf(dt * P.dem.inv_m, f.x, v.x);
+    v.y = fmaf(dt * P.dem.inv_m, f.y, v.y);
+    v.z = fmaf(dt * P.dem.inv_m, f.z, v.z);
+    float r3[3] = {fmaf(dt, v.x, x.x), fmaf(dt, v.y, x.y), fmaf(dt, v.z, x.z)};
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+      if (P.box.per[d]) r3[d] = wrap1(r3[d], P.box.lo[d], P.box.hi[d], P.box.L[d]);
+    const float4 xn = make_float4(r3[0], r3[1], r3[2], x.w);
+    float4 w = B.omega[ci][i];
+    w.x = fmaf(dt * P.dem.inv_I, t.x, w.x);
+    w.y = fmaf(dt * P.dem.inv_I, t.y, w.y);
+    w.z = fmaf(dt * P.dem.inv_I, t.z, w.z);
+    B.omega[ci][i] = w;
+    B.pos[cp ^ 1][i] = xn;
+    B.vel[cp ^ 1][i] = v;
+    const float4 xr = B.xref[i];
+    const float dx = pair_delta1(xr.x, xn.x, P.box.L[0], P.box.halfL[0], P.box.per[0]);
+    const float dy = pair_delta1(xr.y, xn.y, P.box.L[1], P.box.halfL[1], P.box.per[1]);
+    const float dz = pair_delta1(xr.z, xn.z, P.box.L[2], P.box.halfL[2], P.box.per[2]);
+    far = dist2(dx, dy, dz) > P.half_skin2;
+    for (int d = 0; d < 3; ++d)
+      if (!P.box.per[d] && (r3[d] < P.box.lo[d] || r3[d] >= P.box.hi[d])) far = true;
+  }
+  if (__any_sync(0xffffffffu, far) && (threadIdx.x & 31) == 0) st->need_rebuild = 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->pending_flip = 1;
+}
+
+// After a rebuild: the history of each new list slot (i, j) is the old
+// slot with the same partner gid in the old row of the same particle
+// (old index perm[i]); 0 for new contacts.
+__global__ void __launch_bounds__(256) k_dem_remap(Bufs B, int n, int ci_old) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int ci = B.st->cur_id;
+  const int o = B.perm[i];
+  const int64_t *gnew = B.gid[ci], *gold = B.gid[ci_old];
+  const int64_t obase = B.slice_off_old[o >> 5] * 32 + (o & 31);
+  const int ocnt = B.cnt_old[o];
+  const int64_t base = nbr_row_base(B, i);
+  const int cnt = B.cnt[i];
+  for (int k = 0; k < cnt; ++k) {
+    const int64_t slot = base + ((int64_t)k << 5);
+    const int64_t gj = gnew[B.nbr[slot]];
+    float4 h = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q = 0; q < ocnt; ++q) {
+      const int64_t os = obase + ((int64_t)q << 5);
+      if (gold[B.nbr_old[os]] == gj) {
+        h = B.hist_old[os];
+        break;
+      }
+    }
+    B.hist[slot] = h;
+  }
+}
+
+inline unsigned nb(int64_t n) { return (unsigned)((n + 255) / 256); }
+
+}  // namespace
+
+void launch_dem_forces(const Params &P, const Bufs &B, int64_t n, float dt, cudaStream_t s) {
+  if (n > 0) k_dem_forces<<<nb(n), 256, 0, s>>>(P, B, (int)n, dt);
+}
+
+void launch_dem_integrate(const Params &P, const Bufs &B, int64_t n, float dt, cudaStream_t s) {
+  if (n > 0) k_dem_integrate<<<nb(n), 256, 0, s>>>(P, B, (int)n, dt);
+}
+
+void launch_dem_remap(const Bufs &B, int64_t n, int ci_old, cudaStream_t s) {
+  if (n > 0) k_dem_remap<<<nb(n), 256, 0, s>>>(B, (int)n, ci_old);
+}
+
+}  // namespace pm

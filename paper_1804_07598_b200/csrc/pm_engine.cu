@@ -49,6 +49,8 @@ struct pm_ctx_s {
   int nbr_cap = 0;        // widest slice of the current layout
 
   bool have_domain = false, have_cutoff = false, have_lj = false, have_sph = false;
+  bool have_dem = false;
+  int64_t dem_pcap = -1, dem_ints = -1, dem_old_ints = -1, dem_old_slices = -1;
   float r_cut = 0.f, skin = 0.f, rv = 0.f;
   bool cells_valid = false, list_valid = false, forces_valid = false, rho_valid = false;
   double lj_eps = 1.0, lj_sigma = 1.0;
@@ -657,6 +659,10 @@ void pm_destroy(pm_ctx c) {
                   B.sorttmp, B.scan_tmp, B.nbr, B.cnt, B.st, B.slice_off, B.big_cells};
   for (void *p : ptrs)
     if (p) cudaFree(p);
+  void *dem_ptrs[] = {B.omega[0], B.omega[1], B.torque, B.hist, B.hist_old, B.nbr_old,
+                      B.slice_off_old, B.cnt_old};
+  for (void *p : dem_ptrs)
+    if (p) cudaFree(p);
   void *dptrs[] = {c->d_mask, c->d_blk, c->d_order, c->d_dirbase, c->d_list,
                    c->d_send_idx, c->d_gslot, c->d_tot, B.invperm};
   for (void *p : dptrs)
@@ -786,6 +792,11 @@ pm_status pm_place(pm_ctx c, int64_t n, const float *pos4, const float *vel4, co
     if (kind) CUDA_TRY(c, cudaMemcpyAsync(B.kind[0], kind, sizeof(int32_t) * n, k, c->stream));
     else CUDA_TRY(c, cudaMemsetAsync(B.kind[0], 0, sizeof(int32_t) * n, c->stream));
     CUDA_TRY(c, cudaMemcpyAsync(B.xref, B.pos[0], sizeof(float4) * n, cudaMemcpyDeviceToDevice, c->stream));
+    for (int b = 0; b < 2; ++b)  // DEM: angular velocities start at rest
+      if (B.omega[b] && c->dem_pcap == c->pcap)
+        CUDA_TRY(c, cudaMemsetAsync(B.omega[b], 0, sizeof(float4) * n, c->stream));
+    if (B.hist && c->dem_ints == c->nbr_ints)
+      CUDA_TRY(c, cudaMemsetAsync(B.hist, 0, sizeof(float4) * c->nbr_ints, c->stream));
   }
   std::memset(c->st_h, 0, sizeof(State));
   c->st_h->err_gid = -1;
@@ -854,6 +865,155 @@ pm_status pm_sph_forces(pm_ctx c) {
   cudaSetDevice(c->device);
   launch_sph_forces(c->P, c->B, c->n, c->stream);
   return sync_check(c, "pm_sph_forces");
+}
+
+pm_status pm_set_dem(pm_ctx c, const pm_dem_params *p) {
+  if (!c || !p) return PM_E_INVAL;
+  if (!(p->R > 0.f) || !(p->m > 0.f) || !(p->I > 0.f) || !(p->kn > 0.f) || !(p->kt > 0.f) ||
+      !(p->gamma_n >= 0.f) || !(p->gamma_t >= 0.f) || !(p->mu >= 0.f))
+    return set_err(c, PM_E_INVAL, "pm_set_dem: R, m, I, kn, kt > 0 and gamma, mu >= 0");
+  DEM &d = c->P.dem;
+  d.R = p->R;
+  d.m = p->m;
+  d.inv_m = 1.0f / p->m;
+  d.inv_I = 1.0f / p->I;
+  d.kn = p->kn;
+  d.kt = p->kt;
+  d.gn = p->gamma_n;
+  d.gt = p->gamma_t;
+  d.mu = p->mu;
+  d.meff = 0.5f * p->m;
+  for (int k = 0; k < 3; ++k) d.g[k] = p->g[k];
+  for (int k = 0; k < 6; ++k) {
+    if (p->walls[k] && c->have_domain && c->P.box.per[k / 2])
+      return set_err(c, PM_E_INVAL, "pm_set_dem: wall on periodic axis %d", k / 2);
+    d.walls[k] = p->walls[k] ? 1 : 0;
+  }
+  c->have_dem = true;
+  destroy_graph(c);
+  return PM_OK;
+}
+
+// DEM buffers: angular velocities (by cur_id), torques, the per-slot contact
+// history (sized like the list) and the copies kept across a rebuild.
+static pm_status dem_alloc(pm_ctx c, bool old_copies) {
+  Bufs &B = c->B;
+  if (c->dem_pcap != c->pcap) {
+    for (int b = 0; b < 2; ++b) {
+      CUDA_TRY(c, dalloc(&B.omega[b], c->pcap));
+      CUDA_TRY(c, cudaMemsetAsync(B.omega[b], 0, 16 * c->pcap, c->stream));
+    }
+    CUDA_TRY(c, dalloc(&B.torque, c->pcap));
+    CUDA_TRY(c, dalloc(&B.cnt_old, c->pcap));
+    c->dem_pcap = c->pcap;
+  }
+  if (c->dem_ints != c->nbr_ints) {
+    CUDA_TRY(c, dalloc(&B.hist, c->nbr_ints));
+    CUDA_TRY(c, cudaMemsetAsync(B.hist, 0, 16 * c->nbr_ints, c->stream));
+    c->dem_ints = c->nbr_ints;
+  }
+  if (old_copies) {
+    if (c->dem_old_ints != c->nbr_ints) {
+      CUDA_TRY(c, dalloc(&B.hist_old, c->nbr_ints));
+      CUDA_TRY(c, dalloc(&B.nbr_old, c->nbr_ints));
+      c->dem_old_ints = c->nbr_ints;
+    }
+    if (c->dem_old_slices != c->slice_cap) {
+      CUDA_TRY(c, dalloc(&B.slice_off_old, c->slice_cap));
+      c->dem_old_slices = c->slice_cap;
+    }
+  }
+  return PM_OK;
+}
+
+pm_status pm_dem_run(pm_ctx c, float dt, int64_t nsteps, int64_t *rebuilds) {
+  pm_status s = check_ready(c);
+  if (s) return s;
+  if (rebuilds) *rebuilds = 0;
+  if (!c->have_dem) return set_err(c, PM_E_STATE, "pm_set_dem not called");
+  if (c->dist) return set_err(c, PM_E_STATE, "pm_dem_run: single (non-decomposed) context only");
+  if (!(dt > 0.f) || nsteps < 0) return set_err(c, PM_E_INVAL, "pm_dem_run: dt must be > 0");
+  if (!(c->skin > 0.f)) return set_err(c, PM_E_INVAL, "pm_dem_run: needs a Verlet skin > 0");
+  cudaSetDevice(c->device);
+  if (nsteps == 0) return PM_OK;
+  Bufs &B = c->B;
+  if (!c->P.dem_state) {  // the cell-sort reorder now carries the angular velocities
+    c->P.dem_state = 1;
+    destroy_graph(c);
+  }
+  if ((s = dem_alloc(c, false))) return s;
+  if (!c->list_valid) {
+    s = build_list(c);
+    if (s) return s;
+    if ((s = dem_alloc(c, false))) return s;
+    CUDA_TRY(c, cudaMemsetAsync(B.hist, 0, 16 * c->nbr_ints, c->stream));
+  }
+  s = read_state(c);
+  if (s) return s;
+  const long long reb0 = c->st_h->n_rebuilds;
+  k_clear_rebuild<<<1, 1, 0, c->stream>>>(B.st);
+  int64_t done = 0;
+  for (; done < nsteps; ++done) {
+    s = read_state(c);
+    if (s) return s;
+    if (c->st_h->abort) break;
+    if (c->st_h->need_rebuild) {
+      // keep the old list and histories, rebuild, carry the histories over
+      if ((s = dem_alloc(c, true))) return s;
+      const int ci_old = c->st_h->cur_id;
+      CUDA_TRY(c, cudaMemcpyAsync(B.nbr_old, B.nbr, 4 * c->nbr_ints, cudaMemcpyDeviceToDevice,
+                                  c->stream));
+      CUDA_TRY(c, cudaMemcpyAsync(B.hist_old, B.hist, 16 * c->nbr_ints,
+                                  cudaMemcpyDeviceToDevice, c->stream));
+      CUDA_TRY(c, cudaMemcpyAsync(B.cnt_old, B.cnt, 4 * c->n, cudaMemcpyDeviceToDevice,
+                                  c->stream));
+      CUDA_TRY(c, cudaMemcpyAsync(B.slice_off_old, B.slice_off, 8 * c->slice_cap,
+                                  cudaMemcpyDeviceToDevice, c->stream));
+      enqueue_rebuild(c, c->stream, 1);
+      s = sync_check(c, "pm_dem_run (rebuild)");
+      if (s == PM_E_CAPACITY) {
+        c->sticky = 0;
+        c->err.clear();
+        k_clear_abort<<<1, 1, 0, c->stream>>>(B.st);
+        s = layout_from_counts(c);
+        if (s) return s;
+        launch_verlet(c->P, B, c->n, c->stream);
+        s = sync_check(c, "pm_dem_run (rebuild retry)");
+      }
+      if (s) return s;
+      if ((s = dem_alloc(c, false))) return s;
+      launch_dem_remap(c->B, c->n, ci_old, c->stream);
+    }
+    launch_dem_forces(c->P, B, c->n, dt, c->stream);
+    launch_dem_integrate(c->P, B, c->n, dt, c->stream);
+    k_apply_pending<<<1, 1, 0, c->stream>>>(B.st);
+  }
+  s = read_state(c);
+  if (s) return s;
+  if (c->st_h->abort)
+    return set_err(c, c->st_h->abort, "pm_dem_run: %s (gid %lld) after %lld steps",
+                   device_error_name(c->st_h->abort), (long long)c->st_h->err_gid,
+                   (long long)done);
+  c->forces_valid = false;
+  if (rebuilds) *rebuilds = c->st_h->n_rebuilds - reb0;
+  return check_launch(c, "pm_dem_run");
+}
+
+pm_status pm_get_dem(pm_ctx c, float *omega4, float *torque4) {
+  if (!c) return PM_E_INVAL;
+  if (!c->have_dem || !c->B.omega[0]) return set_err(c, PM_E_STATE, "pm_get_dem: no DEM state");
+  cudaSetDevice(c->device);
+  pm_status s = read_state(c);
+  if (s) return s;
+  const int64_t n = c->n;
+  if (n == 0) return PM_OK;
+  if (omega4)
+    CUDA_TRY(c, cudaMemcpyAsync(omega4, c->B.omega[c->st_h->cur_id], 16 * n,
+                                cudaMemcpyDeviceToHost, c->stream));
+  if (torque4)
+    CUDA_TRY(c, cudaMemcpyAsync(torque4, c->B.torque, 16 * n, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return PM_OK;
 }
 
 pm_status pm_set_rho(pm_ctx c, const float *rho, int32_t mem) {

@@ -79,6 +79,13 @@ struct SPH {
   float g[3];
 };
 
+// DEM (Eqs. 9-13; readings R29-R33)
+struct DEM {
+  float R, m, inv_m, inv_I, kn, kt, gn, gt, mu, meff;
+  float g[3];
+  int walls[6];  // plane walls at the box faces x-lo, x-hi, y-lo, y-hi, z-lo, z-hi
+};
+
 struct Params {
   Box box;
   Grid grid;
@@ -92,6 +99,8 @@ struct Params {
   int dist;         // 1: sub-domain context (ghosts present, skip them as rows)
   float vmax;       // velocity limit (reading R22), 0 = off
   int sph_state;    // 1: the cell-sort reorder also permutes the SPH stepping state
+  int dem_state;    // 1: ... and the DEM angular velocities
+  DEM dem;
 };
 
 // Device buffers (pointers fixed between reallocations; captured in graphs).
@@ -108,6 +117,13 @@ struct Bufs {
   float4 *vold[2];     // SPH stepping: velocities of the previous step (Verlet)
   float *rold[2];      // SPH stepping: densities of the previous step
   float *drho;         // SPH stepping: density rate (Eq. 2), current order
+  float4 *omega[2];    // DEM angular velocities (by State::cur_id)
+  float4 *torque;      // DEM torques, current order
+  float4 *hist;        // DEM tangential displacement per list slot (SELL layout of nbr)
+  float4 *hist_old;    // ... of the previous list, kept across a rebuild
+  int32_t *nbr_old;    // previous list (rows, layout, lengths) for the history remap
+  int64_t *slice_off_old;
+  int32_t *cnt_old;
   int32_t *cell_of;    // cell id in the storage order the build started from
   int32_t *slot;       // unordered slot within the cell (atomic claim)
   int32_t *count;      // [ncell]
@@ -262,6 +278,9 @@ void launch_ke(const Params &P, const Bufs &B, int64_t n, cudaStream_t s);
 void launch_sph_density(const Params &P, const Bufs &B, int64_t n, cudaStream_t s);
 void launch_sph_forces(const Params &P, const Bufs &B, int64_t n, cudaStream_t s);
 void launch_sph_init_run(const Bufs &B, int64_t n, cudaStream_t s);
+void launch_dem_forces(const Params &P, const Bufs &B, int64_t n, float dt, cudaStream_t s);
+void launch_dem_integrate(const Params &P, const Bufs &B, int64_t n, float dt, cudaStream_t s);
+void launch_dem_remap(const Bufs &B, int64_t n, int ci_old, cudaStream_t s);
 void launch_sph_set_rho(const Params &P, const Bufs &B, int64_t n, const float *rho,
                         cudaStream_t s);
 void launch_sph_step(const Params &P, const Bufs &B, int64_t n, float cfl, int every,

@@ -41,6 +41,12 @@ class SPHParams(C.Structure):
                 ("g", C.c_float * 3)]
 
 
+class DEMParams(C.Structure):
+    _fields_ = [("R", C.c_float), ("m", C.c_float), ("I", C.c_float), ("kn", C.c_float),
+                ("kt", C.c_float), ("gamma_n", C.c_float), ("gamma_t", C.c_float),
+                ("mu", C.c_float), ("g", C.c_float * 3), ("walls", C.c_int32 * 6)]
+
+
 class SPHRunStats(C.Structure):
     _fields_ = [("steps", C.c_int64), ("rebuilds", C.c_int64), ("time", C.c_double),
                 ("dt_min", C.c_float), ("dt_max", C.c_float), ("dt_last", C.c_float)]
@@ -83,6 +89,9 @@ def lib(path: str = LIB_PATH):
         "pm_sph_forces": (st, [vp]),
         "pm_sph_run": (st, [vp, C.c_int64, C.c_float, C.c_int32, C.POINTER(SPHRunStats)]),
         "pm_set_rho": (st, [vp, vp, C.c_int32]),
+        "pm_set_dem": (st, [vp, C.POINTER(DEMParams)]),
+        "pm_dem_run": (st, [vp, C.c_float, C.c_int64, vp]),
+        "pm_get_dem": (st, [vp, vp, vp]),
         "pm_step_vv": (st, [vp, C.c_float, C.c_int64, C.POINTER(RunStats)]),
         "pm_count": (st, [vp, vp, vp, vp, vp]),
         "pm_get_cells": (st, [vp, vp, vp, vp]),
@@ -222,6 +231,26 @@ class Context:
 
     def sph_forces(self):
         self._check(self.L.pm_sph_forces(self.h))
+
+    def set_dem(self, p):
+        """p: dict with R, m, I, kn, kt, gn, gt, mu, g (3), walls (6 flags)."""
+        d = DEMParams(float(p["R"]), float(p["m"]), float(p["I"]), float(p["kn"]),
+                      float(p["kt"]), float(p["gn"]), float(p["gt"]), float(p["mu"]),
+                      (C.c_float * 3)(*[float(x) for x in p["g"]]),
+                      (C.c_int32 * 6)(*[int(x) for x in p["walls"]]))
+        self._check(self.L.pm_set_dem(self.h, C.byref(d)))
+
+    def dem_run(self, dt, nsteps):
+        reb = C.c_int64(0)
+        self._check(self.L.pm_dem_run(self.h, float(dt), int(nsteps), C.byref(reb)))
+        return int(reb.value)
+
+    def get_dem(self):
+        n = self.count()["n_owned"]
+        w = np.zeros((n, 4), np.float32)
+        t = np.zeros((n, 4), np.float32)
+        self._check(self.L.pm_get_dem(self.h, w.ctypes.data, t.ctypes.data))
+        return dict(omega=w, torque=t)
 
     def set_rho(self, rho):
         """Densities in the current internal order (as get_state returns them)."""

@@ -544,3 +544,48 @@ def test_sph_run_parity_small_dam(pm, orc):
     b = s.kind == 1
     assert np.array_equal(st["pos"][order][b], s.pos[b])
     c.close()
+
+
+def test_dem_parity_granular_packing(pm, orc):
+    """DEM (pm_dem_run, Eqs. 9-13, readings
+    R29-R33) against the fp64 oracle: 800 grains with walls, periodic y,
+    gravity, friction; after 200 and 1000 steps (the latter with ~20 Verlet
+    rebuilds that carry the contact histories over by gid) positions,
+    velocities and spins follow the oracle up to fp32 drift; a smaller skin
+    (more rebuilds) gives the same trajectory."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "dem_check", os.path.join(os.path.dirname(__file__), "..", "tools", "dem_check.py"))
+    dc = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(dc)
+    P = dc.P
+    pos, vel, gid, lo, hi, per = dc.granular()
+
+    def gpu(nsteps, skin):
+        c = pm.Context()
+        c.set_domain(lo, hi, per)
+        c.set_cutoff(2 * P["R"], skin)
+        c.set_dem(P)
+        c.place(pos, vel, gid)
+        reb = c.dem_run(2e-4, nsteps)
+        st = c.get_state()
+        w = c.get_dem()["omega"]
+        o = np.argsort(st["gid"])
+        c.close()
+        return st["pos"][o, :3].astype(np.float64), st["vel"][o, :3].astype(np.float64), \
+            w[o, :3].astype(np.float64), reb
+
+    for nsteps, tx, tv, tw in ((200, 1e-3, 2e-3, 2e-2), (1000, 5e-3, 5e-3, 2e-2)):
+        x, v, w, reb = gpu(nsteps, 0.02)
+        xr, vr, wr, _ = orc.dem_run(pos, vel, np.zeros_like(pos), gid, lo, hi, per, P["walls"], P,
+                                    2e-4, nsteps)
+        assert np.max(np.abs(x - xr)) / P["R"] < tx
+        assert np.max(np.abs(v - vr)) / np.max(np.abs(vr)) < tv
+        assert np.max(np.abs(w - wr)) / np.max(np.abs(wr)) < tw
+        if nsteps == 1000:
+            assert reb >= 10
+            x2, v2, w2, reb2 = gpu(nsteps, 0.008)
+            assert reb2 > reb
+            assert np.max(np.abs(x2 - x)) / P["R"] < tx
+            assert np.max(np.abs(w2 - w)) / np.max(np.abs(wr)) < tw

@@ -463,3 +463,66 @@ def test_sph_run_conserves_momentum(orc):
     m0 = vel[:, :3].astype(np.float64).sum(axis=0)
     assert np.max(np.abs(v.sum(axis=0) - m0)) < 1e-11 * np.abs(vel[:, :3]).sum()
     assert np.all(dt > 0) and np.all(np.isfinite(rho))
+
+
+# ------------------------------------------------------------------ DEM (NEXT-4)
+DEM_P = dict(R=0.06, m=1.0, I=1.44e-3, kn=7849.0, kt=2243.0, gn=3.401, gt=0.0, mu=0.5,
+             g=(0.0, 0.0, -9.81))
+
+
+def test_dem_free_fall_leapfrog(orc):
+    """Eq. 13 leapfrog without contacts: v_n = n dt g, x_n = x0 + dt^2 g n(n+1)/2."""
+    pos = np.array([[0.5, 0.5, 0.5, 0.0]], np.float32)
+    z = np.zeros((1, 4), np.float32)
+    dt, n = 1e-3, 200
+    x, v, w, nh = orc.dem_run(pos, z, z, np.array([0]), [0, 0, 0], [1, 1, 1], [0, 0, 0],
+                              [0] * 6, DEM_P, dt, n)
+    assert v[0, 2] == pytest.approx(-9.81 * n * dt, rel=1e-12)
+    assert x[0, 2] == pytest.approx(0.5 - 9.81 * dt * dt * n * (n + 1) / 2, rel=1e-12)
+    assert nh == 0 and np.all(w == 0)
+
+
+def test_dem_resting_on_floor_closed_form(orc):
+    """A damped particle on the z-lo wall settles where the Hertz force
+    sqrt(delta/2R) kn delta balances m g: delta* = (m g sqrt(2R)/kn)^(2/3)
+    (Eqs. 9, 11); gamma_n raised so the oscillation dies out quickly."""
+    p = dict(DEM_P, gn=300.0)
+    pos = np.array([[0.5, 0.5, p["R"], 0.0]], np.float32)
+    z = np.zeros((1, 4), np.float32)
+    x, v, _, _ = orc.dem_run(pos, z, z, np.array([0]), [0, 0, 0], [1, 1, 1], [0, 0, 0],
+                             [0, 0, 0, 0, 1, 0], p, 1e-3, 20000)
+    ds = (p["m"] * 9.81 * math.sqrt(2 * p["R"]) / p["kn"]) ** (2.0 / 3.0)
+    assert x[0, 2] == pytest.approx(p["R"] - ds, rel=1e-6)
+    assert abs(v[0, 2]) < 1e-9
+
+
+def test_dem_elastic_head_on_and_momentum(orc):
+    """gamma_n = 0, no gravity: a head-on Hertz collision is elastic (speeds
+    come back to v0 up to O(dt)) and conserves momentum exactly (F_qp = -F_pq);
+    no tangential motion, no spin."""
+    p = dict(DEM_P, gn=0.0, g=(0.0, 0.0, 0.0))
+    pos = np.array([[0.4, 0.5, 0.5, 0], [0.6, 0.5, 0.5, 0]], np.float32)
+    vel = np.array([[0.5, 0, 0, 0], [-0.5, 0, 0, 0]], np.float32)
+    z = np.zeros((2, 4), np.float32)
+    x, v, w, nh = orc.dem_run(pos, vel, z, np.array([0, 1]), [0, 0, 0], [1, 1, 1], [0, 0, 0],
+                              [0] * 6, p, 2e-5, 20000)
+    assert nh == 0  # separated again
+    assert v[0, 0] == pytest.approx(-0.5, rel=2e-3) and v[1, 0] == pytest.approx(0.5, rel=2e-3)
+    assert abs(v[:, 0].sum()) < 1e-12 and np.all(w == 0)
+
+
+def test_dem_oblique_friction_momentum_and_spin(orc):
+    """An oblique collision with friction (Eqs. 10, 12, Coulomb cap): linear
+    momentum is conserved to rounding, both grains get the same torque
+    (-R n x F_t for each ordered pair), so they spin equally, and friction
+    takes kinetic energy away."""
+    p = dict(DEM_P, g=(0.0, 0.0, 0.0))
+    pos = np.array([[0.4, 0.5, 0.5, 0], [0.6, 0.53, 0.5, 0]], np.float32)
+    vel = np.array([[0.5, 0, 0, 0], [-0.5, 0, 0, 0]], np.float32)
+    z = np.zeros((2, 4), np.float32)
+    x, v, w, nh = orc.dem_run(pos, vel, z, np.array([0, 1]), [0, 0, 0], [1, 1, 1], [0, 0, 0],
+                              [0] * 6, p, 2e-5, 20000)
+    assert np.max(np.abs(v.sum(axis=0))) < 1e-12
+    assert np.abs(w[0, 2]) > 1e-3 and w[0] == pytest.approx(w[1], rel=1e-9, abs=1e-12)
+    ke0, ke1 = 0.5 * 2 * 0.25, 0.5 * np.sum(v * v) + 0.5 * p["I"] * np.sum(w * w)
+    assert ke1 < ke0
