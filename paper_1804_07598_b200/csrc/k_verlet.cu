@@ -119,7 +119,7 @@ __device__ __forceinline__ void scan_any(const Params &P, const float4 *__restri
 // (the extra candidates of the union are farther than r_v and rejected by
 // the same pinned test).  All lanes read the same position each iteration
 // (broadcast), there is no divergence, and rows come out in a fixed order.
-__global__ void __launch_bounds__(256, 3) k_verlet(Params P, Bufs B, int n) {
+__global__ void __launch_bounds__(256, 4) k_verlet(Params P, Bufs B, int n) {
   State *st = B.st;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
