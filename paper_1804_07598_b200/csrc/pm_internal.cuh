@@ -257,6 +257,53 @@ PM_DEV void raise_error(State *st, int code, long long gid) {
   if (atomicCAS(&st->abort, 0, code) == 0) st->err_gid = gid;
 }
 
+// ----------------------------------------------------------------------------
+// TMA bulk copies (cp.async.bulk, sm_90+) completing on a shared-memory
+// mbarrier: one elected thread sets the expected byte count, any thread may
+// issue copies (16-byte aligned, sizes multiple of 16), every thread waits.
+// ----------------------------------------------------------------------------
+PM_DEV uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+PM_DEV void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+PM_DEV void mbar_arrive_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+PM_DEV void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Bounded wait: returns false if the phase did not complete within ~2^24
+// polls (a byte-count mismatch would otherwise hang the GPU; the caller
+// raises a device error instead).
+PM_DEV bool mbar_wait(uint64_t *bar, unsigned parity) {
+  for (int it = 0; it < (1 << 24); ++it) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return true;
+  }
+  return false;
+}
+
+
+
 }  // namespace pm
 
 // ----------------------------------------------------------------------------
