@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(256) k_sph_density(Params P, Bufs B, int n) {
   if (!isfinite(rho + pr)) raise_error(st, -8 /*PM_E_NONFINITE*/, (long long)B.gid[st->cur_id][i]);
 }
 
-__global__ void __launch_bounds__(256) k_sph_forces(Params P, Bufs B, int n) {
+__global__ void __launch_bounds__(256, 3) k_sph_forces(Params P, Bufs B, int n) {
   State *st = B.st;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -139,19 +139,18 @@ __global__ void __launch_bounds__(256) k_sph_forces(Params P, Bufs B, int n) {
   const int *nb = B.nbr + nbr_row_base(B, i);
   float ax = 0.f, ay = 0.f, az = 0.f;
   const float acb = P.sph.alpha * P.sph.cbar;
-  auto pair = [&](int j, bool valid) {
-    const float3 d = delta3(P, xi, __ldg(pos + j));  // x_j - x_i
+  // gathers of the four pairs first, approximate divisions (as k_sph_rates)
+  auto pair = [&](const float4 &xj, const float4 &vj, const float2 &rpj, bool valid) {
+    const float3 d = delta3(P, xi, xj);  // x_j - x_i
     const float d2 = dist2(d.x, d.y, d.z);
     const float rinv = fast_rsqrt(d2);
     const float q = d2 * rinv * P.sph.inv_h;
     const float dwdr = P.sph.dw_norm * dw_shape(q);
-    const float4 vj = __ldg(vel + j);
-    const float2 rpj = __ldg(rhoP + j);
     // v_ij . r_ij with r_ij = x_i - x_j = -d
     const float vr = -((vi.x - vj.x) * d.x + (vi.y - vj.y) * d.y + (vi.z - vj.z) * d.z);
-    const float mu = P.sph.h * vr / (d2 + P.sph.eta2);
-    const float pi_ij = vr < 0.0f ? -acb * mu / (0.5f * (rpi.x + rpj.x)) : 0.0f;
-    const float coef = P.sph.mass * ((rpi.y + rpj.y) / (rpi.x * rpj.x) + pi_ij);
+    const float mu = __fdividef(P.sph.h * vr, d2 + P.sph.eta2);
+    const float pi_ij = vr < 0.0f ? __fdividef(-2.0f * acb * mu, rpi.x + rpj.x) : 0.0f;
+    const float coef = P.sph.mass * (__fdividef(rpi.y + rpj.y, rpi.x * rpj.x) + pi_ij);
     // a_i -= coef * grad_i W,  grad_i W = (x_i - x_j)/r dW/dr = -d rinv dwdr
     const float sc = (valid && q < 2.0f) ? coef * rinv * dwdr : 0.0f;
     ax = fmaf(sc, d.x, ax);
@@ -159,10 +158,16 @@ __global__ void __launch_bounds__(256) k_sph_forces(Params P, Bufs B, int n) {
     az = fmaf(sc, d.z, az);
   };
   for_row(nb, cnt, [&](int ja, int jb, int jc, int jd, int rem) {
-    pair(ja, true);
-    pair(jb, rem > 1);
-    pair(jc, rem > 2);
-    pair(jd, rem > 3);
+    const float4 xa = __ldg(pos + ja), xb = __ldg(pos + jb);
+    const float4 xc = __ldg(pos + jc), xd = __ldg(pos + jd);
+    const float4 va = __ldg(vel + ja), vb = __ldg(vel + jb);
+    const float4 vc = __ldg(vel + jc), vd = __ldg(vel + jd);
+    const float2 ra = __ldg(rhoP + ja), rb = __ldg(rhoP + jb);
+    const float2 rc = __ldg(rhoP + jc), rd = __ldg(rhoP + jd);
+    pair(xa, va, ra, true);
+    pair(xb, vb, rb, rem > 1);
+    pair(xc, vc, rc, rem > 2);
+    pair(xd, vd, rd, rem > 3);
   });
   ax += P.sph.g[0];
   ay += P.sph.g[1];
@@ -191,39 +196,40 @@ __device__ __forceinline__ void warp_min_atomic(unsigned *dst, float v) {
   if ((threadIdx.x & 31) == 0) atomicMin(dst, u);
 }
 
-__global__ void __launch_bounds__(256) k_sph_rates(Params P, Bufs B, int n) {
+__global__ void __launch_bounds__(256, 3) k_sph_rates(Params P, Bufs B, int n) {
   State *st = B.st;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = i < n;
   const int cp = st->cur_pv, ci = st->cur_id;
+  // pos.w = P and vel.w = rho during a run (k_sph_init_run, k_sph_verlet):
+  // two 16-byte gathers per pair instead of three.
   const float4 *__restrict__ pos = B.pos[cp];
   const float4 *__restrict__ vel = B.vel[cp];
-  const float2 *__restrict__ rhoP = B.rhoP[ci];
   float ax = 0.f, ay = 0.f, az = 0.f, D = 0.f, mumax = 0.f;
   bool fluid = false;
   if (active) {
     fluid = !(B.kind[ci][i] & 1);
     const float4 xi = pos[i];
     const float4 vi = vel[i];
-    const float2 rpi = rhoP[i];
     const float acb = P.sph.alpha * P.sph.cbar;
-    auto pair = [&](int j, bool valid) {
-      const float3 d = delta3(P, xi, __ldg(pos + j));  // x_j - x_i
+    // The four pairs' gathers are issued before any of their arithmetic
+    // (memory-level parallelism per thread), and the divisions are the
+    // approximate MUFU.RCP kind (no IEEE slow path branching the loop).
+    auto pair = [&](const float4 &xj, const float4 &vj, bool valid) {
+      const float3 d = delta3(P, xi, xj);  // x_j - x_i
       const float d2 = dist2(d.x, d.y, d.z);
       const float rinv = fast_rsqrt(d2);
       const float q = d2 * rinv * P.sph.inv_h;
       const bool in = valid && q < 2.0f && d2 > 0.0f;
       const float dwdr = P.sph.dw_norm * dw_shape(q);
-      const float4 vj = __ldg(vel + j);
-      const float2 rpj = __ldg(rhoP + j);
       // r_ij = x_i - x_j = -d;  grad_i W = r_ij / r dW/dr = -d rinv dwdr
       const float vx = vi.x - vj.x, vy = vi.y - vj.y, vz = vi.z - vj.z;
       const float vd = vx * d.x + vy * d.y + vz * d.z;  // = -(v_ij . r_ij)
       const float gsc = rinv * dwdr;
       const float vr = -vd;
-      const float mu = P.sph.h * vr / (d2 + P.sph.eta2);
-      const float pi_ij = vr < 0.0f ? -acb * mu / (0.5f * (rpi.x + rpj.x)) : 0.0f;
-      const float coef = P.sph.mass * ((rpi.y + rpj.y) / (rpi.x * rpj.x) + pi_ij);
+      const float mu = __fdividef(P.sph.h * vr, d2 + P.sph.eta2);
+      const float pi_ij = vr < 0.0f ? __fdividef(-2.0f * acb * mu, vi.w + vj.w) : 0.0f;
+      const float coef = P.sph.mass * (__fdividef(xi.w + xj.w, vi.w * vj.w) + pi_ij);
       const float sc = in ? coef * gsc : 0.0f;
       ax = fmaf(sc, d.x, ax);  // a_i -= coef grad_i W
       ay = fmaf(sc, d.y, ay);
@@ -234,10 +240,14 @@ __global__ void __launch_bounds__(256) k_sph_rates(Params P, Bufs B, int n) {
     const int cnt = B.cnt[i];
     const int *nb = B.nbr + nbr_row_base(B, i);
     for_row(nb, cnt, [&](int ja, int jb, int jc, int jd, int rem) {
-      pair(ja, true);
-      pair(jb, rem > 1);
-      pair(jc, rem > 2);
-      pair(jd, rem > 3);
+      const float4 xa = __ldg(pos + ja), xb = __ldg(pos + jb);
+      const float4 xc = __ldg(pos + jc), xd = __ldg(pos + jd);
+      const float4 va = __ldg(vel + ja), vb = __ldg(vel + jb);
+      const float4 vc = __ldg(vel + jc), vd = __ldg(vel + jd);
+      pair(xa, va, true);
+      pair(xb, vb, rem > 1);
+      pair(xc, vc, rem > 2);
+      pair(xd, vd, rem > 3);
     });
     if (fluid) {
       ax += P.sph.g[0];
@@ -298,8 +308,9 @@ __global__ void __launch_bounds__(256) k_sph_verlet(Params P, Bufs B, int n) {
     const float D = B.drho[i];
     const float rho = B.rhoP[ci][i].x, rold = B.rold[ci][i];
     const float rn = euler ? fmaf(dt, D, rho) : fmaf(2.0f * dt, D, rold);
+    const float pn = tait(P, rn);
     B.rold[ci][i] = rho;
-    B.rhoP[ci][i] = make_float2(rn, tait(P, rn));
+    B.rhoP[ci][i] = make_float2(rn, pn);
     const float4 x = B.pos[cp][i];
     const float4 v = B.vel[cp][i];
     float4 xn = x, vn = v;
@@ -315,7 +326,7 @@ __global__ void __launch_bounds__(256) k_sph_verlet(Params P, Bufs B, int n) {
 #pragma unroll
       for (int d = 0; d < 3; ++d)
         if (P.box.per[d]) r3[d] = wrap1(r3[d], P.box.lo[d], P.box.hi[d], P.box.L[d]);
-      xn = make_float4(r3[0], r3[1], r3[2], x.w);
+      xn = make_float4(r3[0], r3[1], r3[2], 0.f);
       const float4 xr = B.xref[i];
       const float dx = pair_delta1(xr.x, xn.x, P.box.L[0], P.box.halfL[0], P.box.per[0]);
       const float dy = pair_delta1(xr.y, xn.y, P.box.L[1], P.box.halfL[1], P.box.per[1]);
@@ -326,6 +337,8 @@ __global__ void __launch_bounds__(256) k_sph_verlet(Params P, Bufs B, int n) {
       if (!P.box.per[2] && (xn.z < P.box.lo[2] || xn.z >= P.box.hi[2])) far = true;
     }
     B.vold[ci][i] = v;
+    xn.w = pn;  // the packed P and rho k_sph_rates gathers
+    vn.w = rn;
     B.pos[cp ^ 1][i] = xn;
     B.vel[cp ^ 1][i] = vn;
   }
@@ -343,7 +356,10 @@ __global__ void __launch_bounds__(256) k_sph_init_run(Bufs B, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int ci = st->cur_id;
   if (i < n) {
-    B.rold[ci][i] = B.rhoP[ci][i].x;
+    const float2 rp = B.rhoP[ci][i];
+    B.rold[ci][i] = rp.x;
+    B.pos[st->cur_pv][i].w = rp.y;  // packed for k_sph_rates
+    B.vel[st->cur_pv][i].w = rp.x;
     B.vold[ci][i] = B.vel[st->cur_pv][i];
   }
   if (i == 0) {
