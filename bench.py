@@ -185,6 +185,37 @@ def sph_pass(dev, stream, repeats=10):
                     "rebuilds": r["rebuilds"], "dt_min": r["dt_min"], "dt_max": r["dt_max"]}}
 
 
+def dem_run(dev, stream, warm=300, steps=500):
+    """DEM avalanche (inputs.dem_avalanche, 679,140 grains,
+    PAPER.md:540-548) stepped by pm_dem_run; CUDA events on the context
+    stream around `steps` steps after `warm` settling steps from the lattice."""
+    import torch
+    from paper_1804_07598_b200 import inputs, pm
+    s = inputs.dem_avalanche()
+    p = s.params
+    c = pm.Context(device=dev, stream=stream.cuda_stream)
+    c.set_domain(s.lo, s.hi, s.periodic)
+    c.set_cutoff(2.0 * p["R"], p["skin"])
+    c.set_dem(p)
+    c.place(s.pos, s.vel, s.gid)
+    c.dem_run(p["dt"], warm)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    reb = c.dem_run(p["dt"], steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    nnz = c.count()["nnz"]
+    c.close()
+    return {"workload": "DEM avalanche (PAPER.md:540-548): %d grains, R=0.06, lattice start, "
+                        "30-degree incline, walls x and floor, periodic y, Hertz + tangential "
+                        "history + Coulomb, leapfrog, dt=2e-4, skin 0.02" % s.n,
+            "n_particles": s.n, "steps": steps, "after_steps": warm, "ms_per_step": ms,
+            "value": s.n / (ms * 1e-3), "unit": UNIT, "rebuilds": reb,
+            "mean_row": nnz / s.n}
+
+
 def run_reference(args):
     """--impl reference: the oracle as it stands on the host cores, on this
     arm's config/metric; each step a bounded sample of cfg2 particles."""
@@ -312,6 +343,7 @@ def run_ours(args):
     d2h = (out_pos.numel() * 4 + out_vel.numel() * 4)
 
     sph = sph_pass(dev, stream)
+    dem = dem_run(dev, stream)
     cpu = cpu_baseline() if not args.no_cpu_baseline else None
     launches = 2 * args.steps + 11 * stats["rebuilds"] + 3
     line = {
@@ -339,6 +371,7 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clk,
         "sph": sph,
+        "dem": dem,
     }
     # pairs/s: ordered pairs inside r_cut ~ measured once from the energy pass
     print(json.dumps(line), flush=True)

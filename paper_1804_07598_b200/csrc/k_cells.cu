@@ -166,17 +166,9 @@ __device__ __forceinline__ bool same_pos(const float4 &a, const float4 &b) {
   return a.x == b.x && a.y == b.y && a.z == b.z;
 }
 
-__global__ void __launch_bounds__(256) k_segsort(Bufs B, const int32_t *__restrict__ tmp,
-                                                 int ncell) {
-  const int cell = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  const int lane = threadIdx.x & 31;
-  if (cell >= ncell) return;  // whole warp exits together
-  const int s = B.start[cell], e = B.start[cell + 1], m = e - s;
-  if (m == 0) return;
-  if (m == 1) {
-    if (lane == 0) B.perm[s] = tmp[s];
-    return;
-  }
+// One cell of m >= 2 members, s = its first slot, by the whole warp.
+__device__ __forceinline__ void warp_cell(const Bufs &B, const int32_t *__restrict__ tmp,
+                                          int cell, int s, int m, int lane) {
   State *st = B.st;
   const float4 *__restrict__ pos = B.pos[st->cur_pv];
   const unsigned full = 0xffffffffu;
@@ -215,6 +207,81 @@ __global__ void __launch_bounds__(256) k_segsort(Bufs B, const int32_t *__restri
   }
   // more than 32 members: defer to the block-level sort (k_segsort_big)
   if (lane == 0) B.big_cells[atomicAdd(&st->n_big, 1)] = cell;
+}
+
+
+__global__ void __launch_bounds__(256) k_segsort(Bufs B, const int32_t *__restrict__ tmp,
+                                                 int ncell) {
+  const int cell = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (cell >= ncell) return;  // whole warp exits together
+  const int s = B.start[cell], e = B.start[cell + 1], m = e - s;
+  if (m == 0) return;
+  if (m == 1) {
+    if (lane == 0) B.perm[s] = tmp[s];
+    return;
+  }
+  warp_cell(B, tmp, cell, s, m, lane);
+}
+
+// Sparse grids (fewer than ~4 particles per cell, e.g. a granular bed in a
+// large domain): one lane per cell.  Cells of <= 8 members are sorted in
+// registers by an optimal 19-comparator network and checked pairwise for
+// coincident positions by their own lane; wider cells are taken by the whole
+// warp, one after another (warp_cell).  Same result as k_segsort.
+constexpr int kThinMax = 8;
+
+__device__ __forceinline__ void cswap(int &a, int &b) {
+  const int lo = min(a, b), hi = max(a, b);
+  a = lo;
+  b = hi;
+}
+
+__global__ void __launch_bounds__(256) k_segsort_thin(Bufs B, const int32_t *__restrict__ tmp,
+                                                      int ncell) {
+  const int cell = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  int s = 0, m = 0;
+  if (cell < ncell) {
+    s = B.start[cell];
+    m = B.start[cell + 1] - s;
+  }
+  if (m == 1) B.perm[s] = tmp[s];
+  if (m >= 2 && m <= kThinMax) {
+    int v[kThinMax];
+#pragma unroll
+    for (int k = 0; k < kThinMax; ++k) v[k] = (k < m) ? tmp[s + k] : 0x7fffffff;
+    cswap(v[0], v[2]); cswap(v[1], v[3]); cswap(v[4], v[6]); cswap(v[5], v[7]);
+    cswap(v[0], v[4]); cswap(v[1], v[5]); cswap(v[2], v[6]); cswap(v[3], v[7]);
+    cswap(v[0], v[1]); cswap(v[2], v[3]); cswap(v[4], v[5]); cswap(v[6], v[7]);
+    cswap(v[2], v[4]); cswap(v[3], v[5]);
+    cswap(v[1], v[4]); cswap(v[3], v[6]);
+    cswap(v[1], v[2]); cswap(v[3], v[4]); cswap(v[5], v[6]);
+    State *st = B.st;
+    const float4 *__restrict__ pos = B.pos[st->cur_pv];
+    float4 p[kThinMax];
+#pragma unroll
+    for (int k = 0; k < kThinMax; ++k) {
+      if (k < m) {
+        B.perm[s + k] = v[k];
+        p[k] = pos[v[k]];
+      }
+    }
+    int dup = -1;
+#pragma unroll
+    for (int k = 1; k < kThinMax; ++k)
+#pragma unroll
+      for (int l = 0; l < k; ++l)
+        if (k < m && same_pos(p[k], p[l])) dup = v[k];
+    if (dup >= 0) st->coinc_gid = (long long)B.gid[st->cur_id][dup];
+  }
+  unsigned wide = __ballot_sync(0xffffffffu, m > kThinMax);
+  while (wide) {
+    const int l = __ffs(wide) - 1;
+    wide &= wide - 1;
+    const int ws = __shfl_sync(0xffffffffu, s, l), wm = __shfl_sync(0xffffffffu, m, l);
+    warp_cell(B, tmp, cell - lane + l, ws, wm, lane);
+  }
 }
 
 // Cells with more than 32 members (clustered inputs, up to ~3000): one block
@@ -284,7 +351,7 @@ __global__ void __launch_bounds__(256) k_reorder(Bufs B, int64_t n, int sph_stat
     B.vold[ci ^ 1][k] = B.vold[ci][j];
     B.rold[ci ^ 1][k] = B.rold[ci][j];
   }
-  if (dem_state) B.omega[ci ^ 1][k] = B.omega[ci][j];
+  if (dem_state) B.omega[cp ^ 1][k] = B.omega[cp][j];  // double-buffered per step
 }
 
 __global__ void k_flip(Bufs B, int flip_pv, int flip_id, int count_rebuild) {
@@ -326,7 +393,10 @@ void launch_sort_reorder(const Params &P, const Bufs &B, int64_t n, cudaStream_t
   if (n <= 0) return;
   int32_t *tmp = B.sorttmp;
   k_scatter<<<blocks_for(n, 256), 256, 0, s>>>(B, tmp, n);
-  k_segsort<<<blocks_for((int64_t)P.grid.ncell * 32, 256), 256, 0, s>>>(B, tmp, P.grid.ncell);
+  if (n < 4 * (int64_t)P.grid.ncell)  // sparse grid: lane per cell
+    k_segsort_thin<<<blocks_for(P.grid.ncell, 256), 256, 0, s>>>(B, tmp, P.grid.ncell);
+  else
+    k_segsort<<<blocks_for((int64_t)P.grid.ncell * 32, 256), 256, 0, s>>>(B, tmp, P.grid.ncell);
   k_segsort_big<<<148, 512, 0, s>>>(B, tmp);
   k_reorder<<<blocks_for(n, 256), 256, 0, s>>>(B, n, P.sph_state, P.dem_state);
 }

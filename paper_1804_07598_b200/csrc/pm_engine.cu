@@ -62,6 +62,13 @@ struct pm_ctx_s {
   float graph_dt = 0.f;
   bool graph_prof = false;
   cudaGraphNode_t ev_node[2] = {nullptr, nullptr};
+  // DEM step graph (pm_dem_run); rebuilt whenever what it captured changes
+  cudaGraphExec_t dem_exec = nullptr;
+  cudaGraph_t dem_graph = nullptr;
+  Params dem_key_P{};
+  Bufs dem_key_B{};
+  int64_t dem_key_n = -1;
+  float dem_key_dt = 0.f;
 
   // multi-GPU decomposition (pm_set_decomposition)
   bool dist = false;
@@ -164,6 +171,14 @@ void destroy_graph(pm_ctx c) {
   c->exec = nullptr;
   c->graph = nullptr;
   c->graph_valid = false;
+}
+
+void destroy_dem_graph(pm_ctx c) {
+  if (c->dem_exec) cudaGraphExecDestroy(c->dem_exec);
+  if (c->dem_graph) cudaGraphDestroy(c->dem_graph);
+  c->dem_exec = nullptr;
+  c->dem_graph = nullptr;
+  c->dem_key_n = -1;
 }
 
 pm_status check_launch(pm_ctx c, const char *what) {
@@ -647,6 +662,7 @@ void pm_destroy(pm_ctx c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   destroy_graph(c);
+  destroy_dem_graph(c);
   Bufs &B = c->B;
   for (int b = 0; b < 2; ++b) {
     cudaFree(B.pos[b]);
@@ -926,6 +942,61 @@ static pm_status dem_alloc(pm_ctx c, bool old_copies) {
   return PM_OK;
 }
 
+// One DEM rebuild: keep the old rows and histories, cell sort + Verlet build,
+// carry the histories over by partner gid (also the graph's IF body).
+static void enqueue_dem_rebuild(pm_ctx c, cudaStream_t s) {
+  launch_dem_save(c->B, c->n, s);
+  enqueue_rebuild(c, s, 1);
+  launch_dem_remap(c->B, c->n, s);
+}
+
+// The DEM step graph: k_dem_step_begin -> IF(need_rebuild) { save ->
+// cell sort -> Verlet -> remap } -> k_dem_step (contacts + leapfrog).  No host
+// round trip per step; a Verlet capacity overflow inside the graph aborts the
+// remaining steps (every kernel checks st->abort) and pm_dem_run resumes.
+static pm_status dem_graph_ready(pm_ctx c, float dt) {
+  if (c->dem_exec && c->dem_key_n == c->n && c->dem_key_dt == dt &&
+      !std::memcmp(&c->dem_key_P, &c->P, sizeof(Params)) &&
+      !std::memcmp(&c->dem_key_B, &c->B, sizeof(Bufs)))
+    return PM_OK;
+  destroy_dem_graph(c);
+  cudaGraph_t g = nullptr;
+  CUDA_TRY(c, cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  CUDA_TRY(c, cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
+  cudaStream_t cs = c->cap_stream;
+  const cudaStreamCaptureMode mode = cudaStreamCaptureModeThreadLocal;
+  CUDA_TRY(c, cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, mode));
+  launch_dem_step_begin(c->B, h, cs);
+  CUDA_TRY(c, cudaStreamEndCapture(cs, &g));
+  size_t nn = 0;
+  CUDA_TRY(c, cudaGraphGetNodes(g, nullptr, &nn));
+  if (nn != 1) return set_err(c, PM_E_CUDA, "dem graph: expected 1 node, got %zu", nn);
+  cudaGraphNode_t nA;
+  CUDA_TRY(c, cudaGraphGetNodes(g, &nA, &nn));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeIf;
+  cp.conditional.size = 1;
+  cudaGraphNode_t nC;
+  CUDA_TRY(c, cudaGraphAddNode(&nC, g, &nA, 1, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CUDA_TRY(c, cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, mode));
+  enqueue_dem_rebuild(c, cs);
+  CUDA_TRY(c, cudaStreamEndCapture(cs, &body));
+  CUDA_TRY(c, cudaStreamBeginCaptureToGraph(cs, g, &nC, nullptr, 1, mode));
+  launch_dem_step(c->P, c->B, c->n, dt, cs);
+  CUDA_TRY(c, cudaStreamEndCapture(cs, &g));
+  CUDA_TRY(c, cudaGraphInstantiate(&c->dem_exec, g, 0));
+  c->dem_graph = g;
+  c->dem_key_P = c->P;
+  c->dem_key_B = c->B;
+  c->dem_key_n = c->n;
+  c->dem_key_dt = dt;
+  return PM_OK;
+}
+
 pm_status pm_dem_run(pm_ctx c, float dt, int64_t nsteps, int64_t *rebuilds) {
   pm_status s = check_ready(c);
   if (s) return s;
@@ -948,45 +1019,64 @@ pm_status pm_dem_run(pm_ctx c, float dt, int64_t nsteps, int64_t *rebuilds) {
     if ((s = dem_alloc(c, false))) return s;
     CUDA_TRY(c, cudaMemsetAsync(B.hist, 0, 16 * c->nbr_ints, c->stream));
   }
+  if ((s = dem_alloc(c, true))) return s;
   s = read_state(c);
   if (s) return s;
   const long long reb0 = c->st_h->n_rebuilds;
   k_clear_rebuild<<<1, 1, 0, c->stream>>>(B.st);
   int64_t done = 0;
-  for (; done < nsteps; ++done) {
-    s = read_state(c);
-    if (s) return s;
-    if (c->st_h->abort) break;
-    if (c->st_h->need_rebuild) {
-      // keep the old list and histories, rebuild, carry the histories over
-      if ((s = dem_alloc(c, true))) return s;
-      const int ci_old = c->st_h->cur_id;
-      CUDA_TRY(c, cudaMemcpyAsync(B.nbr_old, B.nbr, 4 * c->nbr_ints, cudaMemcpyDeviceToDevice,
-                                  c->stream));
-      CUDA_TRY(c, cudaMemcpyAsync(B.hist_old, B.hist, 16 * c->nbr_ints,
-                                  cudaMemcpyDeviceToDevice, c->stream));
-      CUDA_TRY(c, cudaMemcpyAsync(B.cnt_old, B.cnt, 4 * c->n, cudaMemcpyDeviceToDevice,
-                                  c->stream));
-      CUDA_TRY(c, cudaMemcpyAsync(B.slice_off_old, B.slice_off, 8 * c->slice_cap,
-                                  cudaMemcpyDeviceToDevice, c->stream));
-      enqueue_rebuild(c, c->stream, 1);
-      s = sync_check(c, "pm_dem_run (rebuild)");
-      if (s == PM_E_CAPACITY) {
-        c->sticky = 0;
-        c->err.clear();
-        k_clear_abort<<<1, 1, 0, c->stream>>>(B.st);
-        s = layout_from_counts(c);
-        if (s) return s;
-        launch_verlet(c->P, B, c->n, c->stream);
-        s = sync_check(c, "pm_dem_run (rebuild retry)");
-      }
+  if (c->use_graphs) {
+    // every resume completes the aborted step, so nsteps + 1 passes suffice
+    for (int64_t attempt = 0; attempt <= nsteps && done < nsteps; ++attempt) {
+      if ((s = dem_graph_ready(c, dt))) return s;
+      k_run_init<<<1, 1, 0, c->stream>>>(B.st, (long long)(nsteps - done));
+      for (int64_t k = done; k < nsteps; ++k) CUDA_TRY(c, cudaGraphLaunch(c->dem_exec, c->stream));
+      k_apply_pending<<<1, 1, 0, c->stream>>>(B.st);
+      s = read_state(c);
       if (s) return s;
+      done += c->st_h->steps_done;
+      if (c->st_h->abort != PM_E_CAPACITY || done >= nsteps) break;
+      // the Verlet build of step `done` overflowed: the cells are sorted and
+      // the old rows saved; grow the layout from the exact counts, build,
+      // remap, and finish that step outside the graph
+      k_clear_abort<<<1, 1, 0, c->stream>>>(B.st);
+      if ((s = layout_from_counts(c))) return s;
+      launch_verlet(c->P, B, c->n, c->stream);
+      if ((s = sync_check(c, "pm_dem_run (rebuild retry)"))) return s;
       if ((s = dem_alloc(c, false))) return s;
-      launch_dem_remap(c->B, c->n, ci_old, c->stream);
+      launch_dem_remap(B, c->n, c->stream);
+      launch_dem_step(c->P, B, c->n, dt, c->stream);
+      k_apply_pending<<<1, 1, 0, c->stream>>>(B.st);
+      if ((s = sync_check(c, "pm_dem_run (resumed step)"))) return s;
+      done += 1;
+      if ((s = dem_alloc(c, true))) return s;
     }
-    launch_dem_forces(c->P, B, c->n, dt, c->stream);
-    launch_dem_integrate(c->P, B, c->n, dt, c->stream);
-    k_apply_pending<<<1, 1, 0, c->stream>>>(B.st);
+  } else {
+    for (; done < nsteps; ++done) {
+      s = read_state(c);
+      if (s) return s;
+      if (c->st_h->abort) break;
+      if (c->st_h->need_rebuild) {
+        if ((s = dem_alloc(c, true))) return s;
+        enqueue_dem_rebuild(c, c->stream);
+        s = sync_check(c, "pm_dem_run (rebuild)");
+        if (s == PM_E_CAPACITY) {
+          c->sticky = 0;
+          c->err.clear();
+          k_clear_abort<<<1, 1, 0, c->stream>>>(B.st);
+          s = layout_from_counts(c);
+          if (s) return s;
+          launch_verlet(c->P, B, c->n, c->stream);
+          s = sync_check(c, "pm_dem_run (rebuild retry)");
+          if (s) return s;
+          if ((s = dem_alloc(c, false))) return s;
+          launch_dem_remap(B, c->n, c->stream);
+        }
+        if (s) return s;
+      }
+      launch_dem_step(c->P, B, c->n, dt, c->stream);
+      k_apply_pending<<<1, 1, 0, c->stream>>>(B.st);
+    }
   }
   s = read_state(c);
   if (s) return s;
@@ -1008,7 +1098,7 @@ pm_status pm_get_dem(pm_ctx c, float *omega4, float *torque4) {
   const int64_t n = c->n;
   if (n == 0) return PM_OK;
   if (omega4)
-    CUDA_TRY(c, cudaMemcpyAsync(omega4, c->B.omega[c->st_h->cur_id], 16 * n,
+    CUDA_TRY(c, cudaMemcpyAsync(omega4, c->B.omega[c->st_h->cur_pv], 16 * n,
                                 cudaMemcpyDeviceToHost, c->stream));
   if (torque4)
     CUDA_TRY(c, cudaMemcpyAsync(torque4, c->B.torque, 16 * n, cudaMemcpyDeviceToHost, c->stream));

@@ -325,9 +325,10 @@ void launch_ke(const Params &P, const Bufs &B, int64_t n, cudaStream_t s);
 void launch_sph_density(const Params &P, const Bufs &B, int64_t n, cudaStream_t s);
 void launch_sph_forces(const Params &P, const Bufs &B, int64_t n, cudaStream_t s);
 void launch_sph_init_run(const Bufs &B, int64_t n, cudaStream_t s);
-void launch_dem_forces(const Params &P, const Bufs &B, int64_t n, float dt, cudaStream_t s);
-void launch_dem_integrate(const Params &P, const Bufs &B, int64_t n, float dt, cudaStream_t s);
-void launch_dem_remap(const Bufs &B, int64_t n, int ci_old, cudaStream_t s);
+void launch_dem_step(const Params &P, const Bufs &B, int64_t n, float dt, cudaStream_t s);
+void launch_dem_remap(const Bufs &B, int64_t n, cudaStream_t s);
+void launch_dem_save(const Bufs &B, int64_t n, cudaStream_t s);
+void launch_dem_step_begin(const Bufs &B, cudaGraphConditionalHandle h, cudaStream_t s);
 void launch_sph_set_rho(const Params &P, const Bufs &B, int64_t n, const float *rho,
                         cudaStream_t s);
 void launch_sph_step(const Params &P, const Bufs &B, int64_t n, float cfl, int every,

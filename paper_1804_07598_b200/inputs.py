@@ -235,3 +235,35 @@ def random_box(n: int, L: float, key, periodic=(1, 1, 1)) -> System:
                   lo=np.zeros(3, np.float32), hi=np.full(3, np.float32(L)),
                   periodic=np.asarray(periodic, np.int32),
                   params=dict(epsilon=1.0, sigma=1.0, mass=1.0, r_cut=2.5, skin=0.3, dt=0.005))
+
+
+DEM_G = 9.81
+
+
+def dem_avalanche(nx=147, ny=105, nz=44, incline_deg=30.0, key=(71,), vjit=0.01) -> System:
+    """DEM avalanche down an inclined plane (PAPER.md:540-548 §4.5, Figs. 10-11;
+    reading R34 in DESIGN.md): grains of radius R = 0.06 on a Cartesian
+    lattice of spacing a = 2R (1 + 1e-3) (no initial overlap) filling
+    [0, nx a) x [0, ny a) x [0, nz a); the default 147 x 105 x 44 = 679,140
+    grains stand in for the paper's 677,310 with the aspect of its
+    4.26 x 3.06 x 1.26 start box.  The domain stretches that box by the
+    paper's 8.4/4.26 in x and 3.18/1.26 in z; walls at both x faces and the
+    floor, free +z, periodic y (length ny a); gravity rotated by the
+    incline about y.  Velocities U(-vjit, vjit) break the lattice symmetry.
+    params: the Silbert constants of P:540 (k_n, k_t read x1000, R34) and
+    mu = 0.5, gamma_t = 0 (R31-R32), dt = 2e-4, skin = 0.02."""
+    R = 0.06
+    a = 2.0 * R * (1.0 + 1e-3)
+    g = np.stack(np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij"), -1)
+    xyz = (g.reshape(-1, 3).astype(np.float64) + 0.5) * a
+    n = xyz.shape[0]
+    vel = np.zeros((n, 4), np.float32)
+    vel[:, :3] = rng(*key).uniform(-vjit, vjit, (n, 3)).astype(np.float32)
+    lo = np.zeros(3, np.float32)
+    hi = np.array([nx * a * 8.4 / 4.26, ny * a, nz * a * 3.18 / 1.26], np.float32)
+    th = np.deg2rad(incline_deg)
+    params = dict(R=R, m=1.0, I=1.44e-3, kn=7849.0, kt=2243.0, gn=3.401, gt=0.0, mu=0.5,
+                  g=(DEM_G * np.sin(th), 0.0, -DEM_G * np.cos(th)), walls=(1, 1, 0, 0, 1, 0),
+                  dt=2e-4, skin=0.02)
+    return System(pos=_as_pos4(xyz), vel=vel, gid=np.arange(n, dtype=np.int64), lo=lo, hi=hi,
+                  periodic=np.array([0, 1, 0], np.int32), params=params)

@@ -49,10 +49,15 @@ def idx_of_gid(s):
 
 
 # ---------------------------------------------------------------- cells
-@pytest.mark.parametrize("name", ["cfg1_shuffled", "cfg2", "faces_bigcell"])
+@pytest.mark.parametrize("name", ["cfg1_shuffled", "cfg2", "faces_bigcell", "sparse_thin"])
 def test_cells_bit_exact(pm, orc, name):
     if name == "cfg1_shuffled":
         s = inputs.shuffled(inputs.cfg1(), (11,))
+    elif name == "sparse_thin":  # < 4 particles per cell: lane-per-cell sort (k_segsort_thin)
+        s = inputs.random_box(6000, 40.0, (17,))
+        r = np.random.default_rng(5)  # a few crowded cells take the warp path inside it
+        pts = r.uniform(10.0, 12.7, (60, 3)).astype(np.float32)
+        s.pos[:60, :3] = pts
     elif name == "cfg2":
         s = inputs.cfg2()
     else:
@@ -456,6 +461,18 @@ def test_error_paths(pm):
         c.build_verlet()
     assert e.value.code == -7
     c.close()
+    # coincident pair in a sparse grid (lane-per-cell sort) and in a crowded
+    # cell of it (the warp path inside the same kernel)
+    for k0, k1, crowd in ((0, 1, 0), (2, 3, 20)):
+        s4 = inputs.random_box(3000, 40.0, (18,))
+        if crowd:
+            s4.pos[:crowd, :3] = np.random.default_rng(9).uniform(20.0, 22.7, (crowd, 3))
+        s4.pos[k1, :3] = s4.pos[k0, :3]
+        c = make_ctx(pm, s4)
+        with pytest.raises(pm.PMError) as e:
+            c.build_verlet()
+        assert e.value.code == -7
+        c.close()
     # outside a non-periodic axis
     s3 = s.subset(np.arange(s.n))
     s3.periodic = np.array([1, 1, 0], np.int32)
@@ -589,3 +606,87 @@ def test_dem_parity_granular_packing(pm, orc):
             assert reb2 > reb
             assert np.max(np.abs(x2 - x)) / P["R"] < tx
             assert np.max(np.abs(w2 - w)) / np.max(np.abs(wr)) < tw
+
+
+def _dem_ctx(pm, s):
+    p = s.params
+    c = pm.Context()
+    c.set_domain(s.lo, s.hi, s.periodic)
+    c.set_cutoff(2.0 * p["R"], p["skin"])
+    c.set_dem(p)
+    c.place(s.pos, s.vel, s.gid)
+    return c
+
+
+def test_dem_avalanche_small_parity(pm, orc):
+    """The avalanche recipe (inputs.dem_avalanche, reading R34)
+    at 12 x 8 x 6 grains: tilted gravity, x walls and floor, periodic y;
+    300 steps from the lattice (the column compresses and starts to slide)
+    against the fp64 oracle."""
+    s = inputs.dem_avalanche(12, 8, 6)
+    p = s.params
+    c = _dem_ctx(pm, s)
+    c.dem_run(p["dt"], 300)
+    st = c.get_state()
+    w = c.get_dem()["omega"]
+    o = np.argsort(st["gid"])
+    c.close()
+    xr, vr, wr, nh = orc.dem_run(s.pos, s.vel, np.zeros_like(s.pos), s.gid, s.lo, s.hi,
+                                 s.periodic, p["walls"], p, p["dt"], 300)
+    assert nh > s.n  # a dense contact network formed
+    assert np.max(np.abs(st["pos"][o, :3] - xr)) / p["R"] < 1e-3
+    assert np.max(np.abs(st["vel"][o, :3] - vr)) / np.max(np.abs(vr)) < 2e-3
+    assert np.max(np.abs(w[o, :3] - wr)) / np.max(np.abs(wr)) < 2e-2
+
+
+def test_dem_avalanche_full_size_momentum(pm):
+    """Full size (679,140 grains, the bench's DEM workload): the ordered-pair
+    forces are exact negatives of each other (exactly negated r_pq, n, v_pq
+    and histories) and walls push only along x and z, so the y momentum
+    changes by accumulation rounding only; every grain stays inside."""
+    s = inputs.dem_avalanche()
+    p = s.params
+    c = _dem_ctx(pm, s)
+    py0 = s.vel[:, 1].astype(np.float64).sum()
+    reb = c.dem_run(p["dt"], 400)
+    st = c.get_state()
+    c.close()
+    assert st["gid"].shape[0] == s.n and np.array_equal(np.sort(st["gid"]), s.gid)
+    py1 = st["vel"][:, 1].astype(np.float64).sum()
+    impulse = s.n * 9.81 * p["dt"] * 400  # |g| t N m: the scale of the x/z momentum change
+    assert abs(py1 - py0) < 1e-6 * impulse, (py0, py1)
+    assert np.all(st["pos"][:, :3] >= s.lo) and np.all(st["pos"][:, :3] < s.hi)
+    assert reb >= 0
+
+
+def test_dem_graph_matches_host_loop_with_resume(pm):
+    """pm_dem_run's CUDA graph (conditional rebuild node, no host round trip
+    per step) gives bit-identical trajectories to the plain host loop (same
+    kernels, same order), including a resume after a neighbour-capacity
+    overflow inside the graph: the initial rows of the lattice avalanche fit
+    8 slots (bulk rows 6), the collapsing packing needs more."""
+    s = inputs.dem_avalanche(12, 8, 10)
+    p = s.params
+
+    def run(graphs):
+        c = pm.Context(nbr_cap=8, use_graphs=graphs)
+        c.set_domain(s.lo, s.hi, s.periodic)
+        c.set_cutoff(2.0 * p["R"], p["skin"])
+        c.set_dem(p)
+        c.place(s.pos, s.vel, s.gid)
+        c.build_verlet()
+        rp0, _ = c.get_verlet()
+        reb = c.dem_run(p["dt"], 1500)
+        st = c.get_state()
+        w = c.get_dem()["omega"]
+        rp1, _ = c.get_verlet()
+        c.close()
+        return st, w, reb, np.diff(rp0).max(), np.diff(rp1).max()
+
+    a = run(True)
+    b = run(False)
+    assert a[3] <= 8 and a[4] > 8  # the list outgrew the first layout inside the graph
+    assert a[2] == b[2] and a[2] > 0
+    for k in ("pos", "vel", "gid"):
+        assert np.array_equal(a[0][k], b[0][k]), k
+    assert np.array_equal(a[1], b[1])
