@@ -270,11 +270,12 @@ pm_status pm_get_profile(pm_ctx ctx, double *force_ms, int64_t *force_launches,
  * copies): pair distances use the global-box rule R4, so a pair's d2 is the
  * same whether the partner is a ghost or a local periodic image.
  * ---------------------------------------------------------------------- */
-enum { PM_MSG_MIGRATE = 0, PM_MSG_GHOST = 1, PM_MSG_REFRESH = 2 };
+enum { PM_MSG_MIGRATE = 0, PM_MSG_GHOST = 1, PM_MSG_REFRESH = 2, PM_MSG_REFRESH_PV = 3 };
 enum { PM_PHASE_PROLOGUE = 0, PM_PHASE_STEP = 1, PM_PHASE_FINAL = 2, PM_PHASE_FORCES = 3 };
 
-/* Bytes per message record: migrate 48 (pos, vel, gid, kind), ghost 32
- * (pos, gid, kind), refresh 16 (pos).  Returns -1 for an unknown kind. */
+/* Bytes per message record: migrate 64 (pos, vel, SPH previous-step
+ * velocity, gid, kind), ghost 32 (pos, gid, kind), refresh 16 (pos), refresh
+ * with velocities 32 (pos, vel; SPH runs).  Returns -1 for an unknown kind. */
 int32_t pm_record_bytes(int32_t what);
 
 /* This context owns cuboid pcoord of a pgrid[0] x pgrid[1] x pgrid[2]
@@ -330,6 +331,29 @@ pm_status pm_dist_refresh_unpack(pm_ctx ctx, const void *recv_dev);
  * (nullable): synchronise and return (and clear) the local flag "some owned
  * particle moved more than skin/2 since the last build". */
 pm_status pm_dist_step(pm_ctx ctx, float dt, int32_t phase, int32_t *need_rebuild);
+
+/* Decomposed WCSPH time stepping (SURVEY §8(f) NEXT-3 "multi-GPU SPH ghosts
+ * (vel/rho/P)"; PAPER.md:335 Eq. 2, :358 Verlet scheme with dynamic step
+ * size; the per-step operations of pm_sph_run, readings R26-R28).  Per step
+ * every rank calls
+ *   pm_dist_sph_rates  -> its local step bound (synchronises);
+ *   the caller reduces the bounds to their global minimum over all ranks;
+ *   pm_dist_sph_update(bound) -> dt = cfl * bound, Verlet / Euler update of
+ *                        the owned particles; need_rebuild as pm_dist_step;
+ *   a rebuild (MIGRATE, GHOST rounds + pm_dist_finish) when any rank asks;
+ *   the ghost refresh with velocities (pm_dist_refresh_pv_*: 32 B per ghost,
+ *   position and velocity whose w lanes carry P and rho).
+ * pm_dist_sph_init (after pm_set_sph and the initial densities, pm_set_rho,
+ * before the first rebuild) packs rho and P into the velocity and position w
+ * lanes and starts the Verlet state; migration records carry it.  Ghost
+ * copies have no row, no rate and no step bound.  Decomposed axes must be
+ * periodic (pm_set_decomposition). */
+pm_status pm_dist_sph_init(pm_ctx ctx);
+pm_status pm_dist_sph_rates(pm_ctx ctx, float *bound);
+pm_status pm_dist_sph_update(pm_ctx ctx, float bound, float cfl, int32_t every,
+                             int32_t *need_rebuild);
+pm_status pm_dist_refresh_pv_pack(pm_ctx ctx, void *send_dev);
+pm_status pm_dist_refresh_pv_unpack(pm_ctx ctx, const void *recv_dev);
 
 #ifdef __cplusplus
 }

@@ -349,7 +349,6 @@ __global__ void __launch_bounds__(256) k_reorder(Bufs B, int64_t n, int sph_stat
   if (sph_state) {  // SPH time stepping state travels with the particles
     B.rhoP[ci ^ 1][k] = B.rhoP[ci][j];
     B.vold[ci ^ 1][k] = B.vold[ci][j];
-    B.rold[ci ^ 1][k] = B.rold[ci][j];
   }
   if (dem_state) B.omega[cp ^ 1][k] = B.omega[cp][j];  // double-buffered per step
 }

@@ -189,9 +189,10 @@ __global__ void __launch_bounds__(kDirBlock) k_dist_fill(const uint32_t *__restr
   }
 }
 
-// migration record: pos, vel, gid, kind (48 B); ghost record: pos, gid, kind (32 B)
+// migration record: pos, vel, vold, gid, kind (64 B; vold is the SPH stepping
+// state, zero when none is allocated); ghost record: pos, gid, kind (32 B)
 struct MigRec {
-  float4 pos, vel;
+  float4 pos, vel, vold;
   long long gid;
   int kind, pad;
 };
@@ -212,6 +213,7 @@ __global__ void k_dist_pack(Bufs B, int what, const int *__restrict__ list, int 
     MigRec r;
     r.pos = B.pos[cp][i];
     r.vel = B.vel[cp][i];
+    r.vold = B.vold[ci] ? B.vold[ci][i] : make_float4(0.f, 0.f, 0.f, 0.f);
     r.gid = B.gid[ci][i];
     r.kind = B.kind[ci][i];
     r.pad = 0;
@@ -237,6 +239,8 @@ __global__ void k_dist_compact(Bufs B, const int *__restrict__ stay, int n_stay)
   B.vel[cp ^ 1][k] = B.vel[cp][j];
   B.gid[ci ^ 1][k] = B.gid[ci][j];
   B.kind[ci ^ 1][k] = B.kind[ci][j];
+  B.rhoP[ci ^ 1][k] = B.rhoP[ci][j];
+  if (B.vold[ci]) B.vold[ci ^ 1][k] = B.vold[ci][j];
 }
 
 __global__ void k_dist_unpack(Bufs B, int what, const void *__restrict__ in, int nrecv, int base) {
@@ -251,6 +255,8 @@ __global__ void k_dist_unpack(Bufs B, int what, const void *__restrict__ in, int
     B.vel[cp][k] = r.vel;
     B.gid[ci][k] = r.gid;
     B.kind[ci][k] = r.kind;
+    B.rhoP[ci][k] = make_float2(r.vel.w, r.pos.w);  // an SPH run packs rho, P there
+    if (B.vold[ci]) B.vold[ci][k] = r.vold;
   } else {
     const GhostRec r = reinterpret_cast<const GhostRec *>(in)[e];
     B.pos[cp][k] = r.pos;
@@ -280,12 +286,35 @@ __global__ void k_refresh_unpack(Bufs B, const int *__restrict__ ghost_slot, int
   if (e < nghost) B.pos[B.st->cur_pv][ghost_slot[e]] = in[e];
 }
 
+// SPH runs (NEXT-3): positions and velocities, with P and rho in their w
+// lanes -- everything the stepping sweep reads of a partner (32 B per ghost)
+__global__ void k_refresh_pack_pv(Bufs B, const int *__restrict__ send_idx, int nsend,
+                                  float4 *__restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < nsend) {
+    const int cp = B.st->cur_pv, i = send_idx[e];
+    out[2 * e] = B.pos[cp][i];
+    out[2 * e + 1] = B.vel[cp][i];
+  }
+}
+
+__global__ void k_refresh_unpack_pv(Bufs B, const int *__restrict__ ghost_slot, int nghost,
+                                    const float4 *__restrict__ in) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < nghost) {
+    const int cp = B.st->cur_pv, k = ghost_slot[e];
+    B.pos[cp][k] = in[2 * e];
+    B.vel[cp][k] = in[2 * e + 1];
+  }
+}
+
 inline unsigned nb(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
 
 int dist_record_bytes(int what) {
-  return what == 0 ? (int)sizeof(MigRec) : what == 1 ? (int)sizeof(GhostRec) : 16;
+  return what == 0 ? (int)sizeof(MigRec) : what == 1 ? (int)sizeof(GhostRec)
+                                                     : what == 2 ? 16 : what == 3 ? 32 : -1;
 }
 
 void launch_dist_plan(const Params &P, const Bufs &B, const Dist &D, int n_owned, int what,
@@ -323,6 +352,15 @@ void launch_refresh_pack(const Bufs &B, const int *send_idx, int nsend, void *ou
                          cudaStream_t s) {
   if (nsend > 0)
     k_refresh_pack<<<nb(nsend), 256, 0, s>>>(B, send_idx, nsend, reinterpret_cast<float4 *>(out));
+}
+
+void launch_refresh_pv(const Bufs &B, int pack, const int *idx, int m, void *buf,
+                       cudaStream_t s) {
+  if (m <= 0) return;
+  if (pack)
+    k_refresh_pack_pv<<<nb(m), 256, 0, s>>>(B, idx, m, reinterpret_cast<float4 *>(buf));
+  else
+    k_refresh_unpack_pv<<<nb(m), 256, 0, s>>>(B, idx, m, reinterpret_cast<const float4 *>(buf));
 }
 
 void launch_refresh_unpack(const Bufs &B, const int *ghost_slot, int nghost, const void *in,

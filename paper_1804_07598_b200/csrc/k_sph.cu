@@ -186,8 +186,11 @@ __global__ void __launch_bounds__(256, 3) k_sph_forces(Params P, Bufs B, int n) 
 //   k_sph_dt    : dt = cfl * min(bounds); Euler step on the first and every
 //                 `every`-th step, else leapfrog Verlet;
 //   k_sph_verlet: rho' (all), v', x' (fluid), P' = EOS(rho'), rebuild test.
-// fp32 like the sweeps; the previous-step state (vold, rold) and rhoP travel
-// with the particles through the cell-sort reorder (Params::sph_state).
+// fp32 like the sweeps.  During a run the density and pressure ride in
+// vel.w and pos.w (what the sweep gathers) and the previous-step velocity and
+// density in vold (w = density); vold and rhoP (the getters' copy) travel with
+// the particles through the cell-sort reorder (Params::sph_state) and the
+// multi-GPU migration records; ghosts receive pos and vel each step.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void warp_min_atomic(unsigned *dst, float v) {
   unsigned u = __float_as_uint(v);  // v >= 0: uint order = float order
@@ -199,8 +202,9 @@ __device__ __forceinline__ void warp_min_atomic(unsigned *dst, float v) {
 __global__ void __launch_bounds__(256, 3) k_sph_rates(Params P, Bufs B, int n) {
   State *st = B.st;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = i < n;
   const int cp = st->cur_pv, ci = st->cur_id;
+  // ghost copies of a decomposed context: no row, no rate, no step bound
+  const bool active = i < n && !(P.dist && (B.kind[ci][i] & kGhostBit));
   // pos.w = P and vel.w = rho during a run (k_sph_init_run, k_sph_verlet):
   // two 16-byte gathers per pair instead of three.
   const float4 *__restrict__ pos = B.pos[cp];
@@ -285,6 +289,13 @@ __global__ void k_sph_dt(State *st, float cfl, int every) {
   }
 }
 
+// decomposed runs: the global minimum of the ranks' step bounds replaces the
+// local one before k_sph_dt
+__global__ void k_sph_set_bound(State *st, float bound) {
+  st->dtf_bits = __float_as_uint(bound);
+  st->dtcv_bits = 0x7f800000u;
+}
+
 __device__ __forceinline__ float tait(const Params &P, float rho) {
   const float x = rho * P.sph.inv_rho0;
   float xg;
@@ -303,44 +314,48 @@ __global__ void __launch_bounds__(256) k_sph_verlet(Params P, Bufs B, int n) {
   const int cp = st->cur_pv, ci = st->cur_id;
   bool far = false;
   if (i < n) {
-    const float dt = st->sph_dt;
-    const bool euler = st->mode == 1;
-    const float D = B.drho[i];
-    const float rho = B.rhoP[ci][i].x, rold = B.rold[ci][i];
-    const float rn = euler ? fmaf(dt, D, rho) : fmaf(2.0f * dt, D, rold);
-    const float pn = tait(P, rn);
-    B.rold[ci][i] = rho;
-    B.rhoP[ci][i] = make_float2(rn, pn);
     const float4 x = B.pos[cp][i];
     const float4 v = B.vel[cp][i];
-    float4 xn = x, vn = v;
-    if (!(B.kind[ci][i] & 1)) {
-      const float4 a = B.force[i];
+    if (P.dist && (B.kind[ci][i] & kGhostBit)) {  // ghost copy: refreshed by its owner
+      B.pos[cp ^ 1][i] = x;
+      B.vel[cp ^ 1][i] = v;
+    } else {
+      const float dt = st->sph_dt;
+      const bool euler = st->mode == 1;
+      const float D = B.drho[i];
       const float4 vo = B.vold[ci][i];
-      const float h2 = 0.5f * dt * dt;
-      vn.x = euler ? fmaf(dt, a.x, v.x) : fmaf(2.0f * dt, a.x, vo.x);
-      vn.y = euler ? fmaf(dt, a.y, v.y) : fmaf(2.0f * dt, a.y, vo.y);
-      vn.z = euler ? fmaf(dt, a.z, v.z) : fmaf(2.0f * dt, a.z, vo.z);
-      float r3[3] = {fmaf(h2, a.x, fmaf(dt, v.x, x.x)), fmaf(h2, a.y, fmaf(dt, v.y, x.y)),
-                     fmaf(h2, a.z, fmaf(dt, v.z, x.z))};
+      const float rho = v.w, rold = vo.w;
+      const float rn = euler ? fmaf(dt, D, rho) : fmaf(2.0f * dt, D, rold);
+      const float pn = tait(P, rn);
+      B.rhoP[ci][i] = make_float2(rn, pn);
+      float4 xn = x, vn = v;
+      if (!(B.kind[ci][i] & 1)) {
+        const float4 a = B.force[i];
+        const float h2 = 0.5f * dt * dt;
+        vn.x = euler ? fmaf(dt, a.x, v.x) : fmaf(2.0f * dt, a.x, vo.x);
+        vn.y = euler ? fmaf(dt, a.y, v.y) : fmaf(2.0f * dt, a.y, vo.y);
+        vn.z = euler ? fmaf(dt, a.z, v.z) : fmaf(2.0f * dt, a.z, vo.z);
+        float r3[3] = {fmaf(h2, a.x, fmaf(dt, v.x, x.x)), fmaf(h2, a.y, fmaf(dt, v.y, x.y)),
+                       fmaf(h2, a.z, fmaf(dt, v.z, x.z))};
 #pragma unroll
-      for (int d = 0; d < 3; ++d)
-        if (P.box.per[d]) r3[d] = wrap1(r3[d], P.box.lo[d], P.box.hi[d], P.box.L[d]);
-      xn = make_float4(r3[0], r3[1], r3[2], 0.f);
-      const float4 xr = B.xref[i];
-      const float dx = pair_delta1(xr.x, xn.x, P.box.L[0], P.box.halfL[0], P.box.per[0]);
-      const float dy = pair_delta1(xr.y, xn.y, P.box.L[1], P.box.halfL[1], P.box.per[1]);
-      const float dz = pair_delta1(xr.z, xn.z, P.box.L[2], P.box.halfL[2], P.box.per[2]);
-      far = dist2(dx, dy, dz) > P.half_skin2;
-      if (!P.box.per[0] && (xn.x < P.box.lo[0] || xn.x >= P.box.hi[0])) far = true;
-      if (!P.box.per[1] && (xn.y < P.box.lo[1] || xn.y >= P.box.hi[1])) far = true;
-      if (!P.box.per[2] && (xn.z < P.box.lo[2] || xn.z >= P.box.hi[2])) far = true;
+        for (int d = 0; d < 3; ++d)
+          if (P.box.per[d]) r3[d] = wrap1(r3[d], P.box.lo[d], P.box.hi[d], P.box.L[d]);
+        xn = make_float4(r3[0], r3[1], r3[2], 0.f);
+        const float4 xr = B.xref[i];
+        const float dx = pair_delta1(xr.x, xn.x, P.box.L[0], P.box.halfL[0], P.box.per[0]);
+        const float dy = pair_delta1(xr.y, xn.y, P.box.L[1], P.box.halfL[1], P.box.per[1]);
+        const float dz = pair_delta1(xr.z, xn.z, P.box.L[2], P.box.halfL[2], P.box.per[2]);
+        far = dist2(dx, dy, dz) > P.half_skin2;
+        if (!P.box.per[0] && (xn.x < P.box.lo[0] || xn.x >= P.box.hi[0])) far = true;
+        if (!P.box.per[1] && (xn.y < P.box.lo[1] || xn.y >= P.box.hi[1])) far = true;
+        if (!P.box.per[2] && (xn.z < P.box.lo[2] || xn.z >= P.box.hi[2])) far = true;
+      }
+      B.vold[ci][i] = v;  // w = rho: the previous-step density of the next step
+      xn.w = pn;          // the packed P and rho k_sph_rates gathers
+      vn.w = rn;
+      B.pos[cp ^ 1][i] = xn;
+      B.vel[cp ^ 1][i] = vn;
     }
-    B.vold[ci][i] = v;
-    xn.w = pn;  // the packed P and rho k_sph_rates gathers
-    vn.w = rn;
-    B.pos[cp ^ 1][i] = xn;
-    B.vel[cp ^ 1][i] = vn;
   }
   if (__any_sync(0xffffffffu, far) && (threadIdx.x & 31) == 0) st->need_rebuild = 1;
   if (blockIdx.x == 0 && threadIdx.x == 0) st->pending_flip = 1;
@@ -357,10 +372,9 @@ __global__ void __launch_bounds__(256) k_sph_init_run(Bufs B, int n) {
   const int ci = st->cur_id;
   if (i < n) {
     const float2 rp = B.rhoP[ci][i];
-    B.rold[ci][i] = rp.x;
     B.pos[st->cur_pv][i].w = rp.y;  // packed for k_sph_rates
     B.vel[st->cur_pv][i].w = rp.x;
-    B.vold[ci][i] = B.vel[st->cur_pv][i];
+    B.vold[ci][i] = B.vel[st->cur_pv][i];  // w = rho: the previous-step density
   }
   if (i == 0) {
     st->sph_step = 0;
@@ -392,6 +406,19 @@ void launch_sph_set_rho(const Params &P, const Bufs &B, int64_t n, const float *
 
 void launch_sph_init_run(const Bufs &B, int64_t n, cudaStream_t s) {
   k_sph_init_run<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(B, (int)n);
+}
+
+void launch_sph_rates(const Params &P, const Bufs &B, int64_t n, cudaStream_t s) {
+  if (n > 0) k_sph_rates<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, B, (int)n);
+}
+
+// dt from `bound` (the global minimum) -> integrate (the caller applies the flip)
+void launch_sph_update(const Params &P, const Bufs &B, int64_t n, float bound, float cfl,
+                       int every, cudaStream_t s) {
+  if (n <= 0) return;
+  k_sph_set_bound<<<1, 1, 0, s>>>(B.st, bound);
+  k_sph_dt<<<1, 1, 0, s>>>(B.st, cfl, every);
+  k_sph_verlet<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, B, (int)n);
 }
 
 // rates -> dt -> integrate (the caller applies the buffer flip)

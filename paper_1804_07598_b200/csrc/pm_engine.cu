@@ -248,14 +248,9 @@ pm_status ensure_particles(pm_ctx c, int64_t n, int64_t keep = 0) {
   CUDA_TRY(c, dalloc(&B.force, cap));
   CUDA_TRY(c, dalloc(&B.rhoP[0], cap));
   CUDA_TRY(c, dalloc(&B.rhoP[1], cap));
-  for (int b = 0; b < 2; ++b) {  // SPH stepping state: allocated by pm_sph_run
-    if (B.vold[b]) cudaFree(B.vold[b]);
-    if (B.rold[b]) cudaFree(B.rold[b]);
-    B.vold[b] = nullptr;
-    B.rold[b] = nullptr;
-  }
-  if (B.drho) cudaFree(B.drho);
-  B.drho = nullptr;
+  for (int b = 0; b < 2; ++b)  // SPH stepping state (allocated by the first SPH run)
+    if (B.vold[b]) CUDA_TRY(c, grow_keep(&B.vold[b], cap, keep, c->stream));
+  if (B.drho) CUDA_TRY(c, dalloc(&B.drho, cap));
   CUDA_TRY(c, dalloc(&B.cell_of, cap));
   CUDA_TRY(c, dalloc(&B.slot, cap));
   CUDA_TRY(c, dalloc(&B.perm, cap));
@@ -670,8 +665,7 @@ void pm_destroy(pm_ctx c) {
     cudaFree(B.gid[b]);
     cudaFree(B.kind[b]);
   }
-  void *ptrs[] = {B.xref, B.force, B.rhoP[0], B.rhoP[1], B.vold[0], B.vold[1], B.rold[0],
-                  B.rold[1], B.drho, B.cell_of, B.slot, B.count, B.start, B.perm,
+  void *ptrs[] = {B.xref, B.force, B.rhoP[0], B.rhoP[1], B.vold[0], B.vold[1], B.drho, B.cell_of, B.slot, B.count, B.start, B.perm,
                   B.sorttmp, B.scan_tmp, B.nbr, B.cnt, B.st, B.slice_off, B.big_cells};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -1129,6 +1123,29 @@ pm_status pm_set_rho(pm_ctx c, const float *rho, int32_t mem) {
   return PM_OK;
 }
 
+static float bits_to_float(unsigned u) {
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+// The SPH stepping state (previous-step velocity/density, density rate);
+// from now on the cell-sort reorder carries it with the particles.
+static pm_status sph_step_alloc(pm_ctx c) {
+  Bufs &B = c->B;
+  for (int b = 0; b < 2; ++b)
+    if (!B.vold[b]) {
+      CUDA_TRY(c, dalloc(&B.vold[b], c->pcap));
+      CUDA_TRY(c, cudaMemsetAsync(B.vold[b], 0, 16 * c->pcap, c->stream));
+    }
+  if (!B.drho) CUDA_TRY(c, dalloc(&B.drho, c->pcap));
+  if (!c->P.sph_state) {
+    c->P.sph_state = 1;
+    destroy_graph(c);
+  }
+  return PM_OK;
+}
+
 pm_status pm_sph_run(pm_ctx c, int64_t nsteps, float cfl, int32_t every,
                      pm_sph_run_stats *out) {
   pm_status s = check_ready(c);
@@ -1143,11 +1160,7 @@ pm_status pm_sph_run(pm_ctx c, int64_t nsteps, float cfl, int32_t every,
   cudaSetDevice(c->device);
   if (nsteps == 0) return PM_OK;
   Bufs &B = c->B;
-  for (int b = 0; b < 2; ++b) {
-    if (!B.vold[b]) CUDA_TRY(c, dalloc(&B.vold[b], c->pcap));
-    if (!B.rold[b]) CUDA_TRY(c, dalloc(&B.rold[b], c->pcap));
-  }
-  if (!B.drho) CUDA_TRY(c, dalloc(&B.drho, c->pcap));
+  if ((s = sph_step_alloc(c))) return s;
   if (!c->P.sph_state) {  // the cell-sort reorder now carries the stepping state
     c->P.sph_state = 1;
     destroy_graph(c);
@@ -1407,7 +1420,7 @@ pm_status pm_get_profile(pm_ctx c, double *force_ms, int64_t *force_launches, do
 
 
 int32_t pm_record_bytes(int32_t what) {
-  return (what >= 0 && what <= 2) ? dist_record_bytes(what) : -1;
+  return (what >= 0 && what <= 3) ? dist_record_bytes(what) : -1;
 }
 
 pm_status pm_set_decomposition(pm_ctx c, const int32_t pgrid[3], const int32_t pcoord[3]) {
@@ -1637,6 +1650,68 @@ pm_status pm_dist_step(pm_ctx c, float dt, int32_t phase, int32_t *need_rebuild)
     k_clear_rebuild<<<1, 1, 0, c->stream>>>(c->B.st);
   }
   return check_launch(c, "pm_dist_step");
+}
+
+pm_status pm_dist_refresh_pv_pack(pm_ctx c, void *send_dev) {
+  if (!c) return PM_E_INVAL;
+  if (c->sticky) return c->sticky;
+  if (c->n_send > 0 && !send_dev) return set_err(c, PM_E_INVAL, "null buffer");
+  launch_refresh_pv(c->B, 1, c->d_send_idx, (int)c->n_send, send_dev, c->stream);
+  return check_launch(c, "pm_dist_refresh_pv_pack");
+}
+
+pm_status pm_dist_refresh_pv_unpack(pm_ctx c, const void *recv_dev) {
+  if (!c) return PM_E_INVAL;
+  if (c->sticky) return c->sticky;
+  if (c->n_ghost > 0 && !recv_dev) return set_err(c, PM_E_INVAL, "null buffer");
+  launch_refresh_pv(c->B, 0, c->d_gslot, (int)c->n_ghost, const_cast<void *>(recv_dev),
+                    c->stream);
+  return check_launch(c, "pm_dist_refresh_pv_unpack");
+}
+
+pm_status pm_dist_sph_init(pm_ctx c) {
+  pm_status s = check_ready(c);
+  if (s) return s;
+  if (!c->have_sph) return set_err(c, PM_E_STATE, "pm_set_sph not called");
+  if (!c->dist) return set_err(c, PM_E_STATE, "pm_dist_sph_init: decomposed contexts only");
+  cudaSetDevice(c->device);
+  if ((s = sph_step_alloc(c))) return s;
+  launch_sph_init_run(c->B, c->n, c->stream);
+  return check_launch(c, "pm_dist_sph_init");
+}
+
+pm_status pm_dist_sph_rates(pm_ctx c, float *bound) {
+  pm_status s = check_ready(c);
+  if (s) return s;
+  if (!bound) return set_err(c, PM_E_INVAL, "pm_dist_sph_rates: null bound");
+  if (!c->dist || !c->P.sph_state)
+    return set_err(c, PM_E_STATE, "pm_dist_sph_rates: call pm_dist_sph_init first");
+  if (!c->list_valid) return set_err(c, PM_E_STATE, "pm_dist_sph_rates: no Verlet list");
+  cudaSetDevice(c->device);
+  launch_sph_rates(c->P, c->B, c->n, c->stream);
+  if ((s = sync_check(c, "pm_dist_sph_rates"))) return s;
+  *bound = std::min(bits_to_float(c->st_h->dtf_bits), bits_to_float(c->st_h->dtcv_bits));
+  return PM_OK;
+}
+
+pm_status pm_dist_sph_update(pm_ctx c, float bound, float cfl, int32_t every,
+                             int32_t *need_rebuild) {
+  pm_status s = check_ready(c);
+  if (s) return s;
+  if (!c->dist || !c->P.sph_state)
+    return set_err(c, PM_E_STATE, "pm_dist_sph_update: call pm_dist_sph_init first");
+  if (!(cfl > 0.f) || every < 0 || !(bound > 0.f))
+    return set_err(c, PM_E_INVAL, "pm_dist_sph_update: cfl and bound must be > 0, every >= 0");
+  cudaSetDevice(c->device);
+  launch_sph_update(c->P, c->B, c->n, bound, cfl, every, c->stream);
+  k_apply_pending<<<1, 1, 0, c->stream>>>(c->B.st);
+  c->forces_valid = false;
+  if (need_rebuild) {
+    if ((s = sync_check(c, "pm_dist_sph_update"))) return s;
+    *need_rebuild = c->st_h->need_rebuild;
+    k_clear_rebuild<<<1, 1, 0, c->stream>>>(c->B.st);
+  }
+  return check_launch(c, "pm_dist_sph_update");
 }
 
 }  // extern "C"

@@ -114,8 +114,8 @@ struct Bufs {
   float4 *force;       // forces / SPH accelerations (current order)
   float2 *rhoP[2];     // SPH density, pressure (by State::cur_id: the stepping
                        // reorder permutes them with the particles)
-  float4 *vold[2];     // SPH stepping: velocities of the previous step (Verlet)
-  float *rold[2];      // SPH stepping: densities of the previous step
+  float4 *vold[2];     // SPH stepping: velocities of the previous step (Verlet);
+                       // w = the density of the previous step
   float *drho;         // SPH stepping: density rate (Eq. 2), current order
   float4 *omega[2];    // DEM angular velocities (by State::cur_id)
   float4 *torque;      // DEM torques, current order
@@ -331,6 +331,9 @@ void launch_dem_save(const Bufs &B, int64_t n, cudaStream_t s);
 void launch_dem_step_begin(const Bufs &B, cudaGraphConditionalHandle h, cudaStream_t s);
 void launch_sph_set_rho(const Params &P, const Bufs &B, int64_t n, const float *rho,
                         cudaStream_t s);
+void launch_sph_rates(const Params &P, const Bufs &B, int64_t n, cudaStream_t s);
+void launch_sph_update(const Params &P, const Bufs &B, int64_t n, float bound, float cfl,
+                       int every, cudaStream_t s);
 void launch_sph_step(const Params &P, const Bufs &B, int64_t n, float cfl, int every,
                      cudaStream_t s);
 void launch_verlet_export(const Bufs &B, int64_t n, const int64_t *row_ptr, int64_t *col_gid,
@@ -350,6 +353,8 @@ void launch_dist_remap(const int *invperm, int *send_idx, int nsend, int *ghost_
                        int n_owned, cudaStream_t s);
 void launch_refresh_pack(const Bufs &B, const int *send_idx, int nsend, void *out,
                          cudaStream_t s);
+void launch_refresh_pv(const Bufs &B, int pack, const int *idx, int m, void *buf,
+                       cudaStream_t s);
 void launch_refresh_unpack(const Bufs &B, const int *ghost_slot, int nghost, const void *in,
                            cudaStream_t s);
 }  // namespace pm

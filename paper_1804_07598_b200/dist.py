@@ -160,6 +160,14 @@ class TorchTransport:
         self.dist.all_reduce(v)
         return v.cpu().numpy()
 
+    def allreduce_min_f32(self, x):
+        """Exact global minimum of one fp32 value (the SPH step bound)."""
+        t = self.torch
+        dev = self.device if self.device is not None else "cpu"
+        v = t.tensor([x], dtype=t.float32, device=dev)
+        self.dist.all_reduce(v, op=self.dist.ReduceOp.MIN)
+        return float(v.item())
+
 
 class LoopbackTransport:
     """All ranks live in this process (lock-step): a message from rank r to
@@ -244,6 +252,9 @@ class HybridTransport:
 
     def allreduce_max(self, x):
         return x if self.tr is None else self.tr.allreduce_max(x)
+
+    def allreduce_min_f32(self, x):
+        return x if self.tr is None else self.tr.allreduce_min_f32(x)
 
     def allreduce_sum(self, arr):
         return np.asarray(arr, np.float64) if self.tr is None else self.tr.allreduce_sum(arr)
@@ -364,29 +375,31 @@ class DistSim:
         with self._ctxmgr():
             self._refresh()
 
-    def _refresh(self):
-        """Positions-only ghost refresh with the last ghost plan's layout."""
+    def _refresh(self, pv=False):
+        """Ghost refresh with the last ghost plan's layout: positions only
+        (16 B per ghost), or positions and velocities (pv, 32 B: SPH runs)."""
+        rsz = 32 if pv else 16
         sends, recvs = {}, {}
         for r, ctx in self.m.items():
             nsend = sum(n for _, n in self.ghost_seg[r].values())
-            buf = self._buf(("rsend", r), nsend * 16)
-            ctx.refresh_pack(buf if nsend else None)
-            sends[r] = {p: buf[o * 16:(o + n) * 16] for p, (o, n) in self.ghost_seg[r].items()}
+            buf = self._buf(("rsend", r), nsend * rsz)
+            ctx.refresh_pack(buf if nsend else None, pv=pv)
+            sends[r] = {p: buf[o * rsz:(o + n) * rsz] for p, (o, n) in self.ghost_seg[r].items()}
         rb = {}
         for r in self.m:
             peers = self.D.peers(r)
             tot = sum(self.ghost_recv[r][p] for p in peers)
-            buf = self._buf(("rrecv", r), tot * 16)
+            buf = self._buf(("rrecv", r), tot * rsz)
             rb[r] = (buf, tot)
             off, recvs[r] = 0, {}
             for p in peers:
                 n = self.ghost_recv[r][p]
-                recvs[r][p] = buf[off * 16:(off + n) * 16]
+                recvs[r][p] = buf[off * rsz:(off + n) * rsz]
                 off += n
         self._exchange(sends, recvs)
         for r, ctx in self.m.items():
             buf, tot = rb[r]
-            ctx.refresh_unpack(buf if tot else None)
+            ctx.refresh_unpack(buf if tot else None, pv=pv)
 
     def start(self):
         """After pm_place on every member: first decomposition + forces."""
@@ -422,6 +435,37 @@ class DistSim:
             flag = 0 if last else self._allreduce_max(flags)
         return reb
 
+    def _allreduce_min(self, vals):
+        v = min(vals.values())
+        return v if self.loop else self.tr.allreduce_min_f32(v)
+
+    def sph_start(self):
+        """After pm_place, pm_set_sph and pm_set_rho on every member: start
+        the SPH Verlet state, first decomposition, ghosts with velocities."""
+        with self._ctxmgr():
+            for ctx in self.m.values():
+                ctx.dist_sph_init()
+            self._rebuild()
+            self._refresh(pv=True)
+
+    def sph_run(self, nsteps, cfl=0.2, every=40):
+        """nsteps decomposed WCSPH steps (pm.h
+        pm_dist_sph_*): local rates -> global min step bound -> update ->
+        rebuild when any rank asks -> ghost refresh with velocities.
+        Returns (rebuilds, simulated time)."""
+        with self._ctxmgr():
+            reb, t = 0, 0.0
+            for _ in range(nsteps):
+                bound = self._allreduce_min({r: ctx.dist_sph_rates() for r, ctx in self.m.items()})
+                t += cfl * bound
+                flag = self._allreduce_max({r: ctx.dist_sph_update(bound, cfl, every)
+                                            for r, ctx in self.m.items()})
+                if flag:
+                    self._rebuild()
+                    reb += 1
+                self._refresh(pv=True)
+            return reb, t
+
     def thermo(self):
         """Global KE, U_shift, npairs (sums over ranks)."""
         vals = np.zeros(3)
@@ -433,9 +477,11 @@ class DistSim:
         return dict(ke=vals[0], pe_shift=vals[1], npairs=vals[2])
 
 
-def make_member(system, decomp, rank, device=0, stream=None, rc=2.5, skin=0.3, r_min=0.0):
+def make_member(system, decomp, rank, device=0, stream=None, rc=2.5, skin=0.3, r_min=0.0,
+                sph=None):
     """A DistContext for `rank` of `decomp`, with the rank's particles of
-    `system` (an inputs.System) placed."""
+    `system` (an inputs.System) placed; `sph`: WCSPH parameters (pm_set_sph)
+    instead of the LJ ones."""
     from . import pm
     # `stream`: the torch.cuda.Stream the DistSim will run on (never the
     # legacy default stream, whose handle 0 would mean "library-owned stream")
@@ -443,7 +489,10 @@ def make_member(system, decomp, rank, device=0, stream=None, rc=2.5, skin=0.3, r
     ctx = pm.DistContext(device=device, stream=handle)
     ctx.set_domain(system.lo, system.hi, system.periodic)
     ctx.set_cutoff(rc, skin)
-    ctx.set_lj(1.0, 1.0, 1.0, r_min)
+    if sph is not None:
+        ctx.set_sph(sph)
+    else:
+        ctx.set_lj(1.0, 1.0, 1.0, r_min)
     if decomp.cuts is None:
         ctx.set_decomposition(decomp.grid, decomp.coord(rank))
     else:

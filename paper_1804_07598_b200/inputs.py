@@ -267,3 +267,31 @@ def dem_avalanche(nx=147, ny=105, nz=44, incline_deg=30.0, key=(71,), vjit=0.01)
                   dt=2e-4, skin=0.02)
     return System(pos=_as_pos4(xyz), vel=vel, gid=np.arange(n, dtype=np.int64), lo=lo, hi=hi,
                   periodic=np.array([0, 1, 0], np.int32), params=params)
+
+
+def sph_layer(dp=1.0 / 160.0, nx=24, ny=24, nz=8, layers=3, vel_key=(106,), vmax=0.1) -> System:
+    """A WCSPH fluid layer periodic in x and y (NEXT-3 multi-GPU stepping
+    cases: decomposed axes must be periodic): fluid lattice (i + 0.5) dp on
+    nx x ny x nz, `layers` fixed boundary layers below it, open top; the same
+    constants as cfg4 with h_swl = nz dp; fluid velocities U(-vmax, vmax) key
+    vel_key (0 if None)."""
+    ix, iy, iz = np.arange(nx), np.arange(ny), np.arange(-layers, nz)
+    IZ, IY, IX = np.meshgrid(iz, iy, ix, indexing="ij")
+    xyz = (np.stack([IX.ravel(), IY.ravel(), IZ.ravel()], axis=1).astype(np.float64) + 0.5) * dp
+    kind = (IZ.ravel() < 0).astype(np.int32)
+    n = xyz.shape[0]
+    vel = np.zeros((n, 4), np.float32)
+    if vel_key is not None:
+        v = rng(*vel_key).uniform(-vmax, vmax, size=(n, 3))
+        v[kind == 1] = 0.0
+        vel[:, :3] = v.astype(np.float32)
+    lo = np.array([0.0, 0.0, -layers * dp], np.float32)
+    hi = np.array([nx * dp, ny * dp, (nz + 6) * dp], np.float32)
+    h = 1.3 * dp
+    h_swl = nz * dp
+    c0 = SPH_COEF_SOUND * np.sqrt(SPH_G * h_swl)
+    params = dict(dp=dp, h=h, mass=SPH_RHO0 * dp ** 3, rho0=SPH_RHO0, gamma=SPH_GAMMA,
+                  c0=c0, b=c0 * c0 * SPH_RHO0 / SPH_GAMMA, g=(0.0, 0.0, -SPH_G), h_swl=h_swl,
+                  alpha=0.1, eta2=0.01 * h * h)
+    return System(pos=_as_pos4(xyz), vel=vel, gid=np.arange(n, dtype=np.int64), lo=lo, hi=hi,
+                  periodic=np.array([1, 1, 0], np.int32), kind=kind, params=params)

@@ -112,6 +112,11 @@ def lib(path: str = LIB_PATH):
         "pm_dist_refresh_pack": (st, [vp, vp]),
         "pm_dist_refresh_unpack": (st, [vp, vp]),
         "pm_dist_step": (st, [vp, C.c_float, C.c_int32, vp]),
+        "pm_dist_sph_init": (st, [vp]),
+        "pm_dist_sph_rates": (st, [vp, vp]),
+        "pm_dist_sph_update": (st, [vp, C.c_float, C.c_float, C.c_int32, vp]),
+        "pm_dist_refresh_pv_pack": (st, [vp, vp]),
+        "pm_dist_refresh_pv_unpack": (st, [vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -347,7 +352,7 @@ class Context:
         return dict(force_ms=fm.value, force_launches=fl.value, step_ms=sm.value, steps=ns.value)
 
 
-PM_MSG_MIGRATE, PM_MSG_GHOST, PM_MSG_REFRESH = 0, 1, 2
+PM_MSG_MIGRATE, PM_MSG_GHOST, PM_MSG_REFRESH, PM_MSG_REFRESH_PV = 0, 1, 2, 3
 PM_PHASE_PROLOGUE, PM_PHASE_STEP, PM_PHASE_FINAL, PM_PHASE_FORCES = 0, 1, 2, 3
 GHOST_BIT = 1 << 30
 
@@ -393,11 +398,27 @@ class DistContext(Context):
     def dist_finish(self):
         self._check(self.L.pm_dist_finish(self.h))
 
-    def refresh_pack(self, send):
-        self._check(self.L.pm_dist_refresh_pack(self.h, _dev_ptr(send)))
+    def refresh_pack(self, send, pv=False):
+        f = self.L.pm_dist_refresh_pv_pack if pv else self.L.pm_dist_refresh_pack
+        self._check(f(self.h, _dev_ptr(send)))
 
-    def refresh_unpack(self, recv):
-        self._check(self.L.pm_dist_refresh_unpack(self.h, _dev_ptr(recv)))
+    def refresh_unpack(self, recv, pv=False):
+        f = self.L.pm_dist_refresh_pv_unpack if pv else self.L.pm_dist_refresh_unpack
+        self._check(f(self.h, _dev_ptr(recv)))
+
+    def dist_sph_init(self):
+        self._check(self.L.pm_dist_sph_init(self.h))
+
+    def dist_sph_rates(self):
+        b = C.c_float(0.0)
+        self._check(self.L.pm_dist_sph_rates(self.h, C.byref(b)))
+        return float(b.value)
+
+    def dist_sph_update(self, bound, cfl=0.2, every=40):
+        f = C.c_int32(0)
+        self._check(self.L.pm_dist_sph_update(self.h, float(bound), float(cfl), int(every),
+                                              C.byref(f)))
+        return int(f.value)
 
     def get_kind(self):
         c = self.count()

@@ -242,3 +242,79 @@ def test_hybrid_transport_over_decomposition_gloo_world2():
             expect += [[q_, d, k] for d in order_q if d in D.valid_dirs() and D.peer(q_, d) == r
                        for k in range(cnt_q[d])]
         assert res[r][1] == expect
+
+
+class FakeSPHCtx(FakeCtx):
+    """FakeCtx plus the SPH stepping calls: a rank-dependent local step bound,
+    and a record of the bound each update was given."""
+
+    def __init__(self, rank, D, rng_key):
+        super().__init__(rank, D, rng_key)
+        self.bounds_seen = []
+        self.step = 0
+
+    def dist_sph_init(self):
+        pass
+
+    def dist_sph_rates(self):
+        self.step += 1
+        return float(np.float32(1e-4 * (1.0 + 0.5 * ((self.rank + self.step) % 3))))
+
+    def dist_sph_update(self, bound, cfl, every):
+        self.bounds_seen.append(bound)
+        return int(self.rank == 1 and self.step == 2)  # one rank asks for a rebuild once
+
+    def refresh_pack(self, buf, pv=False):
+        assert pv
+        import torch
+        n = buf.numel() // 32 if buf is not None else 0
+        if n:
+            buf.view(torch.float32)[:] = float(self.rank)
+
+    def refresh_unpack(self, buf, pv=False):
+        import torch
+        self.refreshed = [] if buf is None else sorted(set(buf.view(torch.float32).tolist()))
+
+
+def _sph_worker(rank, world, port, grid, out):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1804_07598_b200.pm as pmm
+    pmm.record_bytes = lambda what: 24
+    D = Decomp(grid)
+    ctx = FakeSPHCtx(rank, D, rng_key=(21, rank))
+    sim = DistSim(D, {rank: ctx}, TorchTransport(device=None), device="cpu")
+    sim.sph_start()
+    reb, t = sim.sph_run(4, cfl=0.5, every=10)
+    out.put((rank, ctx.bounds_seen, reb, t, ctx.refreshed))
+    dist.destroy_process_group()
+
+
+def test_sph_stepping_protocol_gloo_world2():
+    """DistSim.sph_run over world-size-2 gloo (NEXT-3 multi-GPU SPH): every
+    update gets the global minimum of the ranks' fp32 step bounds (exact
+    MIN all-reduce), a rebuild asked by one rank happens on both, and the
+    ghost refresh moves 32-byte records from the peer."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sph_worker, args=(r, 2, port, (2, 1, 1), q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        item = q.get(timeout=120)
+        res[item[0]] = item[1:]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    expect = [float(np.float32(1e-4 * (1.0 + 0.5 * min((r + s) % 3 for r in (0, 1)))))
+              for s in range(1, 5)]
+    for r in (0, 1):
+        bounds, reb, t, refreshed = res[r]
+        assert bounds == expect
+        assert reb == 1
+        assert t == pytest.approx(0.5 * sum(expect))
+        assert refreshed == [float(1 - r)]

@@ -244,3 +244,76 @@ def test_over_decomposition_hybrid_clustered(env):
     for c in sim.m.values():
         c.close()
     ref.close()
+
+
+def _hydro_rho(z, p):
+    P = p["rho0"] * 9.81 * np.maximum(p["h_swl"] - np.asarray(z, np.float64), 0.0)
+    return (p["rho0"] * (1.0 + P / p["b"]) ** (1.0 / p["gamma"])).astype(np.float32)
+
+
+@pytest.mark.parametrize("grid", [(2, 1, 1), (2, 2, 1)])
+def test_decomposed_sph_stepping_matches_single(env, grid):
+    """NEXT-3 multi-GPU SPH (pm_dist_sph_*): a periodic fluid layer with
+    random velocities stepped 60 times (dynamic dt from the global minimum
+    step bound, Euler every 10) on P sub-domains whose ghosts carry position,
+    velocity, rho and P each step, against the same run on one context and
+    against the fp64 oracle.  The pair sets are identical; only fp32
+    summation order differs.  (Random velocities up to 0.3 m/s: several
+    rebuilds with migrations within the 60 steps.)"""
+    import torch
+    pm, dist = env
+    from oracle import oracle as orc
+    s = inputs.sph_layer(vmax=0.3)
+    p = s.params
+    rc, skin = 2.0 * p["h"], 0.1 * p["h"]
+    rho0 = _hydro_rho(s.pos[:, 2], p)
+    nsteps, cfl, every = 60, 0.2, 10
+    # one context
+    c = pm.Context()
+    c.set_domain(s.lo, s.hi, s.periodic)
+    c.set_cutoff(rc, skin)
+    c.set_sph(p)
+    c.place(s.pos, s.vel, s.gid, s.kind)
+    c.build_verlet()
+    c.set_rho(_hydro_rho(c.get_state()["pos"][:, 2], p))
+    r1 = c.sph_run(nsteps, cfl=cfl, every=every)
+    one = pm.sorted_by_gid(c.get_state())
+    c.close()
+    # decomposed, loopback transport on this GPU
+    D = dist.Decomp(grid)
+    owner = dist.owner_of(s, D)
+    stream = torch.cuda.Stream()
+    members = {}
+    for r in range(D.size):
+        idx = np.where(owner == r)[0]
+        m = dist.make_member(s.subset(idx), D, r, stream=stream, rc=rc, skin=skin, sph=p)
+        m.set_rho(rho0[idx])
+        members[r] = m
+    sim = dist.DistSim(D, members, dist.LoopbackTransport(members), stream=stream)
+    sim.sph_start()
+    reb, t = sim.sph_run(nsteps, cfl=cfl, every=every)
+    torch.cuda.synchronize()
+    assert reb >= 2 and r1["rebuilds"] >= 2  # migrations and new ghost layers on the way
+    got = owned_union(pm, sim)
+    assert np.array_equal(got["gid"], s.gid)  # every particle owned exactly once
+    assert t == pytest.approx(r1["time"], rel=1e-5)
+    dp = p["dp"]
+    x, x1 = got["pos"][:, :3].astype(np.float64), one["pos"][:, :3].astype(np.float64)
+    L = (s.hi - s.lo).astype(np.float64)
+    dx = x - x1
+    dx[:, :2] -= L[:2] * np.round(dx[:, :2] / L[:2])  # periodic images
+    assert np.max(np.abs(dx)) < 1e-4 * dp
+    v, v1 = got["vel"][:, :3].astype(np.float64), one["vel"][:, :3].astype(np.float64)
+    assert np.max(np.abs(v - v1)) / np.max(np.abs(v1)) < 1e-3
+    assert np.max(np.abs(got["rho"].astype(np.float64) - one["rho"])) / p["rho0"] < 1e-5
+    # the oracle on the same run
+    xr, vr, rr, dtr = orc.sph_run(s.pos, s.vel, rho0.astype(np.float64), s.kind, s.lo, s.hi,
+                                  s.periodic, p, nsteps, cfl=cfl, every=every)
+    assert t == pytest.approx(dtr.sum(), rel=1e-4)
+    dx = x - xr
+    dx[:, :2] -= L[:2] * np.round(dx[:, :2] / L[:2])
+    assert np.max(np.abs(dx)) < 1e-4 * dp
+    assert np.max(np.abs(v - vr)) / np.max(np.abs(vr)) < 1e-3
+    assert np.max(np.abs(got["rho"] - rr)) / p["rho0"] < 1e-5
+    for m in members.values():
+        m.close()
