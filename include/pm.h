@@ -93,6 +93,18 @@ pm_status pm_set_cutoff(pm_ctx ctx, float r_cut, float skin);
  * (r_eff = max(r, r_min)), 0 the plain potential. */
 pm_status pm_set_lj(pm_ctx ctx, float epsilon, float sigma, float mass, float r_min);
 
+/* Half (Newton) neighbour lists, SURVEY §8(f) NEXT-1 ("compute
+ * every interaction pair only once"; the symmetric cell/Verlet lists of
+ * getCellListSym).  on = 1: each row keeps only j > i in the
+ * current (cell) order, the force sweep adds f (x_i - x_j) to F_i and
+ * f (x_j - x_i) to F_j with vectorised global reductions, and the
+ * velocity-Verlet update runs as a separate kernel; forces, energies and the
+ * virial agree with the full list up to summation order (not bit-
+ * reproducible run to run).  The lists are rebuilt at the next call that
+ * needs them.  LJ only: SPH, DEM and decomposed contexts return PM_E_STATE
+ * with half lists.  Default 0 (full lists: atomic-free, deterministic). */
+pm_status pm_set_newton(pm_ctx ctx, int32_t on);
+
 /* Velocity limit of reading R22 (clustered BASELINE.json configs[4]): after
  * every kick, v <- v * min(1, vmax / |v|), so no particle drifts more than
  * vmax * dt per step.  vmax = 0 (default) disables the limit. */

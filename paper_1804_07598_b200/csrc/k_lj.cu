@@ -250,18 +250,11 @@ __device__ __forceinline__ void kick_limited(float4 &v, float k, const Acc &a, f
 //  inner: F(x); v += dt F/m (2nd half-kick of this step + 1st of the next);
 //         x' = wrap(x + dt v); displacement test vs xref; -> alternate buffers
 //  final: F(x); v += dt/2 F/m; F stored; x copied  -> alternate buffers
-template <bool CAPPED>
-__global__ void __launch_bounds__(256) k_lj_step(Params P, Bufs B, int n, float dt, int mode_arg) {
-  State *st = B.st;
-  if (st->abort) return;
-  const int mode = mode_arg >= 0 ? mode_arg : st->mode;
-  const int cp = st->cur_pv;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = i < n;
-  const float4 *__restrict__ pos = B.pos[cp];
-  const float4 xi = active ? pos[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-  Acc a = lj_force_of<CAPPED, false>(P, B, pos, i, active, xi);
-  bool far = false;
+// The velocity-Verlet epilogue of one particle after its force a (see
+// k_lj_step); writes the alternate buffers and sets `far`.
+__device__ __forceinline__ void vv_epilogue(const Params &P, const Bufs &B, State *st, int i,
+                                            bool active, const float4 &xi, const Acc &a,
+                                            float dt, int mode, int cp, bool &far) {
   // ghost copies (multi-GPU) are not integrated: after an inner step the
   // refresh overwrites them; the final step (positions unchanged) carries
   // them over so the state stays consistent for getters / energy passes
@@ -291,6 +284,145 @@ __global__ void __launch_bounds__(256) k_lj_step(Params P, Bufs B, int n, float 
     B.vel[cp ^ 1][i] = v;
     if (!isfinite(a.fx + a.fy + a.fz))
       raise_error(st, -8 /*PM_E_NONFINITE*/, (long long)B.gid[st->cur_id][i]);
+  }
+}
+
+// One fused velocity-Verlet step (pm_step_vv), mode read from the state:
+//  inner: F(x); v += dt F/m (2nd half-kick of this step + 1st of the next);
+//         x' = wrap(x + dt v); displacement test vs xref; -> alternate buffers
+//  final: F(x); v += dt/2 F/m; F stored; x copied  -> alternate buffers
+template <bool CAPPED>
+__global__ void __launch_bounds__(256) k_lj_step(Params P, Bufs B, int n, float dt, int mode_arg) {
+  State *st = B.st;
+  if (st->abort) return;
+  const int mode = mode_arg >= 0 ? mode_arg : st->mode;
+  const int cp = st->cur_pv;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = i < n;
+  const float4 *__restrict__ pos = B.pos[cp];
+  const float4 xi = active ? pos[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  Acc a = lj_force_of<CAPPED, false>(P, B, pos, i, active, xi);
+  bool far = false;
+  vv_epilogue(P, B, st, i, active, xi, a, dt, mode, cp, far);
+  if (__any_sync(0xffffffffu, far) && (threadIdx.x & 31) == 0) st->need_rebuild = 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->pending_flip = 1;
+    st->steps_done += 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Half (Newton) list, SURVEY §8(f) NEXT-1 ("compute every
+// interaction pair only once"): row i holds j > i only; the sweep adds
+// f (x_i - x_j) to its own accumulator and f (x_j - x_i) to F_j with one
+// vectorised fire-and-forget reduction (red.global.add.v4.f32, sm_90+); the
+// integrator runs as a separate epilogue kernel once all reductions landed.
+// Sums are not bit-reproducible (reduction order); single-GPU contexts only.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void red_add4(float4 *p, float x, float y, float z) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(x), "f"(y),
+               "f"(z), "f"(0.f)
+               : "memory");
+}
+
+template <bool MI, bool CAPPED, bool ENERGY>
+__device__ __forceinline__ void lj_pair_half(const Params &P, const float4 &xi, const float4 &xj,
+                                             int j, bool valid, Acc &a, float4 *__restrict__ F) {
+  float dx, dy, dz;
+  if (MI) {
+    dx = P.box.per[0] ? r4_delta(xi.x, xj.x, P.box.L[0], P.box.halfL[0]) : __fsub_rn(xj.x, xi.x);
+    dy = P.box.per[1] ? r4_delta(xi.y, xj.y, P.box.L[1], P.box.halfL[1]) : __fsub_rn(xj.y, xi.y);
+    dz = P.box.per[2] ? r4_delta(xi.z, xj.z, P.box.L[2], P.box.halfL[2]) : __fsub_rn(xj.z, xi.z);
+  } else {
+    dx = __fsub_rn(xj.x, xi.x);
+    dy = __fsub_rn(xj.y, xi.y);
+    dz = __fsub_rn(xj.z, xi.z);
+  }
+  const float d2 = dist2(dx, dy, dz);
+  const bool in = valid && (d2 < P.lj.rc2);
+  float f, r6i;
+  if (CAPPED) {
+    const float r2e = fmaxf(d2, P.lj.r_min * P.lj.r_min);
+    const float r2ie = fast_rcp(r2e);
+    r6i = r2ie * r2ie * r2ie;
+    const float g = r6i * (P.lj.c12 * r6i - P.lj.c6);
+    f = g * fast_rsqrt(r2e) * fast_rsqrt(d2);
+  } else {
+    const float r2i = fast_rcp(d2);
+    r6i = r2i * r2i * r2i;
+    f = r2i * (r6i * (P.lj.c12 * r6i - P.lj.c6));
+  }
+  if (in) {
+    a.fx = fmaf(-f, dx, a.fx);
+    a.fy = fmaf(-f, dy, a.fy);
+    a.fz = fmaf(-f, dz, a.fz);
+    red_add4(F + j, f * dx, f * dy, f * dz);
+    if (ENERGY) {
+      a.u += r6i * (P.lj.e12 * r6i - P.lj.e6);  // the whole pair: both halves
+      a.w += f * d2;
+      a.np += 2;
+    }
+  }
+}
+
+template <bool MI, bool CAPPED, bool ENERGY>
+__device__ __forceinline__ void lj_row_half(const Params &P, const float4 *__restrict__ pos,
+                                            const int *__restrict__ nb, int cnt,
+                                            const float4 &xi, Acc &a, float4 *__restrict__ F) {
+  const int ng = (cnt + 3) >> 2;
+  if (ng == 0) return;
+  Idx4 j0 = ld_idx4(nb);
+  Idx4 j1 = (ng > 1) ? ld_idx4(nb + 128) : j0;
+  for (int g = 0; g < ng; ++g) {
+    const Idx4 j2 = (g + 2 < ng) ? ld_idx4(nb + (g + 2) * 128) : j1;
+    const int rem = cnt - 4 * g;
+    const float4 x0 = __ldg(pos + j0.a), x1 = __ldg(pos + j0.b);
+    const float4 x2 = __ldg(pos + j0.c), x3 = __ldg(pos + j0.d);
+    lj_pair_half<MI, CAPPED, ENERGY>(P, xi, x0, j0.a, true, a, F);
+    lj_pair_half<MI, CAPPED, ENERGY>(P, xi, x1, j0.b, rem > 1, a, F);
+    lj_pair_half<MI, CAPPED, ENERGY>(P, xi, x2, j0.c, rem > 2, a, F);
+    lj_pair_half<MI, CAPPED, ENERGY>(P, xi, x3, j0.d, rem > 3, a, F);
+    j0 = j1;
+    j1 = j2;
+  }
+}
+
+// F must be zero on entry (the launcher clears it).
+template <bool CAPPED, bool ENERGY>
+__global__ void __launch_bounds__(256) k_lj_half(Params P, Bufs B, int n) {
+  State *st = B.st;
+  if (st->abort) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = i < n;
+  const float4 *__restrict__ pos = B.pos[st->cur_pv];
+  const float4 xi = active ? pos[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  Acc a = {0.f, 0.f, 0.f, 0.f, 0.f, 0};
+  const bool mi = __any_sync(0xffffffffu, active && near_periodic_face(P, xi));
+  if (active) {
+    const int cnt = B.cnt[i];
+    const int *nb = B.nbr + nbr_row_base(B, i);
+    if (mi) lj_row_half<true, CAPPED, ENERGY>(P, pos, nb, cnt, xi, a, B.force);
+    else lj_row_half<false, CAPPED, ENERGY>(P, pos, nb, cnt, xi, a, B.force);
+    red_add4(B.force + i, a.fx, a.fy, a.fz);
+  }
+  if (ENERGY) block_add_energy(st, (double)a.u, (double)a.w, (double)a.np);
+}
+
+// The integrator of the Newton path: the epilogue of k_lj_step on F = force.
+__global__ void __launch_bounds__(256) k_lj_half_vv(Params P, Bufs B, int n, float dt,
+                                                     int mode_arg) {
+  State *st = B.st;
+  if (st->abort) return;
+  const int mode = mode_arg >= 0 ? mode_arg : st->mode;
+  const int cp = st->cur_pv;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = i < n;
+  bool far = false;
+  if (active) {
+    const float4 xi = B.pos[cp][i];
+    const float4 f = B.force[i];
+    const Acc a = {f.x, f.y, f.z, 0.f, 0.f, 0};
+    vv_epilogue(P, B, st, i, true, xi, a, dt, mode, cp, far);
   }
   if (__any_sync(0xffffffffu, far) && (threadIdx.x & 31) == 0) st->need_rebuild = 1;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -363,8 +495,25 @@ inline unsigned nb(int64_t n) { return (unsigned)((n + 255) / 256); }
 
 }  // namespace
 
+static void launch_lj_half(const Params &P, const Bufs &B, int64_t n, int want_energy,
+                           cudaStream_t s) {
+  cudaMemsetAsync(B.force, 0, sizeof(float4) * (size_t)n, s);
+  const bool capped = P.lj.r_min > 0.f;
+  if (capped) {
+    if (want_energy) k_lj_half<true, true><<<nb(n), 256, 0, s>>>(P, B, (int)n);
+    else k_lj_half<true, false><<<nb(n), 256, 0, s>>>(P, B, (int)n);
+  } else {
+    if (want_energy) k_lj_half<false, true><<<nb(n), 256, 0, s>>>(P, B, (int)n);
+    else k_lj_half<false, false><<<nb(n), 256, 0, s>>>(P, B, (int)n);
+  }
+}
+
 void launch_lj(const Params &P, const Bufs &B, int64_t n, int want_energy, cudaStream_t s) {
   if (n <= 0) return;
+  if (P.newton) {
+    launch_lj_half(P, B, n, want_energy, s);
+    return;
+  }
   const bool capped = P.lj.r_min > 0.f;
   if (capped) {
     if (want_energy) k_lj<true, true><<<nb(n), 256, 0, s>>>(P, B, (int)n);
@@ -378,6 +527,11 @@ void launch_lj(const Params &P, const Bufs &B, int64_t n, int want_energy, cudaS
 void launch_lj_step_mode(const Params &P, const Bufs &B, int64_t n, float dt, int mode,
                          cudaStream_t s) {
   if (n <= 0) return;
+  if (P.newton) {  // clear F -> half sweep -> integrator
+    launch_lj_half(P, B, n, 0, s);
+    k_lj_half_vv<<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode);
+    return;
+  }
   if (P.lj.r_min > 0.f) k_lj_step<true><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode);
   else k_lj_step<false><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode);
 }

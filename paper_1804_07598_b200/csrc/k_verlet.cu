@@ -90,7 +90,12 @@ __device__ __forceinline__ void scan_run(const Params &P, const float4 *__restri
       if (rem > 24) test8<SHIFTJ, PAIRMI, 24, true>(P, pos, j0, e, xi_eff, csh, pmi, msk);
       msk &= (1u << rem) - 1u;
     }
-    if (self >= j0 && self < j0 + 32) msk &= ~(1u << (self - j0));
+    if (P.newton) {  // half list (NEXT-1): only j > i, each pair once
+      const int t = self - j0;
+      msk &= t < 0 ? 0xffffffffu : (t >= 31 ? 0u : (0xffffffffu << (t + 1)));
+    } else if (self >= j0 && self < j0 + 32) {
+      msk &= ~(1u << (self - j0));
+    }
     while (msk) {
       const int u = __ffs(msk) - 1;
       msk &= msk - 1u;

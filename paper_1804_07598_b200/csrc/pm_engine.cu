@@ -744,6 +744,18 @@ pm_status pm_set_lj(pm_ctx c, float eps, float sigma, float mass, float r_min) {
   return PM_OK;
 }
 
+pm_status pm_set_newton(pm_ctx c, int32_t on) {
+  if (!c) return PM_E_INVAL;
+  if (on && c->dist)
+    return set_err(c, PM_E_STATE, "pm_set_newton: single (non-decomposed) contexts only");
+  c->P.newton = on ? 1 : 0;
+  c->list_valid = false;  // the next build emits the other kind of rows
+  c->forces_valid = false;
+  destroy_graph(c);
+  destroy_dem_graph(c);
+  return PM_OK;
+}
+
 pm_status pm_set_vlimit(pm_ctx c, float vmax) {
   if (!c) return PM_E_INVAL;
   if (!(vmax >= 0.f)) return set_err(c, PM_E_INVAL, "pm_set_vlimit: vmax must be >= 0");
@@ -858,6 +870,7 @@ pm_status pm_thermo_compute(pm_ctx c) { return pm_compute_lj(c, 1); }
 pm_status pm_sph_density(pm_ctx c) {
   pm_status s = check_ready(c);
   if (s) return s;
+  if (c->P.newton) return set_err(c, PM_E_STATE, "SPH needs full lists (pm_set_newton 0)");
   if (!c->list_valid) return set_err(c, PM_E_STATE, "pm_sph_density: no Verlet list");
   if (!c->have_sph) return set_err(c, PM_E_STATE, "pm_set_sph not called");
   cudaSetDevice(c->device);
@@ -871,6 +884,7 @@ pm_status pm_sph_density(pm_ctx c) {
 pm_status pm_sph_forces(pm_ctx c) {
   pm_status s = check_ready(c);
   if (s) return s;
+  if (c->P.newton) return set_err(c, PM_E_STATE, "SPH needs full lists (pm_set_newton 0)");
   if (!c->rho_valid) return set_err(c, PM_E_STATE, "pm_sph_forces: densities not computed");
   cudaSetDevice(c->device);
   launch_sph_forces(c->P, c->B, c->n, c->stream);
@@ -994,6 +1008,7 @@ static pm_status dem_graph_ready(pm_ctx c, float dt) {
 pm_status pm_dem_run(pm_ctx c, float dt, int64_t nsteps, int64_t *rebuilds) {
   pm_status s = check_ready(c);
   if (s) return s;
+  if (c->P.newton) return set_err(c, PM_E_STATE, "DEM needs full lists (pm_set_newton 0)");
   if (rebuilds) *rebuilds = 0;
   if (!c->have_dem) return set_err(c, PM_E_STATE, "pm_set_dem not called");
   if (c->dist) return set_err(c, PM_E_STATE, "pm_dem_run: single (non-decomposed) context only");
@@ -1150,6 +1165,7 @@ pm_status pm_sph_run(pm_ctx c, int64_t nsteps, float cfl, int32_t every,
                      pm_sph_run_stats *out) {
   pm_status s = check_ready(c);
   if (s) return s;
+  if (c->P.newton) return set_err(c, PM_E_STATE, "SPH needs full lists (pm_set_newton 0)");
   if (out) std::memset(out, 0, sizeof *out);
   if (!c->have_sph) return set_err(c, PM_E_STATE, "pm_set_sph not called");
   if (c->dist) return set_err(c, PM_E_STATE, "pm_sph_run: single (non-decomposed) context only");
@@ -1425,6 +1441,7 @@ int32_t pm_record_bytes(int32_t what) {
 
 pm_status pm_set_decomposition(pm_ctx c, const int32_t pgrid[3], const int32_t pcoord[3]) {
   if (!c || !pgrid || !pcoord) return PM_E_INVAL;
+  if (c->P.newton) return set_err(c, PM_E_STATE, "decomposed contexts need full lists");
   if (!c->have_domain || !c->have_cutoff)
     return set_err(c, PM_E_STATE, "pm_set_decomposition: set the domain and cutoff first");
   cudaSetDevice(c->device);

@@ -100,6 +100,7 @@ struct Params {
   float vmax;       // velocity limit (reading R22), 0 = off
   int sph_state;    // 1: the cell-sort reorder also permutes the SPH stepping state
   int dem_state;    // 1: ... and the DEM angular velocities
+  int newton;       // 1: half (Newton) list, j > i in cell order (NEXT-1)
   DEM dem;
 };
 

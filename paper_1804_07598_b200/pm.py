@@ -112,6 +112,7 @@ def lib(path: str = LIB_PATH):
         "pm_dist_refresh_pack": (st, [vp, vp]),
         "pm_dist_refresh_unpack": (st, [vp, vp]),
         "pm_dist_step": (st, [vp, C.c_float, C.c_int32, vp]),
+        "pm_set_newton": (st, [vp, C.c_int32]),
         "pm_dist_sph_init": (st, [vp]),
         "pm_dist_sph_rates": (st, [vp, vp]),
         "pm_dist_sph_update": (st, [vp, C.c_float, C.c_float, C.c_int32, vp]),
@@ -236,6 +237,10 @@ class Context:
 
     def sph_forces(self):
         self._check(self.L.pm_sph_forces(self.h))
+
+    def set_newton(self, on: bool):
+        """Half (Newton) lists with reductions for the j side (NEXT-1)."""
+        self._check(self.L.pm_set_newton(self.h, 1 if on else 0))
 
     def set_dem(self, p):
         """p: dict with R, m, I, kn, kt, gn, gt, mu, g (3), walls (6 flags)."""

@@ -193,6 +193,86 @@ def test_lj_forces_parity(pm, orc, name):
     c.close()
 
 
+@pytest.mark.parametrize("name", ["cfg1", "cfg2_sampled", "random_mixed_bc"])
+def test_newton_half_lists_and_forces(pm, orc, name):
+    """NEXT-1 half (Newton) lists (pm_set_newton): every row is exactly the
+    oracle's full row restricted to partners later in the current (cell)
+    order, so each unordered pair appears once; the reduction sweep gives the
+    oracle's forces within the north_star bar, and the whole-system pair
+    count, energy and virial."""
+    if name == "cfg1":
+        s = inputs.shuffled(inputs.cfg1(), (14,))
+        pick = None
+    elif name == "cfg2_sampled":
+        s = inputs.cfg2()
+        pick = np.random.default_rng(3).choice(s.n, 400, replace=False)
+    else:
+        s = inputs.lj_lattice_system(14, 14, 14, jitter_key=(15,), jitter=0.12)
+        s.periodic = np.array([1, 1, 0], np.int32)
+        s.hi[2] = s.hi[2] + np.float32(0.5)
+        pick = None
+    c = pm.Context()
+    c.set_newton(True)
+    c.set_domain(s.lo, s.hi, s.periodic)
+    c.set_cutoff(2.5, 0.3)
+    c.set_lj(1.0, 1.0, 1.0, 0.0)
+    c.place(s.pos, s.vel, s.gid, s.kind)
+    c.build_verlet()
+    rp, col = c.get_verlet()
+    st = c.get_state()
+    cur_of_gid = np.empty(int(s.gid.max()) + 1, np.int64)
+    cur_of_gid[st["gid"]] = np.arange(s.n)
+    inv = idx_of_gid(s)
+    rows = np.arange(s.n) if pick is None else pick
+    rrp, rcols, _ = orc.verlet_rows(s.pos, s.lo, s.hi, s.periodic, rv32(2.5, 0.3),
+                                    rows=inv[st["gid"][rows]], want_shift=False)
+    for t, i in enumerate(rows):
+        full = s.gid[rcols[rrp[t]:rrp[t + 1]]]
+        half = np.sort(full[cur_of_gid[full] > i])
+        assert np.array_equal(np.sort(col[rp[i]:rp[i + 1]]), half), f"row {i}"
+    if pick is None:
+        assert rp[-1] * 2 == len(rcols)  # each unordered pair once
+    c.compute_lj(want_energy=True)
+    st = c.get_state()
+    th = c.thermo(recompute=False)
+    ref = orc.lj_rows(s.pos, s.lo, s.hi, s.periodic, rc=2.5, rows=inv[st["gid"][rows]])
+    err = orc.normalized_max_err(st["force"][rows, :3].astype(np.float64), ref["F"])
+    assert err <= TOL, err
+    if pick is None:
+        assert th["npairs"] == int(ref["npair"].sum())
+        assert th["pe_raw"] == pytest.approx(ref["U"].sum(), rel=1e-5)
+        assert th["virial"] == pytest.approx(ref["W"].sum(), rel=1e-5)
+    c.close()
+
+
+def test_newton_nve_matches_full_list(pm):
+    """The Newton path through pm_step_vv (clear F -> half sweep with
+    reductions -> velocity-Verlet kernel, in the CUDA graph with the
+    conditional rebuild) follows the full-list trajectory over 30 steps with
+    rebuilds (differences: fp32 summation order only); SPH, DEM and
+    decomposition refuse half lists."""
+    s = inputs.lj_lattice_system(24, 24, 24, jitter_key=(16,), vel_key=(116,))
+    out = {}
+    for newton in (False, True):
+        c = pm.Context()
+        c.set_newton(newton)
+        c.set_domain(s.lo, s.hi, s.periodic)
+        c.set_cutoff(2.5, 0.3)
+        c.set_lj(1.0, 1.0, 1.0, 0.0)
+        c.place(s.pos, s.vel, s.gid, s.kind)
+        r = c.step_vv(0.005, 30)
+        out[newton] = (pm.sorted_by_gid(c.get_state()), r["rebuilds"])
+        if newton:
+            with pytest.raises(pm.PMError) as e:
+                c.sph_density()
+            assert e.value.code == -2
+        c.close()
+    a, b = out[False][0], out[True][0]
+    assert out[False][1] == out[True][1] and out[True][1] >= 2
+    assert np.max(np.abs(a["pos"][:, :3] - b["pos"][:, :3])) < 1e-4
+    assert np.max(np.abs(a["vel"][:, :3] - b["vel"][:, :3])) < 1e-3
+
+
 def test_lj_perfect_lattice_closed_form(pm):
     """Exactly representable SC lattice: F = 0 and U/N = lattice sum (pinned in
     tests/test_oracle_pins.py by integer enumeration)."""
