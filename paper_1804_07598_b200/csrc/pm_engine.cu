@@ -1175,6 +1175,10 @@ pm_status pm_sph_run(pm_ctx c, int64_t nsteps, float cfl, int32_t every,
     return set_err(c, PM_E_INVAL, "pm_sph_run: needs a Verlet skin > 0 (pm_set_cutoff)");
   cudaSetDevice(c->device);
   if (nsteps == 0) return PM_OK;
+  if (c->n == 0) {  // nothing to step (and no step bound to take dt from)
+    if (out) out->steps = nsteps;
+    return PM_OK;
+  }
   Bufs &B = c->B;
   if ((s = sph_step_alloc(c))) return s;
   if (!c->P.sph_state) {  // the cell-sort reorder now carries the stepping state
@@ -1243,6 +1247,10 @@ pm_status pm_step_vv(pm_ctx c, float dt, int64_t nsteps, pm_run_stats *out) {
   cudaSetDevice(c->device);
   if (out) std::memset(out, 0, sizeof *out);
   if (nsteps == 0) return PM_OK;
+  if (c->n == 0) {  // nothing to integrate: the steps are trivially done
+    if (out) out->steps = nsteps;
+    return PM_OK;
+  }
   if (!c->list_valid) {
     s = build_list(c);
     if (s) return s;

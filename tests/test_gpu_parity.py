@@ -595,6 +595,55 @@ def test_tiny_and_ragged_sizes(pm, orc):
         c.close()
 
 
+def test_empty_inputs(pm):
+    """Zero particles: before any placement the calls report PM_E_STATE; a
+    context emptied by pm_place(n = 0) builds, sweeps and steps nothing
+    (every launcher guards n = 0) and returns empty arrays."""
+    s = inputs.cfg1()
+    empty = np.zeros((0, 4), np.float32)
+    c = pm.Context()
+    c.set_domain(s.lo, s.hi, s.periodic)
+    c.set_cutoff(2.5, 0.3)
+    c.set_lj(1.0, 1.0, 1.0, 0.0)
+    c.place(empty, empty, np.zeros(0, np.int64))
+    with pytest.raises(pm.PMError) as e:
+        c.build_verlet()
+    assert e.value.code == -2
+    c.place(s.pos, s.vel, s.gid)
+    c.build_verlet()
+    c.place(empty, empty, np.zeros(0, np.int64))
+    c.build_verlet()
+    c.compute_lj(want_energy=True)
+    r = c.step_vv(0.005, 3)
+    assert r["steps"] == 3 and r["rebuilds"] == 0
+    assert c.count()["nnz"] == 0
+    st = c.get_state()
+    assert st["pos"].shape == (0, 4) and st["gid"].shape == (0,)
+    rp, col = c.get_verlet()
+    assert rp.tolist() == [0] and col.size == 0
+    assert c.thermo()["npairs"] == 0
+    c.close()
+    # SPH stepping and DEM on an emptied context
+    s4 = inputs.cfg4(dp=1.0 / 16.0)
+    c = pm.Context()
+    c.set_domain(s4.lo, s4.hi, s4.periodic)
+    c.set_cutoff(2.0 * s4.params["h"], 0.1 * s4.params["h"])
+    c.set_sph(s4.params)
+    c.place(s4.pos, s4.vel, s4.gid, s4.kind)
+    c.place(empty, empty, np.zeros(0, np.int64), np.zeros(0, np.int32))
+    assert c.sph_run(5)["steps"] == 5
+    c.close()
+    s5 = inputs.dem_avalanche(4, 4, 4)
+    c = pm.Context()
+    c.set_domain(s5.lo, s5.hi, s5.periodic)
+    c.set_cutoff(2.0 * s5.params["R"], s5.params["skin"])
+    c.set_dem(s5.params)
+    c.place(s5.pos, s5.vel, s5.gid)
+    c.place(empty, empty, np.zeros(0, np.int64))
+    assert c.dem_run(s5.params["dt"], 5) == 0
+    c.close()
+
+
 def hydrostatic_rho(z, p):
     """Initial density of a fluid column at rest (the DualSPHysics dam-break
     start): P = rho0 |g| (h_swl - z) for z < h_swl, rho = rho0 (1 + P/b)^(1/gamma)
