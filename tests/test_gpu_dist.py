@@ -317,3 +317,44 @@ def test_decomposed_sph_stepping_matches_single(env, grid):
     assert np.max(np.abs(got["rho"] - rr)) / p["rho0"] < 1e-5
     for m in members.values():
         m.close()
+
+
+def test_cfg3_full_size_decomposed_sampled_parity(env):
+    """BJ configs[2] at full size in the launch configuration of the N = 2
+    bench (one 128^3 block = 2,097,152 particles per sub-domain, grid
+    (2,1,1), 4.2M particles in two contexts on this GPU): every particle owned
+    once, sampled rows' neighbour sets (gid pairs, ghosts included) and
+    forces against the fp64 oracle on the global system, then 10 steps with
+    the per-step ghost refresh."""
+    pm, dist = env
+    from oracle import oracle as orc
+    grid = (2, 1, 1)
+    s = inputs.cfg3_global(grid)
+    sim = decomposed(pm, dist, s, grid)
+    sim.start()
+    inv = np.empty(s.n, np.int64)
+    inv[s.gid] = np.arange(s.n)
+    rng = np.random.default_rng(9)
+    rv = np.float32(np.float32(2.5) + np.float32(0.3))
+    seen = 0
+    for ctx in sim.m.values():
+        st = ctx.get_state()
+        kind = ctx.get_kind()
+        own = np.where((kind & pm.GHOST_BIT) == 0)[0]
+        seen += own.size
+        pick = rng.choice(own, 150, replace=False)
+        rp, col = ctx.get_verlet()
+        rrp, rcols, _ = orc.verlet_rows(s.pos, s.lo, s.hi, s.periodic, rv,
+                                        rows=inv[st["gid"][pick]], want_shift=False)
+        for t, i in enumerate(pick):
+            assert np.array_equal(np.sort(col[rp[i]:rp[i + 1]]),
+                                  np.sort(s.gid[rcols[rrp[t]:rrp[t + 1]]])), f"row {i}"
+        ref = orc.lj_rows(s.pos, s.lo, s.hi, s.periodic, rc=2.5, rows=inv[st["gid"][pick]])
+        err = orc.normalized_max_err(st["force"][pick, :3].astype(np.float64), ref["F"])
+        assert err <= 1e-4, err
+    assert seen == s.n
+    sim.run(10)
+    got = owned_union(pm, sim)
+    assert np.array_equal(got["gid"], np.sort(s.gid))
+    for ctx in sim.m.values():
+        ctx.close()
