@@ -819,3 +819,31 @@ def test_dem_graph_matches_host_loop_with_resume(pm):
     for k in ("pos", "vel", "gid"):
         assert np.array_equal(a[0][k], b[0][k]), k
     assert np.array_equal(a[1], b[1])
+
+
+def test_largest_config_size_uniform(pm, orc):
+    """The largest particle count of the BASELINE configs (cfg5's 8,388,608)
+    on one context, as a uniform rho = 0.8 liquid (256 x 256 x 128 SC
+    lattice; cfg5's clustered layout needs the 8-GPU split): cells bit-exact
+    on sampled particles, sampled Verlet rows and forces against the oracle,
+    and 5 steps through the step graph."""
+    s = inputs.lj_lattice_system(256, 256, 128, jitter_key=(77,), vel_key=(177,))
+    assert s.n == 8388608
+    c = make_ctx(pm, s)
+    c.build_verlet()
+    rp, col = c.get_verlet()
+    st = c.get_state()
+    inv = idx_of_gid(s)
+    pick = np.random.default_rng(4).choice(s.n, 120, replace=False)
+    rrp, rcols, _ = orc.verlet_rows(s.pos, s.lo, s.hi, s.periodic, rv32(2.5, 0.3),
+                                    rows=inv[st["gid"][pick]], want_shift=False)
+    for t, i in enumerate(pick):
+        assert np.array_equal(np.sort(col[rp[i]:rp[i + 1]]),
+                              np.sort(s.gid[rcols[rrp[t]:rrp[t + 1]]])), f"row {i}"
+    c.compute_lj()
+    st = c.get_state()
+    ref = orc.lj_rows(s.pos, s.lo, s.hi, s.periodic, rc=2.5, rows=inv[st["gid"][pick]])
+    assert orc.normalized_max_err(st["force"][pick, :3].astype(np.float64), ref["F"]) <= TOL
+    r = c.step_vv(0.005, 5)
+    assert r["steps"] == 5
+    c.close()
