@@ -282,12 +282,21 @@ pm_status pm_get_profile(pm_ctx ctx, double *force_ms, int64_t *force_launches,
  * copies): pair distances use the global-box rule R4, so a pair's d2 is the
  * same whether the partner is a ghost or a local periodic image.
  * ---------------------------------------------------------------------- */
-enum { PM_MSG_MIGRATE = 0, PM_MSG_GHOST = 1, PM_MSG_REFRESH = 2, PM_MSG_REFRESH_PV = 3 };
+enum {
+  PM_MSG_MIGRATE = 0,
+  PM_MSG_GHOST = 1,
+  PM_MSG_REFRESH = 2,
+  PM_MSG_REFRESH_PV = 3,   /* SPH runs: position + velocity */
+  PM_MSG_REFRESH_PVW = 4,  /* DEM runs: position + velocity + angular velocity */
+  PM_MSG_MIGRATE_HIST = 5  /* DEM runs: contact histories of the migrating grains */
+};
 enum { PM_PHASE_PROLOGUE = 0, PM_PHASE_STEP = 1, PM_PHASE_FINAL = 2, PM_PHASE_FORCES = 3 };
 
-/* Bytes per message record: migrate 64 (pos, vel, SPH previous-step
- * velocity, gid, kind), ghost 32 (pos, gid, kind), refresh 16 (pos), refresh
- * with velocities 32 (pos, vel; SPH runs).  Returns -1 for an unknown kind. */
+/* Bytes per message record: migrate 64 (pos, vel, SPH previous-step velocity
+ * or DEM angular velocity, gid, kind), ghost 32 (pos, gid, kind), refresh 16
+ * (pos), refresh with velocities 32 (pos, vel; SPH runs), refresh with
+ * angular velocities 48 (DEM runs), migrating contact histories 592 (gid,
+ * count, up to 24 (partner gid, u_t) pairs).  Returns -1 for an unknown kind. */
 int32_t pm_record_bytes(int32_t what);
 
 /* This context owns cuboid pcoord of a pgrid[0] x pgrid[1] x pgrid[2]
@@ -343,6 +352,28 @@ pm_status pm_dist_refresh_unpack(pm_ctx ctx, const void *recv_dev);
  * (nullable): synchronise and return (and clear) the local flag "some owned
  * particle moved more than skin/2 since the last build". */
 pm_status pm_dist_step(pm_ctx ctx, float dt, int32_t phase, int32_t *need_rebuild);
+
+/* Decomposed DEM (SURVEY §8(f) NEXT-4 on the §8(e) decomposition; PAPER.md:
+ * 479 "collisions involving ghost particles need to be properly accounted for
+ * in the lists of the respective source particles", §4.5).  Each owner keeps
+ * the tangential history of its own ordered pairs, ghost partners included,
+ * so between rebuilds nothing but the ghosts' x, v, omega travels
+ * (pm_dist_refresh_pvw_*, 48 B per ghost).  At a rebuild:
+ *   pm_dist_plan(MIGRATE) also saves every local row with its histories and
+ *   partner gids; pm_dist_pack(PM_MSG_MIGRATE_HIST) BEFORE pm_dist_pack
+ *   (MIGRATE) writes each leaver's nonzero histories as (partner gid, u_t)
+ *   pairs (same list and order as MIGRATE: the caller ships both with the
+ *   same counts); pm_dist_unpack(MIGRATE_HIST) after pm_dist_unpack(MIGRATE);
+ *   pm_dist_finish carries every history onto the new rows by partner gid.
+ * A grain with more than 24 live contacts at a migration raises
+ * PM_E_CAPACITY.  Walls apply on non-decomposed axes only (decomposed axes
+ * are periodic).  pm_dist_dem_init after pm_set_dem, before the first
+ * rebuild; pm_dist_dem_step = contacts + leapfrog of the owned grains
+ * (ghosts carried), need_rebuild as pm_dist_step. */
+pm_status pm_dist_dem_init(pm_ctx ctx);
+pm_status pm_dist_dem_step(pm_ctx ctx, float dt, int32_t *need_rebuild);
+pm_status pm_dist_refresh_pvw_pack(pm_ctx ctx, void *send_dev);
+pm_status pm_dist_refresh_pvw_unpack(pm_ctx ctx, const void *recv_dev);
 
 /* Decomposed WCSPH time stepping (SURVEY §8(f) NEXT-3 "multi-GPU SPH ghosts
  * (vel/rho/P)"; PAPER.md:335 Eq. 2, :358 Verlet scheme with dynamic step

@@ -38,7 +38,13 @@ __global__ void __launch_bounds__(256, 4) k_dem_step(Params P, Bufs B, int n, fl
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int cp = st->cur_pv, ci = st->cur_id;
   bool far = false;
-  if (i < n) {
+  if (i < n && P.dist && (B.kind[ci][i] & kGhostBit)) {
+    // ghost copy of a decomposed context: carried through the buffer flip,
+    // refreshed (x, v, omega) by its owner before the next step
+    B.pos[cp ^ 1][i] = B.pos[cp][i];
+    B.vel[cp ^ 1][i] = B.vel[cp][i];
+    B.omega[cp ^ 1][i] = B.omega[cp][i];
+  } else if (i < n) {
     const float4 *__restrict__ pos = B.pos[cp];
     const float4 *__restrict__ vel = B.vel[cp];
     const float4 *__restrict__ om = B.omega[cp];
@@ -175,6 +181,7 @@ __global__ void __launch_bounds__(256) k_dem_save(Bufs B, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i <= (n + 31) / 32) B.slice_off_old[i] = B.slice_off[i];
   if (i >= n) return;
+  if (B.gid_old) B.gid_old[i] = B.gid[st->cur_id][i];  // decomposed: partners by gid
   const int cnt = B.cnt[i];
   B.cnt_old[i] = cnt;
   const int64_t base = nbr_row_base(B, i);
@@ -226,6 +233,105 @@ __global__ void __launch_bounds__(256) k_dem_remap(Bufs B, int n) {
   }
 }
 
+// Decomposed DEM ("collisions involving ghost particles need to
+// be properly accounted for in the lists of the respective source
+// particles"): a grain that migrates takes its contact histories along, as
+// (partner gid, u_t) pairs next to its migration record (PM_MSG_MIGRATE_HIST,
+// same list and order as PM_MSG_MIGRATE).  Contacts with ghosts are kept by
+// each owner for its own ordered pair, so nothing else travels.
+struct DemHistEntry {
+  long long gid;
+  float ux, uy, uz, pad;
+};
+struct DemHistRec {
+  long long gid;
+  int n, pad;
+  DemHistEntry e[kDemHist];
+};
+
+__global__ void __launch_bounds__(256) k_dem_hist_pack(Bufs B, const int *__restrict__ list,
+                                                        int nsend, DemHistRec *__restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nsend) return;
+  State *st = B.st;
+  const int ci = st->cur_id;
+  const int i = list[e];
+  const int64_t *g = B.gid[ci];
+  DemHistRec &r = out[e];
+  r.gid = g[i];
+  r.pad = 0;
+  int m = 0;
+  const int64_t base = nbr_row_base(B, i);
+  for (int k = 0; k < B.cnt[i]; ++k) {
+    const int64_t slot = base + ((int64_t)k << 5);
+    const float4 h = B.hist[slot];
+    if (h.x == 0.f && h.y == 0.f && h.z == 0.f) continue;
+    if (m == kDemHist) {
+      raise_error(st, -9 /*PM_E_CAPACITY*/, (long long)g[i]);
+      break;
+    }
+    r.e[m].gid = g[B.nbr[slot]];
+    r.e[m].ux = h.x;
+    r.e[m].uy = h.y;
+    r.e[m].uz = h.z;
+    r.e[m].pad = 0.f;
+    ++m;
+  }
+  r.n = m;
+}
+
+// After a decomposed rebuild: new particle i came from pre-sort index
+// q = perm[i] = a stayer (pre-migration index stay_old[q], rows saved by
+// k_dem_save) or arrival q - n_stay (its DemHistRec); ghosts have no row.
+__global__ void __launch_bounds__(256) k_dem_remap_dist(Bufs B, int n,
+                                                         const int *__restrict__ stay_old,
+                                                         int n_stay,
+                                                         const DemHistRec *__restrict__ hin,
+                                                         int n_arr) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  State *st = B.st;
+  if (i >= n || st->abort) return;
+  const int ci = st->cur_id;
+  if (B.kind[ci][i] & kGhostBit) return;
+  const int q = B.perm[i];
+  const int64_t *gnew = B.gid[ci];
+  const int64_t base = nbr_row_base(B, i);
+  const int cnt = B.cnt[i];
+  if (q < n_stay) {
+    const int o = stay_old[q];
+    const int64_t obase = B.slice_off_old[o >> 5] * 32 + (o & 31);
+    const int ocnt = B.cnt_old[o];
+    for (int k = 0; k < cnt; ++k) {
+      const int64_t slot = base + ((int64_t)k << 5);
+      const int64_t gj = gnew[B.nbr[slot]];
+      float4 h = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int t = 0; t < ocnt; ++t) {
+        const int64_t os = obase + ((int64_t)t << 5);
+        if (B.gid_old[B.nbr_old[os]] == gj) {
+          h = B.hist_old[os];
+          break;
+        }
+      }
+      B.hist[slot] = h;
+    }
+  } else {
+    const int a = q - n_stay;
+    const DemHistRec *r = (a < n_arr) ? hin + a : nullptr;
+    const int m = r ? r->n : 0;
+    for (int k = 0; k < cnt; ++k) {
+      const int64_t slot = base + ((int64_t)k << 5);
+      const int64_t gj = gnew[B.nbr[slot]];
+      float4 h = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int t = 0; t < m; ++t)
+        if (r->e[t].gid == gj) {
+          h = make_float4(r->e[t].ux, r->e[t].uy, r->e[t].uz, 0.f);
+          break;
+        }
+      B.hist[slot] = h;
+    }
+  }
+}
+
 inline unsigned nb(int64_t n) { return (unsigned)((n + 255) / 256); }
 
 }  // namespace
@@ -240,6 +346,20 @@ void launch_dem_remap(const Bufs &B, int64_t n, cudaStream_t s) {
 
 void launch_dem_save(const Bufs &B, int64_t n, cudaStream_t s) {
   if (n > 0) k_dem_save<<<nb(n + 64), 256, 0, s>>>(B, (int)n);
+}
+
+int dem_hist_record_bytes() { return (int)sizeof(DemHistRec); }
+
+void launch_dem_hist_pack(const Bufs &B, const int *list, int nsend, void *out, cudaStream_t s) {
+  if (nsend > 0)
+    k_dem_hist_pack<<<nb(nsend), 256, 0, s>>>(B, list, nsend, reinterpret_cast<DemHistRec *>(out));
+}
+
+void launch_dem_remap_dist(const Bufs &B, int64_t n, const int *stay_old, int n_stay,
+                           const void *hist_in, int n_arr, cudaStream_t s) {
+  if (n > 0)
+    k_dem_remap_dist<<<nb(n), 256, 0, s>>>(B, (int)n, stay_old, n_stay,
+                                           reinterpret_cast<const DemHistRec *>(hist_in), n_arr);
 }
 
 void launch_dem_step_begin(const Bufs &B, cudaGraphConditionalHandle h, cudaStream_t s) {

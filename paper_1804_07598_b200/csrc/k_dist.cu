@@ -189,10 +189,11 @@ __global__ void __launch_bounds__(kDirBlock) k_dist_fill(const uint32_t *__restr
   }
 }
 
-// migration record: pos, vel, vold, gid, kind (64 B; vold is the SPH stepping
-// state, zero when none is allocated); ghost record: pos, gid, kind (32 B)
+// migration record: pos, vel, aux, gid, kind (64 B; aux is the SPH stepping
+// state v_old, or the DEM angular velocity, zero otherwise); ghost record:
+// pos, gid, kind (32 B)
 struct MigRec {
-  float4 pos, vel, vold;
+  float4 pos, vel, aux;
   long long gid;
   int kind, pad;
 };
@@ -213,7 +214,9 @@ __global__ void k_dist_pack(Bufs B, int what, const int *__restrict__ list, int 
     MigRec r;
     r.pos = B.pos[cp][i];
     r.vel = B.vel[cp][i];
-    r.vold = B.vold[ci] ? B.vold[ci][i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    r.aux = B.vold[ci]    ? B.vold[ci][i]
+            : B.omega[cp] ? B.omega[cp][i]
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
     r.gid = B.gid[ci][i];
     r.kind = B.kind[ci][i];
     r.pad = 0;
@@ -241,6 +244,7 @@ __global__ void k_dist_compact(Bufs B, const int *__restrict__ stay, int n_stay)
   B.kind[ci ^ 1][k] = B.kind[ci][j];
   B.rhoP[ci ^ 1][k] = B.rhoP[ci][j];
   if (B.vold[ci]) B.vold[ci ^ 1][k] = B.vold[ci][j];
+  if (B.omega[cp]) B.omega[cp ^ 1][k] = B.omega[cp][j];
 }
 
 __global__ void k_dist_unpack(Bufs B, int what, const void *__restrict__ in, int nrecv, int base) {
@@ -256,11 +260,13 @@ __global__ void k_dist_unpack(Bufs B, int what, const void *__restrict__ in, int
     B.gid[ci][k] = r.gid;
     B.kind[ci][k] = r.kind;
     B.rhoP[ci][k] = make_float2(r.vel.w, r.pos.w);  // an SPH run packs rho, P there
-    if (B.vold[ci]) B.vold[ci][k] = r.vold;
+    if (B.vold[ci]) B.vold[ci][k] = r.aux;
+    else if (B.omega[cp]) B.omega[cp][k] = r.aux;
   } else {
     const GhostRec r = reinterpret_cast<const GhostRec *>(in)[e];
     B.pos[cp][k] = r.pos;
     B.vel[cp][k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (B.omega[cp]) B.omega[cp][k] = make_float4(0.f, 0.f, 0.f, 0.f);
     B.gid[ci][k] = r.gid;
     B.kind[ci][k] = r.kind | kGhostBit;
   }
@@ -287,24 +293,29 @@ __global__ void k_refresh_unpack(Bufs B, const int *__restrict__ ghost_slot, int
 }
 
 // SPH runs (NEXT-3): positions and velocities, with P and rho in their w
-// lanes -- everything the stepping sweep reads of a partner (32 B per ghost)
+// lanes -- everything the stepping sweep reads of a partner (32 B per ghost);
+// DEM runs (W = 3): also the angular velocity (48 B)
+template <int W>
 __global__ void k_refresh_pack_pv(Bufs B, const int *__restrict__ send_idx, int nsend,
                                   float4 *__restrict__ out) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < nsend) {
     const int cp = B.st->cur_pv, i = send_idx[e];
-    out[2 * e] = B.pos[cp][i];
-    out[2 * e + 1] = B.vel[cp][i];
+    out[W * e] = B.pos[cp][i];
+    out[W * e + 1] = B.vel[cp][i];
+    if (W == 3) out[W * e + 2] = B.omega[cp][i];
   }
 }
 
+template <int W>
 __global__ void k_refresh_unpack_pv(Bufs B, const int *__restrict__ ghost_slot, int nghost,
                                     const float4 *__restrict__ in) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < nghost) {
     const int cp = B.st->cur_pv, k = ghost_slot[e];
-    B.pos[cp][k] = in[2 * e];
-    B.vel[cp][k] = in[2 * e + 1];
+    B.pos[cp][k] = in[W * e];
+    B.vel[cp][k] = in[W * e + 1];
+    if (W == 3) B.omega[cp][k] = in[W * e + 2];
   }
 }
 
@@ -313,8 +324,15 @@ inline unsigned nb(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t);
 }  // namespace
 
 int dist_record_bytes(int what) {
-  return what == 0 ? (int)sizeof(MigRec) : what == 1 ? (int)sizeof(GhostRec)
-                                                     : what == 2 ? 16 : what == 3 ? 32 : -1;
+  switch (what) {
+    case 0: return (int)sizeof(MigRec);
+    case 1: return (int)sizeof(GhostRec);
+    case 2: return 16;
+    case 3: return 32;
+    case 4: return 48;
+    case 5: return dem_hist_record_bytes();
+    default: return -1;
+  }
 }
 
 void launch_dist_plan(const Params &P, const Bufs &B, const Dist &D, int n_owned, int what,
@@ -354,13 +372,14 @@ void launch_refresh_pack(const Bufs &B, const int *send_idx, int nsend, void *ou
     k_refresh_pack<<<nb(nsend), 256, 0, s>>>(B, send_idx, nsend, reinterpret_cast<float4 *>(out));
 }
 
-void launch_refresh_pv(const Bufs &B, int pack, const int *idx, int m, void *buf,
+void launch_refresh_pv(const Bufs &B, int pack, const int *idx, int m, void *buf, int with_w,
                        cudaStream_t s) {
   if (m <= 0) return;
-  if (pack)
-    k_refresh_pack_pv<<<nb(m), 256, 0, s>>>(B, idx, m, reinterpret_cast<float4 *>(buf));
-  else
-    k_refresh_unpack_pv<<<nb(m), 256, 0, s>>>(B, idx, m, reinterpret_cast<const float4 *>(buf));
+  float4 *f = reinterpret_cast<float4 *>(buf);
+  if (pack && with_w) k_refresh_pack_pv<3><<<nb(m), 256, 0, s>>>(B, idx, m, f);
+  else if (pack) k_refresh_pack_pv<2><<<nb(m), 256, 0, s>>>(B, idx, m, f);
+  else if (with_w) k_refresh_unpack_pv<3><<<nb(m), 256, 0, s>>>(B, idx, m, f);
+  else k_refresh_unpack_pv<2><<<nb(m), 256, 0, s>>>(B, idx, m, f);
 }
 
 void launch_refresh_unpack(const Bufs &B, const int *ghost_slot, int nghost, const void *in,

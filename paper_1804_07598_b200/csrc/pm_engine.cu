@@ -80,6 +80,13 @@ struct pm_ctx_s {
   long long *d_tot = nullptr, *h_tot = nullptr;
   int64_t mask_cap = 0, blk_cap = 0, list_cap = 0, send_cap = 0, gslot_cap = 0;
   int plan_what = -1;
+  // decomposed DEM: the stay list of the last migration (pre-migration
+  // indices), arrivals' contact histories, saved-rows flag
+  int *d_stay_old = nullptr;
+  int64_t stay_cap = 0, n_stay_old = 0, gid_old_cap = 0;
+  char *d_hist_in = nullptr;
+  int64_t hist_in_cap = 0, n_arr = 0;
+  bool dem_saved = false;
   int64_t plan_send = 0, plan_stay = 0, n_send = 0;
 
   // profiling
@@ -250,6 +257,12 @@ pm_status ensure_particles(pm_ctx c, int64_t n, int64_t keep = 0) {
   CUDA_TRY(c, dalloc(&B.rhoP[1], cap));
   for (int b = 0; b < 2; ++b)  // SPH stepping state (allocated by the first SPH run)
     if (B.vold[b]) CUDA_TRY(c, grow_keep(&B.vold[b], cap, keep, c->stream));
+  if (B.omega[0] && c->dem_pcap == c->pcap) {  // DEM state (pm_dem_run / pm_dist_dem_init)
+    for (int b = 0; b < 2; ++b) CUDA_TRY(c, grow_keep(&B.omega[b], cap, keep, c->stream));
+    CUDA_TRY(c, dalloc(&B.torque, cap));
+    CUDA_TRY(c, grow_keep(&B.cnt_old, cap, c->pcap, c->stream));  // saved pre-migration counts
+    c->dem_pcap = cap;
+  }
   if (B.drho) CUDA_TRY(c, dalloc(&B.drho, cap));
   CUDA_TRY(c, dalloc(&B.cell_of, cap));
   CUDA_TRY(c, dalloc(&B.slot, cap));
@@ -1444,7 +1457,7 @@ pm_status pm_get_profile(pm_ctx c, double *force_ms, int64_t *force_launches, do
 
 
 int32_t pm_record_bytes(int32_t what) {
-  return (what >= 0 && what <= 3) ? dist_record_bytes(what) : -1;
+  return (what >= 0 && what <= 5) ? dist_record_bytes(what) : -1;
 }
 
 pm_status pm_set_decomposition(pm_ctx c, const int32_t pgrid[3], const int32_t pcoord[3]) {
@@ -1558,16 +1571,48 @@ pm_status pm_dist_plan(pm_ctx c, int32_t what, const int32_t order[26], int64_t 
   c->plan_what = what;
   c->plan_send = send;
   c->plan_stay = c->h_tot[13];
+  if (what == PM_MSG_MIGRATE && c->P.dem_state) {
+    // decomposed DEM: keep the rows, histories and gids of every local index
+    // for k_dem_remap_dist (stayers) before the migration compacts them
+    c->n_arr = 0;
+    c->dem_saved = c->list_valid;
+    if (c->dem_saved) {
+      if ((s = dem_alloc(c, true))) return s;
+      if ((s = ensure_dev(c, &c->B.gid_old, c->gid_old_cap, c->n + 1))) return s;
+      launch_dem_save(c->B, c->n, c->stream);
+    }
+  }
   return PM_OK;
 }
 
 pm_status pm_dist_pack(pm_ctx c, int32_t what, void *send_dev) {
   if (!c) return PM_E_INVAL;
   if (c->sticky) return c->sticky;
+  if (what == PM_MSG_MIGRATE_HIST) {  // before the MIGRATE pack, same list and order
+    if (c->plan_what != PM_MSG_MIGRATE || !c->P.dem_state)
+      return set_err(c, PM_E_STATE, "pm_dist_pack: MIGRATE_HIST needs a DEM MIGRATE plan");
+    cudaSetDevice(c->device);
+    if (c->plan_send > 0 && !send_dev) return set_err(c, PM_E_INVAL, "pm_dist_pack: null buffer");
+    if (c->dem_saved) {
+      launch_dem_hist_pack(c->B, c->d_list, (int)c->plan_send, send_dev, c->stream);
+    } else if (c->plan_send > 0) {  // no list yet: no contact history
+      CUDA_TRY(c, cudaMemsetAsync(send_dev, 0, (size_t)c->plan_send * dem_hist_record_bytes(),
+                                  c->stream));
+    }
+    return check_launch(c, "pm_dist_pack (MIGRATE_HIST)");
+  }
   if (c->plan_what != what) return set_err(c, PM_E_STATE, "pm_dist_pack: no matching plan");
   cudaSetDevice(c->device);
   if (c->plan_send > 0 && !send_dev) return set_err(c, PM_E_INVAL, "pm_dist_pack: null buffer");
   launch_dist_pack(c->B, what, c->d_list, (int)c->plan_send, send_dev, c->stream);
+  if (what == PM_MSG_MIGRATE && c->P.dem_state) {  // pre-migration index of every stayer
+    pm_status s = ensure_dev(c, &c->d_stay_old, c->stay_cap, c->plan_stay + 1);
+    if (s) return s;
+    if (c->plan_stay > 0)
+      CUDA_TRY(c, cudaMemcpyAsync(c->d_stay_old, c->d_list + c->plan_send,
+                                  sizeof(int) * c->plan_stay, cudaMemcpyDeviceToDevice, c->stream));
+    c->n_stay_old = c->dem_saved ? c->plan_stay : 0;
+  }
   if (what == PM_MSG_MIGRATE) {
     // stable compaction of the stayers (list entries after the 26 directions)
     launch_dist_compact(c->B, c->d_list + c->plan_send, (int)c->plan_stay, c->stream);
@@ -1592,6 +1637,23 @@ pm_status pm_dist_pack(pm_ctx c, int32_t what, void *send_dev) {
 pm_status pm_dist_unpack(pm_ctx c, int32_t what, const void *recv_dev, int64_t nrecv) {
   if (!c || nrecv < 0) return PM_E_INVAL;
   if (c->sticky) return c->sticky;
+  if (what == PM_MSG_MIGRATE_HIST) {  // the k-th record belongs to the k-th arrival
+    if (nrecv > 0 && !recv_dev) return set_err(c, PM_E_INVAL, "pm_dist_unpack: null buffer");
+    cudaSetDevice(c->device);
+    const int64_t bytes = nrecv * dem_hist_record_bytes();
+    if ((bytes > c->hist_in_cap)) {
+      if (c->d_hist_in) cudaFree(c->d_hist_in);
+      c->d_hist_in = nullptr;
+      c->hist_in_cap = 0;
+      CUDA_TRY(c, cudaMalloc((void **)&c->d_hist_in, (size_t)(bytes * 5 / 4 + 1024)));
+      c->hist_in_cap = bytes * 5 / 4 + 1024;
+    }
+    if (bytes > 0)
+      CUDA_TRY(c, cudaMemcpyAsync(c->d_hist_in, recv_dev, (size_t)bytes, cudaMemcpyDeviceToDevice,
+                                  c->stream));
+    c->n_arr = nrecv;
+    return check_launch(c, "pm_dist_unpack (MIGRATE_HIST)");
+  }
   if (what != PM_MSG_MIGRATE && what != PM_MSG_GHOST)
     return set_err(c, PM_E_INVAL, "pm_dist_unpack: bad kind");
   if (nrecv > 0 && !recv_dev) return set_err(c, PM_E_INVAL, "pm_dist_unpack: null buffer");
@@ -1622,6 +1684,13 @@ pm_status pm_dist_finish(pm_ctx c) {
   if ((s = ensure_dev(c, &c->d_gslot, c->gslot_cap, c->n_ghost + 1))) return s;
   launch_dist_remap(c->B.invperm, c->d_send_idx, (int)c->n_send, c->d_gslot, (int)c->n_ghost,
                     (int)c->n_owned, c->stream);
+  if (c->P.dem_state) {  // contact histories onto the new rows (stayers and arrivals)
+    if ((s = dem_alloc(c, false))) return s;
+    launch_dem_remap_dist(c->B, c->n, c->d_stay_old, (int)c->n_stay_old, c->d_hist_in,
+                          (int)c->n_arr, c->stream);
+    c->n_stay_old = 0;
+    c->n_arr = 0;
+  }
   return sync_check(c, "pm_dist_finish");
 }
 
@@ -1681,7 +1750,7 @@ pm_status pm_dist_refresh_pv_pack(pm_ctx c, void *send_dev) {
   if (!c) return PM_E_INVAL;
   if (c->sticky) return c->sticky;
   if (c->n_send > 0 && !send_dev) return set_err(c, PM_E_INVAL, "null buffer");
-  launch_refresh_pv(c->B, 1, c->d_send_idx, (int)c->n_send, send_dev, c->stream);
+  launch_refresh_pv(c->B, 1, c->d_send_idx, (int)c->n_send, send_dev, 0, c->stream);
   return check_launch(c, "pm_dist_refresh_pv_pack");
 }
 
@@ -1689,9 +1758,62 @@ pm_status pm_dist_refresh_pv_unpack(pm_ctx c, const void *recv_dev) {
   if (!c) return PM_E_INVAL;
   if (c->sticky) return c->sticky;
   if (c->n_ghost > 0 && !recv_dev) return set_err(c, PM_E_INVAL, "null buffer");
-  launch_refresh_pv(c->B, 0, c->d_gslot, (int)c->n_ghost, const_cast<void *>(recv_dev),
+  launch_refresh_pv(c->B, 0, c->d_gslot, (int)c->n_ghost, const_cast<void *>(recv_dev), 0,
                     c->stream);
   return check_launch(c, "pm_dist_refresh_pv_unpack");
+}
+
+pm_status pm_dist_refresh_pvw_pack(pm_ctx c, void *send_dev) {
+  if (!c) return PM_E_INVAL;
+  if (c->sticky) return c->sticky;
+  if (!c->B.omega[0]) return set_err(c, PM_E_STATE, "pm_dist_refresh_pvw_pack: no DEM state");
+  if (c->n_send > 0 && !send_dev) return set_err(c, PM_E_INVAL, "null buffer");
+  launch_refresh_pv(c->B, 1, c->d_send_idx, (int)c->n_send, send_dev, 1, c->stream);
+  return check_launch(c, "pm_dist_refresh_pvw_pack");
+}
+
+pm_status pm_dist_refresh_pvw_unpack(pm_ctx c, const void *recv_dev) {
+  if (!c) return PM_E_INVAL;
+  if (c->sticky) return c->sticky;
+  if (!c->B.omega[0]) return set_err(c, PM_E_STATE, "pm_dist_refresh_pvw_unpack: no DEM state");
+  if (c->n_ghost > 0 && !recv_dev) return set_err(c, PM_E_INVAL, "null buffer");
+  launch_refresh_pv(c->B, 0, c->d_gslot, (int)c->n_ghost, const_cast<void *>(recv_dev), 1,
+                    c->stream);
+  return check_launch(c, "pm_dist_refresh_pvw_unpack");
+}
+
+pm_status pm_dist_dem_init(pm_ctx c) {
+  pm_status s = check_ready(c);
+  if (s) return s;
+  if (!c->have_dem) return set_err(c, PM_E_STATE, "pm_set_dem not called");
+  if (!c->dist) return set_err(c, PM_E_STATE, "pm_dist_dem_init: decomposed contexts only");
+  if (!(c->skin > 0.f)) return set_err(c, PM_E_INVAL, "pm_dist_dem_init: needs a Verlet skin > 0");
+  cudaSetDevice(c->device);
+  if (!c->P.dem_state) {  // the cell sort, migration and refresh now carry omega
+    c->P.dem_state = 1;
+    destroy_graph(c);
+  }
+  if ((s = dem_alloc(c, false))) return s;
+  return check_launch(c, "pm_dist_dem_init");
+}
+
+pm_status pm_dist_dem_step(pm_ctx c, float dt, int32_t *need_rebuild) {
+  pm_status s = check_ready(c);
+  if (s) return s;
+  if (!c->dist || !c->P.dem_state)
+    return set_err(c, PM_E_STATE, "pm_dist_dem_step: call pm_dist_dem_init first");
+  if (!c->list_valid) return set_err(c, PM_E_STATE, "pm_dist_dem_step: no Verlet list");
+  if (!(dt > 0.f)) return set_err(c, PM_E_INVAL, "pm_dist_dem_step: dt must be > 0");
+  cudaSetDevice(c->device);
+  launch_dem_step(c->P, c->B, c->n, dt, c->stream);
+  k_apply_pending<<<1, 1, 0, c->stream>>>(c->B.st);
+  c->forces_valid = false;
+  if (need_rebuild) {
+    if ((s = sync_check(c, "pm_dist_dem_step"))) return s;
+    *need_rebuild = c->st_h->need_rebuild;
+    k_clear_rebuild<<<1, 1, 0, c->stream>>>(c->B.st);
+  }
+  return check_launch(c, "pm_dist_dem_step");
 }
 
 pm_status pm_dist_sph_init(pm_ctx c) {

@@ -125,6 +125,7 @@ struct Bufs {
   int32_t *nbr_old;    // previous list (rows, layout, lengths) for the history remap
   int64_t *slice_off_old;
   int32_t *cnt_old;
+  int64_t *gid_old;    // decomposed DEM: gid of every local index before a rebuild
   int32_t *cell_of;    // cell id in the storage order the build started from
   int32_t *slot;       // unordered slot within the cell (atomic claim)
   int32_t *count;      // [ncell]
@@ -326,6 +327,11 @@ void launch_ke(const Params &P, const Bufs &B, int64_t n, cudaStream_t s);
 void launch_sph_density(const Params &P, const Bufs &B, int64_t n, cudaStream_t s);
 void launch_sph_forces(const Params &P, const Bufs &B, int64_t n, cudaStream_t s);
 void launch_sph_init_run(const Bufs &B, int64_t n, cudaStream_t s);
+constexpr int kDemHist = 24;  // contacts a migrating grain carries (PM_MSG_MIGRATE_HIST)
+int dem_hist_record_bytes();
+void launch_dem_hist_pack(const Bufs &B, const int *list, int nsend, void *out, cudaStream_t s);
+void launch_dem_remap_dist(const Bufs &B, int64_t n, const int *stay_old, int n_stay,
+                           const void *hist_in, int n_arr, cudaStream_t s);
 void launch_dem_step(const Params &P, const Bufs &B, int64_t n, float dt, cudaStream_t s);
 void launch_dem_remap(const Bufs &B, int64_t n, cudaStream_t s);
 void launch_dem_save(const Bufs &B, int64_t n, cudaStream_t s);
@@ -354,7 +360,7 @@ void launch_dist_remap(const int *invperm, int *send_idx, int nsend, int *ghost_
                        int n_owned, cudaStream_t s);
 void launch_refresh_pack(const Bufs &B, const int *send_idx, int nsend, void *out,
                          cudaStream_t s);
-void launch_refresh_pv(const Bufs &B, int pack, const int *idx, int m, void *buf,
+void launch_refresh_pv(const Bufs &B, int pack, const int *idx, int m, void *buf, int with_w,
                        cudaStream_t s);
 void launch_refresh_unpack(const Bufs &B, const int *ghost_slot, int nghost, const void *in,
                            cudaStream_t s);

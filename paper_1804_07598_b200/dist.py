@@ -295,6 +295,7 @@ class DistSim:
         self.dt = dt
         self.loop = isinstance(transport, LoopbackTransport)
         self.multi = hasattr(transport, "exchange_all")  # all local members at once
+        self.dem = False      # DEM runs: migrations carry contact histories
         self.ghost_seg = {}   # rank -> {peer: (off, n)} of the last ghost plan (send side)
         self.ghost_recv = {}  # rank -> {peer: n} received ghosts
         self.rebuilds = 0
@@ -330,31 +331,49 @@ class DistSim:
         """plan -> pack -> counts -> exchange -> unpack for MIGRATE / GHOST."""
         from . import pm
         rb = pm.record_bytes(what)
+        dem = self.dem and what == pm.PM_MSG_MIGRATE
+        hb = pm.record_bytes(pm.PM_MSG_MIGRATE_HIST) if dem else 0
+        hist_sends = {} if dem else None
         sends, seg, counts = {}, {}, {}
         for r, ctx in self.m.items():
             cnt = ctx.dist_plan(what, self.D.send_order(r))
             seg[r] = self.D.segments(r, cnt)
             nsend = sum(n for _, n in seg[r].values())
+            if dem:  # before the MIGRATE pack removes the leavers
+                hbuf = self._buf(("hsend", r), nsend * hb)
+                ctx.dist_pack(pm.PM_MSG_MIGRATE_HIST, hbuf if nsend else None)
+                hist_sends[r] = {p: hbuf[o * hb:(o + n) * hb] for p, (o, n) in seg[r].items()}
             buf = self._buf(("send", what, r), nsend * rb)
             ctx.dist_pack(what, buf if nsend else None)
             sends[r] = {p: buf[o * rb:(o + n) * rb] for p, (o, n) in seg[r].items()}
             counts[r] = {p: n for p, (o, n) in seg[r].items()}
         recv_counts = self._exchange_counts(counts)
-        recvs, rbufs = {}, {}
-        for r in self.m:
-            peers = self.D.peers(r)
-            tot = sum(recv_counts[r][p] for p in peers)
-            buf = self._buf(("recv", what, r), tot * rb)
-            rbufs[r] = (buf, tot)
-            off, recvs[r] = 0, {}
-            for p in peers:  # arrivals concatenated in peer order
-                n = recv_counts[r][p]
-                recvs[r][p] = buf[off * rb:(off + n) * rb]
-                off += n
+
+        def recv_bufs(kind, rsz):
+            recvs, rbufs = {}, {}
+            for r in self.m:
+                peers = self.D.peers(r)
+                tot = sum(recv_counts[r][p] for p in peers)
+                buf = self._buf(("recv", kind, r), tot * rsz)
+                rbufs[r] = (buf, tot)
+                off, recvs[r] = 0, {}
+                for p in peers:  # arrivals concatenated in peer order
+                    n = recv_counts[r][p]
+                    recvs[r][p] = buf[off * rsz:(off + n) * rsz]
+                    off += n
+            return recvs, rbufs
+
+        recvs, rbufs = recv_bufs(what, rb)
         self._exchange(sends, recvs)
         for r, ctx in self.m.items():
             buf, tot = rbufs[r]
             ctx.dist_unpack(what, buf if tot else None, tot)
+        if hist_sends is not None:  # DEM: the leavers' contact histories, same counts
+            recvs, rbufs = recv_bufs(pm.PM_MSG_MIGRATE_HIST, hb)
+            self._exchange(hist_sends, recvs)
+            for r, ctx in self.m.items():
+                buf, tot = rbufs[r]
+                ctx.dist_unpack(pm.PM_MSG_MIGRATE_HIST, buf if tot else None, tot)
         if what == pm.PM_MSG_GHOST:
             self.ghost_seg = seg
             self.ghost_recv = recv_counts
@@ -377,8 +396,9 @@ class DistSim:
 
     def _refresh(self, pv=False):
         """Ghost refresh with the last ghost plan's layout: positions only
-        (16 B per ghost), or positions and velocities (pv, 32 B: SPH runs)."""
-        rsz = 32 if pv else 16
+        (16 B per ghost), positions and velocities (pv, 32 B: SPH runs), or
+        also angular velocities (pv="pvw", 48 B: DEM runs)."""
+        rsz = {False: 16, True: 32, "pv": 32, "pvw": 48}[pv]
         sends, recvs = {}, {}
         for r, ctx in self.m.items():
             nsend = sum(n for _, n in self.ghost_seg[r].values())
@@ -439,6 +459,31 @@ class DistSim:
         v = min(vals.values())
         return v if self.loop else self.tr.allreduce_min_f32(v)
 
+    def dem_start(self):
+        """After pm_place and pm_set_dem on every member: DEM state, first
+        decomposition, ghosts with velocities and angular velocities."""
+        self.dem = True
+        with self._ctxmgr():
+            for ctx in self.m.values():
+                ctx.dist_dem_init()
+            self._rebuild()
+            self._refresh(pv="pvw")
+
+    def dem_run(self, nsteps, dt):
+        """nsteps decomposed DEM steps (pm.h pm_dist_dem_*): contacts +
+        leapfrog of the owned grains -> rebuild when any rank asks (contact
+        histories migrate with their grains) -> ghost refresh (x, v, omega).
+        Returns the number of rebuilds."""
+        reb = 0
+        with self._ctxmgr():
+            for _ in range(nsteps):
+                flag = self._allreduce_max({r: ctx.dist_dem_step(dt) for r, ctx in self.m.items()})
+                if flag:
+                    self._rebuild()
+                    reb += 1
+                self._refresh(pv="pvw")
+        return reb
+
     def sph_start(self):
         """After pm_place, pm_set_sph and pm_set_rho on every member: start
         the SPH Verlet state, first decomposition, ghosts with velocities."""
@@ -478,10 +523,10 @@ class DistSim:
 
 
 def make_member(system, decomp, rank, device=0, stream=None, rc=2.5, skin=0.3, r_min=0.0,
-                sph=None):
+                sph=None, dem=None):
     """A DistContext for `rank` of `decomp`, with the rank's particles of
-    `system` (an inputs.System) placed; `sph`: WCSPH parameters (pm_set_sph)
-    instead of the LJ ones."""
+    `system` (an inputs.System) placed; `sph` / `dem`: WCSPH / DEM parameters
+    (pm_set_sph / pm_set_dem) instead of the LJ ones."""
     from . import pm
     # `stream`: the torch.cuda.Stream the DistSim will run on (never the
     # legacy default stream, whose handle 0 would mean "library-owned stream")
@@ -491,6 +536,8 @@ def make_member(system, decomp, rank, device=0, stream=None, rc=2.5, skin=0.3, r
     ctx.set_cutoff(rc, skin)
     if sph is not None:
         ctx.set_sph(sph)
+    elif dem is not None:
+        ctx.set_dem(dem)
     else:
         ctx.set_lj(1.0, 1.0, 1.0, r_min)
     if decomp.cuts is None:

@@ -240,7 +240,8 @@ def random_box(n: int, L: float, key, periodic=(1, 1, 1)) -> System:
 DEM_G = 9.81
 
 
-def dem_avalanche(nx=147, ny=105, nz=44, incline_deg=30.0, key=(71,), vjit=0.01) -> System:
+def dem_avalanche(nx=147, ny=105, nz=44, incline_deg=30.0, key=(71,), vjit=0.01,
+                  gap=1e-3) -> System:
     """DEM avalanche down an inclined plane (PAPER.md:540-548 §4.5, Figs. 10-11;
     reading R34 in DESIGN.md): grains of radius R = 0.06 on a Cartesian
     lattice of spacing a = 2R (1 + 1e-3) (no initial overlap) filling
@@ -251,9 +252,10 @@ def dem_avalanche(nx=147, ny=105, nz=44, incline_deg=30.0, key=(71,), vjit=0.01)
     floor, free +z, periodic y (length ny a); gravity rotated by the
     incline about y.  Velocities U(-vjit, vjit) break the lattice symmetry.
     params: the Silbert constants of P:540 (k_n, k_t read x1000, R34) and
-    mu = 0.5, gamma_t = 0 (R31-R32), dt = 2e-4, skin = 0.02."""
+    mu = 0.5, gamma_t = 0 (R31-R32), dt = 2e-4, skin = 0.02.  `gap` widens the
+    lattice spacing to 2R (1 + gap) (loose starts for the multi-GPU tests)."""
     R = 0.06
-    a = 2.0 * R * (1.0 + 1e-3)
+    a = 2.0 * R * (1.0 + gap)
     g = np.stack(np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij"), -1)
     xyz = (g.reshape(-1, 3).astype(np.float64) + 0.5) * a
     n = xyz.shape[0]

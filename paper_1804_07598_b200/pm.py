@@ -113,6 +113,10 @@ def lib(path: str = LIB_PATH):
         "pm_dist_refresh_unpack": (st, [vp, vp]),
         "pm_dist_step": (st, [vp, C.c_float, C.c_int32, vp]),
         "pm_set_newton": (st, [vp, C.c_int32]),
+        "pm_dist_dem_init": (st, [vp]),
+        "pm_dist_dem_step": (st, [vp, C.c_float, vp]),
+        "pm_dist_refresh_pvw_pack": (st, [vp, vp]),
+        "pm_dist_refresh_pvw_unpack": (st, [vp, vp]),
         "pm_dist_sph_init": (st, [vp]),
         "pm_dist_sph_rates": (st, [vp, vp]),
         "pm_dist_sph_update": (st, [vp, C.c_float, C.c_float, C.c_int32, vp]),
@@ -256,7 +260,8 @@ class Context:
         return int(reb.value)
 
     def get_dem(self):
-        n = self.count()["n_owned"]
+        c = self.count()
+        n = c["n_owned"] + c["n_ghost"]  # local rows incl. ghost copies, as get_state
         w = np.zeros((n, 4), np.float32)
         t = np.zeros((n, 4), np.float32)
         self._check(self.L.pm_get_dem(self.h, w.ctypes.data, t.ctypes.data))
@@ -358,6 +363,7 @@ class Context:
 
 
 PM_MSG_MIGRATE, PM_MSG_GHOST, PM_MSG_REFRESH, PM_MSG_REFRESH_PV = 0, 1, 2, 3
+PM_MSG_REFRESH_PVW, PM_MSG_MIGRATE_HIST = 4, 5
 PM_PHASE_PROLOGUE, PM_PHASE_STEP, PM_PHASE_FINAL, PM_PHASE_FORCES = 0, 1, 2, 3
 GHOST_BIT = 1 << 30
 
@@ -404,12 +410,25 @@ class DistContext(Context):
         self._check(self.L.pm_dist_finish(self.h))
 
     def refresh_pack(self, send, pv=False):
-        f = self.L.pm_dist_refresh_pv_pack if pv else self.L.pm_dist_refresh_pack
+        """pv: False (positions), True / "pv" (+ velocities, SPH), "pvw"
+        (+ angular velocities, DEM)."""
+        f = {False: self.L.pm_dist_refresh_pack, True: self.L.pm_dist_refresh_pv_pack,
+             "pv": self.L.pm_dist_refresh_pv_pack, "pvw": self.L.pm_dist_refresh_pvw_pack}[pv]
         self._check(f(self.h, _dev_ptr(send)))
 
     def refresh_unpack(self, recv, pv=False):
-        f = self.L.pm_dist_refresh_pv_unpack if pv else self.L.pm_dist_refresh_unpack
+        f = {False: self.L.pm_dist_refresh_unpack, True: self.L.pm_dist_refresh_pv_unpack,
+             "pv": self.L.pm_dist_refresh_pv_unpack,
+             "pvw": self.L.pm_dist_refresh_pvw_unpack}[pv]
         self._check(f(self.h, _dev_ptr(recv)))
+
+    def dist_dem_init(self):
+        self._check(self.L.pm_dist_dem_init(self.h))
+
+    def dist_dem_step(self, dt):
+        f = C.c_int32(0)
+        self._check(self.L.pm_dist_dem_step(self.h, float(dt), C.byref(f)))
+        return int(f.value)
 
     def dist_sph_init(self):
         self._check(self.L.pm_dist_sph_init(self.h))

@@ -318,3 +318,63 @@ def test_sph_stepping_protocol_gloo_world2():
         assert reb == 1
         assert t == pytest.approx(0.5 * sum(expect))
         assert refreshed == [float(1 - r)]
+
+
+class FakeDEMCtx(FakeCtx):
+    """FakeCtx that also packs the MIGRATE_HIST records of a DEM migration:
+    (1000 + rank, direction, k) for the k-th leaver towards each direction."""
+
+    def dist_pack(self, what, buf):
+        import torch
+        from paper_1804_07598_b200 import pm
+        if what == pm.PM_MSG_MIGRATE_HIST:
+            cnt, order = self.counts[pm.PM_MSG_MIGRATE]
+            recs = [(1000 + self.rank, d, k) for d in order for k in range(int(cnt[d]))]
+            if recs:
+                arr = torch.tensor(recs, dtype=torch.int64).flatten()
+                buf.view(torch.int64)[:arr.numel()] = arr
+            return
+        super().dist_pack(what, buf)
+
+
+def _dem_worker(rank, world, port, grid, out):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1804_07598_b200.pm as pmm
+    pmm.record_bytes = lambda what: 24
+    D = Decomp(grid)
+    ctx = FakeDEMCtx(rank, D, rng_key=(31, rank))
+    sim = DistSim(D, {rank: ctx}, TorchTransport(device=None), device="cpu")
+    sim.dem = True
+    sim._message_round(pmm.PM_MSG_MIGRATE)
+    out.put((rank, ctx.arrived[pmm.PM_MSG_MIGRATE], ctx.arrived[pmm.PM_MSG_MIGRATE_HIST]))
+    dist.destroy_process_group()
+
+
+def test_dem_migration_histories_ride_with_grains_gloo_world2():
+    """A decomposed DEM migration round over world-size-2 gloo: the contact
+    history records (PM_MSG_MIGRATE_HIST) use the MIGRATE counts and
+    segments, so the k-th history record that arrives belongs to the k-th
+    grain that arrives."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dem_worker, args=(r, 2, port, (2, 1, 1), q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        item = q.get(timeout=120)
+        res[item[0]] = item[1:]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    total = 0
+    for r in (0, 1):
+        mig, hist = res[r]
+        assert len(mig) == len(hist)
+        assert [[a - 1000, d, k] for a, d, k in hist] == mig
+        total += len(mig)
+    assert total > 0
