@@ -23,7 +23,9 @@ __device__ __forceinline__ float dw_shape(float q) {
   return 0.0f;
 }
 
-__device__ __forceinline__ float3 delta3(const Params &P, const float4 &xi, const float4 &xj) {
+template <bool PER>
+__device__ __forceinline__ float3 delta3t(const Params &P, const float4 &xi, const float4 &xj) {
+  if (!PER) return make_float3(__fsub_rn(xj.x, xi.x), __fsub_rn(xj.y, xi.y), __fsub_rn(xj.z, xi.z));
   return make_float3(pair_delta1(xi.x, xj.x, P.box.L[0], P.box.halfL[0], P.box.per[0]),
                      pair_delta1(xi.y, xj.y, P.box.L[1], P.box.halfL[1], P.box.per[1]),
                      pair_delta1(xi.z, xj.z, P.box.L[2], P.box.halfL[2], P.box.per[2]));
@@ -74,6 +76,7 @@ __device__ __forceinline__ void for_row(const int *__restrict__ nb, int cnt, F &
   }
 }
 
+template <bool PER>
 __device__ __forceinline__ double w_of(const Params &P, const float4 &xi, const float4 &xj,
                                        double inv_h) {
   double d[3];
@@ -81,13 +84,14 @@ __device__ __forceinline__ double w_of(const Params &P, const float4 &xi, const 
   for (int a = 0; a < 3; ++a) {
     const float xa = a == 0 ? xi.x : a == 1 ? xi.y : xi.z;
     const float xb = a == 0 ? xj.x : a == 1 ? xj.y : xj.z;
-    d[a] = P.box.per[a] ? (double)pair_delta1(xa, xb, P.box.L[a], P.box.halfL[a], 1)
-                        : (double)xb - (double)xa;
+    d[a] = (PER && P.box.per[a]) ? (double)pair_delta1(xa, xb, P.box.L[a], P.box.halfL[a], 1)
+                                 : (double)xb - (double)xa;
   }
   const double r = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
   return w_shape64(r * inv_h);
 }
 
+template <bool PER>
 __global__ void __launch_bounds__(256) k_sph_density(Params P, Bufs B, int n) {
   State *st = B.st;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -101,10 +105,10 @@ __global__ void __launch_bounds__(256) k_sph_density(Params P, Bufs B, int n) {
   for_row(nb, cnt, [&](int ja, int jb, int jc, int jd, int rem) {
     const float4 xa = __ldg(pos + ja), xb = __ldg(pos + jb);
     const float4 xc = __ldg(pos + jc), xd = __ldg(pos + jd);
-    s += w_of(P, xi, xa, inv_h);
-    if (rem > 1) s += w_of(P, xi, xb, inv_h);
-    if (rem > 2) s += w_of(P, xi, xc, inv_h);
-    if (rem > 3) s += w_of(P, xi, xd, inv_h);
+    s += w_of<PER>(P, xi, xa, inv_h);
+    if (rem > 1) s += w_of<PER>(P, xi, xb, inv_h);
+    if (rem > 2) s += w_of<PER>(P, xi, xc, inv_h);
+    if (rem > 3) s += w_of<PER>(P, xi, xd, inv_h);
   });
   const double h = P.sph.h;
   const double rho = (double)P.sph.mass / (3.14159265358979323846 * h * h * h) * (1.0 + s);
@@ -121,6 +125,7 @@ __global__ void __launch_bounds__(256) k_sph_density(Params P, Bufs B, int n) {
   if (!isfinite(rho + pr)) raise_error(st, -8 /*PM_E_NONFINITE*/, (long long)B.gid[st->cur_id][i]);
 }
 
+template <bool PER>
 __global__ void __launch_bounds__(256, 3) k_sph_forces(Params P, Bufs B, int n) {
   State *st = B.st;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -141,7 +146,7 @@ __global__ void __launch_bounds__(256, 3) k_sph_forces(Params P, Bufs B, int n) 
   const float acb = P.sph.alpha * P.sph.cbar;
   // gathers of the four pairs first, approximate divisions (as k_sph_rates)
   auto pair = [&](const float4 &xj, const float4 &vj, const float2 &rpj, bool valid) {
-    const float3 d = delta3(P, xi, xj);  // x_j - x_i
+    const float3 d = delta3t<PER>(P, xi, xj);  // x_j - x_i
     const float d2 = dist2(d.x, d.y, d.z);
     const float rinv = fast_rsqrt(d2);
     const float q = d2 * rinv * P.sph.inv_h;
@@ -199,6 +204,7 @@ __device__ __forceinline__ void warp_min_atomic(unsigned *dst, float v) {
   if ((threadIdx.x & 31) == 0) atomicMin(dst, u);
 }
 
+template <bool PER>
 __global__ void __launch_bounds__(256, 3) k_sph_rates(Params P, Bufs B, int n) {
   State *st = B.st;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -220,7 +226,7 @@ __global__ void __launch_bounds__(256, 3) k_sph_rates(Params P, Bufs B, int n) {
     // (memory-level parallelism per thread), and the divisions are the
     // approximate MUFU.RCP kind (no IEEE slow path branching the loop).
     auto pair = [&](const float4 &xj, const float4 &vj, bool valid) {
-      const float3 d = delta3(P, xi, xj);  // x_j - x_i
+      const float3 d = delta3t<PER>(P, xi, xj);  // x_j - x_i
       const float d2 = dist2(d.x, d.y, d.z);
       const float rinv = fast_rsqrt(d2);
       const float q = d2 * rinv * P.sph.inv_h;
@@ -391,12 +397,19 @@ inline unsigned nb(int64_t n) { return (unsigned)((n + 255) / 256); }
 
 }  // namespace
 
+static bool any_periodic(const Params &P) { return P.box.per[0] || P.box.per[1] || P.box.per[2]; }
+
+// non-periodic boxes (the dam break) take the plain pair difference
 void launch_sph_density(const Params &P, const Bufs &B, int64_t n, cudaStream_t s) {
-  if (n > 0) k_sph_density<<<nb(n), 256, 0, s>>>(P, B, (int)n);
+  if (n <= 0) return;
+  if (any_periodic(P)) k_sph_density<true><<<nb(n), 256, 0, s>>>(P, B, (int)n);
+  else k_sph_density<false><<<nb(n), 256, 0, s>>>(P, B, (int)n);
 }
 
 void launch_sph_forces(const Params &P, const Bufs &B, int64_t n, cudaStream_t s) {
-  if (n > 0) k_sph_forces<<<nb(n), 256, 0, s>>>(P, B, (int)n);
+  if (n <= 0) return;
+  if (any_periodic(P)) k_sph_forces<true><<<nb(n), 256, 0, s>>>(P, B, (int)n);
+  else k_sph_forces<false><<<nb(n), 256, 0, s>>>(P, B, (int)n);
 }
 
 void launch_sph_set_rho(const Params &P, const Bufs &B, int64_t n, const float *rho,
@@ -409,7 +422,11 @@ void launch_sph_init_run(const Bufs &B, int64_t n, cudaStream_t s) {
 }
 
 void launch_sph_rates(const Params &P, const Bufs &B, int64_t n, cudaStream_t s) {
-  if (n > 0) k_sph_rates<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, B, (int)n);
+  if (n <= 0) return;
+  if (P.box.per[0] || P.box.per[1] || P.box.per[2])
+    k_sph_rates<true><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, B, (int)n);
+  else
+    k_sph_rates<false><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, B, (int)n);
 }
 
 // dt from `bound` (the global minimum) -> integrate (the caller applies the flip)
@@ -426,7 +443,10 @@ void launch_sph_step(const Params &P, const Bufs &B, int64_t n, float cfl, int e
                      cudaStream_t s) {
   if (n <= 0) return;
   const unsigned nb = (unsigned)((n + 255) / 256);
-  k_sph_rates<<<nb, 256, 0, s>>>(P, B, (int)n);
+  if (P.box.per[0] || P.box.per[1] || P.box.per[2])
+    k_sph_rates<true><<<nb, 256, 0, s>>>(P, B, (int)n);
+  else
+    k_sph_rates<false><<<nb, 256, 0, s>>>(P, B, (int)n);
   k_sph_dt<<<1, 1, 0, s>>>(B.st, cfl, every);
   k_sph_verlet<<<nb, 256, 0, s>>>(P, B, (int)n);
 }
