@@ -62,9 +62,14 @@ class Decomp:
         return (c[0] % px) + px * ((c[1] % py) + py * (c[2] % pz))
 
     def valid_dirs(self):
-        """Directions that exist: no component along an undecomposed axis."""
-        return [d for d, a in enumerate(DIRS)
-                if d != SELF and all(a[k] == 0 or self.grid[k] >= 2 for k in range(3))]
+        """Directions that exist: no component along an undecomposed axis
+        (computed once per grid: the rebuild path asks for it per message)."""
+        key = tuple(self.grid)
+        cache = self.__dict__.setdefault("_vd", {})
+        if key not in cache:
+            cache[key] = [d for d, a in enumerate(DIRS)
+                          if d != SELF and all(a[k] == 0 or self.grid[k] >= 2 for k in range(3))]
+        return cache[key]
 
     def peer(self, rank, d):
         c = self.coord(rank)
@@ -77,17 +82,22 @@ class Decomp:
     def send_order(self, rank):
         """Packing order of the 26 directions: grouped by peer (ascending),
         then by direction index; non-existent directions last (always empty)."""
-        v = self.valid_dirs()
-        order = sorted(v, key=lambda d: (self.peer(rank, d), d))
-        order += [d for d in range(27) if d != SELF and d not in v]
-        return order
+        key = (tuple(self.grid), rank)
+        cache = self.__dict__.setdefault("_so", {})
+        if key not in cache:
+            v = self.valid_dirs()
+            order = sorted(v, key=lambda d: (self.peer(rank, d), d))
+            order += [d for d in range(27) if d != SELF and d not in v]
+            cache[key] = order
+        return list(cache[key])
 
     def segments(self, rank, counts):
         """Per peer: (first record, number of records) of its segment in the
         buffer packed in send_order (counts = per-direction records)."""
         seg, off = {}, 0
+        valid = set(self.valid_dirs())
         for d in self.send_order(rank):
-            if d not in self.valid_dirs():
+            if d not in valid:
                 assert counts[d] == 0
                 continue
             p = self.peer(rank, d)
