@@ -353,6 +353,11 @@ pm_status pm_dist_refresh_unpack(pm_ctx ctx, const void *recv_dev);
  * particle moved more than skin/2 since the last build". */
 pm_status pm_dist_step(pm_ctx ctx, float dt, int32_t phase, int32_t *need_rebuild);
 
+/* Synchronise and return (and clear) the local rebuild flag -- the
+ * need_rebuild of pm_dist_step as a separate call, so a caller can time the
+ * step kernels with events before the host round trip. */
+pm_status pm_dist_read_flag(pm_ctx ctx, int32_t *need_rebuild);
+
 /* Decomposed DEM (SURVEY §8(f) NEXT-4 on the §8(e) decomposition; PAPER.md:
  * 479 "collisions involving ghost particles need to be properly accounted for
  * in the lists of the respective source particles", §4.5).  Each owner keeps

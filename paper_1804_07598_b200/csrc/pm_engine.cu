@@ -1763,6 +1763,15 @@ pm_status pm_dist_refresh_pv_unpack(pm_ctx c, const void *recv_dev) {
   return check_launch(c, "pm_dist_refresh_pv_unpack");
 }
 
+pm_status pm_dist_read_flag(pm_ctx c, int32_t *need_rebuild) {
+  if (!c || !need_rebuild) return PM_E_INVAL;
+  pm_status s = sync_check(c, "pm_dist_read_flag");
+  if (s) return s;
+  *need_rebuild = c->st_h->need_rebuild;
+  k_clear_rebuild<<<1, 1, 0, c->stream>>>(c->B.st);
+  return check_launch(c, "pm_dist_read_flag");
+}
+
 pm_status pm_dist_refresh_pvw_pack(pm_ctx c, void *send_dev) {
   if (!c) return PM_E_INVAL;
   if (c->sticky) return c->sticky;

@@ -306,6 +306,7 @@ class DistSim:
         self.loop = isinstance(transport, LoopbackTransport)
         self.multi = hasattr(transport, "exchange_all")  # all local members at once
         self.dem = False      # DEM runs: migrations carry contact histories
+        self.prof = None      # list: (start, end) CUDA events around each step's sweep
         self.ghost_seg = {}   # rank -> {peer: (off, n)} of the last ghost plan (send side)
         self.ghost_recv = {}  # rank -> {peer: n} received ghosts
         self.rebuilds = 0
@@ -460,8 +461,17 @@ class DistSim:
                 self._refresh()
             last = s == nsteps - 1
             phase = pm.PM_PHASE_FINAL if last else pm.PM_PHASE_STEP
-            flags = {r: ctx.dist_step(self.dt, phase, read_flag=not last)
+            if self.prof is not None:  # CUDA events around the force/VV kernels
+                e0 = self.torch.cuda.Event(enable_timing=True)
+                e1 = self.torch.cuda.Event(enable_timing=True)
+                e0.record(self.stream)
+            flags = {r: ctx.dist_step(self.dt, phase, read_flag=False)
                      for r, ctx in self.m.items()}
+            if self.prof is not None:
+                e1.record(self.stream)
+                self.prof.append((e0, e1))
+            if not last:
+                flags = {r: ctx.read_flag() for r, ctx in self.m.items()}
             flag = 0 if last else self._allreduce_max(flags)
         return reb
 
@@ -708,9 +718,20 @@ def bench_main(args):
     tdist.barrier()
     clk = clocks.stop() if clocks else None
     ms = max_ms(e0.elapsed_time(e1))
-    n_tot = torch.tensor([ctx.count()["n_owned"]], dtype=torch.int64, device=red_dev)
+    cnt = ctx.count()
+    n_tot = torch.tensor([cnt["n_owned"]], dtype=torch.int64, device=red_dev)
     tdist.all_reduce(n_tot)
     n = int(n_tot.item())
+    # dominant kernel (the fused force sweep + VV), a second pass timed with
+    # events around each step's sweep on this rank's stream; max over ranks
+    sim.prof = []
+    sim.run(min(args.steps, 50))
+    torch.cuda.synchronize()
+    sweep_ms = sum(a.elapsed_time(b) for a, b in sim.prof) / len(sim.prof)
+    sim.prof = None
+    sweep_ms = max_ms(sweep_ms)
+    nbar = cnt["nnz"] / max(cnt["n_owned"], 1)
+    alg = cnt["n_owned"] * (4.0 * nbar + 64.0)
     ctx.close()
     # ---- end to end: pinned host state in, K steps, owned state out
     pos_h = torch.from_numpy(s.pos).pin_memory()
@@ -736,6 +757,15 @@ def bench_main(args):
         from bench import METRIC, UNIT  # noqa: E402
         h2d = s.n * (16 + 16 + 8)
         d2h = int(out["pos"].nbytes + out["vel"].nbytes)
+        from bench import hbm_peak  # noqa: E402
+        peak, peak_src = hbm_peak()
+        ach = alg / (sweep_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "traffic": None,
+                "kernel": "k_lj_step (force sweep + fused VV), rank 0 sub-domain",
+                "kernel_ms": sweep_ms, "kernel_share_of_step": sweep_ms / (ms / args.steps),
+                "alg_bytes_per_launch": alg, "alg_bytes_formula": "N_owned*(4*nbar + 64)",
+                "peak_source": peak_src}
         line = {"metric": METRIC, "value": n * args.steps / (ms * 1e-3), "unit": UNIT,
                 "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -745,11 +775,14 @@ def bench_main(args):
                                        f"{D.grid}, ghost width r_cut+skin, NVE",
                            "n_particles": n, "parallelism": f"spatial {D.grid} ({backend})",
                            "rebuilds": reb, "l2": "inputs larger than L2 (Verlet lists)"},
-                "roofline": None, "cpu_baseline": None,
+                "roofline": roof, "cpu_baseline": None,
                 "e2e": {"value": n * args.steps / (e2e_ms * 1e-3), "unit": UNIT,
                         "h2d_bytes_per_step": h2d * ws / args.steps,
                         "d2h_bytes_per_step": d2h * ws / args.steps},
-                "gpu_launches": None, "clocks": clk}
+                # per step: refresh pack + unpack, sweep, flag clear (+1 apply)
+                # = 5; per rebuild: 2 x (plan 4 + pack + unpack) + compact +
+                # flip + build 11 + remap = 26; prologue and start 3
+                "gpu_launches": 5 * args.steps + 26 * reb + 3, "clocks": clk}
         print(json.dumps(line), flush=True)
     tdist.destroy_process_group()
     return 0

@@ -113,6 +113,7 @@ def lib(path: str = LIB_PATH):
         "pm_dist_refresh_unpack": (st, [vp, vp]),
         "pm_dist_step": (st, [vp, C.c_float, C.c_int32, vp]),
         "pm_set_newton": (st, [vp, C.c_int32]),
+        "pm_dist_read_flag": (st, [vp, vp]),
         "pm_dist_dem_init": (st, [vp]),
         "pm_dist_dem_step": (st, [vp, C.c_float, vp]),
         "pm_dist_refresh_pvw_pack": (st, [vp, vp]),
@@ -459,6 +460,11 @@ class DistContext(Context):
     def dist_step(self, dt, phase, read_flag=False):
         f = C.c_int32(0)
         self._check(self.L.pm_dist_step(self.h, dt, phase, C.byref(f) if read_flag else None))
+        return int(f.value)
+
+    def read_flag(self):
+        f = C.c_int32(0)
+        self._check(self.L.pm_dist_read_flag(self.h, C.byref(f)))
         return int(f.value)
 
 
