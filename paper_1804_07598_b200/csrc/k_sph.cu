@@ -13,14 +13,12 @@ namespace pm {
 
 namespace {
 
-// dW/dr / dw_norm
+// dW/dr / dw_norm (branch-free: both pieces evaluated and selected)
 __device__ __forceinline__ float dw_shape(float q) {
-  if (q < 1.0f) return q * fmaf(2.25f, q, -3.0f);
-  if (q < 2.0f) {
-    const float t = 2.0f - q;
-    return -0.75f * t * t;
-  }
-  return 0.0f;
+  const float inner = q * fmaf(2.25f, q, -3.0f);
+  const float t = 2.0f - q;
+  const float outer = -0.75f * t * t;
+  return q < 1.0f ? inner : (q < 2.0f ? outer : 0.0f);
 }
 
 template <bool PER>
@@ -144,7 +142,7 @@ __global__ void __launch_bounds__(256, 3) k_sph_forces(Params P, Bufs B, int n) 
   const int *nb = B.nbr + nbr_row_base(B, i);
   float ax = 0.f, ay = 0.f, az = 0.f;
   const float acb = P.sph.alpha * P.sph.cbar;
-  // gathers of the four pairs first, approximate divisions (as k_sph_rates)
+  // gathers of the four pairs first, one approximate reciprocal per pair (as k_sph_rates)
   auto pair = [&](const float4 &xj, const float4 &vj, const float2 &rpj, bool valid) {
     const float3 d = delta3t<PER>(P, xi, xj);  // x_j - x_i
     const float d2 = dist2(d.x, d.y, d.z);
@@ -153,9 +151,11 @@ __global__ void __launch_bounds__(256, 3) k_sph_forces(Params P, Bufs B, int n) 
     const float dwdr = P.sph.dw_norm * dw_shape(q);
     // v_ij . r_ij with r_ij = x_i - x_j = -d
     const float vr = -((vi.x - vj.x) * d.x + (vi.y - vj.y) * d.y + (vi.z - vj.z) * d.z);
-    const float mu = __fdividef(P.sph.h * vr, d2 + P.sph.eta2);
-    const float pi_ij = vr < 0.0f ? __fdividef(-2.0f * acb * mu, rpi.x + rpj.x) : 0.0f;
-    const float coef = P.sph.mass * (__fdividef(rpi.y + rpj.y, rpi.x * rpj.x) + pi_ij);
+    const float den_mu = d2 + P.sph.eta2, rr = rpi.x * rpj.x, rs = rpi.x + rpj.x;
+    const float rcp = fast_rcp(den_mu * rr * rs);  // the three quotients from one reciprocal
+    const float mu = P.sph.h * vr * (rr * rs) * rcp;
+    const float pi_ij = vr < 0.0f ? -2.0f * acb * mu * (den_mu * rr * rcp) : 0.0f;
+    const float coef = P.sph.mass * ((rpi.y + rpj.y) * (den_mu * rs * rcp) + pi_ij);
     // a_i -= coef * grad_i W,  grad_i W = (x_i - x_j)/r dW/dr = -d rinv dwdr
     const float sc = (valid && q < 2.0f) ? coef * rinv * dwdr : 0.0f;
     ax = fmaf(sc, d.x, ax);
@@ -223,8 +223,9 @@ __global__ void __launch_bounds__(256, 3) k_sph_rates(Params P, Bufs B, int n) {
     const float4 vi = vel[i];
     const float acb = P.sph.alpha * P.sph.cbar;
     // The four pairs' gathers are issued before any of their arithmetic
-    // (memory-level parallelism per thread), and the divisions are the
-    // approximate MUFU.RCP kind (no IEEE slow path branching the loop).
+    // (memory-level parallelism per thread); the three quotients of a pair
+    // come from one approximate reciprocal (no IEEE slow path branching the
+    // loop) and the kernel derivative is branch-free.
     auto pair = [&](const float4 &xj, const float4 &vj, bool valid) {
       const float3 d = delta3t<PER>(P, xi, xj);  // x_j - x_i
       const float d2 = dist2(d.x, d.y, d.z);
@@ -237,9 +238,15 @@ __global__ void __launch_bounds__(256, 3) k_sph_rates(Params P, Bufs B, int n) {
       const float vd = vx * d.x + vy * d.y + vz * d.z;  // = -(v_ij . r_ij)
       const float gsc = rinv * dwdr;
       const float vr = -vd;
-      const float mu = __fdividef(P.sph.h * vr, d2 + P.sph.eta2);
-      const float pi_ij = vr < 0.0f ? __fdividef(-2.0f * acb * mu, vi.w + vj.w) : 0.0f;
-      const float coef = P.sph.mass * (__fdividef(xi.w + xj.w, vi.w * vj.w) + pi_ij);
+      // the three quotients from one reciprocal: 1 / [(d2 + eta2) rho_i rho_j
+      // (rho_i + rho_j)]
+      const float den_mu = d2 + P.sph.eta2, rr = vi.w * vj.w, rs = vi.w + vj.w;
+      const float rcp = fast_rcp(den_mu * rr * rs);
+      const float mu = P.sph.h * vr * (rr * rs) * rcp;       // h vr / (d2 + eta2)
+      const float inv_rr = den_mu * rs * rcp;                // 1 / (rho_i rho_j)
+      const float inv_rs = den_mu * rr * rcp;                // 1 / (rho_i + rho_j)
+      const float pi_ij = vr < 0.0f ? -2.0f * acb * mu * inv_rs : 0.0f;
+      const float coef = P.sph.mass * ((xi.w + xj.w) * inv_rr + pi_ij);
       const float sc = in ? coef * gsc : 0.0f;
       ax = fmaf(sc, d.x, ax);  // a_i -= coef grad_i W
       ay = fmaf(sc, d.y, ay);

@@ -27,3 +27,4 @@ r = c.sph_run(200)
 t1 = time.perf_counter()
 print(os.environ.get("PM_LIB", "default"),
       f"{1e3 * (t1 - t0) / r['steps']:.4f} ms/step rebuilds {r['rebuilds']} dt {r['dt_min']:.4e}")
+print("stepping list entries per particle", c.count()["nnz"] / s.n)
