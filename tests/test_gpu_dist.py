@@ -433,3 +433,33 @@ def test_decomposed_dem_matches_single(env):
     assert np.max(np.abs(dx)) < 3 * np.max(np.abs(dx1)) + 1e-6  # no worse than one context
     for m in members.values():
         m.close()
+
+
+def test_api_state_errors(env):
+    """Call-order and mode errors of the newer entry points report
+    PM_E_STATE (-2) / PM_E_INVAL (-1) instead of running: half lists on a
+    decomposed context, SPH / DEM stepping of a decomposed context before
+    its init, SPH and DEM on half lists, the record size of an unknown kind."""
+    pm, dist = env
+    s = inputs.lj_lattice_system(16, 16, 16, jitter_key=(44,))
+    D = dist.Decomp((2, 1, 1))
+    m = dist.make_member(s.subset(np.where(dist.owner_of(s, D) == 0)[0]), D, 0)
+    for call, code in ((lambda: m.set_newton(True), -2), (lambda: m.dist_sph_rates(), -2),
+                       (lambda: m.dist_sph_update(1e-4), -2), (lambda: m.dist_dem_step(1e-4), -2),
+                       (lambda: m.dist_dem_init(), -2)):
+        with pytest.raises(pm.PMError) as e:
+            call()
+        assert e.value.code == code
+    m.close()
+    assert pm.record_bytes(6) == -1 and pm.record_bytes(-1) == -1
+    assert [pm.record_bytes(k) for k in range(6)] == [64, 32, 16, 32, 48, 592]
+    c = pm.Context()
+    c.set_newton(True)
+    c.set_domain(s.lo, s.hi, s.periodic)
+    c.set_cutoff(2.5, 0.3)
+    c.set_sph(inputs.cfg4(dp=1.0 / 16.0).params)
+    c.place(s.pos, s.vel, s.gid)
+    with pytest.raises(pm.PMError) as e:
+        c.sph_run(2)
+    assert e.value.code == -2
+    c.close()
