@@ -240,8 +240,8 @@ pm_status pm_get_verlet(pm_ctx ctx, int64_t *row_ptr, int64_t *col_gid);
 /* Particle state in the current internal order.  Any pointer may be NULL.
  * force4 holds LJ forces or SPH accelerations (last computed); rho/pres the
  * SPH density and pressure.  The fourth components of pos4/vel4 are carried,
- * not computed: after pm_sph_run they hold the pressure and the density the
- * stepping sweep gathers with the positions and velocities. */
+ * not computed: after pm_sph_forces and pm_sph_run they hold the pressure and
+ * the density the SPH sweeps gather with the positions and velocities. */
 pm_status pm_get_state(pm_ctx ctx, float *pos4, float *vel4, float *force4, int64_t *gid,
                        float *rho, float *pres, int32_t mem);
 

@@ -123,6 +123,8 @@ __global__ void __launch_bounds__(256) k_sph_density(Params P, Bufs B, int n) {
   if (!isfinite(rho + pr)) raise_error(st, -8 /*PM_E_NONFINITE*/, (long long)B.gid[st->cur_id][i]);
 }
 
+// Forces of the pass: rho and P were packed into vel.w and pos.w by
+// k_sph_pack_w (as during a run), so a pair costs two 16-byte gathers.
 template <bool PER>
 __global__ void __launch_bounds__(256, 3) k_sph_forces(Params P, Bufs B, int n) {
   State *st = B.st;
@@ -134,16 +136,14 @@ __global__ void __launch_bounds__(256, 3) k_sph_forces(Params P, Bufs B, int n) 
   }
   const float4 *__restrict__ pos = B.pos[st->cur_pv];
   const float4 *__restrict__ vel = B.vel[st->cur_pv];
-  const float2 *__restrict__ rhoP = B.rhoP[st->cur_id];
   const float4 xi = pos[i];
   const float4 vi = vel[i];
-  const float2 rpi = rhoP[i];
   const int cnt = B.cnt[i];
   const int *nb = B.nbr + nbr_row_base(B, i);
   float ax = 0.f, ay = 0.f, az = 0.f;
   const float acb = P.sph.alpha * P.sph.cbar;
   // gathers of the four pairs first, one approximate reciprocal per pair (as k_sph_rates)
-  auto pair = [&](const float4 &xj, const float4 &vj, const float2 &rpj, bool valid) {
+  auto pair = [&](const float4 &xj, const float4 &vj, bool valid) {
     const float3 d = delta3t<PER>(P, xi, xj);  // x_j - x_i
     const float d2 = dist2(d.x, d.y, d.z);
     const float rinv = fast_rsqrt(d2);
@@ -151,11 +151,11 @@ __global__ void __launch_bounds__(256, 3) k_sph_forces(Params P, Bufs B, int n) 
     const float dwdr = P.sph.dw_norm * dw_shape(q);
     // v_ij . r_ij with r_ij = x_i - x_j = -d
     const float vr = -((vi.x - vj.x) * d.x + (vi.y - vj.y) * d.y + (vi.z - vj.z) * d.z);
-    const float den_mu = d2 + P.sph.eta2, rr = rpi.x * rpj.x, rs = rpi.x + rpj.x;
+    const float den_mu = d2 + P.sph.eta2, rr = vi.w * vj.w, rs = vi.w + vj.w;
     const float rcp = fast_rcp(den_mu * rr * rs);  // the three quotients from one reciprocal
     const float mu = P.sph.h * vr * (rr * rs) * rcp;
     const float pi_ij = vr < 0.0f ? -2.0f * acb * mu * (den_mu * rr * rcp) : 0.0f;
-    const float coef = P.sph.mass * ((rpi.y + rpj.y) * (den_mu * rs * rcp) + pi_ij);
+    const float coef = P.sph.mass * ((xi.w + xj.w) * (den_mu * rs * rcp) + pi_ij);
     // a_i -= coef * grad_i W,  grad_i W = (x_i - x_j)/r dW/dr = -d rinv dwdr
     const float sc = (valid && q < 2.0f) ? coef * rinv * dwdr : 0.0f;
     ax = fmaf(sc, d.x, ax);
@@ -167,18 +167,25 @@ __global__ void __launch_bounds__(256, 3) k_sph_forces(Params P, Bufs B, int n) 
     const float4 xc = __ldg(pos + jc), xd = __ldg(pos + jd);
     const float4 va = __ldg(vel + ja), vb = __ldg(vel + jb);
     const float4 vc = __ldg(vel + jc), vd = __ldg(vel + jd);
-    const float2 ra = __ldg(rhoP + ja), rb = __ldg(rhoP + jb);
-    const float2 rc = __ldg(rhoP + jc), rd = __ldg(rhoP + jd);
-    pair(xa, va, ra, true);
-    pair(xb, vb, rb, rem > 1);
-    pair(xc, vc, rc, rem > 2);
-    pair(xd, vd, rd, rem > 3);
+    pair(xa, va, true);
+    pair(xb, vb, rem > 1);
+    pair(xc, vc, rem > 2);
+    pair(xd, vd, rem > 3);
   });
   ax += P.sph.g[0];
   ay += P.sph.g[1];
   az += P.sph.g[2];
   B.force[i] = make_float4(ax, ay, az, 0.f);
   if (!isfinite(ax + ay + az)) raise_error(st, -8 /*PM_E_NONFINITE*/, (long long)B.gid[st->cur_id][i]);
+}
+
+// rho, P of the pass into the w lanes the force sweep gathers
+__global__ void __launch_bounds__(256) k_sph_pack_w(Bufs B, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float2 rp = B.rhoP[B.st->cur_id][i];
+  B.pos[B.st->cur_pv][i].w = rp.y;
+  B.vel[B.st->cur_pv][i].w = rp.x;
 }
 
 // ---------------------------------------------------------------------------
@@ -415,6 +422,7 @@ void launch_sph_density(const Params &P, const Bufs &B, int64_t n, cudaStream_t 
 
 void launch_sph_forces(const Params &P, const Bufs &B, int64_t n, cudaStream_t s) {
   if (n <= 0) return;
+  k_sph_pack_w<<<nb(n), 256, 0, s>>>(B, (int)n);
   if (any_periodic(P)) k_sph_forces<true><<<nb(n), 256, 0, s>>>(P, B, (int)n);
   else k_sph_forces<false><<<nb(n), 256, 0, s>>>(P, B, (int)n);
 }
