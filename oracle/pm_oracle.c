@@ -20,8 +20,10 @@
  *    reorganise (§2: "Cell Lists [45] or Verlet Lists [46] ...
  *    reduces the computational cost to O(N)").
  *
- * Pins: tests/test_oracle_pins.py.  Functions with no independent pin say
- * "parity unpinned" below (only the SPH viscosity constants, R20).
+ * Pins: tests/test_oracle_pins.py.  Parts with no independent pin say
+ * "parity unpinned" below: the SPH viscosity constants (R20), the SPH time
+ * stepping scheme beyond its self-consistency pins (R26-R28) and the DEM
+ * wall model beyond its closed-form pins (R33).
  */
 #include <math.h>
 #include <stdint.h>
@@ -643,7 +645,9 @@ void orc_sph_run(int64_t n, double *x, double *v, double *rho, const int32_t *ki
 /*   planes at the faces) act like a fixed sphere touching the plane:     */
 /*   normal Hertz force with damping only;  gravity g.                    */
 /*   Leapfrog (Eq. 13): v += dt F/m; x += dt v; w += dt T/I.              */
-/* A contact that ends loses its history.                                 */
+/* A contact that ends loses its history.  Pinned by closed forms (free   */
+/* fall, resting depth on a wall, elastic head-on collision, momentum);   */
+/* the wall model itself (R33) is "parity unpinned" beyond those.         */
 /* ------------------------------------------------------------------ */
 typedef struct {
   int64_t a, b;
