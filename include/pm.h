@@ -60,7 +60,9 @@ enum { PM_HOST = 0, PM_DEVICE = 1 };
 
 typedef struct {
   int32_t device;      /* CUDA device ordinal */
-  int32_t cell_div;    /* cells per r_v along each axis: 1 (side >= r_v) */
+  int32_t cell_div;    /* cells per r_v along each axis (reading R2): 1 (side >= r_v,
+                          27-cell stencil) or 2 (side >= r_v/2, 125-cell stencil;
+                          single-GPU contexts); PM_E_INVAL otherwise */
   int32_t nbr_cap;     /* initial neighbour slots per particle (0 = auto from density) */
   int32_t use_graphs;  /* 1: pm_step_vv runs each step as one CUDA graph launch */
   void *cuda_stream;   /* cudaStream_t to run on; NULL = library-owned stream */

@@ -168,7 +168,8 @@ __global__ void __launch_bounds__(256, 4) k_verlet(Params P, Bufs B, int n) {
       cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
     }
     const int cy = seg_row % ny, cz = seg_row / ny;
-    int xa = cmin - 1, xb = cmax + 1;
+    const int R = P.grid.reach;  // stencil half-width: 1 (27 cells) or 2 (125 cells)
+    int xa = cmin - R, xb = cmax + R;
     // per-pair R4 along x: a run covering a whole periodic x-row, or (a
     // decomposed x) a run touching cells that may hold wrapped particles
     int pmi_x = 0;
@@ -181,14 +182,14 @@ __global__ void __launch_bounds__(256, 4) k_verlet(Params P, Bufs B, int n) {
       xb = nx - 1;
       pmi_x = 1;
     }
-    for (int dz = -1; dz <= 1; ++dz) {
+    for (int dz = -R; dz <= R; ++dz) {
       int qz = cz + dz;
       float shz = 0.f, lz = 0.f;  // candidate shift / own shift along z
       if (qz < 0 || qz >= nz) {
         if (!P.grid.wrap[2]) continue;
         if (qz < 0) { qz += nz; shz = Lz; } else { qz -= nz; lz = Lz; }
       }
-      for (int dy = -1; dy <= 1; ++dy) {
+      for (int dy = -R; dy <= R; ++dy) {
         int qy = cy + dy;
         float shy = 0.f, ly = 0.f;
         if (qy < 0 || qy >= ny) {

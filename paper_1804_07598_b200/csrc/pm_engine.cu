@@ -430,6 +430,9 @@ pm_status setup_grid(pm_ctx c) {
       return set_err(c, PM_E_INVAL,
                      "periodic axis %d: extent %g < 3 r_v = %g (27-cell stencil needs 3 cells)", d,
                      ext, 3.0 * rv);
+    if (P.grid.wrap[d] && nd < 2 * c->cell_div + 1)
+      return set_err(c, PM_E_INVAL, "periodic axis %d: %d cells < %d for the cell_div %d stencil",
+                     d, (int)nd, 2 * c->cell_div + 1, c->cell_div);
     if (nd > (double)(1 << 20)) nd = (double)(1 << 20);
     P.grid.n[d] = (int)nd;
     P.grid.inv_w[d] = (float)(nd / ext);
@@ -438,6 +441,7 @@ pm_status setup_grid(pm_ctx c) {
   }
   if (ncell > (int64_t)1 << 30) return set_err(c, PM_E_INVAL, "too many cells (%lld)", (long long)ncell);
   P.grid.ncell = (int)ncell;
+  P.grid.reach = c->dist ? 1 : c->cell_div;
   c->cells_valid = c->list_valid = c->forces_valid = c->rho_valid = false;
   destroy_graph(c);
   return ensure_cells(c);
@@ -631,7 +635,7 @@ pm_status pm_create(const pm_opts *opts, pm_ctx *out) {
   pm_opts o;
   pm_opts_default(&o);
   if (opts) o = *opts;
-  if (o.cell_div != 1) return PM_E_INVAL;  // only side >= r_v grids are implemented
+  if (o.cell_div != 1 && o.cell_div != 2) return PM_E_INVAL;  // R2: side >= r_v or r_v/2
   pm_ctx c = new (std::nothrow) pm_ctx_s();
   if (!c) return PM_E_NOMEM;
   c->device = o.device;
@@ -1463,6 +1467,8 @@ int32_t pm_record_bytes(int32_t what) {
 pm_status pm_set_decomposition(pm_ctx c, const int32_t pgrid[3], const int32_t pcoord[3]) {
   if (!c || !pgrid || !pcoord) return PM_E_INVAL;
   if (c->P.newton) return set_err(c, PM_E_STATE, "decomposed contexts need full lists");
+  if (c->cell_div != 1)
+    return set_err(c, PM_E_STATE, "decomposed contexts use cell_div 1 (cells >= r_v)");
   if (!c->have_domain || !c->have_cutoff)
     return set_err(c, PM_E_STATE, "pm_set_decomposition: set the domain and cutoff first");
   cudaSetDevice(c->device);

@@ -42,6 +42,7 @@ struct Grid {
   int safe_lo[3], safe_hi[3];  // decomposed axes: cells whose extent lies strictly
                                // inside the global box (no wrapped particle)
   int ncell;
+  int reach;       // stencil half-width in cells: 1 (side >= r_v) or 2 (side >= r_v/2)
 };
 
 // Decomposition of the global periodic box into p[0] x p[1] x p[2] cuboids;

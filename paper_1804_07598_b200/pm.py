@@ -153,12 +153,14 @@ def _ptr(a):
 class Context:
     """One pm_ctx (one GPU, one stream)."""
 
-    def __init__(self, device: int = 0, nbr_cap: int = 0, use_graphs=None, stream=None):
+    def __init__(self, device: int = 0, nbr_cap: int = 0, use_graphs=None, stream=None,
+                 cell_div: int = 1):
         L = lib()
         o = Opts()
         L.pm_opts_default(C.byref(o))  # honours PM_USE_GRAPHS=0
         o.device = device
         o.nbr_cap = nbr_cap
+        o.cell_div = cell_div
         if use_graphs is not None:
             o.use_graphs = 1 if use_graphs else 0
         o.cuda_stream = stream

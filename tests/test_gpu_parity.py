@@ -147,6 +147,45 @@ def test_verlet_small_grids_and_sparse(pm, orc, L, n, per):
     c.close()
 
 
+@pytest.mark.parametrize("per", [(1, 1, 1), (1, 0, 1)])
+def test_cell_div2_cells_lists_forces(pm, orc, per):
+    """Reading R2's second grid (pm_opts.cell_div = 2: cells of side >= r_v/2,
+    5 x 5 x 5 stencil): cell ids / starts / perm bit-exact against the
+    oracle's cell_div = 2 grid, the same Verlet sets as the brute-force
+    oracle, forces within the bar, and a short run that follows the
+    cell_div = 1 one."""
+    s = inputs.random_box(3000, 15.0, (19,), periodic=per)
+    s2 = inputs.lj_lattice_system(14, 14, 14, jitter_key=(18,), vel_key=(118,))
+    c = make_ctx(pm, s, r_min=0.8, cell_div=2)
+    c.build_cells()
+    g = c.get_cells()
+    ref = orc.cell_list(s.pos, s.lo, s.hi, s.periodic, rv=rv32(2.5, 0.3), cell_div=2)
+    assert np.array_equal(g["cell_of"], ref["cell_of"])
+    assert np.array_equal(g["start"], ref["start"])
+    assert np.array_equal(g["perm"], ref["perm"])
+    c.build_verlet()
+    rp, col = c.get_verlet()
+    st = c.get_state()
+    rrp, rcols, _ = orc.verlet_rows(s.pos, s.lo, s.hi, s.periodic, rv32(2.5, 0.3),
+                                    rows=idx_of_gid(s)[st["gid"]], want_shift=False)
+    bad = _row_sets_equal(rp, col, st["gid"], rrp, rcols, s.gid)
+    assert bad < 0, f"row {bad} differs"
+    c.compute_lj()
+    st = c.get_state()
+    fr = orc.lj_rows(s.pos, s.lo, s.hi, s.periodic, rc=2.5, r_min=0.8,
+                     rows=idx_of_gid(s)[st["gid"]])
+    assert orc.normalized_max_err(st["force"][:, :3].astype(np.float64), fr["F"]) <= TOL
+    c.close()
+    out = []
+    for cd in (1, 2):
+        c = make_ctx(pm, s2, cell_div=cd)
+        r = c.step_vv(0.005, 20)
+        out.append((pm.sorted_by_gid(c.get_state()), r["rebuilds"]))
+        c.close()
+    assert out[0][1] == out[1][1]
+    assert np.max(np.abs(out[0][0]["pos"][:, :3] - out[1][0]["pos"][:, :3])) < 1e-4
+
+
 def test_verlet_capacity_overflow_retry(pm, orc):
     """A tiny initial capacity overflows; the library grows it and retries."""
     s = inputs.cfg1()
