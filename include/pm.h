@@ -239,6 +239,14 @@ pm_status pm_get_cells(pm_ctx ctx, int32_t *cell_of, int32_t *cell_start, int32_
  * neighbour).  Caller-allocated. */
 pm_status pm_get_verlet(pm_ctx ctx, int64_t *row_ptr, int64_t *col_gid);
 
+/* Image shift of every entry of pm_get_verlet's CSR (same order): col_shift
+ * [3 * nnz] int8, per axis -1 when the R4 rule moved the partner by -L,
+ * +1 when it moved this particle by -L (partner seen at +L), 0 otherwise
+ * (positions of the last build).  With periodic extents >= 3 r_v a pair has
+ * at most one image, so (gid_i, gid_j, shift) is the list's complete set
+ * description.  Caller-allocated. */
+pm_status pm_get_verlet_shifts(pm_ctx ctx, int8_t *col_shift);
+
 /* Particle state in the current internal order.  Any pointer may be NULL.
  * force4 holds LJ forces or SPH accelerations (last computed); rho/pres the
  * SPH density and pressure.  The fourth components of pos4/vel4 are carried,

@@ -269,11 +269,40 @@ __global__ void __launch_bounds__(256) k_verlet_export(Bufs B, int n,
   for (int k = 0; k < c; ++k) col_gid[row_ptr[i] + k] = gid[nb[k << 5]];
 }
 
+// Image shift of every list entry (R4/R5 sets of (gid_i, gid_j, shift)): per
+// periodic axis -1 / +1 when the pinned rule moved x_j by -L / x_i by -L at
+// the build (positions of the last build, xref), 0 otherwise.
+__global__ void __launch_bounds__(256) k_verlet_shifts(Params P, Bufs B, int n,
+                                                      const int64_t *__restrict__ row_ptr,
+                                                      int8_t *__restrict__ col_shift) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int *nb = B.nbr + nbr_row_base(B, i);
+  const int c = B.cnt[i];
+  const float4 xi = B.xref[i];
+  for (int k = 0; k < c; ++k) {
+    const float4 xj = B.xref[nb[k << 5]];
+    const float a[3] = {xi.x, xi.y, xi.z}, b[3] = {xj.x, xj.y, xj.z};
+    int8_t *o = col_shift + 3 * (row_ptr[i] + k);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const float e = __fsub_rn(b[d], a[d]);
+      o[d] = (int8_t)(P.box.per[d] ? (e > P.box.halfL[d] ? -1 : (e < -P.box.halfL[d] ? 1 : 0)) : 0);
+    }
+  }
+}
+
 }  // namespace
 
 void launch_verlet(const Params &P, const Bufs &B, int64_t n, cudaStream_t s) {
   k_reset_build_stats<<<1, 1, 0, s>>>(B.st);
   if (n > 0) k_verlet<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, B, (int)n);
+}
+
+void launch_verlet_shifts(const Params &P, const Bufs &B, int64_t n, const int64_t *row_ptr,
+                          int8_t *col_shift, cudaStream_t s) {
+  if (n > 0)
+    k_verlet_shifts<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, B, (int)n, row_ptr, col_shift);
 }
 
 void launch_verlet_export(const Bufs &B, int64_t n, const int64_t *row_ptr, int64_t *col_gid,

@@ -1382,6 +1382,31 @@ pm_status pm_get_verlet(pm_ctx c, int64_t *row_ptr, int64_t *col_gid) {
   return check_launch(c, "pm_get_verlet");
 }
 
+pm_status pm_get_verlet_shifts(pm_ctx c, int8_t *col_shift) {
+  if (!c || !col_shift) return PM_E_INVAL;
+  if (!c->list_valid) return set_err(c, PM_E_STATE, "pm_get_verlet_shifts: no Verlet list");
+  cudaSetDevice(c->device);
+  const int64_t n = c->n;
+  std::vector<int32_t> cnt((size_t)n);
+  if (n) CUDA_TRY(c, cudaMemcpyAsync(cnt.data(), c->B.cnt, 4 * n, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  std::vector<int64_t> rp((size_t)n + 1, 0);
+  for (int64_t i = 0; i < n; ++i) rp[(size_t)i + 1] = rp[(size_t)i] + cnt[(size_t)i];
+  const int64_t nnz = rp[(size_t)n];
+  if (nnz == 0) return PM_OK;
+  int64_t *d_rp = nullptr;
+  int8_t *d_sh = nullptr;
+  CUDA_TRY(c, cudaMalloc((void **)&d_rp, 8 * (n + 1)));
+  CUDA_TRY(c, cudaMalloc((void **)&d_sh, 3 * nnz));
+  CUDA_TRY(c, cudaMemcpyAsync(d_rp, rp.data(), 8 * (n + 1), cudaMemcpyHostToDevice, c->stream));
+  launch_verlet_shifts(c->P, c->B, n, d_rp, d_sh, c->stream);
+  CUDA_TRY(c, cudaMemcpyAsync(col_shift, d_sh, 3 * nnz, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  cudaFree(d_rp);
+  cudaFree(d_sh);
+  return check_launch(c, "pm_get_verlet_shifts");
+}
+
 pm_status pm_get_state(pm_ctx c, float *pos4, float *vel4, float *force4, int64_t *gid, float *rho,
                        float *pres, int32_t mem) {
   if (!c) return PM_E_INVAL;

@@ -344,6 +344,8 @@ void launch_sph_update(const Params &P, const Bufs &B, int64_t n, float bound, f
                        int every, cudaStream_t s);
 void launch_sph_step(const Params &P, const Bufs &B, int64_t n, float cfl, int every,
                      cudaStream_t s);
+void launch_verlet_shifts(const Params &P, const Bufs &B, int64_t n, const int64_t *row_ptr,
+                          int8_t *col_shift, cudaStream_t s);
 void launch_verlet_export(const Bufs &B, int64_t n, const int64_t *row_ptr, int64_t *col_gid,
                           cudaStream_t s);
 void launch_lj_step_mode(const Params &P, const Bufs &B, int64_t n, float dt, int mode,

@@ -113,6 +113,7 @@ def lib(path: str = LIB_PATH):
         "pm_dist_refresh_unpack": (st, [vp, vp]),
         "pm_dist_step": (st, [vp, C.c_float, C.c_int32, vp]),
         "pm_set_newton": (st, [vp, C.c_int32]),
+        "pm_get_verlet_shifts": (st, [vp, vp]),
         "pm_dist_read_flag": (st, [vp, vp]),
         "pm_dist_dem_init": (st, [vp]),
         "pm_dist_dem_step": (st, [vp, C.c_float, vp]),
@@ -315,6 +316,13 @@ class Context:
         col = np.zeros(max(int(rp[-1]), 1), np.int64)
         self._check(self.L.pm_get_verlet(self.h, rp.ctypes.data, col.ctypes.data))
         return rp, col[:int(rp[-1])]
+
+    def get_verlet_shifts(self):
+        """(nnz, 3) int8 image shifts in get_verlet()'s order."""
+        rp, _ = self.get_verlet(cols=False)
+        sh = np.zeros((max(int(rp[-1]), 1), 3), np.int8)
+        self._check(self.L.pm_get_verlet_shifts(self.h, sh.ctypes.data))
+        return sh[:int(rp[-1])]
 
     def get_state(self):
         c = self.count()

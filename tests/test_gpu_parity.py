@@ -186,6 +186,31 @@ def test_cell_div2_cells_lists_forces(pm, orc, per):
     assert np.max(np.abs(out[0][0]["pos"][:, :3] - out[1][0]["pos"][:, :3])) < 1e-4
 
 
+@pytest.mark.parametrize("L,n,per", [(8.5, 600, (1, 1, 1)), (14.5, 2500, (1, 0, 1))])
+def test_verlet_sets_with_image_shifts(pm, orc, L, n, per):
+    """R5 compares lists as sets of (gid_i, gid_j, image shift): with 3-5
+    cells per periodic axis every stencil wraps; the shifts of
+    pm_get_verlet_shifts equal the oracle's, entry for entry."""
+    s = inputs.random_box(n, L, (33, n), periodic=per)
+    c = make_ctx(pm, s)
+    c.build_verlet()
+    rp, col = c.get_verlet()
+    sh = c.get_verlet_shifts()
+    st = c.get_state()
+    inv = idx_of_gid(s)
+    rrp, rcols, rsh = orc.verlet_rows(s.pos, s.lo, s.hi, s.periodic, rv32(2.5, 0.3),
+                                      rows=inv[st["gid"]], want_shift=True)
+    nonzero = 0
+    for r in range(s.n):
+        got = sorted(zip(col[rp[r]:rp[r + 1]].tolist(), map(tuple, sh[rp[r]:rp[r + 1]].tolist())))
+        exp = sorted(zip(s.gid[rcols[rrp[r]:rrp[r + 1]]].tolist(),
+                         map(tuple, rsh[rrp[r]:rrp[r + 1]].tolist())))
+        assert got == exp, f"row {r}"
+        nonzero += sum(1 for _, t in got if any(t))
+    assert nonzero > 0  # some pairs cross a periodic face
+    c.close()
+
+
 def test_verlet_capacity_overflow_retry(pm, orc):
     """A tiny initial capacity overflows; the library grows it and retries."""
     s = inputs.cfg1()
