@@ -71,7 +71,7 @@ __device__ __forceinline__ void test8(const Params &P, const float4 *__restrict_
 // cell sort).  Lanes outside the current segment carry xi = +inf and never
 // hit.  An overflowing row keeps rewriting its last slot (min(k, cap-1)) and
 // the build is retried.
-template <bool SHIFTJ, bool PAIRMI>
+template <bool SHIFTJ, bool PAIRMI, bool NEWTON>
 __device__ __forceinline__ void scan_run(const Params &P, const float4 *__restrict__ pos, int b,
                                          int e, const float4 &xi_eff, float3 csh, int pmi,
                                          int self, int cap, int *__restrict__ row, int &k) {
@@ -90,10 +90,10 @@ __device__ __forceinline__ void scan_run(const Params &P, const float4 *__restri
       if (rem > 24) test8<SHIFTJ, PAIRMI, 24, true>(P, pos, j0, e, xi_eff, csh, pmi, msk);
       msk &= (1u << rem) - 1u;
     }
-    if (P.newton) {  // half list (NEXT-1): only j > i, each pair once
+    if (NEWTON) {  // half list (NEXT-1): only j > i, each pair once
       const int t = self - j0;
       msk &= t < 0 ? 0xffffffffu : (t >= 31 ? 0u : (0xffffffffu << (t + 1)));
-    } else if (self >= j0 && self < j0 + 32) {
+    } else if (self >= j0 && self < j0 + 32) {  // drop the particle itself
       msk &= ~(1u << (self - j0));
     }
     while (msk) {
@@ -105,13 +105,14 @@ __device__ __forceinline__ void scan_run(const Params &P, const float4 *__restri
   }
 }
 
+template <bool NEWTON>
 __device__ __forceinline__ void scan_any(const Params &P, const float4 *__restrict__ pos, int b,
                                          int e, const float4 &xi_eff, float3 csh, int pmi,
                                          int self, int cap, int *__restrict__ row, int &k) {
   const bool sj = csh.x != 0.f || csh.y != 0.f || csh.z != 0.f;
-  if (pmi) scan_run<true, true>(P, pos, b, e, xi_eff, csh, pmi, self, cap, row, k);
-  else if (sj) scan_run<true, false>(P, pos, b, e, xi_eff, csh, 0, self, cap, row, k);
-  else scan_run<false, false>(P, pos, b, e, xi_eff, csh, 0, self, cap, row, k);
+  if (pmi) scan_run<true, true, NEWTON>(P, pos, b, e, xi_eff, csh, pmi, self, cap, row, k);
+  else if (sj) scan_run<true, false, NEWTON>(P, pos, b, e, xi_eff, csh, 0, self, cap, row, k);
+  else scan_run<false, false, NEWTON>(P, pos, b, e, xi_eff, csh, 0, self, cap, row, k);
 }
 
 // Thread per particle (row), warp-uniform candidate stream.  The warp's 32
@@ -124,6 +125,9 @@ __device__ __forceinline__ void scan_any(const Params &P, const float4 *__restri
 // (the extra candidates of the union are farther than r_v and rejected by
 // the same pinned test).  All lanes read the same position each iteration
 // (broadcast), there is no divergence, and rows come out in a fixed order.
+// RCH: stencil half-width in cells (P.reach), 1 (27 cells) or 2 (125 cells);
+// NEWTON: half lists (P.newton)
+template <int RCH, bool NEWTON>
 __global__ void __launch_bounds__(256, 4) k_verlet(Params P, Bufs B, int n) {
   State *st = B.st;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -168,7 +172,7 @@ __global__ void __launch_bounds__(256, 4) k_verlet(Params P, Bufs B, int n) {
       cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
     }
     const int cy = seg_row % ny, cz = seg_row / ny;
-    const int R = P.grid.reach;  // stencil half-width: 1 (27 cells) or 2 (125 cells)
+    constexpr int R = RCH;
     int xa = cmin - R, xb = cmax + R;
     // per-pair R4 along x: a run covering a whole periodic x-row, or (a
     // decomposed x) a run touching cells that may hold wrapped particles
@@ -216,13 +220,13 @@ __global__ void __launch_bounds__(256, 4) k_verlet(Params P, Bufs B, int n) {
         const float4 xe0 = mine ? make_float4(__fsub_rn(xi.x, lx0), __fsub_rn(xi.y, ly),
                                               __fsub_rn(xi.z, lz), 0.f)
                                 : make_float4(INF, INF, INF, 0.f);
-        scan_any(P, pos, B.start[rowc + a0], B.start[rowc + b0 + 1], xe0,
+        scan_any<NEWTON>(P, pos, B.start[rowc + a0], B.start[rowc + b0 + 1], xe0,
                  make_float3((pmi & 1) ? 0.f : sx0, shy, shz), pmi, i, cap, row, k);
         if (b1 >= a1) {
           const float4 xe1 = mine ? make_float4(__fsub_rn(xi.x, lx1), __fsub_rn(xi.y, ly),
                                                 __fsub_rn(xi.z, lz), 0.f)
                                   : make_float4(INF, INF, INF, 0.f);
-          scan_any(P, pos, B.start[rowc + a1], B.start[rowc + b1 + 1], xe1,
+          scan_any<NEWTON>(P, pos, B.start[rowc + a1], B.start[rowc + b1 + 1], xe1,
                    make_float3(sx1, shy, shz), pmi & ~1, i, cap, row, k);
         }
       }
@@ -296,7 +300,15 @@ __global__ void __launch_bounds__(256) k_verlet_shifts(Params P, Bufs B, int n,
 
 void launch_verlet(const Params &P, const Bufs &B, int64_t n, cudaStream_t s) {
   k_reset_build_stats<<<1, 1, 0, s>>>(B.st);
-  if (n > 0) k_verlet<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, B, (int)n);
+  if (n <= 0) return;
+  const unsigned g = (unsigned)((n + 255) / 256);
+  if (P.reach == 2) {
+    if (P.newton) k_verlet<2, true><<<g, 256, 0, s>>>(P, B, (int)n);
+    else k_verlet<2, false><<<g, 256, 0, s>>>(P, B, (int)n);
+  } else {
+    if (P.newton) k_verlet<1, true><<<g, 256, 0, s>>>(P, B, (int)n);
+    else k_verlet<1, false><<<g, 256, 0, s>>>(P, B, (int)n);
+  }
 }
 
 void launch_verlet_shifts(const Params &P, const Bufs &B, int64_t n, const int64_t *row_ptr,

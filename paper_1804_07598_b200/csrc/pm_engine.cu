@@ -441,7 +441,7 @@ pm_status setup_grid(pm_ctx c) {
   }
   if (ncell > (int64_t)1 << 30) return set_err(c, PM_E_INVAL, "too many cells (%lld)", (long long)ncell);
   P.grid.ncell = (int)ncell;
-  P.grid.reach = c->dist ? 1 : c->cell_div;
+  P.reach = c->dist ? 1 : c->cell_div;
   c->cells_valid = c->list_valid = c->forces_valid = c->rho_valid = false;
   destroy_graph(c);
   return ensure_cells(c);

@@ -42,7 +42,6 @@ struct Grid {
   int safe_lo[3], safe_hi[3];  // decomposed axes: cells whose extent lies strictly
                                // inside the global box (no wrapped particle)
   int ncell;
-  int reach;       // stencil half-width in cells: 1 (side >= r_v) or 2 (side >= r_v/2)
 };
 
 // Decomposition of the global periodic box into p[0] x p[1] x p[2] cuboids;
@@ -102,6 +101,8 @@ struct Params {
   int sph_state;    // 1: the cell-sort reorder also permutes the SPH stepping state
   int dem_state;    // 1: ... and the DEM angular velocities
   int newton;       // 1: half (Newton) list, j > i in cell order (NEXT-1)
+  int reach;        // stencil half-width in cells: 1 (side >= r_v) or 2 (side >= r_v/2);
+                    // kept out of Grid: the sweeps' hot constants stay where they were
   DEM dem;
 };
 
