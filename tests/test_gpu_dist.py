@@ -463,3 +463,50 @@ def test_api_state_errors(env):
         c.sph_run(2)
     assert e.value.code == -2
     c.close()
+
+
+def test_decomposed_dem_2x2_periodic_layer(env):
+    """Decomposed DEM on a (2,2,1) grid: a granular layer periodic in x and y
+    on a floor (walls only at z-lo), gravity tilted along x so grains flow
+    across the x faces and collide across the y faces; histories migrate in
+    all in-plane directions including the diagonals.  Matches one context."""
+    import torch
+    pm, dist = env
+    s = inputs.dem_avalanche(12, 12, 5, vjit=1.5, gap=0.5)
+    s.periodic = np.array([1, 1, 0], np.int32)
+    s.hi[0] = np.float32(12 * 2 * 0.06 * 1.5)  # periodic x: the lattice length
+    p = dict(s.params)
+    p["walls"] = (0, 0, 0, 0, 1, 0)
+    nsteps = 400
+    c = pm.Context()
+    c.set_domain(s.lo, s.hi, s.periodic)
+    c.set_cutoff(2.0 * p["R"], p["skin"])
+    c.set_dem(p)
+    c.place(s.pos, s.vel, s.gid)
+    c.dem_run(p["dt"], nsteps)
+    one = pm.sorted_by_gid(c.get_state())
+    c.close()
+    D = dist.Decomp((2, 2, 1))
+    owner0 = dist.owner_of(s, D)
+    stream = torch.cuda.Stream()
+    members = {r: dist.make_member(s.subset(np.where(owner0 == r)[0]), D, r, stream=stream,
+                                   rc=2.0 * p["R"], skin=p["skin"], dem=p)
+               for r in range(D.size)}
+    sim = dist.DistSim(D, members, dist.LoopbackTransport(members), stream=stream)
+    sim.dem_start()
+    reb = sim.dem_run(nsteps, p["dt"])
+    torch.cuda.synchronize()
+    got = pm.sorted_by_gid({k: np.concatenate([m.owned_state()[k] for m in members.values()])
+                            for k in ("gid", "pos", "vel")})
+    assert np.array_equal(got["gid"], s.gid)
+    own1 = dist.owner_of(inputs.System(pos=got["pos"], vel=s.vel, gid=s.gid, lo=s.lo, hi=s.hi,
+                                       periodic=s.periodic), D)
+    assert reb >= 2 and (own1 != owner0).sum() >= 5
+    L = (s.hi - s.lo).astype(np.float64)
+    dx = got["pos"][:, :3].astype(np.float64) - one["pos"][:, :3]
+    dx[:, :2] -= L[:2] * np.round(dx[:, :2] / L[:2])
+    assert np.max(np.abs(dx)) / p["R"] < 1e-3
+    v1 = one["vel"][:, :3].astype(np.float64)
+    assert np.max(np.abs(got["vel"][:, :3] - v1)) / np.max(np.abs(v1)) < 2e-3
+    for m in members.values():
+        m.close()
