@@ -32,6 +32,9 @@ __device__ __forceinline__ float3 cross3(const float3 &a, const float3 &b) {
 // from buffer cur_pv and written to cur_pv ^ 1, so the sweep reads only the
 // old state.  Contacts are processed two at a time with all their loads
 // (partner x, v, omega and the slot's history) issued before the arithmetic.
+// PM: periodic axes as a compile-time bit mask (the contact loop's pair
+// difference takes the R4 branches only on those axes)
+template <int PM>
 __global__ void __launch_bounds__(256, 4) k_dem_step(Params P, Bufs B, int n, float dt) {
   State *st = B.st;
   if (st->abort) return;  // a failed in-graph rebuild: the host resumes here
@@ -58,9 +61,9 @@ __global__ void __launch_bounds__(256, 4) k_dem_step(Params P, Bufs B, int n, fl
     auto contact = [&](const float4 &xj, const float4 &vj, const float4 &wj, const float4 &h,
                        int64_t slot) {
       // r_pq = x_i - x_j (R4 minimum image on periodic axes)
-      const float rx = -pair_delta1(xi.x, xj.x, P.box.L[0], P.box.halfL[0], P.box.per[0]);
-      const float ry = -pair_delta1(xi.y, xj.y, P.box.L[1], P.box.halfL[1], P.box.per[1]);
-      const float rz = -pair_delta1(xi.z, xj.z, P.box.L[2], P.box.halfL[2], P.box.per[2]);
+      const float rx = -pair_delta1(xi.x, xj.x, P.box.L[0], P.box.halfL[0], PM & 1);
+      const float ry = -pair_delta1(xi.y, xj.y, P.box.L[1], P.box.halfL[1], (PM >> 1) & 1);
+      const float rz = -pair_delta1(xi.z, xj.z, P.box.L[2], P.box.halfL[2], (PM >> 2) & 1);
       const float r2 = rx * rx + ry * ry + rz * rz;
       const float rr = sqrtf(r2);
       const float delta = twoR - rr;
@@ -337,7 +340,18 @@ inline unsigned nb(int64_t n) { return (unsigned)((n + 255) / 256); }
 }  // namespace
 
 void launch_dem_step(const Params &P, const Bufs &B, int64_t n, float dt, cudaStream_t s) {
-  if (n > 0) k_dem_step<<<nb(n), 256, 0, s>>>(P, B, (int)n, dt);
+  if (n <= 0) return;
+  const int pm = (P.box.per[0] ? 1 : 0) | (P.box.per[1] ? 2 : 0) | (P.box.per[2] ? 4 : 0);
+  switch (pm) {
+    case 0: k_dem_step<0><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt); break;
+    case 1: k_dem_step<1><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt); break;
+    case 2: k_dem_step<2><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt); break;
+    case 3: k_dem_step<3><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt); break;
+    case 4: k_dem_step<4><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt); break;
+    case 5: k_dem_step<5><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt); break;
+    case 6: k_dem_step<6><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt); break;
+    default: k_dem_step<7><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt); break;
+  }
 }
 
 void launch_dem_remap(const Bufs &B, int64_t n, cudaStream_t s) {
