@@ -214,6 +214,7 @@ __device__ __forceinline__ void warp_min_atomic(unsigned *dst, float v) {
 template <bool PER>
 __global__ void __launch_bounds__(256, 3) k_sph_rates(Params P, Bufs B, int n) {
   State *st = B.st;
+  if (st->abort) return;  // a failed in-graph rebuild: the host resumes
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int cp = st->cur_pv, ci = st->cur_id;
   // ghost copies of a decomposed context: no row, no rate, no step bound
@@ -294,6 +295,7 @@ __global__ void __launch_bounds__(256, 3) k_sph_rates(Params P, Bufs B, int n) {
 }
 
 __global__ void k_sph_dt(State *st, float cfl, int every) {
+  if (st->abort) return;
   const float dt = cfl * fminf(__uint_as_float(st->dtf_bits), __uint_as_float(st->dtcv_bits));
   st->sph_dt = dt;
   st->sph_dt_min = fminf(st->sph_dt_min, dt);
@@ -330,6 +332,7 @@ __device__ __forceinline__ float tait(const Params &P, float rho) {
 
 __global__ void __launch_bounds__(256) k_sph_verlet(Params P, Bufs B, int n) {
   State *st = B.st;
+  if (st->abort) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int cp = st->cur_pv, ci = st->cur_id;
   bool far = false;
@@ -378,7 +381,10 @@ __global__ void __launch_bounds__(256) k_sph_verlet(Params P, Bufs B, int n) {
     }
   }
   if (__any_sync(0xffffffffu, far) && (threadIdx.x & 31) == 0) st->need_rebuild = 1;
-  if (blockIdx.x == 0 && threadIdx.x == 0) st->pending_flip = 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->pending_flip = 1;
+    st->steps_done += 1;
+  }
 }
 
 __global__ void __launch_bounds__(256) k_sph_set_rho(Params P, Bufs B, int n, const float *rho) {

@@ -66,6 +66,14 @@ struct pm_ctx_s {
   cudaGraphExec_t dem_exec = nullptr;
   cudaGraph_t dem_graph = nullptr;
   Params dem_key_P{};
+  // SPH stepping graph (pm_sph_run), same scheme
+  cudaGraphExec_t sph_exec = nullptr;
+  cudaGraph_t sph_graph = nullptr;
+  Params sph_key_P{};
+  Bufs sph_key_B{};
+  int64_t sph_key_n = -1;
+  float sph_key_cfl = 0.f;
+  int sph_key_every = -1;
   Bufs dem_key_B{};
   int64_t dem_key_n = -1;
   float dem_key_dt = 0.f;
@@ -178,6 +186,14 @@ void destroy_graph(pm_ctx c) {
   c->exec = nullptr;
   c->graph = nullptr;
   c->graph_valid = false;
+}
+
+void destroy_sph_graph(pm_ctx c) {
+  if (c->sph_exec) cudaGraphExecDestroy(c->sph_exec);
+  if (c->sph_graph) cudaGraphDestroy(c->sph_graph);
+  c->sph_exec = nullptr;
+  c->sph_graph = nullptr;
+  c->sph_key_n = -1;
 }
 
 void destroy_dem_graph(pm_ctx c) {
@@ -675,6 +691,7 @@ void pm_destroy(pm_ctx c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   destroy_graph(c);
   destroy_dem_graph(c);
+  destroy_sph_graph(c);
   Bufs &B = c->B;
   for (int b = 0; b < 2; ++b) {
     cudaFree(B.pos[b]);
@@ -1178,6 +1195,54 @@ static pm_status sph_step_alloc(pm_ctx c) {
   return PM_OK;
 }
 
+// The SPH stepping graph: step head (apply the pending flip, open the
+// rebuild branch) -> IF(need_rebuild) { cell sort -> Verlet } -> rates ->
+// dt -> Verlet update.  No host round trip per step; a capacity overflow
+// inside the graph aborts the remaining steps and pm_sph_run resumes.
+static pm_status sph_graph_ready(pm_ctx c, float cfl, int every) {
+  if (c->sph_exec && c->sph_key_n == c->n && c->sph_key_cfl == cfl &&
+      c->sph_key_every == every && !std::memcmp(&c->sph_key_P, &c->P, sizeof(Params)) &&
+      !std::memcmp(&c->sph_key_B, &c->B, sizeof(Bufs)))
+    return PM_OK;
+  destroy_sph_graph(c);
+  cudaGraph_t g = nullptr;
+  CUDA_TRY(c, cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  CUDA_TRY(c, cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
+  cudaStream_t cs = c->cap_stream;
+  const cudaStreamCaptureMode mode = cudaStreamCaptureModeThreadLocal;
+  CUDA_TRY(c, cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, mode));
+  launch_dem_step_begin(c->B, h, cs);  // generic step head (flip + rebuild condition)
+  CUDA_TRY(c, cudaStreamEndCapture(cs, &g));
+  size_t nn = 0;
+  CUDA_TRY(c, cudaGraphGetNodes(g, nullptr, &nn));
+  if (nn != 1) return set_err(c, PM_E_CUDA, "sph graph: expected 1 node, got %zu", nn);
+  cudaGraphNode_t nA;
+  CUDA_TRY(c, cudaGraphGetNodes(g, &nA, &nn));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeIf;
+  cp.conditional.size = 1;
+  cudaGraphNode_t nC;
+  CUDA_TRY(c, cudaGraphAddNode(&nC, g, &nA, 1, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CUDA_TRY(c, cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, mode));
+  enqueue_rebuild(c, cs, 1);
+  CUDA_TRY(c, cudaStreamEndCapture(cs, &body));
+  CUDA_TRY(c, cudaStreamBeginCaptureToGraph(cs, g, &nC, nullptr, 1, mode));
+  launch_sph_step(c->P, c->B, c->n, cfl, every, cs);
+  CUDA_TRY(c, cudaStreamEndCapture(cs, &g));
+  CUDA_TRY(c, cudaGraphInstantiate(&c->sph_exec, g, 0));
+  c->sph_graph = g;
+  c->sph_key_P = c->P;
+  c->sph_key_B = c->B;
+  c->sph_key_n = c->n;
+  c->sph_key_cfl = cfl;
+  c->sph_key_every = every;
+  return PM_OK;
+}
+
 pm_status pm_sph_run(pm_ctx c, int64_t nsteps, float cfl, int32_t every,
                      pm_sph_run_stats *out) {
   pm_status s = check_ready(c);
@@ -1216,26 +1281,50 @@ pm_status pm_sph_run(pm_ctx c, int64_t nsteps, float cfl, int32_t every,
   launch_sph_init_run(B, c->n, c->stream);
   k_clear_rebuild<<<1, 1, 0, c->stream>>>(B.st);
   int64_t done = 0;
-  for (; done < nsteps; ++done) {
-    s = read_state(c);  // the rebuild decision of the previous step
-    if (s) return s;
-    if (c->st_h->abort) break;
-    if (c->st_h->need_rebuild) {
-      enqueue_rebuild(c, c->stream, 1);
-      s = sync_check(c, "pm_sph_run (rebuild)");
-      if (s == PM_E_CAPACITY) {  // grow the rows and rebuild from the sorted order
-        c->sticky = 0;
-        c->err.clear();
-        k_clear_abort<<<1, 1, 0, c->stream>>>(B.st);
-        s = layout_from_counts(c);
-        if (s) return s;
-        launch_verlet(c->P, B, c->n, c->stream);
-        s = sync_check(c, "pm_sph_run (rebuild retry)");
-      }
+  if (c->use_graphs) {
+    // every resume completes the aborted step, so nsteps + 1 passes suffice
+    for (int64_t attempt = 0; attempt <= nsteps && done < nsteps; ++attempt) {
+      if ((s = sph_graph_ready(c, cfl, every))) return s;
+      k_run_init<<<1, 1, 0, c->stream>>>(B.st, (long long)(nsteps - done));
+      for (int64_t k = done; k < nsteps; ++k) CUDA_TRY(c, cudaGraphLaunch(c->sph_exec, c->stream));
+      k_apply_pending<<<1, 1, 0, c->stream>>>(B.st);
+      s = read_state(c);
       if (s) return s;
+      done += c->st_h->steps_done;
+      if (c->st_h->abort != PM_E_CAPACITY || done >= nsteps) break;
+      // the Verlet build of step `done` overflowed (cells already sorted):
+      // grow the rows from the exact counts, build, finish that step here
+      k_clear_abort<<<1, 1, 0, c->stream>>>(B.st);
+      if ((s = layout_from_counts(c))) return s;
+      launch_verlet(c->P, B, c->n, c->stream);
+      if ((s = sync_check(c, "pm_sph_run (rebuild retry)"))) return s;
+      launch_sph_step(c->P, B, c->n, cfl, every, c->stream);
+      k_apply_pending<<<1, 1, 0, c->stream>>>(B.st);
+      if ((s = sync_check(c, "pm_sph_run (resumed step)"))) return s;
+      done += 1;
     }
-    launch_sph_step(c->P, B, c->n, cfl, every, c->stream);
-    k_apply_pending<<<1, 1, 0, c->stream>>>(B.st);
+  } else {
+    for (; done < nsteps; ++done) {
+      s = read_state(c);  // the rebuild decision of the previous step
+      if (s) return s;
+      if (c->st_h->abort) break;
+      if (c->st_h->need_rebuild) {
+        enqueue_rebuild(c, c->stream, 1);
+        s = sync_check(c, "pm_sph_run (rebuild)");
+        if (s == PM_E_CAPACITY) {  // grow the rows and rebuild from the sorted order
+          c->sticky = 0;
+          c->err.clear();
+          k_clear_abort<<<1, 1, 0, c->stream>>>(B.st);
+          s = layout_from_counts(c);
+          if (s) return s;
+          launch_verlet(c->P, B, c->n, c->stream);
+          s = sync_check(c, "pm_sph_run (rebuild retry)");
+        }
+        if (s) return s;
+      }
+      launch_sph_step(c->P, B, c->n, cfl, every, c->stream);
+      k_apply_pending<<<1, 1, 0, c->stream>>>(B.st);
+    }
   }
   s = read_state(c);
   if (s) return s;
