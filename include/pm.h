@@ -64,7 +64,11 @@ typedef struct {
                           27-cell stencil) or 2 (side >= r_v/2, 125-cell stencil;
                           single-GPU contexts); PM_E_INVAL otherwise */
   int32_t nbr_cap;     /* initial neighbour slots per particle (0 = auto from density) */
-  int32_t use_graphs;  /* 1: pm_step_vv runs each step as one CUDA graph launch */
+  int32_t use_graphs;  /* 1: pm_step_vv, pm_sph_run and pm_dem_run run each step as
+                          one CUDA graph launch (rebuild as a conditional node, no
+                          host round trip per step); 0: plain launches, one host
+                          read of the rebuild flag per step (PM_USE_GRAPHS=0 in the
+                          environment sets the default to 0: profiling) */
   void *cuda_stream;   /* cudaStream_t to run on; NULL = library-owned stream */
 } pm_opts;
 
