@@ -367,6 +367,28 @@ pm_status pm_dist_refresh_unpack(pm_ctx ctx, const void *recv_dev);
  * particle moved more than skin/2 since the last build". */
 pm_status pm_dist_step(pm_ctx ctx, float dt, int32_t phase, int32_t *need_rebuild);
 
+/* Fused ghost refresh (SURVEY §8(e) "the K6 epilogue ... stores straight into
+ * peer windows"): after a rebuild, each sub-domain registers, for every entry
+ * of its ghost send list (pm_dist_plan(GHOST) order), the receiving peer
+ * (index into the peer tables) and the receiver's ghost slot (the receiver's
+ * pm_dist_ghost_slots, in its arrival order), plus each peer's two position
+ * buffers (pm_dist_pos_buffers; across processes opened through CUDA IPC:
+ * pm_dist_ipc_handles / pm_dist_ipc_open).  PM_PHASE_STEP of pm_dist_step
+ * then writes every new position of a sent particle into the peers' next
+ * position buffer from the sweep's epilogue (no pack, no message, no
+ * unpack); the caller only orders the step before the peers' next step (the
+ * per-step flag all-reduce).  pm_dist_finish disables it until the next
+ * setup; npeers = 0 disables it.  dst_peer / dst_slot: device int32[n_send]. */
+pm_status pm_dist_pos_buffers(pm_ctx ctx, void **pos0, void **pos1);
+pm_status pm_dist_ghost_slots(pm_ctx ctx, int32_t *dev_out);
+pm_status pm_dist_peer_setup(pm_ctx ctx, int32_t npeers, void *const *peer_pos0,
+                             void *const *peer_pos1, const int32_t *dst_peer,
+                             const int32_t *dst_slot);
+/* 128 bytes: CUDA IPC handles of this context's two position buffers. */
+pm_status pm_dist_ipc_handles(pm_ctx ctx, void *out);
+pm_status pm_dist_ipc_open(pm_ctx ctx, const void *in, void **pos0, void **pos1);
+pm_status pm_dist_ipc_close_all(pm_ctx ctx);
+
 /* Synchronise and return (and clear) the local rebuild flag -- the
  * need_rebuild of pm_dist_step as a separate call, so a caller can time the
  * step kernels with events before the host round trip. */

@@ -388,6 +388,18 @@ void launch_scan(const Params &P, const Bufs &B, int64_t n, cudaStream_t s) {
   k_scan_add<<<ntiles, kScanThreads, 0, s>>>(B.start, B.scan_tmp, ncell);
 }
 
+// Generic exclusive scan of n ints (count is zeroed, start[n] = total);
+// tmp needs scan_tiles(n) ints.
+int scan_tiles(int n) { return (n + kScanTile - 1) / kScanTile; }
+
+void launch_exclusive_scan(int32_t *count, int32_t *start, int32_t *tmp, int n, cudaStream_t s) {
+  const int ntiles = scan_tiles(n);
+  if (ntiles == 0) return;
+  k_scan_tiles<<<ntiles, kScanThreads, 0, s>>>(count, start, tmp, n);
+  k_scan_sums<<<1, 1024, 0, s>>>(tmp, ntiles, start, n);
+  k_scan_add<<<ntiles, kScanThreads, 0, s>>>(start, tmp, n);
+}
+
 void launch_sort_reorder(const Params &P, const Bufs &B, int64_t n, cudaStream_t s) {
   if (n <= 0) return;
   int32_t *tmp = B.sorttmp;

@@ -319,6 +319,22 @@ __global__ void k_refresh_unpack_pv(Bufs B, const int *__restrict__ ghost_slot, 
   }
 }
 
+// fused refresh tables: per send entry e (send order), its particle
+// send_idx[e] and its destination (peer, ghost slot) -> CSR by particle
+__global__ void k_peer_count(const int *__restrict__ send_idx, int nsend, int32_t *cnt) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < nsend) atomicAdd(&cnt[send_idx[e]], 1);
+}
+
+__global__ void k_peer_fill(const int *__restrict__ send_idx, const int *__restrict__ dst_peer,
+                            const int *__restrict__ dst_slot, int nsend,
+                            const int32_t *__restrict__ off, int32_t *fill, int2 *__restrict__ dst) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nsend) return;
+  const int i = send_idx[e];
+  dst[off[i] + atomicAdd(&fill[i], 1)] = make_int2(dst_peer[e], dst_slot[e]);
+}
+
 inline unsigned nb(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
@@ -380,6 +396,17 @@ void launch_refresh_pv(const Bufs &B, int pack, const int *idx, int m, void *buf
   else if (pack) k_refresh_pack_pv<2><<<nb(m), 256, 0, s>>>(B, idx, m, f);
   else if (with_w) k_refresh_unpack_pv<3><<<nb(m), 256, 0, s>>>(B, idx, m, f);
   else k_refresh_unpack_pv<2><<<nb(m), 256, 0, s>>>(B, idx, m, f);
+}
+
+// cnt: n + 1 zeroed ints; tmp: scan_tiles(n + 1) ints; B.ps_off: n + 1 ints;
+// B.ps_dst: nsend int2
+void launch_peer_csr(const Bufs &B, const int *send_idx, const int *dst_peer, const int *dst_slot,
+                     int nsend, int32_t *cnt, int n, int32_t *tmp, cudaStream_t s) {
+  if (nsend > 0) k_peer_count<<<nb(nsend), 256, 0, s>>>(send_idx, nsend, cnt);
+  launch_exclusive_scan(cnt, B.ps_off, tmp, n + 1, s);  // zeroes cnt again
+  if (nsend > 0)
+    k_peer_fill<<<nb(nsend), 256, 0, s>>>(send_idx, dst_peer, dst_slot, nsend, B.ps_off, cnt,
+                                          B.ps_dst);
 }
 
 void launch_refresh_unpack(const Bufs &B, const int *ghost_slot, int nghost, const void *in,

@@ -252,6 +252,7 @@ __device__ __forceinline__ void kick_limited(float4 &v, float k, const Acc &a, f
 //  final: F(x); v += dt/2 F/m; F stored; x copied  -> alternate buffers
 // The velocity-Verlet epilogue of one particle after its force a (see
 // k_lj_step); writes the alternate buffers and sets `far`.
+template <bool PEER = false>
 __device__ __forceinline__ void vv_epilogue(const Params &P, const Bufs &B, State *st, int i,
                                             bool active, const float4 &xi, const Acc &a,
                                             float dt, int mode, int cp, bool &far) {
@@ -275,7 +276,15 @@ __device__ __forceinline__ void vv_epilogue(const Params &P, const Bufs &B, Stat
       }
       const float3 xn = wrap3(P, fmaf(dt, v.x, xi.x), fmaf(dt, v.y, xi.y), fmaf(dt, v.z, xi.z));
       far = moved_too_far(P, xn, B.xref[i]);
-      B.pos[cp ^ 1][i] = make_float4(xn.x, xn.y, xn.z, xi.w);
+      const float4 x4 = make_float4(xn.x, xn.y, xn.z, xi.w);
+      B.pos[cp ^ 1][i] = x4;
+      if (PEER) {  // fused ghost refresh: straight into the peers' ghost slots
+        const int e1 = B.ps_off[i + 1];
+        for (int e = B.ps_off[i]; e < e1; ++e) {
+          const int2 d = B.ps_dst[e];
+          P.peer_pos[d.x][cp ^ 1][d.y] = x4;
+        }
+      }
     } else {
       kick_limited(v, 0.5f * dt * im, a, P.vmax);
       B.pos[cp ^ 1][i] = xi;
@@ -291,7 +300,7 @@ __device__ __forceinline__ void vv_epilogue(const Params &P, const Bufs &B, Stat
 //  inner: F(x); v += dt F/m (2nd half-kick of this step + 1st of the next);
 //         x' = wrap(x + dt v); displacement test vs xref; -> alternate buffers
 //  final: F(x); v += dt/2 F/m; F stored; x copied  -> alternate buffers
-template <bool CAPPED>
+template <bool CAPPED, bool PEER = false>
 __global__ void __launch_bounds__(256) k_lj_step(Params P, Bufs B, int n, float dt, int mode_arg) {
   State *st = B.st;
   if (st->abort) return;
@@ -303,7 +312,7 @@ __global__ void __launch_bounds__(256) k_lj_step(Params P, Bufs B, int n, float 
   const float4 xi = active ? pos[i] : make_float4(0.f, 0.f, 0.f, 0.f);
   Acc a = lj_force_of<CAPPED, false>(P, B, pos, i, active, xi);
   bool far = false;
-  vv_epilogue(P, B, st, i, active, xi, a, dt, mode, cp, far);
+  vv_epilogue<PEER>(P, B, st, i, active, xi, a, dt, mode, cp, far);
   if (__any_sync(0xffffffffu, far) && (threadIdx.x & 31) == 0) st->need_rebuild = 1;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st->pending_flip = 1;
@@ -530,6 +539,11 @@ void launch_lj_step_mode(const Params &P, const Bufs &B, int64_t n, float dt, in
   if (P.newton) {  // clear F -> half sweep -> integrator
     launch_lj_half(P, B, n, 0, s);
     k_lj_half_vv<<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode);
+    return;
+  }
+  if (P.peer_n > 0) {  // decomposed run with the fused ghost refresh
+    if (P.lj.r_min > 0.f) k_lj_step<true, true><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode);
+    else k_lj_step<false, true><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode);
     return;
   }
   if (P.lj.r_min > 0.f) k_lj_step<true><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode);

@@ -90,6 +90,10 @@ struct pm_ctx_s {
   int plan_what = -1;
   // decomposed DEM: the stay list of the last migration (pre-migration
   // indices), arrivals' contact histories, saved-rows flag
+  // fused ghost refresh tables
+  int32_t *d_pcnt = nullptr, *d_ptmp = nullptr;
+  int64_t pcnt_cap = 0, ptmp_cap = 0, psoff_cap = 0, psdst_cap = 0;
+  std::vector<void *> ipc_open;  // peer buffers opened through CUDA IPC
   int *d_stay_old = nullptr;
   int64_t stay_cap = 0, n_stay_old = 0, gid_old_cap = 0;
   char *d_hist_in = nullptr;
@@ -692,6 +696,12 @@ void pm_destroy(pm_ctx c) {
   destroy_graph(c);
   destroy_dem_graph(c);
   destroy_sph_graph(c);
+  for (void *p : c->ipc_open) cudaIpcCloseMemHandle(p);
+  c->ipc_open.clear();
+  cudaFree(c->d_pcnt);
+  cudaFree(c->d_ptmp);
+  cudaFree(c->B.ps_off);
+  cudaFree(c->B.ps_dst);
   Bufs &B = c->B;
   for (int b = 0; b < 2; ++b) {
     cudaFree(B.pos[b]);
@@ -1804,6 +1814,7 @@ pm_status pm_dist_finish(pm_ctx c) {
   if ((s = ensure_dev(c, &c->d_gslot, c->gslot_cap, c->n_ghost + 1))) return s;
   launch_dist_remap(c->B.invperm, c->d_send_idx, (int)c->n_send, c->d_gslot, (int)c->n_ghost,
                     (int)c->n_owned, c->stream);
+  c->P.peer_n = 0;  // new send lists and ghost slots: pm_dist_peer_setup again
   if (c->P.dem_state) {  // contact histories onto the new rows (stayers and arrivals)
     if ((s = dem_alloc(c, false))) return s;
     launch_dem_remap_dist(c->B, c->n, c->d_stay_old, (int)c->n_stay_old, c->d_hist_in,
@@ -1881,6 +1892,87 @@ pm_status pm_dist_refresh_pv_unpack(pm_ctx c, const void *recv_dev) {
   launch_refresh_pv(c->B, 0, c->d_gslot, (int)c->n_ghost, const_cast<void *>(recv_dev), 0,
                     c->stream);
   return check_launch(c, "pm_dist_refresh_pv_unpack");
+}
+
+pm_status pm_dist_pos_buffers(pm_ctx c, void **pos0, void **pos1) {
+  if (!c || !pos0 || !pos1) return PM_E_INVAL;
+  *pos0 = c->B.pos[0];
+  *pos1 = c->B.pos[1];
+  return PM_OK;
+}
+
+pm_status pm_dist_ghost_slots(pm_ctx c, int32_t *dev_out) {
+  if (!c) return PM_E_INVAL;
+  if (!c->dist) return set_err(c, PM_E_STATE, "pm_dist_ghost_slots: no decomposition");
+  if (c->n_ghost > 0 && !dev_out) return set_err(c, PM_E_INVAL, "null buffer");
+  cudaSetDevice(c->device);
+  if (c->n_ghost > 0)
+    CUDA_TRY(c, cudaMemcpyAsync(dev_out, c->d_gslot, sizeof(int) * c->n_ghost,
+                                cudaMemcpyDeviceToDevice, c->stream));
+  return check_launch(c, "pm_dist_ghost_slots");
+}
+
+pm_status pm_dist_peer_setup(pm_ctx c, int32_t npeers, void *const *peer_pos0,
+                             void *const *peer_pos1, const int32_t *dst_peer,
+                             const int32_t *dst_slot) {
+  pm_status s = check_ready(c);
+  if (s) return s;
+  if (!c->dist) return set_err(c, PM_E_STATE, "pm_dist_peer_setup: no decomposition");
+  if (npeers < 0 || npeers > 26) return set_err(c, PM_E_INVAL, "pm_dist_peer_setup: npeers");
+  cudaSetDevice(c->device);
+  if (npeers == 0) {
+    c->P.peer_n = 0;
+    return PM_OK;
+  }
+  if (!peer_pos0 || !peer_pos1 || (c->n_send > 0 && (!dst_peer || !dst_slot)))
+    return set_err(c, PM_E_INVAL, "pm_dist_peer_setup: null argument");
+  const int64_t n = c->n;
+  if ((s = ensure_dev(c, &c->d_pcnt, c->pcnt_cap, n + 1))) return s;
+  if ((s = ensure_dev(c, &c->d_ptmp, c->ptmp_cap, scan_tiles((int)n + 1) + 1))) return s;
+  if ((s = ensure_dev(c, &c->B.ps_off, c->psoff_cap, n + 2))) return s;
+  if ((s = ensure_dev(c, &c->B.ps_dst, c->psdst_cap, c->n_send + 1))) return s;
+  CUDA_TRY(c, cudaMemsetAsync(c->d_pcnt, 0, sizeof(int32_t) * (n + 1), c->stream));
+  launch_peer_csr(c->B, c->d_send_idx, dst_peer, dst_slot, (int)c->n_send, c->d_pcnt, (int)n,
+                  c->d_ptmp, c->stream);
+  for (int q = 0; q < npeers; ++q) {
+    c->P.peer_pos[q][0] = static_cast<float4 *>(peer_pos0[q]);
+    c->P.peer_pos[q][1] = static_cast<float4 *>(peer_pos1[q]);
+  }
+  c->P.peer_n = npeers;
+  return check_launch(c, "pm_dist_peer_setup");
+}
+
+pm_status pm_dist_ipc_handles(pm_ctx c, void *out) {
+  if (!c || !out) return PM_E_INVAL;
+  cudaSetDevice(c->device);
+  cudaIpcMemHandle_t h[2];
+  for (int b = 0; b < 2; ++b) CUDA_TRY(c, cudaIpcGetMemHandle(&h[b], c->B.pos[b]));
+  std::memcpy(out, h, sizeof h);
+  return PM_OK;
+}
+
+pm_status pm_dist_ipc_open(pm_ctx c, const void *in, void **pos0, void **pos1) {
+  if (!c || !in || !pos0 || !pos1) return PM_E_INVAL;
+  cudaSetDevice(c->device);
+  cudaIpcMemHandle_t h[2];
+  std::memcpy(h, in, sizeof h);
+  void *p[2];
+  for (int b = 0; b < 2; ++b) {
+    CUDA_TRY(c, cudaIpcOpenMemHandle(&p[b], h[b], cudaIpcMemLazyEnablePeerAccess));
+    c->ipc_open.push_back(p[b]);
+  }
+  *pos0 = p[0];
+  *pos1 = p[1];
+  return PM_OK;
+}
+
+pm_status pm_dist_ipc_close_all(pm_ctx c) {
+  if (!c) return PM_E_INVAL;
+  cudaSetDevice(c->device);
+  for (void *p : c->ipc_open) cudaIpcCloseMemHandle(p);
+  c->ipc_open.clear();
+  c->P.peer_n = 0;
+  return PM_OK;
 }
 
 pm_status pm_dist_read_flag(pm_ctx c, int32_t *need_rebuild) {

@@ -104,6 +104,11 @@ struct Params {
   int reach;        // stencil half-width in cells: 1 (side >= r_v) or 2 (side >= r_v/2);
                     // kept out of Grid: the sweeps' hot constants stay where they were
   DEM dem;
+  // fused ghost refresh (decomposed LJ): the sweep's epilogue stores each new
+  // position straight into the peers' ghost slots (peer_pos[peer][buffer]);
+  // appended last so the hot constants above keep their offsets
+  int peer_n;
+  float4 *peer_pos[26][2];
 };
 
 // Device buffers (pointers fixed between reallocations; captured in graphs).
@@ -141,6 +146,8 @@ struct Bufs {
   int32_t *big_cells;  // cells with > 32 particles (block-level sort)
   int32_t *cnt;        // [n] neighbour row lengths
   struct State *st;    // device-resident state
+  int32_t *ps_off;     // fused refresh: per local particle, its destinations
+  int2 *ps_dst;        //   ps_dst[ps_off[i] .. ps_off[i+1]) = (peer, ghost slot)
 };
 
 // Device-resident mutable state (one per context).
@@ -349,6 +356,10 @@ void launch_verlet_shifts(const Params &P, const Bufs &B, int64_t n, const int64
                           int8_t *col_shift, cudaStream_t s);
 void launch_verlet_export(const Bufs &B, int64_t n, const int64_t *row_ptr, int64_t *col_gid,
                           cudaStream_t s);
+void launch_exclusive_scan(int32_t *count, int32_t *start, int32_t *tmp, int n, cudaStream_t s);
+int scan_tiles(int n);
+void launch_peer_csr(const Bufs &B, const int *send_idx, const int *dst_peer, const int *dst_slot,
+                     int nsend, int32_t *cnt, int n, int32_t *tmp, cudaStream_t s);
 void launch_lj_step_mode(const Params &P, const Bufs &B, int64_t n, float dt, int mode,
                          cudaStream_t s);
 int dist_record_bytes(int what);

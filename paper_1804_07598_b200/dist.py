@@ -289,7 +289,7 @@ class DistSim:
     member per process) or LoopbackTransport (all members local)."""
 
     def __init__(self, decomp: Decomp, members: dict, transport, dt=0.005, device="cuda",
-                 stream=None):
+                 stream=None, peer=None):
         import contextlib
         import torch
         self.torch = torch
@@ -307,6 +307,11 @@ class DistSim:
         self.multi = hasattr(transport, "exchange_all")  # all local members at once
         self.dem = False      # DEM runs: migrations carry contact histories
         self.prof = None      # list: (start, end) CUDA events around each step's sweep
+        # fused ghost refresh: the sweep stores new positions straight into
+        # the peers' ghost slots (loopback: same-process pointers; processes:
+        # CUDA IPC).  Opt-in: PM_DIST_PEER=1 or peer=True.
+        self.peer = bool(int(os.environ.get("PM_DIST_PEER", "0"))) if peer is None else peer
+        self._ipc_key = None
         self.ghost_seg = {}   # rank -> {peer: (off, n)} of the last ghost plan (send side)
         self.ghost_recv = {}  # rank -> {peer: n} received ghosts
         self.rebuilds = 0
@@ -399,7 +404,66 @@ class DistSim:
         self._message_round(pm.PM_MSG_GHOST)
         for ctx in self.m.values():
             ctx.dist_finish()
+        if self.peer:
+            self._peer_setup()
         self.rebuilds += 1
+
+    def _recv_off(self, q, r):
+        """First record of sender r among receiver q's ghost arrivals."""
+        off = 0
+        for p in self.D.peers(q):
+            if p == r:
+                return off
+            off += self.ghost_recv[q][p]
+        raise KeyError((q, r))
+
+    def _peer_setup(self):
+        """Fused ghost refresh tables after a rebuild: per ghost send entry its
+        peer index and the receiver's ghost slot; the peers' position buffers."""
+        t = self.torch
+        slots = {}
+        for r, ctx in self.m.items():
+            ng = sum(self.ghost_recv[r].values())
+            buf = t.empty(max(ng, 1), dtype=t.int32, device=self.device)
+            ctx.ghost_slots(buf if ng else None)
+            slots[r] = buf
+        if self.loop:
+            bufs = {r: ctx.pos_buffers() for r, ctx in self.m.items()}
+            for r, ctx in self.m.items():
+                peers = self.D.peers(r)
+                nsend = sum(n for _, n in self.ghost_seg[r].values())
+                dp = t.empty(max(nsend, 1), dtype=t.int32, device=self.device)
+                ds = t.empty(max(nsend, 1), dtype=t.int32, device=self.device)
+                for k, q in enumerate(peers):
+                    o, n = self.ghost_seg[r][q]
+                    if n:
+                        ro = self._recv_off(q, r)
+                        dp[o:o + n] = k
+                        ds[o:o + n] = slots[q][ro:ro + n]
+                ctx.peer_setup([bufs[q] for q in peers], dp, ds)
+            return
+        # processes: the receivers return their slot slices (reverse of the
+        # ghost round), position buffers through CUDA IPC
+        (r, ctx), = self.m.items()
+        peers = self.D.peers(r)
+        sends = {q: slots[r][self._recv_off(r, q):self._recv_off(r, q) + self.ghost_recv[r][q]]
+                 for q in peers}
+        nsend = sum(n for _, n in self.ghost_seg[r].values())
+        ds = t.empty(max(nsend, 1), dtype=t.int32, device=self.device)
+        dp = t.empty(max(nsend, 1), dtype=t.int32, device=self.device)
+        recvs = {q: ds[o:o + n] for q, (o, n) in self.ghost_seg[r].items()}
+        self.tr.exchange(sends, recvs)
+        for k, q in enumerate(peers):
+            o, n = self.ghost_seg[r][q]
+            dp[o:o + n] = k
+        import torch.distributed as tdist
+        hs = [None] * tdist.get_world_size()
+        tdist.all_gather_object(hs, ctx.ipc_handles())  # any rank may have reallocated
+        if self._ipc_key != hs:
+            ctx.ipc_close_all()
+            self._peer_bufs = [ctx.ipc_open(hs[q]) for q in peers]
+            self._ipc_key = hs
+        ctx.peer_setup(self._peer_bufs, dp, ds)
 
     def refresh(self):
         with self._ctxmgr():
@@ -457,7 +521,7 @@ class DistSim:
             if flag:
                 self._rebuild()
                 reb += 1
-            else:
+            elif not self.peer or s == 0:  # peer mode: the sweep refreshed the ghosts
                 self._refresh()
             last = s == nsteps - 1
             phase = pm.PM_PHASE_FINAL if last else pm.PM_PHASE_STEP

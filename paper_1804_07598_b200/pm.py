@@ -115,6 +115,12 @@ def lib(path: str = LIB_PATH):
         "pm_set_newton": (st, [vp, C.c_int32]),
         "pm_get_verlet_shifts": (st, [vp, vp]),
         "pm_dist_read_flag": (st, [vp, vp]),
+        "pm_dist_pos_buffers": (st, [vp, vp, vp]),
+        "pm_dist_ghost_slots": (st, [vp, vp]),
+        "pm_dist_peer_setup": (st, [vp, C.c_int32, vp, vp, vp, vp]),
+        "pm_dist_ipc_handles": (st, [vp, vp]),
+        "pm_dist_ipc_open": (st, [vp, vp, vp, vp]),
+        "pm_dist_ipc_close_all": (st, [vp]),
         "pm_dist_dem_init": (st, [vp]),
         "pm_dist_dem_step": (st, [vp, C.c_float, vp]),
         "pm_dist_refresh_pvw_pack": (st, [vp, vp]),
@@ -471,6 +477,38 @@ class DistContext(Context):
         f = C.c_int32(0)
         self._check(self.L.pm_dist_step(self.h, dt, phase, C.byref(f) if read_flag else None))
         return int(f.value)
+
+    def pos_buffers(self):
+        a, b = vp(), vp()
+        self._check(self.L.pm_dist_pos_buffers(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def ghost_slots(self, out):
+        """Copy the ghost slots (arrival order) into the int32 device tensor out."""
+        self._check(self.L.pm_dist_ghost_slots(self.h, _dev_ptr(out)))
+
+    def peer_setup(self, peer_bufs, dst_peer, dst_slot):
+        """peer_bufs: [(pos0, pos1)] device pointers per peer index; dst_peer /
+        dst_slot: int32 device tensors over the ghost send list."""
+        k = len(peer_bufs)
+        p0 = (vp * max(k, 1))(*[b[0] for b in peer_bufs])
+        p1 = (vp * max(k, 1))(*[b[1] for b in peer_bufs])
+        self._check(self.L.pm_dist_peer_setup(self.h, k, p0, p1, _dev_ptr(dst_peer),
+                                              _dev_ptr(dst_slot)))
+
+    def ipc_handles(self):
+        buf = (C.c_char * 128)()
+        self._check(self.L.pm_dist_ipc_handles(self.h, buf))
+        return bytes(buf)
+
+    def ipc_open(self, handles: bytes):
+        buf = (C.c_char * 128).from_buffer_copy(handles)
+        a, b = vp(), vp()
+        self._check(self.L.pm_dist_ipc_open(self.h, buf, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def ipc_close_all(self):
+        self._check(self.L.pm_dist_ipc_close_all(self.h))
 
     def read_flag(self):
         f = C.c_int32(0)
