@@ -364,7 +364,11 @@ def run_ours(args):
                      "kernel": "k_lj_step (force sweep + fused VV)",
                      "kernel_ms": force_ms, "kernel_share_of_step": force_ms / (ms / args.steps),
                      "alg_bytes_per_launch": alg_bytes,
-                     "alg_bytes_formula": "N*(4*nbar + 64)", "peak_source": peak_src},
+                     "alg_bytes_formula": "N*(4*nbar + 64)", "peak_source": peak_src,
+                     # SURVEY §8(d) second fraction: measured DRAM bytes (ncu
+                     # capture) over the same live duration
+                     "measured_frac": (traffic / (force_ms * 1e-3) / 1e9 / peak
+                                       if traffic else None)},
         "cpu_baseline": cpu,
         "e2e": {"value": n * args.steps / (e2e_ms * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps},
