@@ -342,8 +342,8 @@ def run_ours(args):
     h2d = (pos_h.numel() * 4 + vel_h.numel() * 4 + gid_h.numel() * 8)
     d2h = (out_pos.numel() * 4 + out_vel.numel() * 4)
 
-    sph = sph_pass(dev, stream)
-    dem = dem_run(dev, stream)
+    sph = None if args.no_extras else sph_pass(dev, stream)
+    dem = None if args.no_extras else dem_run(dev, stream)
     cpu = cpu_baseline() if not args.no_cpu_baseline else None
     launches = 2 * args.steps + 11 * stats["rebuilds"] + 3
     line = {
@@ -389,6 +389,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the SPH / DEM lines (tests)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

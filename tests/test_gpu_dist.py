@@ -539,3 +539,31 @@ def test_fused_ghost_refresh_matches_message_refresh(env, grid):
     assert ra == rb and ra >= 2
     for k in ("gid", "pos", "vel", "force"):
         assert np.array_equal(a[k], b[k]), k
+
+
+def test_bench_single_gpu_contract(env, tmp_path):
+    """`python bench.py` at N = 1 (short run): one JSON line with the
+    contract's keys -- whole-job value, roofline of the dominant kernel with
+    its fraction of the measured peak, e2e through host buffers, launch
+    count, clocks."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--steps", "30",
+                        "--warmup", "3", "--no-cpu-baseline", "--no-extras"],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    b = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "dtype", "config", "roofline", "e2e",
+              "gpu_launches", "clocks"):
+        assert k in b, k
+    assert b["n_gpus"] == 1 and b["steps"] == 30 and b["value"] > 1e9
+    rf = b["roofline"]
+    assert rf["bound"] == "hbm" and 0.1 < rf["frac"] < 1.0 and rf["achieved"] > 0
+    assert b["e2e"]["h2d_bytes_per_step"] > 0 and b["e2e"]["d2h_bytes_per_step"] > 0
+    assert b["gpu_launches"] >= 2 * 30
