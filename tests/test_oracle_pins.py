@@ -67,6 +67,28 @@ def test_lj_two_particle_spec_example(orc):
     assert res["F"][0, 0] > 0
 
 
+def test_lj_capped_force_closed_form(orc):
+    """Reading R22 (cfg5's capped LJ): below r_min = 0.8 sigma the pair force
+    has the magnitude of the plain force at r_min, 24 (2/0.8^13 - 1/0.8^7) =
+    758.674 (the SURVEY §8(c) value), along the pair axis, and the energy is
+    V(r_min); at and above r_min the capped pair is the plain one."""
+    f08 = 24.0 * (2.0 / 0.8 ** 13 - 1.0 / 0.8 ** 7)
+    assert f08 == pytest.approx(758.67, abs=5e-3)
+    pos = np.zeros((2, 4), np.float32)
+    pos[0, :3] = [2.0, 2.0, 2.0]
+    for d, capped in ((0.5, True), (0.25, True), (0.8125, False), (1.5, False)):
+        pos[1, :3] = [2.0, 2.0 + d, 2.0]  # exact fp32 offsets along y
+        res = orc.lj_rows(pos, [0, 0, 0], [8, 8, 8], [1, 1, 1], rc=2.5, r_min=0.8)
+        plain = orc.lj_rows(pos, [0, 0, 0], [8, 8, 8], [1, 1, 1], rc=2.5)
+        if capped:
+            assert res["F"][0] == pytest.approx([0.0, -f08, 0.0], rel=1e-12, abs=1e-9)
+            assert res["F"][1] == pytest.approx([0.0, f08, 0.0], rel=1e-12, abs=1e-9)
+            assert res["U"].sum() == pytest.approx(orc.lj_V(0.8), rel=1e-12)
+        else:
+            assert np.array_equal(res["F"], plain["F"])
+            assert res["U"].sum() == pytest.approx(plain["U"].sum(), rel=1e-15)
+
+
 def test_lj_cutoff_strict_and_periodic_image(orc):
     """R6 strict inclusion; the minimum image across a periodic face gives the
     same force as the direct pair (PAPER.md:166 periodic BCs)."""
