@@ -15,7 +15,7 @@ timeout 600 ncu --set full --import-source on --clock-control none -k regex:"k_l
   --launch-skip 20 --launch-count 12 -f -o gpurun_out/step_full python tools/prof_step.py --steps 200 \
   > gpurun_out/step_full.log 2>&1
 echo "step capture rc=$?"
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_sph_rates \
+PM_USE_GRAPHS=0 timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_sph_rates \
   --launch-skip 50 --launch-count 1 -f -o gpurun_out/sph_rates_full python tools/exp_sph_rate.py \
   > gpurun_out/sph_full.log 2>&1
 echo "sph capture rc=$?"

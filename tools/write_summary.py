@@ -26,7 +26,7 @@ for name in ("step_full", "sph_rates_full", "dem_step_full"):
     for r in summary(os.path.join(G, name + ".ncu-rep")):
         k = r["kernel"].replace("void ", "").replace("unnamed>::", "")
         caps.setdefault(k, []).append(r)
-lj = caps["k_lj_step<0>"]
+lj = next(v for k, v in caps.items() if k.startswith("k_lj_step<0"))
 traffic = sum(r["dram_read_MB"] + r["dram_write_MB"] for r in lj) / len(lj) * 1e6
 json.dump({"kernel": "k_lj_step<0> (force sweep + fused VV)", "bytes_per_launch": traffic,
            "source": "profiles/r01_ncu_summary.md (ncu --set full, tools/prof_step.py cfg2 "
@@ -46,9 +46,10 @@ L.append("- value %.4g particle-updates/s, %.1f us/step, %d rebuilds in %d steps
             b["config"]["mean_row"]))
 L.append("- dominant kernel %s: %.1f us/launch (CUDA events in the step graph), %.0f GB/s "
          "algorithmic = %.3f of measured HBM %.1f GB/s; share of step %.2f; DRAM traffic "
-         "%.0f MB/launch vs %.0f MB algorithmic"
+         "%.0f MB/launch vs %.0f MB algorithmic (measured-DRAM fraction %.3f)"
          % (rf["kernel"], 1e3 * rf["kernel_ms"], rf["achieved"], rf["frac"], rf["peak"],
-            rf["kernel_share_of_step"], traffic / 1e6, rf["alg_bytes_per_launch"] / 1e6))
+            rf["kernel_share_of_step"], traffic / 1e6, rf["alg_bytes_per_launch"] / 1e6,
+            traffic / (rf["kernel_ms"] * 1e-3) / 1e9 / rf["peak"]))
 L.append("- e2e (pinned host in/out through the C-ABI): %.4g PU/s" % b["e2e"]["value"])
 L.append("- SPH pass (cfg4, %d particles): %.2f ms; SPH time stepping (pm_sph_run): %.3f ms/step "
          "= %.4g particle-steps/s" % (b["sph"]["n_particles"], b["sph"]["pass_ms"],
