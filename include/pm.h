@@ -107,8 +107,9 @@ pm_status pm_set_lj(pm_ctx ctx, float epsilon, float sigma, float mass, float r_
  * velocity-Verlet update runs as a separate kernel; forces, energies and the
  * virial agree with the full list up to summation order (not bit-
  * reproducible run to run).  The lists are rebuilt at the next call that
- * needs them.  LJ only: SPH, DEM and decomposed contexts return PM_E_STATE
- * with half lists.  Default 0 (full lists: atomic-free, deterministic). */
+ * needs them.  LJ only: SPH and DEM return PM_E_STATE with half lists;
+ * decomposed contexts step them with the NEWTON_* phases and
+ * pm_dist_ghost_put_*.  Default 0 (full lists: atomic-free, deterministic). */
 pm_status pm_set_newton(pm_ctx ctx, int32_t on);
 
 /* Velocity limit of reading R22 (clustered BASELINE.json configs[4]): after
@@ -304,7 +305,15 @@ enum {
   PM_MSG_REFRESH_PVW = 4,  /* DEM runs: position + velocity + angular velocity */
   PM_MSG_MIGRATE_HIST = 5  /* DEM runs: contact histories of the migrating grains */
 };
-enum { PM_PHASE_PROLOGUE = 0, PM_PHASE_STEP = 1, PM_PHASE_FINAL = 2, PM_PHASE_FORCES = 3 };
+enum {
+  PM_PHASE_PROLOGUE = 0,
+  PM_PHASE_STEP = 1,
+  PM_PHASE_FINAL = 2,
+  PM_PHASE_FORCES = 3,
+  PM_PHASE_NEWTON_FORCES = 4,  /* half lists: F = 0, sweep (ghost shares stay on the ghosts) */
+  PM_PHASE_NEWTON_STEP = 5,    /* half lists, after pm_dist_ghost_put: kick / drift */
+  PM_PHASE_NEWTON_FINAL = 6    /* ... last half kick, forces kept */
+};
 
 /* Bytes per message record: migrate 64 (pos, vel, SPH previous-step velocity
  * or DEM angular velocity, gid, kind), ghost 32 (pos, gid, kind), refresh 16
@@ -393,6 +402,18 @@ pm_status pm_dist_ipc_close_all(pm_ctx ctx);
  * need_rebuild of pm_dist_step as a separate call, so a caller can time the
  * step kernels with events before the host round trip. */
 pm_status pm_dist_read_flag(pm_ctx ctx, int32_t *need_rebuild);
+
+/* Half (Newton) lists on a decomposed context (SURVEY §8(f) NEXT-1 with its
+ * reverse exchange; PAPER.md:116 ghost_put, :164 "compute every interaction
+ * pair only once"): rows keep owned partners later in the local order and
+ * ghost partners with a larger gid, so every pair -- also across a
+ * sub-domain face -- is computed on exactly one rank.  A step:
+ * pm_dist_step(NEWTON_FORCES) -> ghost_put (pack the shares accumulated on
+ * the ghost copies, 16 B each in arrival order, send them back to the owners
+ * with the ghost round's counts reversed, add them there) ->
+ * pm_dist_step(NEWTON_STEP or NEWTON_FINAL). */
+pm_status pm_dist_ghost_put_pack(pm_ctx ctx, void *send_dev);
+pm_status pm_dist_ghost_put_unpack(pm_ctx ctx, const void *recv_dev);
 
 /* Decomposed DEM (SURVEY §8(f) NEXT-4 on the §8(e) decomposition; PAPER.md:
  * 479 "collisions involving ghost particles need to be properly accounted for

@@ -335,6 +335,26 @@ __global__ void k_peer_fill(const int *__restrict__ send_idx, const int *__restr
   dst[off[i] + atomicAdd(&fill[i], 1)] = make_int2(dst_peer[e], dst_slot[e]);
 }
 
+// ghost_put (half lists across sub-domains, SURVEY NEXT-1 / PAPER.md:116):
+// the force shares a sub-domain accumulated on its ghost copies go back to
+// the owners (arrival order -> the owners' send order) and are added there
+__global__ void k_ghost_put_pack(Bufs B, const int *__restrict__ ghost_slot, int nghost,
+                                 float4 *__restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < nghost) out[e] = B.force[ghost_slot[e]];
+}
+
+__global__ void k_ghost_put_add(Bufs B, const int *__restrict__ send_idx, int nsend,
+                                const float4 *__restrict__ in) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nsend) return;
+  const float4 f = in[e];
+  float4 *p = B.force + send_idx[e];
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(f.x), "f"(f.y),
+               "f"(f.z), "f"(0.f)
+               : "memory");
+}
+
 inline unsigned nb(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
@@ -407,6 +427,12 @@ void launch_peer_csr(const Bufs &B, const int *send_idx, const int *dst_peer, co
   if (nsend > 0)
     k_peer_fill<<<nb(nsend), 256, 0, s>>>(send_idx, dst_peer, dst_slot, nsend, B.ps_off, cnt,
                                           B.ps_dst);
+}
+
+void launch_ghost_put(const Bufs &B, int pack, const int *idx, int m, void *buf, cudaStream_t s) {
+  if (m <= 0) return;
+  if (pack) k_ghost_put_pack<<<nb(m), 256, 0, s>>>(B, idx, m, reinterpret_cast<float4 *>(buf));
+  else k_ghost_put_add<<<nb(m), 256, 0, s>>>(B, idx, m, reinterpret_cast<const float4 *>(buf));
 }
 
 void launch_refresh_unpack(const Bufs &B, const int *ghost_slot, int nghost, const void *in,

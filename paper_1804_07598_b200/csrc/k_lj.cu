@@ -533,6 +533,18 @@ void launch_lj(const Params &P, const Bufs &B, int64_t n, int want_energy, cudaS
   }
 }
 
+// Decomposed half lists: the sweep alone (ghost shares accumulate in the
+// ghost slots until pm_dist_ghost_put), then the integrator alone.
+void launch_lj_half_forces(const Params &P, const Bufs &B, int64_t n, int want_energy,
+                           cudaStream_t s) {
+  if (n > 0) launch_lj_half(P, B, n, want_energy, s);
+}
+
+void launch_lj_half_integrate(const Params &P, const Bufs &B, int64_t n, float dt, int mode,
+                              cudaStream_t s) {
+  if (n > 0) k_lj_half_vv<<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode);
+}
+
 void launch_lj_step_mode(const Params &P, const Bufs &B, int64_t n, float dt, int mode,
                          cudaStream_t s) {
   if (n <= 0) return;

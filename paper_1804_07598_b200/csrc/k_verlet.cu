@@ -71,10 +71,21 @@ __device__ __forceinline__ void test8(const Params &P, const float4 *__restrict_
 // cell sort).  Lanes outside the current segment carry xi = +inf and never
 // hit.  An overflowing row keeps rewriting its last slot (min(k, cap-1)) and
 // the build is retried.
-template <bool SHIFTJ, bool PAIRMI, bool NEWTON>
+// NMODE: 0 full rows; 1 half rows (j > i); 2 half rows of a decomposed
+// context: owned partners j > i, ghost partners by the globally consistent
+// rule gid_j > gid_i (each cross-boundary pair on exactly one rank, which
+// returns the partner's share by pm_dist_ghost_put)
+struct GhostRule {
+  const int32_t *kind;
+  const int64_t *gid;
+  long long gid_self;
+};
+
+template <bool SHIFTJ, bool PAIRMI, int NMODE>
 __device__ __forceinline__ void scan_run(const Params &P, const float4 *__restrict__ pos, int b,
                                          int e, const float4 &xi_eff, float3 csh, int pmi,
-                                         int self, int cap, int *__restrict__ row, int &k) {
+                                         int self, int cap, int *__restrict__ row, int &k,
+                                         const GhostRule &gr) {
   for (int j0 = b; j0 < e; j0 += 32) {
     unsigned msk = 0u;
     if (j0 + 32 <= e) {
@@ -90,7 +101,7 @@ __device__ __forceinline__ void scan_run(const Params &P, const float4 *__restri
       if (rem > 24) test8<SHIFTJ, PAIRMI, 24, true>(P, pos, j0, e, xi_eff, csh, pmi, msk);
       msk &= (1u << rem) - 1u;
     }
-    if (NEWTON) {  // half list (NEXT-1): only j > i, each pair once
+    if (NMODE == 1) {  // half list (NEXT-1): only j > i, each pair once
       const int t = self - j0;
       msk &= t < 0 ? 0xffffffffu : (t >= 31 ? 0u : (0xffffffffu << (t + 1)));
     } else if (self >= j0 && self < j0 + 32) {  // drop the particle itself
@@ -99,20 +110,25 @@ __device__ __forceinline__ void scan_run(const Params &P, const float4 *__restri
     while (msk) {
       const int u = __ffs(msk) - 1;
       msk &= msk - 1u;
+      if (NMODE == 2) {
+        const int j = j0 + u;
+        if ((gr.kind[j] & kGhostBit) ? (gr.gid[j] < gr.gid_self) : (j < self)) continue;
+      }
       row[(int64_t)min(k, cap - 1) << 5] = j0 + u;
       ++k;
     }
   }
 }
 
-template <bool NEWTON>
+template <int NMODE>
 __device__ __forceinline__ void scan_any(const Params &P, const float4 *__restrict__ pos, int b,
                                          int e, const float4 &xi_eff, float3 csh, int pmi,
-                                         int self, int cap, int *__restrict__ row, int &k) {
+                                         int self, int cap, int *__restrict__ row, int &k,
+                                         const GhostRule &gr) {
   const bool sj = csh.x != 0.f || csh.y != 0.f || csh.z != 0.f;
-  if (pmi) scan_run<true, true, NEWTON>(P, pos, b, e, xi_eff, csh, pmi, self, cap, row, k);
-  else if (sj) scan_run<true, false, NEWTON>(P, pos, b, e, xi_eff, csh, 0, self, cap, row, k);
-  else scan_run<false, false, NEWTON>(P, pos, b, e, xi_eff, csh, 0, self, cap, row, k);
+  if (pmi) scan_run<true, true, NMODE>(P, pos, b, e, xi_eff, csh, pmi, self, cap, row, k, gr);
+  else if (sj) scan_run<true, false, NMODE>(P, pos, b, e, xi_eff, csh, 0, self, cap, row, k, gr);
+  else scan_run<false, false, NMODE>(P, pos, b, e, xi_eff, csh, 0, self, cap, row, k, gr);
 }
 
 // Thread per particle (row), warp-uniform candidate stream.  The warp's 32
@@ -126,8 +142,8 @@ __device__ __forceinline__ void scan_any(const Params &P, const float4 *__restri
 // the same pinned test).  All lanes read the same position each iteration
 // (broadcast), there is no divergence, and rows come out in a fixed order.
 // RCH: stencil half-width in cells (P.reach), 1 (27 cells) or 2 (125 cells);
-// NEWTON: half lists (P.newton)
-template <int RCH, bool NEWTON>
+// NMODE: row kind (scan_run)
+template <int RCH, int NMODE>
 __global__ void __launch_bounds__(256, 4) k_verlet(Params P, Bufs B, int n) {
   State *st = B.st;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -141,6 +157,12 @@ __global__ void __launch_bounds__(256, 4) k_verlet(Params P, Bufs B, int n) {
   const int nx = P.grid.n[0], ny = P.grid.n[1], nz = P.grid.n[2];
   const float4 *__restrict__ pos = B.pos[st->cur_pv];
   const float4 xi = active ? pos[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  GhostRule gr{nullptr, nullptr, 0};
+  if (NMODE == 2) {
+    gr.kind = B.kind[st->cur_id];
+    gr.gid = B.gid[st->cur_id];
+    gr.gid_self = active ? B.gid[st->cur_id][i] : 0;
+  }
   int cell = -1;
   if (active) {
     const int c0 = local_coord(P.box, P.grid, 0, xi.x);
@@ -220,14 +242,14 @@ __global__ void __launch_bounds__(256, 4) k_verlet(Params P, Bufs B, int n) {
         const float4 xe0 = mine ? make_float4(__fsub_rn(xi.x, lx0), __fsub_rn(xi.y, ly),
                                               __fsub_rn(xi.z, lz), 0.f)
                                 : make_float4(INF, INF, INF, 0.f);
-        scan_any<NEWTON>(P, pos, B.start[rowc + a0], B.start[rowc + b0 + 1], xe0,
-                 make_float3((pmi & 1) ? 0.f : sx0, shy, shz), pmi, i, cap, row, k);
+        scan_any<NMODE>(P, pos, B.start[rowc + a0], B.start[rowc + b0 + 1], xe0,
+                 make_float3((pmi & 1) ? 0.f : sx0, shy, shz), pmi, i, cap, row, k, gr);
         if (b1 >= a1) {
           const float4 xe1 = mine ? make_float4(__fsub_rn(xi.x, lx1), __fsub_rn(xi.y, ly),
                                                 __fsub_rn(xi.z, lz), 0.f)
                                   : make_float4(INF, INF, INF, 0.f);
-          scan_any<NEWTON>(P, pos, B.start[rowc + a1], B.start[rowc + b1 + 1], xe1,
-                   make_float3(sx1, shy, shz), pmi & ~1, i, cap, row, k);
+          scan_any<NMODE>(P, pos, B.start[rowc + a1], B.start[rowc + b1 + 1], xe1,
+                   make_float3(sx1, shy, shz), pmi & ~1, i, cap, row, k, gr);
         }
       }
     }
@@ -302,12 +324,14 @@ void launch_verlet(const Params &P, const Bufs &B, int64_t n, cudaStream_t s) {
   k_reset_build_stats<<<1, 1, 0, s>>>(B.st);
   if (n <= 0) return;
   const unsigned g = (unsigned)((n + 255) / 256);
+  const int nm = P.newton ? (P.dist ? 2 : 1) : 0;
   if (P.reach == 2) {
-    if (P.newton) k_verlet<2, true><<<g, 256, 0, s>>>(P, B, (int)n);
-    else k_verlet<2, false><<<g, 256, 0, s>>>(P, B, (int)n);
+    if (nm == 1) k_verlet<2, 1><<<g, 256, 0, s>>>(P, B, (int)n);
+    else k_verlet<2, 0><<<g, 256, 0, s>>>(P, B, (int)n);
   } else {
-    if (P.newton) k_verlet<1, true><<<g, 256, 0, s>>>(P, B, (int)n);
-    else k_verlet<1, false><<<g, 256, 0, s>>>(P, B, (int)n);
+    if (nm == 2) k_verlet<1, 2><<<g, 256, 0, s>>>(P, B, (int)n);
+    else if (nm == 1) k_verlet<1, 1><<<g, 256, 0, s>>>(P, B, (int)n);
+    else k_verlet<1, 0><<<g, 256, 0, s>>>(P, B, (int)n);
   }
 }
 

@@ -790,8 +790,6 @@ pm_status pm_set_lj(pm_ctx c, float eps, float sigma, float mass, float r_min) {
 
 pm_status pm_set_newton(pm_ctx c, int32_t on) {
   if (!c) return PM_E_INVAL;
-  if (on && c->dist)
-    return set_err(c, PM_E_STATE, "pm_set_newton: single (non-decomposed) contexts only");
   c->P.newton = on ? 1 : 0;
   c->list_valid = false;  // the next build emits the other kind of rows
   c->forces_valid = false;
@@ -905,7 +903,7 @@ pm_status pm_compute_lj(pm_ctx c, int32_t want_energy) {
   launch_lj(c->P, c->B, c->n, want_energy, c->stream);
   s = sync_check(c, "pm_compute_lj");
   if (s) return s;
-  c->forces_valid = true;
+  c->forces_valid = !(c->P.newton && c->dist);  // decomposed half lists: ghost_put first
   return PM_OK;
 }
 
@@ -1590,7 +1588,6 @@ int32_t pm_record_bytes(int32_t what) {
 
 pm_status pm_set_decomposition(pm_ctx c, const int32_t pgrid[3], const int32_t pcoord[3]) {
   if (!c || !pgrid || !pcoord) return PM_E_INVAL;
-  if (c->P.newton) return set_err(c, PM_E_STATE, "decomposed contexts need full lists");
   if (c->cell_div != 1)
     return set_err(c, PM_E_STATE, "decomposed contexts use cell_div 1 (cells >= r_v)");
   if (!c->have_domain || !c->have_cutoff)
@@ -1854,6 +1851,8 @@ pm_status pm_dist_step(pm_ctx c, float dt, int32_t phase, int32_t *need_rebuild)
       break;
     case PM_PHASE_STEP:
     case PM_PHASE_FINAL:
+      if (c->P.newton)
+        return set_err(c, PM_E_STATE, "pm_dist_step: half lists step in NEWTON_* phases");
       if (!c->list_valid) return set_err(c, PM_E_STATE, "pm_dist_step: no Verlet list");
       launch_lj_step_mode(c->P, c->B, c->n, dt, phase == PM_PHASE_STEP ? kModeInner : kModeFinal,
                           c->stream);
@@ -1862,7 +1861,21 @@ pm_status pm_dist_step(pm_ctx c, float dt, int32_t phase, int32_t *need_rebuild)
     case PM_PHASE_FORCES:
       if (!c->list_valid) return set_err(c, PM_E_STATE, "pm_dist_step: no Verlet list");
       launch_lj(c->P, c->B, c->n, 0, c->stream);
-      c->forces_valid = true;
+      c->forces_valid = !c->P.newton;  // half lists: valid after pm_dist_ghost_put
+      break;
+    case PM_PHASE_NEWTON_FORCES:
+      if (!c->P.newton) return set_err(c, PM_E_STATE, "pm_dist_step: no half lists");
+      if (!c->list_valid) return set_err(c, PM_E_STATE, "pm_dist_step: no Verlet list");
+      launch_lj_half_forces(c->P, c->B, c->n, 0, c->stream);
+      c->forces_valid = false;  // until the ghost shares are back (pm_dist_ghost_put)
+      break;
+    case PM_PHASE_NEWTON_STEP:
+    case PM_PHASE_NEWTON_FINAL:
+      if (!c->P.newton || !c->forces_valid)
+        return set_err(c, PM_E_STATE, "pm_dist_step: half-list forces not complete");
+      launch_lj_half_integrate(c->P, c->B, c->n, dt,
+                               phase == PM_PHASE_NEWTON_STEP ? kModeInner : kModeFinal,
+                               c->stream);
       break;
     default:
       return set_err(c, PM_E_INVAL, "pm_dist_step: bad phase");
@@ -1973,6 +1986,24 @@ pm_status pm_dist_ipc_close_all(pm_ctx c) {
   c->ipc_open.clear();
   c->P.peer_n = 0;
   return PM_OK;
+}
+
+pm_status pm_dist_ghost_put_pack(pm_ctx c, void *send_dev) {
+  if (!c) return PM_E_INVAL;
+  if (c->sticky) return c->sticky;
+  if (c->n_ghost > 0 && !send_dev) return set_err(c, PM_E_INVAL, "null buffer");
+  launch_ghost_put(c->B, 1, c->d_gslot, (int)c->n_ghost, send_dev, c->stream);
+  return check_launch(c, "pm_dist_ghost_put_pack");
+}
+
+pm_status pm_dist_ghost_put_unpack(pm_ctx c, const void *recv_dev) {
+  if (!c) return PM_E_INVAL;
+  if (c->sticky) return c->sticky;
+  if (c->n_send > 0 && !recv_dev) return set_err(c, PM_E_INVAL, "null buffer");
+  launch_ghost_put(c->B, 0, c->d_send_idx, (int)c->n_send, const_cast<void *>(recv_dev),
+                   c->stream);
+  c->forces_valid = true;
+  return check_launch(c, "pm_dist_ghost_put_unpack");
 }
 
 pm_status pm_dist_read_flag(pm_ctx c, int32_t *need_rebuild) {

@@ -360,6 +360,11 @@ void launch_exclusive_scan(int32_t *count, int32_t *start, int32_t *tmp, int n, 
 int scan_tiles(int n);
 void launch_peer_csr(const Bufs &B, const int *send_idx, const int *dst_peer, const int *dst_slot,
                      int nsend, int32_t *cnt, int n, int32_t *tmp, cudaStream_t s);
+void launch_lj_half_forces(const Params &P, const Bufs &B, int64_t n, int want_energy,
+                           cudaStream_t s);
+void launch_lj_half_integrate(const Params &P, const Bufs &B, int64_t n, float dt, int mode,
+                              cudaStream_t s);
+void launch_ghost_put(const Bufs &B, int pack, const int *idx, int m, void *buf, cudaStream_t s);
 void launch_lj_step_mode(const Params &P, const Bufs &B, int64_t n, float dt, int mode,
                          cudaStream_t s);
 int dist_record_bytes(int what);

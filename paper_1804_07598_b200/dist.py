@@ -289,7 +289,7 @@ class DistSim:
     member per process) or LoopbackTransport (all members local)."""
 
     def __init__(self, decomp: Decomp, members: dict, transport, dt=0.005, device="cuda",
-                 stream=None, peer=None):
+                 stream=None, peer=None, newton=False):
         import contextlib
         import torch
         self.torch = torch
@@ -312,6 +312,12 @@ class DistSim:
         # CUDA IPC).  Opt-in: PM_DIST_PEER=1 or peer=True.
         self.peer = bool(int(os.environ.get("PM_DIST_PEER", "0"))) if peer is None else peer
         self._ipc_key = None
+        # half (Newton) lists across sub-domains: pairs once, the ghosts'
+        # force shares go back to their owners every step (ghost_put)
+        self.newton = newton
+        if newton:
+            for ctx in members.values():
+                ctx.set_newton(True)
         self.ghost_seg = {}   # rank -> {peer: (off, n)} of the last ghost plan (send side)
         self.ghost_recv = {}  # rank -> {peer: n} received ghosts
         self.rebuilds = 0
@@ -501,8 +507,40 @@ class DistSim:
         from . import pm
         with self._ctxmgr():
             self._rebuild()
+            if self.newton:
+                self._newton_forces()
+            else:
+                for ctx in self.m.values():
+                    ctx.dist_step(self.dt, pm.PM_PHASE_FORCES)
+
+    def _newton_forces(self):
+        from . import pm
         for ctx in self.m.values():
-            ctx.dist_step(self.dt, pm.PM_PHASE_FORCES)
+            ctx.dist_step(self.dt, pm.PM_PHASE_NEWTON_FORCES)
+        self._ghost_put()
+
+    def _ghost_put(self):
+        """The force shares on the ghost copies back to their owners (16 B per
+        ghost): the ghost round reversed -- a receiver's arrivals per peer go
+        back to that peer, which adds them in its send order."""
+        sends, recvs, rb = {}, {}, {}
+        for r, ctx in self.m.items():
+            ng = sum(self.ghost_recv[r].values())
+            buf = self._buf(("gpsend", r), ng * 16)
+            ctx.ghost_put_pack(buf if ng else None)
+            off, sends[r] = 0, {}
+            for p in self.D.peers(r):
+                n = self.ghost_recv[r][p]
+                sends[r][p] = buf[off * 16:(off + n) * 16]
+                off += n
+            nsend = sum(n for _, n in self.ghost_seg[r].values())
+            rbuf = self._buf(("gprecv", r), nsend * 16)
+            rb[r] = (rbuf, nsend)
+            recvs[r] = {p: rbuf[o * 16:(o + n) * 16] for p, (o, n) in self.ghost_seg[r].items()}
+        self._exchange(sends, recvs)
+        for r, ctx in self.m.items():
+            rbuf, nsend = rb[r]
+            ctx.ghost_put_unpack(rbuf if nsend else None)
 
     def run(self, nsteps):
         """nsteps velocity-Verlet steps (forces valid on entry and exit)."""
@@ -524,7 +562,11 @@ class DistSim:
             elif not self.peer or s == 0:  # peer mode: the sweep refreshed the ghosts
                 self._refresh()
             last = s == nsteps - 1
-            phase = pm.PM_PHASE_FINAL if last else pm.PM_PHASE_STEP
+            if self.newton:  # sweep, shares back to the owners, then integrate
+                self._newton_forces()
+                phase = pm.PM_PHASE_NEWTON_FINAL if last else pm.PM_PHASE_NEWTON_STEP
+            else:
+                phase = pm.PM_PHASE_FINAL if last else pm.PM_PHASE_STEP
             if self.prof is not None:  # CUDA events around the force/VV kernels
                 e0 = self.torch.cuda.Event(enable_timing=True)
                 e1 = self.torch.cuda.Event(enable_timing=True)
@@ -601,6 +643,9 @@ class DistSim:
         for ctx in self.m.values():
             th = ctx.thermo()
             vals += [th["ke"], th["pe_shift"], th["npairs"]]
+        if self.newton:  # the energy pass rewrote F without the ghost shares
+            with self._ctxmgr():
+                self._newton_forces()
         if not self.loop:
             vals = self.tr.allreduce_sum(vals)
         return dict(ke=vals[0], pe_shift=vals[1], npairs=vals[2])

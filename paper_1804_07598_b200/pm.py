@@ -115,6 +115,8 @@ def lib(path: str = LIB_PATH):
         "pm_set_newton": (st, [vp, C.c_int32]),
         "pm_get_verlet_shifts": (st, [vp, vp]),
         "pm_dist_read_flag": (st, [vp, vp]),
+        "pm_dist_ghost_put_pack": (st, [vp, vp]),
+        "pm_dist_ghost_put_unpack": (st, [vp, vp]),
         "pm_dist_pos_buffers": (st, [vp, vp, vp]),
         "pm_dist_ghost_slots": (st, [vp, vp]),
         "pm_dist_peer_setup": (st, [vp, C.c_int32, vp, vp, vp, vp]),
@@ -382,6 +384,7 @@ class Context:
 PM_MSG_MIGRATE, PM_MSG_GHOST, PM_MSG_REFRESH, PM_MSG_REFRESH_PV = 0, 1, 2, 3
 PM_MSG_REFRESH_PVW, PM_MSG_MIGRATE_HIST = 4, 5
 PM_PHASE_PROLOGUE, PM_PHASE_STEP, PM_PHASE_FINAL, PM_PHASE_FORCES = 0, 1, 2, 3
+PM_PHASE_NEWTON_FORCES, PM_PHASE_NEWTON_STEP, PM_PHASE_NEWTON_FINAL = 4, 5, 6
 GHOST_BIT = 1 << 30
 
 
@@ -477,6 +480,12 @@ class DistContext(Context):
         f = C.c_int32(0)
         self._check(self.L.pm_dist_step(self.h, dt, phase, C.byref(f) if read_flag else None))
         return int(f.value)
+
+    def ghost_put_pack(self, send):
+        self._check(self.L.pm_dist_ghost_put_pack(self.h, _dev_ptr(send)))
+
+    def ghost_put_unpack(self, recv):
+        self._check(self.L.pm_dist_ghost_put_unpack(self.h, _dev_ptr(recv)))
 
     def pos_buffers(self):
         a, b = vp(), vp()

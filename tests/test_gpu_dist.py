@@ -437,19 +437,23 @@ def test_decomposed_dem_matches_single(env):
 
 def test_api_state_errors(env):
     """Call-order and mode errors of the newer entry points report
-    PM_E_STATE (-2) / PM_E_INVAL (-1) instead of running: half lists on a
-    decomposed context, SPH / DEM stepping of a decomposed context before
-    its init, SPH and DEM on half lists, the record size of an unknown kind."""
+    PM_E_STATE (-2) / PM_E_INVAL (-1) instead of running: SPH / DEM stepping
+    of a decomposed context before its init, full-list step phases on half
+    lists, SPH and DEM on half lists, the record size of an unknown kind."""
     pm, dist = env
     s = inputs.lj_lattice_system(16, 16, 16, jitter_key=(44,))
     D = dist.Decomp((2, 1, 1))
     m = dist.make_member(s.subset(np.where(dist.owner_of(s, D) == 0)[0]), D, 0)
-    for call, code in ((lambda: m.set_newton(True), -2), (lambda: m.dist_sph_rates(), -2),
+    for call, code in ((lambda: m.dist_sph_rates(), -2),
                        (lambda: m.dist_sph_update(1e-4), -2), (lambda: m.dist_dem_step(1e-4), -2),
                        (lambda: m.dist_dem_init(), -2)):
         with pytest.raises(pm.PMError) as e:
             call()
         assert e.value.code == code
+    m.set_newton(True)  # decomposed half lists step in the NEWTON_* phases only
+    with pytest.raises(pm.PMError) as e:
+        m.dist_step(0.005, pm.PM_PHASE_STEP)
+    assert e.value.code == -2
     m.close()
     assert pm.record_bytes(6) == -1 and pm.record_bytes(-1) == -1
     assert [pm.record_bytes(k) for k in range(6)] == [64, 32, 16, 32, 48, 592]
@@ -567,3 +571,52 @@ def test_bench_single_gpu_contract(env, tmp_path):
     assert rf["bound"] == "hbm" and 0.1 < rf["frac"] < 1.0 and rf["achieved"] > 0
     assert b["e2e"]["h2d_bytes_per_step"] > 0 and b["e2e"]["d2h_bytes_per_step"] > 0
     assert b["gpu_launches"] >= 2 * 30
+
+
+@pytest.mark.parametrize("grid", [(2, 1, 1), (2, 2, 2)])
+def test_decomposed_newton_lists_with_ghost_put(env, grid):
+    """Half (Newton) lists across sub-domains (NEXT-1 with ghost_put): every
+    pair -- also across a face -- is computed on exactly one rank (owned
+    partners later in the local order, ghost partners with a larger gid), the
+    ghosts' force shares go back to their owners.  Forces match the
+    single-context full-list forces, the global pair count equals it exactly
+    (each pair counted twice as ordered pairs), and 40 steps with rebuilds and
+    migration follow the full-list trajectory."""
+    import torch
+    pm, dist = env
+    s = inputs.lj_lattice_system(18, 18, 18, jitter_key=(46,), vel_key=(146,))
+    ref = single(pm, s)
+    ref.build_verlet()
+    ref.compute_lj(want_energy=True)
+    rst = pm.sorted_by_gid(ref.get_state())
+    th_ref = ref.thermo(recompute=False)
+    D = dist.Decomp(grid)
+    owner = dist.owner_of(s, D)
+    stream = torch.cuda.Stream()
+    members = {r: dist.make_member(s.subset(np.where(owner == r)[0]), D, r, stream=stream)
+               for r in range(D.size)}
+    sim = dist.DistSim(D, members, dist.LoopbackTransport(members), stream=stream, newton=True)
+    sim.start()
+    torch.cuda.synchronize()
+    got = owned_union(pm, sim)
+    F, Fr = got["force"][:, :3].astype(np.float64), rst["force"][:, :3].astype(np.float64)
+    assert np.max(np.abs(F - Fr)) / np.sqrt(np.mean(Fr ** 2)) <= 1e-4
+    th = sim.thermo()
+    assert th["npairs"] == th_ref["npairs"]
+    assert th["pe_shift"] == pytest.approx(th_ref["pe_shift"], rel=1e-5)
+    got = owned_union(pm, sim)  # forces restored after the energy pass
+    assert np.max(np.abs(got["force"][:, :3] - Fr)) / np.sqrt(np.mean(Fr ** 2)) <= 1e-4
+    r1 = ref.step_vv(0.005, 40)
+    reb = sim.run(40)
+    torch.cuda.synchronize()
+    assert reb >= 2 and r1["rebuilds"] >= 2
+    got = owned_union(pm, sim)
+    rst = pm.sorted_by_gid(ref.get_state())
+    L = s.hi.astype(np.float64)
+    d = got["pos"][:, :3].astype(np.float64) - rst["pos"][:, :3]
+    d -= L * np.round(d / L)
+    assert np.max(np.abs(d)) < 1e-3
+    assert np.max(np.abs(got["vel"][:, :3] - rst["vel"][:, :3])) < 1e-2
+    ref.close()
+    for m in members.values():
+        m.close()
