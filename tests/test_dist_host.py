@@ -378,3 +378,61 @@ def test_dem_migration_histories_ride_with_grains_gloo_world2():
         assert [[a - 1000, d, k] for a, d, k in hist] == mig
         total += len(mig)
     assert total > 0
+
+
+class FakePutCtx(FakeCtx):
+    """Packs one 16-byte record per arrived ghost: (rank, arrival index)."""
+
+    def ghost_put_pack(self, buf):
+        import torch
+        n = buf.numel() // 16 if buf is not None else 0
+        if n:
+            v = buf.view(torch.int64).view(-1, 2)
+            v[:, 0] = self.rank
+            v[:, 1] = torch.arange(n)
+
+    def ghost_put_unpack(self, buf):
+        import torch
+        self.put = [] if buf is None else buf.view(torch.int64).view(-1, 2).tolist()
+
+
+def _put_worker(rank, world, port, grid, out):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1804_07598_b200.pm as pmm
+    pmm.record_bytes = lambda what: 24
+    D = Decomp(grid)
+    ctx = FakePutCtx(rank, D, rng_key=(41, rank))
+    sim = DistSim(D, {rank: ctx}, TorchTransport(device=None), device="cpu")
+    sim._message_round(pmm.PM_MSG_GHOST)
+    sim._ghost_put()
+    sent = ctx.counts[pmm.PM_MSG_GHOST][0].tolist()
+    out.put((rank, sent, sim.ghost_recv[rank], ctx.put))
+    dist.destroy_process_group()
+
+
+def test_ghost_put_reverses_the_ghost_round_gloo_world2():
+    """ghost_put (NEXT-1 half lists across sub-domains) over world-size-2
+    gloo: each arrived ghost's share goes back to the rank that sent the
+    ghost, landing in that rank's send order."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_put_worker, args=(r, 2, port, (2, 1, 1), q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        item = q.get(timeout=120)
+        res[item[0]] = item[1:]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in (0, 1):
+        sent, _, put = res[r]
+        other = 1 - r
+        n_sent = sum(sent)  # records r packed as ghosts for the other rank
+        assert res[other][1][r] == n_sent  # the other rank received them
+        assert put == [[other, k] for k in range(n_sent)]
