@@ -315,6 +315,8 @@ class DistSim:
         # half (Newton) lists across sub-domains: pairs once, the ghosts'
         # force shares go back to their owners every step (ghost_put)
         self.newton = newton
+        if newton and self.peer:  # the half-list integrator has no fused stores
+            raise ValueError("DistSim: the fused ghost refresh needs full lists (newton=False)")
         if newton:
             for ctx in members.values():
                 ctx.set_newton(True)
