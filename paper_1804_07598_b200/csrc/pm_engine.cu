@@ -1932,6 +1932,8 @@ pm_status pm_dist_peer_setup(pm_ctx c, int32_t npeers, void *const *peer_pos0,
   if (s) return s;
   if (!c->dist) return set_err(c, PM_E_STATE, "pm_dist_peer_setup: no decomposition");
   if (npeers < 0 || npeers > 26) return set_err(c, PM_E_INVAL, "pm_dist_peer_setup: npeers");
+  if (npeers > 0 && c->P.newton)
+    return set_err(c, PM_E_STATE, "pm_dist_peer_setup: the fused refresh needs full lists");
   cudaSetDevice(c->device);
   if (npeers == 0) {
     c->P.peer_n = 0;
