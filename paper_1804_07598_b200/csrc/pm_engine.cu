@@ -242,6 +242,18 @@ pm_status sync_check(pm_ctx c, const char *what) {
   return PM_OK;
 }
 
+// Scratch device allocation freed on every return path of a getter.
+template <class T>
+struct DevTmp {
+  T *p = nullptr;
+  DevTmp() = default;
+  DevTmp(const DevTmp &) = delete;
+  DevTmp &operator=(const DevTmp &) = delete;
+  ~DevTmp() {
+    if (p) cudaFree(p);
+  }
+};
+
 template <class T>
 cudaError_t grow_keep(T **p, int64_t count, int64_t keep, cudaStream_t s) {
   T *q = nullptr;
@@ -1166,15 +1178,14 @@ pm_status pm_set_rho(pm_ctx c, const float *rho, int32_t mem) {
   const int64_t n = c->n;
   if (n == 0) return PM_OK;
   const float *d = rho;
-  float *tmp = nullptr;
+  DevTmp<float> tmp;
   if (mem != PM_DEVICE) {
-    CUDA_TRY(c, cudaMalloc((void **)&tmp, 4 * n));
-    CUDA_TRY(c, cudaMemcpyAsync(tmp, rho, 4 * n, cudaMemcpyHostToDevice, c->stream));
-    d = tmp;
+    CUDA_TRY(c, cudaMalloc((void **)&tmp.p, 4 * n));
+    CUDA_TRY(c, cudaMemcpyAsync(tmp.p, rho, 4 * n, cudaMemcpyHostToDevice, c->stream));
+    d = tmp.p;
   }
   launch_sph_set_rho(c->P, c->B, n, d, c->stream);
   s = sync_check(c, "pm_set_rho");
-  if (tmp) cudaFree(tmp);
   if (s) return s;
   c->rho_valid = true;
   return PM_OK;
@@ -1467,15 +1478,13 @@ pm_status pm_get_verlet(pm_ctx c, int64_t *row_ptr, int64_t *col_gid) {
   for (int64_t i = 0; i < n; ++i) row_ptr[i + 1] = row_ptr[i] + cnt[(size_t)i];
   const int64_t nnz = row_ptr[n];
   if (!col_gid || nnz == 0) return PM_OK;
-  int64_t *d_rp = nullptr, *d_col = nullptr;
-  CUDA_TRY(c, cudaMalloc((void **)&d_rp, 8 * (n + 1)));
-  CUDA_TRY(c, cudaMalloc((void **)&d_col, 8 * nnz));
-  CUDA_TRY(c, cudaMemcpyAsync(d_rp, row_ptr, 8 * (n + 1), cudaMemcpyHostToDevice, c->stream));
-  launch_verlet_export(c->B, n, d_rp, d_col, c->stream);
-  CUDA_TRY(c, cudaMemcpyAsync(col_gid, d_col, 8 * nnz, cudaMemcpyDeviceToHost, c->stream));
+  DevTmp<int64_t> d_rp, d_col;
+  CUDA_TRY(c, cudaMalloc((void **)&d_rp.p, 8 * (n + 1)));
+  CUDA_TRY(c, cudaMalloc((void **)&d_col.p, 8 * nnz));
+  CUDA_TRY(c, cudaMemcpyAsync(d_rp.p, row_ptr, 8 * (n + 1), cudaMemcpyHostToDevice, c->stream));
+  launch_verlet_export(c->B, n, d_rp.p, d_col.p, c->stream);
+  CUDA_TRY(c, cudaMemcpyAsync(col_gid, d_col.p, 8 * nnz, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  cudaFree(d_rp);
-  cudaFree(d_col);
   return check_launch(c, "pm_get_verlet");
 }
 
@@ -1491,16 +1500,14 @@ pm_status pm_get_verlet_shifts(pm_ctx c, int8_t *col_shift) {
   for (int64_t i = 0; i < n; ++i) rp[(size_t)i + 1] = rp[(size_t)i] + cnt[(size_t)i];
   const int64_t nnz = rp[(size_t)n];
   if (nnz == 0) return PM_OK;
-  int64_t *d_rp = nullptr;
-  int8_t *d_sh = nullptr;
-  CUDA_TRY(c, cudaMalloc((void **)&d_rp, 8 * (n + 1)));
-  CUDA_TRY(c, cudaMalloc((void **)&d_sh, 3 * nnz));
-  CUDA_TRY(c, cudaMemcpyAsync(d_rp, rp.data(), 8 * (n + 1), cudaMemcpyHostToDevice, c->stream));
-  launch_verlet_shifts(c->P, c->B, n, d_rp, d_sh, c->stream);
-  CUDA_TRY(c, cudaMemcpyAsync(col_shift, d_sh, 3 * nnz, cudaMemcpyDeviceToHost, c->stream));
+  DevTmp<int64_t> d_rp;
+  DevTmp<int8_t> d_sh;
+  CUDA_TRY(c, cudaMalloc((void **)&d_rp.p, 8 * (n + 1)));
+  CUDA_TRY(c, cudaMalloc((void **)&d_sh.p, 3 * nnz));
+  CUDA_TRY(c, cudaMemcpyAsync(d_rp.p, rp.data(), 8 * (n + 1), cudaMemcpyHostToDevice, c->stream));
+  launch_verlet_shifts(c->P, c->B, n, d_rp.p, d_sh.p, c->stream);
+  CUDA_TRY(c, cudaMemcpyAsync(col_shift, d_sh.p, 3 * nnz, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  cudaFree(d_rp);
-  cudaFree(d_sh);
   return check_launch(c, "pm_get_verlet_shifts");
 }
 
