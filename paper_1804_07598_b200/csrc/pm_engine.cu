@@ -726,7 +726,7 @@ void pm_destroy(pm_ctx c) {
   for (void *p : ptrs)
     if (p) cudaFree(p);
   void *dem_ptrs[] = {B.omega[0], B.omega[1], B.torque, B.hist, B.hist_old, B.nbr_old,
-                      B.slice_off_old, B.cnt_old};
+                      B.slice_off_old, B.cnt_old, B.gid_old, c->d_stay_old, c->d_hist_in};
   for (void *p : dem_ptrs)
     if (p) cudaFree(p);
   void *dptrs[] = {c->d_mask, c->d_blk, c->d_order, c->d_dirbase, c->d_list,
