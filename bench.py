@@ -185,6 +185,36 @@ def sph_pass(dev, stream, repeats=10):
                     "rebuilds": r["rebuilds"], "dt_min": r["dt_min"], "dt_max": r["dt_max"]}}
 
 
+def cfg1_latency(dev, stream, repeats=20):
+    """BJ configs[0]: one K1-K6 pass on 4,096 particles --
+    cell list + Verlet build + LJ forces -- latency in us (launch-bound: the
+    data sits in L1/L2, so no roofline is meaningful here)."""
+    import torch
+    from paper_1804_07598_b200 import inputs, pm
+    s = inputs.cfg1()
+    c = pm.Context(device=dev, stream=stream.cuda_stream)
+    c.set_domain(s.lo, s.hi, s.periodic)
+    c.set_cutoff(2.5, 0.3)
+    c.set_lj(1.0, 1.0, 1.0, 0.0)
+    c.place(s.pos, s.vel, s.gid)
+    for _ in range(3):
+        c.build_verlet()
+        c.compute_lj()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(repeats):
+        c.build_verlet()
+        c.compute_lj()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    us = 1e3 * e0.elapsed_time(e1) / repeats
+    c.close()
+    return {"workload": "cfg1 (BJ configs[0]): SC 16^3 LJ, one pass = cell list + Verlet "
+                        "build + forces (each API call synchronises)",
+            "n_particles": s.n, "pass_us": us, "value": s.n / (us * 1e-6), "unit": UNIT}
+
+
 def dem_run(dev, stream, warm=300, steps=500):
     """DEM avalanche (inputs.dem_avalanche, 679,140 grains,
     PAPER.md:540-548) stepped by pm_dem_run; CUDA events on the context
@@ -342,6 +372,7 @@ def run_ours(args):
     h2d = (pos_h.numel() * 4 + vel_h.numel() * 4 + gid_h.numel() * 8)
     d2h = (out_pos.numel() * 4 + out_vel.numel() * 4)
 
+    cfg1 = None if args.no_extras else cfg1_latency(dev, stream)
     sph = None if args.no_extras else sph_pass(dev, stream)
     dem = None if args.no_extras else dem_run(dev, stream)
     cpu = cpu_baseline() if not args.no_cpu_baseline else None
@@ -374,6 +405,7 @@ def run_ours(args):
                 "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps},
         "gpu_launches": launches,
         "clocks": clk,
+        "cfg1": cfg1,
         "sph": sph,
         "dem": dem,
     }
