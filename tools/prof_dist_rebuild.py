@@ -1,3 +1,5 @@
+"""cProfile of DistSim rebuilds (loopback, cfg3 (2,1,1)): where the host time of
+a decomposed rebuild goes.  Usage: python tools/prof_dist_rebuild.py"""
 import cProfile, pstats, sys, os
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch

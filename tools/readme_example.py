@@ -1,3 +1,4 @@
+"""The README usage example, runnable: cfg2, 1000 velocity-Verlet steps."""
 import sys; sys.path.insert(0, '.')
 from paper_1804_07598_b200 import build, inputs, pm
 build.build()

@@ -1,4 +1,7 @@
-import sys; sys.path.insert(0,'/root/repo')
+"""CPU model of the sweep's gather locality: distinct 128-byte lines per
+gather instruction for lane mappings P particles x E lanes.
+Usage: python tools/sim_gather_lines.py"""
+import sys; sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 import numpy as np
 from scipy.spatial import cKDTree
 from paper_1804_07598_b200 import inputs
