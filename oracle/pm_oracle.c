@@ -20,8 +20,12 @@
  *    reorganise (§2: "Cell Lists [45] or Verlet Lists [46] ...
  *    reduces the computational cost to O(N)").
  *
- * Pins: tests/test_oracle_pins.py.  Parts with no independent pin say
- * "parity unpinned" below: the SPH viscosity constants (R20), the SPH time
+ * Pins: tests/test_oracle_pins.py.  The Eq. 5 viscosity VALUE is pinned by a
+ * hand-computed pair (tests/golden/sph_viscosity_pair.txt), the virial by a
+ * closed form and the dilation identity W = -dU_s/dlambda, the image shifts
+ * by reconstruction of the minimum image.  Parts with no independent pin say
+ * "parity unpinned" below: the CHOICE of the viscosity constants alpha, eta
+ * (R20: the paper gives none; the formula with them is pinned), the SPH time
  * stepping scheme beyond its self-consistency pins (R26-R28) and the DEM
  * wall model beyond its closed-form pins (R33).
  */

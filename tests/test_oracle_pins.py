@@ -548,3 +548,114 @@ def test_dem_oblique_friction_momentum_and_spin(orc):
     assert np.abs(w[0, 2]) > 1e-3 and w[0] == pytest.approx(w[1], rel=1e-9, abs=1e-12)
     ke0, ke1 = 0.5 * 2 * 0.25, 0.5 * np.sum(v * v) + 0.5 * p["I"] * np.sum(w * w)
     assert ke1 < ke0
+
+
+# ------------------------------------------------------------------ round-2 pins
+def _gold_vec(name, key):
+    for row in _golden_rows(name):
+        if row[0] == key:
+            return np.array([float(v) for v in row[1:4]])
+    raise KeyError(key)
+
+
+def test_sph_viscosity_value_hand_computed(orc):
+    """Eq. 5 VALUE (not only its branch): Pi_pq and the resulting two-particle
+    accelerations of an approaching pair, hand-computed in
+    tests/golden/sph_viscosity_pair.txt from PAPER.md:332, 344-350 with the
+    R20 constants.  Distinct densities and an oblique, non-axis velocity make a
+    dropped h in mu, rho_p in place of rhobar, a dropped eta^2, a flipped
+    branch or a transposed v/r fail."""
+    h = 0.01
+    prm = dict(h=h, mass=1e-3, alpha=0.1, c0=44.29446918449, eta2=0.01 * h * h,
+               g=(0.0, 0.0, 0.0))
+    pos = np.array([[0.5, 0.5, 0.25, 0], [0.5078125, 0.50390625, 0.25, 0]], np.float32)
+    vel = np.array([[0.375, -0.125, 0.25, 0], [-0.25, 0.125, 0.0, 0]], np.float32)
+    rho = np.array([1000.0, 1010.0])
+    P = np.array([500.0, 1500.0])
+    lo, hi, per = [0, 0, 0], [1, 1, 1], [0, 0, 0]
+    a = orc.sph_accel_rows(pos, vel, rho, P, np.zeros(2, np.int32), lo, hi, per, prm)
+    ap = _gold_vec("sph_viscosity_pair.txt", "a_p")
+    assert a[0] == pytest.approx(ap, rel=1e-12, abs=1e-9)
+    assert a[1] == pytest.approx(-ap, rel=1e-12, abs=1e-9)  # equal masses: a_q = -a_p
+    # the same pair receding (velocities negated): Pi = 0, pressure term only
+    a_rec = orc.sph_accel_rows(pos, -vel, rho, P, np.zeros(2, np.int32), lo, hi, per, prm)
+    ap0 = _gold_vec("sph_viscosity_pair.txt", "a_p_no_visc")
+    assert a_rec[0] == pytest.approx(ap0, rel=1e-12, abs=1e-9)
+    # the viscous part alone is -m Pi grad_p W: its ratio to the pressure part
+    # is Pi / ((P_p + P_q)/(rho_p rho_q)) (hand value of Pi)
+    Pi = _gold_vec("sph_viscosity_pair.txt", "Pi")[0]
+    assert (a[0, 0] - a_rec[0, 0]) / a_rec[0, 0] == pytest.approx(Pi / (2000.0 / 1.01e6),
+                                                                    rel=1e-10)
+
+
+def test_lj_virial_pair_closed_form(orc):
+    """Virial W = 1/2 sum_i sum_j (x_i - x_j) . F_ij of
+    one pair at r = 1.5 sigma equals r F(r) = -1.7370432465692334 (hand value,
+    tests/golden/sph_viscosity_pair.txt); a wrong sign or a missing 1/2 fails."""
+    pos = np.zeros((2, 4), np.float32)
+    pos[0, :3] = [2.0, 3.0, 3.0]
+    pos[1, :3] = [3.5, 3.0, 3.0]
+    res = orc.lj_rows(pos, [0, 0, 0], [8, 8, 8], [1, 1, 1], rc=2.5)
+    W = _gold_vec("sph_viscosity_pair.txt", "lj_virial_r1.5")[0]
+    assert res["W"].sum() == pytest.approx(W, rel=1e-12)
+    assert res["W"][0] == pytest.approx(W / 2, rel=1e-12)
+
+
+def test_lj_virial_is_minus_scaling_derivative(orc):
+    """Thermodynamic identity, independent of the oracle's virial code: for a
+    uniform dilation x -> lambda x of positions and box, the shifted energy
+    U_s (pairs crossing r_c add V(r_c) - V(r_c) = 0, so U_s is continuous)
+    satisfies dU_s/dlambda = sum_pairs r dV/dr = -W at lambda = 1."""
+    s = inputs.lj_lattice_system(10, 10, 10, jitter_key=(31,))
+    x64 = s.pos[:, :3].astype(np.float64)
+    hi64 = s.hi.astype(np.float64)
+    vrc = orc.lj_V(2.5)
+
+    def Us(lam):
+        p = np.zeros_like(s.pos)
+        p[:, :3] = (x64 * lam).astype(np.float32)
+        hi = (hi64 * lam).astype(np.float32)
+        r = orc.lj_rows(p, [0, 0, 0], hi, [1, 1, 1], rc=2.5)
+        return r["U"].sum() - 0.5 * r["npair"].sum() * vrc, r["W"].sum()
+
+    eps = 2e-4
+    up, _ = Us(1 + eps)
+    um, _ = Us(1 - eps)
+    _, W = Us(1.0)
+    dU = (up - um) / (2 * eps)
+    assert W == pytest.approx(-dU, rel=2e-4)
+    assert abs(W) > 100.0  # a non-trivial virial (jittered dense liquid)
+
+
+@pytest.mark.parametrize("per", [(1, 1, 1), (1, 0, 1)])
+def test_verlet_shift_reconstructs_minimum_image(orc, per):
+    """Image-shift codes of the Verlet sets: for every
+    listed pair x_j + shift L - x_i is the fp64 minimum-image difference (a
+    flipped sign is off by 2L), |.| < r_v, and shift = 0 on open axes.  The
+    particles sit in slabs next to the faces so most pairs cross one."""
+    r = np.random.default_rng(77)
+    L = 9.0
+    n = 900
+    x = r.uniform(0, L, (n, 3))
+    face = r.integers(0, 2, (n, 3)).astype(bool)
+    x = np.where(face, r.uniform(0, 1.4, (n, 3)), L - r.uniform(1e-3, 1.4, (n, 3)))
+    pos = np.zeros((n, 4), np.float32)
+    pos[:, :3] = x.astype(np.float32)
+    lo, hi = np.zeros(3, np.float32), np.full(3, L, np.float32)
+    rv = 2.8
+    rp, cols, sh = orc.verlet_rows(pos, lo, hi, np.asarray(per, np.int32), rv)
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    xi = pos[rows, :3].astype(np.float64)
+    xj = pos[cols, :3].astype(np.float64)
+    Lv = hi.astype(np.float64) - lo.astype(np.float64)
+    rec = xj + sh.astype(np.float64) * Lv - xi
+    e = xj - xi
+    for d in range(3):
+        if per[d]:
+            e[:, d] = np.where(e[:, d] > Lv[d] / 2, e[:, d] - Lv[d],
+                               np.where(e[:, d] < -Lv[d] / 2, e[:, d] + Lv[d], e[:, d]))
+        else:
+            assert np.all(sh[:, d] == 0)
+    assert np.max(np.abs(rec - e)) < 1e-5
+    assert np.all(np.sqrt((rec * rec).sum(1)) < rv * (1 + 1e-6))
+    assert np.count_nonzero(sh) > 0.3 * sh.shape[0]  # the case is face-dominated
