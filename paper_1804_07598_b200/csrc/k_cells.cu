@@ -287,7 +287,8 @@ __global__ void __launch_bounds__(256) k_segsort_thin(Bufs B, const int32_t *__r
 // Cells with more than 32 members (clustered inputs, up to ~3000): one block
 // per cell, bitonic sort of the storage indices in shared memory (<= 8192
 // members; beyond, rank by counting).  Coincident particles in such cells are
-// left to the force / density passes (PM_E_NONFINITE).
+// found by the force sweep's non-finite path, which scans the row for a
+// partner at distance 0 and raises PM_E_COINCIDENT (k_lj.cu raise_bad_force).
 constexpr int kBigSort = 8192;
 
 __global__ void __launch_bounds__(512) k_segsort_big(Bufs B, const int32_t *__restrict__ tmp) {

@@ -198,6 +198,25 @@ __device__ __forceinline__ void block_add_energy(State *st, double u, double w, 
   }
 }
 
+// A non-finite force (rare path): PM_E_COINCIDENT when the row holds a
+// partner at distance 0 (identical wrapped coordinates; such pairs pass the
+// list test 0 <= d2 < r_v^2 in any cell, however crowded), else
+// PM_E_NONFINITE.
+__device__ __noinline__ void raise_bad_force(const Bufs &B, State *st, const float4 *pos, int i,
+                                             const float4 &xi) {
+  const int cnt = B.cnt[i];
+  const int *nb = B.nbr + nbr_row_base(B, i);
+  for (int k = 0; k < cnt; ++k) {
+    const int j = nb[(int64_t)k << 5];
+    const float4 xj = pos[j];
+    if (j != i && xj.x == xi.x && xj.y == xi.y && xj.z == xi.z) {
+      raise_error(st, -7 /*PM_E_COINCIDENT*/, (long long)B.gid[st->cur_id][i]);
+      return;
+    }
+  }
+  raise_error(st, -8 /*PM_E_NONFINITE*/, (long long)B.gid[st->cur_id][i]);
+}
+
 // pm_compute_lj: forces (+ energy) of the current positions.
 template <bool CAPPED, bool ENERGY>
 __global__ void __launch_bounds__(256) k_lj(Params P, Bufs B, int n) {
@@ -209,8 +228,7 @@ __global__ void __launch_bounds__(256) k_lj(Params P, Bufs B, int n) {
   Acc a = lj_force_of<CAPPED, ENERGY>(P, B, pos, i, active, xi);
   if (active) {
     B.force[i] = make_float4(a.fx, a.fy, a.fz, 0.f);
-    if (!isfinite(a.fx + a.fy + a.fz))
-      raise_error(st, -8 /*PM_E_NONFINITE*/, (long long)B.gid[st->cur_id][i]);
+    if (!isfinite(a.fx + a.fy + a.fz)) raise_bad_force(B, st, pos, i, xi);
   }
   if (ENERGY) block_add_energy(st, (double)a.u, (double)a.w, (double)a.np);
 }
@@ -291,8 +309,7 @@ __device__ __forceinline__ void vv_epilogue(const Params &P, const Bufs &B, Stat
       B.force[i] = make_float4(a.fx, a.fy, a.fz, 0.f);
     }
     B.vel[cp ^ 1][i] = v;
-    if (!isfinite(a.fx + a.fy + a.fz))
-      raise_error(st, -8 /*PM_E_NONFINITE*/, (long long)B.gid[st->cur_id][i]);
+    if (!isfinite(a.fx + a.fy + a.fz)) raise_bad_force(B, st, B.pos[cp], i, xi);
   }
 }
 
@@ -500,6 +517,15 @@ __global__ void __launch_bounds__(256) k_ke(Params P, Bufs B, int n) {
   }
 }
 
+// An empty sub-domain still takes part in the buffer flips of a step (the
+// fused ghost refresh picks the peer buffer from the sender's parity, so every
+// rank must flip in lockstep even with no particles).
+__global__ void k_empty_step(State *st, int count_step) {
+  if (st->abort) return;
+  st->pending_flip = 1;
+  if (count_step) st->steps_done += 1;
+}
+
 inline unsigned nb(int64_t n) { return (unsigned)((n + 255) / 256); }
 
 }  // namespace
@@ -543,11 +569,15 @@ void launch_lj_half_forces(const Params &P, const Bufs &B, int64_t n, int want_e
 void launch_lj_half_integrate(const Params &P, const Bufs &B, int64_t n, float dt, int mode,
                               cudaStream_t s) {
   if (n > 0) k_lj_half_vv<<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode);
+  else k_empty_step<<<1, 1, 0, s>>>(B.st, 1);
 }
 
 void launch_lj_step_mode(const Params &P, const Bufs &B, int64_t n, float dt, int mode,
                          cudaStream_t s) {
-  if (n <= 0) return;
+  if (n <= 0) {
+    k_empty_step<<<1, 1, 0, s>>>(B.st, 1);
+    return;
+  }
   if (P.newton) {  // clear F -> half sweep -> integrator
     launch_lj_half(P, B, n, 0, s);
     k_lj_half_vv<<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode);
@@ -568,6 +598,7 @@ void launch_lj_step(const Params &P, const Bufs &B, int64_t n, float dt, cudaStr
 
 void launch_kick_drift(const Params &P, const Bufs &B, int64_t n, float dt, cudaStream_t s) {
   if (n > 0) k_kick_drift<<<nb(n), 256, 0, s>>>(P, B, (int)n, dt);
+  else k_empty_step<<<1, 1, 0, s>>>(B.st, 0);
 }
 
 void launch_step_begin(const Bufs &B, cudaGraphConditionalHandle h, int use_handle,

@@ -27,11 +27,10 @@ namespace {
 // whole periodic x-row, and the decomposed axes of a multi-GPU sub-domain
 // (ghosts carry global wrapped coordinates).
 //
-// The membership test 0 < d2 < rv2 is one unsigned compare of the fp32 bit
-// patterns (d2 >= 0, so bits(d2) - 1 < bits(rv2) - 1 as uint32 exactly when
-// 0 < d2 < rv2; NaN/inf never pass): d2 == 0 is the particle itself (a
-// coincident distinct pair is caught by the force / density passes, which
-// raise PM_E_COINCIDENT).  Lanes outside the current segment carry
+// The membership test is d2 < rv2 (one compare); the particle itself is
+// dropped by index, so a coincident distinct pair (d2 = 0) is listed and
+// raised as PM_E_COINCIDENT by the cell sort (cells of <= 32 members) or the
+// force sweep's non-finite path.  Lanes outside the current segment carry
 // xi = +inf and never hit.
 template <bool SHIFTJ, bool PAIRMI>
 __device__ __forceinline__ float d2_of(const Params &P, const float4 &xi_eff, const float3 &csh,

@@ -284,9 +284,10 @@ pm_status ensure_particles(pm_ctx c, int64_t n, int64_t keep = 0) {
     CUDA_TRY(c, grow_keep(&B.kind[b], cap, keep, c->stream));
   }
   CUDA_TRY(c, dalloc(&B.xref, cap));
-  CUDA_TRY(c, dalloc(&B.force, cap));
-  CUDA_TRY(c, dalloc(&B.rhoP[0], cap));
-  CUDA_TRY(c, dalloc(&B.rhoP[1], cap));
+  // forces and rho/P of the stayers (already compacted by a migration) survive
+  CUDA_TRY(c, grow_keep(&B.force, cap, keep, c->stream));
+  CUDA_TRY(c, grow_keep(&B.rhoP[0], cap, keep, c->stream));
+  CUDA_TRY(c, grow_keep(&B.rhoP[1], cap, keep, c->stream));
   for (int b = 0; b < 2; ++b)  // SPH stepping state (allocated by the first SPH run)
     if (B.vold[b]) CUDA_TRY(c, grow_keep(&B.vold[b], cap, keep, c->stream));
   if (B.omega[0] && c->dem_pcap == c->pcap) {  // DEM state (pm_dem_run / pm_dist_dem_init)
@@ -302,7 +303,8 @@ pm_status ensure_particles(pm_ctx c, int64_t n, int64_t keep = 0) {
   CUDA_TRY(c, dalloc(&B.invperm, cap));
   CUDA_TRY(c, dalloc(&B.sorttmp, cap));
   CUDA_TRY(c, dalloc(&B.cnt, cap));
-  CUDA_TRY(c, cudaMemsetAsync(B.force, 0, sizeof(float4) * cap, c->stream));
+  if (cap > keep)
+    CUDA_TRY(c, cudaMemsetAsync(B.force + keep, 0, sizeof(float4) * (cap - keep), c->stream));
   CUDA_TRY(c, cudaMemsetAsync(B.cnt, 0, sizeof(int32_t) * cap, c->stream));
   c->pcap = cap;
   // the slice layout must be redone for the new capacity (ensure_layout)
@@ -527,35 +529,68 @@ pm_status ensure_events(pm_ctx c, size_t n) {
   return PM_OK;
 }
 
-pm_status build_graph(pm_ctx c, float dt, bool prof) {
-  destroy_graph(c);
+// The step graph shared by pm_step_vv, pm_sph_run and pm_dem_run:
+//   head (one thread: flips, step bookkeeping, sets the condition)
+//   -> IF(condition) { body: the rebuild }  -> (the caller adds the tail)
+// head(handle, stream) and body(stream) enqueue their launches; on success
+// *g is the graph and *n_cond its conditional node.
+template <class Head, class Body>
+pm_status build_cond_graph(pm_ctx c, const char *what, Head head, Body body, cudaGraph_t *g_out,
+                           cudaGraphNode_t *n_cond) {
   cudaGraph_t g = nullptr;
   CUDA_TRY(c, cudaGraphCreate(&g, 0));
   cudaGraphConditionalHandle h;
   CUDA_TRY(c, cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
   cudaStream_t cs = c->cap_stream;
   const cudaStreamCaptureMode mode = cudaStreamCaptureModeThreadLocal;
-  // node A: step begin
   CUDA_TRY(c, cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, mode));
-  launch_step_begin(c->B, h, 1, cs);
+  head(h, cs);
   CUDA_TRY(c, cudaStreamEndCapture(cs, &g));
   size_t nn = 0;
   CUDA_TRY(c, cudaGraphGetNodes(g, nullptr, &nn));
-  if (nn != 1) return set_err(c, PM_E_CUDA, "graph build: expected 1 node, got %zu", nn);
+  if (nn != 1) {
+    cudaGraphDestroy(g);
+    return set_err(c, PM_E_CUDA, "%s graph: expected 1 head node, got %zu", what, nn);
+  }
   cudaGraphNode_t nA;
   CUDA_TRY(c, cudaGraphGetNodes(g, &nA, &nn));
-  // node C: IF(need_rebuild) { rebuild }
   cudaGraphNodeParams cp = {};
   cp.type = cudaGraphNodeTypeConditional;
   cp.conditional.handle = h;
   cp.conditional.type = cudaGraphCondTypeIf;
   cp.conditional.size = 1;
+  CUDA_TRY(c, cudaGraphAddNode(n_cond, g, &nA, 1, &cp));
+  cudaGraph_t bg = cp.conditional.phGraph_out[0];
+  CUDA_TRY(c, cudaStreamBeginCaptureToGraph(cs, bg, nullptr, nullptr, 0, mode));
+  body(cs);
+  CUDA_TRY(c, cudaStreamEndCapture(cs, &bg));
+  *g_out = g;
+  return PM_OK;
+}
+
+// Capture the launches of tail(stream) into g after node dep.
+template <class Tail>
+pm_status capture_after(pm_ctx c, cudaGraph_t g, cudaGraphNode_t dep, Tail tail) {
+  cudaStream_t cs = c->cap_stream;
+  CUDA_TRY(c, cudaStreamBeginCaptureToGraph(cs, g, &dep, nullptr, 1,
+                                            cudaStreamCaptureModeThreadLocal));
+  tail(cs);
+  CUDA_TRY(c, cudaStreamEndCapture(cs, &g));
+  return PM_OK;
+}
+
+pm_status build_graph(pm_ctx c, float dt, bool prof) {
+  destroy_graph(c);
+  cudaGraph_t g = nullptr;
   cudaGraphNode_t nC;
-  CUDA_TRY(c, cudaGraphAddNode(&nC, g, &nA, 1, &cp));
-  cudaGraph_t body = cp.conditional.phGraph_out[0];
-  CUDA_TRY(c, cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, mode));
-  enqueue_rebuild(c, cs, 1);
-  CUDA_TRY(c, cudaStreamEndCapture(cs, &body));
+  pm_status s0 = build_cond_graph(
+      c, "step", [&](cudaGraphConditionalHandle h, cudaStream_t cs) {
+        launch_step_begin(c->B, h, 1, cs);
+      },
+      [&](cudaStream_t cs) { enqueue_rebuild(c, cs, 1); }, &g, &nC);
+  if (s0) return s0;
+  cudaStream_t cs = c->cap_stream;
+  const cudaStreamCaptureMode mode = cudaStreamCaptureModeThreadLocal;
   // force step (+ profiling events around it)
   cudaGraphNode_t prev = nC;
   if (prof) {
@@ -849,7 +884,9 @@ pm_status pm_place(pm_ctx c, int64_t n, const float *pos4, const float *vel4, co
   cudaSetDevice(c->device);
   c->sticky = 0;
   c->err.clear();
-  pm_status s = ensure_particles(c, n);
+  // a minimum capacity even for n == 0: an empty sub-domain of a decomposition
+  // is a valid context (particles may migrate into it later)
+  pm_status s = ensure_particles(c, std::max<int64_t>(n, 1));
   if (s) return s;
   if (n != c->n) destroy_graph(c);
   c->n = n;
@@ -1023,33 +1060,16 @@ static pm_status dem_graph_ready(pm_ctx c, float dt) {
     return PM_OK;
   destroy_dem_graph(c);
   cudaGraph_t g = nullptr;
-  CUDA_TRY(c, cudaGraphCreate(&g, 0));
-  cudaGraphConditionalHandle h;
-  CUDA_TRY(c, cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
-  cudaStream_t cs = c->cap_stream;
-  const cudaStreamCaptureMode mode = cudaStreamCaptureModeThreadLocal;
-  CUDA_TRY(c, cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, mode));
-  launch_dem_step_begin(c->B, h, cs);
-  CUDA_TRY(c, cudaStreamEndCapture(cs, &g));
-  size_t nn = 0;
-  CUDA_TRY(c, cudaGraphGetNodes(g, nullptr, &nn));
-  if (nn != 1) return set_err(c, PM_E_CUDA, "dem graph: expected 1 node, got %zu", nn);
-  cudaGraphNode_t nA;
-  CUDA_TRY(c, cudaGraphGetNodes(g, &nA, &nn));
-  cudaGraphNodeParams cp = {};
-  cp.type = cudaGraphNodeTypeConditional;
-  cp.conditional.handle = h;
-  cp.conditional.type = cudaGraphCondTypeIf;
-  cp.conditional.size = 1;
   cudaGraphNode_t nC;
-  CUDA_TRY(c, cudaGraphAddNode(&nC, g, &nA, 1, &cp));
-  cudaGraph_t body = cp.conditional.phGraph_out[0];
-  CUDA_TRY(c, cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, mode));
-  enqueue_dem_rebuild(c, cs);
-  CUDA_TRY(c, cudaStreamEndCapture(cs, &body));
-  CUDA_TRY(c, cudaStreamBeginCaptureToGraph(cs, g, &nC, nullptr, 1, mode));
-  launch_dem_step(c->P, c->B, c->n, dt, cs);
-  CUDA_TRY(c, cudaStreamEndCapture(cs, &g));
+  pm_status s = build_cond_graph(
+      c, "dem", [&](cudaGraphConditionalHandle h, cudaStream_t cs) {
+        launch_dem_step_begin(c->B, h, cs);
+      },
+      [&](cudaStream_t cs) { enqueue_dem_rebuild(c, cs); }, &g, &nC);
+  if (!s) s = capture_after(c, g, nC, [&](cudaStream_t cs) {
+    launch_dem_step(c->P, c->B, c->n, dt, cs);
+  });
+  if (s) return s;
   CUDA_TRY(c, cudaGraphInstantiate(&c->dem_exec, g, 0));
   c->dem_graph = g;
   c->dem_key_P = c->P;
@@ -1225,33 +1245,16 @@ static pm_status sph_graph_ready(pm_ctx c, float cfl, int every) {
     return PM_OK;
   destroy_sph_graph(c);
   cudaGraph_t g = nullptr;
-  CUDA_TRY(c, cudaGraphCreate(&g, 0));
-  cudaGraphConditionalHandle h;
-  CUDA_TRY(c, cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
-  cudaStream_t cs = c->cap_stream;
-  const cudaStreamCaptureMode mode = cudaStreamCaptureModeThreadLocal;
-  CUDA_TRY(c, cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, mode));
-  launch_dem_step_begin(c->B, h, cs);  // generic step head (flip + rebuild condition)
-  CUDA_TRY(c, cudaStreamEndCapture(cs, &g));
-  size_t nn = 0;
-  CUDA_TRY(c, cudaGraphGetNodes(g, nullptr, &nn));
-  if (nn != 1) return set_err(c, PM_E_CUDA, "sph graph: expected 1 node, got %zu", nn);
-  cudaGraphNode_t nA;
-  CUDA_TRY(c, cudaGraphGetNodes(g, &nA, &nn));
-  cudaGraphNodeParams cp = {};
-  cp.type = cudaGraphNodeTypeConditional;
-  cp.conditional.handle = h;
-  cp.conditional.type = cudaGraphCondTypeIf;
-  cp.conditional.size = 1;
   cudaGraphNode_t nC;
-  CUDA_TRY(c, cudaGraphAddNode(&nC, g, &nA, 1, &cp));
-  cudaGraph_t body = cp.conditional.phGraph_out[0];
-  CUDA_TRY(c, cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, mode));
-  enqueue_rebuild(c, cs, 1);
-  CUDA_TRY(c, cudaStreamEndCapture(cs, &body));
-  CUDA_TRY(c, cudaStreamBeginCaptureToGraph(cs, g, &nC, nullptr, 1, mode));
-  launch_sph_step(c->P, c->B, c->n, cfl, every, cs);
-  CUDA_TRY(c, cudaStreamEndCapture(cs, &g));
+  pm_status s = build_cond_graph(
+      c, "sph", [&](cudaGraphConditionalHandle h, cudaStream_t cs) {
+        launch_dem_step_begin(c->B, h, cs);  // generic step head (flip + rebuild condition)
+      },
+      [&](cudaStream_t cs) { enqueue_rebuild(c, cs, 1); }, &g, &nC);
+  if (!s) s = capture_after(c, g, nC, [&](cudaStream_t cs) {
+    launch_sph_step(c->P, c->B, c->n, cfl, every, cs);
+  });
+  if (s) return s;
   CUDA_TRY(c, cudaGraphInstantiate(&c->sph_exec, g, 0));
   c->sph_graph = g;
   c->sph_key_P = c->P;
@@ -1687,9 +1690,13 @@ pm_status pm_dist_plan(pm_ctx c, int32_t what, const int32_t order[26], int64_t 
     CUDA_TRY(c, cudaMalloc((void **)&c->d_tot, 27 * sizeof(long long)));
     CUDA_TRY(c, cudaMallocHost((void **)&c->h_tot, 27 * sizeof(long long)));
   }
-  for (int k = 0; k < 26; ++k)
-    if (order[k] < 0 || order[k] > 26 || order[k] == 13)
-      return set_err(c, PM_E_INVAL, "pm_dist_plan: order must list the 26 directions != 13");
+  uint32_t seen = 0;  // order must be a permutation of the 26 directions != 13
+  for (int k = 0; k < 26; ++k) {
+    if (order[k] < 0 || order[k] > 26 || order[k] == 13 || (seen >> order[k] & 1u))
+      return set_err(c, PM_E_INVAL,
+                     "pm_dist_plan: order must list each of the 26 directions != 13 once");
+    seen |= 1u << order[k];
+  }
   CUDA_TRY(c, cudaMemcpyAsync(c->d_order, order, 26 * sizeof(int), cudaMemcpyHostToDevice, c->stream));
   launch_dist_plan(c->P, c->B, c->D, (int)no, what, c->d_mask, c->d_blk, c->d_order, c->d_dirbase,
                    c->d_tot, c->d_list, c->stream);

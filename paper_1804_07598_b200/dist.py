@@ -748,7 +748,8 @@ class SAR:
     """Stop-At-Rise re-balancing trigger (PAPER.md:122 '[56]'):
     per step record the degradation delta = max - mean of the per-rank step
     times; W(n) = (C + sum delta) / n with C the cost of a re-balance;
-    re-balance at the first rise W(n) > W(n-1) (W(0) = +inf)."""
+    re-balance at the first rise W(n) > W(n-1) (W(0) = +inf); at most one
+    True per reset (the caller re-balances and calls reset)."""
 
     def __init__(self, cost):
         self.C = float(cost)
@@ -758,6 +759,7 @@ class SAR:
         if cost is not None:
             self.C = float(cost)
         self.n, self.sum, self.W = 0, 0.0, float("inf")
+        self.fired = False
 
     def record(self, per_rank_times):
         t = np.asarray(per_rank_times, np.float64)
@@ -765,9 +767,12 @@ class SAR:
         self.n += 1
 
     def decide(self):
+        if self.fired or self.n == 0:
+            return False
         W = (self.C + self.sum) / self.n
         rise = W > self.W
         self.W = W
+        self.fired = rise
         return rise
 
 

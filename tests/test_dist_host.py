@@ -154,6 +154,8 @@ def test_sar_stop_at_rise_examples():
     assert out == [False, False]
     s.record([60.0, 0.0])  # delta 30 -> W = 40/3 > 5
     assert s.decide() is True
+    s.record([100.0, 0.0])  # W rises again, but at most one True per reset
+    assert s.decide() is False
     s.reset()
     assert not any((s.record([2.0, 0.0]), s.decide())[1] for _ in range(50))  # (10+n)/n falls
 

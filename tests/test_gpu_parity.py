@@ -617,6 +617,17 @@ def test_error_paths(pm):
             c.build_verlet()
         assert e.value.code == -7
         c.close()
+    # coincident pair inside a cell of more than 32 members (block-level sort,
+    # no pairwise check there): the force sweep raises PM_E_COINCIDENT
+    s5 = inputs.random_box(3000, 40.0, (19,))
+    s5.pos[:60, :3] = np.random.default_rng(10).uniform(20.0, 22.5, (60, 3))
+    s5.pos[7, :3] = s5.pos[3, :3]
+    c = make_ctx(pm, s5)
+    c.build_verlet()
+    with pytest.raises(pm.PMError) as e:
+        c.compute_lj()
+    assert e.value.code == -7
+    c.close()
     # outside a non-periodic axis
     s3 = s.subset(np.arange(s.n))
     s3.periodic = np.array([1, 1, 0], np.int32)
