@@ -100,27 +100,53 @@ def dist_env():
     return ws, rank, local
 
 
-def cpu_baseline(n_target_s=15.0):
-    """The oracle as it stands (fp64 brute-force O(N) LJ force per particle +
-    velocity-Verlet update) on a bounded sample of cfg2 particles."""
+def _cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def _oracle_md_rate(sys_, steps, threads):
+    """Particle-updates/s of the fp64 CPU method (oracle.md_cells_run: cell
+    list + Verlet list with skin + velocity Verlet, rebuilds included as they
+    happen) on `threads` host threads: N * steps / (t(steps) - t(0)), where
+    t(0) is the set-up (first list build + first forces)."""
+    from oracle import oracle
+    oracle.set_num_threads(threads)
+    t0 = time.perf_counter()
+    oracle.md_cells_run(sys_.pos, sys_.vel, sys_.lo, sys_.hi, sys_.periodic, RC, SKIN, DT, 0,
+                        trace=False)
+    t_setup = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    _, _, _, nb = oracle.md_cells_run(sys_.pos, sys_.vel, sys_.lo, sys_.hi, sys_.periodic, RC,
+                                      SKIN, DT, steps, trace=False)
+    t = time.perf_counter() - t0
+    dt_steps = max(t - t_setup, 1e-9)
+    return sys_.n * steps / dt_steps, dt_steps, t_setup, nb - 1
+
+
+def cpu_baseline():
+    """SURVEY §8(d) oracle timing: the method itself in fp64 on the host
+    (oracle.md_cells_run, pinned against the brute-force trajectory) on the
+    full cfg2 system -- single-threaded and on all host cores (OpenMP)."""
     from oracle import oracle
     from paper_1804_07598_b200 import inputs
     s = inputs.cfg2()
-    rng = np.random.default_rng(0)
-    rows = rng.choice(s.n, 64, replace=False)
-    t0 = time.perf_counter()
-    oracle.lj_rows(s.pos, s.lo, s.hi, s.periodic, rc=RC, rows=rows)
-    t1 = time.perf_counter()
-    m = int(max(64, min(s.n, 64 * n_target_s / max(t1 - t0, 1e-6))))
-    rows = rng.choice(s.n, m, replace=False)
-    t0 = time.perf_counter()
-    r = oracle.lj_rows(s.pos, s.lo, s.hi, s.periodic, rc=RC, rows=rows)
-    v = s.vel[rows, :3].astype(np.float64) + DT * r["F"]  # kick (m = 1)
-    _ = s.pos[rows, :3].astype(np.float64) + DT * v        # drift
-    t = time.perf_counter() - t0
-    return {"value": m / t, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"{m} of {s.n} cfg2 particles: fp64 brute-force O(N) LJ force + VV update "
-                      f"each ({t:.1f} s)"}
+    nall = os.cpu_count() or 1
+    v1, t1, su1, nb1 = _oracle_md_rate(s, 2, 1)
+    vn, tn, sun, nbn = _oracle_md_rate(s, 20, nall)
+    oracle.set_num_threads(nall)
+    return {"value": vn, "unit": UNIT, "cores": nall, "kind": "oracle",
+            "threads": {"1": v1, str(nall): vn}, "cpu_model": _cpu_model(), "nproc": nall,
+            "sample": f"full cfg2 ({s.n} particles): fp64 cell list + Verlet list (skin 0.3, "
+                      f"rebuild at skin/2) + velocity Verlet (oracle.md_cells_run); "
+                      f"{nall} threads: 20 steps in {tn:.1f} s ({nbn} rebuilds) after a "
+                      f"{sun:.1f} s set-up; 1 thread: 2 steps in {t1:.1f} s ({nb1} rebuilds) "
+                      f"after a {su1:.1f} s set-up"}
 
 
 def sph_pass(dev, stream, repeats=10):
@@ -248,39 +274,40 @@ def dem_run(dev, stream, warm=300, steps=500):
 
 def run_reference(args):
     """--impl reference: the oracle as it stands on the host cores, on this
-    arm's config/metric; each step a bounded sample of cfg2 particles."""
+    arm's metric: the fp64 CPU method (oracle.md_cells_run) on a periodic
+    block of the cfg2 liquid (same lattice density, jitter and temperature),
+    its size bounded so that warm-up + timed steps take about two minutes."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
     from oracle import oracle
     from paper_1804_07598_b200 import inputs
-    s = inputs.cfg2()
-    rng = np.random.default_rng(0)
-    probe = rng.choice(s.n, 32, replace=False)
-    t0 = time.perf_counter()
-    oracle.lj_rows(s.pos, s.lo, s.hi, s.periodic, rc=RC, rows=probe)
-    t_row = (time.perf_counter() - t0) / 32
+    nall = os.cpu_count() or 1
+    oracle.set_num_threads(nall)
+    probe = inputs.lj_lattice_system(24, 24, 24, jitter_key=(2,), vel_key=(102,))
+    rate, _, _, _ = _oracle_md_rate(probe, 3, nall)  # particle-updates/s of this host
     budget = 120.0
-    rows_per_step = int(max(1, min(4096, budget / max(1, args.steps + args.warmup) / t_row)))
-    tot = 0.0
-    for k in range(args.warmup + args.steps):
-        rows = rng.choice(s.n, rows_per_step, replace=False)
-        t0 = time.perf_counter()
-        r = oracle.lj_rows(s.pos, s.lo, s.hi, s.periodic, rc=RC, rows=rows)
-        v = s.vel[rows, :3].astype(np.float64) + DT * r["F"]
-        _ = s.pos[rows, :3].astype(np.float64) + DT * v
-        if k >= args.warmup:
-            tot += time.perf_counter() - t0
-    value = rows_per_step * args.steps / tot
+    n_target = rate * budget / max(1, args.steps + args.warmup)
+    m = int(max(8, min(128, round((n_target / 2) ** (1 / 3)))))  # m x m x m/2 block
+    s = inputs.lj_lattice_system(m, m, max(4, m // 2), jitter_key=(2,), vel_key=(102,))
+    x, v = s.pos.copy(), s.vel.copy()
+    if args.warmup:
+        xw, vw, _, _ = oracle.md_cells_run(x, v, s.lo, s.hi, s.periodic, RC, SKIN, DT,
+                                           args.warmup, trace=False)
+        x[:, :3], v[:, :3] = xw.astype(np.float32), vw.astype(np.float32)
+    s.pos, s.vel = x, v
+    value, t, _, nb = _oracle_md_rate(s, args.steps, nall)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+            "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "cfg2 (BJ configs[1]) LJ fluid 1,048,576 particles; each step "
-                                   f"= oracle on {rows_per_step} sampled particles"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(),
-                             "kind": "oracle",
-                             "sample": f"{rows_per_step} sampled cfg2 particles per step"},
+            "config": {"workload": f"cfg2-class LJ liquid (BJ configs[1] recipe) on a periodic "
+                                   f"{m}x{m}x{max(4, m // 2)} block ({s.n} particles) per step; "
+                                   "fp64 cell list + Verlet + velocity Verlet on the host"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": nall, "kind": "oracle",
+                             "cpu_model": _cpu_model(),
+                             "sample": f"{s.n}-particle periodic block of the cfg2 liquid, "
+                                       f"{args.steps} steps ({nb} list rebuilds)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

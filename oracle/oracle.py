@@ -89,6 +89,10 @@ def lib():
                                   C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
                                   C.c_double, C.c_double, C.c_double, f64p, C.c_double,
                                   C.c_int64, C.c_int64, f64p]
+        L.orc_md_cells_run.restype = C.c_int64
+        L.orc_md_cells_run.argtypes = [C.c_int64, f64p, f64p, f64p, f64p, i32p, C.c_double,
+                                       C.c_double, C.c_double, C.c_double, C.c_double,
+                                       C.c_double, C.c_double, C.c_int64, C.c_void_p]
         _lib = L
     return _lib
 
@@ -216,6 +220,28 @@ def vv_run(pos4, vel4, lo, hi, per, rc, dt, nsteps, eps=1.0, sigma=1.0, mass=1.0
                      float(eps), float(sigma), float(r_min), float(mass), float(dt),
                      int(nsteps), tr)
     return x, v, tr.reshape(nsteps + 1, 4)
+
+
+def md_cells_run(pos4, vel4, lo, hi, per, rc, skin, dt, nsteps, eps=1.0, sigma=1.0, mass=1.0,
+                 r_min=0.0, trace=True):
+    """The method itself on the CPU (SURVEY §8(d) oracle timing): fp64 cell
+    list + Verlet list with skin (rebuild at skin/2) + velocity Verlet
+    (Listing 4.1 at PAPER.md:291-320).  Same
+    trajectory as vv_run up to summation order.  Returns (x, v, trace or
+    None, number of list builds)."""
+    x = np.ascontiguousarray(np.asarray(pos4)[:, :3], dtype=np.float64).copy()
+    v = np.ascontiguousarray(np.asarray(vel4)[:, :3], dtype=np.float64).copy()
+    n = x.shape[0]
+    tr = np.zeros((nsteps + 1) * 4, np.float64) if trace else None
+    lo64 = np.ascontiguousarray(np.asarray(lo, np.float32).astype(np.float64))
+    hi64 = np.ascontiguousarray(np.asarray(hi, np.float32).astype(np.float64))
+    nb = lib().orc_md_cells_run(n, x.reshape(-1), v.reshape(-1), lo64, hi64, _i3(per),
+                                float(rc), float(skin), float(eps), float(sigma), float(r_min),
+                                float(mass), float(dt), int(nsteps),
+                                tr.ctypes.data if tr is not None else None)
+    if nb < 0:
+        raise ValueError("md_cells_run: a periodic axis has fewer than 3 cells of side r_v")
+    return x, v, (tr.reshape(nsteps + 1, 4) if tr is not None else None), int(nb)
 
 
 # ---------------------------------------------------------------- SPH

@@ -783,3 +783,216 @@ int64_t orc_dem_run(int64_t n, double *x, double *v, double *w, const int64_t *g
   free(nhist);
   return nh;
 }
+
+/* ------------------------------------------------------------------ */
+/* CPU baseline of the method itself (SURVEY §8(d) "Oracle timing"):     */
+/* fp64 cell list + Verlet list with skin + velocity Verlet, the O(N)    */
+/* reorganisation of orc_vv_run's O(N^2) sum (§2 "Cell Lists */
+/* [45] or Verlet Lists [46] ... reduces the computational cost to O(N)"; */
+/* PAPER.md:164 Verlet lists; PAPER.md:166 velocity Verlet; Listing 4.1   */
+/* order at PAPER.md:291-320).  Plain code, no blocking: cells of side    */
+/* >= r_v = rc + skin (n_d = floor(L_d / r_v) >= 3 per periodic axis),    */
+/* row i = every j != i with fp64 minimum-image r^2 < r_v^2 over the 27   */
+/* neighbour cells, rebuilt when a particle moved more than skin/2 since  */
+/* the last build; forces over the row with r^2 < rc^2 (OpenMP over rows, */
+/* full rows, no atomics).  Pinned against orc_vv_run (same trajectory up */
+/* to summation order) in tests/test_oracle_pins.py.                      */
+/* Returns the number of list builds, or -1 if a periodic axis has fewer  */
+/* than 3 cells.  trace as orc_vv_run (may be NULL).                      */
+/* ------------------------------------------------------------------ */
+typedef struct {
+  int nc[3];
+  double inv_w[3];
+  int64_t *start, *idx; /* cell starts (ncell + 1), particles by cell */
+  int64_t *row_ptr;     /* n + 1 */
+  int32_t *cols;
+  int64_t cols_cap;
+} md_lists_t;
+
+static int md_cell_coord(double x, double lo, double inv_w, int nc) {
+  int c = (int)floor((x - lo) * inv_w);
+  if (c < 0) c = 0;
+  if (c > nc - 1) c = nc - 1;
+  return c;
+}
+
+static double md_min_image(double e, double L, int per) {
+  if (per) {
+    if (e > 0.5 * L) e -= L;
+    else if (e < -0.5 * L) e += L;
+  }
+  return e;
+}
+
+static void md_build(int64_t n, const double *x, const double lo[3], const double L[3],
+                     const int32_t per[3], double rv, md_lists_t *M) {
+  int64_t ncell = (int64_t)M->nc[0] * M->nc[1] * M->nc[2];
+  int64_t *cell = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+  memset(M->start, 0, sizeof(int64_t) * (size_t)(ncell + 1));
+  for (int64_t i = 0; i < n; ++i) {
+    int c0 = md_cell_coord(x[3 * i + 0], lo[0], M->inv_w[0], M->nc[0]);
+    int c1 = md_cell_coord(x[3 * i + 1], lo[1], M->inv_w[1], M->nc[1]);
+    int c2 = md_cell_coord(x[3 * i + 2], lo[2], M->inv_w[2], M->nc[2]);
+    cell[i] = c0 + (int64_t)M->nc[0] * (c1 + (int64_t)M->nc[1] * c2);
+    M->start[cell[i] + 1]++;
+  }
+  for (int64_t c = 0; c < ncell; ++c) M->start[c + 1] += M->start[c];
+  int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * (size_t)(ncell > 0 ? ncell : 1));
+  memcpy(fill, M->start, sizeof(int64_t) * (size_t)ncell);
+  for (int64_t i = 0; i < n; ++i) M->idx[fill[cell[i]]++] = i;
+  free(fill);
+  double rv2 = rv * rv;
+  /* two passes over the rows: count, then fill */
+  for (int pass = 0; pass < 2; ++pass) {
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t i = 0; i < n; ++i) {
+      int64_t cc = cell[i];
+      int c[3] = {(int)(cc % M->nc[0]), (int)((cc / M->nc[0]) % M->nc[1]),
+                  (int)(cc / ((int64_t)M->nc[0] * M->nc[1]))};
+      int64_t k = pass ? M->row_ptr[i] : 0;
+      for (int dz = -1; dz <= 1; ++dz)
+        for (int dy = -1; dy <= 1; ++dy)
+          for (int dx = -1; dx <= 1; ++dx) {
+            int q[3] = {c[0] + dx, c[1] + dy, c[2] + dz}, ok = 1;
+            for (int d = 0; d < 3; ++d) {
+              if (q[d] < 0 || q[d] >= M->nc[d]) {
+                if (!per[d]) ok = 0;
+                else q[d] = (q[d] + M->nc[d]) % M->nc[d];
+              }
+            }
+            if (!ok) continue;
+            int64_t qc = q[0] + (int64_t)M->nc[0] * (q[1] + (int64_t)M->nc[1] * q[2]);
+            for (int64_t t = M->start[qc]; t < M->start[qc + 1]; ++t) {
+              int64_t j = M->idx[t];
+              if (j == i) continue;
+              double r2 = 0.0;
+              for (int d = 0; d < 3; ++d) {
+                double e = md_min_image(x[3 * i + d] - x[3 * j + d], L[d], per[d]);
+                r2 += e * e;
+              }
+              if (r2 < rv2) {
+                if (pass) M->cols[k] = (int32_t)j;
+                k++;
+              }
+            }
+          }
+      if (!pass) M->row_ptr[i + 1] = k;
+    }
+    if (!pass) {
+      M->row_ptr[0] = 0;
+      for (int64_t i = 0; i < n; ++i) M->row_ptr[i + 1] += M->row_ptr[i];
+      if (M->row_ptr[n] > M->cols_cap) {
+        free(M->cols);
+        M->cols_cap = M->row_ptr[n] + M->row_ptr[n] / 4 + 1;
+        M->cols = (int32_t *)malloc(sizeof(int32_t) * (size_t)M->cols_cap);
+      }
+    }
+  }
+  free(cell);
+}
+
+static void md_forces(int64_t n, const double *x, const double L[3], const int32_t per[3],
+                      const md_lists_t *M, double rc, double eps, double sig, double r_min,
+                      double *F, double *Uraw, double *Ushift, double *npairs) {
+  double vrc = lj_V(rc, eps, sig), rc2 = rc * rc;
+  double u = 0, us = 0, np = 0;
+#pragma omp parallel for schedule(dynamic, 256) reduction(+ : u, us, np)
+  for (int64_t i = 0; i < n; ++i) {
+    double f[3] = {0, 0, 0};
+    for (int64_t t = M->row_ptr[i]; t < M->row_ptr[i + 1]; ++t) {
+      int64_t j = M->cols[t];
+      double dl[3], r2 = 0.0;
+      for (int d = 0; d < 3; ++d) {
+        dl[d] = md_min_image(x[3 * i + d] - x[3 * j + d], L[d], per[d]);
+        r2 += dl[d] * dl[d];
+      }
+      if (!(r2 < rc2) || r2 == 0.0) continue;
+      double rr = sqrt(r2);
+      double re = (r_min > 0 && rr < r_min) ? r_min : rr;
+      double fm = lj_mdVdr(re, eps, sig);
+      for (int d = 0; d < 3; ++d) f[d] += fm * dl[d] / rr;
+      double v = lj_V(re, eps, sig);
+      u += 0.5 * v;
+      us += 0.5 * (v - vrc);
+      np += 1.0;
+    }
+    F[3 * i + 0] = f[0];
+    F[3 * i + 1] = f[1];
+    F[3 * i + 2] = f[2];
+  }
+  *Uraw = u;
+  *Ushift = us;
+  *npairs = np;
+}
+
+int64_t orc_md_cells_run(int64_t n, double *x, double *v, const double lo[3], const double hi[3],
+                         const int32_t per[3], double rc, double skin, double eps, double sigma,
+                         double r_min, double mass, double dt, int64_t nsteps, double *trace) {
+  double L[3] = {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]};
+  double rv = rc + skin;
+  md_lists_t M;
+  memset(&M, 0, sizeof M);
+  for (int d = 0; d < 3; ++d) {
+    M.nc[d] = (int)floor(L[d] / rv);
+    if (M.nc[d] < 1) M.nc[d] = 1;
+    if (per[d] && M.nc[d] < 3) return -1;
+    M.inv_w[d] = M.nc[d] / L[d];
+  }
+  int64_t ncell = (int64_t)M.nc[0] * M.nc[1] * M.nc[2];
+  size_t nn = (size_t)(n > 0 ? n : 1);
+  M.start = (int64_t *)malloc(sizeof(int64_t) * (size_t)(ncell + 1));
+  M.idx = (int64_t *)malloc(sizeof(int64_t) * nn);
+  M.row_ptr = (int64_t *)malloc(sizeof(int64_t) * (nn + 1));
+  double *F = (double *)malloc(sizeof(double) * 3 * nn);
+  double *xref = (double *)malloc(sizeof(double) * 3 * nn);
+  int64_t builds = 0;
+  md_build(n, x, lo, L, per, rv, &M);
+  memcpy(xref, x, sizeof(double) * 3 * (size_t)n);
+  builds++;
+  double u, us, np;
+  md_forces(n, x, L, per, &M, rc, eps, sigma, r_min, F, &u, &us, &np);
+  double half2 = 0.25 * skin * skin;
+  for (int64_t s = 0;; ++s) {
+    if (trace) {
+      double ke = 0;
+      for (int64_t i = 0; i < 3 * n; ++i) ke += 0.5 * mass * v[i] * v[i];
+      trace[4 * s + 0] = ke;
+      trace[4 * s + 1] = u;
+      trace[4 * s + 2] = us;
+      trace[4 * s + 3] = np;
+    }
+    if (s == nsteps) break;
+    int far = 0;
+#pragma omp parallel for schedule(static) reduction(| : far)
+    for (int64_t i = 0; i < n; ++i) {
+      double d2 = 0.0;
+      for (int d = 0; d < 3; ++d) {
+        v[3 * i + d] += 0.5 * dt * F[3 * i + d] / mass;
+        double xx = x[3 * i + d] + dt * v[3 * i + d];
+        if (per[d]) {
+          if (xx >= hi[d]) xx -= L[d];
+          else if (xx < lo[d]) xx += L[d];
+        }
+        x[3 * i + d] = xx;
+        double e = md_min_image(xx - xref[3 * i + d], L[d], per[d]);
+        d2 += e * e;
+      }
+      if (d2 > half2) far = 1;
+    }
+    if (far) {
+      md_build(n, x, lo, L, per, rv, &M);
+      memcpy(xref, x, sizeof(double) * 3 * (size_t)n);
+      builds++;
+    }
+    md_forces(n, x, L, per, &M, rc, eps, sigma, r_min, F, &u, &us, &np);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < 3 * n; ++i) v[i] += 0.5 * dt * F[i] / mass;
+  }
+  free(M.start);
+  free(M.idx);
+  free(M.row_ptr);
+  free(M.cols);
+  free(F);
+  free(xref);
+  return builds;
+}

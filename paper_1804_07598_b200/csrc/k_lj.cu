@@ -202,19 +202,24 @@ __device__ __forceinline__ void block_add_energy(State *st, double u, double w, 
 // partner at distance 0 (identical wrapped coordinates; such pairs pass the
 // list test 0 <= d2 < r_v^2 in any cell, however crowded), else
 // PM_E_NONFINITE.
-__device__ __noinline__ void raise_bad_force(const Bufs &B, State *st, const float4 *pos, int i,
-                                             const float4 &xi) {
-  const int cnt = B.cnt[i];
-  const int *nb = B.nbr + nbr_row_base(B, i);
+__device__ __noinline__ void raise_bad_force(const int *nb, int cnt, const float4 *pos, int i,
+                                             float xx, float xy, float xz, long long gid,
+                                             State *st) {
   for (int k = 0; k < cnt; ++k) {
     const int j = nb[(int64_t)k << 5];
     const float4 xj = pos[j];
-    if (j != i && xj.x == xi.x && xj.y == xi.y && xj.z == xi.z) {
-      raise_error(st, -7 /*PM_E_COINCIDENT*/, (long long)B.gid[st->cur_id][i]);
+    if (j != i && xj.x == xx && xj.y == xy && xj.z == xz) {
+      raise_error(st, -7 /*PM_E_COINCIDENT*/, gid);
       return;
     }
   }
-  raise_error(st, -8 /*PM_E_NONFINITE*/, (long long)B.gid[st->cur_id][i]);
+  raise_error(st, -8 /*PM_E_NONFINITE*/, gid);
+}
+
+__device__ __forceinline__ void bad_force(const Bufs &B, State *st, const float4 *pos, int i,
+                                          const float4 &xi) {
+  raise_bad_force(B.nbr + nbr_row_base(B, i), B.cnt[i], pos, i, xi.x, xi.y, xi.z,
+                  (long long)B.gid[st->cur_id][i], st);
 }
 
 // pm_compute_lj: forces (+ energy) of the current positions.
@@ -228,7 +233,7 @@ __global__ void __launch_bounds__(256) k_lj(Params P, Bufs B, int n) {
   Acc a = lj_force_of<CAPPED, ENERGY>(P, B, pos, i, active, xi);
   if (active) {
     B.force[i] = make_float4(a.fx, a.fy, a.fz, 0.f);
-    if (!isfinite(a.fx + a.fy + a.fz)) raise_bad_force(B, st, pos, i, xi);
+    if (!isfinite(a.fx + a.fy + a.fz)) bad_force(B, st, pos, i, xi);
   }
   if (ENERGY) block_add_energy(st, (double)a.u, (double)a.w, (double)a.np);
 }
@@ -309,7 +314,7 @@ __device__ __forceinline__ void vv_epilogue(const Params &P, const Bufs &B, Stat
       B.force[i] = make_float4(a.fx, a.fy, a.fz, 0.f);
     }
     B.vel[cp ^ 1][i] = v;
-    if (!isfinite(a.fx + a.fy + a.fz)) raise_bad_force(B, st, B.pos[cp], i, xi);
+    if (!isfinite(a.fx + a.fy + a.fz)) bad_force(B, st, B.pos[cp], i, xi);
   }
 }
 

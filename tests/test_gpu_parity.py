@@ -680,10 +680,14 @@ def test_empty_inputs(pm):
     c.set_domain(s.lo, s.hi, s.periodic)
     c.set_cutoff(2.5, 0.3)
     c.set_lj(1.0, 1.0, 1.0, 0.0)
-    c.place(empty, empty, np.zeros(0, np.int64))
     with pytest.raises(pm.PMError) as e:
         c.build_verlet()
     assert e.value.code == -2
+    # an empty placement is a valid (empty) system: an empty sub-domain of a
+    # decomposition must build and step
+    c.place(empty, empty, np.zeros(0, np.int64))
+    c.build_verlet()
+    assert c.step_vv(0.005, 2)["steps"] == 2
     c.place(s.pos, s.vel, s.gid)
     c.build_verlet()
     c.place(empty, empty, np.zeros(0, np.int64))
