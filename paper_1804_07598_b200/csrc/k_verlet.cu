@@ -10,6 +10,7 @@
 #include "pm_internal.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace pm {
 
@@ -276,6 +277,412 @@ __global__ void __launch_bounds__(256, 4) k_verlet(Params P, Bufs B, int n) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Staged build (the default whenever the widest slice fits in shared memory).
+// Same segments, runs and pinned test as k_verlet, mapped differently:
+//  * per (dy, dz) stencil row, lane t computes the row's candidate runs (up to
+//    two pieces split at the periodic seam) into a per-warp piece table;
+//  * the warp walks the pieces in stages of 128 candidates: each lane loads 4
+//    candidates with coalesced 16-byte loads one stage AHEAD (registers), the
+//    stage is written to shared memory with the run's candidate shift applied
+//    (x, y of candidate pairs interleaved for paired fp32 arithmetic);
+//  * every lane tests its own particle against the staged candidates two at a
+//    time with sub/mul/fma.rn.f32x2 (FADD2/FMUL2/FFMA2: each half is the
+//    single-rounded operation of R4/R4', so d2 is bit-identical to the scalar
+//    test); hits are appended to the warp's rows kept in shared memory in the
+//    SELL-32 layout of the slice (entry k of lane l at [k][l], conflict-free);
+//  * at the end the slice's rows leave as full 128-byte lines (16-byte stores
+//    over a contiguous range): no partial-line writes, no write amplification.
+// ---------------------------------------------------------------------------
+namespace stg {
+constexpr int kWarps = 4;       // warps per block (independent of each other)
+constexpr int kStage = 128;     // candidates per stage
+constexpr int kOffBits = 10;    // row entry in shared memory: piece << 10 | offset
+constexpr int kMaxPieceLen = 1 << kOffBits;
+constexpr int kStageBytes = kStage / 2 * 16 + kStage / 2 * 8;  // A + Z
+template <int RCH>
+struct Geo {
+  static constexpr int NR = (2 * RCH + 1) * (2 * RCH + 1);  // stencil rows
+  static constexpr int NP = 2 * NR;                        // pieces (seam split)
+  static constexpr int kTable = NP * 40;                   // be + csh + osh
+  __host__ __device__ static size_t warp_bytes(int wcap) {
+    return (size_t)((kStageBytes + kTable + wcap * 64 + 15) & ~15);
+  }
+};
+}  // namespace stg
+
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 f2_pack(float lo, float hi) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(u64 v, float &lo, float &hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ u64 f2_sub(u64 a, u64 b) {
+  u64 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 f2_mul(u64 a, u64 b) {
+  u64 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 f2_fma(u64 a, u64 b, u64 c) {
+  u64 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+// The staged build's rows while a segment is scanned: per lane either 16-bit
+// codes in shared memory (piece << 10 | offset in the piece, decoded when the
+// segment ends) or, for segments with pieces longer than 1024 candidates
+// (crowded cells), int32 indices stored straight into the global row.
+struct StRows {
+  unsigned short *sm;  // [k][lane] codes (64 bytes per line)
+  int *gl;             // global row of this lane: entry k at gl[k << 5]
+  bool direct;
+};
+
+// Append the hits of one group of 32 staged candidates (indices jg + u, codes
+// cg + u) through the bit mask (overflow, per-pair R4, half lists).
+template <int NMODE>
+__device__ __forceinline__ void st_expand(unsigned msk, int jg, int cg, int self, int cap,
+                                          int lane, const StRows &R, int &k,
+                                          const GhostRule &gr) {
+  if (NMODE == 1) {
+    const int t = self - jg;
+    msk &= t < 0 ? 0xffffffffu : (t >= 31 ? 0u : (0xffffffffu << (t + 1)));
+  } else if (self >= jg && self < jg + 32) {
+    msk &= ~(1u << (self - jg));
+  }
+  while (msk) {
+    const int u = __ffs(msk) - 1;
+    msk &= msk - 1u;
+    const int j = jg + u;
+    if (NMODE == 2) {
+      if ((gr.kind[j] & kGhostBit) ? (gr.gid[j] < gr.gid_self) : (j < self)) continue;
+    }
+    const int kk = min(k, cap - 1);
+    if (R.direct) R.gl[(int64_t)kk << 5] = j;
+    else R.sm[(kk << 5) + lane] = (unsigned short)(cg + u);
+    ++k;
+  }
+}
+
+template <int RCH, int NMODE>
+__global__ void __launch_bounds__(stg::kWarps * 32, 5)
+    k_verlet_st(Params P, Bufs B, int n, int wcap) {
+  using namespace stg;
+  constexpr int NR = Geo<RCH>::NR, NP = Geo<RCH>::NP;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char *wbase_s = smem_raw + (size_t)wid * Geo<RCH>::warp_bytes(wcap);
+  float4 *SA = reinterpret_cast<float4 *>(wbase_s);
+  float2 *SZ = reinterpret_cast<float2 *>(wbase_s + kStage / 2 * 16);
+  int2 *PBE = reinterpret_cast<int2 *>(wbase_s + kStageBytes);
+  float4 *PCS = reinterpret_cast<float4 *>(wbase_s + kStageBytes + NP * 8);
+  float4 *POS = PCS + NP;
+  unsigned short *rows = reinterpret_cast<unsigned short *>(wbase_s + kStageBytes + NP * 40);
+  State *st = B.st;
+  const int i = (blockIdx.x * kWarps + wid) * 32 + lane;
+  const int wbase = i - lane;
+  if (wbase >= n) return;  // whole warp out of range
+  const bool active = i < n && !(P.dist && (B.kind[st->cur_id][i] & kGhostBit));
+  const int cap = nbr_row_cap(B, wbase);
+  int *grow = B.nbr + B.slice_off[wbase >> 5] * 32 + lane;
+  const int nx = P.grid.n[0], ny = P.grid.n[1], nz = P.grid.n[2];
+  const float4 *__restrict__ pos = B.pos[st->cur_pv];
+  const float4 xi = active ? pos[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  GhostRule gr{nullptr, nullptr, 0};
+  if (NMODE == 2) {
+    gr.kind = B.kind[st->cur_id];
+    gr.gid = B.gid[st->cur_id];
+    gr.gid_self = active ? B.gid[st->cur_id][i] : 0;
+  }
+  int cell = -1;
+  if (active) {
+    const int c0 = local_coord(P.box, P.grid, 0, xi.x);
+    const int c1 = local_coord(P.box, P.grid, 1, xi.y);
+    const int c2 = local_coord(P.box, P.grid, 2, xi.z);
+    cell = c0 + nx * (c1 + ny * c2);
+  }
+  const int pmi_dec = (P.box.per[0] && !P.grid.wrap[0] ? 1 : 0) |
+                      (P.box.per[1] && !P.grid.wrap[1] ? 2 : 0) |
+                      (P.box.per[2] && !P.grid.wrap[2] ? 4 : 0);
+  const int row_id = active ? cell / nx : 0x7fffffff;
+  int k = 0;
+  const float INF = __int_as_float(0x7f800000);
+  const float rv2 = P.rv2;
+  unsigned todo = __ballot_sync(0xffffffffu, active);
+  while (todo) {
+    const int lead = __ffs(todo) - 1;
+    const int seg_row = __shfl_sync(0xffffffffu, row_id, lead);
+    const bool mine = active && row_id == seg_row;
+    const unsigned seg = __ballot_sync(0xffffffffu, mine);
+    todo &= ~seg;
+    int cmin = mine ? cell % nx : 0x7fffffff, cmax = mine ? cell % nx : -1;
+    cmin = __reduce_min_sync(0xffffffffu, cmin);
+    cmax = __reduce_max_sync(0xffffffffu, cmax);
+    const int cy = seg_row % ny, cz = seg_row / ny;
+    int xa = cmin - RCH, xb = cmax + RCH;
+    int pmi_x = 0;
+    if (!P.grid.wrap[0]) {
+      xa = max(xa, 0);
+      xb = min(xb, nx - 1);
+      if ((pmi_dec & 1) && !(xa >= P.grid.safe_lo[0] && xb <= P.grid.safe_hi[0])) pmi_x = 1;
+    } else if (xb - xa + 1 >= nx) {
+      xa = 0;
+      xb = nx - 1;
+      pmi_x = 1;
+    }
+    __syncwarp();  // the previous segment's readers are done with the table
+    bool long_piece = false;
+    for (int t = lane; t < NR; t += 32) {  // stencil row t = (dz, dy), dz outer
+      const int dz = t / (2 * RCH + 1) - RCH, dy = t % (2 * RCH + 1) - RCH;
+      int2 be0 = make_int2(0, 0), be1 = make_int2(0, 0);
+      float4 c0 = make_float4(0.f, 0.f, 0.f, 0.f), o0 = c0, c1 = c0, o1 = c0;
+      bool ok = true;
+      int qz = cz + dz;
+      float shz = 0.f, lz = 0.f;
+      if (qz < 0 || qz >= nz) {
+        if (!P.grid.wrap[2]) ok = false;
+        else if (qz < 0) { qz += nz; shz = P.box.L[2]; }
+        else { qz -= nz; lz = P.box.L[2]; }
+      }
+      int qy = cy + dy;
+      float shy = 0.f, ly = 0.f;
+      if (qy < 0 || qy >= ny) {
+        if (!P.grid.wrap[1]) ok = false;
+        else if (qy < 0) { qy += ny; shy = P.box.L[1]; }
+        else { qy -= ny; ly = P.box.L[1]; }
+      }
+      if (ok) {
+        const int rowc = nx * (qy + ny * qz);
+        const int pmi = pmi_x |
+                        ((pmi_dec & 2) && !(min(cy, qy) >= P.grid.safe_lo[1] &&
+                                            max(cy, qy) <= P.grid.safe_hi[1]) ? 2 : 0) |
+                        ((pmi_dec & 4) && !(min(cz, qz) >= P.grid.safe_lo[2] &&
+                                            max(cz, qz) <= P.grid.safe_hi[2]) ? 4 : 0);
+        int a0 = xa, b0 = xb, a1 = 0, b1 = -1;
+        float sx0 = 0.f, lx0 = 0.f, sx1 = 0.f, lx1 = 0.f;
+        if (xa < 0) {
+          a0 = xa + nx; b0 = nx - 1; sx0 = P.box.L[0];
+          a1 = 0; b1 = xb;
+        } else if (xb > nx - 1) {
+          a0 = xa; b0 = nx - 1;
+          a1 = 0; b1 = xb - nx; lx1 = P.box.L[0];
+        }
+        be0 = make_int2(B.start[rowc + a0], B.start[rowc + b0 + 1]);
+        c0 = make_float4((pmi & 1) ? 0.f : sx0, shy, shz, __int_as_float(pmi));
+        o0 = make_float4(lx0, ly, lz, 0.f);
+        if (b1 >= a1) {
+          be1 = make_int2(B.start[rowc + a1], B.start[rowc + b1 + 1]);
+          c1 = make_float4(sx1, shy, shz, __int_as_float(pmi & ~1));
+          o1 = make_float4(lx1, ly, lz, 0.f);
+        }
+      }
+      long_piece |= (be0.y - be0.x > kMaxPieceLen) || (be1.y - be1.x > kMaxPieceLen);
+      PBE[2 * t] = be0;
+      PCS[2 * t] = c0;
+      POS[2 * t] = o0;
+      PBE[2 * t + 1] = be1;
+      PCS[2 * t + 1] = c1;
+      POS[2 * t + 1] = o1;
+    }
+    const StRows R{rows, grow, __any_sync(0xffffffffu, long_piece) != 0};
+    __syncwarp();
+    // stage iterator over the pieces: (p, o) = piece, offset inside it
+    int p = 0;
+    while (p < NP && PBE[p].x >= PBE[p].y) ++p;
+    int o = 0;
+    float4 pre[4];
+    if (p < NP) {
+      const int2 be = PBE[p];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = be.x + lane + 32 * q;
+        pre[q] = (j < be.y) ? pos[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    while (p < NP) {
+      const int2 be = PBE[p];
+      const int jb = be.x + o;
+      const int cntc = min(kStage, be.y - jb);
+      const float4 csh = PCS[p], osh = POS[p];
+      const int pmi = __float_as_int(csh.w);
+      __syncwarp();  // the previous stage's readers are done
+      const int cnt8 = (cntc + 7) & ~7;  // the tail up to a multiple of 8 holds +inf
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int u = lane + 32 * q;
+        if (u < cnt8) {
+          float *a = reinterpret_cast<float *>(&SA[u >> 1]);
+          float *z = reinterpret_cast<float *>(&SZ[u >> 1]);
+          const bool v = u < cntc;
+          a[u & 1] = v ? __fsub_rn(pre[q].x, csh.x) : INF;
+          a[2 + (u & 1)] = v ? __fsub_rn(pre[q].y, csh.y) : INF;
+          z[u & 1] = v ? __fsub_rn(pre[q].z, csh.z) : INF;
+        }
+      }
+      // advance and prefetch the next stage (overlaps this stage's tests)
+      int pn = p, on = o + kStage;
+      if (on >= be.y - be.x) {
+        on = 0;
+        ++pn;
+        while (pn < NP && PBE[pn].x >= PBE[pn].y) ++pn;
+      }
+      if (pn < NP) {
+        const int2 bn = PBE[pn];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = bn.x + on + lane + 32 * q;
+          pre[q] = (j < bn.y) ? pos[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      __syncwarp();
+      const float4 xe = mine ? make_float4(__fsub_rn(xi.x, osh.x), __fsub_rn(xi.y, osh.y),
+                                           __fsub_rn(xi.z, osh.z), 0.f)
+                             : make_float4(INF, INF, INF, 0.f);
+      const u64 XI = f2_pack(xe.x, xe.x), YI = f2_pack(xe.y, xe.y), ZI = f2_pack(xe.z, xe.z);
+      const int cb = (p << kOffBits) + o;  // code of the stage's first candidate
+      for (int g = 0; g < cntc; g += 32) {
+        const int gn = min(32, cntc - g);
+        if (NMODE == 0 && !pmi && !R.direct && !__any_sync(0xffffffffu, k + gn > cap)) {
+          // fast path: every candidate's code is stored at the row's next
+          // slot and the slot advances on a hit (no mask, no divergent
+          // expansion); the +inf tail of the stage never hits
+          const int k0 = k;
+          const unsigned rows_sa = smem_u32(rows);
+          unsigned bo = rows_sa + (unsigned)(((k << 5) + lane) << 1);
+#pragma unroll
+          for (int u8 = 0; u8 < 4; ++u8) {
+            if (u8 >= ((gn + 7) >> 3)) break;
+            // 8 candidates: loads first, then the arithmetic, then the appends
+            float4 a[4];
+            float4 z[2];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) a[q] = SA[(g >> 1) + 4 * u8 + q];
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+              z[q] = reinterpret_cast<const float4 *>(SZ)[(g >> 2) + 2 * u8 + q];
+            float sd[8];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float zl = (q & 1) ? z[q >> 1].z : z[q >> 1].x;
+              const float zh = (q & 1) ? z[q >> 1].w : z[q >> 1].y;
+              const u64 dx = f2_sub(f2_pack(a[q].x, a[q].y), XI);
+              const u64 dy = f2_sub(f2_pack(a[q].z, a[q].w), YI);
+              const u64 dz = f2_sub(f2_pack(zl, zh), ZI);
+              u64 s2 = f2_mul(dx, dx);
+              s2 = f2_fma(dy, dy, s2);
+              s2 = f2_fma(dz, dz, s2);
+              f2_unpack(s2, sd[2 * q], sd[2 * q + 1]);
+            }
+            const int c0 = cb + g + 8 * u8;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t.reg .u32 v;\n\t"
+                "st.shared.u16 [%0], %1;\n\t"
+                "setp.lt.f32 p, %2, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
+                "add.u32 v, %1, 1;\n\tst.shared.u16 [%0], v;\n\t"
+                "setp.lt.f32 p, %3, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
+                "add.u32 v, %1, 2;\n\tst.shared.u16 [%0], v;\n\t"
+                "setp.lt.f32 p, %4, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
+                "add.u32 v, %1, 3;\n\tst.shared.u16 [%0], v;\n\t"
+                "setp.lt.f32 p, %5, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
+                "add.u32 v, %1, 4;\n\tst.shared.u16 [%0], v;\n\t"
+                "setp.lt.f32 p, %6, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
+                "add.u32 v, %1, 5;\n\tst.shared.u16 [%0], v;\n\t"
+                "setp.lt.f32 p, %7, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
+                "add.u32 v, %1, 6;\n\tst.shared.u16 [%0], v;\n\t"
+                "setp.lt.f32 p, %8, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
+                "add.u32 v, %1, 7;\n\tst.shared.u16 [%0], v;\n\t"
+                "setp.lt.f32 p, %9, %10;\n\t@p add.u32 %0, %0, 64;\n\t}"
+                : "+r"(bo)
+                : "r"(c0), "f"(sd[0]), "f"(sd[1]), "f"(sd[2]), "f"(sd[3]), "f"(sd[4]),
+                  "f"(sd[5]), "f"(sd[6]), "f"(sd[7]), "f"(rv2));
+          }
+          asm volatile("" ::: "memory");  // the C++ reads below see the appends
+          k = (int)((bo - rows_sa) >> 6);
+          // the particle itself (d2 = 0) was appended once: swap-remove it
+          const int jg = jb + g;
+          if (i >= jg && i < jg + gn) {
+            const unsigned short sc = (unsigned short)(cb + g + (i - jg));
+            for (int t = k0; t < k; ++t) {
+              if (rows[(t << 5) + lane] == sc) {
+                rows[(t << 5) + lane] = rows[((k - 1) << 5) + lane];
+                --k;
+                break;
+              }
+            }
+          }
+          continue;
+        }
+        unsigned msk = 0u;
+        if (pmi) {  // per-pair R4 on the axes in pmi (scalar, rare)
+          for (int u = 0; u < gn; ++u) {
+            const int v = g + u;
+            const float *a = reinterpret_cast<const float *>(&SA[v >> 1]);
+            const float *z = reinterpret_cast<const float *>(&SZ[v >> 1]);
+            const float4 xj = make_float4(a[v & 1], a[2 + (v & 1)], z[v & 1], 0.f);
+            if (d2_of<false, true>(P, xe, make_float3(0.f, 0.f, 0.f), pmi, xj) < rv2)
+              msk |= 1u << u;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            if (2 * q >= gn) break;
+            const float4 a = SA[(g >> 1) + q];
+            const float2 z = SZ[(g >> 1) + q];
+            const u64 dx = f2_sub(f2_pack(a.x, a.y), XI);
+            const u64 dy = f2_sub(f2_pack(a.z, a.w), YI);
+            const u64 dz = f2_sub(f2_pack(z.x, z.y), ZI);
+            u64 s2 = f2_mul(dx, dx);
+            s2 = f2_fma(dy, dy, s2);
+            s2 = f2_fma(dz, dz, s2);
+            float s0, s1;
+            f2_unpack(s2, s0, s1);
+            if (s0 < rv2) msk |= 1u << (2 * q);
+            if (s1 < rv2) msk |= 2u << (2 * q);
+          }
+          if (gn < 32) msk &= (1u << gn) - 1u;
+        }
+        st_expand<NMODE>(msk, jb + g, cb + g, i, cap, lane, R, k, gr);
+      }
+      p = pn;
+      o = on;
+    }
+    // segment end: the segment's rows go to global memory (decoded), padded
+    // to a multiple of 4 with the particle's own index (the sweeps read groups
+    // of 4 and mask padding slots)
+    __syncwarp();
+    const int kseg = __reduce_max_sync(0xffffffffu, mine ? min(k, cap) : 0);
+    if (!R.direct) {
+      for (int kk = 0; kk < kseg; ++kk) {
+        if (mine && kk < k) {
+          const unsigned c = rows[(kk << 5) + lane];
+          grow[(int64_t)kk << 5] = PBE[c >> kOffBits].x + (int)(c & (kMaxPieceLen - 1));
+        }
+      }
+    }
+    if (mine)
+      for (int q = min(k, cap); q < cap && (q & 3) != 0; ++q) grow[(int64_t)q << 5] = i;
+  }
+  if (i < n) B.cnt[i] = active ? k : 0;
+  const int kmax = __reduce_max_sync(0xffffffffu, k);
+  const unsigned ksum = __reduce_add_sync(0xffffffffu, (unsigned)k);
+  if (lane == 0 && ksum > 0) {
+    atomicMax(&st->max_row, kmax);
+    atomicAdd(reinterpret_cast<unsigned long long *>(&st->nnz), (unsigned long long)ksum);
+    if (kmax > cap) {
+      atomicMax(&st->overflow_need, kmax);
+      raise_error(st, -9 /*PM_E_CAPACITY*/, -1);
+    }
+  }
+}
+
 __global__ void k_reset_build_stats(State *st) {
   st->max_row = 0;
   st->nnz = 0;
@@ -319,11 +726,47 @@ __global__ void __launch_bounds__(256) k_verlet_shifts(Params P, Bufs B, int n,
 
 }  // namespace
 
+// Shared memory of the staged build per block; 0 when the widest slice does
+// not fit (clustered inputs with rows of thousands of entries: k_verlet).
+template <int RCH>
+static size_t staged_smem(int wcap) {
+  const size_t tot = stg::kWarps * stg::Geo<RCH>::warp_bytes(wcap);
+  return (wcap > 0 && tot <= 200 * 1024) ? tot : 0;
+}
+
+template <int RCH, int NMODE>
+static void launch_st(const Params &P, const Bufs &B, int64_t n, size_t sm, cudaStream_t s) {
+  static size_t set = 0;
+  if (sm > set) {
+    cudaFuncSetAttribute(k_verlet_st<RCH, NMODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
+    set = sm;
+  }
+  const unsigned g = (unsigned)((n + stg::kWarps * 32 - 1) / (stg::kWarps * 32));
+  k_verlet_st<RCH, NMODE><<<g, stg::kWarps * 32, sm, s>>>(P, B, (int)n, P.nbr_cap);
+}
+
 void launch_verlet(const Params &P, const Bufs &B, int64_t n, cudaStream_t s) {
   k_reset_build_stats<<<1, 1, 0, s>>>(B.st);
   if (n <= 0) return;
   const unsigned g = (unsigned)((n + 255) / 256);
   const int nm = P.newton ? (P.dist ? 2 : 1) : 0;
+  const size_t sm = P.reach == 2 ? staged_smem<2>(P.nbr_cap) : staged_smem<1>(P.nbr_cap);
+  static const int staged_env = [] {
+    const char *e = std::getenv("PM_VERLET_STAGED");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  if (sm && staged_env) {
+    if (P.reach == 2) {
+      if (nm == 1) launch_st<2, 1>(P, B, n, sm, s);
+      else launch_st<2, 0>(P, B, n, sm, s);
+    } else {
+      if (nm == 2) launch_st<1, 2>(P, B, n, sm, s);
+      else if (nm == 1) launch_st<1, 1>(P, B, n, sm, s);
+      else launch_st<1, 0>(P, B, n, sm, s);
+    }
+    return;
+  }
   if (P.reach == 2) {
     if (nm == 1) k_verlet<2, 1><<<g, 256, 0, s>>>(P, B, (int)n);
     else k_verlet<2, 0><<<g, 256, 0, s>>>(P, B, (int)n);
