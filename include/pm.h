@@ -460,6 +460,74 @@ pm_status pm_dist_sph_update(pm_ctx ctx, float bound, float cfl, int32_t every,
 pm_status pm_dist_refresh_pv_pack(pm_ctx ctx, void *send_dev);
 pm_status pm_dist_refresh_pv_unpack(pm_ctx ctx, const void *recv_dev);
 
+/* ---------------------------------------------------------------------------
+ * Multi-GPU groups: map() and ghost_get<>() behind the ABI (SURVEY §8(b),
+ * §8(e); §3.1 sub-domains with a ghost layer of interaction
+ * width; §3.4 map / ghost_get "only communicate"; Listing
+ * 4.1 map() and ghost_get<>() at PAPER.md:299-303).
+ *
+ * A group is one px x py x pz cuboid decomposition of the periodic box (as
+ * pm_set_decomposition); each member context owns one sub-domain, index
+ * cx + px (cy + py cz).  Members are created by pm_create_dist (one per
+ * process and GPU, a library-owned NCCL communicator; nranks = px py pz) or
+ * pm_create_dist_local (all sub-domains in this process on one GPU: the
+ * in-process loopback group, messages as device copies -- or through NCCL
+ * self-communication with via_nccl = 1, to exercise the NCCL path on one
+ * GPU).  Every member is then set up as a plain context: pm_set_domain,
+ * pm_set_cutoff, pm_set_lj, pm_place (any particles: map sends them to their
+ * owners; the decomposition is applied at the first pm_map).  Decomposed axes
+ * must be periodic and sub-domains at least 2 r_v thick (PM_E_INVAL).
+ *
+ * Collective calls: every member calls them, in the same order; the call of
+ * the LAST local member does the work for all local members (so one host
+ * thread drives a loopback group member by member) and writes the outputs;
+ * earlier members' calls return PM_OK without touching their outputs.
+ * Members of one process share one CUDA stream (opts.cuda_stream, or a
+ * group-owned stream) on which NCCL is called.  Errors: PM_E_NCCL when NCCL
+ * cannot be loaded or a communicator call fails; PM_E_STATE when members call
+ * different collectives.  pm_destroy of the last member frees the group and
+ * its communicator. */
+
+/* 128 bytes of an NCCL unique id (rank 0 creates it and broadcasts it, e.g.
+ * with torch.distributed.broadcast_object_list). */
+pm_status pm_nccl_unique_id(uint8_t id[128]);
+
+/* The member of rank `rank` (its sub-domain index) of an nranks-process group
+ * with decomposition grid[3] (grid[0] grid[1] grid[2] == nranks); initialises
+ * the group's NCCL communicator (ncclCommInitRank, collective over ranks). */
+pm_status pm_create_dist(const pm_opts *opts, int32_t rank, int32_t nranks, const uint8_t id[128],
+                         const int32_t grid[3], pm_ctx *out);
+
+/* All grid[0] grid[1] grid[2] members in this process: out[sub-domain]. */
+pm_status pm_create_dist_local(const pm_opts *opts, const int32_t grid[3], int32_t via_nccl,
+                               pm_ctx *out);
+
+/* This member's sub-domain, the number of sub-domains, its rank and the
+ * number of ranks.  PM_E_STATE for a context that is not a group member. */
+pm_status pm_dist_info(pm_ctx ctx, int32_t *sub_domain, int32_t *nsub, int32_t *rank,
+                       int32_t *nranks);
+
+/* map() (collective): every owned particle outside its sub-domain moves to
+ * the owner (64-byte records, ghosts dropped).  Synchronises (counts). */
+pm_status pm_map(pm_ctx ctx);
+
+/* ghost_get<>() (collective): ghost copies of every owned particle within r_v
+ * of a neighbour's face, edge or corner (32-byte records), then each member's
+ * cell list over owned + ghosts and Verlet rows of its owned particles. */
+pm_status pm_ghost_get(pm_ctx ctx);
+
+/* nsteps velocity-Verlet steps of the whole group (collective): per step the
+ * positions-only ghost refresh (16 B per ghost), the fused force sweep and
+ * kick/drift of every member, and the global rebuild flag (MAX all-reduce);
+ * when any particle moved more than skin/2, pm_map + pm_ghost_get.  Forces
+ * are computed first when not valid.  out: steps and rebuilds (performer). */
+pm_status pm_dist_run(pm_ctx ctx, float dt, int64_t nsteps, pm_run_stats *out);
+
+/* Global (all sub-domains) kinetic energy, raw and shifted LJ energy, virial
+ * and ordered pair count (collective; recomputes the energy pass). */
+pm_status pm_dist_thermo(pm_ctx ctx, double *ke, double *pe_raw, double *pe_shift,
+                         double *virial, int64_t *npairs);
+
 #ifdef __cplusplus
 }
 #endif

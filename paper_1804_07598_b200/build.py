@@ -65,7 +65,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     tmp = LIB + f".tmp{os.getpid()}"
     objs = [obj for _, obj, _ in results]
     res = subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o",
-                          tmp, *objs], capture_output=True, text=True)
+                          tmp, *objs, "-ldl"], capture_output=True, text=True)
     for o in objs:
         os.remove(o)
     if res.returncode != 0:

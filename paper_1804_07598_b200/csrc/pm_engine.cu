@@ -677,6 +677,20 @@ pm_status run_steps(pm_ctx c, float dt, int64_t nsteps) {
 
 }  // namespace
 
+// Internal accessors for the multi-GPU group layer (pm_group.cu).
+namespace pm {
+void group_detach(pm_ctx c);  // pm_group.cu
+cudaStream_t ctx_stream(pm_ctx c) { return c->stream; }
+int ctx_device(pm_ctx c) { return c->device; }
+bool ctx_decomposed(pm_ctx c) { return c->dist; }
+bool ctx_forces_valid(pm_ctx c) { return c->forces_valid; }
+bool ctx_list_valid(pm_ctx c) { return c->list_valid; }
+bool ctx_ready(pm_ctx c) { return c->have_domain && c->have_cutoff; }
+pm_status ctx_error(pm_ctx c, pm_status code, const char *msg) {
+  return set_err(c, code, "%s", msg);
+}
+}  // namespace pm
+
 // ===========================================================================
 extern "C" {
 
@@ -774,6 +788,9 @@ void pm_destroy(pm_ctx c) {
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
+  // a group member: the group (its stream, buffers, communicator) goes with
+  // its last member (the pointer is only a key there)
+  pm::group_detach(c);
 }
 
 const char *pm_last_error(pm_ctx c) { return c ? c->err.c_str() : "null context"; }

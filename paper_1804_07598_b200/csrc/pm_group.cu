@@ -1,0 +1,807 @@
+// pm_group.cu -- multi-GPU groups behind the C-ABI: map() and ghost_get<>()
+// (SURVEY §8(b) pm_map / pm_ghost_get / pm_nccl_unique_id / pm_create_dist;
+// §8(e)).
+//
+// PAPER.md:62 (§3.1): the domain is split into sub-domains, each extended by
+// a ghost layer of interaction width; PAPER.md:112-118 (§3.4): map() sends
+// the particles that left a sub-domain to the processor that owns them and
+// ghost_get() fills the ghost layers ("mappings that only communicate",
+// non-blocking point-to-point messages); Listing 4.1 calls
+// map() and ghost_get<>() every step.
+//
+// A group is the set of sub-domains of one px x py x pz cuboid decomposition
+// (pm_set_decomposition).  Its members are pm_ctx contexts; a process owns
+// one member per rank (pm_create_dist: one GPU per process, a library-owned
+// NCCL communicator) or all of them (pm_create_dist_local: the in-process
+// loopback group of SURVEY C2 -- P sub-domains on one GPU, messages as device
+// copies, or through NCCL self-communication when asked).  Every group call
+// is collective: each member calls it once, in the same order, and the last
+// local member to call performs the work for all local members (so one host
+// thread can drive a loopback group member by member, and a process with one
+// member per rank just works).
+//
+// Message protocol (identical to the host reference in dist.py, which the
+// gloo tests check): directions d = (ax+1) + 3 (ay+1) + 9 (az+1), d != 13;
+// a direction exists when every nonzero component is along an axis with >= 2
+// sub-domains; records are packed in the order "peer ascending, then
+// direction"; per message round, first the record counts (int64 per peer),
+// then one payload per (sender, receiver) pair, received concatenated in
+// ascending sender order.  NCCL matches sends and receives between two ranks
+// in issue order: both sides issue them in ascending (sender, receiver)
+// sub-domain order inside one ncclGroupStart/End.
+//
+// The particle work (selection, packing, unpacking, cell lists, Verlet rows,
+// forces, integration) is the single-context kernels behind pm_dist_*; this
+// file only decides who talks to whom and moves bytes.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/pm.h"
+
+namespace pm {
+cudaStream_t ctx_stream(pm_ctx c);
+int ctx_device(pm_ctx c);
+bool ctx_decomposed(pm_ctx c);
+bool ctx_forces_valid(pm_ctx c);
+bool ctx_list_valid(pm_ctx c);
+bool ctx_ready(pm_ctx c);
+pm_status ctx_error(pm_ctx c, pm_status code, const char *msg);
+void group_detach(pm_ctx c);
+}  // namespace pm
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// NCCL, resolved at run time: the one torch already loaded when present
+// (RTLD_NOLOAD), else the system library.  No link-time dependency, so the
+// library loads on machines without NCCL (single-GPU use).
+struct Nccl {
+  bool tried = false, ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t,
+                       cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t,
+                            ncclComm_t, cudaStream_t) = nullptr;
+  const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+Nccl &nccl() {
+  static Nccl N;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (N.tried) return N;
+  N.tried = true;
+  void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return N;
+#define PM_SYM(field, name) N.field = reinterpret_cast<decltype(N.field)>(dlsym(h, name))
+  PM_SYM(GetUniqueId, "ncclGetUniqueId");
+  PM_SYM(CommInitRank, "ncclCommInitRank");
+  PM_SYM(CommDestroy, "ncclCommDestroy");
+  PM_SYM(GroupStart, "ncclGroupStart");
+  PM_SYM(GroupEnd, "ncclGroupEnd");
+  PM_SYM(Send, "ncclSend");
+  PM_SYM(Recv, "ncclRecv");
+  PM_SYM(AllReduce, "ncclAllReduce");
+  PM_SYM(GetErrorString, "ncclGetErrorString");
+#undef PM_SYM
+  N.ok = N.GetUniqueId && N.CommInitRank && N.CommDestroy && N.GroupStart && N.GroupEnd &&
+         N.Send && N.Recv && N.AllReduce && N.GetErrorString;
+  return N;
+}
+
+// ---------------------------------------------------------------------------
+constexpr int kSelf = 13;
+
+struct Dirs {
+  int a[27][3];
+  Dirs() {
+    for (int d = 0; d < 27; ++d) {
+      a[d][0] = d % 3 - 1;
+      a[d][1] = (d / 3) % 3 - 1;
+      a[d][2] = d / 9 - 1;
+    }
+  }
+};
+const Dirs kDirs;
+
+enum Op { kOpNone = 0, kOpMap, kOpGhost, kOpRun, kOpThermo };
+
+struct Member {
+  pm_ctx ctx = nullptr;
+  int sd = -1;  // sub-domain index (cx + px (cy + py cz))
+  std::vector<int> peers;               // ascending
+  std::vector<int> order;               // 26 directions, send order
+  std::vector<int64_t> seg_off, seg_n;  // send segment per peer (records)
+  std::vector<int64_t> recv_n;          // records received per peer
+  std::vector<int64_t> ghost_seg_n, ghost_recv_n;  // the last GHOST round (refresh)
+  void *sbuf = nullptr, *rbuf = nullptr;
+  size_t scap = 0, rcap = 0;
+  int64_t *d_cnt = nullptr;  // [2][26] device: counts sent / received (NCCL)
+  int64_t *h_cnt = nullptr;  // pinned mirror
+  int flag = 0;              // last local rebuild flag
+  pm_run_stats stats{};
+  double thermo[5] = {0, 0, 0, 0, 0};
+};
+
+struct Group {
+  int grid[3] = {1, 1, 1};
+  int P = 1;
+  int nranks = 1, rank = 0;
+  std::vector<int> owner;  // sub-domain -> rank
+  std::vector<Member> m;   // local members
+  ncclComm_t comm = nullptr;
+  bool via_nccl = false;   // local messages through NCCL self-communication (tests)
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int device = 0;
+  int op = kOpNone, entered = 0;
+  float run_dt = 0.f;
+  int64_t run_steps = 0;
+  int *d_flag = nullptr;
+  int *h_flag = nullptr;
+  double *d_red = nullptr;
+  double *h_red = nullptr;
+  int64_t rebuilds = 0;
+
+  int coord(int sd, int d) const {
+    return d == 0 ? sd % grid[0] : d == 1 ? (sd / grid[0]) % grid[1] : sd / (grid[0] * grid[1]);
+  }
+  bool valid_dir(int d) const {
+    if (d == kSelf) return false;
+    for (int k = 0; k < 3; ++k)
+      if (kDirs.a[d][k] != 0 && grid[k] < 2) return false;
+    return true;
+  }
+  int peer(int sd, int d) const {
+    int c[3];
+    for (int k = 0; k < 3; ++k) {
+      c[k] = coord(sd, k) + kDirs.a[d][k];
+      c[k] = ((c[k] % grid[k]) + grid[k]) % grid[k];
+    }
+    return c[0] + grid[0] * (c[1] + grid[1] * c[2]);
+  }
+  bool local(int sd) const { return owner[sd] == rank; }
+  Member *member_of(int sd) {
+    for (auto &x : m)
+      if (x.sd == sd) return &x;
+    return nullptr;
+  }
+};
+
+std::mutex g_mu;
+std::map<pm_ctx, std::pair<Group *, int>> g_members;  // ctx -> (group, local index)
+
+void setup_member_tables(Group &G, Member &M) {
+  std::vector<int> valid;
+  for (int d = 0; d < 27; ++d)
+    if (G.valid_dir(d)) valid.push_back(d);
+  std::vector<int> peers;
+  for (int d : valid) peers.push_back(G.peer(M.sd, d));
+  std::sort(peers.begin(), peers.end());
+  peers.erase(std::unique(peers.begin(), peers.end()), peers.end());
+  M.peers = peers;
+  std::vector<int> order = valid;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    const int pa = G.peer(M.sd, a), pb = G.peer(M.sd, b);
+    return pa != pb ? pa < pb : a < b;
+  });
+  for (int d = 0; d < 27; ++d)
+    if (d != kSelf && std::find(valid.begin(), valid.end(), d) == valid.end()) order.push_back(d);
+  M.order = order;
+  const size_t np = peers.size();
+  M.seg_off.assign(np, 0);
+  M.seg_n.assign(np, 0);
+  M.recv_n.assign(np, 0);
+  M.ghost_seg_n.assign(np, 0);
+  M.ghost_recv_n.assign(np, 0);
+}
+
+int peer_index(const Member &M, int q) {
+  for (size_t k = 0; k < M.peers.size(); ++k)
+    if (M.peers[k] == q) return (int)k;
+  return -1;
+}
+
+pm_status cuda_err(pm_ctx c, cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return PM_OK;
+  char buf[256];
+  std::snprintf(buf, sizeof buf, "%s: %s", what, cudaGetErrorString(e));
+  return pm::ctx_error(c, e == cudaErrorMemoryAllocation ? PM_E_NOMEM : PM_E_CUDA, buf);
+}
+
+pm_status nccl_err(pm_ctx c, ncclResult_t r, const char *what) {
+  if (r == ncclSuccess) return PM_OK;
+  char buf[256];
+  std::snprintf(buf, sizeof buf, "%s: %s", what, nccl().GetErrorString(r));
+  return pm::ctx_error(c, PM_E_NCCL, buf);
+}
+
+pm_status ensure_buf(pm_ctx c, void **p, size_t *cap, size_t need) {
+  if (need <= *cap && *p) return PM_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  const size_t n = std::max<size_t>(need + need / 4, 256);
+  pm_status s = cuda_err(c, cudaMalloc(p, n), "group buffer");
+  if (!s) *cap = n;
+  return s;
+}
+
+// Does a message between these two sub-domains go through NCCL?
+bool via_nccl(const Group &G, int a, int b) {
+  return G.comm && (!G.local(a) || !G.local(b) || G.via_nccl);
+}
+
+// Record counts of one round: every local sender's counts reach its peers.
+pm_status exchange_counts(Group &G, std::vector<std::vector<int64_t>> &send_n) {
+  // local pairs on the host
+  for (auto &R : G.m)
+    for (size_t k = 0; k < R.peers.size(); ++k) R.recv_n[k] = -1;
+  for (size_t r = 0; r < G.m.size(); ++r) {
+    Member &R = G.m[r];
+    for (size_t k = 0; k < R.peers.size(); ++k) {
+      const int q = R.peers[k];
+      if (via_nccl(G, R.sd, q)) continue;
+      Member *Q = G.member_of(q);
+      Q->recv_n[peer_index(*Q, R.sd)] = send_n[r][k];
+    }
+  }
+  if (!G.comm) return PM_OK;
+  // the rest through NCCL (device int64 per pair), ascending (sender, receiver)
+  bool any = false;
+  for (size_t r = 0; r < G.m.size(); ++r) {
+    Member &R = G.m[r];
+    for (size_t k = 0; k < R.peers.size(); ++k) R.h_cnt[k] = send_n[r][k];
+    cudaError_t e = cudaMemcpyAsync(R.d_cnt, R.h_cnt, sizeof(int64_t) * 26,
+                                    cudaMemcpyHostToDevice, G.stream);
+    if (e != cudaSuccess) return cuda_err(R.ctx, e, "counts");
+  }
+  Nccl &N = nccl();
+  N.GroupStart();
+  for (int a = 0; a < G.P; ++a) {    // sender a
+    for (int b = 0; b < G.P; ++b) {  // receiver b
+      if (!via_nccl(G, a, b)) continue;
+      Member *A = G.local(a) ? G.member_of(a) : nullptr;
+      Member *Bm = G.local(b) ? G.member_of(b) : nullptr;
+      const int ka = A ? peer_index(*A, b) : -1;
+      const int kb = Bm ? peer_index(*Bm, a) : -1;
+      if (A && ka >= 0) {
+        N.Send(A->d_cnt + ka, 1, ncclInt64, G.owner[b], G.comm, G.stream);
+        any = true;
+      }
+      if (Bm && kb >= 0) {
+        N.Recv(Bm->d_cnt + 26 + kb, 1, ncclInt64, G.owner[a], G.comm, G.stream);
+        any = true;
+      }
+    }
+  }
+  pm_status s = nccl_err(G.m[0].ctx, N.GroupEnd(), "count exchange");
+  if (s || !any) return s;
+  for (auto &R : G.m) {
+    cudaError_t e = cudaMemcpyAsync(R.h_cnt + 26, R.d_cnt + 26, sizeof(int64_t) * 26,
+                                    cudaMemcpyDeviceToHost, G.stream);
+    if (e != cudaSuccess) return cuda_err(R.ctx, e, "counts");
+  }
+  cudaError_t e = cudaStreamSynchronize(G.stream);
+  if (e != cudaSuccess) return cuda_err(G.m[0].ctx, e, "counts");
+  for (auto &R : G.m)
+    for (size_t k = 0; k < R.peers.size(); ++k)
+      if (via_nccl(G, R.peers[k], R.sd)) R.recv_n[k] = R.h_cnt[26 + k];
+  return PM_OK;
+}
+
+// Offset (records) of sender a's segment among receiver R's arrivals.
+int64_t recv_offset(const Member &R, int a) {
+  int64_t off = 0;
+  for (size_t k = 0; k < R.peers.size(); ++k) {
+    if (R.peers[k] == a) return off;
+    off += R.recv_n[k];
+  }
+  return -1;
+}
+
+// Payloads: member r's segment for peer q -> q's receive buffer at r's offset.
+pm_status exchange_payload(Group &G, size_t rec) {
+  for (auto &R : G.m) {  // local pairs: device copies
+    for (size_t k = 0; k < R.peers.size(); ++k) {
+      const int q = R.peers[k];
+      if (via_nccl(G, R.sd, q) || R.seg_n[k] == 0) continue;
+      Member *Q = G.member_of(q);
+      const int64_t off = recv_offset(*Q, R.sd);
+      cudaError_t e = cudaMemcpyAsync(static_cast<char *>(Q->rbuf) + off * rec,
+                                      static_cast<char *>(R.sbuf) + R.seg_off[k] * rec,
+                                      R.seg_n[k] * rec, cudaMemcpyDeviceToDevice, G.stream);
+      if (e != cudaSuccess) return cuda_err(R.ctx, e, "payload copy");
+    }
+  }
+  if (!G.comm) return PM_OK;
+  Nccl &N = nccl();
+  N.GroupStart();
+  for (int a = 0; a < G.P; ++a) {
+    for (int b = 0; b < G.P; ++b) {
+      if (!via_nccl(G, a, b)) continue;
+      Member *A = G.local(a) ? G.member_of(a) : nullptr;
+      Member *Bm = G.local(b) ? G.member_of(b) : nullptr;
+      const int ka = A ? peer_index(*A, b) : -1;
+      const int kb = Bm ? peer_index(*Bm, a) : -1;
+      if (A && ka >= 0 && A->seg_n[ka] > 0)
+        N.Send(static_cast<char *>(A->sbuf) + A->seg_off[ka] * rec, A->seg_n[ka] * rec,
+               ncclUint8, G.owner[b], G.comm, G.stream);
+      if (Bm && kb >= 0 && Bm->recv_n[kb] > 0)
+        N.Recv(static_cast<char *>(Bm->rbuf) + recv_offset(*Bm, a) * rec, Bm->recv_n[kb] * rec,
+               ncclUint8, G.owner[a], G.comm, G.stream);
+    }
+  }
+  return nccl_err(G.m[0].ctx, N.GroupEnd(), "payload exchange");
+}
+
+// plan -> pack -> counts -> payload -> unpack of one MIGRATE / GHOST round.
+pm_status message_round(Group &G, int what) {
+  const size_t rec = (size_t)pm_record_bytes(what);
+  std::vector<std::vector<int64_t>> send_n(G.m.size());
+  for (size_t r = 0; r < G.m.size(); ++r) {
+    Member &R = G.m[r];
+    int64_t counts[27];
+    pm_status s = pm_dist_plan(R.ctx, what, R.order.data(), counts);
+    if (s) return s;
+    int64_t off = 0;
+    for (size_t k = 0; k < R.peers.size(); ++k) {
+      R.seg_off[k] = off;
+      R.seg_n[k] = 0;
+      for (int d : R.order)
+        if (G.valid_dir(d) && G.peer(R.sd, d) == R.peers[k]) R.seg_n[k] += counts[d];
+      off += R.seg_n[k];
+    }
+    if ((s = ensure_buf(R.ctx, &R.sbuf, &R.scap, (size_t)off * rec))) return s;
+    if ((s = pm_dist_pack(R.ctx, what, off ? R.sbuf : nullptr))) return s;
+    send_n[r] = R.seg_n;
+  }
+  pm_status s = exchange_counts(G, send_n);
+  if (s) return s;
+  for (auto &R : G.m) {
+    int64_t tot = 0;
+    for (int64_t v : R.recv_n) tot += v;
+    if ((s = ensure_buf(R.ctx, &R.rbuf, &R.rcap, (size_t)tot * rec))) return s;
+  }
+  if ((s = exchange_payload(G, rec))) return s;
+  for (auto &R : G.m) {
+    int64_t tot = 0;
+    for (int64_t v : R.recv_n) tot += v;
+    if ((s = pm_dist_unpack(R.ctx, what, tot ? R.rbuf : nullptr, tot))) return s;
+    if (what == PM_MSG_GHOST) {
+      R.ghost_seg_n = R.seg_n;
+      R.ghost_recv_n = R.recv_n;
+    }
+  }
+  return PM_OK;
+}
+
+// Positions-only ghost refresh with the last GHOST round's layout (16 B per
+// ghost, "only the properties that are needed").
+pm_status refresh(Group &G) {
+  const size_t rec = (size_t)pm_record_bytes(PM_MSG_REFRESH);
+  pm_status s;
+  for (auto &R : G.m) {
+    int64_t off = 0;
+    for (size_t k = 0; k < R.peers.size(); ++k) {
+      R.seg_off[k] = off;
+      R.seg_n[k] = R.ghost_seg_n[k];
+      off += R.seg_n[k];
+    }
+    R.recv_n = R.ghost_recv_n;
+    if ((s = ensure_buf(R.ctx, &R.sbuf, &R.scap, (size_t)off * rec))) return s;
+    if ((s = pm_dist_refresh_pack(R.ctx, off ? R.sbuf : nullptr))) return s;
+    int64_t tot = 0;
+    for (int64_t v : R.recv_n) tot += v;
+    if ((s = ensure_buf(R.ctx, &R.rbuf, &R.rcap, (size_t)tot * rec))) return s;
+  }
+  if ((s = exchange_payload(G, rec))) return s;
+  for (auto &R : G.m) {
+    int64_t tot = 0;
+    for (int64_t v : R.recv_n) tot += v;
+    if ((s = pm_dist_refresh_unpack(R.ctx, tot ? R.rbuf : nullptr))) return s;
+  }
+  return PM_OK;
+}
+
+// Global MAX of the local rebuild flags (NCCL all-reduce across ranks).
+pm_status allreduce_flag(Group &G, int *flag) {
+  int f = 0;
+  for (auto &R : G.m) f = std::max(f, R.flag);
+  if (G.comm && G.nranks > 1) {
+    *G.h_flag = f;
+    cudaMemcpyAsync(G.d_flag, G.h_flag, sizeof(int), cudaMemcpyHostToDevice, G.stream);
+    pm_status s = nccl_err(G.m[0].ctx,
+                           nccl().AllReduce(G.d_flag, G.d_flag, 1, ncclInt32, ncclMax, G.comm,
+                                            G.stream),
+                           "flag all-reduce");
+    if (s) return s;
+    cudaMemcpyAsync(G.h_flag, G.d_flag, sizeof(int), cudaMemcpyDeviceToHost, G.stream);
+    cudaError_t e = cudaStreamSynchronize(G.stream);
+    if (e != cudaSuccess) return cuda_err(G.m[0].ctx, e, "flag all-reduce");
+    f = *G.h_flag;
+  }
+  *flag = f;
+  return PM_OK;
+}
+
+pm_status ensure_decomposed(Group &G) {
+  for (auto &R : G.m) {
+    if (G.P > 1 && !pm::ctx_decomposed(R.ctx)) {
+      if (!pm::ctx_ready(R.ctx))
+        return pm::ctx_error(R.ctx, PM_E_STATE, "group member: pm_set_domain / pm_set_cutoff first");
+      const int32_t c[3] = {G.coord(R.sd, 0), G.coord(R.sd, 1), G.coord(R.sd, 2)};
+      pm_status s = pm_set_decomposition(R.ctx, G.grid, c);
+      if (s) return s;
+    }
+  }
+  return PM_OK;
+}
+
+pm_status do_map(Group &G) {
+  pm_status s = ensure_decomposed(G);
+  if (s || G.P == 1) return s;  // one sub-domain: nothing leaves it (the wrap is local)
+  return message_round(G, PM_MSG_MIGRATE);
+}
+
+pm_status do_ghost_get(Group &G) {
+  pm_status s = ensure_decomposed(G);
+  if (s) return s;
+  if (G.P == 1) return pm_build_verlet(G.m[0].ctx);
+  if ((s = message_round(G, PM_MSG_GHOST))) return s;
+  for (auto &R : G.m)
+    if ((s = pm_dist_finish(R.ctx))) return s;
+  return PM_OK;
+}
+
+pm_status rebuild(Group &G) {
+  pm_status s = do_map(G);
+  if (!s) s = do_ghost_get(G);
+  if (!s) ++G.rebuilds;
+  return s;
+}
+
+// Velocity-Verlet steps of the whole group in lock step (Listing 4.1's loop,
+// PAPER.md:282-320, with the Verlet skin: map + ghost_get only when a
+// particle of any sub-domain moved more than skin/2; otherwise the
+// positions-only ghost refresh).
+pm_status do_run(Group &G, float dt, int64_t nsteps) {
+  pm_status s;
+  for (auto &R : G.m) std::memset(&R.stats, 0, sizeof R.stats);
+  if (G.P == 1) return pm_step_vv(G.m[0].ctx, dt, nsteps, &G.m[0].stats);
+  if (nsteps <= 0) return PM_OK;
+  bool need_forces = false;
+  for (auto &R : G.m) need_forces |= !pm::ctx_forces_valid(R.ctx) || !pm::ctx_list_valid(R.ctx);
+  if (need_forces) {
+    for (auto &R : G.m)
+      if (!pm::ctx_list_valid(R.ctx)) {
+        if ((s = rebuild(G))) return s;
+        break;
+      }
+    for (auto &R : G.m)
+      if ((s = pm_dist_step(R.ctx, dt, PM_PHASE_FORCES, nullptr))) return s;
+  }
+  const int64_t reb0 = G.rebuilds;
+  for (auto &R : G.m)
+    if ((s = pm_dist_step(R.ctx, dt, PM_PHASE_PROLOGUE, &R.flag))) return s;
+  int flag = 0;
+  if ((s = allreduce_flag(G, &flag))) return s;
+  for (int64_t k = 0; k < nsteps; ++k) {
+    if ((s = flag ? rebuild(G) : refresh(G))) return s;
+    const bool last = k == nsteps - 1;
+    for (auto &R : G.m)
+      if ((s = pm_dist_step(R.ctx, dt, last ? PM_PHASE_FINAL : PM_PHASE_STEP, nullptr))) return s;
+    if (last) break;
+    for (auto &R : G.m)
+      if ((s = pm_dist_read_flag(R.ctx, &R.flag))) return s;
+    if ((s = allreduce_flag(G, &flag))) return s;
+  }
+  for (auto &R : G.m) {
+    R.stats.steps = nsteps;
+    R.stats.rebuilds = G.rebuilds - reb0;
+  }
+  return PM_OK;
+}
+
+pm_status do_thermo(Group &G) {
+  for (auto &R : G.m) {
+    double ke, pe, pes, vir;
+    int64_t np;
+    pm_status s = pm_thermo_compute(R.ctx);
+    if (!s) s = pm_get_thermo(R.ctx, &ke, &pe, &pes, &vir, &np);
+    if (s) return s;
+    R.thermo[0] = ke;
+    R.thermo[1] = pe;
+    R.thermo[2] = pes;
+    R.thermo[3] = vir;
+    R.thermo[4] = (double)np;
+  }
+  double sum[5] = {0, 0, 0, 0, 0};
+  for (auto &R : G.m)
+    for (int k = 0; k < 5; ++k) sum[k] += R.thermo[k];
+  if (G.comm && G.nranks > 1) {
+    std::memcpy(G.h_red, sum, sizeof sum);
+    cudaMemcpyAsync(G.d_red, G.h_red, sizeof sum, cudaMemcpyHostToDevice, G.stream);
+    pm_status s = nccl_err(G.m[0].ctx,
+                           nccl().AllReduce(G.d_red, G.d_red, 5, ncclFloat64, ncclSum, G.comm,
+                                            G.stream),
+                           "thermo all-reduce");
+    if (s) return s;
+    cudaMemcpyAsync(G.h_red, G.d_red, sizeof sum, cudaMemcpyDeviceToHost, G.stream);
+    cudaError_t e = cudaStreamSynchronize(G.stream);
+    if (e != cudaSuccess) return cuda_err(G.m[0].ctx, e, "thermo all-reduce");
+    std::memcpy(sum, G.h_red, sizeof sum);
+  }
+  for (auto &R : G.m) std::memcpy(R.thermo, sum, sizeof sum);
+  return PM_OK;
+}
+
+// Collective entry: the last local member to enter performs `op`.
+pm_status enter(pm_ctx c, int op, Group **gout, int *idx, bool *perform) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_members.find(c);
+  if (it == g_members.end()) return pm::ctx_error(c, PM_E_STATE, "not a group member");
+  Group *G = it->second.first;
+  if (G->op != kOpNone && G->op != op)
+    return pm::ctx_error(c, PM_E_STATE, "group call order differs between members");
+  G->op = op;
+  G->entered += 1;
+  *gout = G;
+  *idx = it->second.second;
+  *perform = G->entered == (int)G->m.size();
+  if (*perform) {
+    G->op = kOpNone;
+    G->entered = 0;
+  }
+  return PM_OK;
+}
+
+Group *new_group(const int32_t grid[3], int nranks, int rank, int device, void *stream) {
+  Group *G = new Group();
+  for (int d = 0; d < 3; ++d) G->grid[d] = grid[d];
+  G->P = grid[0] * grid[1] * grid[2];
+  G->nranks = nranks;
+  G->rank = rank;
+  G->device = device;
+  cudaSetDevice(device);
+  if (stream) {
+    G->stream = (cudaStream_t)stream;
+  } else {
+    cudaStreamCreateWithFlags(&G->stream, cudaStreamNonBlocking);
+    G->own_stream = true;
+  }
+  cudaMalloc((void **)&G->d_flag, sizeof(int));
+  cudaMallocHost((void **)&G->h_flag, sizeof(int));
+  cudaMalloc((void **)&G->d_red, 8 * sizeof(double));
+  cudaMallocHost((void **)&G->h_red, 8 * sizeof(double));
+  return G;
+}
+
+void free_group(Group *G) {
+  cudaSetDevice(G->device);
+  if (G->stream) cudaStreamSynchronize(G->stream);
+  for (auto &R : G->m) {
+    if (R.sbuf) cudaFree(R.sbuf);
+    if (R.rbuf) cudaFree(R.rbuf);
+    if (R.d_cnt) cudaFree(R.d_cnt);
+    if (R.h_cnt) cudaFreeHost(R.h_cnt);
+  }
+  if (G->comm) nccl().CommDestroy(G->comm);
+  cudaFree(G->d_flag);
+  cudaFreeHost(G->h_flag);
+  cudaFree(G->d_red);
+  cudaFreeHost(G->h_red);
+  if (G->own_stream) cudaStreamDestroy(G->stream);
+  delete G;
+}
+
+pm_status add_member(Group *G, const pm_opts *opts, int sd, pm_ctx *out) {
+  pm_opts o;
+  pm_opts_default(&o);
+  if (opts) o = *opts;
+  o.cuda_stream = G->stream;  // every local member on the group stream
+  pm_ctx c = nullptr;
+  pm_status s = pm_create(&o, &c);
+  if (s) return s;
+  Member M;
+  M.ctx = c;
+  M.sd = sd;
+  setup_member_tables(*G, M);
+  if (cudaMalloc((void **)&M.d_cnt, sizeof(int64_t) * 52) != cudaSuccess ||
+      cudaMallocHost((void **)&M.h_cnt, sizeof(int64_t) * 52) != cudaSuccess) {
+    pm_destroy(c);
+    return PM_E_NOMEM;
+  }
+  std::memset(M.h_cnt, 0, sizeof(int64_t) * 52);
+  G->m.push_back(M);
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_members[c] = {G, (int)G->m.size() - 1};
+  }
+  *out = c;
+  return PM_OK;
+}
+
+pm_status check_grid(const int32_t grid[3]) {
+  if (!grid) return PM_E_INVAL;
+  for (int d = 0; d < 3; ++d)
+    if (grid[d] < 1 || grid[d] > 64) return PM_E_INVAL;
+  return PM_OK;
+}
+
+}  // namespace
+
+namespace pm {
+// pm_destroy of a member: the group (and its communicator) goes with its last
+// member.
+void group_detach(pm_ctx c) {
+  Group *G = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_members.find(c);
+    if (it == g_members.end()) return;
+    G = it->second.first;
+    g_members.erase(it);
+    for (auto &R : G->m)
+      if (R.ctx == c) R.ctx = nullptr;
+    for (auto &R : G->m)
+      if (R.ctx) return;
+  }
+  free_group(G);
+}
+}  // namespace pm
+
+extern "C" {
+
+pm_status pm_nccl_unique_id(uint8_t id[128]) {
+  if (!id) return PM_E_INVAL;
+  Nccl &N = nccl();
+  if (!N.ok) return PM_E_NCCL;
+  ncclUniqueId u;
+  if (N.GetUniqueId(&u) != ncclSuccess) return PM_E_NCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(id, &u, 128);
+  return PM_OK;
+}
+
+pm_status pm_create_dist(const pm_opts *opts, int32_t rank, int32_t nranks, const uint8_t id[128],
+                         const int32_t grid[3], pm_ctx *out) {
+  if (!out || !id || check_grid(grid)) return PM_E_INVAL;
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks || grid[0] * grid[1] * grid[2] != nranks)
+    return PM_E_INVAL;
+  Nccl &N = nccl();
+  if (!N.ok) return PM_E_NCCL;
+  pm_opts o;
+  pm_opts_default(&o);
+  if (opts) o = *opts;
+  Group *G = new_group(grid, nranks, rank, o.device, o.cuda_stream);
+  G->owner.resize(G->P);
+  for (int s = 0; s < G->P; ++s) G->owner[s] = s;
+  ncclUniqueId u;
+  std::memcpy(&u, id, 128);
+  cudaSetDevice(o.device);
+  if (N.CommInitRank(&G->comm, nranks, u, rank) != ncclSuccess) {
+    G->comm = nullptr;
+    free_group(G);
+    return PM_E_NCCL;
+  }
+  pm_status s = add_member(G, &o, rank, out);
+  if (s) free_group(G);
+  return s;
+}
+
+pm_status pm_create_dist_local(const pm_opts *opts, const int32_t grid[3], int32_t via_nccl,
+                               pm_ctx *out) {
+  if (!out || check_grid(grid)) return PM_E_INVAL;
+  pm_opts o;
+  pm_opts_default(&o);
+  if (opts) o = *opts;
+  Group *G = new_group(grid, 1, 0, o.device, o.cuda_stream);
+  G->owner.assign(G->P, 0);
+  if (via_nccl) {
+    Nccl &N = nccl();
+    ncclUniqueId u;
+    if (!N.ok || N.GetUniqueId(&u) != ncclSuccess ||
+        N.CommInitRank(&G->comm, 1, u, 0) != ncclSuccess) {
+      G->comm = nullptr;
+      free_group(G);
+      return PM_E_NCCL;
+    }
+    G->via_nccl = true;
+  }
+  for (int sd = 0; sd < G->P; ++sd) {
+    pm_status s = add_member(G, &o, sd, &out[sd]);
+    if (s) {
+      for (int k = 0; k < sd; ++k) pm_destroy(out[k]);  // the last one frees the group
+      if (sd == 0) free_group(G);
+      return s;
+    }
+  }
+  return PM_OK;
+}
+
+pm_status pm_dist_info(pm_ctx c, int32_t *sub_domain, int32_t *nsub, int32_t *rank,
+                       int32_t *nranks) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_members.find(c);
+  if (it == g_members.end()) return PM_E_STATE;
+  const Group *G = it->second.first;
+  if (sub_domain) *sub_domain = G->m[it->second.second].sd;
+  if (nsub) *nsub = G->P;
+  if (rank) *rank = G->rank;
+  if (nranks) *nranks = G->nranks;
+  return PM_OK;
+}
+
+pm_status pm_map(pm_ctx c) {
+  Group *G;
+  int idx;
+  bool go;
+  pm_status s = enter(c, kOpMap, &G, &idx, &go);
+  if (s || !go) return s;
+  cudaSetDevice(G->device);
+  return do_map(*G);
+}
+
+pm_status pm_ghost_get(pm_ctx c) {
+  Group *G;
+  int idx;
+  bool go;
+  pm_status s = enter(c, kOpGhost, &G, &idx, &go);
+  if (s || !go) return s;
+  cudaSetDevice(G->device);
+  return do_ghost_get(*G);
+}
+
+pm_status pm_dist_run(pm_ctx c, float dt, int64_t nsteps, pm_run_stats *out) {
+  Group *G;
+  int idx;
+  bool go;
+  if (!(dt > 0.f) || nsteps < 0) return PM_E_INVAL;
+  pm_status s = enter(c, kOpRun, &G, &idx, &go);
+  if (s) return s;
+  if (go) {
+    cudaSetDevice(G->device);
+    s = do_run(*G, dt, nsteps);
+  }
+  if (go && out) *out = G->m[idx].stats;
+  return s;
+}
+
+pm_status pm_dist_thermo(pm_ctx c, double *ke, double *pe_raw, double *pe_shift, double *virial,
+                         int64_t *npairs) {
+  Group *G;
+  int idx;
+  bool go;
+  pm_status s = enter(c, kOpThermo, &G, &idx, &go);
+  if (s || !go) return s;
+  cudaSetDevice(G->device);
+  if ((s = do_thermo(*G))) return s;
+  const double *t = G->m[idx].thermo;
+  if (ke) *ke = t[0];
+  if (pe_raw) *pe_raw = t[1];
+  if (pe_shift) *pe_shift = t[2];
+  if (virial) *virial = t[3];
+  if (npairs) *npairs = (int64_t)t[4];
+  return PM_OK;
+}
+
+}  // extern "C"

@@ -132,6 +132,14 @@ def lib(path: str = LIB_PATH):
         "pm_dist_sph_update": (st, [vp, C.c_float, C.c_float, C.c_int32, vp]),
         "pm_dist_refresh_pv_pack": (st, [vp, vp]),
         "pm_dist_refresh_pv_unpack": (st, [vp, vp]),
+        "pm_nccl_unique_id": (st, [vp]),
+        "pm_create_dist": (st, [C.POINTER(Opts), C.c_int32, C.c_int32, vp, vp, C.POINTER(vp)]),
+        "pm_create_dist_local": (st, [C.POINTER(Opts), vp, C.c_int32, vp]),
+        "pm_dist_info": (st, [vp, vp, vp, vp, vp]),
+        "pm_map": (st, [vp]),
+        "pm_ghost_get": (st, [vp]),
+        "pm_dist_run": (st, [vp, C.c_float, C.c_int64, C.POINTER(RunStats)]),
+        "pm_dist_thermo": (st, [vp, vp, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -163,7 +171,7 @@ class Context:
     """One pm_ctx (one GPU, one stream)."""
 
     def __init__(self, device: int = 0, nbr_cap: int = 0, use_graphs=None, stream=None,
-                 cell_div: int = 1):
+                 cell_div: int = 1, _handle=None):
         L = lib()
         o = Opts()
         L.pm_opts_default(C.byref(o))  # honours PM_USE_GRAPHS=0
@@ -173,11 +181,14 @@ class Context:
         if use_graphs is not None:
             o.use_graphs = 1 if use_graphs else 0
         o.cuda_stream = stream
+        self.L = L
+        self.n = 0
+        if _handle is not None:  # a group member created by pm_create_dist[_local]
+            self.h = _handle
+            return
         h = vp()
         self._check(L.pm_create(C.byref(o), C.byref(h)))
         self.h = h
-        self.L = L
-        self.n = 0
 
     def close(self):
         if getattr(self, "h", None):
@@ -523,6 +534,79 @@ class DistContext(Context):
         f = C.c_int32(0)
         self._check(self.L.pm_dist_read_flag(self.h, C.byref(f)))
         return int(f.value)
+
+
+# ---------------------------------------------------------------- groups (pm.h)
+def _opts(device=0, stream=None, nbr_cap=0):
+    o = Opts()
+    lib().pm_opts_default(C.byref(o))
+    o.device = device
+    o.nbr_cap = nbr_cap
+    o.cuda_stream = stream
+    return o
+
+
+def nccl_unique_id() -> bytes:
+    """pm_nccl_unique_id: 128 bytes for rank 0 to broadcast."""
+    buf = (C.c_char * 128)()
+    code = lib().pm_nccl_unique_id(buf)
+    if code != PM_OK:
+        raise PMError(code, "pm_nccl_unique_id")
+    return bytes(buf)
+
+
+class GroupMember(DistContext):
+    """A member of a multi-GPU group (pm_create_dist / pm_create_dist_local).
+    map / ghost_get / dist_run / dist_thermo are collective: call them on
+    every member (the last local member's call does the work)."""
+
+    def map(self):
+        self._check(self.L.pm_map(self.h))
+
+    def ghost_get(self):
+        self._check(self.L.pm_ghost_get(self.h))
+
+    def dist_run(self, dt, nsteps):
+        r = RunStats()
+        self._check(self.L.pm_dist_run(self.h, float(dt), int(nsteps), C.byref(r)))
+        return dict(steps=r.steps, rebuilds=r.rebuilds)
+
+    def dist_thermo(self):
+        v = [C.c_double(0.0) for _ in range(4)]
+        npair = C.c_int64(0)
+        self._check(self.L.pm_dist_thermo(self.h, *[C.byref(x) for x in v], C.byref(npair)))
+        return dict(ke=v[0].value, pe_raw=v[1].value, pe_shift=v[2].value, virial=v[3].value,
+                    npairs=int(npair.value))
+
+    def dist_info(self):
+        v = [C.c_int32(0) for _ in range(4)]
+        self._check(self.L.pm_dist_info(self.h, *[C.byref(x) for x in v]))
+        return dict(sub_domain=v[0].value, nsub=v[1].value, rank=v[2].value, nranks=v[3].value)
+
+
+def create_dist(rank, nranks, uid: bytes, grid, device=0, stream=None, nbr_cap=0):
+    """pm_create_dist: this process's member of an nranks-GPU group."""
+    o = _opts(device, stream, nbr_cap)
+    g = np.ascontiguousarray(grid, np.int32)
+    idb = (C.c_char * 128).from_buffer_copy(uid)
+    h = vp()
+    code = lib().pm_create_dist(C.byref(o), int(rank), int(nranks), idb, g.ctypes.data,
+                                C.byref(h))
+    if code != PM_OK:
+        raise PMError(code, "pm_create_dist")
+    return GroupMember(device=device, stream=stream, _handle=h)
+
+
+def create_dist_local(grid, device=0, stream=None, via_nccl=False, nbr_cap=0):
+    """pm_create_dist_local: all sub-domains of `grid` in this process."""
+    o = _opts(device, stream, nbr_cap)
+    g = np.ascontiguousarray(grid, np.int32)
+    P = int(np.prod(g))
+    hs = (vp * P)()
+    code = lib().pm_create_dist_local(C.byref(o), g.ctypes.data, 1 if via_nccl else 0, hs)
+    if code != PM_OK:
+        raise PMError(code, "pm_create_dist_local")
+    return [GroupMember(device=device, stream=stream, _handle=vp(hs[k])) for k in range(P)]
 
 
 def sorted_by_gid(state: dict) -> dict:
