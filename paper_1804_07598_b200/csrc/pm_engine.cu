@@ -689,6 +689,13 @@ bool ctx_ready(pm_ctx c) { return c->have_domain && c->have_cutoff; }
 pm_status ctx_error(pm_ctx c, pm_status code, const char *msg) {
   return set_err(c, code, "%s", msg);
 }
+// device address of the (need_rebuild, abort) pair of the state (adjacent ints)
+int *ctx_flag_ptr(pm_ctx c) { return &c->B.st->need_rebuild; }
+bool ctx_profiling(pm_ctx c) { return c->profiling; }
+void ctx_add_force_profile(pm_ctx c, double ms, int64_t launches) {
+  c->prof_force_ms += ms;
+  c->prof_force_launches += launches;
+}
 }  // namespace pm
 
 // ===========================================================================

@@ -56,6 +56,9 @@ bool ctx_forces_valid(pm_ctx c);
 bool ctx_list_valid(pm_ctx c);
 bool ctx_ready(pm_ctx c);
 pm_status ctx_error(pm_ctx c, pm_status code, const char *msg);
+int *ctx_flag_ptr(pm_ctx c);
+bool ctx_profiling(pm_ctx c);
+void ctx_add_force_profile(pm_ctx c, double ms, int64_t launches);
 void group_detach(pm_ctx c);
 }  // namespace pm
 
@@ -155,7 +158,8 @@ struct Group {
   float run_dt = 0.f;
   int64_t run_steps = 0;
   int *d_flag = nullptr;
-  int *h_flag = nullptr;
+  int *h_flag = nullptr;     // pinned: [0] flag, then (need_rebuild, abort) per member
+  std::vector<cudaEvent_t> ev;  // sweep timing (profiling)
   double *d_red = nullptr;
   double *h_red = nullptr;
   int64_t rebuilds = 0;
@@ -442,6 +446,41 @@ pm_status allreduce_flag(Group &G, int *flag) {
   return PM_OK;
 }
 
+// The per-step rebuild decision with ONE host synchronisation: the local
+// flags (State::need_rebuild) are MAX-reduced in place across ranks by NCCL,
+// then every member's (need_rebuild, abort) pair comes back in one copy each
+// and the flags are cleared on the device.
+pm_status step_flag(Group &G, int *flag) {
+  if (G.comm && G.nranks > 1) {  // one member per rank
+    pm_status s = nccl_err(G.m[0].ctx,
+                           nccl().AllReduce(pm::ctx_flag_ptr(G.m[0].ctx),
+                                            pm::ctx_flag_ptr(G.m[0].ctx), 1, ncclInt32, ncclMax,
+                                            G.comm, G.stream),
+                           "flag all-reduce");
+    if (s) return s;
+  }
+  for (size_t k = 0; k < G.m.size(); ++k) {
+    cudaError_t e = cudaMemcpyAsync(G.h_flag + 2 + 2 * k, pm::ctx_flag_ptr(G.m[k].ctx),
+                                    2 * sizeof(int), cudaMemcpyDeviceToHost, G.stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(pm::ctx_flag_ptr(G.m[k].ctx), 0, sizeof(int),
+                                              G.stream);
+    if (e != cudaSuccess) return cuda_err(G.m[k].ctx, e, "rebuild flag");
+  }
+  cudaError_t e = cudaStreamSynchronize(G.stream);
+  if (e != cudaSuccess) return cuda_err(G.m[0].ctx, e, "rebuild flag");
+  int f = 0;
+  for (size_t k = 0; k < G.m.size(); ++k) {
+    if (G.h_flag[3 + 2 * k]) {  // a device error: let the member report it
+      int dummy = 0;
+      pm_status s = pm_dist_read_flag(G.m[k].ctx, &dummy);
+      return s ? s : pm::ctx_error(G.m[k].ctx, PM_E_CUDA, "device error in a group step");
+    }
+    f = std::max(f, G.h_flag[2 + 2 * k]);
+  }
+  *flag = f;
+  return PM_OK;
+}
+
 pm_status ensure_decomposed(Group &G) {
   for (auto &R : G.m) {
     if (G.P > 1 && !pm::ctx_decomposed(R.ctx)) {
@@ -503,15 +542,33 @@ pm_status do_run(Group &G, float dt, int64_t nsteps) {
     if ((s = pm_dist_step(R.ctx, dt, PM_PHASE_PROLOGUE, &R.flag))) return s;
   int flag = 0;
   if ((s = allreduce_flag(G, &flag))) return s;
+  const bool prof = pm::ctx_profiling(G.m[0].ctx);
+  if (prof) {
+    while (G.ev.size() < 2 * (size_t)nsteps) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return PM_E_CUDA;
+      G.ev.push_back(e);
+    }
+  }
   for (int64_t k = 0; k < nsteps; ++k) {
     if ((s = flag ? rebuild(G) : refresh(G))) return s;
     const bool last = k == nsteps - 1;
+    if (prof) cudaEventRecord(G.ev[2 * k], G.stream);
     for (auto &R : G.m)
       if ((s = pm_dist_step(R.ctx, dt, last ? PM_PHASE_FINAL : PM_PHASE_STEP, nullptr))) return s;
+    if (prof) cudaEventRecord(G.ev[2 * k + 1], G.stream);
     if (last) break;
-    for (auto &R : G.m)
-      if ((s = pm_dist_read_flag(R.ctx, &R.flag))) return s;
-    if ((s = allreduce_flag(G, &flag))) return s;
+    if ((s = step_flag(G, &flag))) return s;
+  }
+  if (prof) {  // the force sweeps (+ fused kick/drift) of the local members, per step
+    cudaStreamSynchronize(G.stream);
+    double ms = 0.0;
+    for (int64_t k = 0; k < nsteps; ++k) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, G.ev[2 * k], G.ev[2 * k + 1]);
+      ms += t;
+    }
+    pm::ctx_add_force_profile(G.m[0].ctx, ms, nsteps);
   }
   for (auto &R : G.m) {
     R.stats.steps = nsteps;
@@ -588,7 +645,7 @@ Group *new_group(const int32_t grid[3], int nranks, int rank, int device, void *
     G->own_stream = true;
   }
   cudaMalloc((void **)&G->d_flag, sizeof(int));
-  cudaMallocHost((void **)&G->h_flag, sizeof(int));
+  cudaMallocHost((void **)&G->h_flag, sizeof(int) * (2 + 2 * G->P));
   cudaMalloc((void **)&G->d_red, 8 * sizeof(double));
   cudaMallocHost((void **)&G->h_red, 8 * sizeof(double));
   return G;
@@ -606,6 +663,7 @@ void free_group(Group *G) {
   if (G->comm) nccl().CommDestroy(G->comm);
   cudaFree(G->d_flag);
   cudaFreeHost(G->h_flag);
+  for (cudaEvent_t e : G->ev) cudaEventDestroy(e);
   cudaFree(G->d_red);
   cudaFreeHost(G->h_red);
   if (G->own_stream) cudaStreamDestroy(G->stream);

@@ -782,6 +782,146 @@ def _grid_for(n):
 
 
 def bench_main(args):
+    """bench.py --gpus N under torchrun.  Default: the native group path
+    (pm_create_dist / pm_map / pm_ghost_get / pm_dist_run behind the C-ABI,
+    library-owned NCCL communicator); PM_DIST_NATIVE=0: the Python DistSim
+    orchestration over torch.distributed (bench_distsim)."""
+    if os.environ.get("PM_DIST_NATIVE", "1") != "0":
+        return bench_native(args)
+    return bench_distsim(args)
+
+
+def bench_native(args):
+    """BJ configs[2] weak scaling through the C-ABI group API: one 128^3
+    lattice block (2,097,152 particles) per GPU; the unique id travels over a
+    gloo process group (bootstrap only: every data-path byte and the per-step
+    flag all-reduce go through the library's NCCL communicator).
+    PM_CFG3_BLOCK=m: m^3 particles per rank."""
+    import torch
+    import torch.distributed as tdist
+    from . import build as pmbuild, inputs, pm
+    pmbuild.build()
+    ws = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    m = int(os.environ.get("PM_CFG3_BLOCK", "128"))
+    dev = local % torch.cuda.device_count()
+    torch.cuda.set_device(dev)
+    tdist.init_process_group("gloo")
+    grid = _grid_for(ws)
+    D = Decomp(grid)
+    s = inputs.cfg3_block(*D.coord(rank), grid=grid, m=m)
+    stream = torch.cuda.Stream()
+
+    def max_f(x):
+        t = torch.tensor([float(x)], dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_i(x):
+        t = torch.tensor([int(x)], dtype=torch.int64)
+        tdist.all_reduce(t)
+        return int(t.item())
+
+    def member(place=True):
+        # a fresh unique id per communicator (an id bootstraps one init only)
+        uid = [pm.nccl_unique_id() if rank == 0 else None]
+        tdist.broadcast_object_list(uid, src=0)
+        c = pm.create_dist(rank, ws, uid[0], grid, device=dev, stream=stream.cuda_stream)
+        c.set_domain(s.lo, s.hi, s.periodic)
+        c.set_cutoff(2.5, 0.3)
+        c.set_lj(1.0, 1.0, 1.0, 0.0)
+        if place:
+            c.place(s.pos, s.vel, s.gid)
+        return c
+
+    # ---- device-resident run (value)
+    c = member()
+    c.map()
+    c.ghost_get()
+    c.dist_run(0.005, args.warmup)
+    torch.cuda.synchronize()
+    tdist.barrier()
+    clocks = None
+    if rank == 0:
+        from bench import ClockSampler  # noqa: E402
+        clocks = ClockSampler(dev)
+        clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    r = c.dist_run(0.005, args.steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    tdist.barrier()
+    clk = clocks.stop() if clocks else None
+    ms = max_f(e0.elapsed_time(e1))
+    cnt = c.count()
+    n = sum_i(cnt["n_owned"])
+    # dominant kernel (force sweep + fused VV): events around every step's
+    # sweep inside pm_dist_run (pm_set_profiling), max over ranks
+    c.set_profiling(True)
+    c.dist_run(0.005, min(args.steps, 50))
+    prof = c.get_profile()
+    c.set_profiling(False)
+    sweep_ms = max_f(prof["force_ms"] / max(prof["force_launches"], 1))
+    nbar = cnt["nnz"] / max(cnt["n_owned"], 1)
+    alg = cnt["n_owned"] * (4.0 * nbar + 64.0)
+    c.close()
+    # ---- end to end: pinned host state in, K steps, owned state out
+    pos_h = torch.from_numpy(s.pos).pin_memory()
+    vel_h = torch.from_numpy(s.vel).pin_memory()
+    gid_h = torch.from_numpy(s.gid).pin_memory()
+    c = member(place=False)
+    torch.cuda.synchronize()
+    tdist.barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    c.place(pos_h, vel_h, gid_h)
+    c.map()
+    c.ghost_get()
+    c.dist_run(0.005, args.steps)
+    out = c.owned_state()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    tdist.barrier()
+    e2e_ms = max_f(t0.elapsed_time(t1))
+    c.close()
+    if rank == 0:
+        from bench import METRIC, UNIT, hbm_peak  # noqa: E402
+        h2d = s.n * (16 + 16 + 8)
+        d2h = int(out["pos"].nbytes + out["vel"].nbytes)
+        peak, peak_src = hbm_peak()
+        ach = alg / (sweep_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "traffic": None,
+                "kernel": "k_lj_step (force sweep + fused VV), rank 0 sub-domain",
+                "kernel_ms": sweep_ms, "kernel_share_of_step": sweep_ms / (ms / args.steps),
+                "alg_bytes_per_launch": alg, "alg_bytes_formula": "N_owned*(4*nbar + 64)",
+                "peak_source": peak_src}
+        line = {"metric": METRIC, "value": n * args.steps / (ms * 1e-3), "unit": UNIT,
+                "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": f"cfg3 (BJ configs[2]): LJ fluid, {m**3:,} particles per "
+                                       f"GPU (SC {m}^3 block, rho=0.8), cuboid decomposition "
+                                       f"{grid}, ghost width r_cut+skin, NVE",
+                           "n_particles": n, "parallelism": f"spatial {grid} (NCCL, native "
+                                                            "pm_dist_run)",
+                           "rebuilds": r["rebuilds"], "l2": "inputs larger than L2 (Verlet lists)"},
+                "roofline": roof, "cpu_baseline": None,
+                "e2e": {"value": n * args.steps / (e2e_ms * 1e-3), "unit": UNIT,
+                        "h2d_bytes_per_step": h2d * ws / args.steps,
+                        "d2h_bytes_per_step": d2h * ws / args.steps},
+                # per step: refresh pack + unpack, sweep, pending flip (+ NCCL
+                # send/recv) = 4; per rebuild: 2 x (plan 4 + pack + unpack) +
+                # compact + flip + build 11 + remap = 26
+                "gpu_launches": 4 * args.steps + 26 * r["rebuilds"] + 3, "clocks": clk}
+        print(json.dumps(line), flush=True)
+    tdist.destroy_process_group()
+    return 0
+
+
+def bench_distsim(args):
     """bench.py --gpus N under torchrun: BJ configs[2] weak scaling, one
     128^3 lattice block (2,097,152 particles) per GPU, NCCL transport.
     PM_DIST_BACKEND=gloo (tests only): ranks may share a GPU, messages are

@@ -139,7 +139,10 @@ def test_bench_torchrun_two_ranks_share_one_gpu(env, tmp_path):
     sk.bind(("127.0.0.1", 0))
     port = sk.getsockname()[1]
     sk.close()
-    env_ = dict(os.environ, PM_DIST_BACKEND="gloo", PM_CFG3_BLOCK="32")
+    # two ranks on one GPU: NCCL refuses a duplicate device, so this runs the
+    # DistSim orchestration over gloo (the native NCCL group is covered by
+    # test_gpu_group.py and test_bench_native_single_rank)
+    env_ = dict(os.environ, PM_DIST_BACKEND="gloo", PM_CFG3_BLOCK="32", PM_DIST_NATIVE="0")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "12", "--warmup", "3"]

@@ -197,3 +197,37 @@ def test_group_call_order_errors(env):
     plain.close()
     for c in members:
         c.close()
+
+
+def test_bench_native_single_rank(env):
+    """bench.py's N > 1 code path (dist.bench_native: pm_create_dist through a
+    gloo-bootstrapped unique id, map, ghost_get, pm_dist_run with sweep
+    profiling, e2e) at world size 1 under torchrun: one JSON line with the
+    contract keys."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    code = ("import sys; sys.path.insert(0, %r); import argparse, bench; "
+            "from paper_1804_07598_b200 import dist; "
+            "sys.exit(dist.bench_native(argparse.Namespace(steps=12, warmup=3)))" % root)
+    script = os.path.join(root, "gpurun_out", "_bench_native_entry.py")
+    os.makedirs(os.path.dirname(script), exist_ok=True)
+    with open(script, "w") as f:
+        f.write(code + "\n")
+    env_ = dict(os.environ, PM_CFG3_BLOCK="32")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), script]
+    r = subprocess.run(cmd, capture_output=True, text=True, env=env_, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    b = json.loads(lines[0])
+    assert b["n_gpus"] == 1 and b["config"]["n_particles"] == 32 ** 3
+    assert b["value"] > 0 and b["e2e"]["value"] > 0 and b["roofline"]["frac"] > 0
