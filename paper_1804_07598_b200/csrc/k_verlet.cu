@@ -372,6 +372,98 @@ __device__ __forceinline__ void st_expand(unsigned msk, int jg, int cg, int self
   }
 }
 
+// R4 along one axis for two candidates at once (b = pair, a = the lane's
+// coordinate): e = b - a; e > L/2: (b - L) - a; e < -L/2: b - (a - L); else e
+// -- the single-rounded operations of pair_delta1, so bit-identical.  An axis
+// without the per-pair rule passes hL = +inf (always e).
+__device__ __forceinline__ u64 f2_r4(u64 B, float a, float L, float hL) {
+  const u64 A = f2_pack(a, a);
+  const u64 E = f2_sub(B, A);
+  const u64 U = f2_sub(f2_sub(B, f2_pack(L, L)), A);
+  const float am = __fsub_rn(a, L);
+  const u64 D = f2_sub(B, f2_pack(am, am));
+  float e0, e1, u0, u1, d0, d1;
+  f2_unpack(E, e0, e1);
+  f2_unpack(U, u0, u1);
+  f2_unpack(D, d0, d1);
+  const float r0 = e0 > hL ? u0 : (e0 < -hL ? d0 : e0);
+  const float r1 = e1 > hL ? u1 : (e1 < -hL ? d1 : e1);
+  return f2_pack(r0, r1);
+}
+
+// One group of up to 32 staged candidates (g .. g + gn, padded with +inf to
+// a multiple of 8), appended to the lane's 16-bit row by predicated stores.
+// PMI: the per-pair R4 rule on the axes in pmi (decomposed axes near the
+// global faces, runs covering a whole periodic row).
+template <bool PMI>
+__device__ __forceinline__ void st_fast_group(const float4 *__restrict__ SA,
+                                              const float2 *__restrict__ SZ, int g, int gn,
+                                              const float4 &xe, const Box &box, int pmi,
+                                              float rv2, int cb, unsigned short *rows, int lane,
+                                              int &k) {
+  const float INF = __int_as_float(0x7f800000);
+  const u64 XI = f2_pack(xe.x, xe.x), YI = f2_pack(xe.y, xe.y), ZI = f2_pack(xe.z, xe.z);
+  const float hx = (pmi & 1) ? box.halfL[0] : INF, hy = (pmi & 2) ? box.halfL[1] : INF,
+              hz = (pmi & 4) ? box.halfL[2] : INF;
+  const unsigned rows_sa = smem_u32(rows);
+  unsigned bo = rows_sa + (unsigned)(((k << 5) + lane) << 1);
+#pragma unroll
+  for (int u8 = 0; u8 < 4; ++u8) {
+    if (u8 >= ((gn + 7) >> 3)) break;
+    // 8 candidates: loads first, then the arithmetic, then the appends
+    float4 a[4];
+    float4 z[2];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) a[q] = SA[(g >> 1) + 4 * u8 + q];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) z[q] = reinterpret_cast<const float4 *>(SZ)[(g >> 2) + 2 * u8 + q];
+    float sd[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float zl = (q & 1) ? z[q >> 1].z : z[q >> 1].x;
+      const float zh = (q & 1) ? z[q >> 1].w : z[q >> 1].y;
+      u64 dx, dy, dz;
+      if (PMI) {
+        dx = f2_r4(f2_pack(a[q].x, a[q].y), xe.x, box.L[0], hx);
+        dy = f2_r4(f2_pack(a[q].z, a[q].w), xe.y, box.L[1], hy);
+        dz = f2_r4(f2_pack(zl, zh), xe.z, box.L[2], hz);
+      } else {
+        dx = f2_sub(f2_pack(a[q].x, a[q].y), XI);
+        dy = f2_sub(f2_pack(a[q].z, a[q].w), YI);
+        dz = f2_sub(f2_pack(zl, zh), ZI);
+      }
+      u64 s2 = f2_mul(dx, dx);
+      s2 = f2_fma(dy, dy, s2);
+      s2 = f2_fma(dz, dz, s2);
+      f2_unpack(s2, sd[2 * q], sd[2 * q + 1]);
+    }
+    const int c0 = cb + g + 8 * u8;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .u32 v;\n\t"
+        "st.shared.u16 [%0], %1;\n\t"
+        "setp.lt.f32 p, %2, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
+        "add.u32 v, %1, 1;\n\tst.shared.u16 [%0], v;\n\t"
+        "setp.lt.f32 p, %3, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
+        "add.u32 v, %1, 2;\n\tst.shared.u16 [%0], v;\n\t"
+        "setp.lt.f32 p, %4, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
+        "add.u32 v, %1, 3;\n\tst.shared.u16 [%0], v;\n\t"
+        "setp.lt.f32 p, %5, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
+        "add.u32 v, %1, 4;\n\tst.shared.u16 [%0], v;\n\t"
+        "setp.lt.f32 p, %6, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
+        "add.u32 v, %1, 5;\n\tst.shared.u16 [%0], v;\n\t"
+        "setp.lt.f32 p, %7, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
+        "add.u32 v, %1, 6;\n\tst.shared.u16 [%0], v;\n\t"
+        "setp.lt.f32 p, %8, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
+        "add.u32 v, %1, 7;\n\tst.shared.u16 [%0], v;\n\t"
+        "setp.lt.f32 p, %9, %10;\n\t@p add.u32 %0, %0, 64;\n\t}"
+        : "+r"(bo)
+        : "r"(c0), "f"(sd[0]), "f"(sd[1]), "f"(sd[2]), "f"(sd[3]), "f"(sd[4]), "f"(sd[5]),
+          "f"(sd[6]), "f"(sd[7]), "f"(rv2));
+  }
+  asm volatile("" ::: "memory");  // the C++ reads after this see the appends
+  k = (int)((bo - rows_sa) >> 6);
+}
+
 template <int RCH, int NMODE>
 __global__ void __launch_bounds__(stg::kWarps * 32, 5)
     k_verlet_st(Params P, Bufs B, int n, int wcap) {
@@ -550,62 +642,13 @@ __global__ void __launch_bounds__(stg::kWarps * 32, 5)
       const int cb = (p << kOffBits) + o;  // code of the stage's first candidate
       for (int g = 0; g < cntc; g += 32) {
         const int gn = min(32, cntc - g);
-        if (NMODE == 0 && !pmi && !R.direct && !__any_sync(0xffffffffu, k + gn > cap)) {
+        if (NMODE == 0 && !R.direct && !__any_sync(0xffffffffu, k + gn > cap)) {
           // fast path: every candidate's code is stored at the row's next
           // slot and the slot advances on a hit (no mask, no divergent
           // expansion); the +inf tail of the stage never hits
           const int k0 = k;
-          const unsigned rows_sa = smem_u32(rows);
-          unsigned bo = rows_sa + (unsigned)(((k << 5) + lane) << 1);
-#pragma unroll
-          for (int u8 = 0; u8 < 4; ++u8) {
-            if (u8 >= ((gn + 7) >> 3)) break;
-            // 8 candidates: loads first, then the arithmetic, then the appends
-            float4 a[4];
-            float4 z[2];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) a[q] = SA[(g >> 1) + 4 * u8 + q];
-#pragma unroll
-            for (int q = 0; q < 2; ++q)
-              z[q] = reinterpret_cast<const float4 *>(SZ)[(g >> 2) + 2 * u8 + q];
-            float sd[8];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const float zl = (q & 1) ? z[q >> 1].z : z[q >> 1].x;
-              const float zh = (q & 1) ? z[q >> 1].w : z[q >> 1].y;
-              const u64 dx = f2_sub(f2_pack(a[q].x, a[q].y), XI);
-              const u64 dy = f2_sub(f2_pack(a[q].z, a[q].w), YI);
-              const u64 dz = f2_sub(f2_pack(zl, zh), ZI);
-              u64 s2 = f2_mul(dx, dx);
-              s2 = f2_fma(dy, dy, s2);
-              s2 = f2_fma(dz, dz, s2);
-              f2_unpack(s2, sd[2 * q], sd[2 * q + 1]);
-            }
-            const int c0 = cb + g + 8 * u8;
-            asm volatile(
-                "{\n\t.reg .pred p;\n\t.reg .u32 v;\n\t"
-                "st.shared.u16 [%0], %1;\n\t"
-                "setp.lt.f32 p, %2, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
-                "add.u32 v, %1, 1;\n\tst.shared.u16 [%0], v;\n\t"
-                "setp.lt.f32 p, %3, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
-                "add.u32 v, %1, 2;\n\tst.shared.u16 [%0], v;\n\t"
-                "setp.lt.f32 p, %4, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
-                "add.u32 v, %1, 3;\n\tst.shared.u16 [%0], v;\n\t"
-                "setp.lt.f32 p, %5, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
-                "add.u32 v, %1, 4;\n\tst.shared.u16 [%0], v;\n\t"
-                "setp.lt.f32 p, %6, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
-                "add.u32 v, %1, 5;\n\tst.shared.u16 [%0], v;\n\t"
-                "setp.lt.f32 p, %7, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
-                "add.u32 v, %1, 6;\n\tst.shared.u16 [%0], v;\n\t"
-                "setp.lt.f32 p, %8, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
-                "add.u32 v, %1, 7;\n\tst.shared.u16 [%0], v;\n\t"
-                "setp.lt.f32 p, %9, %10;\n\t@p add.u32 %0, %0, 64;\n\t}"
-                : "+r"(bo)
-                : "r"(c0), "f"(sd[0]), "f"(sd[1]), "f"(sd[2]), "f"(sd[3]), "f"(sd[4]),
-                  "f"(sd[5]), "f"(sd[6]), "f"(sd[7]), "f"(rv2));
-          }
-          asm volatile("" ::: "memory");  // the C++ reads below see the appends
-          k = (int)((bo - rows_sa) >> 6);
+          if (pmi) st_fast_group<true>(SA, SZ, g, gn, xe, P.box, pmi, rv2, cb, rows, lane, k);
+          else st_fast_group<false>(SA, SZ, g, gn, xe, P.box, 0, rv2, cb, rows, lane, k);
           // the particle itself (d2 = 0) was appended once: swap-remove it
           const int jg = jb + g;
           if (i >= jg && i < jg + gn) {

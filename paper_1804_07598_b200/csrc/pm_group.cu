@@ -38,6 +38,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -500,18 +501,31 @@ pm_status do_map(Group &G) {
   return message_round(G, PM_MSG_MIGRATE);
 }
 
+double g_t_map = 0, g_t_ghost = 0, g_t_finish = 0;  // PM_GROUP_TIMING
+
 pm_status do_ghost_get(Group &G) {
   pm_status s = ensure_decomposed(G);
   if (s) return s;
   if (G.P == 1) return pm_build_verlet(G.m[0].ctx);
+  static const bool timing = std::getenv("PM_GROUP_TIMING") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
   if ((s = message_round(G, PM_MSG_GHOST))) return s;
+  if (timing) cudaStreamSynchronize(G.stream);
+  auto t1 = std::chrono::steady_clock::now();
   for (auto &R : G.m)
     if ((s = pm_dist_finish(R.ctx))) return s;
+  auto t2 = std::chrono::steady_clock::now();
+  g_t_ghost += std::chrono::duration<double, std::milli>(t1 - t0).count();
+  g_t_finish += std::chrono::duration<double, std::milli>(t2 - t1).count();
   return PM_OK;
 }
 
 pm_status rebuild(Group &G) {
+  auto t0 = std::chrono::steady_clock::now();
   pm_status s = do_map(G);
+  if (std::getenv("PM_GROUP_TIMING")) cudaStreamSynchronize(G.stream);
+  g_t_map += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                 .count();
   if (!s) s = do_ghost_get(G);
   if (!s) ++G.rebuilds;
   return s;
@@ -550,16 +564,33 @@ pm_status do_run(Group &G, float dt, int64_t nsteps) {
       G.ev.push_back(e);
     }
   }
+  static const bool timing = std::getenv("PM_GROUP_TIMING") != nullptr;
+  using clk = std::chrono::steady_clock;
+  double t_reb = 0, t_ref = 0, t_step = 0, t_flag = 0;
   for (int64_t k = 0; k < nsteps; ++k) {
+    auto t0 = clk::now();
+    if (timing) cudaStreamSynchronize(G.stream);
     if ((s = flag ? rebuild(G) : refresh(G))) return s;
+    if (timing) cudaStreamSynchronize(G.stream);
+    auto t1 = clk::now();
+    (flag ? t_reb : t_ref) += std::chrono::duration<double, std::milli>(t1 - t0).count();
     const bool last = k == nsteps - 1;
     if (prof) cudaEventRecord(G.ev[2 * k], G.stream);
     for (auto &R : G.m)
       if ((s = pm_dist_step(R.ctx, dt, last ? PM_PHASE_FINAL : PM_PHASE_STEP, nullptr))) return s;
     if (prof) cudaEventRecord(G.ev[2 * k + 1], G.stream);
+    if (timing) cudaStreamSynchronize(G.stream);
+    auto t2 = clk::now();
+    t_step += std::chrono::duration<double, std::milli>(t2 - t1).count();
     if (last) break;
     if ((s = step_flag(G, &flag))) return s;
+    t_flag += std::chrono::duration<double, std::milli>(clk::now() - t2).count();
   }
+  if (timing)
+    std::fprintf(stderr, "pm_dist_run %lld steps: rebuild %.3f ms, refresh %.3f ms, step %.3f ms, "
+                 "flag %.3f ms (synchronised phases); rebuilds so far: map %.3f, ghost round "
+                 "%.3f, finish %.3f ms\n", (long long)nsteps, t_reb, t_ref, t_step, t_flag,
+                 g_t_map, g_t_ghost, g_t_finish);
   if (prof) {  // the force sweeps (+ fused kick/drift) of the local members, per step
     cudaStreamSynchronize(G.stream);
     double ms = 0.0;
