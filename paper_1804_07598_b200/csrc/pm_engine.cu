@@ -86,6 +86,8 @@ struct pm_ctx_s {
   int *d_blk = nullptr, *d_order = nullptr, *d_dirbase = nullptr, *d_list = nullptr;
   int *d_send_idx = nullptr, *d_gslot = nullptr;
   long long *d_tot = nullptr, *h_tot = nullptr;
+  int *h_order = nullptr;  // pinned copy of the plan's direction order
+  int plan_pending = -1;   // dist_plan_async issued, dist_plan_complete due
   int64_t mask_cap = 0, blk_cap = 0, list_cap = 0, send_cap = 0, gslot_cap = 0;
   int plan_what = -1;
   // decomposed DEM: the stay list of the last migration (pre-migration
@@ -790,6 +792,7 @@ void pm_destroy(pm_ctx c) {
   for (void *p : dptrs)
     if (p) cudaFree(p);
   if (c->h_tot) cudaFreeHost(c->h_tot);
+  if (c->h_order) cudaFreeHost(c->h_order);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->st_h) cudaFreeHost(c->st_h);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
@@ -1693,7 +1696,13 @@ pm_status pm_set_decomposition_cuts(pm_ctx c, const int32_t pgrid[3], const int3
   return setup_grid(c);
 }
 
-pm_status pm_dist_plan(pm_ctx c, int32_t what, const int32_t order[26], int64_t counts[27]) {
+extern "C++" {
+namespace pm {
+// pm_dist_plan without its synchronisation: the plan kernels, then the counts
+// and the state copied to the host asynchronously; dist_plan_complete (after
+// the caller synchronised the stream) checks and books them.  A group
+// synchronises once for all its members.
+pm_status dist_plan_async(pm_ctx c, int32_t what, const int32_t order[26]) {
   pm_status s = check_ready(c);
   if (s) return s;
   if (!c->dist) return set_err(c, PM_E_STATE, "pm_dist_plan: no decomposition");
@@ -1713,6 +1722,7 @@ pm_status pm_dist_plan(pm_ctx c, int32_t what, const int32_t order[26], int64_t 
     CUDA_TRY(c, cudaMalloc((void **)&c->d_dirbase, 27 * sizeof(int)));
     CUDA_TRY(c, cudaMalloc((void **)&c->d_tot, 27 * sizeof(long long)));
     CUDA_TRY(c, cudaMallocHost((void **)&c->h_tot, 27 * sizeof(long long)));
+    CUDA_TRY(c, cudaMallocHost((void **)&c->h_order, 26 * sizeof(int)));
   }
   uint32_t seen = 0;  // order must be a permutation of the 26 directions != 13
   for (int k = 0; k < 26; ++k) {
@@ -1720,14 +1730,26 @@ pm_status pm_dist_plan(pm_ctx c, int32_t what, const int32_t order[26], int64_t 
       return set_err(c, PM_E_INVAL,
                      "pm_dist_plan: order must list each of the 26 directions != 13 once");
     seen |= 1u << order[k];
+    c->h_order[k] = order[k];
   }
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_order, order, 26 * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_order, c->h_order, 26 * sizeof(int), cudaMemcpyHostToDevice,
+                              c->stream));
   launch_dist_plan(c->P, c->B, c->D, (int)no, what, c->d_mask, c->d_blk, c->d_order, c->d_dirbase,
                    c->d_tot, c->d_list, c->stream);
   CUDA_TRY(c, cudaMemcpyAsync(c->h_tot, c->d_tot, 27 * sizeof(long long), cudaMemcpyDeviceToHost,
                               c->stream));
-  s = sync_check(c, "pm_dist_plan");
-  if (s) return s;
+  CUDA_TRY(c, cudaMemcpyAsync(c->st_h, c->B.st, sizeof(State), cudaMemcpyDeviceToHost, c->stream));
+  c->plan_pending = what;
+  return check_launch(c, "pm_dist_plan");
+}
+
+pm_status dist_plan_complete(pm_ctx c, int64_t counts[27]) {
+  if (c->plan_pending < 0) return set_err(c, PM_E_STATE, "pm_dist_plan: nothing planned");
+  const int what = c->plan_pending;
+  c->plan_pending = -1;
+  if (c->st_h->abort)
+    return set_err(c, c->st_h->abort, "pm_dist_plan: %s (gid %lld)",
+                   device_error_name(c->st_h->abort), (long long)c->st_h->err_gid);
   int64_t send = 0;
   for (int d = 0; d < 27; ++d) {
     if (counts) counts[d] = c->h_tot[d];
@@ -1742,12 +1764,64 @@ pm_status pm_dist_plan(pm_ctx c, int32_t what, const int32_t order[26], int64_t 
     c->n_arr = 0;
     c->dem_saved = c->list_valid;
     if (c->dem_saved) {
+      pm_status s;
       if ((s = dem_alloc(c, true))) return s;
       if ((s = ensure_dev(c, &c->B.gid_old, c->gid_old_cap, c->n + 1))) return s;
       launch_dem_save(c->B, c->n, c->stream);
     }
   }
   return PM_OK;
+}
+
+// pm_dist_finish in two halves around one group synchronisation: the cell
+// sort and Verlet build enqueued with the state copy; then the capacity check
+// (a rare overflow re-lays the slices out and rebuilds synchronously) and the
+// refresh remap, left asynchronous (errors surface at the next step's flag).
+pm_status dist_finish_async(pm_ctx c) {
+  pm_status s = check_ready(c);
+  if (s) return s;
+  if (!c->dist) return set_err(c, PM_E_STATE, "pm_dist_finish: no decomposition");
+  cudaSetDevice(c->device);
+  if ((s = ensure_layout(c))) return s;
+  enqueue_rebuild(c, c->stream, 0);
+  CUDA_TRY(c, cudaMemcpyAsync(c->st_h, c->B.st, sizeof(State), cudaMemcpyDeviceToHost, c->stream));
+  return check_launch(c, "pm_dist_finish");
+}
+
+pm_status dist_finish_complete(pm_ctx c) {
+  pm_status s = PM_OK;
+  if (c->st_h->abort == PM_E_CAPACITY) {
+    k_clear_abort<<<1, 1, 0, c->stream>>>(c->B.st);
+    if ((s = layout_from_counts(c))) return s;
+    launch_verlet(c->P, c->B, c->n, c->stream);
+    if ((s = sync_check(c, "pm_dist_finish (retry)"))) return s;
+  } else if (c->st_h->abort) {
+    return set_err(c, c->st_h->abort, "pm_dist_finish: %s (gid %lld)",
+                   device_error_name(c->st_h->abort), (long long)c->st_h->err_gid);
+  }
+  c->cells_valid = c->list_valid = true;
+  c->forces_valid = c->rho_valid = false;
+  if ((s = ensure_dev(c, &c->d_gslot, c->gslot_cap, c->n_ghost + 1))) return s;
+  launch_dist_remap(c->B.invperm, c->d_send_idx, (int)c->n_send, c->d_gslot, (int)c->n_ghost,
+                    (int)c->n_owned, c->stream);
+  c->P.peer_n = 0;  // new send lists and ghost slots: pm_dist_peer_setup again
+  if (c->P.dem_state) {  // contact histories onto the new rows (stayers and arrivals)
+    if ((s = dem_alloc(c, false))) return s;
+    launch_dem_remap_dist(c->B, c->n, c->d_stay_old, (int)c->n_stay_old, c->d_hist_in,
+                          (int)c->n_arr, c->stream);
+    c->n_stay_old = 0;
+    c->n_arr = 0;
+  }
+  return check_launch(c, "pm_dist_finish");
+}
+}  // namespace pm
+}  // extern "C++"
+
+pm_status pm_dist_plan(pm_ctx c, int32_t what, const int32_t order[26], int64_t counts[27]) {
+  pm_status s = pm::dist_plan_async(c, what, order);
+  if (s) return s;
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return pm::dist_plan_complete(c, counts);
 }
 
 pm_status pm_dist_pack(pm_ctx c, int32_t what, void *send_dev) {
@@ -1840,23 +1914,10 @@ pm_status pm_dist_unpack(pm_ctx c, int32_t what, const void *recv_dev, int64_t n
 }
 
 pm_status pm_dist_finish(pm_ctx c) {
-  pm_status s = check_ready(c);
+  pm_status s = pm::dist_finish_async(c);
   if (s) return s;
-  if (!c->dist) return set_err(c, PM_E_STATE, "pm_dist_finish: no decomposition");
-  cudaSetDevice(c->device);
-  s = build_list(c);  // cells over owned + ghosts, Verlet rows for owned
-  if (s) return s;
-  if ((s = ensure_dev(c, &c->d_gslot, c->gslot_cap, c->n_ghost + 1))) return s;
-  launch_dist_remap(c->B.invperm, c->d_send_idx, (int)c->n_send, c->d_gslot, (int)c->n_ghost,
-                    (int)c->n_owned, c->stream);
-  c->P.peer_n = 0;  // new send lists and ghost slots: pm_dist_peer_setup again
-  if (c->P.dem_state) {  // contact histories onto the new rows (stayers and arrivals)
-    if ((s = dem_alloc(c, false))) return s;
-    launch_dem_remap_dist(c->B, c->n, c->d_stay_old, (int)c->n_stay_old, c->d_hist_in,
-                          (int)c->n_arr, c->stream);
-    c->n_stay_old = 0;
-    c->n_arr = 0;
-  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if ((s = pm::dist_finish_complete(c))) return s;
   return sync_check(c, "pm_dist_finish");
 }
 

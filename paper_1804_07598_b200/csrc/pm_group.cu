@@ -60,6 +60,10 @@ pm_status ctx_error(pm_ctx c, pm_status code, const char *msg);
 int *ctx_flag_ptr(pm_ctx c);
 bool ctx_profiling(pm_ctx c);
 void ctx_add_force_profile(pm_ctx c, double ms, int64_t launches);
+pm_status dist_plan_async(pm_ctx c, int32_t what, const int32_t order[26]);
+pm_status dist_plan_complete(pm_ctx c, int64_t counts[27]);
+pm_status dist_finish_async(pm_ctx c);
+pm_status dist_finish_complete(pm_ctx c);
 void group_detach(pm_ctx c);
 }  // namespace pm
 
@@ -361,10 +365,16 @@ pm_status exchange_payload(Group &G, size_t rec) {
 pm_status message_round(Group &G, int what) {
   const size_t rec = (size_t)pm_record_bytes(what);
   std::vector<std::vector<int64_t>> send_n(G.m.size());
+  for (auto &R : G.m) {  // every member's plan, then one synchronisation
+    pm_status s = pm::dist_plan_async(R.ctx, what, R.order.data());
+    if (s) return s;
+  }
+  cudaError_t e = cudaStreamSynchronize(G.stream);
+  if (e != cudaSuccess) return cuda_err(G.m[0].ctx, e, "plan");
   for (size_t r = 0; r < G.m.size(); ++r) {
     Member &R = G.m[r];
     int64_t counts[27];
-    pm_status s = pm_dist_plan(R.ctx, what, R.order.data(), counts);
+    pm_status s = pm::dist_plan_complete(R.ctx, counts);
     if (s) return s;
     int64_t off = 0;
     for (size_t k = 0; k < R.peers.size(); ++k) {
@@ -512,8 +522,12 @@ pm_status do_ghost_get(Group &G) {
   if ((s = message_round(G, PM_MSG_GHOST))) return s;
   if (timing) cudaStreamSynchronize(G.stream);
   auto t1 = std::chrono::steady_clock::now();
+  for (auto &R : G.m)  // cell lists + Verlet rows of every member, one synchronisation
+    if ((s = pm::dist_finish_async(R.ctx))) return s;
+  cudaError_t e = cudaStreamSynchronize(G.stream);
+  if (e != cudaSuccess) return cuda_err(G.m[0].ctx, e, "finish");
   for (auto &R : G.m)
-    if ((s = pm_dist_finish(R.ctx))) return s;
+    if ((s = pm::dist_finish_complete(R.ctx))) return s;
   auto t2 = std::chrono::steady_clock::now();
   g_t_ghost += std::chrono::duration<double, std::milli>(t1 - t0).count();
   g_t_finish += std::chrono::duration<double, std::milli>(t2 - t1).count();
