@@ -13,6 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpm.so")
+LIB_CHECKS = os.path.join(HERE, "libpm_checks.so")  # -DPM_CHECKS: device bounds checks
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -32,25 +33,28 @@ def deps():
         os.path.join(ROOT, "include", "pm.h")]
 
 
-def stale() -> bool:
-    if not os.path.exists(LIB):
+def stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return any(os.path.getmtime(p) > t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile every csrc/*.cu to an object in parallel, then link libpm.so."""
-    if not force and not stale():
-        return LIB
+def build(force: bool = False, verbose: bool = False, checks: bool = False) -> str:
+    """Compile every csrc/*.cu to an object in parallel, then link libpm.so
+    (checks=True: libpm_checks.so with the device bounds checks PM_CHECK;
+    load it with PM_LIB=<path>)."""
+    target = LIB_CHECKS if checks else LIB
+    if not force and not stale(target):
+        return target
     from concurrent.futures import ThreadPoolExecutor
     nvcc = os.environ.get("NVCC", "nvcc")
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
-    flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    flags = [f for f in NVCC_FLAGS if f != "-shared"] + (["-DPM_CHECKS"] if checks else [])
 
     def compile_one(src):
-        obj = os.path.join(objdir, os.path.basename(src) + f".{os.getpid()}.o")
+        obj = os.path.join(objdir, os.path.basename(src) + f".{os.getpid()}{'.chk' if checks else ''}.o")
         cmd = [nvcc, *flags, "-I", os.path.join(ROOT, "include"), "-c", "-o", obj, src]
         res = subprocess.run(cmd, capture_output=True, text=True)
         return src, obj, res
@@ -62,7 +66,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n" + res.stdout + res.stderr)
         log.append(res.stderr)
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = target + f".tmp{os.getpid()}"
     objs = [obj for _, obj, _ in results]
     res = subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o",
                           tmp, *objs, "-ldl"], capture_output=True, text=True)
@@ -72,10 +76,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc link failed:\n" + res.stdout + res.stderr)
     if verbose:
         print("".join(log))
-    os.replace(tmp, LIB)
-    with open(os.path.join(HERE, "libpm.ptxas.txt"), "w") as f:
-        f.write("".join(log))
-    return LIB
+    os.replace(tmp, target)
+    if not checks:
+        with open(os.path.join(HERE, "libpm.ptxas.txt"), "w") as f:
+            f.write("".join(log))
+    return target
 
 
 if __name__ == "__main__":

@@ -209,6 +209,7 @@ __global__ void k_dist_pack(Bufs B, int what, const int *__restrict__ list, int 
   if (e >= nsend) return;
   State *st = B.st;
   const int i = list[e];
+  PM_CHECK(i >= 0);
   const int cp = st->cur_pv, ci = st->cur_id;
   if (what == 0) {
     MigRec r;
@@ -276,7 +277,10 @@ __global__ void k_dist_unpack(Bufs B, int what, const void *__restrict__ in, int
 __global__ void k_dist_remap(const int *__restrict__ invperm, int *__restrict__ send_idx,
                              int nsend, int *__restrict__ ghost_slot, int nghost, int n_owned) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e < nsend) send_idx[e] = invperm[send_idx[e]];
+  if (e < nsend) {
+    PM_CHECK(send_idx[e] >= 0 && send_idx[e] < n_owned);
+    send_idx[e] = invperm[send_idx[e]];
+  }
   if (e < nghost) ghost_slot[e] = invperm[n_owned + e];
 }
 
@@ -289,7 +293,10 @@ __global__ void k_refresh_pack(Bufs B, const int *__restrict__ send_idx, int nse
 __global__ void k_refresh_unpack(Bufs B, const int *__restrict__ ghost_slot, int nghost,
                                  const float4 *__restrict__ in) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e < nghost) B.pos[B.st->cur_pv][ghost_slot[e]] = in[e];
+  if (e < nghost) {
+    PM_CHECK(ghost_slot[e] >= 0);
+    B.pos[B.st->cur_pv][ghost_slot[e]] = in[e];
+  }
 }
 
 // SPH runs (NEXT-3): positions and velocities, with P and rho in their w

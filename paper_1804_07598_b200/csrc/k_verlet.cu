@@ -366,6 +366,7 @@ __device__ __forceinline__ void st_expand(unsigned msk, int jg, int cg, int self
       if ((gr.kind[j] & kGhostBit) ? (gr.gid[j] < gr.gid_self) : (j < self)) continue;
     }
     const int kk = min(k, cap - 1);
+    PM_CHECK(j >= 0 && kk >= 0);
     if (R.direct) R.gl[(int64_t)kk << 5] = j;
     else R.sm[(kk << 5) + lane] = (unsigned short)(cg + u);
     ++k;
@@ -462,6 +463,7 @@ __device__ __forceinline__ void st_fast_group(const float4 *__restrict__ SA,
   }
   asm volatile("" ::: "memory");  // the C++ reads after this see the appends
   k = (int)((bo - rows_sa) >> 6);
+  PM_CHECK(((bo - rows_sa) & 63u) == (unsigned)(lane << 1));
 }
 
 template <int RCH, int NMODE>
@@ -642,7 +644,8 @@ __global__ void __launch_bounds__(stg::kWarps * 32, 5)
       const int cb = (p << kOffBits) + o;  // code of the stage's first candidate
       for (int g = 0; g < cntc; g += 32) {
         const int gn = min(32, cntc - g);
-        if (NMODE == 0 && !R.direct && !__any_sync(0xffffffffu, k + gn > cap)) {
+        // (every store of the group, the +inf padding included, stays below cap)
+        if (NMODE == 0 && !R.direct && !__any_sync(0xffffffffu, k + ((gn + 7) & ~7) > cap)) {
           // fast path: every candidate's code is stored at the row's next
           // slot and the slot advances on a hit (no mask, no divergent
           // expansion); the +inf tail of the stage never hits
@@ -706,7 +709,10 @@ __global__ void __launch_bounds__(stg::kWarps * 32, 5)
       for (int kk = 0; kk < kseg; ++kk) {
         if (mine && kk < k) {
           const unsigned c = rows[(kk << 5) + lane];
-          grow[(int64_t)kk << 5] = PBE[c >> kOffBits].x + (int)(c & (kMaxPieceLen - 1));
+          PM_CHECK((int)(c >> kOffBits) < NP);
+          const int j = PBE[c >> kOffBits].x + (int)(c & (kMaxPieceLen - 1));
+          PM_CHECK(j >= 0 && j < n && j != i && j < PBE[c >> kOffBits].y);
+          grow[(int64_t)kk << 5] = j;
         }
       }
     }

@@ -13,6 +13,25 @@
 #define PM_DEV __device__ __forceinline__
 #endif
 
+// Device-side bounds checks of the debug build (build.build(checks=True) ->
+// libpm_checks.so, -DPM_CHECKS): a failed check prints its location and traps
+// the kernel (the call then reports PM_E_CUDA).  compute-sanitizer is not
+// available on the GPU pool (profiles/r02_compute_sanitizer_refused.txt).
+#ifdef PM_CHECKS
+#include <cstdio>
+#define PM_CHECK(cond)                                                          \
+  do {                                                                          \
+    if (!(cond)) {                                                              \
+      printf("PM_CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond);        \
+      __trap();                                                                 \
+    }                                                                           \
+  } while (0)
+#else
+#define PM_CHECK(cond) \
+  do {                 \
+  } while (0)
+#endif
+
 namespace pm {
 
 constexpr int kWarp = 32;

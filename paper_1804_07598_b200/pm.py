@@ -61,11 +61,14 @@ _lib = None
 vp = C.c_void_p
 
 
-def lib(path: str = LIB_PATH):
-    """Load libpm.so (raises if it is missing -- the product has no fallback)."""
+def lib(path: str = None):
+    """Load libpm.so (raises if it is missing -- the product has no fallback).
+    PM_LIB=<path> loads another build of the same library (the bounds-checked
+    libpm_checks.so of build.build(checks=True))."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("PM_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise RuntimeError(f"libpm.so not found at {path}; run __graft_entry__.build()")
     L = C.CDLL(path)
