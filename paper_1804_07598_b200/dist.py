@@ -320,6 +320,8 @@ class DistSim:
         if newton:
             for ctx in members.values():
                 ctx.set_newton(True)
+        self.sar = None       # SAR trigger: runtime re-balancing (enable_rebalance)
+        self.rebalances = 0
         self.ghost_seg = {}   # rank -> {peer: (off, n)} of the last ghost plan (send side)
         self.ghost_recv = {}  # rank -> {peer: n} received ghosts
         self.rebuilds = 0
@@ -346,6 +348,55 @@ class DistSim:
             return self.tr.exchange_counts_all(counts)
         (r,) = list(self.m)
         return {r: self.tr.exchange_counts(counts[r])}
+
+    # ---- runtime re-balancing (§3.5)
+    def enable_rebalance(self, cost_ms=1.0, bins=4096):
+        """Stop-At-Rise re-balancing inside run(): every step records the
+        per-rank step times (CUDA events around each rank's sweep); when SAR
+        fires, the cuts are recomputed from all-reduced pair-work histograms
+        (histogram_cuts), every member gets them (pm_set_decomposition_cuts)
+        and the next step migrates (map) and rebuilds the ghosts.  cost_ms:
+        the first estimate of a re-balance (then the measured one)."""
+        self.sar = SAR(cost_ms)
+        self._bins = bins
+
+    def _allsum(self, arr):
+        arr = np.asarray(arr, np.float64)
+        if self.loop:
+            return arr
+        return self.tr.allreduce_sum(arr)
+
+    def _rank_times(self, local):
+        """{rank: ms} of the local members -> the vector over all ranks."""
+        v = np.zeros(self.D.size)
+        for r, t in local.items():
+            v[r] = t
+        return self._allsum(v)
+
+    def rebalance(self):
+        """New load-balanced cuts from the current particles (no gather: each
+        member contributes a histogram of its owned coordinates weighted by
+        its Verlet row lengths), applied to every member; the caller rebuilds
+        (map + ghost_get).  Returns the new Decomp."""
+        from . import pm
+        pos, w = [], []
+        for ctx in self.m.values():
+            st = ctx.get_state()
+            rp, _ = ctx.get_verlet(cols=False)
+            own = (ctx.get_kind() & pm.GHOST_BIT) == 0
+            pos.append(st["pos"][own, :3])
+            w.append(np.diff(rp)[own] + 1.0)  # pair work (+1: the particle itself)
+        ctx0 = next(iter(self.m.values()))
+        lo, hi = ctx0._box
+        rv = ctx0._rv
+        cuts = histogram_cuts(self.D.grid, np.concatenate(pos), np.concatenate(w), lo, hi, rv,
+                              self._allsum, self._bins)
+        D = Decomp(self.D.grid, cuts)
+        for r, ctx in self.m.items():
+            ctx.set_decomposition_cuts(D.grid, D.coord(r), cuts)
+        self.D = D
+        self.rebalances += 1
+        return D
 
     def _allreduce_max(self, vals):
         v = max(vals.values())
@@ -573,14 +624,34 @@ class DistSim:
                 e0 = self.torch.cuda.Event(enable_timing=True)
                 e1 = self.torch.cuda.Event(enable_timing=True)
                 e0.record(self.stream)
-            flags = {r: ctx.dist_step(self.dt, phase, read_flag=False)
-                     for r, ctx in self.m.items()}
+            if self.sar is not None:  # per-rank sweep times for Stop-At-Rise
+                ev = {}
+                for r, ctx in self.m.items():
+                    a = self.torch.cuda.Event(enable_timing=True)
+                    b = self.torch.cuda.Event(enable_timing=True)
+                    a.record(self.stream)
+                    ctx.dist_step(self.dt, phase, read_flag=False)
+                    b.record(self.stream)
+                    ev[r] = (a, b)
+            else:
+                for r, ctx in self.m.items():
+                    ctx.dist_step(self.dt, phase, read_flag=False)
             if self.prof is not None:
                 e1.record(self.stream)
                 self.prof.append((e0, e1))
             if not last:
                 flags = {r: ctx.read_flag() for r, ctx in self.m.items()}
             flag = 0 if last else self._allreduce_max(flags)
+            if self.sar is not None and not last:
+                self.sar.record(self._rank_times({r: a.elapsed_time(b) for r, (a, b) in ev.items()}))
+                if self.sar.decide():
+                    t0 = time.perf_counter()
+                    self.rebalance()
+                    self._rebuild()
+                    reb += 1
+                    self.torch.cuda.synchronize()
+                    self.sar.reset(cost=1e3 * (time.perf_counter() - t0))
+                    flag = 0  # just rebuilt; the next step refreshes
         return reb
 
     def _allreduce_min(self, vals):
@@ -716,8 +787,13 @@ def weighted_cuts(x, w, p, lo, hi, min_width):
         targets = cw[-1] * np.arange(1, p) / p
         k = np.searchsorted(cw, targets)
         cuts = xs[np.minimum(k, xs.size - 1)]
-    cuts = np.asarray(cuts, np.float64)
-    # enforce the minimum slab width: forward, then backward passes
+    return _min_width(cuts, p, lo, hi, min_width)
+
+
+def _min_width(cuts, p, lo, hi, min_width):
+    """Move interior cuts apart so that every slab is at least min_width wide
+    (forward, then backward pass)."""
+    cuts = np.asarray(cuts, np.float64).copy()
     span = hi - lo
     if span < p * min_width * (1 + 1e-6):
         raise ValueError("box too small for p slabs of min_width")
@@ -727,6 +803,39 @@ def weighted_cuts(x, w, p, lo, hi, min_width):
     for i in range(p - 2, -1, -1):
         cuts[i] = min(cuts[i], (cuts[i + 1] if i < p - 2 else hi) - mw)
     return cuts.astype(np.float32)
+
+
+def histogram_cuts(grid, local_pos, local_w, lo, hi, rv, allreduce_sum, bins=4096):
+    """Load-balanced tensor-product cuts WITHOUT gathering particles
+    (§3.5): every rank bins its owned particles' coordinates,
+    weighted by their pair work, into `bins` slabs per decomposed axis; the
+    histograms are summed over ranks (allreduce_sum) and every rank cuts the
+    same global histogram at the weighted quantiles k/p (upper edge of the
+    crossing bin), then enforces slabs >= 2 r_v.  Identical cuts on every
+    rank."""
+    local_pos = np.asarray(local_pos, np.float64).reshape(-1, 3)
+    local_w = np.asarray(local_w, np.float64).reshape(-1)
+    hs = []
+    for d in range(3):
+        h, _ = np.histogram(local_pos[:, d], bins=bins, range=(float(lo[d]), float(hi[d])),
+                            weights=local_w)
+        hs.append(h)
+    H = np.asarray(allreduce_sum(np.concatenate(hs)), np.float64).reshape(3, bins)
+    cuts = []
+    for d in range(3):
+        p = grid[d]
+        if p <= 1:
+            cuts.append(np.zeros(0, np.float32))
+            continue
+        edges = np.linspace(float(lo[d]), float(hi[d]), bins + 1)
+        cw = np.cumsum(H[d])
+        if cw[-1] <= 0:
+            c = float(lo[d]) + (float(hi[d]) - float(lo[d])) * np.arange(1, p) / p
+        else:
+            k = np.searchsorted(cw, cw[-1] * np.arange(1, p) / p)
+            c = edges[np.minimum(k + 1, bins)]
+        cuts.append(_min_width(c, p, float(lo[d]), float(hi[d]), 2.0 * float(rv) * (1 + 1e-5)))
+    return tuple(cuts)
 
 
 def balanced_decomp(grid, pos, weights, lo, hi, rv):

@@ -221,9 +221,11 @@ class Context:
         hi = np.ascontiguousarray(hi, np.float32)
         per = np.ascontiguousarray(periodic, np.int32)
         self._check(self.L.pm_set_domain(self.h, lo.ctypes.data, hi.ctypes.data, per.ctypes.data))
+        self._box = (lo.copy(), hi.copy())
 
     def set_cutoff(self, r_cut, skin):
         self._check(self.L.pm_set_cutoff(self.h, r_cut, skin))
+        self._rv = float(np.float32(np.float32(r_cut) + np.float32(skin)))
 
     def set_lj(self, epsilon=1.0, sigma=1.0, mass=1.0, r_min=0.0):
         self._check(self.L.pm_set_lj(self.h, epsilon, sigma, mass, r_min))

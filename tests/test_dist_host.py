@@ -438,3 +438,39 @@ def test_ghost_put_reverses_the_ghost_round_gloo_world2():
         n_sent = sum(sent)  # records r packed as ghosts for the other rank
         assert res[other][1][r] == n_sent  # the other rank received them
         assert put == [[other, k] for k in range(n_sent)]
+
+
+def test_histogram_cuts_match_gathered_quantiles_and_are_rank_independent():
+    """NEXT-2 without a global gather: cuts from summed
+    per-rank histograms equal (to one bin) the weighted quantiles of the
+    gathered particles, do not depend on how the particles are split over
+    ranks, and keep slabs >= 2 r_v."""
+    from paper_1804_07598_b200.dist import histogram_cuts, weighted_cuts
+    rng = np.random.default_rng(5)
+    L = 120.0
+    x = np.concatenate([rng.normal(30, 6, (40000, 3)), rng.uniform(0, L, (20000, 3))]) % L
+    w = rng.uniform(20, 80, x.shape[0])
+    grid = (4, 2, 1)
+    lo, hi = np.zeros(3), np.full(3, L)
+    parts = np.array_split(rng.permutation(x.shape[0]), 3)  # three "ranks"
+    hs = []
+
+    def collect(h):
+        hs.append(h)
+        return h
+    # every rank's histogram, then their sum (what an all-reduce would return)
+    for p_ in parts:
+        histogram_cuts(grid, x[p_], w[p_], lo, hi, 2.8, collect, bins=4096)
+    tot = sum(hs)
+    c_split = histogram_cuts(grid, x[parts[0]], w[parts[0]], lo, hi, 2.8, lambda h: tot,
+                             bins=4096)
+    c_all = histogram_cuts(grid, x, w, lo, hi, 2.8, lambda h: h, bins=4096)
+    for d in range(3):
+        assert np.array_equal(c_split[d], c_all[d])
+        if grid[d] > 1:
+            q = weighted_cuts(x[:, d], w, grid[d], 0.0, L, 2.8 * 2 * (1 + 1e-5))
+            assert np.all(np.abs(q - c_all[d]) <= L / 4096 + 1e-3)
+            edges = np.concatenate([[0.0], c_all[d], [L]])
+            assert np.all(np.diff(edges) >= 5.6)
+        else:
+            assert c_all[d].size == 0

@@ -623,3 +623,45 @@ def test_decomposed_newton_lists_with_ghost_put(env, grid):
     ref.close()
     for m in members.values():
         m.close()
+
+
+def test_runtime_rebalance_sar_clustered(env):
+    """SURVEY NEXT-2 at run time (§3.5 "dynamic load
+    balancing", SAR [56]): a clustered system (8 Gaussian clusters, capped LJ,
+    velocity limit -- reading R22) starts on EQUAL cuts of a 2x2x2 loopback
+    decomposition; DistSim.run with Stop-At-Rise re-balancing records the
+    per-rank sweep times, re-cuts from all-reduced pair-work histograms (no
+    gather) and migrates mid-run.  After the run: at least one re-balance,
+    lower work imbalance than the equal cuts, every particle owned once, and
+    sampled rows' forces equal the fp64 oracle on the global system."""
+    import torch
+    pm, dist = env
+    from oracle import oracle as orc
+    s = inputs.cfg5(n_clusters=8, per_cluster=8192, sigma_c=6.0, rho=0.3, key=57)
+    D = dist.Decomp((2, 2, 2))
+    owner = dist.owner_of(s, D)
+    stream = torch.cuda.Stream()
+    members = {r: dist.make_member(s.subset(np.where(owner == r)[0]), D, r, stream=stream,
+                                   r_min=0.8) for r in range(D.size)}
+    for ctx in members.values():
+        ctx.set_vlimit(0.15 / 0.005)
+    sim = dist.DistSim(D, members, dist.LoopbackTransport(members), stream=stream)
+    sim.start()
+    work0 = [ctx.count()["nnz"] for ctx in sim.m.values()]
+    sim.enable_rebalance(cost_ms=0.0)
+    sim.run(30)
+    assert sim.rebalances >= 1
+    assert sim.D.cuts is not None
+    work1 = [ctx.count()["nnz"] for ctx in sim.m.values()]
+    assert dist.imbalance(work1) < dist.imbalance(work0)
+    got = owned_union(pm, sim)
+    assert np.array_equal(got["gid"], np.sort(s.gid))
+    pos = np.zeros_like(s.pos)
+    pos[:, :3] = got["pos"][:, :3]  # gid g at row g (gids are 0..n-1)
+    assert np.array_equal(got["gid"], np.arange(s.n))
+    rows = np.random.default_rng(4).choice(s.n, 300, replace=False)
+    ref = orc.lj_rows(pos, s.lo, s.hi, s.periodic, rc=2.5, r_min=0.8, rows=rows)
+    err = orc.normalized_max_err(got["force"][rows, :3].astype(np.float64), ref["F"])
+    assert err <= 1e-4, err
+    for ctx in sim.m.values():
+        ctx.close()
