@@ -586,7 +586,9 @@ __global__ void __launch_bounds__(stg::kWarps * 32, 5)
       PCS[2 * t + 1] = c1;
       POS[2 * t + 1] = o1;
     }
-    const StRows R{rows, grow, __any_sync(0xffffffffu, long_piece) != 0};
+    // wcap == 0: no shared-memory rows at all (rows too long for shared memory,
+    // clustered inputs): every segment appends straight to its global rows
+    const StRows R{rows, grow, wcap == 0 || __any_sync(0xffffffffu, long_piece) != 0};
     __syncwarp();
     // stage iterator over the pieces: (p, o) = piece, offset inside it
     int p = 0;
@@ -784,7 +786,8 @@ static size_t staged_smem(int wcap) {
 }
 
 template <int RCH, int NMODE>
-static void launch_st(const Params &P, const Bufs &B, int64_t n, size_t sm, cudaStream_t s) {
+static void launch_st(const Params &P, const Bufs &B, int64_t n, size_t sm, int wcap,
+                      cudaStream_t s) {
   static size_t set = 0;
   if (sm > set) {
     cudaFuncSetAttribute(k_verlet_st<RCH, NMODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -792,7 +795,7 @@ static void launch_st(const Params &P, const Bufs &B, int64_t n, size_t sm, cuda
     set = sm;
   }
   const unsigned g = (unsigned)((n + stg::kWarps * 32 - 1) / (stg::kWarps * 32));
-  k_verlet_st<RCH, NMODE><<<g, stg::kWarps * 32, sm, s>>>(P, B, (int)n, P.nbr_cap);
+  k_verlet_st<RCH, NMODE><<<g, stg::kWarps * 32, sm, s>>>(P, B, (int)n, wcap);
 }
 
 void launch_verlet(const Params &P, const Bufs &B, int64_t n, cudaStream_t s) {
@@ -800,19 +803,26 @@ void launch_verlet(const Params &P, const Bufs &B, int64_t n, cudaStream_t s) {
   if (n <= 0) return;
   const unsigned g = (unsigned)((n + 255) / 256);
   const int nm = P.newton ? (P.dist ? 2 : 1) : 0;
-  const size_t sm = P.reach == 2 ? staged_smem<2>(P.nbr_cap) : staged_smem<1>(P.nbr_cap);
+  // rows in shared memory when the widest slice fits, else the same kernel
+  // appending straight to global rows (wcap = 0)
+  size_t sm = P.reach == 2 ? staged_smem<2>(P.nbr_cap) : staged_smem<1>(P.nbr_cap);
+  int wcap = P.nbr_cap;
+  if (!sm) {
+    wcap = 0;
+    sm = stg::kWarps * (P.reach == 2 ? stg::Geo<2>::warp_bytes(0) : stg::Geo<1>::warp_bytes(0));
+  }
   static const int staged_env = [] {
     const char *e = std::getenv("PM_VERLET_STAGED");
     return (e && e[0] == '0') ? 0 : 1;
   }();
-  if (sm && staged_env) {
+  if (staged_env) {
     if (P.reach == 2) {
-      if (nm == 1) launch_st<2, 1>(P, B, n, sm, s);
-      else launch_st<2, 0>(P, B, n, sm, s);
+      if (nm == 1) launch_st<2, 1>(P, B, n, sm, wcap, s);
+      else launch_st<2, 0>(P, B, n, sm, wcap, s);
     } else {
-      if (nm == 2) launch_st<1, 2>(P, B, n, sm, s);
-      else if (nm == 1) launch_st<1, 1>(P, B, n, sm, s);
-      else launch_st<1, 0>(P, B, n, sm, s);
+      if (nm == 2) launch_st<1, 2>(P, B, n, sm, wcap, s);
+      else if (nm == 1) launch_st<1, 1>(P, B, n, sm, wcap, s);
+      else launch_st<1, 0>(P, B, n, sm, wcap, s);
     }
     return;
   }
