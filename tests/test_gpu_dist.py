@@ -665,3 +665,25 @@ def test_runtime_rebalance_sar_clustered(env):
     assert err <= 1e-4, err
     for ctx in sim.m.values():
         ctx.close()
+
+
+def test_torchrun_ipc_fused_refresh_two_processes(env):
+    """The fused ghost refresh across PROCESSES (CUDA IPC mappings of the
+    peer's position buffers, DistSim(peer=True)): two ranks on this GPU over
+    gloo, 40 steps with rebuilds; the union of the owned states equals one
+    context (tools/dist_peer_check.py asserts and prints "peer-ipc OK")."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(root, "tools", "dist_peer_check.py"), "24"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "peer-ipc OK" in r.stdout, r.stdout[-2000:]
