@@ -144,6 +144,12 @@ struct Member {
   int64_t *d_cnt = nullptr;  // [2][26] device: counts sent / received (NCCL)
   int64_t *h_cnt = nullptr;  // pinned mirror
   int flag = 0;              // last local rebuild flag
+  // fused ghost refresh (the sweep's epilogue stores into the peers' ghost
+  // slots): this member's ghost slots, per send entry (peer, receiver slot)
+  int *d_slots = nullptr, *d_dst_peer = nullptr, *d_dst_slot = nullptr;
+  size_t slots_cap = 0, dst_cap = 0, dst2_cap = 0;
+  std::vector<uint8_t> peer_handles;  // IPC handles the peers' buffers were opened from
+  std::vector<void *> peer_p0, peer_p1;
   pm_run_stats stats{};
   double thermo[5] = {0, 0, 0, 0, 0};
 };
@@ -168,6 +174,10 @@ struct Group {
   double *d_red = nullptr;
   double *h_red = nullptr;
   int64_t rebuilds = 0;
+  bool fused = false;       // fused ghost refresh enabled (PM_GROUP_FUSED, default 1)
+  bool fused_ready = false; // set up for the current ghost layout
+  uint8_t *d_handles = nullptr;  // NCCL all-gather of the members' IPC handles
+  uint8_t *h_handles = nullptr;
 
   int coord(int sd, int d) const {
     return d == 0 ? sd % grid[0] : d == 1 ? (sd / grid[0]) % grid[1] : sd / (grid[0] * grid[1]);
@@ -436,6 +446,128 @@ pm_status refresh(Group &G) {
   return PM_OK;
 }
 
+__global__ void k_fill_i32(int *p, int64_t n, int v) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+pm_status ensure_i32(pm_ctx c, int **p, size_t *cap, size_t need) {
+  if (need <= *cap && *p) return PM_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  const size_t n = std::max<size_t>(need + need / 4, 64);
+  pm_status s = cuda_err(c, cudaMalloc((void **)p, n * sizeof(int)), "fused refresh tables");
+  if (!s) *cap = n;
+  return s;
+}
+
+// Fused ghost refresh ("the K6 epilogue ... stores straight
+// into peer windows"): after a rebuild every member registers, per entry of
+// its ghost send list, the receiving peer and the receiver's ghost slot (the
+// receiver's arrival order: the ghost round reversed) and the peers' two
+// position buffers -- same-process pointers for local peers, CUDA IPC
+// mappings (handles all-gathered over NCCL) for peers in other processes.
+// From then on the force sweep's velocity-Verlet epilogue writes x(s+1) of
+// every sent particle into the peers' next position buffer: no pack, no
+// message, no unpack per step; the per-step flag all-reduce orders it before
+// the peers' next sweep.
+pm_status setup_fused(Group &G) {
+  pm_status s;
+  for (auto &R : G.m) {  // ghost slots in arrival order
+    int64_t ng = 0;
+    for (int64_t v : R.ghost_recv_n) ng += v;
+    if ((s = ensure_i32(R.ctx, &R.d_slots, &R.slots_cap, (size_t)ng + 1))) return s;
+    if ((s = pm_dist_ghost_slots(R.ctx, ng ? R.d_slots : nullptr))) return s;
+  }
+  // peers' position buffers: local pointers, or IPC across processes
+  const bool remote = G.comm && G.nranks > 1;
+  if (remote) {
+    Member &R = G.m[0];  // one member per rank
+    uint8_t mine[128];
+    if ((s = pm_dist_ipc_handles(R.ctx, mine))) return s;
+    std::memcpy(G.h_handles + 128 * G.rank, mine, 128);
+    cudaMemcpyAsync(G.d_handles + 128 * G.rank, mine, 128, cudaMemcpyHostToDevice, G.stream);
+    Nccl &N = nccl();
+    N.GroupStart();
+    for (int r = 0; r < G.nranks; ++r)  // all-gather as point-to-point (no extra API)
+      if (r != G.rank) {
+        N.Send(G.d_handles + 128 * G.rank, 128, ncclUint8, r, G.comm, G.stream);
+        N.Recv(G.d_handles + 128 * r, 128, ncclUint8, r, G.comm, G.stream);
+      }
+    if ((s = nccl_err(R.ctx, N.GroupEnd(), "IPC handle exchange"))) return s;
+    cudaMemcpyAsync(G.h_handles, G.d_handles, 128 * (size_t)G.nranks, cudaMemcpyDeviceToHost,
+                    G.stream);
+    cudaError_t e = cudaStreamSynchronize(G.stream);
+    if (e != cudaSuccess) return cuda_err(R.ctx, e, "IPC handle exchange");
+    std::vector<uint8_t> all(G.h_handles, G.h_handles + 128 * (size_t)G.nranks);
+    if (all != R.peer_handles) {  // (re)open when any rank reallocated
+      if ((s = pm_dist_ipc_close_all(R.ctx))) return s;
+      R.peer_p0.assign(R.peers.size(), nullptr);
+      R.peer_p1.assign(R.peers.size(), nullptr);
+      for (size_t k = 0; k < R.peers.size(); ++k)
+        if ((s = pm_dist_ipc_open(R.ctx, G.h_handles + 128 * G.owner[R.peers[k]], &R.peer_p0[k],
+                                  &R.peer_p1[k])))
+          return s;
+      R.peer_handles = all;
+    }
+  } else {
+    for (auto &R : G.m) {
+      R.peer_p0.assign(R.peers.size(), nullptr);
+      R.peer_p1.assign(R.peers.size(), nullptr);
+      for (size_t k = 0; k < R.peers.size(); ++k)
+        if ((s = pm_dist_pos_buffers(G.member_of(R.peers[k])->ctx, &R.peer_p0[k],
+                                     &R.peer_p1[k])))
+          return s;
+    }
+  }
+  // per send entry: peer index and the receiver's slot
+  for (auto &R : G.m) {
+    int64_t nsend = 0;
+    for (int64_t v : R.ghost_seg_n) nsend += v;
+    if ((s = ensure_i32(R.ctx, &R.d_dst_peer, &R.dst_cap, (size_t)nsend + 1))) return s;
+    if ((s = ensure_i32(R.ctx, &R.d_dst_slot, &R.dst2_cap, (size_t)nsend + 1))) return s;
+    int64_t off = 0;
+    for (size_t k = 0; k < R.peers.size(); ++k) {
+      const int64_t n = R.ghost_seg_n[k];
+      if (n > 0) {
+        k_fill_i32<<<(unsigned)((n + 255) / 256), 256, 0, G.stream>>>(R.d_dst_peer + off, n,
+                                                                    (int)k);
+        if (!remote) {
+          Member *Q = G.member_of(R.peers[k]);
+          const int64_t ro = recv_offset(*Q, R.sd);
+          cudaMemcpyAsync(R.d_dst_slot + off, Q->d_slots + ro, n * sizeof(int),
+                          cudaMemcpyDeviceToDevice, G.stream);
+        }
+      }
+      off += n;
+    }
+  }
+  if (remote) {  // the receivers hand their slot slices back (the ghost round reversed)
+    Nccl &N = nccl();
+    Member &R = G.m[0];
+    N.GroupStart();
+    int64_t off = 0;
+    for (size_t k = 0; k < R.peers.size(); ++k) {
+      const int q = R.peers[k];
+      const int64_t n_out = R.ghost_recv_n[k], n_in = R.ghost_seg_n[k];
+      if (n_out > 0)
+        N.Send(R.d_slots + recv_offset(R, q), n_out, ncclInt32, G.owner[q], G.comm, G.stream);
+      if (n_in > 0) N.Recv(R.d_dst_slot + off, n_in, ncclInt32, G.owner[q], G.comm, G.stream);
+      off += n_in;
+    }
+    if ((s = nccl_err(R.ctx, N.GroupEnd(), "ghost slot exchange"))) return s;
+  }
+  for (auto &R : G.m) {
+    std::vector<void *> p0 = R.peer_p0, p1 = R.peer_p1;
+    if ((s = pm_dist_peer_setup(R.ctx, (int32_t)R.peers.size(), p0.data(), p1.data(),
+                                R.d_dst_peer, R.d_dst_slot)))
+      return s;
+  }
+  G.fused_ready = true;
+  return PM_OK;
+}
+
 // Global MAX of the local rebuild flags (NCCL all-reduce across ranks).
 pm_status allreduce_flag(Group &G, int *flag) {
   int f = 0;
@@ -511,12 +643,13 @@ pm_status do_map(Group &G) {
   return message_round(G, PM_MSG_MIGRATE);
 }
 
-double g_t_map = 0, g_t_ghost = 0, g_t_finish = 0;  // PM_GROUP_TIMING
+double g_t_map = 0, g_t_ghost = 0, g_t_finish = 0, g_t_fused = 0;  // PM_GROUP_TIMING
 
 pm_status do_ghost_get(Group &G) {
   pm_status s = ensure_decomposed(G);
   if (s) return s;
   if (G.P == 1) return pm_build_verlet(G.m[0].ctx);
+  G.fused_ready = false;  // new send lists and ghost slots
   static const bool timing = std::getenv("PM_GROUP_TIMING") != nullptr;
   auto t0 = std::chrono::steady_clock::now();
   if ((s = message_round(G, PM_MSG_GHOST))) return s;
@@ -581,10 +714,23 @@ pm_status do_run(Group &G, float dt, int64_t nsteps) {
   static const bool timing = std::getenv("PM_GROUP_TIMING") != nullptr;
   using clk = std::chrono::steady_clock;
   double t_reb = 0, t_ref = 0, t_step = 0, t_flag = 0;
+  g_t_map = g_t_ghost = g_t_finish = g_t_fused = 0;
+  const int64_t reb_start = G.rebuilds;
+  const bool fused = G.fused && G.P > 1;
   for (int64_t k = 0; k < nsteps; ++k) {
     auto t0 = clk::now();
     if (timing) cudaStreamSynchronize(G.stream);
-    if ((s = flag ? rebuild(G) : refresh(G))) return s;
+    if (flag) {
+      if ((s = rebuild(G))) return s;
+    } else if (!fused || k == 0) {  // k = 0: the prologue's drift has no fused stores
+      if ((s = refresh(G))) return s;
+    }
+    if (fused && !G.fused_ready) {
+      auto tf = clk::now();
+      if ((s = setup_fused(G))) return s;
+      if (timing) cudaStreamSynchronize(G.stream);
+      g_t_fused += std::chrono::duration<double, std::milli>(clk::now() - tf).count();
+    }
     if (timing) cudaStreamSynchronize(G.stream);
     auto t1 = clk::now();
     (flag ? t_reb : t_ref) += std::chrono::duration<double, std::milli>(t1 - t0).count();
@@ -602,9 +748,10 @@ pm_status do_run(Group &G, float dt, int64_t nsteps) {
   }
   if (timing)
     std::fprintf(stderr, "pm_dist_run %lld steps: rebuild %.3f ms, refresh %.3f ms, step %.3f ms, "
-                 "flag %.3f ms (synchronised phases); rebuilds so far: map %.3f, ghost round "
-                 "%.3f, finish %.3f ms\n", (long long)nsteps, t_reb, t_ref, t_step, t_flag,
-                 g_t_map, g_t_ghost, g_t_finish);
+                 "flag %.3f ms (synchronised phases); rebuilds: map %.3f, ghost round "
+                 "%.3f, finish %.3f, fused setup %.3f ms (%lld rebuilds)\n", (long long)nsteps,
+                 t_reb, t_ref, t_step, t_flag, g_t_map, g_t_ghost, g_t_finish, g_t_fused,
+                 (long long)(G.rebuilds - reb_start));
   if (prof) {  // the force sweeps (+ fused kick/drift) of the local members, per step
     cudaStreamSynchronize(G.stream);
     double ms = 0.0;
@@ -693,6 +840,10 @@ Group *new_group(const int32_t grid[3], int nranks, int rank, int device, void *
   cudaMallocHost((void **)&G->h_flag, sizeof(int) * (2 + 2 * G->P));
   cudaMalloc((void **)&G->d_red, 8 * sizeof(double));
   cudaMallocHost((void **)&G->h_red, 8 * sizeof(double));
+  cudaMalloc((void **)&G->d_handles, 128 * (size_t)std::max(nranks, 1));
+  cudaMallocHost((void **)&G->h_handles, 128 * (size_t)std::max(nranks, 1));
+  const char *f = std::getenv("PM_GROUP_FUSED");
+  G->fused = !(f && f[0] == '0');
   return G;
 }
 
@@ -700,6 +851,9 @@ void free_group(Group *G) {
   cudaSetDevice(G->device);
   if (G->stream) cudaStreamSynchronize(G->stream);
   for (auto &R : G->m) {
+    if (R.d_slots) cudaFree(R.d_slots);
+    if (R.d_dst_peer) cudaFree(R.d_dst_peer);
+    if (R.d_dst_slot) cudaFree(R.d_dst_slot);
     if (R.sbuf) cudaFree(R.sbuf);
     if (R.rbuf) cudaFree(R.rbuf);
     if (R.d_cnt) cudaFree(R.d_cnt);
@@ -711,6 +865,8 @@ void free_group(Group *G) {
   for (cudaEvent_t e : G->ev) cudaEventDestroy(e);
   cudaFree(G->d_red);
   cudaFreeHost(G->h_red);
+  if (G->d_handles) cudaFree(G->d_handles);
+  if (G->h_handles) cudaFreeHost(G->h_handles);
   if (G->own_stream) cudaStreamDestroy(G->stream);
   delete G;
 }
