@@ -842,8 +842,11 @@ Group *new_group(const int32_t grid[3], int nranks, int rank, int device, void *
   cudaMallocHost((void **)&G->h_red, 8 * sizeof(double));
   cudaMalloc((void **)&G->d_handles, 128 * (size_t)std::max(nranks, 1));
   cudaMallocHost((void **)&G->h_handles, 128 * (size_t)std::max(nranks, 1));
+  // fused refresh: default on in-process (verified against one context on
+  // the GPU); across processes (CUDA IPC over NVLink between ranks) opt-in
+  // with PM_GROUP_FUSED=1 until it has run on more than one GPU
   const char *f = std::getenv("PM_GROUP_FUSED");
-  G->fused = !(f && f[0] == '0');
+  G->fused = f ? f[0] != '0' : nranks == 1;
   return G;
 }
 
