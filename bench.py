@@ -199,11 +199,19 @@ def sph_pass(dev, stream, repeats=10):
     torch.cuda.synchronize()
     run_ms = e0.elapsed_time(e1) / nrun
     c.close()
+    nbar = nnz / s.n
+    peak, peak_src = hbm_peak()
+    alg = s.n * (12.0 * nbar + 70.0)  # list written once, read twice + fields
     return {"workload": "cfg4 (BJ configs[3]): 2,048,000 fluid + 414,060 boundary particles, "
                         "dp=1/160, h=1.3dp, cubic spline, Tait EOS, density summation + "
                         "pressure/viscous forces",
             "n_particles": s.n, "pass_ms": ms, "value": s.n / (ms * 1e-3), "unit": UNIT,
-            "mean_row": nnz / s.n, "includes": "Verlet build + density + forces per pass",
+            "roofline": {"bound": "hbm", "achieved": alg / (ms * 1e-3) / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": alg / (ms * 1e-3) / 1e9 / peak,
+                         "scope": "whole pass (Verlet build + density + forces)",
+                         "alg_bytes_formula": "N*(12*nbar + 70) (SURVEY 8(d) SPH pass)",
+                         "peak_source": peak_src},
+            "mean_row": nbar, "includes": "Verlet build + density + forces per pass",
             "run": {"what": "pm_sph_run: continuity density (Eq. 2) + Verlet time stepping, "
                             "dynamic dt (readings R26-R28), hydrostatic start, skin 0.1h",
                     "steps": r["steps"], "ms_per_step": run_ms,
@@ -270,6 +278,113 @@ def dem_run(dev, stream, warm=300, steps=500):
             "n_particles": s.n, "steps": steps, "after_steps": warm, "ms_per_step": ms,
             "value": s.n / (ms * 1e-3), "unit": UNIT, "rebuilds": reb,
             "mean_row": nnz / s.n}
+
+
+def cfg5_clustered(dev, stream, nc=8, reps=3):
+    """BJ configs[4] local density (reading R22): nc Gaussian
+    clusters x 131,072 (sigma_c 4, rho 0.5 overall; 8 clusters = 1,048,576
+    particles = one GPU's share of the 8.4M system), capped LJ.  Frozen mode:
+    cell list + Verlet build + capped force on the fixed configuration; and the
+    2x2x2 split in loopback with equal cuts vs histogram (pair-work) cuts."""
+    import torch
+    from paper_1804_07598_b200 import dist, inputs, pm
+    s = inputs.cfg5(n_clusters=nc)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    c = pm.Context(device=dev, stream=stream.cuda_stream)
+    c.set_domain(s.lo, s.hi, s.periodic)
+    c.set_cutoff(RC, SKIN)
+    c.set_lj(1.0, 1.0, 1.0, 0.8)
+    c.place(s.pos, s.vel, s.gid)
+    c.build_verlet()
+    c.compute_lj()
+    tb, tf = [], []
+    for _ in range(reps):
+        e0, e1, e2 = ev(), ev(), ev()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        c.build_verlet()
+        e1.record(stream)
+        c.compute_lj()
+        e2.record(stream)
+        torch.cuda.synchronize()
+        tb.append(e0.elapsed_time(e1))
+        tf.append(e1.elapsed_time(e2))
+    cnt = c.count()
+    th = c.thermo(recompute=True)
+    rp, _ = c.get_verlet(cols=False)
+    w = np.zeros(s.n)
+    w[c.get_state()["gid"]] = np.diff(rp)
+    c.close()
+    bms, fms = float(np.median(tb)), float(np.median(tf))
+    nnz = cnt["nnz"]
+    peak, _ = hbm_peak()
+    alg = s.n * (4.0 * nnz / s.n + 32.0)
+    out = {"workload": f"cfg5 local density: {nc} Gaussian clusters x 131,072 (sigma_c 4, "
+                       "rho 0.5), capped LJ r_min 0.8 (reading R22)", "n_particles": s.n,
+           "frozen": {"build_ms": bms, "force_ms": fms, "pass_ms": bms + fms,
+                      "value": s.n / ((bms + fms) * 1e-3), "unit": UNIT,
+                      "list_entries": nnz, "mean_row": nnz / s.n,
+                      "max_row": int(np.max(np.diff(rp))), "pairs_in_rc": int(th["npairs"]),
+                      "pair_interactions_per_s": th["npairs"] / ((bms + fms) * 1e-3),
+                      "force_roofline": {"bound": "hbm", "frac": alg / (fms * 1e-3) / 1e9 / peak,
+                                         "alg_bytes_formula": "N*(4*nbar + 32)"}}}
+    split = {}
+    for name in ("equal", "balanced"):
+        D = dist.Decomp((2, 2, 2)) if name == "equal" else dist.Decomp(
+            (2, 2, 2), dist.histogram_cuts((2, 2, 2), s.pos[:, :3], w + 1.0, s.lo, s.hi,
+                                           RC + SKIN, lambda h: h))
+        owner = dist.owner_of(s, D)
+        mem = {r: dist.make_member(s.subset(np.where(owner == r)[0]), D, r, device=dev,
+                                   stream=stream, r_min=0.8) for r in range(D.size)}
+        sim = dist.DistSim(D, mem, dist.LoopbackTransport(mem), stream=stream)
+        sim.start()
+        times = []
+        for ctx in mem.values():
+            a, b = ev(), ev()
+            torch.cuda.synchronize()
+            a.record(stream)
+            ctx.dist_step(DT, 3)  # PM_PHASE_FORCES
+            b.record(stream)
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b))
+        nz = [ctx.count()["nnz"] for ctx in mem.values()]
+        split[name] = {"n_owned": [ctx.count()["n_owned"] for ctx in mem.values()],
+                       "pair_entries": nz, "sweep_ms": times,
+                       "imbalance_pairs": dist.imbalance(nz), "imbalance_sweep": dist.imbalance(times)}
+        for ctx in mem.values():
+            ctx.close()
+    out["split_2x2x2"] = split
+    return out
+
+
+def cfg3_p1_group(dev, stream, steps, warmup):
+    """The weak-scaling base (BJ configs[2] at P = 1): one 128^3 block
+    (2,097,152 particles) through the same group API as the N > 1 lines
+    (pm_create_dist_local grid (1,1,1) -> pm_map -> pm_ghost_get ->
+    pm_dist_run), so E(P) = t_step(1) / t_step(P) can be formed."""
+    import torch
+    from paper_1804_07598_b200 import inputs, pm
+    s = inputs.cfg3_block(0, 0, 0, grid=(1, 1, 1), m=128)
+    (c,) = pm.create_dist_local((1, 1, 1), device=dev, stream=stream.cuda_stream)
+    c.set_domain(s.lo, s.hi, s.periodic)
+    c.set_cutoff(RC, SKIN)
+    c.set_lj(1.0, 1.0, 1.0, 0.0)
+    c.place(s.pos, s.vel, s.gid)
+    c.map()
+    c.ghost_get()
+    c.dist_run(DT, warmup)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    r = c.dist_run(DT, steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    c.close()
+    return {"workload": "cfg3 (BJ configs[2]) P=1: one 128^3 block, 2,097,152 particles, "
+                        "through pm_dist_run (the N>1 API)", "n_particles": s.n, "steps": steps,
+            "ms_per_step": ms / steps, "value": s.n * steps / (ms * 1e-3), "unit": UNIT,
+            "rebuilds": r["rebuilds"]}
 
 
 def run_reference(args):
@@ -371,7 +486,11 @@ def run_ours(args):
     tp = os.path.join(ROOT, "profiles", "force_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("bytes_per_launch")
+            ft = json.load(open(tp))
+            traffic = ft.get("bytes_per_launch")
+            nb_cap = ft.get("nbar_at_capture")
+            if traffic and nb_cap:  # the capture's bytes at this run's mean row length
+                traffic *= (4.0 * nbar + 64.0) / (4.0 * nb_cap + 64.0)
         except Exception:
             traffic = None
     c.close()
@@ -402,6 +521,9 @@ def run_ours(args):
     cfg1 = None if args.no_extras else cfg1_latency(dev, stream)
     sph = None if args.no_extras else sph_pass(dev, stream)
     dem = None if args.no_extras else dem_run(dev, stream)
+    cfg5 = None if args.no_extras else cfg5_clustered(dev, stream)
+    cfg3 = None if args.no_extras else cfg3_p1_group(dev, stream, min(args.steps, 500),
+                                                      args.warmup)
     cpu = cpu_baseline() if not args.no_cpu_baseline else None
     launches = 2 * args.steps + 11 * stats["rebuilds"] + 3
     line = {
@@ -435,6 +557,8 @@ def run_ours(args):
         "cfg1": cfg1,
         "sph": sph,
         "dem": dem,
+        "cfg5": cfg5,
+        "cfg3_p1": cfg3,
     }
     # pairs/s: ordered pairs inside r_cut ~ measured once from the energy pass
     print(json.dumps(line), flush=True)

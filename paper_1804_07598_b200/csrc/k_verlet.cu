@@ -438,25 +438,26 @@ __device__ __forceinline__ void st_fast_group(const float4 *__restrict__ SA,
       s2 = f2_fma(dz, dz, s2);
       f2_unpack(s2, sd[2 * q], sd[2 * q + 1]);
     }
+    // the hits only: a store with few active lanes costs one shared-memory
+    // wavefront and (almost) never a bank conflict
     const int c0 = cb + g + 8 * u8;
     asm volatile(
         "{\n\t.reg .pred p;\n\t.reg .u32 v;\n\t"
-        "st.shared.u16 [%0], %1;\n\t"
-        "setp.lt.f32 p, %2, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
-        "add.u32 v, %1, 1;\n\tst.shared.u16 [%0], v;\n\t"
-        "setp.lt.f32 p, %3, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
-        "add.u32 v, %1, 2;\n\tst.shared.u16 [%0], v;\n\t"
-        "setp.lt.f32 p, %4, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
-        "add.u32 v, %1, 3;\n\tst.shared.u16 [%0], v;\n\t"
-        "setp.lt.f32 p, %5, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
-        "add.u32 v, %1, 4;\n\tst.shared.u16 [%0], v;\n\t"
-        "setp.lt.f32 p, %6, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
-        "add.u32 v, %1, 5;\n\tst.shared.u16 [%0], v;\n\t"
-        "setp.lt.f32 p, %7, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
-        "add.u32 v, %1, 6;\n\tst.shared.u16 [%0], v;\n\t"
-        "setp.lt.f32 p, %8, %10;\n\t@p add.u32 %0, %0, 64;\n\t"
-        "add.u32 v, %1, 7;\n\tst.shared.u16 [%0], v;\n\t"
-        "setp.lt.f32 p, %9, %10;\n\t@p add.u32 %0, %0, 64;\n\t}"
+        "setp.lt.f32 p, %2, %10;\n\t@p st.shared.u16 [%0], %1;\n\t@p add.u32 %0, %0, 64;\n\t"
+        "add.u32 v, %1, 1;\n\t"
+        "setp.lt.f32 p, %3, %10;\n\t@p st.shared.u16 [%0], v;\n\t@p add.u32 %0, %0, 64;\n\t"
+        "add.u32 v, %1, 2;\n\t"
+        "setp.lt.f32 p, %4, %10;\n\t@p st.shared.u16 [%0], v;\n\t@p add.u32 %0, %0, 64;\n\t"
+        "add.u32 v, %1, 3;\n\t"
+        "setp.lt.f32 p, %5, %10;\n\t@p st.shared.u16 [%0], v;\n\t@p add.u32 %0, %0, 64;\n\t"
+        "add.u32 v, %1, 4;\n\t"
+        "setp.lt.f32 p, %6, %10;\n\t@p st.shared.u16 [%0], v;\n\t@p add.u32 %0, %0, 64;\n\t"
+        "add.u32 v, %1, 5;\n\t"
+        "setp.lt.f32 p, %7, %10;\n\t@p st.shared.u16 [%0], v;\n\t@p add.u32 %0, %0, 64;\n\t"
+        "add.u32 v, %1, 6;\n\t"
+        "setp.lt.f32 p, %8, %10;\n\t@p st.shared.u16 [%0], v;\n\t@p add.u32 %0, %0, 64;\n\t"
+        "add.u32 v, %1, 7;\n\t"
+        "setp.lt.f32 p, %9, %10;\n\t@p st.shared.u16 [%0], v;\n\t@p add.u32 %0, %0, 64;\n\t}"
         : "+r"(bo)
         : "r"(c0), "f"(sd[0]), "f"(sd[1]), "f"(sd[2]), "f"(sd[3]), "f"(sd[4]), "f"(sd[5]),
           "f"(sd[6]), "f"(sd[7]), "f"(rv2));

@@ -21,4 +21,5 @@ c.set_cutoff(2.5, 0.3)
 c.set_lj(1.0, 1.0, 1.0, 0.0)
 c.place(s.pos, s.vel, s.gid)
 r = c.step_vv(0.005, a.steps)
-print(r)
+import json  # noqa: E402
+print(json.dumps(r))

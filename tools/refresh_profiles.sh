@@ -8,7 +8,7 @@ mkdir -p gpurun_out
 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 echo "bench rc=$?"
 PM_USE_GRAPHS=0 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-  --log-file gpurun_out/launches.csv python bench.py --steps 200 --warmup 10 --no-cpu-baseline \
+  --log-file gpurun_out/launches.csv python bench.py --steps 200 --warmup 10 --no-cpu-baseline --no-extras \
   > gpurun_out/launches.log 2>&1
 echo "launch list rc=$?"
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:"k_lj_step|k_verlet" \

@@ -1,12 +1,14 @@
-"""Write profiles/r01_ncu_summary.md and profiles/force_traffic.json from the
-outputs of tools/refresh_profiles.sh (gpurun_out/): the bench line, the ncu
-launch list and the --set full captures.  Usage: python tools/write_summary.py"""
+"""Write profiles/<round>_ncu_summary.md and profiles/force_traffic.json from
+the outputs of tools/refresh_profiles.sh (gpurun_out/): the bench line, the
+ncu launch list and the --set full captures.
+Usage: python tools/write_summary.py [round-tag, default r02]"""
 import json
 import os
 import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TAG = sys.argv[1] if len(sys.argv) > 1 else "r02"
 G = os.path.join(ROOT, "gpurun_out")
 P = os.path.join(ROOT, "profiles")
 
@@ -28,19 +30,25 @@ for name in ("step_full", "sph_rates_full", "dem_step_full"):
         caps.setdefault(k, []).append(r)
 lj = next(v for k, v in caps.items() if k.startswith("k_lj_step<0"))
 traffic = sum(r["dram_read_MB"] + r["dram_write_MB"] for r in lj) / len(lj) * 1e6
+nbar_cap = None
+for line in open(os.path.join(G, "step_full.log")):
+    if line.startswith("{") and "mean_row" in line:
+        nbar_cap = json.loads(line)["mean_row"]
 json.dump({"kernel": "k_lj_step<0> (force sweep + fused VV)", "bytes_per_launch": traffic,
-           "source": "profiles/r01_ncu_summary.md (ncu --set full, tools/prof_step.py cfg2 "
+           "nbar_at_capture": nbar_cap,
+           "source": f"profiles/{TAG}_ncu_summary.md (ncu --set full, tools/prof_step.py cfg2 "
                      "liquid phase, mean over the captured launches of dram__bytes_read.sum + "
-                     "dram__bytes_write.sum)"},
+                     "dram__bytes_write.sum); bench.py scales it by (4 nbar + 64) / (4 "
+                     "nbar_at_capture + 64) to the bench run's mean row"},
           open(os.path.join(P, "force_traffic.json"), "w"), indent=1)
 launches = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_launches.py"),
                            os.path.join(G, "launches.csv")], capture_output=True, text=True,
                           check=True).stdout
 L = []
-L.append("# Round 1 profile summary (B200, sm_100a)\n")
+L.append("# Round %s profile summary (B200, sm_100a)\n" % TAG[1:])
 L.append("Produced by `tools/refresh_profiles.sh` (one gpurun call) and `tools/write_summary.py`.\n")
 L.append("Bench line (`python bench.py`, defaults: %d timed steps after %d warm-up): "
-         "profiles/r01_bench.json\n" % (b["steps"], b["warmup"]))
+         "profiles/%s_bench.json\n" % (b["steps"], b["warmup"], TAG))
 L.append("- value %.4g particle-updates/s, %.1f us/step, %d rebuilds in %d steps, mean row %.2f"
          % (b["value"], 1e3 * b["ms_per_step"], b["config"]["rebuilds"], b["steps"],
             b["config"]["mean_row"]))
@@ -72,15 +80,14 @@ for k, rs in caps.items():
     L.append("| %s | %d | " % (k, len(rs)) + " | ".join(
         ("%.4g" % m[c]) if c != "inst" else ("%.4g" % m[c]) for c in cols) + " |")
 L.append("")
-L.append("k_lj_step: L1/tex data pipe ~80% busy (each float4 neighbour gather touches ~10 "
-         "distinct 128-B lines), issue ~55%, DRAM ~31%.  k_verlet: latency-bound on its L2 "
-         "candidate loads, issue ~64%; it writes ~470 MB for a ~300 MB list (rows appended lane "
-         "by lane).  k_sph_rates: issue-bound after the gather hoisting (issue 68%, ~530M "
-         "instructions).  k_dem_step: short rows (~6 entries), L2-latency bound.\n")
+L.append("k_lj_step: bound by L1/tex data-pipe wavefronts of its scattered float4 neighbour "
+         "gathers (see DESIGN.md §11).  k_verlet_st (staged build): coalesced candidate stages, "
+         "paired fp32 tests, predicated appends into 16-bit shared-memory rows, full-line "
+         "flushes (no write amplification).  k_sph_rates / k_dem_step as in round 1.\n")
 L.append("## Launch list (`PM_USE_GRAPHS=0 ncu --metrics gpu__time_duration.sum --clock-control "
          "none` of `python bench.py --steps 200 --warmup 10 --no-cpu-baseline`; cold-cache, "
          "serialised: compare shares; the SPH and DEM kernels come from the bench's `sph` and "
          "`dem` extras)\n")
 L.append(launches)
-open(os.path.join(P, "r01_ncu_summary.md"), "w").write("\n".join(L))
+open(os.path.join(P, f"{TAG}_ncu_summary.md"), "w").write("\n".join(L))
 print("\n".join(L[:12]))
