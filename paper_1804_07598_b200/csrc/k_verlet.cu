@@ -299,7 +299,9 @@ constexpr int kWarps = 4;       // warps per block (independent of each other)
 constexpr int kStage = 128;     // candidates per stage
 constexpr int kOffBits = 10;    // row entry in shared memory: piece << 10 | offset
 constexpr int kMaxPieceLen = 1 << kOffBits;
-constexpr int kStageBytes = kStage / 2 * 16 + kStage / 2 * 8;  // A + Z
+// stage: A = (x0, x1, y0, y1) and Z = (z0, z1, code0, code1) per candidate
+// pair, then the stage slot of every own lane's self candidate (int[32])
+constexpr int kStageBytes = kStage / 2 * 16 + kStage / 2 * 16 + 32 * 4;
 template <int RCH>
 struct Geo {
   static constexpr int NR = (2 * RCH + 1) * (2 * RCH + 1);  // stencil rows
@@ -346,29 +348,30 @@ struct StRows {
   bool direct;
 };
 
-// Append the hits of one group of 32 staged candidates (indices jg + u, codes
-// cg + u) through the bit mask (overflow, per-pair R4, half lists).
+// Append the hits of one group of 32 staged candidates (stage slots g + u,
+// their codes in SZ) through the bit mask (overflow, half lists, direct rows).
 template <int NMODE>
-__device__ __forceinline__ void st_expand(unsigned msk, int jg, int cg, int self, int cap,
-                                          int lane, const StRows &R, int &k,
+__device__ __forceinline__ void st_expand(unsigned msk, const float4 *__restrict__ SZ, int g,
+                                          const int2 *__restrict__ PBE, int selfslot, int self,
+                                          int cap, int lane, const StRows &R, int &k,
                                           const GhostRule &gr) {
-  if (NMODE == 1) {
-    const int t = self - jg;
-    msk &= t < 0 ? 0xffffffffu : (t >= 31 ? 0u : (0xffffffffu << (t + 1)));
-  } else if (self >= jg && self < jg + 32) {
-    msk &= ~(1u << (self - jg));
-  }
+  if (selfslot >= g && selfslot < g + 32) msk &= ~(1u << (selfslot - g));
   while (msk) {
     const int u = __ffs(msk) - 1;
     msk &= msk - 1u;
-    const int j = jg + u;
+    const int v = g + u;
+    const float4 zc = SZ[v >> 1];
+    const unsigned code = __float_as_uint((v & 1) ? zc.w : zc.z);
+    const int j = R.direct ? (int)code
+                           : PBE[code >> stg::kOffBits].x + (int)(code & (stg::kMaxPieceLen - 1));
+    if (NMODE == 1 && j <= self) continue;  // half rows: j > i only
     if (NMODE == 2) {
       if ((gr.kind[j] & kGhostBit) ? (gr.gid[j] < gr.gid_self) : (j < self)) continue;
     }
     const int kk = min(k, cap - 1);
     PM_CHECK(j >= 0 && kk >= 0);
     if (R.direct) R.gl[(int64_t)kk << 5] = j;
-    else R.sm[(kk << 5) + lane] = (unsigned short)(cg + u);
+    else R.sm[(kk << 5) + lane] = (unsigned short)code;
     ++k;
   }
 }
@@ -398,9 +401,9 @@ __device__ __forceinline__ u64 f2_r4(u64 B, float a, float L, float hL) {
 // global faces, runs covering a whole periodic row).
 template <bool PMI>
 __device__ __forceinline__ void st_fast_group(const float4 *__restrict__ SA,
-                                              const float2 *__restrict__ SZ, int g, int gn,
+                                              const float4 *__restrict__ SZ, int g, int gn,
                                               const float4 &xe, const Box &box, int pmi,
-                                              float rv2, int cb, unsigned short *rows, int lane,
+                                              float rv2, unsigned short *rows, int lane,
                                               int &k) {
   const float INF = __int_as_float(0x7f800000);
   const u64 XI = f2_pack(xe.x, xe.x), YI = f2_pack(xe.y, xe.y), ZI = f2_pack(xe.z, xe.z);
@@ -412,26 +415,23 @@ __device__ __forceinline__ void st_fast_group(const float4 *__restrict__ SA,
   for (int u8 = 0; u8 < 4; ++u8) {
     if (u8 >= ((gn + 7) >> 3)) break;
     // 8 candidates: loads first, then the arithmetic, then the appends
-    float4 a[4];
-    float4 z[2];
+    float4 a[4], z[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) a[q] = SA[(g >> 1) + 4 * u8 + q];
 #pragma unroll
-    for (int q = 0; q < 2; ++q) z[q] = reinterpret_cast<const float4 *>(SZ)[(g >> 2) + 2 * u8 + q];
+    for (int q = 0; q < 4; ++q) z[q] = SZ[(g >> 1) + 4 * u8 + q];
     float sd[8];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const float zl = (q & 1) ? z[q >> 1].z : z[q >> 1].x;
-      const float zh = (q & 1) ? z[q >> 1].w : z[q >> 1].y;
       u64 dx, dy, dz;
       if (PMI) {
         dx = f2_r4(f2_pack(a[q].x, a[q].y), xe.x, box.L[0], hx);
         dy = f2_r4(f2_pack(a[q].z, a[q].w), xe.y, box.L[1], hy);
-        dz = f2_r4(f2_pack(zl, zh), xe.z, box.L[2], hz);
+        dz = f2_r4(f2_pack(z[q].x, z[q].y), xe.z, box.L[2], hz);
       } else {
         dx = f2_sub(f2_pack(a[q].x, a[q].y), XI);
         dy = f2_sub(f2_pack(a[q].z, a[q].w), YI);
-        dz = f2_sub(f2_pack(zl, zh), ZI);
+        dz = f2_sub(f2_pack(z[q].x, z[q].y), ZI);
       }
       u64 s2 = f2_mul(dx, dx);
       s2 = f2_fma(dy, dy, s2);
@@ -439,28 +439,18 @@ __device__ __forceinline__ void st_fast_group(const float4 *__restrict__ SA,
       f2_unpack(s2, sd[2 * q], sd[2 * q + 1]);
     }
     // the hits only: a store with few active lanes costs one shared-memory
-    // wavefront and (almost) never a bank conflict
-    const int c0 = cb + g + 8 * u8;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t.reg .u32 v;\n\t"
-        "setp.lt.f32 p, %2, %10;\n\t@p st.shared.u16 [%0], %1;\n\t@p add.u32 %0, %0, 64;\n\t"
-        "add.u32 v, %1, 1;\n\t"
-        "setp.lt.f32 p, %3, %10;\n\t@p st.shared.u16 [%0], v;\n\t@p add.u32 %0, %0, 64;\n\t"
-        "add.u32 v, %1, 2;\n\t"
-        "setp.lt.f32 p, %4, %10;\n\t@p st.shared.u16 [%0], v;\n\t@p add.u32 %0, %0, 64;\n\t"
-        "add.u32 v, %1, 3;\n\t"
-        "setp.lt.f32 p, %5, %10;\n\t@p st.shared.u16 [%0], v;\n\t@p add.u32 %0, %0, 64;\n\t"
-        "add.u32 v, %1, 4;\n\t"
-        "setp.lt.f32 p, %6, %10;\n\t@p st.shared.u16 [%0], v;\n\t@p add.u32 %0, %0, 64;\n\t"
-        "add.u32 v, %1, 5;\n\t"
-        "setp.lt.f32 p, %7, %10;\n\t@p st.shared.u16 [%0], v;\n\t@p add.u32 %0, %0, 64;\n\t"
-        "add.u32 v, %1, 6;\n\t"
-        "setp.lt.f32 p, %8, %10;\n\t@p st.shared.u16 [%0], v;\n\t@p add.u32 %0, %0, 64;\n\t"
-        "add.u32 v, %1, 7;\n\t"
-        "setp.lt.f32 p, %9, %10;\n\t@p st.shared.u16 [%0], v;\n\t@p add.u32 %0, %0, 64;\n\t}"
-        : "+r"(bo)
-        : "r"(c0), "f"(sd[0]), "f"(sd[1]), "f"(sd[2]), "f"(sd[3]), "f"(sd[4]), "f"(sd[5]),
-          "f"(sd[6]), "f"(sd[7]), "f"(rv2));
+    // wavefront and (almost) never a bank conflict; the codes ride in Z.zw
+#define PM_APPEND(S, C)                                                                \
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %1, %3;\n\t"                      \
+               "@p st.shared.u16 [%0], %2;\n\t@p add.u32 %0, %0, 64;\n\t}"             \
+               : "+r"(bo)                                                              \
+               : "f"(S), "r"(__float_as_uint(C)), "f"(rv2))
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      PM_APPEND(sd[2 * q], z[q].z);
+      PM_APPEND(sd[2 * q + 1], z[q].w);
+    }
+#undef PM_APPEND
   }
   asm volatile("" ::: "memory");  // the C++ reads after this see the appends
   k = (int)((bo - rows_sa) >> 6);
@@ -476,7 +466,8 @@ __global__ void __launch_bounds__(stg::kWarps * 32, 5)
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char *wbase_s = smem_raw + (size_t)wid * Geo<RCH>::warp_bytes(wcap);
   float4 *SA = reinterpret_cast<float4 *>(wbase_s);
-  float2 *SZ = reinterpret_cast<float2 *>(wbase_s + kStage / 2 * 16);
+  float4 *SZ = reinterpret_cast<float4 *>(wbase_s + kStage / 2 * 16);
+  int *SELF = reinterpret_cast<int *>(wbase_s + kStage / 2 * 32);  // stage slot of lane's self
   int2 *PBE = reinterpret_cast<int2 *>(wbase_s + kStageBytes);
   float4 *PCS = reinterpret_cast<float4 *>(wbase_s + kStageBytes + NP * 8);
   float4 *POS = PCS + NP;
@@ -591,6 +582,22 @@ __global__ void __launch_bounds__(stg::kWarps * 32, 5)
     // clustered inputs): every segment appends straight to its global rows
     const StRows R{rows, grow, wcap == 0 || __any_sync(0xffffffffu, long_piece) != 0};
     __syncwarp();
+    // bounding box of the segment's particles: candidates farther than r_v
+    // (+1e-3) from it cannot be a neighbour of any lane and are not staged
+    // (the pinned test decides for the rest; the margin only keeps extras)
+    float bx0 = mine ? xi.x : INF, by0 = mine ? xi.y : INF, bz0 = mine ? xi.z : INF;
+    float bx1 = mine ? xi.x : -INF, by1 = mine ? xi.y : -INF, bz1 = mine ? xi.z : -INF;
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) {
+      bx0 = fminf(bx0, __shfl_xor_sync(0xffffffffu, bx0, o2));
+      by0 = fminf(by0, __shfl_xor_sync(0xffffffffu, by0, o2));
+      bz0 = fminf(bz0, __shfl_xor_sync(0xffffffffu, bz0, o2));
+      bx1 = fmaxf(bx1, __shfl_xor_sync(0xffffffffu, bx1, o2));
+      by1 = fmaxf(by1, __shfl_xor_sync(0xffffffffu, by1, o2));
+      bz1 = fmaxf(bz1, __shfl_xor_sync(0xffffffffu, bz1, o2));
+    }
+    const float rcull = sqrtf(rv2) + 1e-3f;
+    const float rcull2 = rcull * rcull;
     // stage iterator over the pieces: (p, o) = piece, offset inside it
     int p = 0;
     while (p < NP && PBE[p].x >= PBE[p].y) ++p;
@@ -607,22 +614,52 @@ __global__ void __launch_bounds__(stg::kWarps * 32, 5)
     while (p < NP) {
       const int2 be = PBE[p];
       const int jb = be.x + o;
-      const int cntc = min(kStage, be.y - jb);
+      const int craw = min(kStage, be.y - jb);
       const float4 csh = PCS[p], osh = POS[p];
       const int pmi = __float_as_int(csh.w);
       __syncwarp();  // the previous stage's readers are done
-      const int cnt8 = (cntc + 7) & ~7;  // the tail up to a multiple of 8 holds +inf
+      SELF[lane] = -1;
+      // the box in this piece's frame (own shift), the candidates in it
+      // (candidate shift); no culling along per-pair-R4 axes
+      const float lx0 = __fsub_rn(bx0, osh.x), lx1 = __fsub_rn(bx1, osh.x);
+      const float ly0 = __fsub_rn(by0, osh.y), ly1 = __fsub_rn(by1, osh.y);
+      const float lz0 = __fsub_rn(bz0, osh.z), lz1 = __fsub_rn(bz1, osh.z);
+      int cntc = 0;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int u = lane + 32 * q;
-        if (u < cnt8) {
-          float *a = reinterpret_cast<float *>(&SA[u >> 1]);
-          float *z = reinterpret_cast<float *>(&SZ[u >> 1]);
-          const bool v = u < cntc;
-          a[u & 1] = v ? __fsub_rn(pre[q].x, csh.x) : INF;
-          a[2 + (u & 1)] = v ? __fsub_rn(pre[q].y, csh.y) : INF;
-          z[u & 1] = v ? __fsub_rn(pre[q].z, csh.z) : INF;
+        const float cx = __fsub_rn(pre[q].x, csh.x), cy2 = __fsub_rn(pre[q].y, csh.y),
+                    cz2 = __fsub_rn(pre[q].z, csh.z);
+        const float ddx = (pmi & 1) ? 0.f : fmaxf(fmaxf(lx0 - cx, cx - lx1), 0.f);
+        const float ddy = (pmi & 2) ? 0.f : fmaxf(fmaxf(ly0 - cy2, cy2 - ly1), 0.f);
+        const float ddz = (pmi & 4) ? 0.f : fmaxf(fmaxf(lz0 - cz2, cz2 - lz1), 0.f);
+        const bool keep = u < craw && ddx * ddx + ddy * ddy + ddz * ddz < rcull2;
+        const unsigned km = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+          const int v = cntc + __popc(km & ((1u << lane) - 1u));
+          float *a = reinterpret_cast<float *>(&SA[v >> 1]);
+          float *z = reinterpret_cast<float *>(&SZ[v >> 1]);
+          a[v & 1] = cx;
+          a[2 + (v & 1)] = cy2;
+          z[v & 1] = cz2;
+          // the entry's code (piece, offset); rows appended straight to global
+          // memory carry the index itself (pieces may exceed the offset field)
+          z[2 + (v & 1)] = __uint_as_float(R.direct ? (unsigned)(jb + u)
+                                                    : (unsigned)((p << kOffBits) + o + u));
+          const int jj = jb + u - wbase;  // a warp's own particle: its self slot
+          if (jj >= 0 && jj < 32) SELF[jj] = v;
         }
+        cntc += __popc(km);
+      }
+      const int cnt8 = (cntc + 7) & ~7;  // the tail up to a multiple of 8 holds +inf
+      if (lane < cnt8 - cntc) {
+        const int v = cntc + lane;
+        float *a = reinterpret_cast<float *>(&SA[v >> 1]);
+        float *z = reinterpret_cast<float *>(&SZ[v >> 1]);
+        a[v & 1] = INF;
+        a[2 + (v & 1)] = INF;
+        z[v & 1] = INF;
+        z[2 + (v & 1)] = 0.f;
       }
       // advance and prefetch the next stage (overlaps this stage's tests)
       int pn = p, on = o + kStage;
@@ -644,7 +681,7 @@ __global__ void __launch_bounds__(stg::kWarps * 32, 5)
                                            __fsub_rn(xi.z, osh.z), 0.f)
                              : make_float4(INF, INF, INF, 0.f);
       const u64 XI = f2_pack(xe.x, xe.x), YI = f2_pack(xe.y, xe.y), ZI = f2_pack(xe.z, xe.z);
-      const int cb = (p << kOffBits) + o;  // code of the stage's first candidate
+      const int sslot = SELF[lane];  // this lane's own candidate in this stage (-1: none)
       for (int g = 0; g < cntc; g += 32) {
         const int gn = min(32, cntc - g);
         // (every store of the group, the +inf padding included, stays below cap)
@@ -653,12 +690,11 @@ __global__ void __launch_bounds__(stg::kWarps * 32, 5)
           // slot and the slot advances on a hit (no mask, no divergent
           // expansion); the +inf tail of the stage never hits
           const int k0 = k;
-          if (pmi) st_fast_group<true>(SA, SZ, g, gn, xe, P.box, pmi, rv2, cb, rows, lane, k);
-          else st_fast_group<false>(SA, SZ, g, gn, xe, P.box, 0, rv2, cb, rows, lane, k);
+          if (pmi) st_fast_group<true>(SA, SZ, g, gn, xe, P.box, pmi, rv2, rows, lane, k);
+          else st_fast_group<false>(SA, SZ, g, gn, xe, P.box, 0, rv2, rows, lane, k);
           // the particle itself (d2 = 0) was appended once: swap-remove it
-          const int jg = jb + g;
-          if (i >= jg && i < jg + gn) {
-            const unsigned short sc = (unsigned short)(cb + g + (i - jg));
+          if (mine && sslot >= g && sslot < g + gn) {
+            const unsigned short sc = (unsigned short)((p << kOffBits) + (i - PBE[p].x));
             for (int t = k0; t < k; ++t) {
               if (rows[(t << 5) + lane] == sc) {
                 rows[(t << 5) + lane] = rows[((k - 1) << 5) + lane];
@@ -675,7 +711,7 @@ __global__ void __launch_bounds__(stg::kWarps * 32, 5)
             const int v = g + u;
             const float *a = reinterpret_cast<const float *>(&SA[v >> 1]);
             const float *z = reinterpret_cast<const float *>(&SZ[v >> 1]);
-            const float4 xj = make_float4(a[v & 1], a[2 + (v & 1)], z[v & 1], 0.f);
+            const float4 xj = make_float4(a[v & 1], a[2 + (v & 1)], z[v & 1], 0.f);  // z.xy
             if (d2_of<false, true>(P, xe, make_float3(0.f, 0.f, 0.f), pmi, xj) < rv2)
               msk |= 1u << u;
           }
@@ -684,7 +720,7 @@ __global__ void __launch_bounds__(stg::kWarps * 32, 5)
           for (int q = 0; q < 16; ++q) {
             if (2 * q >= gn) break;
             const float4 a = SA[(g >> 1) + q];
-            const float2 z = SZ[(g >> 1) + q];
+            const float4 z = SZ[(g >> 1) + q];
             const u64 dx = f2_sub(f2_pack(a.x, a.y), XI);
             const u64 dy = f2_sub(f2_pack(a.z, a.w), YI);
             const u64 dz = f2_sub(f2_pack(z.x, z.y), ZI);
@@ -698,7 +734,7 @@ __global__ void __launch_bounds__(stg::kWarps * 32, 5)
           }
           if (gn < 32) msk &= (1u << gn) - 1u;
         }
-        st_expand<NMODE>(msk, jb + g, cb + g, i, cap, lane, R, k, gr);
+        st_expand<NMODE>(msk, SZ, g, PBE, mine ? sslot : -1, i, cap, lane, R, k, gr);
       }
       p = pn;
       o = on;
