@@ -95,9 +95,14 @@ pm_status pm_set_domain(pm_ctx ctx, const float lo[3], const float hi[3],
 pm_status pm_set_cutoff(pm_ctx ctx, float r_cut, float skin);
 
 /* Lennard-Jones parameters: V = 4 eps [(s/r)^12 - (s/r)^6];
- * mass of every particle; r_min > 0 selects the capped force of reading R22
- * (r_eff = max(r, r_min)), 0 the plain potential. */
-pm_status pm_set_lj(pm_ctx ctx, float epsilon, float sigma, float mass, float r_min);
+ * mass of every particle.  flags: PM_LJ_CAPPED selects the capped force of
+ * reading R22 (r_eff = max(r, r_min), BASELINE.json configs[4]); without it
+ * r_min must be 0 (the plain potential).  Errors: PM_E_INVAL for eps, sigma or
+ * mass <= 0, unknown flags, PM_LJ_CAPPED with r_min <= 0, or r_min != 0
+ * without PM_LJ_CAPPED. */
+enum { PM_LJ_CAPPED = 1 };
+pm_status pm_set_lj(pm_ctx ctx, float epsilon, float sigma, float mass, int32_t flags,
+                    float r_min);
 
 /* Half (Newton) neighbour lists, SURVEY §8(f) NEXT-1 ("compute
  * every interaction pair only once"; the symmetric cell/Verlet lists of

@@ -840,10 +840,13 @@ pm_status pm_set_cutoff(pm_ctx c, float r_cut, float skin) {
   return setup_grid(c);
 }
 
-pm_status pm_set_lj(pm_ctx c, float eps, float sigma, float mass, float r_min) {
+pm_status pm_set_lj(pm_ctx c, float eps, float sigma, float mass, int32_t flags, float r_min) {
   if (!c) return PM_E_INVAL;
-  if (!(eps > 0.f) || !(sigma > 0.f) || !(mass > 0.f) || !(r_min >= 0.f))
-    return set_err(c, PM_E_INVAL, "pm_set_lj: eps, sigma, mass must be > 0 and r_min >= 0");
+  if (!(eps > 0.f) || !(sigma > 0.f) || !(mass > 0.f))
+    return set_err(c, PM_E_INVAL, "pm_set_lj: eps, sigma, mass must be > 0");
+  if ((flags & ~PM_LJ_CAPPED) || ((flags & PM_LJ_CAPPED) ? !(r_min > 0.f) : r_min != 0.f))
+    return set_err(c, PM_E_INVAL,
+                   "pm_set_lj: PM_LJ_CAPPED needs r_min > 0; the plain potential r_min = 0");
   LJ &l = c->P.lj;
   const double s6 = std::pow((double)sigma, 6.0), s12 = s6 * s6;
   l.c12 = (float)(48.0 * eps * s12);

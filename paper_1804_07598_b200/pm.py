@@ -81,7 +81,7 @@ def lib(path: str = None):
         "pm_last_error": (C.c_char_p, [vp]),
         "pm_set_domain": (st, [vp, vp, vp, vp]),
         "pm_set_cutoff": (st, [vp, C.c_float, C.c_float]),
-        "pm_set_lj": (st, [vp, C.c_float, C.c_float, C.c_float, C.c_float]),
+        "pm_set_lj": (st, [vp, C.c_float, C.c_float, C.c_float, C.c_int32, C.c_float]),
         "pm_set_vlimit": (st, [vp, C.c_float]),
         "pm_set_sph": (st, [vp, C.POINTER(SPHParams)]),
         "pm_place": (st, [vp, C.c_int64, vp, vp, vp, vp, C.c_int32]),
@@ -228,7 +228,8 @@ class Context:
         self._rv = float(np.float32(np.float32(r_cut) + np.float32(skin)))
 
     def set_lj(self, epsilon=1.0, sigma=1.0, mass=1.0, r_min=0.0):
-        self._check(self.L.pm_set_lj(self.h, epsilon, sigma, mass, r_min))
+        flags = PM_LJ_CAPPED if r_min > 0 else 0  # reading R22's capped force
+        self._check(self.L.pm_set_lj(self.h, epsilon, sigma, mass, flags, r_min))
 
     def set_vlimit(self, vmax):
         self._check(self.L.pm_set_vlimit(self.h, vmax))
@@ -397,6 +398,7 @@ class Context:
         return dict(force_ms=fm.value, force_launches=fl.value, step_ms=sm.value, steps=ns.value)
 
 
+PM_LJ_CAPPED = 1
 PM_MSG_MIGRATE, PM_MSG_GHOST, PM_MSG_REFRESH, PM_MSG_REFRESH_PV = 0, 1, 2, 3
 PM_MSG_REFRESH_PVW, PM_MSG_MIGRATE_HIST = 4, 5
 PM_PHASE_PROLOGUE, PM_PHASE_STEP, PM_PHASE_FINAL, PM_PHASE_FORCES = 0, 1, 2, 3

@@ -951,3 +951,17 @@ def test_sph_run_graph_equals_host_loop(pm):
     assert ra["time"] == rb["time"]
     for k in ("pos", "vel", "rho", "gid"):
         assert np.array_equal(a[k], b[k]), k
+
+
+def test_set_lj_flags_contract(pm):
+    """pm_set_lj(flags, r_min): PM_LJ_CAPPED needs r_min > 0,
+    the plain potential r_min = 0, unknown flags are PM_E_INVAL."""
+    c = pm.Context()
+    L = pm.lib()
+    assert L.pm_set_lj(c.h, 1.0, 1.0, 1.0, 0, 0.0) == 0
+    assert L.pm_set_lj(c.h, 1.0, 1.0, 1.0, pm.PM_LJ_CAPPED, 0.8) == 0
+    assert L.pm_set_lj(c.h, 1.0, 1.0, 1.0, pm.PM_LJ_CAPPED, 0.0) == -1
+    assert L.pm_set_lj(c.h, 1.0, 1.0, 1.0, 0, 0.8) == -1
+    assert L.pm_set_lj(c.h, 1.0, 1.0, 1.0, 4, 0.0) == -1
+    assert L.pm_set_lj(c.h, -1.0, 1.0, 1.0, 0, 0.0) == -1
+    c.close()

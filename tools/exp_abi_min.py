@@ -15,7 +15,7 @@ L = C.CDLL(os.environ["PM_LIB"])
 vp = C.c_void_p
 for name, args in {"pm_opts_default": [vp], "pm_create": [vp, vp], "pm_set_domain": [vp, vp, vp, vp],
                    "pm_set_cutoff": [vp, C.c_float, C.c_float],
-                   "pm_set_lj": [vp, C.c_float, C.c_float, C.c_float, C.c_float],
+                   "pm_set_lj": [vp, C.c_float, C.c_float, C.c_float, C.c_int32, C.c_float],
                    "pm_place": [vp, C.c_int64, vp, vp, vp, vp, C.c_int32],
                    "pm_step_vv": [vp, C.c_float, C.c_int64, vp], "pm_set_profiling": [vp, C.c_int32],
                    "pm_get_profile": [vp, vp, vp, vp, vp]}.items():
@@ -30,7 +30,7 @@ f = lambda a, t=np.float32: np.ascontiguousarray(a, t)
 lo, hi, per = f(s.lo), f(s.hi), f(s.periodic, np.int32)
 assert L.pm_set_domain(h, lo.ctypes.data, hi.ctypes.data, per.ctypes.data) == 0
 assert L.pm_set_cutoff(h, 2.5, 0.3) == 0
-assert L.pm_set_lj(h, 1.0, 1.0, 1.0, 0.0) == 0
+assert L.pm_set_lj(h, 1.0, 1.0, 1.0, 0, 0.0) == 0
 pos, vel, gid = f(s.pos), f(s.vel), f(s.gid, np.int64)
 assert L.pm_place(h, s.n, pos.ctypes.data, vel.ctypes.data, gid.ctypes.data, None, 0) == 0
 rs = RunStats()
