@@ -20,14 +20,19 @@
  *    reorganise (§2: "Cell Lists [45] or Verlet Lists [46] ...
  *    reduces the computational cost to O(N)").
  *
- * Pins: tests/test_oracle_pins.py.  The Eq. 5 viscosity VALUE is pinned by a
- * hand-computed pair (tests/golden/sph_viscosity_pair.txt), the virial by a
- * closed form and the dilation identity W = -dU_s/dlambda, the image shifts
- * by reconstruction of the minimum image.  Parts with no independent pin say
- * "parity unpinned" below: the CHOICE of the viscosity constants alpha, eta
- * (R20: the paper gives none; the formula with them is pinned), the SPH time
- * stepping scheme beyond its self-consistency pins (R26-R28) and the DEM
- * wall model beyond its closed-form pins (R33).
+ * Pins: tests/test_oracle_pins.py -- every function below has at least one
+ * pin that does not re-type it.  The Eq. 5 viscosity VALUE is pinned by a
+ * hand-computed pair (tests/golden/sph_viscosity_pair.txt; the constants
+ * alpha, eta are inputs -- their values are reading R20, the paper gives
+ * none), the virial by a closed form and the dilation identity
+ * W = -dU_s/dlambda, the image shifts by reconstruction of the minimum image,
+ * the CPU method (orc_md_cells_run) by the brute-force trajectory.  Partly
+ * pinned (the pins cover some terms only, noted at the function): the SPH
+ * time stepping (R26-R28: exact free fall fixes the x and v updates of both
+ * the Verlet and the Euler step, the continuity sign and momentum; the
+ * coefficient of the density update is not separately fixed) and the DEM
+ * wall model (R33: the normal wall force by the Hertz resting depth; the
+ * walls have no tangential friction by reading).
  */
 #include <math.h>
 #include <stdint.h>
