@@ -965,3 +965,47 @@ def test_set_lj_flags_contract(pm):
     assert L.pm_set_lj(c.h, 1.0, 1.0, 1.0, 4, 0.0) == -1
     assert L.pm_set_lj(c.h, -1.0, 1.0, 1.0, 0, 0.0) == -1
     c.close()
+
+
+@pytest.mark.parametrize("seed", list(range(12)))
+def test_verlet_randomised_boxes_and_clusters(pm, orc, seed):
+    """Randomised stress of the staged build (bounding-box culling, seam
+    pieces with own / candidate shifts, per-pair R4 rows, shared-memory and
+    direct rows): random box shapes from 3 r_v to 8 r_v per axis, random
+    periodicity, uniform or clustered (a dense blob over a dilute gas, up to
+    ~200 per cell) particles, some placed on faces and at hi - ulp; every row
+    equals the oracle's O(N^2) set, and the list is symmetric."""
+    rng = np.random.default_rng(1000 + seed)
+    rv = float(rv32(2.5, 0.3))
+    ext = rng.uniform(3.05, 8.0, 3) * rv
+    per = rng.integers(0, 2, 3).astype(np.int32)
+    n = int(rng.integers(300, 2500))
+    x = rng.uniform(0.0, 1.0, (n, 3)) * ext
+    if seed % 3 == 0:  # a dense cluster
+        m = n // 3
+        x[:m] = ext * 0.5 + rng.normal(0.0, 0.6, (m, 3))
+        x = np.clip(x, 0.0, ext * (1 - 1e-6))
+    if seed % 4 == 1:  # faces and hi - ulp
+        k = n // 10
+        ax = rng.integers(0, 3, k)
+        x[np.arange(k), ax] = np.where(rng.random(k) < 0.5, 0.0,
+                                       np.nextafter(np.float32(ext[ax]), np.float32(0)))
+    pos = np.zeros((n, 4), np.float32)
+    pos[:, :3] = x.astype(np.float32)
+    hi = ext.astype(np.float32)
+    pos[:, :3] = np.minimum(pos[:, :3], np.nextafter(hi, np.float32(0)))
+    s = inputs.System(pos=pos, vel=np.zeros_like(pos), gid=np.arange(n, dtype=np.int64),
+                      lo=np.zeros(3, np.float32), hi=hi, periodic=per, params={})
+    c = make_ctx(pm, s)
+    c.build_verlet()
+    rp, col = c.get_verlet()
+    st = c.get_state()
+    rrp, rcols, _ = orc.verlet_rows(s.pos, s.lo, s.hi, s.periodic, rv32(2.5, 0.3),
+                                    rows=st["gid"], want_shift=False)
+    bad = _row_sets_equal(rp, col, st["gid"], rrp, rcols, s.gid)
+    assert bad < 0, f"row {bad} differs (seed {seed})"
+    # symmetry of the gid pair sets
+    rows = np.repeat(st["gid"], np.diff(rp))
+    a = set(zip(rows.tolist(), col.tolist()))
+    assert all((j, i) in a for (i, j) in a)
+    c.close()
