@@ -85,9 +85,8 @@ L.append("k_lj_step: bound by L1/tex data-pipe wavefronts of its scattered float
          "paired fp32 tests, predicated appends into 16-bit shared-memory rows, full-line "
          "flushes (no write amplification).  k_sph_rates / k_dem_step as in round 1.\n")
 L.append("## Launch list (`PM_USE_GRAPHS=0 ncu --metrics gpu__time_duration.sum --clock-control "
-         "none` of `python bench.py --steps 200 --warmup 10 --no-cpu-baseline`; cold-cache, "
-         "serialised: compare shares; the SPH and DEM kernels come from the bench's `sph` and "
-         "`dem` extras)\n")
+         "none` of `python bench.py --steps 200 --warmup 10 --no-cpu-baseline --no-extras`: the "
+         "cfg2 step alone; cold-cache, serialised: compare shares)\n")
 L.append(launches)
 open(os.path.join(P, f"{TAG}_ncu_summary.md"), "w").write("\n".join(L))
 print("\n".join(L[:12]))
