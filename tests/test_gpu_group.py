@@ -231,3 +231,22 @@ def test_bench_native_single_rank(env):
     b = json.loads(lines[0])
     assert b["n_gpus"] == 1 and b["config"]["n_particles"] == 32 ** 3
     assert b["value"] > 0 and b["e2e"]["value"] > 0 and b["roofline"]["frac"] > 0
+
+
+def test_group_cfg3_full_size_222(env):
+    """BJ configs[2] at full size on the 2x2x2 grid through the C-ABI group
+    (8 sub-domains of one 128^3 block each = 16,777,216 particles on this
+    GPU, placed on member 0 and distributed by pm_map): every particle owned
+    once, sampled rows (gid sets, ghosts included) and forces of every
+    sub-domain against the fp64 oracle on the global system, then 5 steps."""
+    pm = env
+    grid = (2, 2, 2)
+    s = inputs.cfg3_global(grid)
+    members = make_group(pm, s, grid)
+    forces(members)
+    check_against_oracle(pm, members, s, nrow=24, seed=8)
+    out = [c.dist_run(0.005, 5) for c in members][-1]
+    assert out["steps"] == 5
+    assert sum(c.count()["n_owned"] for c in members) == s.n
+    for c in members:
+        c.close()
