@@ -1,6 +1,8 @@
 """Minimal-ABI timing of cfg2 steps for A/B runs against older library builds
 (declares only the calls it uses, so a libpm.so from an earlier commit
-loads).  Usage: PM_LIB=path python tools/exp_abi_min.py"""
+loads).  Usage: PM_LIB=path python tools/exp_abi_min.py; build the older
+library in a worktree: `git worktree add /tmp/old <commit>` and
+`build.build()` there (exp_libs/ is only a scratch place for such copies)."""
 import ctypes as C
 import os
 import sys

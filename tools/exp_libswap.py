@@ -1,6 +1,8 @@
 """Experiment driver: run tools/prof_step.py-like cfg2 steps with an alternative
 libpm.so (path in PM_LIB) and print the force-kernel time from the bench's
-in-graph event profile."""
+in-graph event profile.  An older library for the A/B: `git worktree add
+/tmp/old <commit> && (cd /tmp/old && python -c "from paper_1804_07598_b200
+import build; build.build()")`, then PM_LIB=/tmp/old/paper_1804_07598_b200/libpm.so."""
 import os
 import sys
 
