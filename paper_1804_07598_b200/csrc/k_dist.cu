@@ -402,6 +402,38 @@ void launch_dist_unpack(const Bufs &B, int what, const void *in, int nrecv, int 
   if (nrecv > 0) k_dist_unpack<<<nb(nrecv), 256, 0, s>>>(B, what, in, nrecv, base);
 }
 
+// Slice classes of a decomposed context after a build (§3.6
+// "interior and ghost iterators ... overlapping communication with
+// computation"): a 32-row slice is interior (0) when none of its particles
+// is a ghost or lies within the ghost width r_g of a decomposed face of the
+// sub-domain -- its rows (built with r_v <= r_g) then hold owned partners
+// only, so its forces can run while the ghost refresh is in flight;
+// otherwise boundary (1).
+__global__ void k_warp_class(Dist D, Bufs B, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if ((i >> 5) >= ((n + 31) >> 5)) return;  // whole warp
+  State *st = B.st;
+  bool near = false;
+  if (i < n) {
+    if (B.kind[st->cur_id][i] & kGhostBit) {
+      near = true;
+    } else {
+      const float4 x = B.pos[st->cur_pv][i];
+      const float c[3] = {x.x, x.y, x.z};
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+        if (D.p[d] > 1)
+          near |= (c[d] - D.slo[d] < D.rg) || (D.shi[d] - c[d] <= D.rg);
+    }
+  }
+  const bool b = __any_sync(0xffffffffu, near);
+  if ((threadIdx.x & 31) == 0) B.wclass[i >> 5] = b ? 1 : 0;
+}
+
+void launch_warp_class(const Dist &D, const Bufs &B, int64_t n, cudaStream_t s) {
+  if (n > 0) k_warp_class<<<nb(n), 256, 0, s>>>(D, B, (int)n);
+}
+
 void launch_dist_remap(const int *invperm, int *send_idx, int nsend, int *ghost_slot, int nghost,
                        int n_owned, cudaStream_t s) {
   const int m = nsend > nghost ? nsend : nghost;

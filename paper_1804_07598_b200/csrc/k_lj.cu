@@ -323,12 +323,20 @@ __device__ __forceinline__ void vv_epilogue(const Params &P, const Bufs &B, Stat
 //         x' = wrap(x + dt v); displacement test vs xref; -> alternate buffers
 //  final: F(x); v += dt/2 F/m; F stored; x copied  -> alternate buffers
 template <bool CAPPED, bool PEER = false>
-__global__ void __launch_bounds__(256) k_lj_step(Params P, Bufs B, int n, float dt, int mode_arg) {
+__global__ void __launch_bounds__(256) k_lj_step(Params P, Bufs B, int n, float dt, int mode_arg,
+                                                 int wphase) {
   State *st = B.st;
   if (st->abort) return;
   const int mode = mode_arg >= 0 ? mode_arg : st->mode;
   const int cp = st->cur_pv;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (wphase >= 0) {  // one half of an overlapped step: interior or boundary slices
+    if (wphase == 1 && blockIdx.x == 0 && threadIdx.x == 0) {
+      st->pending_flip = 1;
+      st->steps_done += 1;
+    }
+    if ((i >> 5) >= ((n + 31) >> 5) || B.wclass[i >> 5] != wphase) return;  // whole warp
+  }
   const bool active = i < n;
   const float4 *__restrict__ pos = B.pos[cp];
   const float4 xi = active ? pos[i] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -336,7 +344,7 @@ __global__ void __launch_bounds__(256) k_lj_step(Params P, Bufs B, int n, float 
   bool far = false;
   vv_epilogue<PEER>(P, B, st, i, active, xi, a, dt, mode, cp, far);
   if (__any_sync(0xffffffffu, far) && (threadIdx.x & 31) == 0) st->need_rebuild = 1;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (wphase < 0 && blockIdx.x == 0 && threadIdx.x == 0) {
     st->pending_flip = 1;
     st->steps_done += 1;
   }
@@ -578,7 +586,7 @@ void launch_lj_half_integrate(const Params &P, const Bufs &B, int64_t n, float d
 }
 
 void launch_lj_step_mode(const Params &P, const Bufs &B, int64_t n, float dt, int mode,
-                         cudaStream_t s) {
+                         cudaStream_t s, int wphase) {
   if (n <= 0) {
     k_empty_step<<<1, 1, 0, s>>>(B.st, 1);
     return;
@@ -589,12 +597,14 @@ void launch_lj_step_mode(const Params &P, const Bufs &B, int64_t n, float dt, in
     return;
   }
   if (P.peer_n > 0) {  // decomposed run with the fused ghost refresh
-    if (P.lj.r_min > 0.f) k_lj_step<true, true><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode);
-    else k_lj_step<false, true><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode);
+    if (P.lj.r_min > 0.f)
+      k_lj_step<true, true><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode, wphase);
+    else
+      k_lj_step<false, true><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode, wphase);
     return;
   }
-  if (P.lj.r_min > 0.f) k_lj_step<true><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode);
-  else k_lj_step<false><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode);
+  if (P.lj.r_min > 0.f) k_lj_step<true><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode, wphase);
+  else k_lj_step<false><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode, wphase);
 }
 
 void launch_lj_step(const Params &P, const Bufs &B, int64_t n, float dt, cudaStream_t s) {

@@ -356,6 +356,8 @@ pm_status upload_layout(pm_ctx c, const std::vector<int64_t> &width) {
   }
   if (ns + 1 > c->slice_cap) {
     CUDA_TRY(c, dalloc(&c->B.slice_off, ns + 1));
+    CUDA_TRY(c, dalloc(&c->B.wclass, ns + 1));
+    CUDA_TRY(c, cudaMemsetAsync(c->B.wclass, 1, ns + 1, c->stream));  // boundary until classified
     c->slice_cap = ns + 1;
     destroy_graph(c);
   }
@@ -691,6 +693,25 @@ bool ctx_ready(pm_ctx c) { return c->have_domain && c->have_cutoff; }
 pm_status ctx_error(pm_ctx c, pm_status code, const char *msg) {
   return set_err(c, code, "%s", msg);
 }
+// One half of an overlapped decomposed step (wphase 0: interior slices, 1:
+// boundary slices, which also does the step's bookkeeping) on `s`.
+pm_status ctx_step_half(pm_ctx c, float dt, int final_step, int wphase, cudaStream_t s) {
+  if (!c->list_valid || c->P.newton || c->P.peer_n > 0)
+    return set_err(c, PM_E_STATE, "overlapped step: needs full lists, no fused refresh");
+  launch_lj_step_mode(c->P, c->B, c->n, dt, final_step ? kModeFinal : kModeInner, s, wphase);
+  if (wphase == 1) {
+    k_apply_pending<<<1, 1, 0, s>>>(c->B.st);
+    c->forces_valid = final_step != 0;
+  }
+  return check_launch(c, "overlapped step");
+}
+// The positions-only ghost refresh unpack on another stream (the overlap's
+// communication stream).
+pm_status ctx_refresh_unpack_on(pm_ctx c, const void *recv, cudaStream_t s) {
+  if (c->n_ghost > 0 && !recv) return set_err(c, PM_E_INVAL, "null buffer");
+  launch_refresh_unpack(c->B, c->d_gslot, (int)c->n_ghost, recv, s);
+  return check_launch(c, "refresh unpack");
+}
 // device address of the (need_rebuild, abort) pair of the state (adjacent ints)
 int *ctx_flag_ptr(pm_ctx c) { return &c->B.st->need_rebuild; }
 bool ctx_profiling(pm_ctx c) { return c->profiling; }
@@ -780,7 +801,8 @@ void pm_destroy(pm_ctx c) {
     cudaFree(B.kind[b]);
   }
   void *ptrs[] = {B.xref, B.force, B.rhoP[0], B.rhoP[1], B.vold[0], B.vold[1], B.drho, B.cell_of, B.slot, B.count, B.start, B.perm,
-                  B.sorttmp, B.scan_tmp, B.nbr, B.cnt, B.st, B.slice_off, B.big_cells};
+                  B.sorttmp, B.scan_tmp, B.nbr, B.cnt, B.st, B.slice_off, B.big_cells,
+                  B.wclass};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   void *dem_ptrs[] = {B.omega[0], B.omega[1], B.torque, B.hist, B.hist_old, B.nbr_old,
@@ -1807,6 +1829,7 @@ pm_status dist_finish_complete(pm_ctx c) {
   if ((s = ensure_dev(c, &c->d_gslot, c->gslot_cap, c->n_ghost + 1))) return s;
   launch_dist_remap(c->B.invperm, c->d_send_idx, (int)c->n_send, c->d_gslot, (int)c->n_ghost,
                     (int)c->n_owned, c->stream);
+  launch_warp_class(c->D, c->B, c->n, c->stream);  // interior / boundary slices
   c->P.peer_n = 0;  // new send lists and ghost slots: pm_dist_peer_setup again
   if (c->P.dem_state) {  // contact histories onto the new rows (stayers and arrivals)
     if ((s = dem_alloc(c, false))) return s;

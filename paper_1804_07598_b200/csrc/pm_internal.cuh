@@ -167,6 +167,8 @@ struct Bufs {
   struct State *st;    // device-resident state
   int32_t *ps_off;     // fused refresh: per local particle, its destinations
   int2 *ps_dst;        //   ps_dst[ps_off[i] .. ps_off[i+1]) = (peer, ghost slot)
+  uint8_t *wclass;     // decomposed contexts, per 32-row slice: 1 if a row of it may
+                       // have ghost partners (boundary), 0 interior (k_warp_class)
 };
 
 // Device-resident mutable state (one per context).
@@ -384,8 +386,12 @@ void launch_lj_half_forces(const Params &P, const Bufs &B, int64_t n, int want_e
 void launch_lj_half_integrate(const Params &P, const Bufs &B, int64_t n, float dt, int mode,
                               cudaStream_t s);
 void launch_ghost_put(const Bufs &B, int pack, const int *idx, int m, void *buf, cudaStream_t s);
+void launch_warp_class(const Dist &D, const Bufs &B, int64_t n, cudaStream_t s);
+// wphase: -1 every row; 0 / 1 only the slices whose wclass is 0 (interior) /
+// 1 (boundary) -- the two halves of an overlapped step (the second one does
+// the step's bookkeeping)
 void launch_lj_step_mode(const Params &P, const Bufs &B, int64_t n, float dt, int mode,
-                         cudaStream_t s);
+                         cudaStream_t s, int wphase = -1);
 int dist_record_bytes(int what);
 void launch_dist_plan(const Params &P, const Bufs &B, const Dist &D, int n_owned, int what,
                       uint32_t *mask, int *blk_counts, const int *order, int *dir_base,

@@ -104,14 +104,19 @@ def test_group_map_ghost_get_vs_oracle(env, grid, via_nccl):
         c.close()
 
 
-@pytest.mark.parametrize("grid,via_nccl", [((2, 1, 1), False), ((2, 2, 2), False),
-                                           ((2, 1, 1), True)])
-def test_group_run_matches_single_context(env, grid, via_nccl):
+@pytest.mark.parametrize("grid,via_nccl,mode", [
+    ((2, 1, 1), False, "fused"), ((2, 2, 2), False, "fused"), ((2, 1, 1), True, "fused"),
+    ((2, 2, 2), False, "overlap"), ((2, 1, 1), True, "overlap"), ((2, 2, 1), False, "plain")])
+def test_group_run_matches_single_context(env, grid, via_nccl, mode, monkeypatch):
     """40 NVE steps through pm_dist_run (rebuilds = pm_map + pm_ghost_get,
     per-step ghost refresh, MAX-reduced rebuild flag) against pm_step_vv on
     one context: positions, velocities and global thermo agree (fp32
-    summation order only)."""
+    summation order only).  Refresh modes: fused into the sweep (default
+    in-process), message exchange overlapped with the interior slices'
+    forces (§3.6; opt-in, PM_GROUP_OVERLAP=1), plain message."""
     pm = env
+    monkeypatch.setenv("PM_GROUP_FUSED", "1" if mode == "fused" else "0")
+    monkeypatch.setenv("PM_GROUP_OVERLAP", "1" if mode == "overlap" else "0")
     s = inputs.lj_lattice_system(24, 24, 24, jitter_key=(52,), vel_key=(152,))
     ref = pm.Context()
     ref.set_domain(s.lo, s.hi, s.periodic)
