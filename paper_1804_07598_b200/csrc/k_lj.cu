@@ -39,19 +39,18 @@ __device__ __forceinline__ float r4_delta(float a, float b, float L, float halfL
 
 // One pair, branch-free: the contribution is selected to zero when the pair
 // is outside r_cut (R6) or the slot is padding (valid == false).
-template <bool MI, bool CAPPED, bool ENERGY, bool MASK>
+// MIM: bit d set = R4 on axis d (the warp has a row near a periodic face
+// of axis d); the other axes take the plain difference, which R4 reduces to
+// there (|e| <= L/2 for every listed pair of such rows).
+template <int MIM, bool CAPPED, bool ENERGY, bool MASK>
 __device__ __forceinline__ void lj_pair(const Params &P, const float4 &xi, const float4 &xj,
                                         bool valid, Acc &a) {
-  float dx, dy, dz;
-  if (MI) {
-    dx = P.box.per[0] ? r4_delta(xi.x, xj.x, P.box.L[0], P.box.halfL[0]) : __fsub_rn(xj.x, xi.x);
-    dy = P.box.per[1] ? r4_delta(xi.y, xj.y, P.box.L[1], P.box.halfL[1]) : __fsub_rn(xj.y, xi.y);
-    dz = P.box.per[2] ? r4_delta(xi.z, xj.z, P.box.L[2], P.box.halfL[2]) : __fsub_rn(xj.z, xi.z);
-  } else {
-    dx = __fsub_rn(xj.x, xi.x);
-    dy = __fsub_rn(xj.y, xi.y);
-    dz = __fsub_rn(xj.z, xi.z);
-  }
+  const float dx = (MIM & 1) ? r4_delta(xi.x, xj.x, P.box.L[0], P.box.halfL[0])
+                             : __fsub_rn(xj.x, xi.x);
+  const float dy = (MIM & 2) ? r4_delta(xi.y, xj.y, P.box.L[1], P.box.halfL[1])
+                             : __fsub_rn(xj.y, xi.y);
+  const float dz = (MIM & 4) ? r4_delta(xi.z, xj.z, P.box.L[2], P.box.halfL[2])
+                             : __fsub_rn(xj.z, xi.z);
   const float d2 = dist2(dx, dy, dz);
   const bool in = (MASK ? valid : true) && (d2 < P.lj.rc2);
   float f, r6i;
@@ -97,20 +96,20 @@ __device__ __forceinline__ Idx4 ld_idx4(const int *__restrict__ p) {
   return r;
 }
 
-template <bool MI, bool CAPPED, bool ENERGY, bool MASK>
+template <int MIM, bool CAPPED, bool ENERGY, bool MASK>
 __device__ __forceinline__ void lj_group(const Params &P, const float4 *__restrict__ pos,
                                          const Idx4 &j, int rem, const float4 &xi, Acc &a) {
   const float4 x0 = __ldg(pos + j.a);
   const float4 x1 = __ldg(pos + j.b);
   const float4 x2 = __ldg(pos + j.c);
   const float4 x3 = __ldg(pos + j.d);
-  lj_pair<MI, CAPPED, ENERGY, false>(P, xi, x0, true, a);
-  lj_pair<MI, CAPPED, ENERGY, MASK>(P, xi, x1, rem > 1, a);
-  lj_pair<MI, CAPPED, ENERGY, MASK>(P, xi, x2, rem > 2, a);
-  lj_pair<MI, CAPPED, ENERGY, MASK>(P, xi, x3, rem > 3, a);
+  lj_pair<MIM, CAPPED, ENERGY, false>(P, xi, x0, true, a);
+  lj_pair<MIM, CAPPED, ENERGY, MASK>(P, xi, x1, rem > 1, a);
+  lj_pair<MIM, CAPPED, ENERGY, MASK>(P, xi, x2, rem > 2, a);
+  lj_pair<MIM, CAPPED, ENERGY, MASK>(P, xi, x3, rem > 3, a);
 }
 
-template <bool MI, bool CAPPED, bool ENERGY>
+template <int MIM, bool CAPPED, bool ENERGY>
 __device__ __forceinline__ void lj_row(const Params &P, const float4 *__restrict__ pos,
                                        const int *__restrict__ nb, int cnt, const float4 &xi,
                                        Acc &a) {
@@ -124,17 +123,17 @@ __device__ __forceinline__ void lj_row(const Params &P, const float4 *__restrict
   for (; g + 2 <= nfull; g += 2) {
     const Idx4 j2 = (g + 2 < ng) ? ld_idx4(nb + (g + 2) * 128) : j1;
     const Idx4 j3 = (g + 3 < ng) ? ld_idx4(nb + (g + 3) * 128) : j1;
-    lj_group<MI, CAPPED, ENERGY, false>(P, pos, j0, 4, xi, a);
-    lj_group<MI, CAPPED, ENERGY, false>(P, pos, j1, 4, xi, a);
+    lj_group<MIM, CAPPED, ENERGY, false>(P, pos, j0, 4, xi, a);
+    lj_group<MIM, CAPPED, ENERGY, false>(P, pos, j1, 4, xi, a);
     j0 = j2;
     j1 = j3;
   }
   if (g < nfull) {
-    lj_group<MI, CAPPED, ENERGY, false>(P, pos, j0, 4, xi, a);
+    lj_group<MIM, CAPPED, ENERGY, false>(P, pos, j0, 4, xi, a);
     j0 = j1;
     ++g;
   }
-  if (g < ng) lj_group<MI, CAPPED, ENERGY, true>(P, pos, j0, cnt - 4 * g, xi, a);
+  if (g < ng) lj_group<MIM, CAPPED, ENERGY, true>(P, pos, j0, cnt - 4 * g, xi, a);
 }
 
 __device__ __forceinline__ bool near_periodic_face(const Params &P, const float4 &x) {
@@ -148,19 +147,37 @@ __device__ __forceinline__ bool near_periodic_face(const Params &P, const float4
   return near;
 }
 
+// The periodic axes along which the warp has a row within r_v + skin of a
+// face (bit d for axis d; warp-uniform): only those axes need R4's
+// minimum-image selection, the others reduce to the plain difference.
+__device__ __forceinline__ int warp_mi_axes(const Params &P, bool active, const float4 &x) {
+  int m = 0;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const float v = (d == 0) ? x.x : (d == 1) ? x.y : x.z;
+    if (active && P.box.per[d] &&
+        (v < P.box.lo[d] + P.mi_margin || v >= P.box.hi[d] - P.mi_margin))
+      m |= 1 << d;
+  }
+  return __reduce_or_sync(0xffffffffu, (unsigned)m);
+}
+
 template <bool CAPPED, bool ENERGY>
 __device__ __forceinline__ Acc lj_force_of(const Params &P, const Bufs &B,
                                            const float4 *__restrict__ pos, int i, bool active,
                                            const float4 &xi) {
   Acc a = {0.f, 0.f, 0.f, 0.f, 0.f, 0};
-  const bool mi = __any_sync(0xffffffffu, active && near_periodic_face(P, xi));
+  const int mim = warp_mi_axes(P, active, xi);
   if (active) {
     const int cnt = B.cnt[i];
     const int *nb = B.nbr + nbr_row_base(B, i);
-    if (mi)
-      lj_row<true, CAPPED, ENERGY>(P, pos, nb, cnt, xi, a);
-    else
-      lj_row<false, CAPPED, ENERGY>(P, pos, nb, cnt, xi, a);
+    switch (mim) {  // warp-uniform
+      case 0: lj_row<0, CAPPED, ENERGY>(P, pos, nb, cnt, xi, a); break;
+      case 1: lj_row<1, CAPPED, ENERGY>(P, pos, nb, cnt, xi, a); break;
+      case 2: lj_row<2, CAPPED, ENERGY>(P, pos, nb, cnt, xi, a); break;
+      case 4: lj_row<4, CAPPED, ENERGY>(P, pos, nb, cnt, xi, a); break;
+      default: lj_row<7, CAPPED, ENERGY>(P, pos, nb, cnt, xi, a); break;  // edges, corners
+    }
   }
   return a;
 }
@@ -323,7 +340,7 @@ __device__ __forceinline__ void vv_epilogue(const Params &P, const Bufs &B, Stat
 //         x' = wrap(x + dt v); displacement test vs xref; -> alternate buffers
 //  final: F(x); v += dt/2 F/m; F stored; x copied  -> alternate buffers
 template <bool CAPPED, bool PEER = false>
-__global__ void __launch_bounds__(256) k_lj_step(Params P, Bufs B, int n, float dt, int mode_arg,
+__global__ void __launch_bounds__(256, PEER ? 5 : 6) k_lj_step(Params P, Bufs B, int n, float dt, int mode_arg,
                                                  int wphase) {
   State *st = B.st;
   if (st->abort) return;
