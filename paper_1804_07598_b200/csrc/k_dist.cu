@@ -165,11 +165,14 @@ __global__ void __launch_bounds__(kDirBlock) k_dist_fill(const uint32_t *__restr
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t m = (i < n) ? mask[i] : 0u;
   const unsigned lt = (1u << lane) - 1u;
-  int rank_in_warp[27];
-#pragma unroll
-  for (int d = 0; d < 27; ++d) {
+  // only the directions present in the warp (usually "stay" plus a face or
+  // two) need a ballot; the others count zero
+  if (lane < 27) wsum[lane][w] = 0;
+  uint32_t wm = __reduce_or_sync(0xffffffffu, m);
+  while (wm) {
+    const int d = __ffs(wm) - 1;
+    wm &= wm - 1;
     const unsigned b = __ballot_sync(0xffffffffu, (m >> d) & 1u);
-    rank_in_warp[d] = __popc(b & lt);
     if (lane == 0) wsum[d][w] = __popc(b);
   }
   __syncthreads();
@@ -182,10 +185,13 @@ __global__ void __launch_bounds__(kDirBlock) k_dist_fill(const uint32_t *__restr
     }
   }
   __syncthreads();
-#pragma unroll
-  for (int d = 0; d < 27; ++d) {
+  wm = __reduce_or_sync(0xffffffffu, m);
+  while (wm) {
+    const int d = __ffs(wm) - 1;
+    wm &= wm - 1;
+    const unsigned b = __ballot_sync(0xffffffffu, (m >> d) & 1u);
     if ((m >> d) & 1u)
-      list[dir_base[d] + blk_off[blockIdx.x * 27 + d] + wsum[d][w] + rank_in_warp[d]] = i;
+      list[dir_base[d] + blk_off[blockIdx.x * 27 + d] + wsum[d][w] + __popc(b & lt)] = i;
   }
 }
 

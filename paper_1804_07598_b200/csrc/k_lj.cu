@@ -340,7 +340,7 @@ __device__ __forceinline__ void vv_epilogue(const Params &P, const Bufs &B, Stat
 //         x' = wrap(x + dt v); displacement test vs xref; -> alternate buffers
 //  final: F(x); v += dt/2 F/m; F stored; x copied  -> alternate buffers
 template <bool CAPPED, bool PEER = false>
-__global__ void __launch_bounds__(256, PEER ? 5 : 6) k_lj_step(Params P, Bufs B, int n, float dt, int mode_arg,
+__global__ void __launch_bounds__(256, 6) k_lj_step(Params P, Bufs B, int n, float dt, int mode_arg,
                                                  int wphase) {
   State *st = B.st;
   if (st->abort) return;

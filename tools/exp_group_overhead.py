@@ -2,7 +2,8 @@
 pm_dist_run) on ONE GPU: the cfg3 global system of grid g (one m^3 block per
 sub-domain) run decomposed vs whole on one context, ms per step over K steps
 (CUDA events on the shared stream), plus the sweep share (profiling pass).
-Usage: python tools/exp_group_overhead.py [m] [K] [gx gy gz]"""
+Usage: python tools/exp_group_overhead.py [m] [K] [gx gy gz]
+(GROUP_ONLY=1 / SINGLE_ONLY=1: one of the two runs)"""
 import os
 import sys
 import time
@@ -40,6 +41,9 @@ if not os.environ.get("GROUP_ONLY"):
     c.step_vv(0.005, 10)
     ms1, _, r1 = timed(lambda: c.step_vv(0.005, K))
     c.close()
+    if os.environ.get("SINGLE_ONLY"):  # (for a launch list of the single context)
+        print(f"one context {ms1 / K:.3f} ms/step ({r1['rebuilds']} rebuilds)")
+        sys.exit(0)
 mem = pm.create_dist_local(grid, stream=stream.cuda_stream)
 for k, x in enumerate(mem):
     x.set_domain(s.lo, s.hi, s.periodic)
