@@ -80,8 +80,11 @@ for k, rs in caps.items():
     L.append("| %s | %d | " % (k, len(rs)) + " | ".join(
         ("%.4g" % m[c]) if c != "inst" else ("%.4g" % m[c]) for c in cols) + " |")
 L.append("")
-L.append("k_lj_step: bound by L1/tex data-pipe wavefronts of its scattered float4 neighbour "
-         "gathers (see DESIGN.md §11).  k_verlet_st (staged build): coalesced candidate stages, "
+L.append("k_lj_step: the L1 data pipe is busy with the scattered float4 gathers, but it is not "
+         "the bound alone: the gather-order microbenchmark (tools/micro/gather_order.cu, "
+         "DESIGN.md §11) cuts L1 wavefronts by 21%% for a 2%% gain, and without any memory stall "
+         "(L1-hit gathers, no index stream) the same loop still takes 0.11 ms -- instruction "
+         "issue plus gather latency (long scoreboard).  k_verlet_st (staged build): coalesced candidate stages, "
          "paired fp32 tests, predicated appends into 16-bit shared-memory rows, full-line "
          "flushes (no write amplification).  k_sph_rates / k_dem_step as in round 1.\n")
 L.append("## Launch list (`PM_USE_GRAPHS=0 ncu --metrics gpu__time_duration.sum --clock-control "
