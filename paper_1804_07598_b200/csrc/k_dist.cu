@@ -293,12 +293,14 @@ __global__ void k_dist_remap(const int *__restrict__ invperm, int *__restrict__ 
 __global__ void k_refresh_pack(Bufs B, const int *__restrict__ send_idx, int nsend,
                                float4 *__restrict__ out) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (B.st->hold) return;  // a held step of a group batch
   if (e < nsend) out[e] = B.pos[B.st->cur_pv][send_idx[e]];
 }
 
 __global__ void k_refresh_unpack(Bufs B, const int *__restrict__ ghost_slot, int nghost,
                                  const float4 *__restrict__ in) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (B.st->hold) return;  // a held step of a group batch
   if (e < nghost) {
     PM_CHECK(ghost_slot[e] >= 0);
     B.pos[B.st->cur_pv][ghost_slot[e]] = in[e];

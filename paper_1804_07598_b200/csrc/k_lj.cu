@@ -343,7 +343,7 @@ template <bool CAPPED, bool PEER = false>
 __global__ void __launch_bounds__(256, 6) k_lj_step(Params P, Bufs B, int n, float dt, int mode_arg,
                                                  int wphase) {
   State *st = B.st;
-  if (st->abort) return;
+  if (st->abort || st->hold) return;
   const int mode = mode_arg >= 0 ? mode_arg : st->mode;
   const int cp = st->cur_pv;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(256) k_ke(Params P, Bufs B, int n) {
 // fused ghost refresh picks the peer buffer from the sender's parity, so every
 // rank must flip in lockstep even with no particles).
 __global__ void k_empty_step(State *st, int count_step) {
-  if (st->abort) return;
+  if (st->abort || st->hold) return;
   st->pending_flip = 1;
   if (count_step) st->steps_done += 1;
 }

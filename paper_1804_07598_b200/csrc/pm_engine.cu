@@ -714,6 +714,30 @@ pm_status ctx_refresh_unpack_on(pm_ctx c, const void *recv, cudaStream_t s) {
 }
 // device address of the (need_rebuild, abort) pair of the state (adjacent ints)
 int *ctx_flag_ptr(pm_ctx c) { return &c->B.st->need_rebuild; }
+int *ctx_hold_ptr(pm_ctx c) { return &c->B.st->hold; }
+const long long *ctx_steps_ptr(pm_ctx c) { return &c->B.st->steps_done; }
+
+// In-process group members: hold = max over the members' rebuild flags (the
+// NCCL MAX all-reduce of a multi-process group, on one device).
+struct GroupHoldArgs {
+  int *need[kGroupHoldMax];
+  int *hold[kGroupHoldMax];
+  int m;
+};
+__global__ void k_group_hold(GroupHoldArgs a) {
+  int f = 0;
+  for (int k = 0; k < a.m; ++k) f = max(f, *a.need[k]);
+  for (int k = 0; k < a.m; ++k) *a.hold[k] = f;
+}
+void launch_group_hold(pm_ctx const *cs, int m, cudaStream_t s) {
+  GroupHoldArgs a;
+  a.m = m;
+  for (int k = 0; k < m; ++k) {
+    a.need[k] = &cs[k]->B.st->need_rebuild;
+    a.hold[k] = &cs[k]->B.st->hold;
+  }
+  k_group_hold<<<1, 1, 0, s>>>(a);
+}
 bool ctx_profiling(pm_ctx c) { return c->profiling; }
 void ctx_add_force_profile(pm_ctx c, double ms, int64_t launches) {
   c->prof_force_ms += ms;

@@ -58,6 +58,9 @@ bool ctx_list_valid(pm_ctx c);
 bool ctx_ready(pm_ctx c);
 pm_status ctx_error(pm_ctx c, pm_status code, const char *msg);
 int *ctx_flag_ptr(pm_ctx c);
+int *ctx_hold_ptr(pm_ctx c);
+const long long *ctx_steps_ptr(pm_ctx c);
+void launch_group_hold(pm_ctx const *cs, int m, cudaStream_t s);
 bool ctx_profiling(pm_ctx c);
 void ctx_add_force_profile(pm_ctx c, double ms, int64_t launches);
 pm_status dist_plan_async(pm_ctx c, int32_t what, const int32_t order[26]);
@@ -178,6 +181,8 @@ struct Group {
   int64_t rebuilds = 0;
   bool fused = false;       // fused ghost refresh enabled (PM_GROUP_FUSED, default 1)
   bool overlap = false;     // message refresh overlapped with interior forces (PM_GROUP_OVERLAP=1)
+  int batch = 4;            // steps enqueued per host synchronisation (PM_GROUP_BATCH)
+  unsigned char *h_bat = nullptr;  // pinned: per member (hold, need, abort, -, steps_done)
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_packed = nullptr, ev_unpacked = nullptr;
   bool fused_ready = false; // set up for the current ghost layout
@@ -696,6 +701,148 @@ pm_status rebuild(Group &G) {
   return s;
 }
 
+// ---------------------------------------------------------------------------
+// Batched steps of pm_dist_run: after each step the rebuild flags are reduced
+// on the device into every member's State::hold (NCCL MAX across ranks, a
+// one-thread kernel across this process's members); the next steps' kernels
+// (sweep, refresh pack / unpack) do nothing while it is set.  The host
+// enqueues `batch` steps, then reads (hold, abort, steps_done) once: the steps
+// that ran, and whether a rebuild (map + ghost_get) comes next.
+// ---------------------------------------------------------------------------
+pm_status hold_update(Group &G) {
+  if (G.comm && G.nranks > 1)  // one member per rank
+    return nccl_err(G.m[0].ctx,
+                    nccl().AllReduce(pm::ctx_flag_ptr(G.m[0].ctx), pm::ctx_hold_ptr(G.m[0].ctx),
+                                     1, ncclInt32, ncclMax, G.comm, G.stream),
+                    "flag all-reduce");
+  std::vector<pm_ctx> cs;
+  for (auto &R : G.m) cs.push_back(R.ctx);
+  pm::launch_group_hold(cs.data(), (int)cs.size(), G.stream);
+  return PM_OK;
+}
+
+pm_status clear_hold(Group &G) {
+  for (auto &R : G.m) {
+    cudaError_t e = cudaMemsetAsync(pm::ctx_flag_ptr(R.ctx), 0, sizeof(int), G.stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(pm::ctx_hold_ptr(R.ctx), 0, sizeof(int), G.stream);
+    if (e != cudaSuccess) return cuda_err(R.ctx, e, "rebuild flag");
+  }
+  return PM_OK;
+}
+
+// (hold, steps_done) of member 0 after everything enqueued; a device error of
+// any member is reported by that member
+pm_status batch_status(Group &G, int *hold, long long *steps) {
+  for (size_t k = 0; k < G.m.size(); ++k) {
+    unsigned char *h = G.h_bat + 32 * k;
+    cudaError_t e = cudaMemcpyAsync(h, pm::ctx_hold_ptr(G.m[k].ctx), sizeof(int),
+                                    cudaMemcpyDeviceToHost, G.stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(h + 4, pm::ctx_flag_ptr(G.m[k].ctx), 2 * sizeof(int),
+                          cudaMemcpyDeviceToHost, G.stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(h + 16, pm::ctx_steps_ptr(G.m[k].ctx), sizeof(long long),
+                          cudaMemcpyDeviceToHost, G.stream);
+    if (e != cudaSuccess) return cuda_err(G.m[k].ctx, e, "batch status");
+  }
+  cudaError_t e = cudaStreamSynchronize(G.stream);
+  if (e != cudaSuccess) return cuda_err(G.m[0].ctx, e, "batch status");
+  for (size_t k = 0; k < G.m.size(); ++k) {
+    int ab;
+    std::memcpy(&ab, G.h_bat + 32 * k + 8, sizeof(int));
+    if (ab) {
+      int dummy = 0;
+      pm_status s = pm_dist_read_flag(G.m[k].ctx, &dummy);
+      return s ? s : pm::ctx_error(G.m[k].ctx, PM_E_CUDA, "device error in a group step");
+    }
+  }
+  std::memcpy(hold, G.h_bat, sizeof(int));
+  std::memcpy(steps, G.h_bat + 16, sizeof(long long));
+  return PM_OK;
+}
+
+// One step enqueued for every member: the refresh (message modes), the sweep
+// with the fused kick/drift (or its interior / boundary halves), profiling
+// events around the sweeps.
+pm_status enqueue_step(Group &G, float dt, bool last, bool do_refresh, bool fused,
+                       int64_t *ev_pair) {
+  pm_status s;
+  bool halves = false;
+  if (do_refresh) {
+    halves = G.overlap && !fused;
+    if ((s = refresh(G, halves))) return s;
+  }
+  if (ev_pair) {
+    const size_t need = 2 * (size_t)(*ev_pair + 1);
+    while (G.ev.size() < need) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return PM_E_CUDA;
+      G.ev.push_back(e);
+    }
+    cudaEventRecord(G.ev[2 * *ev_pair], G.stream);
+  }
+  if (halves) {
+    for (auto &R : G.m)
+      if ((s = pm::ctx_step_half(R.ctx, dt, last, 0, G.stream))) return s;
+    cudaStreamWaitEvent(G.stream, G.ev_unpacked, 0);
+    for (auto &R : G.m)
+      if ((s = pm::ctx_step_half(R.ctx, dt, last, 1, G.stream))) return s;
+  } else {
+    for (auto &R : G.m)
+      if ((s = pm_dist_step(R.ctx, dt, last ? PM_PHASE_FINAL : PM_PHASE_STEP, nullptr)))
+        return s;
+  }
+  if (ev_pair) cudaEventRecord(G.ev[2 * *ev_pair + 1], G.stream);
+  return PM_OK;
+}
+
+pm_status run_batched(Group &G, float dt, int64_t nsteps, int flag, bool prof,
+                      double *prof_ms) {
+  pm_status s;
+  const bool fused = G.fused && G.P > 1;
+  int hold = 0;
+  long long steps0 = 0;
+  if ((s = batch_status(G, &hold, &steps0))) return s;
+  int64_t k = 0, npairs = 0;
+  std::vector<int64_t> pairs;
+  while (k < nsteps) {
+    const bool rebuilt = flag != 0;
+    if (rebuilt) {
+      if ((s = clear_hold(G))) return s;
+      if ((s = rebuild(G))) return s;
+    }
+    if (fused && !G.fused_ready && (s = setup_fused(G))) return s;
+    const int64_t nb = std::min<int64_t>(G.batch, nsteps - k);
+    pairs.clear();
+    for (int64_t j = 0; j < nb; ++j) {
+      const int64_t step = k + j;
+      const bool last = step == nsteps - 1;
+      // after a rebuild the ghosts are current; the fused refresh stores the
+      // next positions from the sweep, except after the prologue's drift
+      const bool do_refresh = !(j == 0 && rebuilt) && (!fused || step == 0);
+      int64_t p = npairs;
+      if ((s = enqueue_step(G, dt, last, do_refresh, fused, prof ? &p : nullptr))) return s;
+      if (prof) pairs.push_back(npairs++);
+      if (!last && (s = hold_update(G))) return s;
+    }
+    long long steps1 = 0;
+    if ((s = batch_status(G, &hold, &steps1))) return s;
+    const int64_t ran = steps1 - steps0;
+    steps0 = steps1;
+    if (ran < 0 || ran > nb || (ran < nb && !hold))
+      return pm::ctx_error(G.m[0].ctx, PM_E_CUDA, "group batch: inconsistent step count");
+    if (prof && prof_ms)
+      for (int64_t q = 0; q < ran; ++q) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, G.ev[2 * pairs[q]], G.ev[2 * pairs[q] + 1]);
+        *prof_ms += t;
+      }
+    k += ran;
+    flag = hold;
+  }
+  return clear_hold(G);
+}
+
 // Velocity-Verlet steps of the whole group in lock step (Listing 4.1's loop,
 // PAPER.md:282-320, with the Verlet skin: map + ghost_get only when a
 // particle of any sub-domain moved more than skin/2; otherwise the
@@ -722,6 +869,17 @@ pm_status do_run(Group &G, float dt, int64_t nsteps) {
   int flag = 0;
   if ((s = allreduce_flag(G, &flag))) return s;
   const bool prof = pm::ctx_profiling(G.m[0].ctx);
+  // (PM_GROUP_TIMING times the synchronised phases of the per-step loop)
+  if (G.batch > 1 && G.m.size() <= 64 && !std::getenv("PM_GROUP_TIMING")) {
+    double ms = 0.0;
+    if ((s = run_batched(G, dt, nsteps, flag, prof, &ms))) return s;
+    if (prof) pm::ctx_add_force_profile(G.m[0].ctx, ms, nsteps);
+    for (auto &R : G.m) {
+      R.stats.steps = nsteps;
+      R.stats.rebuilds = G.rebuilds - reb0;
+    }
+    return PM_OK;
+  }
   if (prof) {
     while (G.ev.size() < 2 * (size_t)nsteps) {
       cudaEvent_t e;
@@ -884,6 +1042,12 @@ Group *new_group(const int32_t grid[3], int nranks, int rank, int device, void *
   // per step on one B200, above the exchange latency it can hide
   const char *ov = std::getenv("PM_GROUP_OVERLAP");
   G->overlap = ov && ov[0] == '1';
+  // steps per host synchronisation of pm_dist_run: the step kernels check the
+  // device-side hold (the previous step's global rebuild flag), so the host
+  // enqueues a batch and reads the flags once (1 = the per-step loop)
+  const char *bt = std::getenv("PM_GROUP_BATCH");
+  G->batch = bt ? std::max(1, std::atoi(bt)) : 4;
+  cudaMallocHost((void **)&G->h_bat, 32 * (size_t)std::max(G->P, 1));
   cudaStreamCreateWithFlags(&G->comm_stream, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&G->ev_packed, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&G->ev_unpacked, cudaEventDisableTiming);
@@ -905,6 +1069,7 @@ void free_group(Group *G) {
   if (G->comm) nccl().CommDestroy(G->comm);
   cudaFree(G->d_flag);
   cudaFreeHost(G->h_flag);
+  if (G->h_bat) cudaFreeHost(G->h_bat);
   for (cudaEvent_t e : G->ev) cudaEventDestroy(e);
   cudaFree(G->d_red);
   cudaFreeHost(G->h_red);

@@ -79,6 +79,7 @@ struct Dist {
 };
 
 constexpr int kGhostBit = 1 << 30;  // kind flag of a ghost copy
+constexpr int kGroupHoldMax = 64;   // in-process group members per hold update
 
 struct LJ {
   float rc2;       // fl32(r_cut * r_cut)
@@ -200,6 +201,10 @@ struct State {
   long long sph_step;   // steps taken (Euler step every `every`)
   double sph_time;      // simulated time
   double acc[4];        // energy: U_raw, virial, npairs, KE
+  int hold;             // group step batches (pm_dist_run): the global rebuild flag
+                        // of the previous step; while set the step kernels of the
+                        // batch's remaining steps (sweep, refresh pack / unpack)
+                        // do nothing, so the host need not synchronise per step
 };
 
 enum { kModeInner = 0, kModeFinal = 1 };
