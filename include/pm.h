@@ -523,9 +523,13 @@ pm_status pm_ghost_get(pm_ctx ctx);
 
 /* nsteps velocity-Verlet steps of the whole group (collective): per step the
  * positions-only ghost refresh (16 B per ghost), the fused force sweep and
- * kick/drift of every member, and the global rebuild flag (MAX all-reduce);
- * when any particle moved more than skin/2, pm_map + pm_ghost_get.  Forces
- * are computed first when not valid.  out: steps and rebuilds (performer). */
+ * kick/drift of every member, and the global rebuild flag (MAX all-reduce on
+ * the device); when any particle moved more than skin/2, pm_map +
+ * pm_ghost_get.  Steps are enqueued in batches (env PM_GROUP_BATCH, default
+ * 4) with one host synchronisation per batch: kernels of steps after a set
+ * flag do nothing.  Forces are computed first when not valid.  out: steps and
+ * rebuilds (performer).  Errors: PM_E_STATE when members call different
+ * collectives; device errors of any member (PM_E_NONFINITE, ...). */
 pm_status pm_dist_run(pm_ctx ctx, float dt, int64_t nsteps, pm_run_stats *out);
 
 /* Global (all sub-domains) kinetic energy, raw and shifted LJ energy, virial
