@@ -23,6 +23,7 @@ namespace pm {
 namespace {
 
 constexpr int kDirBlock = 256;
+constexpr int kDirItems = 8;  // particles per thread in mark / fill
 
 // owner coordinate along a decomposed axis: the pinned fp32 rule (like R3)
 // for equal cuboids, or the number of cut positions <= x for the
@@ -36,17 +37,13 @@ __device__ __forceinline__ int owner_coord(const Dist &D, int d, float x) {
   return cell_coord(x, D.glo[d], D.inv_s[d], D.p[d]);
 }
 
-__global__ void __launch_bounds__(kDirBlock) k_dist_mark(Params P, Bufs B, Dist D, int n_owned,
-                                                         int what, uint32_t *__restrict__ mask) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_owned) return;
+// The direction mask of one owned particle (bit d = message direction d).
+__device__ __forceinline__ uint32_t dist_mask_of(const Params &P, const Bufs &B, const Dist &D,
+                                                 int i, int what) {
   State *st = B.st;
   // after a build owned particles and ghost copies are interleaved in cell
   // order: ghosts belong to no message (a migration drops them)
-  if (B.kind[st->cur_id][i] & kGhostBit) {
-    mask[i] = 0u;
-    return;
-  }
+  if (B.kind[st->cur_id][i] & kGhostBit) return 0u;
   const float4 x4 = B.pos[st->cur_pv][i];
   const float x[3] = {x4.x, x4.y, x4.z};
   uint32_t m = 0;
@@ -84,21 +81,31 @@ __global__ void __launch_bounds__(kDirBlock) k_dist_mark(Params P, Bufs B, Dist 
       }
     }
   }
-  mask[i] = m;
+  return m;
 }
 
-// pass 1: per-block counts per direction
-__global__ void __launch_bounds__(kDirBlock) k_dist_count(const uint32_t *__restrict__ mask, int n,
-                                                          int *__restrict__ blk_counts) {
+// pass 1: direction masks of the block's kDirItems * kDirBlock particles and
+// the block's counts per direction (warp-aggregated: one shared-memory add
+// per direction present in a warp)
+__global__ void __launch_bounds__(kDirBlock) k_dist_mark(Params P, Bufs B, Dist D, int n_owned,
+                                                         int what, uint32_t *__restrict__ mask,
+                                                         int *__restrict__ blk_counts) {
   __shared__ int cnt[27];
   if (threadIdx.x < 27) cnt[threadIdx.x] = 0;
   __syncthreads();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t m = (i < n) ? mask[i] : 0u;
-  while (m) {
-    const int d = __ffs(m) - 1;
-    m &= m - 1;
-    atomicAdd(&cnt[d], 1);
+  const int lane = threadIdx.x & 31;
+  const int base = blockIdx.x * (kDirBlock * kDirItems);
+  for (int it = 0; it < kDirItems; ++it) {
+    const int i = base + it * kDirBlock + threadIdx.x;
+    const uint32_t m = (i < n_owned) ? dist_mask_of(P, B, D, i, what) : 0u;
+    if (i < n_owned) mask[i] = m;
+    uint32_t wm = __reduce_or_sync(0xffffffffu, m);
+    while (wm) {
+      const int d = __ffs(wm) - 1;
+      wm &= wm - 1;
+      const unsigned b = __ballot_sync(0xffffffffu, (m >> d) & 1u);
+      if (lane == 0) atomicAdd(&cnt[d], __popc(b));
+    }
   }
   __syncthreads();
   if (threadIdx.x < 27) blk_counts[blockIdx.x * 27 + threadIdx.x] = cnt[threadIdx.x];
@@ -142,7 +149,8 @@ __global__ void __launch_bounds__(1024) k_dist_scan(int *__restrict__ blk_counts
 }
 
 // pass 3: stable write of particle indices into the per-direction lists
-// direction bases in the caller's packing order (order[0..25], then 13 last)
+// direction bases in the caller's packing order (order[0..25], then 13 last);
+// the block's kDirItems chunks in index order, a running offset per direction
 __global__ void __launch_bounds__(kDirBlock) k_dist_fill(const uint32_t *__restrict__ mask, int n,
                                                          const int *__restrict__ blk_off,
                                                          const long long *__restrict__ totals,
@@ -151,6 +159,7 @@ __global__ void __launch_bounds__(kDirBlock) k_dist_fill(const uint32_t *__restr
                                                          int *__restrict__ list) {
   __shared__ int wsum[27][kDirBlock / 32];
   __shared__ int dir_base[27];
+  __shared__ int run[27];
   if (threadIdx.x == 0) {
     long long base = 0;
     for (int k = 0; k < 26; ++k) {
@@ -161,37 +170,42 @@ __global__ void __launch_bounds__(kDirBlock) k_dist_fill(const uint32_t *__restr
     if (blockIdx.x == 0)
       for (int k = 0; k < 27; ++k) dir_base_out[k] = dir_base[k];
   }
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (threadIdx.x < 27) run[threadIdx.x] = blk_off[blockIdx.x * 27 + threadIdx.x];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint32_t m = (i < n) ? mask[i] : 0u;
   const unsigned lt = (1u << lane) - 1u;
-  // only the directions present in the warp (usually "stay" plus a face or
-  // two) need a ballot; the others count zero
-  if (lane < 27) wsum[lane][w] = 0;
-  uint32_t wm = __reduce_or_sync(0xffffffffu, m);
-  while (wm) {
-    const int d = __ffs(wm) - 1;
-    wm &= wm - 1;
-    const unsigned b = __ballot_sync(0xffffffffu, (m >> d) & 1u);
-    if (lane == 0) wsum[d][w] = __popc(b);
-  }
-  __syncthreads();
-  if (threadIdx.x < 27) {  // exclusive scan over the block's warps, per direction
-    int acc = 0;
-    for (int k = 0; k < kDirBlock / 32; ++k) {
-      const int c = wsum[threadIdx.x][k];
-      wsum[threadIdx.x][k] = acc;
-      acc += c;
+  const int base = blockIdx.x * (kDirBlock * kDirItems);
+  for (int it = 0; it < kDirItems; ++it) {
+    const int i = base + it * kDirBlock + threadIdx.x;
+    const uint32_t m = (i < n) ? mask[i] : 0u;
+    // only the directions present in the warp (usually "stay" plus a face or
+    // two) need a ballot; the others count zero
+    if (lane < 27) wsum[lane][w] = 0;
+    uint32_t wm = __reduce_or_sync(0xffffffffu, m);
+    while (wm) {
+      const int d = __ffs(wm) - 1;
+      wm &= wm - 1;
+      const unsigned b = __ballot_sync(0xffffffffu, (m >> d) & 1u);
+      if (lane == 0) wsum[d][w] = __popc(b);
     }
-  }
-  __syncthreads();
-  wm = __reduce_or_sync(0xffffffffu, m);
-  while (wm) {
-    const int d = __ffs(wm) - 1;
-    wm &= wm - 1;
-    const unsigned b = __ballot_sync(0xffffffffu, (m >> d) & 1u);
-    if ((m >> d) & 1u)
-      list[dir_base[d] + blk_off[blockIdx.x * 27 + d] + wsum[d][w] + __popc(b & lt)] = i;
+    __syncthreads();
+    if (threadIdx.x < 27) {  // exclusive scan over the block's warps, per direction
+      int acc = run[threadIdx.x];
+      for (int k = 0; k < kDirBlock / 32; ++k) {
+        const int c = wsum[threadIdx.x][k];
+        wsum[threadIdx.x][k] = acc;
+        acc += c;
+      }
+      run[threadIdx.x] = acc;
+    }
+    __syncthreads();
+    wm = __reduce_or_sync(0xffffffffu, m);
+    while (wm) {
+      const int d = __ffs(wm) - 1;
+      wm &= wm - 1;
+      const unsigned b = __ballot_sync(0xffffffffu, (m >> d) & 1u);
+      if ((m >> d) & 1u) list[dir_base[d] + wsum[d][w] + __popc(b & lt)] = i;
+    }
+    __syncthreads();  // wsum is rewritten by the next chunk
   }
 }
 
@@ -389,9 +403,8 @@ int dist_record_bytes(int what) {
 void launch_dist_plan(const Params &P, const Bufs &B, const Dist &D, int n_owned, int what,
                       uint32_t *mask, int *blk_counts, const int *order, int *dir_base,
                       long long *totals, int *list, cudaStream_t s) {
-  const unsigned g = nb(n_owned > 0 ? n_owned : 1, kDirBlock);
-  if (n_owned > 0) k_dist_mark<<<g, kDirBlock, 0, s>>>(P, B, D, n_owned, what, mask);
-  k_dist_count<<<g, kDirBlock, 0, s>>>(mask, n_owned, blk_counts);
+  const unsigned g = nb(n_owned > 0 ? n_owned : 1, kDirBlock * kDirItems);
+  k_dist_mark<<<g, kDirBlock, 0, s>>>(P, B, D, n_owned, what, mask, blk_counts);
   k_dist_scan<<<27, 1024, 0, s>>>(blk_counts, (int)g, totals);
   k_dist_fill<<<g, kDirBlock, 0, s>>>(mask, n_owned, blk_counts, totals, order, dir_base, list);
 }
