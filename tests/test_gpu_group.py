@@ -145,6 +145,32 @@ def test_group_run_matches_single_context(env, grid, via_nccl, mode, monkeypatch
         c.close()
 
 
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_group_batched_steps_equal_per_step_loop(env, fused, monkeypatch):
+    """pm_dist_run in batches (PM_GROUP_BATCH: the rebuild flag reduced on the
+    device into State::hold, held steps' kernels return at once, one host
+    synchronisation per batch) gives bitwise the same trajectory as the
+    per-step loop (batch 1): same arithmetic, same rebuild points, only the
+    host synchronisations differ.  Batch 3 does not divide the rebuild
+    interval, so held steps occur."""
+    pm = env
+    monkeypatch.setenv("PM_GROUP_FUSED", fused)
+    s = inputs.lj_lattice_system(24, 24, 24, jitter_key=(54,), vel_key=(154,))
+    res = []
+    for batch in ("1", "3"):
+        monkeypatch.setenv("PM_GROUP_BATCH", batch)
+        members = make_group(pm, s, (2, 2, 1))
+        out = [c.dist_run(0.005, 37) for c in members][-1]
+        assert out["steps"] == 37 and out["rebuilds"] >= 2
+        res.append((owned_union(pm, members), out["rebuilds"]))
+        for c in members:
+            c.close()
+    (a, ra), (b, rb) = res
+    assert ra == rb
+    assert np.array_equal(a["gid"], b["gid"])
+    assert np.array_equal(a["pos"], b["pos"]) and np.array_equal(a["vel"], b["vel"])
+
+
 def test_group_empty_sub_domain(env):
     """A sub-domain with no particles: all particles in the lower
     half of x, grid (2,1,1) -- the upper member stays empty (no owned, only

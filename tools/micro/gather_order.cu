@@ -127,6 +127,117 @@ __global__ void __launch_bounds__(256) k_sweep_pf(const float4 *__restrict__ pos
   out[i] = make_float4(fx, fy, fz, (float)acc);
 }
 
+// k_sweep<1> with the index stream staged through shared memory by cp.async
+// (4-byte copies of the lane's own entries, RING groups ahead): the index
+// loads' DRAM latency leaves the dependency chain of the gathers
+template <int RING>
+__global__ void __launch_bounds__(256) k_sweep_cpa(const float4 *__restrict__ pos,
+                                                   const int *__restrict__ nbr,
+                                                   const long long *__restrict__ wbase,
+                                                   const int *__restrict__ cnt, float4 *out,
+                                                   int n, float rc2) {
+  __shared__ int ring[8][RING * 4][32];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const float4 xi = pos[i];
+  const int c = cnt[i];
+  const int ng = (c + 3) >> 2;
+  const int *nb = nbr + wbase[i >> 5] + lane * 4;
+  float fx = 0.f, fy = 0.f, fz = 0.f;
+  auto issue = [&](int g) {
+    if (g < ng) {
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(&ring[w][(g % RING) * 4 + s][lane]);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(nb + (int64_t)g * 128 + s));
+      }
+    }
+    asm volatile("cp.async.commit_group;");
+  };
+#pragma unroll
+  for (int g = 0; g < RING - 1; ++g) issue(g);
+  for (int g = 0; g < ng; ++g) {
+    issue(g + RING - 1);
+    asm volatile("cp.async.wait_group %0;" ::"n"(RING - 1));
+    int jj[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) jj[s] = ring[w][(g % RING) * 4 + s][lane];
+    float4 xj[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) xj[s] = __ldg(pos + (4 * g + s < c ? jj[s] : i));
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const float dx = xj[s].x - xi.x, dy = xj[s].y - xi.y, dz = xj[s].z - xi.z;
+      const float r2 = dx * dx + dy * dy + dz * dz;
+      if (4 * g + s < c && r2 < rc2 && r2 > 0.f) {
+        const float ir2 = 1.f / r2, ir6 = ir2 * ir2 * ir2;
+        const float f = 24.f * ir2 * ir6 * (2.f * ir6 - 1.f);
+        fx -= f * dx;
+        fy -= f * dy;
+        fz -= f * dz;
+      }
+    }
+  }
+  asm volatile("cp.async.wait_all;");
+  out[i] = make_float4(fx, fy, fz, 0.f);
+}
+
+// the same with the warp's 512-byte group chunks copied cooperatively
+// (16 bytes per lane, cp.async.cg: L2 only), a warp-uniform loop over the
+// slice's longest row, lanes past their row masked
+template <int RING>
+__global__ void __launch_bounds__(256) k_sweep_cpw(const float4 *__restrict__ pos,
+                                                   const int *__restrict__ nbr,
+                                                   const long long *__restrict__ wbase,
+                                                   const int *__restrict__ cnt, float4 *out,
+                                                   int n, float rc2) {
+  __shared__ __align__(16) int ring[8][RING][128];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const float4 xi = pos[i];
+  const int c = cnt[i];
+  const int ngm = (__reduce_max_sync(0xffffffffu, c) + 3) >> 2;
+  const int *chunk = nbr + wbase[i >> 5];
+  float fx = 0.f, fy = 0.f, fz = 0.f;
+  auto issue = [&](int g) {
+    if (g < ngm) {
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(&ring[w][g % RING][lane * 4]);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                   "l"(chunk + (int64_t)g * 128 + lane * 4));
+    }
+    asm volatile("cp.async.commit_group;");
+  };
+#pragma unroll
+  for (int g = 0; g < RING - 1; ++g) issue(g);
+  for (int g = 0; g < ngm; ++g) {
+    issue(g + RING - 1);
+    asm volatile("cp.async.wait_group %0;" ::"n"(RING - 1));
+    __syncwarp();
+    int jj[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) jj[s] = ring[w][g % RING][s * 32 + lane];
+    __syncwarp();
+    float4 xj[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) xj[s] = __ldg(pos + (4 * g + s < c ? jj[s] : i));
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const float dx = xj[s].x - xi.x, dy = xj[s].y - xi.y, dz = xj[s].z - xi.z;
+      const float r2 = dx * dx + dy * dy + dz * dz;
+      if (4 * g + s < c && r2 < rc2 && r2 > 0.f) {
+        const float ir2 = 1.f / r2, ir6 = ir2 * ir2 * ir2;
+        const float f = 24.f * ir2 * ir6 * (2.f * ir6 - 1.f);
+        fx -= f * dx;
+        fy -= f * dy;
+        fz -= f * dz;
+      }
+    }
+  }
+  asm volatile("cp.async.wait_all;");
+  out[i] = make_float4(fx, fy, fz, 0.f);
+}
+
 // k_sweep<1> in CTAs of 1024 threads (4 x 256 consecutive rows share an SM)
 __global__ void __launch_bounds__(1024) k_sweep1k(const float4 *__restrict__ pos,
                                                   const int *__restrict__ nbr,
@@ -460,6 +571,10 @@ int main(int argc, char **argv) {
     const int nbk = (n + 255) / 256;
     if (G == 7) { k_sweep_pf<1><<<nbk, 256>>>(dpos, didx[v], dbase[v], dcnt, dout[v], n, rc * rc); return; }
     if (G == 8) { k_sweep_pf<2><<<nbk, 256>>>(dpos, didx[v], dbase[v], dcnt, dout[v], n, rc * rc); return; }
+    if (G == 11) { k_sweep_cpw<3><<<nbk, 256>>>(dpos, didx[v], dbase[v], dcnt, dout[v], n, rc * rc); return; }
+    if (G == 12) { k_sweep_cpw<6><<<nbk, 256>>>(dpos, didx[v], dbase[v], dcnt, dout[v], n, rc * rc); return; }
+    if (G == 9) { k_sweep_cpa<3><<<nbk, 256>>>(dpos, didx[v], dbase[v], dcnt, dout[v], n, rc * rc); return; }
+    if (G == 10) { k_sweep_cpa<5><<<nbk, 256>>>(dpos, didx[v], dbase[v], dcnt, dout[v], n, rc * rc); return; }
     if (G == 6) { k_sweep_pf<0><<<nbk, 256>>>(dpos, didx[v], dbase[v], dcnt, dout[v], n, rc * rc); return; }
     if (G == 5) { k_sweep1k<<<(n + 1023) / 1024, 1024>>>(dpos, didx[v], dbase[v], dcnt, dout[v], n, rc * rc); return; }
     if (G == 1) k_sweep<1><<<nbk, 256>>>(dpos, didx[v], dbase[v], dcnt, dout[v], n, rc * rc);
@@ -468,7 +583,7 @@ int main(int argc, char **argv) {
     if (G == 4 && u16_ok) k_sweep16<<<nbk, 256>>>(dpos, d16[v], db16[v], dpt[v], dcnt, dout[v], n, rc * rc);
   };
   for (int rep = 0; rep < 2; ++rep)
-    for (int G : {6, 7, 8})
+    for (int G : {6, 11, 12, 7, 8})
       for (int v = 0; v < 2; ++v) {
         for (int w = 0; w < 5; ++w) launch(G, v);
         cudaEventRecord(e0);
@@ -477,7 +592,7 @@ int main(int argc, char **argv) {
         CK(cudaEventSynchronize(e1));
         float ms;
         cudaEventElapsedTime(&ms, e0, e1);
-        std::printf("%s %s: %.4f ms per sweep, %.3f ns per particle\n", G == 8 ? "no index loads, L1-hit gathers" : G == 7 ? "index stream, L1-hit gathers" : G == 6 ? "i32 G=1 index prefetch" : G == 5 ? "i32 1024-thread CTAs" : G == 4 ? "u16x8" : G == 1 ? "i32 G=1" : G == 2 ? "i32 G=2" : "i32 G=3", name[v], ms / 50, ms / 50 * 1e6 / n);
+        std::printf("%s %s: %.4f ms per sweep, %.3f ns per particle\n", G == 11 ? "cp.async warp chunks ring 3" : G == 12 ? "cp.async warp chunks ring 6" : G == 9 ? "cp.async index ring 3" : G == 10 ? "cp.async index ring 5" : G == 8 ? "no index loads, L1-hit gathers" : G == 7 ? "index stream, L1-hit gathers" : G == 6 ? "i32 G=1 index prefetch" : G == 5 ? "i32 1024-thread CTAs" : G == 4 ? "u16x8" : G == 1 ? "i32 G=1" : G == 2 ? "i32 G=2" : "i32 G=3", name[v], ms / 50, ms / 50 * 1e6 / n);
       }
   std::vector<float4> f0(n), f1(n);
   launch(4, 0);
