@@ -475,8 +475,9 @@ void orc_sph_density_rows(int64_t n, const float *pos4, const float lo[3], const
 
 /* Eq. 1 with readings R17 (sign: a_p = -sum m (...) grad_p W(x_p - x_q)),
  * R18 ((P_p + P_q)/(rho_p rho_q) as printed), R20 (Pi_pq: Monaghan, nonzero
- * only for v_pq . r_pq < 0; cbar = c0, alpha, eta2 given; "parity unpinned"
- * beyond the branch/sign pins), g added to fluid particles only; boundary
+ * only for v_pq . r_pq < 0; cbar = c0, alpha, eta2 given; pinned by the
+ * branch pins and by one hand-computed approaching pair,
+ * tests/golden/sph_viscosity_pair.txt), g added to fluid particles only; boundary
  * particles (kind 1) get a = 0.  rho/P are per-particle inputs (storage
  * order, fp64) so the force pass can be pinned independently of the
  * density pass. */
