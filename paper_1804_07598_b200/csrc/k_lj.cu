@@ -96,6 +96,16 @@ __device__ __forceinline__ Idx4 ld_idx4(const int *__restrict__ p) {
   return r;
 }
 
+// a group of 4 entries: SELL-32 (4 coalesced lines across the warp) or a
+// row-major row (one 16-byte load of the lane's own row)
+template <bool RM>
+__device__ __forceinline__ Idx4 ld_group(const int *__restrict__ p) {
+  if (!RM) return ld_idx4(p);
+  // (L1-cached: the lane's next group is the other half of the same sector)
+  const int4 v = __ldg(reinterpret_cast<const int4 *>(p));
+  return Idx4{v.x, v.y, v.z, v.w};
+}
+
 template <int MIM, bool CAPPED, bool ENERGY, bool MASK>
 __device__ __forceinline__ void lj_group(const Params &P, const float4 *__restrict__ pos,
                                          const Idx4 &j, int rem, const float4 &xi, Acc &a) {
@@ -109,20 +119,21 @@ __device__ __forceinline__ void lj_group(const Params &P, const float4 *__restri
   lj_pair<MIM, CAPPED, ENERGY, MASK>(P, xi, x3, rem > 3, a);
 }
 
-template <int MIM, bool CAPPED, bool ENERGY>
+template <int MIM, bool CAPPED, bool ENERGY, bool RM = false>
 __device__ __forceinline__ void lj_row(const Params &P, const float4 *__restrict__ pos,
                                        const int *__restrict__ nb, int cnt, const float4 &xi,
                                        Acc &a) {
   const int ng = (cnt + 3) >> 2;  // groups incl. a partial last one
   const int nfull = cnt >> 2;
   if (ng == 0) return;
-  Idx4 j0 = ld_idx4(nb);
-  Idx4 j1 = (ng > 1) ? ld_idx4(nb + 128) : j0;
+  constexpr int GS = RM ? 4 : 128;  // ints between consecutive groups of a row
+  Idx4 j0 = ld_group<RM>(nb);
+  Idx4 j1 = (ng > 1) ? ld_group<RM>(nb + GS) : j0;
   int g = 0;
   // two groups per iteration: the prefetch registers rotate statically
   for (; g + 2 <= nfull; g += 2) {
-    const Idx4 j2 = (g + 2 < ng) ? ld_idx4(nb + (g + 2) * 128) : j1;
-    const Idx4 j3 = (g + 3 < ng) ? ld_idx4(nb + (g + 3) * 128) : j1;
+    const Idx4 j2 = (g + 2 < ng) ? ld_group<RM>(nb + (g + 2) * GS) : j1;
+    const Idx4 j3 = (g + 3 < ng) ? ld_group<RM>(nb + (g + 3) * GS) : j1;
     lj_group<MIM, CAPPED, ENERGY, false>(P, pos, j0, 4, xi, a);
     lj_group<MIM, CAPPED, ENERGY, false>(P, pos, j1, 4, xi, a);
     j0 = j2;
@@ -162,7 +173,7 @@ __device__ __forceinline__ int warp_mi_axes(const Params &P, bool active, const 
   return __reduce_or_sync(0xffffffffu, (unsigned)m);
 }
 
-template <bool CAPPED, bool ENERGY>
+template <bool CAPPED, bool ENERGY, bool RM>
 __device__ __forceinline__ Acc lj_force_of(const Params &P, const Bufs &B,
                                            const float4 *__restrict__ pos, int i, bool active,
                                            const float4 &xi) {
@@ -171,6 +182,11 @@ __device__ __forceinline__ Acc lj_force_of(const Params &P, const Bufs &B,
   if (active) {
     const int cnt = B.cnt[i];
     const int *nb = B.nbr + nbr_row_base(B, i);
+    if (RM) {  // row-major slices (long rows): the general minimum-image variant
+      if (mim) lj_row<7, CAPPED, ENERGY, true>(P, pos, nb, cnt, xi, a);
+      else lj_row<0, CAPPED, ENERGY, true>(P, pos, nb, cnt, xi, a);
+      return a;
+    }
     switch (mim) {  // warp-uniform
       case 0: lj_row<0, CAPPED, ENERGY>(P, pos, nb, cnt, xi, a); break;
       case 1: lj_row<1, CAPPED, ENERGY>(P, pos, nb, cnt, xi, a); break;
@@ -219,11 +235,11 @@ __device__ __forceinline__ void block_add_energy(State *st, double u, double w, 
 // partner at distance 0 (identical wrapped coordinates; such pairs pass the
 // list test 0 <= d2 < r_v^2 in any cell, however crowded), else
 // PM_E_NONFINITE.
-__device__ __noinline__ void raise_bad_force(const int *nb, int cnt, const float4 *pos, int i,
-                                             float xx, float xy, float xz, long long gid,
-                                             State *st) {
+__device__ __noinline__ void raise_bad_force(const int *nb, int stride, int cnt,
+                                             const float4 *pos, int i, float xx, float xy,
+                                             float xz, long long gid, State *st) {
   for (int k = 0; k < cnt; ++k) {
-    const int j = nb[(int64_t)k << 5];
+    const int j = nb[(int64_t)k * stride];
     const float4 xj = pos[j];
     if (j != i && xj.x == xx && xj.y == xy && xj.z == xz) {
       raise_error(st, -7 /*PM_E_COINCIDENT*/, gid);
@@ -235,19 +251,19 @@ __device__ __noinline__ void raise_bad_force(const int *nb, int cnt, const float
 
 __device__ __forceinline__ void bad_force(const Bufs &B, State *st, const float4 *pos, int i,
                                           const float4 &xi) {
-  raise_bad_force(B.nbr + nbr_row_base(B, i), B.cnt[i], pos, i, xi.x, xi.y, xi.z,
+  raise_bad_force(B.nbr + nbr_row_base(B, i), nbr_stride(B), B.cnt[i], pos, i, xi.x, xi.y, xi.z,
                   (long long)B.gid[st->cur_id][i], st);
 }
 
 // pm_compute_lj: forces (+ energy) of the current positions.
-template <bool CAPPED, bool ENERGY>
+template <bool CAPPED, bool ENERGY, bool RM = false>
 __global__ void __launch_bounds__(256) k_lj(Params P, Bufs B, int n) {
   State *st = B.st;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = i < n;
   const float4 *__restrict__ pos = B.pos[st->cur_pv];
   const float4 xi = active ? pos[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-  Acc a = lj_force_of<CAPPED, ENERGY>(P, B, pos, i, active, xi);
+  Acc a = lj_force_of<CAPPED, ENERGY, RM>(P, B, pos, i, active, xi);
   if (active) {
     B.force[i] = make_float4(a.fx, a.fy, a.fz, 0.f);
     if (!isfinite(a.fx + a.fy + a.fz)) bad_force(B, st, pos, i, xi);
@@ -339,7 +355,7 @@ __device__ __forceinline__ void vv_epilogue(const Params &P, const Bufs &B, Stat
 //  inner: F(x); v += dt F/m (2nd half-kick of this step + 1st of the next);
 //         x' = wrap(x + dt v); displacement test vs xref; -> alternate buffers
 //  final: F(x); v += dt/2 F/m; F stored; x copied  -> alternate buffers
-template <bool CAPPED, bool PEER = false>
+template <bool CAPPED, bool PEER = false, bool RM = false>
 __global__ void __launch_bounds__(256, 6) k_lj_step(Params P, Bufs B, int n, float dt, int mode_arg,
                                                  int wphase) {
   State *st = B.st;
@@ -357,7 +373,7 @@ __global__ void __launch_bounds__(256, 6) k_lj_step(Params P, Bufs B, int n, flo
   const bool active = i < n;
   const float4 *__restrict__ pos = B.pos[cp];
   const float4 xi = active ? pos[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-  Acc a = lj_force_of<CAPPED, false>(P, B, pos, i, active, xi);
+  Acc a = lj_force_of<CAPPED, false, RM>(P, B, pos, i, active, xi);
   bool far = false;
   vv_epilogue<PEER>(P, B, st, i, active, xi, a, dt, mode, cp, far);
   if (__any_sync(0xffffffffu, far) && (threadIdx.x & 31) == 0) st->need_rebuild = 1;
@@ -573,20 +589,26 @@ static void launch_lj_half(const Params &P, const Bufs &B, int64_t n, int want_e
   }
 }
 
+template <bool RM>
+void launch_lj_rm(const Params &P, const Bufs &B, int64_t n, int want_energy, cudaStream_t s) {
+  const bool capped = P.lj.r_min > 0.f;
+  if (capped) {
+    if (want_energy) k_lj<true, true, RM><<<nb(n), 256, 0, s>>>(P, B, (int)n);
+    else k_lj<true, false, RM><<<nb(n), 256, 0, s>>>(P, B, (int)n);
+  } else {
+    if (want_energy) k_lj<false, true, RM><<<nb(n), 256, 0, s>>>(P, B, (int)n);
+    else k_lj<false, false, RM><<<nb(n), 256, 0, s>>>(P, B, (int)n);
+  }
+}
+
 void launch_lj(const Params &P, const Bufs &B, int64_t n, int want_energy, cudaStream_t s) {
   if (n <= 0) return;
   if (P.newton) {
     launch_lj_half(P, B, n, want_energy, s);
     return;
   }
-  const bool capped = P.lj.r_min > 0.f;
-  if (capped) {
-    if (want_energy) k_lj<true, true><<<nb(n), 256, 0, s>>>(P, B, (int)n);
-    else k_lj<true, false><<<nb(n), 256, 0, s>>>(P, B, (int)n);
-  } else {
-    if (want_energy) k_lj<false, true><<<nb(n), 256, 0, s>>>(P, B, (int)n);
-    else k_lj<false, false><<<nb(n), 256, 0, s>>>(P, B, (int)n);
-  }
+  if (B.rm) launch_lj_rm<true>(P, B, n, want_energy, s);
+  else launch_lj_rm<false>(P, B, n, want_energy, s);
 }
 
 // Decomposed half lists: the sweep alone (ghost shares accumulate in the
@@ -613,15 +635,25 @@ void launch_lj_step_mode(const Params &P, const Bufs &B, int64_t n, float dt, in
     k_lj_half_vv<<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode);
     return;
   }
-  if (P.peer_n > 0) {  // decomposed run with the fused ghost refresh
-    if (P.lj.r_min > 0.f)
-      k_lj_step<true, true><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode, wphase);
-    else
-      k_lj_step<false, true><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode, wphase);
+  const bool capped = P.lj.r_min > 0.f, peer = P.peer_n > 0;  // peer: fused ghost refresh
+  const unsigned g = nb(n);
+  if (B.rm) {  // row-major slices (long rows)
+    if (peer) {
+      if (capped) k_lj_step<true, true, true><<<g, 256, 0, s>>>(P, B, (int)n, dt, mode, wphase);
+      else k_lj_step<false, true, true><<<g, 256, 0, s>>>(P, B, (int)n, dt, mode, wphase);
+    } else {
+      if (capped) k_lj_step<true, false, true><<<g, 256, 0, s>>>(P, B, (int)n, dt, mode, wphase);
+      else k_lj_step<false, false, true><<<g, 256, 0, s>>>(P, B, (int)n, dt, mode, wphase);
+    }
     return;
   }
-  if (P.lj.r_min > 0.f) k_lj_step<true><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode, wphase);
-  else k_lj_step<false><<<nb(n), 256, 0, s>>>(P, B, (int)n, dt, mode, wphase);
+  if (peer) {
+    if (capped) k_lj_step<true, true><<<g, 256, 0, s>>>(P, B, (int)n, dt, mode, wphase);
+    else k_lj_step<false, true><<<g, 256, 0, s>>>(P, B, (int)n, dt, mode, wphase);
+    return;
+  }
+  if (capped) k_lj_step<true><<<g, 256, 0, s>>>(P, B, (int)n, dt, mode, wphase);
+  else k_lj_step<false><<<g, 256, 0, s>>>(P, B, (int)n, dt, mode, wphase);
 }
 
 void launch_lj_step(const Params &P, const Bufs &B, int64_t n, float dt, cudaStream_t s) {

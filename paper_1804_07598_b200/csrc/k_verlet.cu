@@ -344,8 +344,9 @@ __device__ __forceinline__ u64 f2_fma(u64 a, u64 b, u64 c) {
 // (crowded cells), int32 indices stored straight into the global row.
 struct StRows {
   unsigned short *sm;  // [k][lane] codes (64 bytes per line)
-  int *gl;             // global row of this lane: entry k at gl[k << 5]
+  int *gl;             // global row of this lane: entry k at gl[k * gs]
   bool direct;
+  int gs;              // row stride: 32 (SELL-32 slices) or 1 (row-major slices)
 };
 
 // Append the hits of one group of 32 staged candidates (stage slots g + u,
@@ -370,7 +371,7 @@ __device__ __forceinline__ void st_expand(unsigned msk, const float4 *__restrict
     }
     const int kk = min(k, cap - 1);
     PM_CHECK(j >= 0 && kk >= 0);
-    if (R.direct) R.gl[(int64_t)kk << 5] = j;
+    if (R.direct) R.gl[(int64_t)kk * R.gs] = j;
     else R.sm[(kk << 5) + lane] = (unsigned short)code;
     ++k;
   }
@@ -457,7 +458,7 @@ __device__ __forceinline__ void st_fast_group(const float4 *__restrict__ SA,
   PM_CHECK(((bo - rows_sa) & 63u) == (unsigned)(lane << 1));
 }
 
-template <int RCH, int NMODE>
+template <int RCH, int NMODE, bool RM = false>
 __global__ void __launch_bounds__(stg::kWarps * 32, 5)
     k_verlet_st(Params P, Bufs B, int n, int wcap) {
   using namespace stg;
@@ -478,7 +479,9 @@ __global__ void __launch_bounds__(stg::kWarps * 32, 5)
   if (wbase >= n) return;  // whole warp out of range
   const bool active = i < n && !(P.dist && (B.kind[st->cur_id][i] & kGhostBit));
   const int cap = nbr_row_cap(B, wbase);
-  int *grow = B.nbr + B.slice_off[wbase >> 5] * 32 + lane;
+  // the lane's row (a row of the slice also for i >= n); RM: row-major slices
+  int *grow = B.nbr + B.slice_off[wbase >> 5] * 32 + (RM ? (int64_t)lane * cap : lane);
+  constexpr int gs = RM ? 1 : 32;
   const int nx = P.grid.n[0], ny = P.grid.n[1], nz = P.grid.n[2];
   const float4 *__restrict__ pos = B.pos[st->cur_pv];
   const float4 xi = active ? pos[i] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -580,7 +583,7 @@ __global__ void __launch_bounds__(stg::kWarps * 32, 5)
     }
     // wcap == 0: no shared-memory rows at all (rows too long for shared memory,
     // clustered inputs): every segment appends straight to its global rows
-    const StRows R{rows, grow, wcap == 0 || __any_sync(0xffffffffu, long_piece) != 0};
+    const StRows R{rows, grow, wcap == 0 || __any_sync(0xffffffffu, long_piece) != 0, gs};
     __syncwarp();
     // bounding box of the segment's particles: candidates farther than r_v
     // (+1e-3) from it cannot be a neighbour of any lane and are not staged
@@ -751,12 +754,12 @@ __global__ void __launch_bounds__(stg::kWarps * 32, 5)
           PM_CHECK((int)(c >> kOffBits) < NP);
           const int j = PBE[c >> kOffBits].x + (int)(c & (kMaxPieceLen - 1));
           PM_CHECK(j >= 0 && j < n && j != i && j < PBE[c >> kOffBits].y);
-          grow[(int64_t)kk << 5] = j;
+          grow[(int64_t)kk * gs] = j;
         }
       }
     }
     if (mine)
-      for (int q = min(k, cap); q < cap && (q & 3) != 0; ++q) grow[(int64_t)q << 5] = i;
+      for (int q = min(k, cap); q < cap && (q & 3) != 0; ++q) grow[(int64_t)q * gs] = i;
   }
   if (i < n) B.cnt[i] = active ? k : 0;
   const int kmax = __reduce_max_sync(0xffffffffu, k);
@@ -786,7 +789,8 @@ __global__ void __launch_bounds__(256) k_verlet_export(Bufs B, int n,
   const int64_t *gid = B.gid[B.st->cur_id];
   const int *nb = B.nbr + nbr_row_base(B, i);
   const int c = B.cnt[i];
-  for (int k = 0; k < c; ++k) col_gid[row_ptr[i] + k] = gid[nb[k << 5]];
+  const int gs = nbr_stride(B);
+  for (int k = 0; k < c; ++k) col_gid[row_ptr[i] + k] = gid[nb[(int64_t)k * gs]];
 }
 
 // Image shift of every list entry (R4/R5 sets of (gid_i, gid_j, shift)): per
@@ -801,7 +805,7 @@ __global__ void __launch_bounds__(256) k_verlet_shifts(Params P, Bufs B, int n,
   const int c = B.cnt[i];
   const float4 xi = B.xref[i];
   for (int k = 0; k < c; ++k) {
-    const float4 xj = B.xref[nb[k << 5]];
+    const float4 xj = B.xref[nb[(int64_t)k * nbr_stride(B)]];
     const float a[3] = {xi.x, xi.y, xi.z}, b[3] = {xj.x, xj.y, xj.z};
     int8_t *o = col_shift + 3 * (row_ptr[i] + k);
 #pragma unroll
@@ -822,17 +826,17 @@ static size_t staged_smem(int wcap) {
   return (wcap > 0 && tot <= 200 * 1024) ? tot : 0;
 }
 
-template <int RCH, int NMODE>
+template <int RCH, int NMODE, bool RM = false>
 static void launch_st(const Params &P, const Bufs &B, int64_t n, size_t sm, int wcap,
                       cudaStream_t s) {
   static size_t set = 0;
   if (sm > set) {
-    cudaFuncSetAttribute(k_verlet_st<RCH, NMODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_verlet_st<RCH, NMODE, RM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sm);
     set = sm;
   }
   const unsigned g = (unsigned)((n + stg::kWarps * 32 - 1) / (stg::kWarps * 32));
-  k_verlet_st<RCH, NMODE><<<g, stg::kWarps * 32, sm, s>>>(P, B, (int)n, wcap);
+  k_verlet_st<RCH, NMODE, RM><<<g, stg::kWarps * 32, sm, s>>>(P, B, (int)n, wcap);
 }
 
 void launch_verlet(const Params &P, const Bufs &B, int64_t n, cudaStream_t s) {
@@ -852,13 +856,15 @@ void launch_verlet(const Params &P, const Bufs &B, int64_t n, cudaStream_t s) {
     const char *e = std::getenv("PM_VERLET_STAGED");
     return (e && e[0] == '0') ? 0 : 1;
   }();
-  if (staged_env) {
+  if (staged_env || B.rm) {  // (the round-1 builder writes SELL-32 only)
     if (P.reach == 2) {
       if (nm == 1) launch_st<2, 1>(P, B, n, sm, wcap, s);
+      else if (B.rm) launch_st<2, 0, true>(P, B, n, sm, wcap, s);
       else launch_st<2, 0>(P, B, n, sm, wcap, s);
     } else {
       if (nm == 2) launch_st<1, 2>(P, B, n, sm, wcap, s);
       else if (nm == 1) launch_st<1, 1>(P, B, n, sm, wcap, s);
+      else if (B.rm) launch_st<1, 0, true>(P, B, n, sm, wcap, s);
       else launch_st<1, 0>(P, B, n, sm, wcap, s);
     }
     return;

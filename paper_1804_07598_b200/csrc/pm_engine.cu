@@ -345,6 +345,21 @@ int auto_nbr_cap(pm_ctx c) {
 
 // Upload a SELL slice layout (widths per 32-row slice, multiples of 4) over all
 // pcap/32 slices and make sure the neighbour array can hold it.
+// Row-major slices for long rows (Bufs::rm): LJ full lists only -- the SPH,
+// DEM and half-list kernels read SELL-32.  A change of layout kind drops the
+// list (the next build writes the new kind) and the graphs (B by value).
+void sync_row_major(pm_ctx c) {
+  const char *e = std::getenv("PM_ROW_MAJOR");  // "0": SELL-32 always (A/B, tests)
+  const int want = (c->nbr_cap >= kRowMajorMin && !c->have_sph && !c->have_dem &&
+                    !c->P.newton && !(e && e[0] == '0'))
+                       ? 1 : 0;
+  if (want != c->B.rm) {
+    c->B.rm = want;
+    c->list_valid = false;
+    destroy_graph(c);
+  }
+}
+
 pm_status upload_layout(pm_ctx c, const std::vector<int64_t> &width) {
   const int64_t ns = (int64_t)width.size();
   std::vector<int64_t> off((size_t)ns + 1);
@@ -373,6 +388,7 @@ pm_status upload_layout(pm_ctx c, const std::vector<int64_t> &width) {
   c->nbr_cap = wmax;
   c->P.nbr_cap = wmax;
   c->layout_pcap = c->pcap;
+  sync_row_major(c);
   return PM_OK;
 }
 
@@ -914,6 +930,7 @@ pm_status pm_set_lj(pm_ctx c, float eps, float sigma, float mass, int32_t flags,
 pm_status pm_set_newton(pm_ctx c, int32_t on) {
   if (!c) return PM_E_INVAL;
   c->P.newton = on ? 1 : 0;
+  sync_row_major(c);
   c->list_valid = false;  // the next build emits the other kind of rows
   c->forces_valid = false;
   destroy_graph(c);
@@ -950,6 +967,7 @@ pm_status pm_set_sph(pm_ctx c, const pm_sph_params *p) {
   for (int d = 0; d < 3; ++d) s.g[d] = p->g[d];
   c->have_sph = true;
   c->rho_valid = false;
+  sync_row_major(c);
   return PM_OK;
 }
 
@@ -1082,6 +1100,7 @@ pm_status pm_set_dem(pm_ctx c, const pm_dem_params *p) {
   }
   c->have_dem = true;
   destroy_graph(c);
+  sync_row_major(c);
   return PM_OK;
 }
 

@@ -170,6 +170,8 @@ struct Bufs {
   int2 *ps_dst;        //   ps_dst[ps_off[i] .. ps_off[i+1]) = (peer, ghost slot)
   uint8_t *wclass;     // decomposed contexts, per 32-row slice: 1 if a row of it may
                        // have ghost partners (boundary), 0 interior (k_warp_class)
+  int rm;              // 1: row-major slices (each row contiguous; long rows, LJ
+                       // full lists only -- see nbr_row_base)
 };
 
 // Device-resident mutable state (one per context).
@@ -282,9 +284,19 @@ PM_DEV float fast_rsqrt(float x) {
 // line); the slice's capacity is slice_off[slice + 1] - slice_off[slice].
 // Uniform liquids get equal widths; clustered inputs (rows from 0 to ~12k
 // entries) get widths from the exact counts of the previous build.
+// Row-major slices (Bufs::rm, LJ contexts whose widest slice is >= kRowMajorMin
+// entries): the same slice storage, row i contiguous at slice_off * 32 +
+// lane * width, entry k at + k -- a lane's appends in the build then fill
+// whole sectors in order instead of one slot of a line shared by lanes whose
+// rows drift apart by thousands of entries.
+constexpr int kRowMajorMin = 512;
 PM_DEV int64_t nbr_row_base(const Bufs &B, int i) {
-  return B.slice_off[i >> 5] * 32 + (i & 31);
+  const int64_t s = B.slice_off[i >> 5];
+  if (B.rm) return s * 32 + (int64_t)(i & 31) * (B.slice_off[(i >> 5) + 1] - s);
+  return s * 32 + (i & 31);
 }
+// distance between consecutive entries of a row
+PM_DEV int nbr_stride(const Bufs &B) { return B.rm ? 1 : 32; }
 
 PM_DEV int nbr_row_cap(const Bufs &B, int i) {
   return (int)(B.slice_off[(i >> 5) + 1] - B.slice_off[i >> 5]);

@@ -422,6 +422,28 @@ def test_clustered_cells_lists_forces(pm, orc, clustered):
     c.close()
 
 
+def test_clustered_row_major_equals_sell(pm, clustered, monkeypatch):
+    """Long rows (widest slice >= 512 entries) are stored row-major (each row
+    contiguous: whole-sector appends in the build); the entries and their
+    order are those of the SELL-32 layout, so a short capped run with rebuilds
+    is bitwise the same trajectory either way (PM_ROW_MAJOR=0 forces SELL)."""
+    s = clustered
+    out = []
+    for rm in ("1", "0"):
+        monkeypatch.setenv("PM_ROW_MAJOR", rm)
+        c = make_ctx(pm, s, r_min=0.8)
+        c.set_vlimit(0.15 / 0.005)
+        r = c.step_vv(0.005, 4)
+        assert r["rebuilds"] >= 2
+        st = pm.sorted_by_gid(c.get_state())
+        rp, col = c.get_verlet()
+        out.append((st, np.diff(rp)))
+        c.close()
+    (a, la), (b, lb) = out
+    assert la.max() > 4000 and np.array_equal(np.sort(la), np.sort(lb))
+    assert np.array_equal(a["pos"], b["pos"]) and np.array_equal(a["vel"], b["vel"])
+
+
 def test_clustered_short_run_with_vlimit(pm, clustered):
     """Reading R22 dynamics: capped LJ + velocity limit (skin/2)/dt; runs with a
     rebuild (incl. relayout of the list widths) nearly every step."""
