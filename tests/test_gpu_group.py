@@ -205,6 +205,63 @@ def test_group_empty_sub_domain(env):
         c.close()
 
 
+def test_group_clustered_long_rows_vs_oracle(env):
+    """Clustered input through the group API (BJ configs[4] recipe, 2 clusters
+    of 32,768 at the config's local density, capped LJ r_min = 0.8): rows of
+    thousands of entries (row-major slices, list relayout after the first
+    overflowing build) on both sub-domains of (2,1,1); sampled rows over the
+    length distribution and their capped forces against the oracle, then a
+    short batched run keeps every particle."""
+    pm = env
+    from oracle import oracle as orc
+    s = inputs.cfg5(n_clusters=2, per_cluster=32768)
+    members = pm.create_dist_local((2, 1, 1))
+    for k, c in enumerate(members):
+        c.set_domain(s.lo, s.hi, s.periodic)
+        c.set_cutoff(2.5, 0.3)
+        c.set_lj(1.0, 1.0, 1.0, 0.8)
+        if k == 0:
+            c.place(s.pos, s.vel, s.gid)
+        else:
+            c.place(np.zeros((0, 4), np.float32), np.zeros((0, 4), np.float32),
+                    np.zeros(0, np.int64))
+    for c in members:
+        c.map()
+    for c in members:
+        c.ghost_get()
+    forces(members)
+    inv = np.empty(int(s.gid.max()) + 1, np.int64)
+    inv[s.gid] = np.arange(s.n)
+    rv = np.float32(np.float32(2.5) + np.float32(0.3))
+    longest = 0
+    for c in members:
+        st = c.get_state()
+        own = np.where((c.get_kind() & pm.GHOST_BIT) == 0)[0]
+        rp, col = c.get_verlet()
+        lens = np.diff(rp)
+        longest = max(longest, int(lens[own].max()))
+        pick = own[np.argsort(lens[own])][np.linspace(0, own.size - 1, 24).astype(int)]
+        rrp, rcols, _ = orc.verlet_rows(s.pos, s.lo, s.hi, s.periodic, rv,
+                                        rows=inv[st["gid"][pick]], want_shift=False)
+        for t, i in enumerate(pick):
+            assert np.array_equal(np.sort(col[rp[i]:rp[i + 1]]),
+                                  np.sort(s.gid[rcols[rrp[t]:rrp[t + 1]]])), f"row {i}"
+        ref = orc.lj_rows(s.pos, s.lo, s.hi, s.periodic, rc=2.5, r_min=0.8,
+                          rows=inv[st["gid"][pick]])
+        err = orc.normalized_max_err(st["force"][pick, :3].astype(np.float64), ref["F"])
+        assert err <= 1e-4, err
+    assert longest > 1000
+    for c in members:
+        c.set_vlimit(0.15 / 0.005)
+    out = [c.dist_run(0.005, 6) for c in members][-1]
+    assert out["steps"] == 6
+    got = owned_union(pm, members)
+    assert np.array_equal(got["gid"], np.sort(s.gid))
+    assert np.all(np.isfinite(got["pos"]))
+    for c in members:
+        c.close()
+
+
 def test_group_call_order_errors(env):
     """Members must call the same collective: a member calling pm_ghost_get
     while another is inside pm_map is PM_E_STATE; a plain context is not a
