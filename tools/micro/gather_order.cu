@@ -238,6 +238,63 @@ __global__ void __launch_bounds__(256) k_sweep_cpw(const float4 *__restrict__ po
   out[i] = make_float4(fx, fy, fz, 0.f);
 }
 
+// Balanced rows: a warp's rows concatenated and dealt out evenly (every lane
+// ceil(T/32) or fewer entries, no SELL padding to the longest row); each entry
+// carries its owner lane (bits 27-31); the owner's position comes from shared
+// memory and the partial forces return to the owners by shared atomics.
+// SELL-32 column layout of the dealt entries, 4 per group, one group ahead.
+__global__ void __launch_bounds__(256) k_sweep_bal(const float4 *__restrict__ pos,
+                                                   const int *__restrict__ nbr,
+                                                   const long long *__restrict__ wbase,
+                                                   const int *__restrict__ qn, float4 *out,
+                                                   int n, float rc2) {
+  __shared__ float4 xs[8][32];
+  __shared__ float fs[8][32][4];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  xs[w][lane] = pos[i];
+  fs[w][lane][0] = fs[w][lane][1] = fs[w][lane][2] = 0.f;
+  __syncwarp();
+  const int c = qn[i];  // entries dealt to this lane
+  const int *nb = nbr + wbase[i >> 5] + lane;
+  float fx = 0.f, fy = 0.f, fz = 0.f;
+  int cur = -1;
+  float4 xo = make_float4(0.f, 0.f, 0.f, 0.f);
+  int jn = c > 0 ? __ldcs(nb) : 0;
+  for (int t = 0; t < c; ++t) {
+    const int e = jn;
+    if (t + 1 < c) jn = __ldcs(nb + (int64_t)(t + 1) * 32);
+    const int o = (unsigned)e >> 27, j = e & ((1 << 27) - 1);
+    if (o != cur) {
+      if (cur >= 0) {
+        atomicAdd(&fs[w][cur][0], fx);
+        atomicAdd(&fs[w][cur][1], fy);
+        atomicAdd(&fs[w][cur][2], fz);
+      }
+      fx = fy = fz = 0.f;
+      cur = o;
+      xo = xs[w][o];
+    }
+    const float4 xj = __ldg(pos + j);
+    const float dx = xj.x - xo.x, dy = xj.y - xo.y, dz = xj.z - xo.z;
+    const float r2 = dx * dx + dy * dy + dz * dz;
+    if (r2 < rc2 && r2 > 0.f) {
+      const float ir2 = 1.f / r2, ir6 = ir2 * ir2 * ir2;
+      const float f = 24.f * ir2 * ir6 * (2.f * ir6 - 1.f);
+      fx -= f * dx;
+      fy -= f * dy;
+      fz -= f * dz;
+    }
+  }
+  if (cur >= 0) {
+    atomicAdd(&fs[w][cur][0], fx);
+    atomicAdd(&fs[w][cur][1], fy);
+    atomicAdd(&fs[w][cur][2], fz);
+  }
+  __syncwarp();
+  out[i] = make_float4(fs[w][lane][0], fs[w][lane][1], fs[w][lane][2], 0.f);
+}
+
 // k_sweep<1> in CTAs of 1024 threads (4 x 256 consecutive rows share an SM)
 __global__ void __launch_bounds__(1024) k_sweep1k(const float4 *__restrict__ pos,
                                                   const int *__restrict__ nbr,
@@ -526,6 +583,42 @@ int main(int argc, char **argv) {
               lines_plain / slots, lines_greedy / slots);
   Sell A, B;
   to_sell(rows, A);
+  // balanced layout: per warp, entries dealt evenly (SELL-32 columns, 1 per slot)
+  std::vector<int> balq(n, 0);
+  std::vector<int64_t> balbase(nw + 1, 0);
+  for (int w = 0; w < nw; ++w) {
+    int64_t T = 0;
+    for (int k = 0; k < 32; ++k) T += rows[w * 32 + k].size();
+    const int64_t q = (T + 31) / 32;
+    balbase[w + 1] = balbase[w] + q * 32;
+  }
+  std::vector<int> balidx(balbase[nw], 0);
+  double padded_sell = 0, padded_bal = 0;
+  for (int w = 0; w < nw; ++w) {
+    int64_t T = 0;
+    size_t m = 0;
+    for (int k = 0; k < 32; ++k) T += rows[w * 32 + k].size(), m = std::max(m, rows[w * 32 + k].size());
+    const int64_t q = (T + 31) / 32;
+    padded_sell += 32.0 * m;
+    padded_bal += 32.0 * q;
+    int64_t e = 0;
+    for (int k = 0; k < 32; ++k)
+      for (int j : rows[w * 32 + k]) {
+        const int L = (int)(e / q), t = (int)(e % q);
+        balidx[balbase[w] + (int64_t)t * 32 + L] = (k << 27) | j;
+        balq[w * 32 + L] = t + 1;
+        ++e;
+      }
+  }
+  std::printf("slots per entry: SELL %.3f balanced %.3f\n", padded_sell / (double)A.idx.size() * A.idx.size() / padded_sell * padded_sell / std::max(1.0, [&]{double t=0; for (auto &r : rows) t += r.size(); return t;}()), padded_bal / [&]{double t=0; for (auto &r : rows) t += r.size(); return t;}());
+  int *dbal, *dbalq;
+  long long *dbalbase;
+  CK(cudaMalloc(&dbal, balidx.size() * sizeof(int)));
+  CK(cudaMalloc(&dbalq, n * sizeof(int)));
+  CK(cudaMalloc(&dbalbase, (nw + 1) * sizeof(long long)));
+  CK(cudaMemcpy(dbal, balidx.data(), balidx.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dbalq, balq.data(), n * sizeof(int), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dbalbase, balbase.data(), (nw + 1) * sizeof(long long), cudaMemcpyHostToDevice));
   to_sell(rg, B);
   float4 *dpos, *dout[2];
   int *didx[2], *dcnt;
@@ -575,6 +668,7 @@ int main(int argc, char **argv) {
     if (G == 12) { k_sweep_cpw<6><<<nbk, 256>>>(dpos, didx[v], dbase[v], dcnt, dout[v], n, rc * rc); return; }
     if (G == 9) { k_sweep_cpa<3><<<nbk, 256>>>(dpos, didx[v], dbase[v], dcnt, dout[v], n, rc * rc); return; }
     if (G == 10) { k_sweep_cpa<5><<<nbk, 256>>>(dpos, didx[v], dbase[v], dcnt, dout[v], n, rc * rc); return; }
+    if (G == 13) { k_sweep_bal<<<nbk, 256>>>(dpos, dbal, dbalbase, dbalq, dout[v], n, rc * rc); return; }
     if (G == 6) { k_sweep_pf<0><<<nbk, 256>>>(dpos, didx[v], dbase[v], dcnt, dout[v], n, rc * rc); return; }
     if (G == 5) { k_sweep1k<<<(n + 1023) / 1024, 1024>>>(dpos, didx[v], dbase[v], dcnt, dout[v], n, rc * rc); return; }
     if (G == 1) k_sweep<1><<<nbk, 256>>>(dpos, didx[v], dbase[v], dcnt, dout[v], n, rc * rc);
@@ -583,7 +677,7 @@ int main(int argc, char **argv) {
     if (G == 4 && u16_ok) k_sweep16<<<nbk, 256>>>(dpos, d16[v], db16[v], dpt[v], dcnt, dout[v], n, rc * rc);
   };
   for (int rep = 0; rep < 2; ++rep)
-    for (int G : {6, 11, 12, 7, 8})
+    for (int G : {1, 6, 13})
       for (int v = 0; v < 2; ++v) {
         for (int w = 0; w < 5; ++w) launch(G, v);
         cudaEventRecord(e0);
@@ -592,10 +686,10 @@ int main(int argc, char **argv) {
         CK(cudaEventSynchronize(e1));
         float ms;
         cudaEventElapsedTime(&ms, e0, e1);
-        std::printf("%s %s: %.4f ms per sweep, %.3f ns per particle\n", G == 11 ? "cp.async warp chunks ring 3" : G == 12 ? "cp.async warp chunks ring 6" : G == 9 ? "cp.async index ring 3" : G == 10 ? "cp.async index ring 5" : G == 8 ? "no index loads, L1-hit gathers" : G == 7 ? "index stream, L1-hit gathers" : G == 6 ? "i32 G=1 index prefetch" : G == 5 ? "i32 1024-thread CTAs" : G == 4 ? "u16x8" : G == 1 ? "i32 G=1" : G == 2 ? "i32 G=2" : "i32 G=3", name[v], ms / 50, ms / 50 * 1e6 / n);
+        std::printf("%s %s: %.4f ms per sweep, %.3f ns per particle\n", G == 13 ? "balanced rows (dealt evenly, owner lanes)" : G == 11 ? "cp.async warp chunks ring 3" : G == 12 ? "cp.async warp chunks ring 6" : G == 9 ? "cp.async index ring 3" : G == 10 ? "cp.async index ring 5" : G == 8 ? "no index loads, L1-hit gathers" : G == 7 ? "index stream, L1-hit gathers" : G == 6 ? "i32 G=1 index prefetch" : G == 5 ? "i32 1024-thread CTAs" : G == 4 ? "u16x8" : G == 1 ? "i32 G=1" : G == 2 ? "i32 G=2" : "i32 G=3", name[v], ms / 50, ms / 50 * 1e6 / n);
       }
   std::vector<float4> f0(n), f1(n);
-  launch(4, 0);
+  launch(13, 0);
   CK(cudaMemcpy(f0.data(), dout[0], n * sizeof(float4), cudaMemcpyDeviceToHost));
   launch(1, 0);
   CK(cudaMemcpy(f1.data(), dout[0], n * sizeof(float4), cudaMemcpyDeviceToHost));
@@ -604,6 +698,6 @@ int main(int argc, char **argv) {
     md = std::max(md, (double)std::fabs(f0[i].x - f1[i].x));
     mf = std::max(mf, (double)std::fabs(f0[i].x));
   }
-  std::printf("max |Fx| %.3g, max |dFx| u16 vs i32 (plain) %.3g\n", mf, md);
+  std::printf("max |Fx| %.3g, max |dFx| balanced vs i32 (plain) %.3g\n", mf, md);
   return 0;
 }
