@@ -12,10 +12,18 @@
 //           so the 32 gathers of one instruction touch few 128-byte lines
 // Device: the sweep's gather loop (4 gathers per index group) with the LJ
 // pair, forces written out; CUDA events over 50 launches per layout.
+// Kernel variants (the `launch` switch; DESIGN §11 lists the results):
+//   k_sweep<G>      G index groups per iteration (memory-level parallelism)
+//   k_sweep_pf<M>   indices one group ahead; M = 1: every gather an L1 hit,
+//                   M = 2: no index stream either (the compute floor)
+//   k_sweep16       16-bit codes (piece table per warp), 8 per 16-byte load
+//   k_sweep_cpa/cpw index stream staged through shared memory by cp.async
+//   k_sweep_bal     a warp's rows dealt out evenly (no padding), owner lanes
+//   k_sweep1k       1024-thread CTAs (with brick-ordered cells: argv 2-4)
 //
 // Build: nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a \
 //          -o gather_order tools/micro/gather_order.cu
-// Run:   ./gather_order [lattice|poisson]
+// Run:   ./gather_order [lattice|poisson] [bx by bz] [nz]
 #include <cuda_runtime.h>
 
 #include <algorithm>
