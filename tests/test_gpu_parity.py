@@ -444,6 +444,31 @@ def test_clustered_row_major_equals_sell(pm, clustered, monkeypatch):
     assert np.array_equal(a["pos"], b["pos"]) and np.array_equal(a["vel"], b["vel"])
 
 
+def test_row_major_switches_with_half_lists(pm, clustered):
+    """The list layout follows the context: long LJ rows are row-major, half
+    (Newton) lists are SELL-32 only, so pm_set_newton switches the layout
+    (list and graphs dropped, the next build writes the other kind).  Forces
+    full (row-major) -> half (SELL) -> full again: the half-list forces agree
+    within the parity tolerance, the two full-list passes bit for bit."""
+    s = clustered
+    c = make_ctx(pm, s, r_min=0.8)
+    c.build_verlet()
+    c.compute_lj()
+    f1 = pm.sorted_by_gid(c.get_state())["force"][:, :3].astype(np.float64)
+    c.set_newton(True)
+    c.build_verlet()
+    c.compute_lj()
+    f2 = pm.sorted_by_gid(c.get_state())["force"][:, :3].astype(np.float64)
+    c.set_newton(False)
+    c.build_verlet()
+    c.compute_lj()
+    f3 = pm.sorted_by_gid(c.get_state())["force"][:, :3].astype(np.float64)
+    rms = np.sqrt(np.mean(f1 ** 2))
+    assert np.max(np.abs(f2 - f1)) / rms <= TOL
+    assert np.array_equal(f1, f3)
+    c.close()
+
+
 def test_clustered_short_run_with_vlimit(pm, clustered):
     """Reading R22 dynamics: capped LJ + velocity limit (skin/2)/dt; runs with a
     rebuild (incl. relayout of the list widths) nearly every step."""
