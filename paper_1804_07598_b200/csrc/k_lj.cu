@@ -12,8 +12,9 @@
 // per-thread fp32 accumulation, no atomics.  The neighbour stream is read
 // with streaming loads (ld.global.cs) so the 0.3 GB list does not evict the
 // L2-resident positions.  The periodic minimum-image correction (R4) is only
-// evaluated in warps that have a particle within r_v + skin of a periodic
-// face (warp-uniform branch).  In pm_step_vv the sweep is fused with the
+// evaluated on the axes along which the warp has a particle within r_v +
+// skin of a periodic face (warp-uniform 3-bit mask, one loop variant per
+// case).  In pm_step_vv the sweep is fused with the
 // integrator: the second half-kick of step n, the first half-kick and drift
 // of step n+1, the wrap and the skin/2 displacement test run in the epilogue
 // and write the alternate position/velocity buffers.
