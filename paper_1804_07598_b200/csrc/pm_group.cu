@@ -32,7 +32,11 @@
 //
 // The particle work (selection, packing, unpacking, cell lists, Verlet rows,
 // forces, integration) is the single-context kernels behind pm_dist_*; this
-// file only decides who talks to whom and moves bytes.
+// file only decides who talks to whom and moves bytes.  pm_dist_run enqueues
+// its steps in batches: the rebuild flags are reduced on the device into
+// State::hold (NCCL MAX across ranks, a one-thread kernel across local
+// members), step kernels of held steps return at once, and the host
+// synchronises once per batch (run_batched).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
