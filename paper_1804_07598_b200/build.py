@@ -79,7 +79,9 @@ def build(force: bool = False, verbose: bool = False, checks: bool = False) -> s
     os.replace(tmp, target)
     if not checks:
         with open(os.path.join(HERE, "libpm.ptxas.txt"), "w") as f:
-            f.write("".join(log))
+            # (without ptxas' compile times, so that the log only changes with the code)
+            f.write("".join(l for l in "".join(log).splitlines(True)
+                            if "Compile time" not in l))
     return target
 
 
